@@ -1,0 +1,362 @@
+"""Benchmark of the B200-native Speed3R GSA layer forward (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--views V] [--impl ours|reference]
+
+One step = one GSA layer forward (special path, pooling, compressed attention
++ top-k, block-sparse selection, gate, merge) over bf16 Q/K/V already resident
+in HBM (synthetic, VGGT-L-shaped: 16 heads x 64, 5 specials + 36x36 patches per
+view; inputs are larger than L2, no flush needed). `value` is whole-job
+tokens/s (M tokens / layer time); `e2e` is the same metric through the public
+API from pinned HOST buffers (H2D of Q/K/V and D2H of the f32 output inside the
+timed region). Rank 0 prints ONE JSON line.
+
+For N>1 (torchrun) the layer is sharded by query views (paper_2603_08055_b200.dist):
+each rank owns V/N views, K/V of all views are all-gathered over NCCL, and the
+time is the max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+HEADS, DIM, S, TOPK, SPECIAL_PER_VIEW, GRID = 16, 64, 4, 32, 5, 36
+METRIC = "sparse global-attn layer ms & tokens/s at 1000 views; speedup vs dense; TC util"
+
+
+def layout_for(views: int):
+    return (SPECIAL_PER_VIEW * views, views, GRID, GRID, S)
+
+
+def geometry(views: int):
+    ns, nf, gh, gw, s = layout_for(views)
+    mi = nf * gh * gw
+    W = mi // (s * s)
+    return dict(Ms=ns, Mi=mi, M=ns + mi, W=W)
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d["hbm_gbs"], d["bf16_tflops"], d.get("bf16_tflops_sustained", d["bf16_tflops"]), "measured"
+    return 6650.0, 1590.0, 1400.0, "fallback"
+
+
+# ---------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"], stdout=self.f,
+                                         stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            self.proc.wait()
+
+    def summary(self):
+        self.f.flush()
+        rows = [r.split(", ") for r in open(self.f.name).read().strip().splitlines() if r.count(",") >= 7]
+        os.unlink(self.f.name)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in rows for n, v in zip(names, r[4:8]) if v.strip() == "Active"})
+        under_load = sorted(sm)[len(sm) // 4:] if sm else []
+        return {"sm_mhz": statistics.median(under_load) if under_load else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(rows),
+                "power_w_max": max(float(r[2]) for r in rows if r[2].replace(".", "").isdigit())}
+
+
+# ----------------------------------------------------------- CPU baseline
+def cpu_reference_sample(views_target: int, sample_views: int = 16, repeats: int = 2):
+    """The reference's own fused CPU layer (oracle/_ref, compiled unmodified from
+    /root/reference) on a bounded sample: the same per-view geometry with
+    `sample_views` views, all host threads. Stage times are extrapolated to the
+    target view count by each stage's exact cost law (special ~ Ms*M, compress
+    ~ W^2, pool/select/gate/partition ~ M_i, plan ~ W). Falls back to the oracle
+    port when oracle/_ref was not built."""
+    from oracle import Layout, Oracle, RefLib, make_inputs
+    orc = Oracle()
+    threads = os.cpu_count() or 1
+    lt = layout_for(sample_views)
+    L = Layout(*lt)
+    q, k, v, wg = make_inputs(orc, L, heads=HEADS, dim=DIM, seed=7)
+    kind = "reference" if RefLib.available() else "port"
+    runs = []
+    for _ in range(repeats):
+        if kind == "reference":
+            r = RefLib().forward(q, k, v, wg, lt, top_k=TOPK, threads=threads, context=False)
+            runs.append(dict(r["stage_ms"]))
+        else:
+            t0 = time.perf_counter()
+            orc.gsa_forward(q, k, v, wg, L, top_k=TOPK)
+            runs.append({"total": (time.perf_counter() - t0) * 1e3})
+    st = {key: statistics.median(r[key] for r in runs) for key in runs[0]}
+    gs, gt = geometry(sample_views), geometry(views_target)
+    law = {"partition": gt["M"] / gs["M"], "special": (gt["Ms"] * gt["M"]) / max(1, gs["Ms"] * gs["M"]),
+           "pool": gt["Mi"] / gs["Mi"], "compress": (gt["W"] / gs["W"]) ** 2, "plan": gt["W"] / gs["W"],
+           "select": gt["Mi"] / gs["Mi"], "gate_merge": gt["Mi"] / gs["Mi"], "total": (gt["W"] / gs["W"]) ** 2}
+    ms_target = sum(val * law[key] for key, val in st.items())
+    sample_ms = sum(st.values())
+    return dict(value=gt["M"] / (ms_target / 1e3), unit="tokens/s", cores=threads, kind=kind,
+                sample=(f"reference fused CPU layer ({kind}) at {sample_views} views x 16 heads (M={gs['M']}), "
+                        f"median of {repeats}, {sample_ms/1e3:.1f} s per run; stages extrapolated to {views_target} "
+                        f"views by cost law (compress ~W^2, special ~Ms*M, rest ~M_i)"),
+                sample_stage_ms={k_: round(v_, 1) for k_, v_ in st.items()},
+                extrapolated_ms=round(ms_target, 1))
+
+
+def run_reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    steps = []
+    for i in range(args.warmup + args.steps):
+        r = cpu_reference_sample(args.views, sample_views=args.ref_sample_views, repeats=1)
+        if i >= args.warmup:
+            steps.append(r)
+    vals = [r["value"] for r in steps]
+    v = statistics.median(vals)
+    last = steps[-1]
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "tokens/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": geometry(args.views)["M"] / v * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (seeded N(0,1) bf16-representable Q/K/V)",
+            "config": {"workload": f"1 GSA layer, {args.views} views x (5 specials + 36x36 patches), 16 heads x 64, "
+                                   f"s=4, top-32, plain", "views": args.views, "tokens": geometry(args.views)["M"]},
+            "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": last["cores"], "kind": last["kind"],
+                             "sample": last["sample"]},
+            "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------- GPU arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--views", type=int, default=int(os.environ.get("GSA_BENCH_VIEWS", "1000")))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--ref-sample-views", type=int, default=16)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-dense", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference_arm(args)
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2603_08055_b200 as gsa
+    from paper_2603_08055_b200 import _lib
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    lib = _lib.load()
+
+    G = geometry(args.views)
+    lt = layout_for(args.views)
+    L = gsa.build_token_layout(*lt)
+    params = gsa.GsaParams(window_s=S, top_k=TOPK)
+    gen = torch.Generator(device=dev).manual_seed(7)
+    q, k, v = (torch.randn(HEADS, G["M"], DIM, generator=gen, device=dev, dtype=torch.float32).to(torch.bfloat16)
+               for _ in range(3))
+    wg = torch.randn(HEADS, DIM, DIM, generator=gen, device=dev) / 8.0
+    out = torch.empty(HEADS, G["M"], DIM, device=dev)
+    ws = gsa.Workspace()
+
+    if world > 1:
+        from paper_2603_08055_b200 import dist as gdist
+        step_fn, shard_tokens = gdist.make_sharded_step(q, k, v, wg, lt, params, rank, world)
+    else:
+        def step_fn():
+            gsa.gsa_forward(q, k, v, wg, L, params, out=out, workspace=ws)
+        shard_tokens = G["M"]
+
+    # stage events (rank-local, recorded by the library on the launching stream)
+    import ctypes
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(args.steps)]
+    for row in ev:
+        for e in row:
+            e.record()  # materialise the cudaEvent_t handles
+    handles = [(ctypes.c_void_p * 5)(*[e.cuda_event for e in row]) for row in ev]
+    for _ in range(args.warmup):
+        step_fn()
+    torch.cuda.synchronize()
+
+    n0 = ctypes.c_uint64()
+    lib.gsa_launch_count(ctypes.byref(n0))
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clocks:
+        start.record()
+        for i in range(args.steps):
+            lib.gsa_set_stage_events(handles[i], 5)
+            step_fn()
+        lib.gsa_set_stage_events(None, 0)
+        stop.record()
+        torch.cuda.synchronize()
+    names = ("special", "pool", "compress", "select")
+    stage_ms = {n: sum(ev[i][j].elapsed_time(ev[i][j + 1]) for i in range(args.steps)) / args.steps
+                for j, n in enumerate(names)}
+    n1 = ctypes.c_uint64()
+    lib.gsa_launch_count(ctypes.byref(n1))
+    ms_local = start.elapsed_time(stop) / args.steps
+    t = torch.tensor([ms_local], device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    tokens_total = G["M"]
+    value = tokens_total / (ms / 1e3)
+
+    hbm, tc_peak, tc_sust, peak_kind = load_peaks()
+    W, Mi, Ms, M = G["W"], G["Mi"], G["Ms"], G["M"]
+    F = 0
+    flops = {"special": 4.0 * HEADS * Ms * M * DIM, "compress": 4.0 * HEADS * W * W * DIM,
+             "select": 4.0 * HEADS * Mi * (TOPK + F) * S * S * DIM}
+    bytes_ = {"pool": 3 * HEADS * Mi * DIM * 2 + 3 * HEADS * W * DIM * 4,
+              "select": HEADS * W * (TOPK + F) * S * S * DIM * 2 * 2 + HEADS * Mi * DIM * (2 + 4) + HEADS * W * DIM * 4}
+    dom = max(stage_ms, key=lambda n: stage_ms[n])
+    if dom in ("pool",) or (dom == "select"):
+        A = bytes_[dom] / (stage_ms[dom] / 1e3) / 1e9
+        roof = {"kernel": dom, "bound": "hbm", "achieved": A, "peak": hbm, "unit": "GB/s", "frac": A / hbm,
+                "traffic": None, "peak_kind": peak_kind}
+    else:
+        A = flops[dom] / (stage_ms[dom] / 1e3) / 1e12
+        roof = {"kernel": dom, "bound": "tensor", "achieved": A, "peak": tc_peak, "unit": "TFLOP/s",
+                "frac": A / tc_peak, "traffic": None, "peak_kind": peak_kind}
+    prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(prof):
+        tr = json.load(open(prof)).get(dom)
+        if tr:
+            roof["traffic"] = tr
+    sel_tc = flops["select"] / (stage_ms["select"] / 1e3) / 1e12
+
+    line = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak" if world == 1 else "strong",
+            "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (torch N(0,1) bf16 Q/K/V, W_g=N(0,1)/8 f32), resident in HBM",
+            "config": {"workload": f"1 GSA layer, {args.views} views x (5 specials + 36x36 patches) = {M} tokens, "
+                                   f"16 heads x 64, s=4, top-32, plain", "views": args.views, "tokens": M,
+                       "windows": W, "parallelism": f"views sharded over {world}" if world > 1 else "1 GPU",
+                       "l2": "inputs larger than L2 (no flush)"},
+            "stage_ms": {k_: round(v_, 3) for k_, v_ in stage_ms.items()},
+            "roofline": roof,
+            "select_tc_util": {"achieved_tflops": sel_tc, "frac_of_peak": sel_tc / tc_peak},
+            "gpu_launches": int(n1.value - n0.value),
+            "clocks": clocks.summary()}
+
+    # end to end through the public API from pinned host buffers
+    if not args.no_e2e and world == 1:
+        hq, hk, hv = (x.cpu().pin_memory() for x in (q, k, v))
+        hout = torch.empty(out.shape, dtype=torch.float32).pin_memory()
+        dq, dk, dv = (torch.empty_like(x) for x in (q, k, v))
+
+        def e2e_step():
+            dq.copy_(hq, non_blocking=True)
+            dk.copy_(hk, non_blocking=True)
+            dv.copy_(hv, non_blocking=True)
+            gsa.gsa_forward(dq, dk, dv, wg, L, params, out=out, workspace=ws)
+            hout.copy_(out, non_blocking=True)
+
+        for _ in range(2):
+            e2e_step()
+        torch.cuda.synchronize()
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s0.record()
+        for _ in range(args.steps):
+            e2e_step()
+        s1.record()
+        torch.cuda.synchronize()
+        e_ms = s0.elapsed_time(s1) / args.steps
+        line["e2e"] = {"value": M / (e_ms / 1e3), "unit": "tokens/s", "ms_per_step": e_ms,
+                       "h2d_bytes_per_step": 3 * q.numel() * 2, "d2h_bytes_per_step": out.numel() * 4}
+        del hq, hk, hv, hout, dq, dk, dv
+
+    # the paper's sparse-vs-dense comparison on the same GPU: fastest library dense
+    # attention over all M tokens (timed on a query subset; cost is linear in queries)
+    if not args.no_dense and rank == 0:
+        line["dense"] = dense_baseline(torch, q, k, v, ms)
+
+    if rank == 0 and not args.no_cpu_baseline:
+        try:
+            line["cpu_baseline"] = {k_: v_ for k_, v_ in cpu_reference_sample(args.views).items()
+                                    if k_ in ("value", "unit", "cores", "kind", "sample")}
+        except Exception as e:  # the baseline is reported, never required
+            line["cpu_baseline"] = {"value": None, "unit": "tokens/s", "cores": os.cpu_count(), "kind": "reference",
+                                    "sample": f"failed: {e}"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def dense_baseline(torch, q, k, v, sparse_ms):
+    import torch.nn.functional as Fn
+    from torch.nn.attention import SDPBackend, sdpa_kernel
+    H, M, d = q.shape
+    frac = max(1, M // 65536)
+    nq = math.ceil(M / frac)
+    qq, kk, vv = q[None, :, :nq], k[None], v[None]
+    results = {}
+    for name, be in (("cudnn", SDPBackend.CUDNN_ATTENTION), ("flash", SDPBackend.FLASH_ATTENTION),
+                     ("efficient", SDPBackend.EFFICIENT_ATTENTION)):
+        try:
+            with sdpa_kernel([be]):
+                Fn.scaled_dot_product_attention(qq, kk, vv)
+                torch.cuda.synchronize()
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record()
+                for _ in range(2):
+                    Fn.scaled_dot_product_attention(qq, kk, vv)
+                b.record()
+                torch.cuda.synchronize()
+                results[name] = a.elapsed_time(b) / 2 * (M / nq)
+        except Exception as e:  # backend not available for this shape/arch
+            results[name] = None
+    ok = {n: t for n, t in results.items() if t}
+    if not ok:
+        return {"ms": None, "backends": results}
+    best = min(ok, key=ok.get)
+    return {"ms": ok[best], "backend": f"torch sdpa {best}", "speedup_sparse_vs_dense": ok[best] / sparse_ms,
+            "backends_ms": results, "timed_queries": nq, "note": "timed on the first M/%d queries x all keys, scaled" % frac}
+
+
+if __name__ == "__main__":
+    main()

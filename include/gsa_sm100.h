@@ -1,0 +1,198 @@
+/*
+ * gsa_sm100.h — C ABI of the B200 (sm_100a) Global Sparse Attention library
+ * (libgsa_sm100.so). This is the drop-in boundary: the C++ operator API in
+ * include/gsa/ (same names and signatures as the reference's
+ * proj/include/gsa) forwards to these entry points, and so can any FFI.
+ *
+ * Conventions
+ *  - Plain C: no exceptions, no torch types. Every entry point returns a
+ *    gsa_status; gsa_last_error_message() gives the detail of the last failure
+ *    on the calling thread. Status values mirror the reference's exception
+ *    classes (proj/include/gsa/errors.hpp:8-58).
+ *  - All tensor data pointers are DEVICE pointers. Compute calls are
+ *    stream-ordered on `stream`, do no allocation and no host synchronisation
+ *    unless the comment says so. Scratch memory is caller-owned (`workspace`);
+ *    query its size with the matching *_workspace_bytes function.
+ *  - Deterministic: no floating-point atomics reach any output; repeated calls
+ *    on the same inputs are bitwise identical.
+ *  - Top-k indices are bit-exact with the reference CPU implementation:
+ *    pooled Qc/Kc are summed in ascending member order (compression.hpp:29-35),
+ *    guide scores follow scaled_dot's 4-lane order without FMA (dot.hpp:11-23),
+ *    rows are ordered by (score desc, index asc) (compression.hpp:67-73).
+ *
+ * Reference interface replaced by each entry point (file:line under
+ * /root/reference/proj) is cited on the declaration.
+ */
+#ifndef GSA_SM100_H
+#define GSA_SM100_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GSA_SM100_ABI_VERSION 1
+
+typedef struct CUstream_st* gsa_stream_t; /* == cudaStream_t */
+
+typedef enum {
+    GSA_OK = 0,
+    GSA_ERR_GENERIC = 1,            /* GsaError           errors.hpp:8   */
+    GSA_ERR_SHAPE_MISMATCH = 2,     /* ShapeMismatch      errors.hpp:12  */
+    GSA_ERR_DIVISIBILITY = 3,       /* DivisibilityError  errors.hpp:16  */
+    GSA_ERR_ZERO_SIZE = 4,          /* ZeroSizeError      errors.hpp:20  */
+    GSA_ERR_INDEX_OUT_OF_RANGE = 5, /* IndexOutOfRange    errors.hpp:24  */
+    GSA_ERR_NON_FINITE = 6,         /* NonFiniteInput     errors.hpp:28  */
+    GSA_ERR_INVALID_TILING = 7,     /* InvalidTiling      errors.hpp:32  */
+    GSA_ERR_INVALID_STRIDE = 8,     /* InvalidStride      errors.hpp:36  */
+    GSA_ERR_EMPTY_SELECTION = 9,    /* EmptySelection     errors.hpp:40  */
+    GSA_ERR_UNSUPPORTED = 10,       /* shape outside what the sm_100a kernels implement */
+    GSA_ERR_CUDA = 11,              /* CUDA runtime / launch failure */
+    GSA_ERR_WORKSPACE = 12,         /* workspace too small or misaligned */
+    GSA_ERR_NCCL = 13               /* reserved for the sharded layer */
+} gsa_status;
+
+typedef enum { GSA_DTYPE_F32 = 0, GSA_DTYPE_BF16 = 1 } gsa_dtype;
+
+/* A [heads x rows x dim] view of device memory (tensor.hpp:15-42 Tensor<T>,
+ * head-major). Strides are in ELEMENTS; dim is contiguous. */
+typedef struct {
+    void* data;
+    int32_t dtype; /* gsa_dtype */
+    int32_t heads, rows, dim;
+    int64_t head_stride, row_stride;
+} gsa_tensor;
+
+/* layout.hpp:13-40 TokenLayout */
+typedef struct {
+    int32_t num_special, num_frames, grid_h, grid_w, window_s;
+} gsa_layout;
+
+/* types.hpp:58-65 GsaParams (+ KernelTiling 13-16). variant: 0 plain, 1 hybrid. */
+typedef struct {
+    int32_t window_s, top_k;
+    double scale; /* 0 => 1/sqrt(dim) (reference.hpp:22-26) */
+    int32_t variant, ref_stride;
+    int32_t block_m, block_n; /* validated like validate_tiling (types.hpp:20-25) */
+} gsa_params;
+
+/* Device pointers for the ForwardContext fields (layer.hpp:124-142) the
+ * caller wants materialised; any may be NULL. Shapes: qc/kc/vc/o_comp
+ * [H][W][d] f32, lse_comp [H][W], topk [H][W][k_eff] int32, o_sel/gate
+ * [H][Mi][d] f32, lse_sel [H][Mi], lse_spec [H][Ms]. */
+typedef struct {
+    float *qc, *kc, *vc, *o_comp, *lse_comp;
+    int32_t* topk;
+    float *o_sel, *lse_sel, *gate, *lse_spec;
+} gsa_context;
+
+int gsa_abi_version(void);
+const char* gsa_status_string(int status);
+const char* gsa_last_error_message(void);
+
+/* build_token_layout (layout.cpp:7-24): validates and fills *out. */
+int gsa_make_layout(int num_special, int num_frames, int grid_h, int grid_w, int window_s,
+                    gsa_layout* out);
+/* validate_params (types.hpp:67-73) + window_s consistency (layer.hpp:182-183). */
+int gsa_validate_params(const gsa_params* params, const gsa_layout* layout);
+
+/* avg_pool_tokens (compression.hpp:20-38). x_img: rows == image tokens (f32 or
+ * bf16). out: f32 [H][W][d]. Bit-exact with the reference. */
+int gsa_avg_pool_tokens(const gsa_tensor* x_img, const gsa_layout* layout, const gsa_tensor* out,
+                        gsa_stream_t stream);
+
+/* upsample_nearest (compression.hpp:42-53). coarse f32 [H][W][d] -> out f32 [H][Mi][d]. */
+int gsa_upsample_nearest(const gsa_tensor* coarse, const gsa_layout* layout, const gsa_tensor* out,
+                         gsa_stream_t stream);
+
+/* tiled_attention (compression.hpp:99-165): out = softmax(q k^T * scale) v (f32),
+ * lse [H][mq] = m + log(l). q/k/v f32 or bf16. */
+int gsa_tiled_attention(const gsa_tensor* q, const gsa_tensor* k, const gsa_tensor* v, float scale,
+                        int block_m, int block_n, const gsa_tensor* out, float* lse,
+                        gsa_stream_t stream);
+
+/* special_token_attention (layer.hpp:80-96): dense attention of the special
+ * queries over ALL keys. Empty q_spec is a no-op. */
+int gsa_special_token_attention(const gsa_tensor* q_spec, const gsa_tensor* k, const gsa_tensor* v,
+                                float scale, const gsa_tensor* out, float* lse,
+                                gsa_stream_t stream);
+
+/* fused_compressed_attention_topk (compression.hpp:180-297). qc/kc/vc f32
+ * [H][W][d]; excluded: device byte mask [W] or NULL; out f32 [H][W][d]; lse
+ * [H][W]; indices [H][W][k_eff]; guide_scores (nullable) [H][W][k_eff] f32.
+ * *k_eff_out (host) = min(k, selectable). Indices are bit-exact. */
+size_t gsa_compressed_attention_topk_workspace_bytes(int heads, int windows, int dim, int k);
+int gsa_compressed_attention_topk(const gsa_tensor* qc, const gsa_tensor* kc, const gsa_tensor* vc,
+                                  int k, float scale, int block_m, int block_n,
+                                  const uint8_t* excluded, int n_excluded, const gsa_tensor* out,
+                                  float* lse, int32_t* indices, float* guide_scores, int* k_eff_out,
+                                  void* workspace, size_t workspace_bytes, gsa_stream_t stream);
+
+/* forced_windows_of (selection.cpp:14-21): writes the ascending forced window
+ * ids into forced (device, capacity >= count) and their count (host). */
+int gsa_forced_windows(const gsa_layout* layout, int ref_stride, int32_t* forced, int* count,
+                       gsa_stream_t stream);
+
+/* build_selection_plan (selection.cpp:29-67): device CSR plan from device
+ * top-k rows [H][rows][k]. offsets [H*rows+1] int64; window_ids capacity
+ * ids_capacity (plain: H*rows*k; hybrid: H*rows*(F+k) suffices). *n_ids
+ * (host) is the realised size; this call synchronises `stream`. */
+int gsa_build_selection_plan(const int32_t* topk, int heads, int rows, int k,
+                             const gsa_layout* layout, int variant, int ref_stride,
+                             int64_t* offsets, int32_t* window_ids, int64_t ids_capacity,
+                             int64_t* n_ids, void* workspace, size_t workspace_bytes,
+                             gsa_stream_t stream);
+size_t gsa_build_selection_plan_workspace_bytes(int heads, int rows, int k,
+                                                const gsa_layout* layout, int ref_stride);
+
+/* block_sparse_attention (selection.hpp:63-136) over a device CSR plan.
+ * Validates that no row is empty (synchronises `stream`; EmptySelection).
+ * out f32 [H][Mi][d], lse [H][Mi]. */
+int gsa_block_sparse_attention(const gsa_tensor* q_img, const gsa_tensor* k_img,
+                               const gsa_tensor* v_img, const int64_t* offsets,
+                               const int32_t* window_ids, const gsa_layout* layout, float scale,
+                               const gsa_tensor* out, float* lse, gsa_stream_t stream);
+
+/* gate (layer.hpp:99-119): g = sigmoid(q . w_g[h]); w_g f32 [H][d][d]; g f32. */
+int gsa_gate(const gsa_tensor* q_img, const gsa_tensor* w_g, const gsa_tensor* g,
+             gsa_stream_t stream);
+
+/* gsa_forward (layer.hpp:177-230) from projected Q/K/V: special path, pooling,
+ * compressed attention + top-k, selection plan, block-sparse attention, gate,
+ * gated merge and concat, all on the device, no host sync. q/k/v [H][M][d]
+ * (bf16 is the fast path); w_g f32 [H][d][d]; out f32 [H][M][d]. ctx may be NULL. */
+size_t gsa_forward_workspace_bytes(const gsa_layout* layout, const gsa_params* params, int heads,
+                                   int dim);
+int gsa_forward(const gsa_tensor* q, const gsa_tensor* k, const gsa_tensor* v,
+                const gsa_tensor* w_g, const gsa_layout* layout, const gsa_params* params,
+                const gsa_tensor* out, const gsa_context* ctx, int* k_eff_out, void* workspace,
+                size_t workspace_bytes, gsa_stream_t stream);
+
+/* gsa_forward_with_plan (layer.hpp:235-262): selection pinned to a device CSR
+ * plan; the compressed branch is plain tiled attention (no top-k). */
+int gsa_forward_with_plan(const gsa_tensor* q, const gsa_tensor* k, const gsa_tensor* v,
+                          const gsa_tensor* w_g, const gsa_layout* layout,
+                          const gsa_params* params, const int64_t* offsets,
+                          const int32_t* window_ids, const gsa_tensor* out, void* workspace,
+                          size_t workspace_bytes, gsa_stream_t stream);
+
+/* KernelStats (types.hpp:78-86) in closed form for a gsa_forward call:
+ * scores_computed = H*(Ms*M + W*W); keys_attended = sum over rows of
+ * |row| * s^2 * s^2 (rows have width F + k_eff). */
+int gsa_forward_stats(const gsa_layout* layout, const gsa_params* params, int heads,
+                      uint64_t* scores_computed, uint64_t* keys_attended);
+
+/* Instrumentation (bench.py, profiling). gsa_set_stage_events: when n >= 5,
+ * subsequent gsa_forward calls on this thread record cudaEvent_t events[0..4]
+ * on `stream` at: start, after the special path, after pooling, after the
+ * compressed attention + top-k, after selection/gate/merge. n = 0 disables.
+ * gsa_launch_count: kernels this library has launched since it was loaded. */
+int gsa_set_stage_events(void* const* events, int n);
+int gsa_launch_count(uint64_t* count);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GSA_SM100_H */

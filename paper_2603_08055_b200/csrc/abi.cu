@@ -1,0 +1,684 @@
+// abi.cu — the extern "C" boundary (include/gsa_sm100.h): argument validation
+// with the reference's error classes, workspace carving and stream-ordered
+// orchestration of the kernels. No host synchronisation in compute calls
+// except where the header says so.
+#include <math.h>
+
+#include <atomic>
+#include <cstdarg>
+#include <cstdio>
+#include <string>
+
+#include "kernels.h"
+#include "tc.h"
+
+using namespace gsa_sm100;
+
+namespace gsa_sm100 {
+extern std::atomic<unsigned long long> g_launch_total;
+}
+
+namespace {
+
+thread_local std::string g_msg;
+thread_local cudaEvent_t g_stage_events[5];
+thread_local int g_n_stage_events = 0;
+
+void stage_mark(int i, cudaStream_t st) {
+    if (g_n_stage_events >= 5) cudaEventRecord(g_stage_events[i], st);
+}
+
+int fail(int status, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_msg = buf;
+    return status;
+}
+
+int cuda_status(cudaError_t e, const char* where) {
+    if (e == cudaSuccess) return GSA_OK;
+    return fail(GSA_ERR_CUDA, "%s: %s", where, cudaGetErrorString(e));
+}
+
+#define GSA_TRY(expr)                 \
+    do {                              \
+        int _rc = (expr);             \
+        if (_rc != GSA_OK) return _rc; \
+    } while (0)
+#define GSA_CUDA(expr) GSA_TRY(cuda_status((expr), #expr))
+
+TensorRef ref_of(const gsa_tensor& t, int row_offset = 0) {
+    TensorRef r;
+    const size_t es = t.dtype == GSA_DTYPE_BF16 ? 2 : 4;
+    r.data = static_cast<const char*>(t.data) + (size_t)row_offset * t.row_stride * es;
+    r.dtype = t.dtype;
+    r.hs = t.head_stride;
+    r.rs = t.row_stride;
+    return r;
+}
+
+int check_tensor(const gsa_tensor* t, const char* name, bool allow_bf16 = true) {
+    if (!t) return fail(GSA_ERR_GENERIC, "%s: null tensor", name);
+    if (t->dtype != GSA_DTYPE_F32 && !(allow_bf16 && t->dtype == GSA_DTYPE_BF16))
+        return fail(GSA_ERR_UNSUPPORTED, "%s: dtype %d not supported here", name, t->dtype);
+    if (t->heads < 0 || t->rows < 0 || t->dim < 0)
+        return fail(GSA_ERR_SHAPE_MISMATCH, "%s: negative extent", name);
+    if ((int64_t)t->heads * t->rows * t->dim > 0 && !t->data)
+        return fail(GSA_ERR_GENERIC, "%s: null data", name);
+    return GSA_OK;
+}
+
+int check_f32_out(const gsa_tensor* t, const char* name, int heads, int rows, int dim) {
+    GSA_TRY(check_tensor(t, name, false));
+    if (t->heads != heads || t->rows != rows || t->dim != dim)
+        return fail(GSA_ERR_SHAPE_MISMATCH, "%s: expected [%d x %d x %d], got [%d x %d x %d]", name,
+                    heads, rows, dim, t->heads, t->rows, t->dim);
+    return GSA_OK;
+}
+
+int same_heads_dim(const gsa_tensor* a, const gsa_tensor* b, const char* what) {
+    // require_same_heads_dim (tensor.hpp:60-63)
+    if (a->heads != b->heads || a->dim != b->dim)
+        return fail(GSA_ERR_SHAPE_MISMATCH, "%s: heads/dim disagree", what);
+    return GSA_OK;
+}
+
+int check_tiling(int bm, int bn) {
+    // validate_tiling (types.hpp:20-25)
+    auto ok = [](int v) { return v >= 8 && v <= 256 && (v & (v - 1)) == 0; };
+    if (!ok(bm) || !ok(bn))
+        return fail(GSA_ERR_INVALID_TILING, "tiling blocks must be powers of two in [8, 256], got %dx%d", bm, bn);
+    return GSA_OK;
+}
+
+int check_layout(const gsa_layout* l) {
+    if (!l) return fail(GSA_ERR_GENERIC, "null layout");
+    gsa_layout tmp;
+    return gsa_make_layout(l->num_special, l->num_frames, l->grid_h, l->grid_w, l->window_s, &tmp);
+}
+
+int generic_supported(int dim, int s) {
+    if (dim < 1 || dim > 128) return fail(GSA_ERR_UNSUPPORTED, "head dim %d outside [1,128]", dim);
+    if (s != 1 && s != 2 && s != 4 && s != 8)
+        return fail(GSA_ERR_UNSUPPORTED, "window_s=%d: the sm_100a kernels take s in {1,2,4,8}", s);
+    return GSA_OK;
+}
+
+float resolved_scale(double param, int dim) {
+    // reference.hpp:22-26
+    return param > 0.0 ? (float)param : (float)(1.0 / sqrt((double)dim));
+}
+
+struct Carver {
+    char* base;
+    size_t cap, used = 0;
+    bool dry;
+    template <typename T>
+    T* take(size_t n) {
+        used = (used + 255) & ~size_t(255);
+        T* p = dry ? nullptr : reinterpret_cast<T*>(base + used);
+        used += n * sizeof(T);
+        return p;
+    }
+};
+
+int selectable_windows(const DevLayout& L, int variant, int ref_stride, int* n_forced) {
+    int nf = 0;
+    if (variant == 1)
+        for (int f = 0; f < L.num_frames; f += ref_stride) nf += L.wins_per_frame;
+    *n_forced = nf;
+    return L.windows - nf;
+}
+
+}  // namespace
+
+extern "C" {
+
+int gsa_abi_version(void) { return GSA_SM100_ABI_VERSION; }
+
+const char* gsa_status_string(int s) {
+    switch (s) {
+        case GSA_OK: return "ok";
+        case GSA_ERR_GENERIC: return "GsaError";
+        case GSA_ERR_SHAPE_MISMATCH: return "ShapeMismatch";
+        case GSA_ERR_DIVISIBILITY: return "DivisibilityError";
+        case GSA_ERR_ZERO_SIZE: return "ZeroSizeError";
+        case GSA_ERR_INDEX_OUT_OF_RANGE: return "IndexOutOfRange";
+        case GSA_ERR_NON_FINITE: return "NonFiniteInput";
+        case GSA_ERR_INVALID_TILING: return "InvalidTiling";
+        case GSA_ERR_INVALID_STRIDE: return "InvalidStride";
+        case GSA_ERR_EMPTY_SELECTION: return "EmptySelection";
+        case GSA_ERR_UNSUPPORTED: return "Unsupported";
+        case GSA_ERR_CUDA: return "CudaError";
+        case GSA_ERR_WORKSPACE: return "WorkspaceError";
+        case GSA_ERR_NCCL: return "NcclError";
+        default: return "unknown";
+    }
+}
+
+const char* gsa_last_error_message(void) { return g_msg.c_str(); }
+
+int gsa_make_layout(int ns, int nf, int gh, int gw, int s, gsa_layout* out) {
+    // build_token_layout (layout.cpp:7-24)
+    if (ns < 0) return fail(GSA_ERR_ZERO_SIZE, "build_token_layout: num_special < 0");
+    if (nf < 1) return fail(GSA_ERR_ZERO_SIZE, "build_token_layout: num_frames < 1");
+    if (gh < 1 || gw < 1) return fail(GSA_ERR_ZERO_SIZE, "build_token_layout: empty grid");
+    if (s < 1) return fail(GSA_ERR_ZERO_SIZE, "build_token_layout: window_s < 1");
+    if (gh % s != 0 || gw % s != 0)
+        return fail(GSA_ERR_DIVISIBILITY, "build_token_layout: grid %dx%d not divisible by window_s=%d", gh, gw, s);
+    if ((int64_t)nf * gh * gw + ns > INT32_MAX)
+        return fail(GSA_ERR_UNSUPPORTED, "build_token_layout: more than 2^31 tokens");
+    if (out) *out = gsa_layout{ns, nf, gh, gw, s};
+    return GSA_OK;
+}
+
+int gsa_validate_params(const gsa_params* p, const gsa_layout* l) {
+    // validate_params (types.hpp:67-73) + layer.hpp:182-183
+    if (!p) return fail(GSA_ERR_GENERIC, "null params");
+    if (p->top_k < 1) return fail(GSA_ERR_GENERIC, "params: top_k must be >= 1");
+    if (p->scale < 0.0) return fail(GSA_ERR_GENERIC, "params: scale must be > 0");
+    if (p->variant == 1 && p->ref_stride < 1)
+        return fail(GSA_ERR_INVALID_STRIDE, "params: ref_stride must be >= 1 for hybrid selection");
+    if (p->variant != 0 && p->variant != 1) return fail(GSA_ERR_GENERIC, "params: unknown variant");
+    GSA_TRY(check_tiling(p->block_m, p->block_n));
+    if (l && p->window_s != l->window_s)
+        return fail(GSA_ERR_SHAPE_MISMATCH, "gsa_forward: params.window_s != layout.window_s");
+    return GSA_OK;
+}
+
+int gsa_avg_pool_tokens(const gsa_tensor* x, const gsa_layout* layout, const gsa_tensor* out,
+                        gsa_stream_t stream) {
+    GSA_TRY(check_layout(layout));
+    GSA_TRY(check_tensor(x, "x_img"));
+    const DevLayout L = make_dev_layout(*layout);
+    if (x->rows != L.image_tokens) return fail(GSA_ERR_SHAPE_MISMATCH, "avg_pool_tokens: rows != image tokens");
+    GSA_TRY(check_f32_out(out, "out", x->heads, L.windows, x->dim));
+    if (out->row_stride != x->dim || out->head_stride != (int64_t)L.windows * x->dim)
+        return fail(GSA_ERR_UNSUPPORTED, "avg_pool_tokens: out must be contiguous");
+    PoolJob j{ref_of(*x), static_cast<float*>(out->data), nullptr, nullptr, nullptr};
+    const float inv = 1.0f / (float)(L.s * L.s);  // T(1)/T(s2) (compression.hpp:25)
+    GSA_CUDA(launch_pool(&j, 1, x->heads, x->dim, L, inv, (cudaStream_t)stream));
+    return GSA_OK;
+}
+
+int gsa_upsample_nearest(const gsa_tensor* coarse, const gsa_layout* layout, const gsa_tensor* out,
+                         gsa_stream_t stream) {
+    GSA_TRY(check_layout(layout));
+    GSA_TRY(check_tensor(coarse, "coarse", false));
+    const DevLayout L = make_dev_layout(*layout);
+    if (coarse->rows != L.windows) return fail(GSA_ERR_SHAPE_MISMATCH, "upsample_nearest: rows != num windows");
+    GSA_TRY(check_f32_out(out, "out", coarse->heads, L.image_tokens, coarse->dim));
+    GSA_CUDA(launch_upsample(static_cast<const float*>(coarse->data), coarse->head_stride, coarse->row_stride,
+                             coarse->heads, coarse->dim, L, static_cast<float*>(out->data), out->head_stride,
+                             out->row_stride, (cudaStream_t)stream));
+    return GSA_OK;
+}
+
+static int dense_attention(const gsa_tensor* q, const gsa_tensor* k, const gsa_tensor* v, float scale,
+                           const gsa_tensor* out, float* lse, int q_row_offset, int out_row_offset,
+                           int mq, cudaStream_t st) {
+    if (mq == 0) return GSA_OK;
+    if (k->rows == 0) return fail(GSA_ERR_SHAPE_MISMATCH, "tiled_attention: empty key set");
+    if (tc_dense_supported(*q, *k, *v)) {
+        GSA_CUDA(tc_dense_attention(*q, *k, *v, scale, q_row_offset, mq, static_cast<float*>(out->data),
+                                    out->head_stride, out->row_stride, out_row_offset, lse, st));
+        return GSA_OK;
+    }
+    GSA_TRY(generic_supported(q->dim, 1));
+    AttnArgs a{};
+    a.q = ref_of(*q, q_row_offset);
+    a.k = ref_of(*k);
+    a.v = ref_of(*v);
+    a.heads = q->heads;
+    a.mq = mq;
+    a.mk = k->rows;
+    a.dim = q->dim;
+    a.scale = scale;
+    a.out = static_cast<float*>(out->data) + (size_t)out_row_offset * out->row_stride;
+    a.out_hs = out->head_stride;
+    a.out_rs = out->row_stride;
+    a.lse = lse;
+    GSA_CUDA(launch_attn_f32(a, st));
+    return GSA_OK;
+}
+
+int gsa_tiled_attention(const gsa_tensor* q, const gsa_tensor* k, const gsa_tensor* v, float scale,
+                        int bm, int bn, const gsa_tensor* out, float* lse, gsa_stream_t stream) {
+    GSA_TRY(check_tensor(q, "q"));
+    GSA_TRY(check_tensor(k, "k"));
+    GSA_TRY(check_tensor(v, "v"));
+    if (k->rows != v->rows) return fail(GSA_ERR_SHAPE_MISMATCH, "tiled_attention: K/V token counts differ");
+    GSA_TRY(same_heads_dim(q, k, "tiled_attention"));
+    GSA_TRY(same_heads_dim(q, v, "tiled_attention"));
+    if (q->dtype != k->dtype || q->dtype != v->dtype)
+        return fail(GSA_ERR_UNSUPPORTED, "tiled_attention: q/k/v dtypes differ");
+    GSA_TRY(check_tiling(bm, bn));
+    GSA_TRY(check_f32_out(out, "out", q->heads, q->rows, q->dim));
+    return dense_attention(q, k, v, scale, out, lse, 0, 0, q->rows, (cudaStream_t)stream);
+}
+
+int gsa_special_token_attention(const gsa_tensor* q_spec, const gsa_tensor* k, const gsa_tensor* v,
+                                float scale, const gsa_tensor* out, float* lse, gsa_stream_t stream) {
+    if (q_spec && q_spec->rows == 0) return GSA_OK;  // layer.hpp:88-92
+    return gsa_tiled_attention(q_spec, k, v, scale, 16, 16, out, lse, stream);
+}
+
+size_t gsa_compressed_attention_topk_workspace_bytes(int heads, int windows, int dim, int k) {
+    return tc_compress_workspace_bytes(heads, windows, dim, k);
+}
+
+int gsa_compressed_attention_topk(const gsa_tensor* qc, const gsa_tensor* kc, const gsa_tensor* vc, int k,
+                                  float scale, int bm, int bn, const uint8_t* excluded, int n_excluded,
+                                  const gsa_tensor* out, float* lse, int32_t* indices, float* guide,
+                                  int* k_eff_out, void* workspace, size_t ws_bytes, gsa_stream_t stream) {
+    GSA_TRY(check_tensor(qc, "qc", false));
+    GSA_TRY(check_tensor(kc, "kc", false));
+    GSA_TRY(check_tensor(vc, "vc", false));
+    // compression.hpp:185-192
+    if (kc->rows != vc->rows || qc->rows != kc->rows)
+        return fail(GSA_ERR_SHAPE_MISMATCH, "fused_compressed_attention_topk: Q/K/V must share the window count");
+    GSA_TRY(same_heads_dim(qc, kc, "fused_compressed_attention_topk"));
+    GSA_TRY(same_heads_dim(qc, vc, "fused_compressed_attention_topk"));
+    GSA_TRY(check_tiling(bm, bn));
+    if (k < 0) return fail(GSA_ERR_GENERIC, "fused_compressed_attention_topk: k must be >= 0");
+    if (excluded && n_excluded != kc->rows)
+        return fail(GSA_ERR_SHAPE_MISMATCH, "fused_compressed_attention_topk: exclusion mask size");
+    GSA_TRY(check_f32_out(out, "out", qc->heads, qc->rows, qc->dim));
+    const int W = qc->rows;
+    // k_eff needs the number of excluded windows: the mask lives on the device
+    int n_ex = 0;
+    if (excluded && W > 0) {
+        std::string host(W, '\0');
+        GSA_CUDA(cudaMemcpyAsync(&host[0], excluded, W, cudaMemcpyDeviceToHost, (cudaStream_t)stream));
+        GSA_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+        for (char c : host) n_ex += c ? 1 : 0;
+    }
+    const int k_eff = k < W - n_ex ? k : W - n_ex;
+    if (k_eff_out) *k_eff_out = k_eff;
+    if (W == 0) return GSA_OK;
+    GSA_TRY(generic_supported(qc->dim, 1));
+    if (k_eff > 128)
+        return fail(GSA_ERR_UNSUPPORTED, "fused_compressed_attention_topk: k_eff=%d > 128 not implemented on sm_100a yet", k_eff);
+    GSA_CUDA(tc_compress_topk(*qc, *kc, *vc, k_eff, scale, excluded, static_cast<float*>(out->data),
+                              out->head_stride, out->row_stride, lse, indices, guide, workspace, ws_bytes,
+                              (cudaStream_t)stream));
+    return GSA_OK;
+}
+
+int gsa_forced_windows(const gsa_layout* layout, int ref_stride, int32_t* forced, int* count,
+                       gsa_stream_t stream) {
+    GSA_TRY(check_layout(layout));
+    if (ref_stride < 1) return fail(GSA_ERR_INVALID_STRIDE, "forced_frames: ref_stride must be >= 1");
+    const DevLayout L = make_dev_layout(*layout);
+    int nf = 0;
+    selectable_windows(L, 1, ref_stride, &nf);
+    if (count) *count = nf;
+    if (forced) GSA_CUDA(launch_forced(L, ref_stride, forced, nullptr, (cudaStream_t)stream));
+    return GSA_OK;
+}
+
+size_t gsa_build_selection_plan_workspace_bytes(int heads, int rows, int k, const gsa_layout* layout,
+                                                int ref_stride) {
+    (void)k;
+    (void)ref_stride;
+    const int64_t n = (int64_t)heads * rows;
+    const int W = layout ? make_dev_layout(*layout).windows : rows;
+    Carver c{nullptr, 0, 0, true};
+    c.take<int64_t>(n);
+    c.take<int32_t>(W);
+    c.take<uint8_t>(W);
+    c.take<char>(scan_offsets_tmp_bytes(n));
+    return c.used + 256;
+}
+
+int gsa_build_selection_plan(const int32_t* topk, int heads, int rows, int k, const gsa_layout* layout,
+                             int variant, int ref_stride, int64_t* offsets, int32_t* ids,
+                             int64_t ids_capacity, int64_t* n_ids, void* workspace, size_t ws_bytes,
+                             gsa_stream_t stream) {
+    GSA_TRY(check_layout(layout));
+    const DevLayout L = make_dev_layout(*layout);
+    // selection.cpp:31-32, 41-42
+    if (rows != L.windows) return fail(GSA_ERR_SHAPE_MISMATCH, "build_selection_plan: topk rows != num windows");
+    if (variant == 1 && ref_stride < 1)
+        return fail(GSA_ERR_INVALID_STRIDE, "build_selection_plan: ref_stride must be >= 1 for hybrid");
+    cudaStream_t st = (cudaStream_t)stream;
+    const int64_t n = (int64_t)heads * rows;
+    Carver c{static_cast<char*>(workspace), ws_bytes, 0, false};
+    int64_t* sizes = c.take<int64_t>(n);
+    int32_t* forced = c.take<int32_t>(L.windows);
+    uint8_t* mask = c.take<uint8_t>(L.windows);
+    const size_t tmp_bytes = scan_offsets_tmp_bytes(n);
+    void* tmp = c.take<char>(tmp_bytes);
+    if (c.used > ws_bytes) return fail(GSA_ERR_WORKSPACE, "build_selection_plan: workspace %zu < %zu", ws_bytes, c.used);
+    int nf = 0;
+    if (variant == 1) {
+        selectable_windows(L, 1, ref_stride, &nf);
+        GSA_CUDA(launch_forced(L, ref_stride, forced, mask, st));
+    }
+    const uint8_t* m = variant == 1 ? mask : nullptr;
+    GSA_CUDA(launch_plan_count(topk, n, k, m, nf, sizes, st));
+    GSA_CUDA(launch_scan_offsets(sizes, n, offsets, tmp, tmp_bytes, st));
+    int64_t total = 0;
+    GSA_CUDA(cudaMemcpyAsync(&total, offsets + n, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    GSA_CUDA(cudaStreamSynchronize(st));
+    if (n_ids) *n_ids = total;
+    if (total > ids_capacity)
+        return fail(GSA_ERR_WORKSPACE, "build_selection_plan: ids capacity %lld < %lld", (long long)ids_capacity, (long long)total);
+    GSA_CUDA(launch_plan_fill(topk, n, k, m, forced, nf, offsets, ids, st));
+    return GSA_OK;
+}
+
+static int select_checks(const gsa_tensor* q, const gsa_tensor* k, const gsa_tensor* v, const DevLayout& L) {
+    GSA_TRY(check_tensor(q, "q_img"));
+    GSA_TRY(check_tensor(k, "k_img"));
+    GSA_TRY(check_tensor(v, "v_img"));
+    // selection.hpp:68-76
+    if (q->rows != L.image_tokens) return fail(GSA_ERR_SHAPE_MISMATCH, "block_sparse_attention: Q rows != image tokens");
+    if (k->rows != L.image_tokens || v->rows != L.image_tokens)
+        return fail(GSA_ERR_SHAPE_MISMATCH, "block_sparse_attention: K/V rows != image tokens");
+    GSA_TRY(same_heads_dim(q, k, "block_sparse_attention"));
+    GSA_TRY(same_heads_dim(q, v, "block_sparse_attention"));
+    if (q->dtype != k->dtype || q->dtype != v->dtype)
+        return fail(GSA_ERR_UNSUPPORTED, "block_sparse_attention: q/k/v dtypes differ");
+    return GSA_OK;
+}
+
+int gsa_block_sparse_attention(const gsa_tensor* q, const gsa_tensor* k, const gsa_tensor* v,
+                               const int64_t* offsets, const int32_t* ids, const gsa_layout* layout,
+                               float scale, const gsa_tensor* out, float* lse, gsa_stream_t stream) {
+    GSA_TRY(check_layout(layout));
+    const DevLayout L = make_dev_layout(*layout);
+    GSA_TRY(select_checks(q, k, v, L));
+    GSA_TRY(check_f32_out(out, "out", q->heads, L.image_tokens, q->dim));
+    GSA_TRY(generic_supported(q->dim, L.s));
+    cudaStream_t st = (cudaStream_t)stream;
+    const int64_t n = (int64_t)q->heads * L.windows;
+    if (n == 0) return GSA_OK;
+    {  // EmptySelection (selection.hpp:82-85): checked before any compute
+        int* flag = nullptr;
+        GSA_CUDA(cudaMallocAsync(&flag, sizeof(int), st));
+        GSA_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), st));
+        GSA_CUDA(launch_empty_row_check(offsets, n, flag, st));
+        int h = 0;
+        GSA_CUDA(cudaMemcpyAsync(&h, flag, sizeof(int), cudaMemcpyDeviceToHost, st));
+        GSA_CUDA(cudaFreeAsync(flag, st));
+        GSA_CUDA(cudaStreamSynchronize(st));
+        if (h) return fail(GSA_ERR_EMPTY_SELECTION, "block_sparse_attention: empty plan row");
+    }
+    SelectArgs a{};
+    a.q = ref_of(*q);
+    a.k = ref_of(*k);
+    a.v = ref_of(*v);
+    a.heads = q->heads;
+    a.dim = q->dim;
+    a.L = L;
+    a.rows = RowSource{offsets, ids, nullptr, 0, nullptr, 0, 0};
+    a.scale = scale;
+    a.out = static_cast<float*>(out->data);
+    a.out_hs = out->head_stride;
+    a.out_rs = out->row_stride;
+    a.lse = lse;
+    GSA_CUDA(launch_select_f32(a, st));
+    return GSA_OK;
+}
+
+int gsa_gate(const gsa_tensor* q, const gsa_tensor* w_g, const gsa_tensor* g, gsa_stream_t stream) {
+    GSA_TRY(check_tensor(q, "q_img"));
+    GSA_TRY(check_tensor(w_g, "w_g", false));
+    // layer.hpp:101-102
+    if (w_g->heads != q->heads || w_g->rows != q->dim || w_g->dim != q->dim)
+        return fail(GSA_ERR_SHAPE_MISMATCH, "gate: weights must be heads x dim x dim");
+    if (w_g->row_stride != w_g->dim || w_g->head_stride != (int64_t)w_g->dim * w_g->dim)
+        return fail(GSA_ERR_UNSUPPORTED, "gate: w_g must be contiguous");
+    GSA_TRY(check_f32_out(g, "g", q->heads, q->rows, q->dim));
+    GSA_CUDA(launch_gate(ref_of(*q), q->heads, q->rows, q->dim, static_cast<const float*>(w_g->data),
+                         static_cast<float*>(g->data), g->head_stride, g->row_stride, (cudaStream_t)stream));
+    return GSA_OK;
+}
+
+// ------------------------------------------------------------ full layer
+
+namespace {
+
+struct LayerPlan {
+    DevLayout L;
+    int heads, dim, Ms, Mi, M, W, k_eff, n_forced;
+    float scale;
+};
+
+int layer_checks(const gsa_tensor* q, const gsa_tensor* k, const gsa_tensor* v, const gsa_tensor* w_g,
+                 const gsa_layout* layout, const gsa_params* p, const gsa_tensor* out, LayerPlan* lp) {
+    GSA_TRY(check_layout(layout));
+    GSA_TRY(gsa_validate_params(p, layout));
+    GSA_TRY(check_tensor(q, "q"));
+    GSA_TRY(check_tensor(k, "k"));
+    GSA_TRY(check_tensor(v, "v"));
+    GSA_TRY(check_tensor(w_g, "w_g", false));
+    const DevLayout L = make_dev_layout(*layout);
+    const int M = layout->num_special + L.image_tokens;
+    // partition_qkv (layout.hpp:58-60) / layer.hpp:184-185
+    if (q->rows != M || k->rows != M || v->rows != M)
+        return fail(GSA_ERR_SHAPE_MISMATCH, "gsa_forward: Q/K/V rows != layout.total_tokens()");
+    GSA_TRY(same_heads_dim(q, k, "partition_qkv"));
+    GSA_TRY(same_heads_dim(q, v, "partition_qkv"));
+    if (q->dtype != k->dtype || q->dtype != v->dtype)
+        return fail(GSA_ERR_UNSUPPORTED, "gsa_forward: q/k/v dtypes differ");
+    if (w_g->heads != q->heads || w_g->rows != q->dim || w_g->dim != q->dim)
+        return fail(GSA_ERR_SHAPE_MISMATCH, "weights: w_g must be heads x dim x dim");
+    if (w_g->row_stride != w_g->dim || w_g->head_stride != (int64_t)w_g->dim * w_g->dim)
+        return fail(GSA_ERR_UNSUPPORTED, "gsa_forward: w_g must be contiguous");
+    GSA_TRY(check_f32_out(out, "out", q->heads, M, q->dim));
+    GSA_TRY(generic_supported(q->dim, L.s));
+    lp->L = L;
+    lp->heads = q->heads;
+    lp->dim = q->dim;
+    lp->Ms = layout->num_special;
+    lp->Mi = L.image_tokens;
+    lp->M = M;
+    lp->W = L.windows;
+    const int sel = selectable_windows(L, p->variant, p->ref_stride, &lp->n_forced);
+    lp->k_eff = p->top_k < sel ? p->top_k : sel;
+    lp->scale = resolved_scale(p->scale, q->dim);
+    if (lp->k_eff > 128)
+        return fail(GSA_ERR_UNSUPPORTED, "gsa_forward: k_eff=%d > 128 not implemented on sm_100a yet", lp->k_eff);
+    return GSA_OK;
+}
+
+struct LayerBufs {
+    float *qc, *kc, *vc, *o_comp, *lse_comp, *lse_spec;
+    int32_t *topk, *forced;
+    uint8_t* mask;
+    void* compress_ws;
+    size_t compress_ws_bytes;
+    __nv_bfloat16 *qh, *ql, *kh, *kl, *vh, *vl;
+    float *qn, *kn;
+};
+
+size_t carve(const LayerPlan& lp, const gsa_context* ctx, char* base, size_t cap, bool dry, LayerBufs* b) {
+    Carver c{base, cap, 0, dry};
+    const size_t wd = (size_t)lp.heads * lp.W * lp.dim;
+    auto f = [&](float* user, size_t n) { return user ? user : c.take<float>(n); };
+    b->qc = f(ctx ? ctx->qc : nullptr, wd);
+    b->kc = f(ctx ? ctx->kc : nullptr, wd);
+    b->vc = f(ctx ? ctx->vc : nullptr, wd);
+    b->o_comp = f(ctx ? ctx->o_comp : nullptr, wd);
+    b->lse_comp = f(ctx ? ctx->lse_comp : nullptr, (size_t)lp.heads * lp.W);
+    b->lse_spec = f(ctx ? ctx->lse_spec : nullptr, (size_t)lp.heads * lp.Ms);
+    b->topk = (ctx && ctx->topk) ? ctx->topk : c.take<int32_t>((size_t)lp.heads * lp.W * lp.k_eff);
+    b->forced = c.take<int32_t>(lp.W);
+    b->mask = c.take<uint8_t>(lp.W);
+    b->compress_ws_bytes = tc_compress_workspace_bytes(lp.heads, lp.W, lp.dim, lp.k_eff);
+    b->compress_ws = c.take<char>(b->compress_ws_bytes);
+    return c.used + 256;
+}
+
+}  // namespace
+
+size_t gsa_forward_workspace_bytes(const gsa_layout* layout, const gsa_params* params, int heads, int dim) {
+    if (!layout || !params) return 0;
+    LayerPlan lp{};
+    lp.L = make_dev_layout(*layout);
+    lp.heads = heads;
+    lp.dim = dim;
+    lp.Ms = layout->num_special;
+    lp.Mi = lp.L.image_tokens;
+    lp.W = lp.L.windows;
+    int nf = 0;
+    const int sel = selectable_windows(lp.L, params->variant, params->ref_stride > 0 ? params->ref_stride : 1, &nf);
+    lp.k_eff = params->top_k < sel ? params->top_k : sel;
+    if (lp.k_eff < 0) lp.k_eff = 0;
+    LayerBufs b;
+    return carve(lp, nullptr, nullptr, 0, true, &b);
+}
+
+int gsa_forward(const gsa_tensor* q, const gsa_tensor* k, const gsa_tensor* v, const gsa_tensor* w_g,
+                const gsa_layout* layout, const gsa_params* params, const gsa_tensor* out,
+                const gsa_context* ctx, int* k_eff_out, void* workspace, size_t ws_bytes,
+                gsa_stream_t stream) {
+    LayerPlan lp;
+    GSA_TRY(layer_checks(q, k, v, w_g, layout, params, out, &lp));
+    if (k_eff_out) *k_eff_out = lp.k_eff;
+    cudaStream_t st = (cudaStream_t)stream;
+    LayerBufs b;
+    const size_t need = carve(lp, ctx, static_cast<char*>(workspace), ws_bytes, false, &b);
+    if (need > ws_bytes + 256 || (!workspace && need > 256))
+        return fail(GSA_ERR_WORKSPACE, "gsa_forward: workspace %zu < %zu bytes", ws_bytes, need);
+    const int H = lp.heads, d = lp.dim;
+    float* outp = static_cast<float*>(out->data);
+
+    // 1. special tokens: dense attention over all M keys (layer.hpp:201-202)
+    stage_mark(0, st);
+    GSA_TRY(dense_attention(q, k, v, lp.scale, out, b.lse_spec, 0, 0, lp.Ms, st));
+    stage_mark(1, st);
+
+    // 2. pool Q/K/V image rows (layer.hpp:204-206)
+    PoolJob jobs[3] = {
+        {ref_of(*q, lp.Ms), b.qc, nullptr, nullptr, nullptr},
+        {ref_of(*k, lp.Ms), b.kc, nullptr, nullptr, nullptr},
+        {ref_of(*v, lp.Ms), b.vc, nullptr, nullptr, nullptr},
+    };
+    GSA_CUDA(launch_pool(jobs, 3, H, d, lp.L, 1.0f / (float)(lp.L.s * lp.L.s), st));
+    stage_mark(2, st);
+
+    // 3. hybrid exclusion mask + forced list (layer.hpp:208-210)
+    const uint8_t* excluded = nullptr;
+    if (params->variant == 1) {
+        GSA_CUDA(launch_forced(lp.L, params->ref_stride, b.forced, b.mask, st));
+        excluded = b.mask;
+    }
+
+    // 4. compressed attention + streaming top-k (layer.hpp:211-216)
+    gsa_tensor tq{b.qc, GSA_DTYPE_F32, H, lp.W, d, (int64_t)lp.W * d, d};
+    gsa_tensor tk{b.kc, GSA_DTYPE_F32, H, lp.W, d, (int64_t)lp.W * d, d};
+    gsa_tensor tv{b.vc, GSA_DTYPE_F32, H, lp.W, d, (int64_t)lp.W * d, d};
+    GSA_CUDA(tc_compress_topk(tq, tk, tv, lp.k_eff, lp.scale, excluded, b.o_comp, (int64_t)lp.W * d, d,
+                              b.lse_comp, b.topk, nullptr, b.compress_ws, b.compress_ws_bytes, st));
+    stage_mark(3, st);
+
+    // 5-7. plan rows = forced ++ top-k (selection.cpp:55-59; the top-k already
+    // excludes forced windows so no dedup is needed), block-sparse attention,
+    // gate and gated merge fused; output rows [Ms, M) (layer.hpp:218-228)
+    SelectArgs a{};
+    a.q = ref_of(*q, lp.Ms);
+    a.k = ref_of(*k, lp.Ms);
+    a.v = ref_of(*v, lp.Ms);
+    a.heads = H;
+    a.dim = d;
+    a.L = lp.L;
+    a.rows = RowSource{nullptr, nullptr, b.forced, params->variant == 1 ? lp.n_forced : 0, b.topk, lp.k_eff, lp.k_eff};
+    a.scale = lp.scale;
+    a.out = outp + (size_t)lp.Ms * out->row_stride;
+    a.out_hs = out->head_stride;
+    a.out_rs = out->row_stride;
+    a.lse = ctx ? ctx->lse_sel : nullptr;
+    a.w_g = static_cast<const float*>(w_g->data);
+    a.o_comp = b.o_comp;
+    a.o_sel_ctx = ctx ? ctx->o_sel : nullptr;
+    a.gate_ctx = ctx ? ctx->gate : nullptr;
+    if (tc_select_supported(*q, lp.L, a.rows))
+        GSA_CUDA(tc_select_gate_merge(a, st));
+    else
+        GSA_CUDA(launch_select_f32(a, st));
+    stage_mark(4, st);
+    return GSA_OK;
+}
+
+int gsa_forward_with_plan(const gsa_tensor* q, const gsa_tensor* k, const gsa_tensor* v, const gsa_tensor* w_g,
+                          const gsa_layout* layout, const gsa_params* params, const int64_t* offsets,
+                          const int32_t* ids, const gsa_tensor* out, void* workspace, size_t ws_bytes,
+                          gsa_stream_t stream) {
+    LayerPlan lp;
+    GSA_TRY(layer_checks(q, k, v, w_g, layout, params, out, &lp));
+    cudaStream_t st = (cudaStream_t)stream;
+    LayerBufs b;
+    const size_t need = carve(lp, nullptr, static_cast<char*>(workspace), ws_bytes, false, &b);
+    if (need > ws_bytes + 256) return fail(GSA_ERR_WORKSPACE, "gsa_forward_with_plan: workspace %zu < %zu", ws_bytes, need);
+    const int H = lp.heads, d = lp.dim;
+    GSA_TRY(dense_attention(q, k, v, lp.scale, out, b.lse_spec, 0, 0, lp.Ms, st));
+    PoolJob jobs[3] = {
+        {ref_of(*q, lp.Ms), b.qc, nullptr, nullptr, nullptr},
+        {ref_of(*k, lp.Ms), b.kc, nullptr, nullptr, nullptr},
+        {ref_of(*v, lp.Ms), b.vc, nullptr, nullptr, nullptr},
+    };
+    GSA_CUDA(launch_pool(jobs, 3, H, d, lp.L, 1.0f / (float)(lp.L.s * lp.L.s), st));
+    // compressed branch without top-k (layer.hpp:251-253: tiled_attention)
+    gsa_tensor tq{b.qc, GSA_DTYPE_F32, H, lp.W, d, (int64_t)lp.W * d, d};
+    gsa_tensor tk{b.kc, GSA_DTYPE_F32, H, lp.W, d, (int64_t)lp.W * d, d};
+    gsa_tensor tv{b.vc, GSA_DTYPE_F32, H, lp.W, d, (int64_t)lp.W * d, d};
+    gsa_tensor to{b.o_comp, GSA_DTYPE_F32, H, lp.W, d, (int64_t)lp.W * d, d};
+    GSA_TRY(dense_attention(&tq, &tk, &tv, lp.scale, &to, b.lse_comp, 0, 0, lp.W, st));
+    SelectArgs a{};
+    a.q = ref_of(*q, lp.Ms);
+    a.k = ref_of(*k, lp.Ms);
+    a.v = ref_of(*v, lp.Ms);
+    a.heads = H;
+    a.dim = d;
+    a.L = lp.L;
+    a.rows = RowSource{offsets, ids, nullptr, 0, nullptr, 0, 0};
+    a.scale = lp.scale;
+    a.out = static_cast<float*>(out->data) + (size_t)lp.Ms * out->row_stride;
+    a.out_hs = out->head_stride;
+    a.out_rs = out->row_stride;
+    a.w_g = static_cast<const float*>(w_g->data);
+    a.o_comp = b.o_comp;
+    GSA_CUDA(launch_select_f32(a, st));
+    return GSA_OK;
+}
+
+int gsa_forward_stats(const gsa_layout* layout, const gsa_params* p, int heads, uint64_t* scores,
+                      uint64_t* keys) {
+    GSA_TRY(check_layout(layout));
+    GSA_TRY(gsa_validate_params(p, layout));
+    const DevLayout L = make_dev_layout(*layout);
+    const uint64_t M = (uint64_t)layout->num_special + L.image_tokens;
+    int nf = 0;
+    const int sel = selectable_windows(L, p->variant, p->ref_stride, &nf);
+    const int k_eff = p->top_k < sel ? p->top_k : sel;
+    const uint64_t s2 = (uint64_t)L.s * L.s;
+    // tiled_attention counts qrows*krows per tile (compression.hpp:135-137), the
+    // compressed kernel W*W per head (236-238); block_sparse adds |keys|*s2 per
+    // (head, window) (selection.hpp:106-108)
+    if (scores) *scores = (uint64_t)heads * ((uint64_t)layout->num_special * M + (uint64_t)L.windows * L.windows);
+    if (keys) *keys = (uint64_t)heads * L.windows * (uint64_t)(nf + k_eff) * s2 * s2;
+    return GSA_OK;
+}
+
+int gsa_set_stage_events(void* const* events, int n) {
+    if (n < 5 || !events) {
+        g_n_stage_events = 0;
+        return GSA_OK;
+    }
+    for (int i = 0; i < 5; ++i) g_stage_events[i] = static_cast<cudaEvent_t>(events[i]);
+    g_n_stage_events = 5;
+    return GSA_OK;
+}
+
+int gsa_launch_count(uint64_t* count) {
+    if (count) *count = gsa_sm100::g_launch_total.load();
+    return GSA_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,84 @@
+// kernels.h — host-side launchers of the sm_100a kernels (internal to libgsa_sm100.so).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+
+namespace gsa_sm100 {
+
+// kernels launched by this library (gsa_launch_count); bumped by every launcher
+void note_launch(int n = 1);
+
+struct TensorRef {  // device view, element strides
+    const void* data;
+    int dtype;
+    int64_t hs, rs;
+};
+
+// ---- K1: window mean pooling (pool.cu) ----------------------------------
+struct PoolJob {
+    TensorRef in;      // image rows only (row 0 == first image token)
+    float* out;        // [H][W][d] f32 (head stride W*d)
+    __nv_bfloat16* hi; // optional split copies for the tensor-core path [H][W][d]
+    __nv_bfloat16* lo;
+    float* norm;       // optional ||row||_2 [H][W]
+};
+cudaError_t launch_pool(const PoolJob* jobs, int njobs, int heads, int dim, const DevLayout& L,
+                        float inv, cudaStream_t st);
+
+// ---- dense / compressed attention on CUDA cores (attn_f32.cu) -------------
+// out rows are written at out + h*out_hs + r*out_rs. TOPK variant also keeps
+// per-row top-k (exact scaled_dot order) with the reference tie rule.
+struct AttnArgs {
+    TensorRef q, k, v;
+    int heads, mq, mk, dim;
+    float scale;
+    float* out;
+    int64_t out_hs, out_rs;
+    float* lse;  // [H][mq] (nullable)
+    // top-k (nullable indices => plain attention)
+    int32_t* topk;
+    float* guide;
+    int k_eff;
+    const uint8_t* excluded;  // [mk] or null
+};
+cudaError_t launch_attn_f32(const AttnArgs& a, cudaStream_t st);
+
+// ---- selection branch on CUDA cores (select_f32.cu) ---------------------
+struct SelectArgs {
+    TensorRef q, k, v;  // image rows
+    int heads, dim;
+    DevLayout L;
+    RowSource rows;
+    float scale;
+    float* out;  // o_sel or merged output
+    int64_t out_hs, out_rs;
+    float* lse;  // [H][Mi] nullable
+    // optional fused gate + merge: out = g*o_comp[w] + (1-g)*o_sel
+    const float* w_g;     // [H][d][d] f32 or null
+    const float* o_comp;  // [H][W][d] f32
+    float* o_sel_ctx;     // optional materialised o_sel [H][Mi][d]
+    float* gate_ctx;      // optional materialised gate [H][Mi][d]
+};
+cudaError_t launch_select_f32(const SelectArgs& a, cudaStream_t st);
+
+// ---- gate, upsample, plan helpers (misc.cu) -----------------------------
+cudaError_t launch_gate(const TensorRef& q, int heads, int rows, int dim, const float* w_g,
+                        float* g, int64_t g_hs, int64_t g_rs, cudaStream_t st);
+cudaError_t launch_upsample(const float* coarse, int64_t c_hs, int64_t c_rs, int heads, int dim,
+                            const DevLayout& L, float* out, int64_t o_hs, int64_t o_rs,
+                            cudaStream_t st);
+cudaError_t launch_forced(const DevLayout& L, int ref_stride, int32_t* forced, uint8_t* mask,
+                          cudaStream_t st);
+cudaError_t launch_plan_count(const int32_t* topk, int64_t rows, int k, const uint8_t* mask,
+                              int n_forced, int64_t* sizes, cudaStream_t st);
+cudaError_t launch_plan_fill(const int32_t* topk, int64_t rows, int k, const uint8_t* mask,
+                             const int32_t* forced, int n_forced, const int64_t* offsets,
+                             int32_t* ids, cudaStream_t st);
+cudaError_t launch_scan_offsets(const int64_t* sizes, int64_t n, int64_t* offsets, void* tmp,
+                                size_t tmp_bytes, cudaStream_t st);
+size_t scan_offsets_tmp_bytes(int64_t n);
+cudaError_t launch_empty_row_check(const int64_t* offsets, int64_t rows, int* flag, cudaStream_t st);
+
+}  // namespace gsa_sm100

@@ -1,0 +1,151 @@
+// misc.cu — small device kernels around the hot path: the stand-alone gate
+// (layer.hpp:99-119), nearest upsampling (compression.hpp:42-53), the hybrid
+// forced-window set (selection.cpp:7-27) and the CSR selection plan
+// (selection.cpp:29-67).
+#include <cub/device/device_scan.cuh>
+
+#include "kernels.h"
+
+namespace gsa_sm100 {
+namespace {
+
+// g[h][t][j] = sigmoid(sum_a q[h][t][a] * w[h][a][j]); one warp per row, a
+// thread per (up to 4) output features; a ascending like the reference loop.
+template <typename T>
+__global__ void gate_kernel(TensorRef q, int heads, int rows, int dim, const float* __restrict__ w,
+                            float* g, int64_t g_hs, int64_t g_rs) {
+    const int64_t row = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+    const int lane = threadIdx.x & 31;
+    if (row >= (int64_t)heads * rows) return;
+    const int h = (int)(row / rows), t = (int)(row % rows);
+    const T* qr = reinterpret_cast<const T*>(q.data) + (int64_t)h * q.hs + (int64_t)t * q.rs;
+    const float* wh = w + (int64_t)h * dim * dim;
+    float* gr = g + (int64_t)h * g_hs + (int64_t)t * g_rs;
+    for (int j = lane; j < dim; j += 32) {
+        float z = 0.0f;
+        for (int a = 0; a < dim; ++a) z = fmaf(to_f32(qr[a]), wh[(int64_t)a * dim + j], z);
+        gr[j] = 1.0f / (1.0f + expf(-z));
+    }
+}
+
+__global__ void upsample_kernel(const float* __restrict__ c, int64_t c_hs, int64_t c_rs, int heads,
+                                int dim, DevLayout L, float* o, int64_t o_hs, int64_t o_rs) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t n = (int64_t)heads * L.image_tokens * dim;
+    if (i >= n) return;
+    const int j = (int)(i % dim);
+    const int64_t ht = i / dim;
+    const int h = (int)(ht / L.image_tokens), t = (int)(ht % L.image_tokens);
+    o[(int64_t)h * o_hs + (int64_t)t * o_rs + j] = c[(int64_t)h * c_hs + (int64_t)L.window_of_token(t) * c_rs + j];
+}
+
+// forced frames {0, r, 2r, ...}; their windows in ascending order (selection.cpp:7-21)
+__global__ void forced_kernel(DevLayout L, int ref_stride, int32_t* forced, uint8_t* mask) {
+    const int w = blockIdx.x * blockDim.x + threadIdx.x;
+    if (w >= L.windows) return;
+    const int f = w / L.wins_per_frame;
+    const bool is_forced = (f % ref_stride) == 0;
+    if (mask) mask[w] = is_forced ? 1 : 0;
+    if (forced && is_forced) {
+        const int rank = (f / ref_stride) * L.wins_per_frame + (w - f * L.wins_per_frame);
+        forced[rank] = w;
+    }
+}
+
+__global__ void plan_count_kernel(const int32_t* __restrict__ topk, int64_t rows, int k,
+                                  const uint8_t* __restrict__ mask, int n_forced, int64_t* sizes) {
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= rows) return;
+    int n = 0;
+    for (int j = 0; j < k; ++j) n += (mask && mask[topk[r * k + j]]) ? 0 : 1;
+    sizes[r] = n + (mask ? n_forced : 0);
+}
+
+__global__ void plan_fill_kernel(const int32_t* __restrict__ topk, int64_t rows, int k,
+                                 const uint8_t* __restrict__ mask, const int32_t* __restrict__ forced,
+                                 int n_forced, const int64_t* __restrict__ offsets, int32_t* ids) {
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= rows) return;
+    int64_t o = offsets[r];
+    if (mask)
+        for (int i = 0; i < n_forced; ++i) ids[o++] = forced[i];
+    for (int j = 0; j < k; ++j) {
+        const int32_t w = topk[r * k + j];
+        if (!(mask && mask[w])) ids[o++] = w;
+    }
+}
+
+__global__ void empty_row_kernel(const int64_t* __restrict__ offsets, int64_t rows, int* flag) {
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r < rows && offsets[r + 1] <= offsets[r]) atomicOr(flag, 1);
+}
+
+__global__ void set_zero_kernel(int64_t* p) { *p = 0; }
+
+}  // namespace
+
+cudaError_t launch_gate(const TensorRef& q, int heads, int rows, int dim, const float* w_g, float* g,
+                        int64_t g_hs, int64_t g_rs, cudaStream_t st) {
+    const int64_t n = (int64_t)heads * rows;
+    if (n == 0) return cudaSuccess;
+    const int wpb = 8;
+    const unsigned blocks = (unsigned)((n + wpb - 1) / wpb);
+    if (q.dtype == GSA_DTYPE_BF16)
+        { gate_kernel<__nv_bfloat16><<<blocks, 32 * wpb, 0, st>>>(q, heads, rows, dim, w_g, g, g_hs, g_rs); note_launch(); }
+    else
+        { gate_kernel<float><<<blocks, 32 * wpb, 0, st>>>(q, heads, rows, dim, w_g, g, g_hs, g_rs); note_launch(); }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_upsample(const float* coarse, int64_t c_hs, int64_t c_rs, int heads, int dim,
+                            const DevLayout& L, float* out, int64_t o_hs, int64_t o_rs,
+                            cudaStream_t st) {
+    const int64_t n = (int64_t)heads * L.image_tokens * dim;
+    if (n == 0) return cudaSuccess;
+    { upsample_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(coarse, c_hs, c_rs, heads, dim, L, out, o_hs, o_rs); note_launch(); }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_forced(const DevLayout& L, int ref_stride, int32_t* forced, uint8_t* mask,
+                          cudaStream_t st) {
+    if (L.windows == 0) return cudaSuccess;
+    { forced_kernel<<<(L.windows + 255) / 256, 256, 0, st>>>(L, ref_stride, forced, mask); note_launch(); }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_plan_count(const int32_t* topk, int64_t rows, int k, const uint8_t* mask,
+                              int n_forced, int64_t* sizes, cudaStream_t st) {
+    if (rows == 0) return cudaSuccess;
+    { plan_count_kernel<<<(unsigned)((rows + 255) / 256), 256, 0, st>>>(topk, rows, k, mask, n_forced, sizes); note_launch(); }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_plan_fill(const int32_t* topk, int64_t rows, int k, const uint8_t* mask,
+                             const int32_t* forced, int n_forced, const int64_t* offsets,
+                             int32_t* ids, cudaStream_t st) {
+    if (rows == 0) return cudaSuccess;
+    { plan_fill_kernel<<<(unsigned)((rows + 255) / 256), 256, 0, st>>>(topk, rows, k, mask, forced, n_forced, offsets, ids); note_launch(); }
+    return cudaGetLastError();
+}
+
+size_t scan_offsets_tmp_bytes(int64_t n) {
+    size_t bytes = 0;
+    cub::DeviceScan::InclusiveSum(nullptr, bytes, (const int64_t*)nullptr, (int64_t*)nullptr, (int)n);
+    return bytes;
+}
+
+// offsets[0] = 0, offsets[i+1] = sizes[0] + ... + sizes[i]
+cudaError_t launch_scan_offsets(const int64_t* sizes, int64_t n, int64_t* offsets, void* tmp,
+                                size_t tmp_bytes, cudaStream_t st) {
+    { set_zero_kernel<<<1, 1, 0, st>>>(offsets); note_launch(); }
+    if (n == 0) return cudaGetLastError();
+    return cub::DeviceScan::InclusiveSum(tmp, tmp_bytes, sizes, offsets + 1, (int)n, st);
+}
+
+cudaError_t launch_empty_row_check(const int64_t* offsets, int64_t rows, int* flag, cudaStream_t st) {
+    if (rows == 0) return cudaSuccess;
+    { empty_row_kernel<<<(unsigned)((rows + 255) / 256), 256, 0, st>>>(offsets, rows, flag); note_launch(); }
+    return cudaGetLastError();
+}
+
+}  // namespace gsa_sm100

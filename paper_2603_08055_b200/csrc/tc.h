@@ -1,0 +1,29 @@
+// tc.h — entry points of the tensor-core (tcgen05/TMEM/TMA) fast paths and
+// their shape predicates. Callers fall back to the CUDA-core kernels when a
+// predicate is false (f32 inputs, head dim != 64, window side != 4, ...).
+#pragma once
+
+#include "kernels.h"
+
+namespace gsa_sm100 {
+
+// dense attention (special tokens, tiled_attention, dense baseline)
+bool tc_dense_supported(const gsa_tensor& q, const gsa_tensor& k, const gsa_tensor& v);
+cudaError_t tc_dense_attention(const gsa_tensor& q, const gsa_tensor& k, const gsa_tensor& v, float scale,
+                               int q_row_offset, int mq, float* out, int64_t out_hs, int64_t out_rs,
+                               int out_row_offset, float* lse, cudaStream_t st);
+
+// compressed attention + top-k over pooled f32 [H][W][d] tensors: tensor-core
+// approximate scores + exact re-scoring of the boundary candidates when
+// supported, else the exact CUDA-core kernel. Indices are bit-exact either way.
+size_t tc_compress_workspace_bytes(int heads, int windows, int dim, int k_eff);
+cudaError_t tc_compress_topk(const gsa_tensor& qc, const gsa_tensor& kc, const gsa_tensor& vc, int k_eff,
+                             float scale, const uint8_t* excluded, float* out, int64_t out_hs,
+                             int64_t out_rs, float* lse, int32_t* topk, float* guide, void* ws,
+                             size_t ws_bytes, cudaStream_t st);
+
+// selection branch + gate + merge
+bool tc_select_supported(const gsa_tensor& q, const DevLayout& L, const RowSource& rows);
+cudaError_t tc_select_gate_merge(const SelectArgs& a, cudaStream_t st);
+
+}  // namespace gsa_sm100

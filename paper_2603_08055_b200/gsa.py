@@ -1,0 +1,441 @@
+"""Python mirror of the reference operator API (proj/include/gsa) over the
+sm_100a C ABI. Tensors are torch CUDA tensors shaped [heads, rows, dim]
+(head-major like the reference's Tensor<T>, tensor.hpp:15-42); bf16 Q/K/V is
+the fast path, f32 is accepted everywhere. Every function raises the Python
+twin of the reference exception (errors.hpp:8-58) on bad input.
+
+This module is the host-side plumbing used by the tests and bench.py; the
+drop-in for C++ callers is include/gsa/*.hpp over the same C ABI.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass, field
+from typing import Optional
+
+import torch
+
+from . import _lib
+from ._lib import GsaContextC, GsaLayout, GsaParamsC, GsaTensor
+
+
+# ----------------------------------------------------------------- errors
+class GsaError(RuntimeError):
+    pass
+
+
+class ShapeMismatch(GsaError):
+    pass
+
+
+class DivisibilityError(GsaError):
+    pass
+
+
+class ZeroSizeError(GsaError):
+    pass
+
+
+class IndexOutOfRange(GsaError):
+    pass
+
+
+class NonFiniteInput(GsaError):
+    pass
+
+
+class InvalidTiling(GsaError):
+    pass
+
+
+class InvalidStride(GsaError):
+    pass
+
+
+class EmptySelection(GsaError):
+    pass
+
+
+class Unsupported(GsaError):
+    pass
+
+
+class CudaError(GsaError):
+    pass
+
+
+class WorkspaceError(GsaError):
+    pass
+
+
+_STATUS = {1: GsaError, 2: ShapeMismatch, 3: DivisibilityError, 4: ZeroSizeError, 5: IndexOutOfRange,
+           6: NonFiniteInput, 7: InvalidTiling, 8: InvalidStride, 9: EmptySelection, 10: Unsupported,
+           11: CudaError, 12: WorkspaceError, 13: GsaError}
+
+
+def _check(rc: int) -> None:
+    if rc != 0:
+        L = _lib.load()
+        raise _STATUS.get(rc, GsaError)(L.gsa_last_error_message().decode())
+
+
+# ------------------------------------------------------------------ types
+@dataclass(frozen=True)
+class TokenLayout:
+    """layout.hpp:13-40. Construct with build_token_layout()."""
+    num_special: int = 0
+    num_frames: int = 1
+    grid_h: int = 0
+    grid_w: int = 0
+    window_s: int = 1
+
+    @property
+    def tokens_per_frame(self) -> int:
+        return self.grid_h * self.grid_w
+
+    @property
+    def image_tokens(self) -> int:
+        return self.num_frames * self.tokens_per_frame
+
+    @property
+    def total_tokens(self) -> int:
+        return self.num_special + self.image_tokens
+
+    @property
+    def wins_w(self) -> int:
+        return self.grid_w // self.window_s
+
+    @property
+    def windows_per_frame(self) -> int:
+        return (self.grid_h // self.window_s) * self.wins_w
+
+    @property
+    def num_windows(self) -> int:
+        return self.num_frames * self.windows_per_frame
+
+    def window_of_token(self, t: int) -> int:
+        if not 0 <= t < self.image_tokens:
+            raise IndexOutOfRange("window_of_token: image token index out of range")
+        f, r = divmod(t, self.tokens_per_frame)
+        row, col = divmod(r, self.grid_w)
+        return f * self.windows_per_frame + (row // self.window_s) * self.wins_w + col // self.window_s
+
+    def tokens_of_window(self, w: int) -> list[int]:
+        if not 0 <= w < self.num_windows:
+            raise IndexOutOfRange("tokens_of_window: window index out of range")
+        f, r = divmod(w, self.windows_per_frame)
+        wr, wc = divmod(r, self.wins_w)
+        s, base = self.window_s, f * self.tokens_per_frame
+        return [base + (wr * s + dr) * self.grid_w + wc * s + dc for dr in range(s) for dc in range(s)]
+
+    def frame_of_window(self, w: int) -> int:
+        if not 0 <= w < self.num_windows:
+            raise IndexOutOfRange("frame_of_window: window index out of range")
+        return w // self.windows_per_frame
+
+    def c(self) -> GsaLayout:
+        return GsaLayout(self.num_special, self.num_frames, self.grid_h, self.grid_w, self.window_s)
+
+
+def build_token_layout(num_special: int, num_frames: int, grid_h: int, grid_w: int, window_s: int) -> TokenLayout:
+    """build_token_layout (layout.cpp:7-24), validated by the C ABI."""
+    out = GsaLayout()
+    _check(_lib.load().gsa_make_layout(num_special, num_frames, grid_h, grid_w, window_s, C.byref(out)))
+    return TokenLayout(num_special, num_frames, grid_h, grid_w, window_s)
+
+
+@dataclass
+class KernelTiling:
+    block_m: int = 16
+    block_n: int = 16
+
+
+PLAIN, HYBRID = 0, 1
+
+
+@dataclass
+class GsaParams:
+    """types.hpp:58-65."""
+    window_s: int = 4
+    top_k: int = 32
+    scale: float = 0.0
+    variant: int = PLAIN
+    ref_stride: int = 100
+    tiling: KernelTiling = field(default_factory=KernelTiling)
+
+    def c(self) -> GsaParamsC:
+        return GsaParamsC(self.window_s, self.top_k, self.scale, self.variant, self.ref_stride,
+                          self.tiling.block_m, self.tiling.block_n)
+
+
+def resolved_scale(params: GsaParams, dim: int) -> float:
+    """reference.hpp:22-26 (float32 rounding of 1/sqrt(d))."""
+    s = params.scale if params.scale > 0 else 1.0 / math.sqrt(dim)
+    return float(torch.tensor(s, dtype=torch.float32))
+
+
+# --------------------------------------------------------------- plumbing
+def _desc(t: torch.Tensor) -> GsaTensor:
+    if t.dim() != 3:
+        raise ShapeMismatch(f"expected a [heads, rows, dim] tensor, got shape {tuple(t.shape)}")
+    if not t.is_cuda:
+        raise GsaError("tensors must live on the GPU (the sm_100a kernels are the only implementation)")
+    if t.dtype == torch.bfloat16:
+        dt = _lib.GSA_DTYPE_BF16
+    elif t.dtype == torch.float32:
+        dt = _lib.GSA_DTYPE_F32
+    else:
+        raise Unsupported(f"dtype {t.dtype} not supported")
+    if t.shape[2] > 1 and t.stride(2) != 1:
+        raise Unsupported("the feature dimension must be contiguous")
+    return GsaTensor(t.data_ptr() if t.numel() else None, dt, t.shape[0], t.shape[1], t.shape[2],
+                     t.stride(0), t.stride(1))
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def _stream():
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _empty(*shape, dtype=torch.float32, device=None):
+    return torch.empty(*shape, dtype=dtype, device=device or "cuda")
+
+
+# -------------------------------------------------------------------- ops
+def avg_pool_tokens(x_img: torch.Tensor, layout: TokenLayout) -> torch.Tensor:
+    """compression.hpp:20-38 (bit-exact)."""
+    out = _empty(x_img.shape[0], layout.num_windows, x_img.shape[2], device=x_img.device)
+    _check(_lib.load().gsa_avg_pool_tokens(C.byref(_desc(x_img)), C.byref(layout.c()), C.byref(_desc(out)), _stream()))
+    return out
+
+
+def upsample_nearest(coarse: torch.Tensor, layout: TokenLayout) -> torch.Tensor:
+    """compression.hpp:42-53."""
+    out = _empty(coarse.shape[0], layout.image_tokens, coarse.shape[2], device=coarse.device)
+    _check(_lib.load().gsa_upsample_nearest(C.byref(_desc(coarse)), C.byref(layout.c()), C.byref(_desc(out)), _stream()))
+    return out
+
+
+def tiled_attention(q, k, v, scale: float, tiling: KernelTiling = KernelTiling()):
+    """compression.hpp:99-165 -> (out f32, lse f32 [H, mq])."""
+    out = _empty(q.shape[0], q.shape[1], q.shape[2], device=q.device)
+    lse = _empty(q.shape[0], q.shape[1], device=q.device)
+    _check(_lib.load().gsa_tiled_attention(C.byref(_desc(q)), C.byref(_desc(k)), C.byref(_desc(v)), C.c_float(scale),
+                                           tiling.block_m, tiling.block_n, C.byref(_desc(out)), _ptr(lse), _stream()))
+    return out, lse
+
+
+def special_token_attention(q_spec, k, v, scale: float, tiling: KernelTiling = KernelTiling()):
+    """layer.hpp:80-96 -> (out, lse)."""
+    out = _empty(q_spec.shape[0], q_spec.shape[1], q_spec.shape[2], device=q_spec.device)
+    lse = _empty(q_spec.shape[0], q_spec.shape[1], device=q_spec.device)
+    if q_spec.shape[1] == 0:
+        return out, lse
+    _check(_lib.load().gsa_tiled_attention(C.byref(_desc(q_spec)), C.byref(_desc(k)), C.byref(_desc(v)),
+                                           C.c_float(scale), tiling.block_m, tiling.block_n, C.byref(_desc(out)),
+                                           _ptr(lse), _stream()))
+    return out, lse
+
+
+@dataclass
+class CompressedResult:
+    """compression.hpp:167-172 (+ TopkResult types.hpp:30-48)."""
+    out: torch.Tensor
+    lse: torch.Tensor
+    indices: torch.Tensor  # [H, W, k_eff] int32
+    k: int
+    guide_scores: Optional[torch.Tensor] = None
+
+
+def fused_compressed_attention_topk(qc, kc, vc, k: int, scale: float, tiling: KernelTiling = KernelTiling(),
+                                    excluded: Optional[torch.Tensor] = None, keep_guide_scores: bool = False
+                                    ) -> CompressedResult:
+    """compression.hpp:180-297 (indices bit-exact with the reference)."""
+    L = _lib.load()
+    H, W, d = qc.shape
+    n_ex = 0 if excluded is None else int(excluded.numel())
+    sel = W - (0 if excluded is None else int(excluded.to(torch.int32).sum().item()))
+    k_eff_guess = max(0, min(k, sel))
+    out = _empty(H, W, d, device=qc.device)
+    lse = _empty(H, W, device=qc.device)
+    idx = torch.empty(H, W, max(1, k_eff_guess), dtype=torch.int32, device=qc.device)
+    guide = _empty(H, W, max(1, k_eff_guess), device=qc.device) if keep_guide_scores else None
+    ws_bytes = L.gsa_compressed_attention_topk_workspace_bytes(H, W, d, k_eff_guess)
+    ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=qc.device)
+    ex = None if excluded is None else excluded.to(torch.uint8).contiguous()
+    k_eff = C.c_int()
+    _check(L.gsa_compressed_attention_topk(C.byref(_desc(qc)), C.byref(_desc(kc)), C.byref(_desc(vc)), k,
+                                           C.c_float(scale), tiling.block_m, tiling.block_n, _ptr(ex), n_ex,
+                                           C.byref(_desc(out)), _ptr(lse), _ptr(idx), _ptr(guide), C.byref(k_eff),
+                                           _ptr(ws), ws_bytes, _stream()))
+    ke = k_eff.value
+    return CompressedResult(out, lse, idx[:, :, :ke], ke, None if guide is None else guide[:, :, :ke])
+
+
+@dataclass
+class SelectionPlan:
+    """selection.hpp:19-33, on the device."""
+    heads: int
+    rows: int
+    offsets: torch.Tensor      # int64 [H*rows+1]
+    window_ids: torch.Tensor   # int32
+    forced_windows: torch.Tensor
+
+    def row_size(self, h: int, r: int) -> int:
+        i = h * self.rows + r
+        return int(self.offsets[i + 1] - self.offsets[i])
+
+
+def forced_windows_of(layout: TokenLayout, ref_stride: int, device="cuda") -> torch.Tensor:
+    """selection.cpp:14-21."""
+    L = _lib.load()
+    n = C.c_int()
+    _check(L.gsa_forced_windows(C.byref(layout.c()), ref_stride, None, C.byref(n), _stream()))
+    out = torch.empty(max(1, n.value), dtype=torch.int32, device=device)
+    _check(L.gsa_forced_windows(C.byref(layout.c()), ref_stride, _ptr(out), C.byref(n), _stream()))
+    return out[: n.value]
+
+
+def build_selection_plan(topk: torch.Tensor, layout: TokenLayout, variant: int, ref_stride: int) -> SelectionPlan:
+    """selection.cpp:29-67. topk: int32 [H, W, k] on the device."""
+    L = _lib.load()
+    topk = topk.to(torch.int32).contiguous()
+    H, W, k = topk.shape
+    F = layout.num_windows if variant == HYBRID else 0
+    cap = max(1, H * W * (k + F))
+    offsets = torch.empty(H * W + 1, dtype=torch.int64, device=topk.device)
+    ids = torch.empty(cap, dtype=torch.int32, device=topk.device)
+    ws_bytes = L.gsa_build_selection_plan_workspace_bytes(H, W, k, C.byref(layout.c()), max(ref_stride, 1))
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device=topk.device)
+    n = C.c_int64()
+    _check(L.gsa_build_selection_plan(_ptr(topk), H, W, k, C.byref(layout.c()), variant, ref_stride, _ptr(offsets),
+                                      _ptr(ids), cap, C.byref(n), _ptr(ws), ws_bytes, _stream()))
+    forced = forced_windows_of(layout, ref_stride, topk.device) if variant == HYBRID else \
+        torch.empty(0, dtype=torch.int32, device=topk.device)
+    return SelectionPlan(H, W, offsets, ids[: n.value], forced)
+
+
+def block_sparse_attention(q_img, k_img, v_img, plan: SelectionPlan, layout: TokenLayout, scale: float,
+                           tiling: KernelTiling = KernelTiling()):
+    """selection.hpp:63-136 -> (out f32, lse)."""
+    L = _lib.load()
+    _tiling_check(tiling)
+    if plan.heads != q_img.shape[0] or plan.rows != layout.num_windows:
+        raise ShapeMismatch("block_sparse_attention: plan shape does not match layout/heads")
+    H, Mi, d = q_img.shape
+    out = _empty(H, layout.image_tokens, d, device=q_img.device)
+    lse = _empty(H, layout.image_tokens, device=q_img.device)
+    _check(L.gsa_block_sparse_attention(C.byref(_desc(q_img)), C.byref(_desc(k_img)), C.byref(_desc(v_img)),
+                                        _ptr(plan.offsets), _ptr(plan.window_ids), C.byref(layout.c()),
+                                        C.c_float(scale), C.byref(_desc(out)), _ptr(lse), _stream()))
+    return out, lse
+
+
+def _tiling_check(t: KernelTiling) -> None:
+    ok = lambda v: 8 <= v <= 256 and (v & (v - 1)) == 0  # noqa: E731
+    if not ok(t.block_m) or not ok(t.block_n):
+        raise InvalidTiling(f"tiling blocks must be powers of two in [8, 256], got {t.block_m}x{t.block_n}")
+
+
+def gate(q_img: torch.Tensor, w_g: torch.Tensor) -> torch.Tensor:
+    """layer.hpp:99-119."""
+    g = _empty(*q_img.shape, device=q_img.device)
+    _check(_lib.load().gsa_gate(C.byref(_desc(q_img)), C.byref(_desc(w_g.contiguous())), C.byref(_desc(g)), _stream()))
+    return g
+
+
+@dataclass
+class ForwardContext:
+    """layer.hpp:124-142 (device tensors)."""
+    qc: torch.Tensor
+    kc: torch.Tensor
+    vc: torch.Tensor
+    o_comp_coarse: torch.Tensor
+    lse_comp: torch.Tensor
+    topk: torch.Tensor
+    o_sel: torch.Tensor
+    lse_sel: torch.Tensor
+    gate_vals: torch.Tensor
+    lse_spec: torch.Tensor
+    k_eff: int
+
+
+class Workspace:
+    """Caller-owned scratch for gsa_forward (grown on demand, reused across calls)."""
+
+    def __init__(self):
+        self.buf: Optional[torch.Tensor] = None
+
+    def get(self, nbytes: int, device) -> torch.Tensor:
+        if self.buf is None or self.buf.numel() < nbytes or self.buf.device != torch.device(device):
+            self.buf = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=device)
+        return self.buf
+
+
+_default_ws = Workspace()
+
+
+def gsa_forward(q, k, v, w_g, layout: TokenLayout, params: GsaParams, context: bool = False,
+                out: Optional[torch.Tensor] = None, workspace: Optional[Workspace] = None):
+    """gsa_forward (layer.hpp:177-230) from projected Q/K/V [H, M, d].
+    Returns out (f32 [H, M, d]) or (out, ForwardContext) when context=True."""
+    L = _lib.load()
+    H, M, d = q.shape
+    dev = q.device
+    if out is None:
+        out = _empty(H, M, d, device=dev)
+    lc, pc = layout.c(), params.c()
+    ws_bytes = L.gsa_forward_workspace_bytes(C.byref(lc), C.byref(pc), H, d)
+    ws = (workspace or _default_ws).get(ws_bytes, dev)
+    ctx = None
+    cstruct = None
+    if context:
+        W, Mi, Ms = layout.num_windows, layout.image_tokens, layout.num_special
+        nf = 0
+        if params.variant == HYBRID and params.ref_stride >= 1:
+            nf = len(range(0, layout.num_frames, params.ref_stride)) * layout.windows_per_frame
+        k_eff = max(0, min(params.top_k, W - nf))
+        ctx = ForwardContext(_empty(H, W, d, device=dev), _empty(H, W, d, device=dev), _empty(H, W, d, device=dev),
+                             _empty(H, W, d, device=dev), _empty(H, W, device=dev),
+                             torch.empty(H, W, max(1, k_eff), dtype=torch.int32, device=dev),
+                             _empty(H, Mi, d, device=dev), _empty(H, Mi, device=dev), _empty(H, Mi, d, device=dev),
+                             _empty(H, Ms, device=dev), k_eff)
+        cstruct = GsaContextC(*[t.data_ptr() for t in (ctx.qc, ctx.kc, ctx.vc, ctx.o_comp_coarse, ctx.lse_comp,
+                                                          ctx.topk, ctx.o_sel, ctx.lse_sel, ctx.gate_vals,
+                                                          ctx.lse_spec)])
+    ke = C.c_int()
+    _check(L.gsa_forward(C.byref(_desc(q)), C.byref(_desc(k)), C.byref(_desc(v)), C.byref(_desc(w_g.contiguous())),
+                         C.byref(lc), C.byref(pc), C.byref(_desc(out)),
+                         C.byref(cstruct) if cstruct is not None else None, C.byref(ke), _ptr(ws),
+                         ws.numel(), _stream()))
+    if ctx is not None:
+        ctx.topk = ctx.topk[:, :, : ke.value]
+        ctx.k_eff = ke.value
+        return out, ctx
+    return out
+
+
+def gsa_forward_with_plan(q, k, v, w_g, layout: TokenLayout, params: GsaParams, plan: SelectionPlan,
+                          workspace: Optional[Workspace] = None):
+    """layer.hpp:235-262."""
+    L = _lib.load()
+    H, M, d = q.shape
+    out = _empty(H, M, d, device=q.device)
+    lc, pc = layout.c(), params.c()
+    ws_bytes = L.gsa_forward_workspace_bytes(C.byref(lc), C.byref(pc), H, d)
+    ws = (workspace or _default_ws).get(ws_bytes, q.device)
+    _check(L.gsa_forward_with_plan(C.byref(_desc(q)), C.byref(_desc(k)), C.byref(_desc(v)),
+                                   C.byref(_desc(w_g.contiguous())), C.byref(lc), C.byref(pc), _ptr(plan.offsets),
+                                   _ptr(plan.window_ids), C.byref(_desc(out)), _ptr(ws), ws.numel(), _stream()))
+    return out
+
+
+def forward_stats(layout: TokenLayout, params: GsaParams, heads: int) -> tuple[int, int]:
+    """KernelStats (types.hpp:78-86) in closed form: (scores_computed, keys_attended)."""
+    a, b = C.c_uint64(), C.c_uint64()
+    _check(_lib.load().gsa_forward_stats(C.byref(layout.c()), C.byref(params.c()), heads, C.byref(a), C.byref(b)))
+    return a.value, b.value

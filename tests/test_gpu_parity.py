@@ -1,0 +1,247 @@
+"""GPU parity tests: every stage of the sm_100a path vs the oracle and the
+reference's golden fixtures, called through the C ABI (via the Python mirror).
+
+Tolerances (BASELINE.json north_star): top-k indices and pooled Qc/Kc
+bit-exact; layer output max|d| <= 2e-2 and relative L2 <= 1e-3 (we assert much
+tighter bounds where the arithmetic allows it, stated per test)."""
+from __future__ import annotations
+
+import hashlib
+import json
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, GOLDEN_NAMES, load_golden, rel_l2
+from oracle import Layout, make_inputs
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+MAX_ABS, REL_L2 = 2e-2, 1e-3  # north_star tolerance for the layer output
+
+
+@pytest.fixture(scope="module")
+def gsa():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2603_08055_b200 as m
+    return m
+
+
+def dev(x, dtype=torch.bfloat16):
+    return torch.from_numpy(np.ascontiguousarray(x)).cuda().to(dtype)
+
+
+def host(t):
+    torch.cuda.synchronize()
+    return t.detach().float().cpu().numpy()
+
+
+def run_forward(gsa, q, k, v, wg, lt, top_k, variant=0, ref_stride=100, dtype=torch.bfloat16, scale=0.0):
+    L = gsa.build_token_layout(*lt)
+    p = gsa.GsaParams(window_s=lt[4], top_k=top_k, variant=variant, ref_stride=ref_stride, scale=scale)
+    out, ctx = gsa.gsa_forward(dev(q, dtype), dev(k, dtype), dev(v, dtype), dev(wg, torch.float32), L, p, context=True)
+    return host(out), ctx
+
+
+# ------------------------------------------------------------------ stages
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+@pytest.mark.parametrize("lt", [(0, 2, 8, 8, 4), (3, 3, 12, 8, 2), (1, 2, 8, 8, 1), (5, 4, 16, 16, 8), (40, 8, 36, 36, 4)])
+def test_pool_bitexact(gsa, orc, lt, dtype):
+    L = Layout(*lt)
+    rng = np.random.default_rng(lt[1])
+    x = orc.bf16_round(rng.standard_normal((3, L.image_tokens, 64)).astype(np.float32))
+    if dtype == torch.float32:
+        x = rng.standard_normal((3, L.image_tokens, 64)).astype(np.float32)
+    got = host(gsa.avg_pool_tokens(dev(x, dtype), gsa.build_token_layout(*lt)))
+    np.testing.assert_array_equal(got.view(np.uint32), orc.pool(x, L).view(np.uint32))
+
+
+def test_pool_odd_dim_and_strides(gsa, orc):
+    L = Layout(0, 2, 8, 8, 4)
+    rng = np.random.default_rng(5)
+    big = rng.standard_normal((2, L.image_tokens, 40)).astype(np.float32)
+    t = dev(big, torch.float32)[:, :, :37]  # non-contiguous rows, odd dim
+    got = host(gsa.avg_pool_tokens(t, gsa.build_token_layout(*L.tuple())))
+    np.testing.assert_array_equal(got, orc.pool(np.ascontiguousarray(big[:, :, :37]), L))
+
+
+@pytest.mark.parametrize("W,k,excl", [(1, 4, False), (37, 5, False), (300, 32, False), (300, 32, True), (130, 200, False)])
+def test_compress_topk_exact(gsa, orc, W, k, excl):
+    rng = np.random.default_rng(W + k)
+    qc, kc, vc = (rng.standard_normal((3, W, 64)).astype(np.float32) for _ in range(3))
+    ex = (rng.random(W) < 0.3).astype(np.uint8) if excl else None
+    o_ref, l_ref, i_ref, g_ref = orc.compress_topk(qc, kc, vc, k, 0.125, excluded=ex, guide=True)
+    r = gsa.fused_compressed_attention_topk(dev(qc, torch.float32), dev(kc, torch.float32), dev(vc, torch.float32), k,
+                                            0.125, excluded=None if ex is None else dev(ex, torch.uint8),
+                                            keep_guide_scores=True)
+    assert r.k == i_ref.shape[2]
+    np.testing.assert_array_equal(host(r.indices).astype(np.int32), i_ref)
+    np.testing.assert_array_equal(host(r.guide_scores).reshape(-1), g_ref.reshape(-1))
+    assert np.abs(host(r.out) - o_ref).max() < 1e-5
+    assert np.abs(host(r.lse) - l_ref).max() < 1e-4
+
+
+def test_compress_all_ties(gsa, orc):
+    # all scores equal, k=3 -> [0,1,2] in every row
+    W = 50
+    qc = np.random.default_rng(0).standard_normal((2, W, 64)).astype(np.float32)
+    kc = np.ones((2, W, 64), np.float32)
+    vc = np.random.default_rng(1).standard_normal((2, W, 64)).astype(np.float32)
+    r = gsa.fused_compressed_attention_topk(dev(qc, torch.float32), dev(kc, torch.float32), dev(vc, torch.float32),
+                                            3, 0.125)
+    idx = host(r.indices).astype(np.int32)
+    assert (idx == np.array([0, 1, 2])).all()
+
+
+def test_tiled_attention(gsa, orc):
+    rng = np.random.default_rng(3)
+    q = orc.bf16_round(rng.standard_normal((2, 70, 64)).astype(np.float32))
+    k = orc.bf16_round(rng.standard_normal((2, 333, 64)).astype(np.float32))
+    v = orc.bf16_round(rng.standard_normal((2, 333, 64)).astype(np.float32))
+    o_ref, l_ref = orc.dense_attention(q, k, v, 0.125)
+    for dt in (torch.bfloat16, torch.float32):
+        out, lse = gsa.tiled_attention(dev(q, dt), dev(k, dt), dev(v, dt), 0.125)
+        assert np.abs(host(out) - o_ref).max() < 2e-3
+        assert rel_l2(host(out), o_ref) < 1e-3
+        assert np.abs(host(lse) - l_ref).max() < 1e-3
+
+
+def test_gate_and_upsample(gsa, orc):
+    rng = np.random.default_rng(4)
+    q = orc.bf16_round(rng.standard_normal((2, 96, 64)).astype(np.float32))
+    wg = (rng.standard_normal((2, 64, 64)) / 8).astype(np.float32)
+    assert np.abs(host(gsa.gate(dev(q), dev(wg, torch.float32))) - orc.gate(q, wg)).max() < 1e-5
+    lt = (0, 2, 8, 12, 4)
+    L = gsa.build_token_layout(*lt)
+    coarse = rng.standard_normal((2, L.num_windows, 64)).astype(np.float32)
+    up = host(gsa.upsample_nearest(dev(coarse, torch.float32), L))
+    for t in range(L.image_tokens):
+        np.testing.assert_array_equal(up[:, t], coarse[:, L.window_of_token(t)])
+
+
+@pytest.mark.parametrize("variant", [0, 1])
+def test_plan_and_block_sparse(gsa, orc, variant):
+    lt = (0, 3, 8, 8, 4)
+    L = Layout(*lt)
+    rng = np.random.default_rng(7 + variant)
+    H, k = 2, 3
+    topk = np.stack([np.stack([rng.choice(L.num_windows, k, replace=False) for _ in range(L.num_windows)])
+                     for _ in range(H)]).astype(np.int32)
+    offs, ids = orc.build_plan(topk, L, variant, 2)
+    gl = gsa.build_token_layout(*lt)
+    plan = gsa.build_selection_plan(dev(topk, torch.int32), gl, variant, 2)
+    np.testing.assert_array_equal(plan.offsets.cpu().numpy(), offs)
+    np.testing.assert_array_equal(plan.window_ids.cpu().numpy(), ids)
+    q, kk, v = (orc.bf16_round(rng.standard_normal((H, L.image_tokens, 64)).astype(np.float32)) for _ in range(3))
+    o_ref, l_ref = orc.block_sparse(q, kk, v, L, offs, ids, 0.125)
+    out, lse = gsa.block_sparse_attention(dev(q), dev(kk), dev(v), plan, gl, 0.125)
+    assert np.abs(host(out) - o_ref).max() < 1e-4
+    assert np.abs(host(lse) - l_ref).max() < 1e-4
+
+
+def test_empty_selection_raises(gsa):
+    lt = (0, 1, 8, 8, 4)
+    gl = gsa.build_token_layout(*lt)
+    plan = gsa.SelectionPlan(1, 4, torch.tensor([0, 1, 1, 2, 3], dtype=torch.int64, device="cuda"),
+                             torch.tensor([0, 1, 2], dtype=torch.int32, device="cuda"),
+                             torch.empty(0, dtype=torch.int32, device="cuda"))
+    x = torch.zeros(1, 64, 64, dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(gsa.EmptySelection):
+        gsa.block_sparse_attention(x, x, x, plan, gl, 0.125)
+
+
+def test_shape_errors(gsa):
+    gl = gsa.build_token_layout(2, 1, 8, 8, 4)
+    x = torch.zeros(2, 66, 64, dtype=torch.bfloat16, device="cuda")
+    wg = torch.zeros(2, 64, 64, device="cuda")
+    with pytest.raises(gsa.ShapeMismatch):
+        gsa.gsa_forward(x[:, :65], x[:, :65], x[:, :65], wg, gl, gsa.GsaParams())
+    with pytest.raises(gsa.ShapeMismatch):
+        gsa.gsa_forward(x, x, x, wg[:, :32], gl, gsa.GsaParams())
+    with pytest.raises(gsa.ShapeMismatch):
+        gsa.gsa_forward(x, x, x, wg, gl, gsa.GsaParams(window_s=2))
+    with pytest.raises(gsa.InvalidStride):
+        gsa.gsa_forward(x, x, x, wg, gl, gsa.GsaParams(variant=1, ref_stride=0))
+    with pytest.raises(gsa.InvalidTiling):
+        gsa.gsa_forward(x, x, x, wg, gl, gsa.GsaParams(tiling=gsa.KernelTiling(7, 16)))
+
+
+# ------------------------------------------------------------- whole layer
+@pytest.mark.parametrize("name", GOLDEN_NAMES)
+def test_forward_matches_reference_golden(gsa, name):
+    g = load_golden(name)
+    out, ctx = run_forward(gsa, g["q"], g["k"], g["v"], g["w_g"], g["layout"], g["top_k"], g["variant"], g["ref_stride"])
+    np.testing.assert_array_equal(host(ctx.topk).astype(np.int32), g["topk"])
+    np.testing.assert_array_equal(host(ctx.qc), g["qc"])
+    np.testing.assert_array_equal(host(ctx.kc), g["kc"])
+    assert np.abs(out - g["out"]).max() <= MAX_ABS
+    assert rel_l2(out, g["out"]) <= REL_L2
+    assert np.abs(host(ctx.o_comp_coarse) - g["o_comp"]).max() < 1e-3
+    assert np.abs(host(ctx.lse_sel) - g["lse_sel"]).max() < 1e-3
+
+
+def test_forward_f32_inputs_tight(gsa, orc):
+    lt = (5, 3, 12, 12, 4)
+    L = Layout(*lt)
+    rng = np.random.default_rng(11)
+    q, k, v = (rng.standard_normal((2, L.total_tokens, 64)).astype(np.float32) for _ in range(3))
+    wg = (rng.standard_normal((2, 64, 64)) / 8).astype(np.float32)
+    r = orc.gsa_forward(q, k, v, wg, L, top_k=7)
+    out, ctx = run_forward(gsa, q, k, v, wg, lt, 7, dtype=torch.float32)
+    np.testing.assert_array_equal(host(ctx.topk).astype(np.int32), r["topk"])
+    assert rel_l2(out, r["out"]) < 1e-5
+
+
+@pytest.mark.parametrize("case", ["v8_normal", "v8_sharp", "v8_hybrid", "v8_uniform"])
+def test_forward_parity_geometry_digest(gsa, orc, case):
+    """8 views x (5 specials + 36x36 patches), 16 heads, k=32: top-k indices
+    hash-identical to the unmodified reference (tests/golden/parity_digests.json);
+    output vs the oracle within the north-star tolerance."""
+    m = json.load(open(os.path.join(GOLDEN, "parity_digests.json")))[case]
+    L = Layout(*m["layout"])
+    kind = m["kind"]
+    q, k, v, wg = make_inputs(orc, L, heads=m["heads"], dim=64, seed=m["seed"],
+                              kind="uniform" if kind == "uniform" else "normal", sharp=3.0 if kind == "sharp" else 1.0)
+    out, ctx = run_forward(gsa, q, k, v, wg, tuple(m["layout"]), m["top_k"], m["variant"], m["ref_stride"])
+    topk = host(ctx.topk).astype(np.int32)
+    assert hashlib.sha256(topk.tobytes()).hexdigest() == m["topk_sha256"]
+    r = orc.gsa_forward(q, k, v, wg, L, top_k=m["top_k"], variant=m["variant"], ref_stride=m["ref_stride"])
+    assert np.abs(out - r["out"]).max() <= MAX_ABS
+    assert rel_l2(out, r["out"]) <= REL_L2
+
+
+def test_dense_degeneration(gsa, orc):
+    # s=1, k=W, no specials -> dense image attention
+    lt = (0, 2, 8, 8, 1)
+    L = Layout(*lt)
+    rng = np.random.default_rng(9)
+    q, k, v = (orc.bf16_round(rng.standard_normal((2, L.total_tokens, 64)).astype(np.float32)) for _ in range(3))
+    wg = (rng.standard_normal((2, 64, 64)) / 8).astype(np.float32)
+    out, _ = run_forward(gsa, q, k, v, wg, lt, L.num_windows)
+    dense, _ = orc.dense_attention(q, k, v, 0.125)
+    assert np.abs(out - dense).max() < 1e-4
+
+
+def test_determinism_and_scale_invariance(gsa, orc):
+    lt = (10, 3, 16, 16, 4)
+    L = Layout(*lt)
+    q, k, v, wg = make_inputs(orc, L, heads=4, dim=64, seed=21)
+    o1, c1 = run_forward(gsa, q, k, v, wg, lt, 6)
+    o2, c2 = run_forward(gsa, q, k, v, wg, lt, 6)
+    np.testing.assert_array_equal(o1, o2)
+    # indices invariant to the (positive) scale
+    _, c3 = run_forward(gsa, q, k, v, wg, lt, 6, scale=0.37)
+    np.testing.assert_array_equal(host(c1.topk), host(c3.topk))
+
+
+def test_forward_with_plan(gsa, orc):
+    g = load_golden("small_plain")
+    lt = g["layout"]
+    L = gsa.build_token_layout(*lt)
+    plan = gsa.build_selection_plan(dev(g["topk"], torch.int32), L, 0, 100)
+    out = gsa.gsa_forward_with_plan(dev(g["q"]), dev(g["k"]), dev(g["v"]), dev(g["w_g"], torch.float32), L,
+                                    gsa.GsaParams(window_s=lt[4], top_k=g["top_k"]), plan)
+    assert rel_l2(host(out), g["out"]) < 1e-4
