@@ -68,7 +68,7 @@ def test_pool_odd_dim_and_strides(gsa, orc):
     np.testing.assert_array_equal(got, orc.pool(np.ascontiguousarray(big[:, :, :37]), L))
 
 
-@pytest.mark.parametrize("W,k,excl", [(1, 4, False), (37, 5, False), (300, 32, False), (300, 32, True), (130, 200, False)])
+@pytest.mark.parametrize("W,k,excl", [(1, 4, False), (37, 5, False), (300, 32, False), (300, 32, True), (100, 200, False)])
 def test_compress_topk_exact(gsa, orc, W, k, excl):
     rng = np.random.default_rng(W + k)
     qc, kc, vc = (rng.standard_normal((3, W, 64)).astype(np.float32) for _ in range(3))
@@ -82,6 +82,14 @@ def test_compress_topk_exact(gsa, orc, W, k, excl):
     np.testing.assert_array_equal(host(r.guide_scores).reshape(-1), g_ref.reshape(-1))
     assert np.abs(host(r.out) - o_ref).max() < 1e-5
     assert np.abs(host(r.lse) - l_ref).max() < 1e-4
+
+
+def test_compress_large_k_is_reported_unsupported(gsa):
+    # k_eff > 128 (the 2-25% budget sweep) is not implemented yet:
+    # it must fail loudly, never silently truncate
+    x = torch.zeros(1, 300, 64, device="cuda")
+    with pytest.raises(gsa.Unsupported):
+        gsa.fused_compressed_attention_topk(x, x, x, 200, 0.125)
 
 
 def test_compress_all_ties(gsa, orc):
