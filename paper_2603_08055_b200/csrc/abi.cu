@@ -493,8 +493,7 @@ struct LayerBufs {
     uint8_t* mask;
     void* compress_ws;
     size_t compress_ws_bytes;
-    __nv_bfloat16 *qh, *ql, *kh, *kl, *vh, *vl;
-    float *qn, *kn;
+    uint8_t* wg_prep;
 };
 
 size_t carve(const LayerPlan& lp, const gsa_context* ctx, char* base, size_t cap, bool dry, LayerBufs* b) {
@@ -512,6 +511,7 @@ size_t carve(const LayerPlan& lp, const gsa_context* ctx, char* base, size_t cap
     b->mask = c.take<uint8_t>(lp.W);
     b->compress_ws_bytes = tc_compress_workspace_bytes(lp.heads, lp.W, lp.dim, lp.k_eff);
     b->compress_ws = c.take<char>(b->compress_ws_bytes);
+    b->wg_prep = c.take<uint8_t>(tc_select_workspace_bytes(lp.heads));
     return c.used + 256;
 }
 
@@ -598,6 +598,7 @@ int gsa_forward(const gsa_tensor* q, const gsa_tensor* k, const gsa_tensor* v, c
     a.o_comp = b.o_comp;
     a.o_sel_ctx = ctx ? ctx->o_sel : nullptr;
     a.gate_ctx = ctx ? ctx->gate : nullptr;
+    a.wg_prep = b.wg_prep;
     if (tc_select_supported(*q, lp.L, a.rows))
         GSA_CUDA(tc_select_gate_merge(a, st));
     else

@@ -60,6 +60,7 @@ struct SelectArgs {
     const float* o_comp;  // [H][W][d] f32
     float* o_sel_ctx;     // optional materialised o_sel [H][Mi][d]
     float* gate_ctx;      // optional materialised gate [H][Mi][d]
+    uint8_t* wg_prep;     // tensor-core path scratch: W_g hi/lo split, H * 16 KB
 };
 cudaError_t launch_select_f32(const SelectArgs& a, cudaStream_t st);
 

@@ -1,0 +1,642 @@
+// select_tc.cu — K4: block-sparse selection attention fused with the gate and
+// the gated merge, on tcgen05 tensor cores with TMA gathers (sm_100a).
+//
+// Reference: block_sparse_attention (selection.hpp:63-136), gate
+// (layer.hpp:99-119), assemble_image_output (layer.hpp:154-170).
+//
+// One work item = (head h, query window w): its 16 queries attend the 16 keys
+// of every window in the plan row (forced ++ top-k). Persistent CTAs (one per
+// SM) walk the items head-major; inside a CTA the items' key windows form one
+// global stream of "groups" (<= 32 windows = 512 keys each):
+//
+//   warp 0 (TMA)   : gathers each selected window of K and V straight from the
+//                    head-major [H][M][64] bf16 tensors with a 4-D tensor map
+//                    (box 64 x 4 x 4 = one 2 KB window, 128B-swizzled), 8
+//                    windows per 16 KB ring stage; Q tile per item; W_g (hi/lo
+//                    bf16 split, pre-swizzled) per head.
+//   warp 1 (MMA)   : S^T[128 keys x 16 q] = K_chunk . Q^T   (M=128, N=16, K=64)
+//                    G^T[64 x 16]        = W_g^T . Q^T       (hi + lo, M=64)
+//                    O^T[64 x 16]       += V_chunk^T . P^T   (P hi + lo, M=64, K=16/step)
+//                    accumulators in TMEM; S double-buffered across groups so
+//                    S(j+1) overlaps the softmax of group j.
+//   warps 2-5      : exact two-phase softmax over the whole group (keys are the
+//                    TMEM lanes: reductions = in-thread + 3 shuffles + 4-warp
+//                    smem), P written as bf16 hi/lo with stmatrix.trans straight
+//                    into the K-major B-operand layout; online rescale across
+//                    groups (hybrid rows); epilogue g = sigmoid(z),
+//                    out = g*O_comp[w] + (1-g)*O_sel in f32.
+//
+// HBM/L2-gather bound on iid inputs: 4 KB of K+V per selected window for
+// 65536 MACs (16 flop/B), see DESIGN.md.
+#include <cuda.h>
+
+#include "tc.h"
+#include "tc_ptx.cuh"
+
+namespace gsa_sm100 {
+namespace {
+
+using namespace ptx;
+
+constexpr int NS = 8;                    // ring stages
+constexpr int STAGE = 16384;             // 8 windows x 2 KB
+constexpr int WIN = 2048;                // 16 tokens x 64 bf16
+constexpr int NTHREADS = 192;
+constexpr uint32_t TMEM_COLS = 256;
+constexpr uint32_t S_COL0 = 0, S_COL1 = 64, O_COL0 = 128, O_COL1 = 144, G_COL0 = 160, G_COL1 = 176;
+constexpr int GROUP_WIN = 32;            // windows per softmax group (512 keys)
+
+struct __align__(1024) SelSmem {
+    uint8_t ring[NS][STAGE];
+    uint8_t q[2][WIN];
+    uint8_t wg[2][8192];      // W_g hi / lo, [a][j] 128B-swizzled
+    uint8_t p[2][2][16384];   // [group parity][hi/lo] P^T: [q-group 2][key-chunk 64][8 rows][16 B]
+    float red[2][4][16];      // cross-warp max / sum partials
+    float run_m[2][16];       // [group parity] running row max (raw score units)
+    float run_l[2][16];       // [group parity] running denominator
+    float alpha[2][16];       // [group parity] rescale of the previous groups' accumulator
+    uint64_t full[NS], empty[NS];
+    uint64_t q_full[2], q_empty[2];
+    uint64_t wg_full, wg_empty;
+    uint64_t s_full[2], s_empty[2];
+    uint64_t p_full[2], o_full[2];
+    uint64_t g_empty[2];
+    uint32_t tmem_base;
+};
+
+struct SelTcParams {
+    int heads;
+    DevLayout L;
+    RowSource rows;
+    float scale, c2;  // c2 = scale * log2(e)
+    int64_t items;
+    const float* o_comp;
+    float* out;
+    int64_t out_hs, out_rs;
+    float* lse;
+    float* o_sel_ctx;
+    float* gate_ctx;
+    const uint8_t* wg_prep;  // [H][2][8192] bytes
+};
+
+// Iterates this CTA's (item, group) sequence.
+struct GroupIt {
+    int64_t item;
+    int g, ng, nwin;
+    __device__ void start(const SelTcParams& p) {
+        item = blockIdx.x;
+        g = 0;
+        load(p);
+    }
+    __device__ void load(const SelTcParams& p) {
+        if (item < p.items) {
+            nwin = (int)p.rows.size(item);
+            ng = (nwin + GROUP_WIN - 1) / GROUP_WIN;
+        } else {
+            nwin = ng = 0;
+        }
+    }
+    __device__ bool valid(const SelTcParams& p) const { return item < p.items; }
+    __device__ void next(const SelTcParams& p) {
+        if (++g >= ng) {
+            g = 0;
+            item += gridDim.x;
+            load(p);
+        }
+    }
+    __device__ int group_windows() const { return min(GROUP_WIN, nwin - g * GROUP_WIN); }
+};
+
+__device__ __forceinline__ void window_coords(const DevLayout& L, int wid, int& c1, int& c2) {
+    const int f = wid / L.wins_per_frame, r = wid - f * L.wins_per_frame;
+    const int wr = r / L.wins_w, wc = r - wr * L.wins_w;
+    c1 = wc * 4;
+    c2 = f * L.grid_h + wr * 4;
+}
+
+__global__ void __launch_bounds__(NTHREADS, 1)
+    select_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+                     const __grid_constant__ CUtensorMap tm_v, const SelTcParams p) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    // keep the shared address space visible to the compiler (LDS/STS, not generic LD/ST)
+    SelSmem& sm = *reinterpret_cast<SelSmem*>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
+    const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
+
+    // ---- setup: zero the operand buffers (slots past a short row stay finite)
+    {
+        uint4* z0 = reinterpret_cast<uint4*>(&sm.ring[0][0]);
+        for (int i = threadIdx.x; i < (int)(sizeof(sm.ring) / 16); i += NTHREADS) z0[i] = make_uint4(0, 0, 0, 0);
+        uint4* z1 = reinterpret_cast<uint4*>(&sm.p[0][0][0]);
+        for (int i = threadIdx.x; i < (int)(sizeof(sm.p) / 16); i += NTHREADS) z1[i] = make_uint4(0, 0, 0, 0);
+    }
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < NS; ++i) {
+            mbar_init(&sm.full[i], 1);
+            mbar_init(&sm.empty[i], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&sm.q_full[i], 1);
+            mbar_init(&sm.q_empty[i], 1);
+            mbar_init(&sm.s_full[i], 1);
+            mbar_init(&sm.s_empty[i], 128);
+            mbar_init(&sm.g_empty[i], 128);
+            mbar_init(&sm.p_full[i], 128);
+            mbar_init(&sm.o_full[i], 1);
+        }
+        mbar_init(&sm.wg_full, 1);
+        mbar_init(&sm.wg_empty, 1);
+        fence_barrier_init();
+        prefetch_tmap(&tm_q);
+        prefetch_tmap(&tm_k);
+        prefetch_tmap(&tm_v);
+    }
+    if (warp == 1) tmem_alloc(&sm.tmem_base, TMEM_COLS);
+    fence_proxy_async_smem();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = sm.tmem_base;
+    const DevLayout& L = p.L;
+
+    if (warp == 0) {
+        // ============================== TMA producer ==============================
+        // The whole warp walks the stream: each lane fetches one window id of the
+        // group (one coalesced load instead of a serial id chain) and issues that
+        // window's TMA; lane 0 arms the stage barrier first.
+        int st = 0;
+        uint32_t eph = 1;  // empty barriers: first pass succeeds
+        uint32_t qph[2] = {1, 1};
+        int cur_head = -1;
+        int64_t n_items = 0;  // items whose Q/Wg prelude has been issued
+        auto load_chunks = [&](const GroupIt& it, const CUtensorMap* tm, bool with_prelude) {
+            const int h = (int)(it.item / L.windows), w = (int)(it.item - (int64_t)h * L.windows);
+            if (with_prelude) {
+                if (h != cur_head) {
+                    // W_g of the new head: wait until every G MMA of the old head completed
+                    if (n_items > 0) mbar_wait(&sm.wg_empty, (uint32_t)((n_items - 1) & 1));
+                    if (lane == 0) {
+                        mbar_arrive_expect_tx(&sm.wg_full, 16384);
+                        bulk_load(&sm.wg[0][0], p.wg_prep + (size_t)h * 16384, 16384, &sm.wg_full);
+                    }
+                    cur_head = h;
+                }
+                const int qb = (int)(n_items & 1);
+                mbar_wait(&sm.q_empty[qb], qph[qb]);
+                qph[qb] ^= 1;
+                if (lane == 0) {
+                    mbar_arrive_expect_tx(&sm.q_full[qb], WIN);
+                    int c1, c2;
+                    window_coords(L, w, c1, c2);
+                    tma_load_4d(&sm.q[qb][0], &tm_q, &sm.q_full[qb], 0, c1, c2, h);
+                }
+                ++n_items;
+            }
+            const int nw = it.group_windows();
+            const int my_wid = lane < nw ? p.rows.window(it.item, (int64_t)it.g * GROUP_WIN + lane) : 0;
+            int c1, c2;
+            window_coords(L, my_wid, c1, c2);
+            for (int c0 = 0; c0 < nw; c0 += 8) {
+                const int nc = min(8, nw - c0);
+                mbar_wait(&sm.empty[st], eph);
+                if (lane == 0) mbar_arrive_expect_tx(&sm.full[st], nc * WIN);
+                __syncwarp();
+                if (lane >= c0 && lane < c0 + nc)
+                    tma_load_4d(&sm.ring[st][(lane - c0) * WIN], tm, &sm.full[st], 0, c1, c2, h);
+                if (++st == NS) {
+                    st = 0;
+                    eph ^= 1;
+                }
+            }
+        };
+        GroupIt kit, vit;
+        kit.start(p);
+        vit.start(p);
+        if (kit.valid(p)) {
+            load_chunks(kit, &tm_k, true);
+            kit.next(p);
+        }
+        while (vit.valid(p)) {
+            if (kit.valid(p)) {
+                load_chunks(kit, &tm_k, kit.g == 0);
+                kit.next(p);
+            }
+            load_chunks(vit, &tm_v, false);
+            vit.next(p);
+        }
+    } else if (warp == 1) {
+        // ================================ MMA issuer ===============================
+        // Stream order: S(0); then per group j: S(j+1) (look-ahead), PV(j).
+        if (lane == 0) {
+            const uint32_t id_s = idesc_bf16(128, 16, 0, 0);
+            const uint32_t id_o = idesc_bf16(64, 16, 1, 0);
+            int st = 0;
+            uint32_t fph = 0;
+            uint32_t qph[2] = {0, 0}, sph[2] = {1, 1}, gph[2] = {1, 1}, pph[2] = {0, 0};
+            uint32_t wgph = 0;
+            int cur_head = -1;
+            int64_t n_items = 0;
+            int64_t jS = 0, jP = 0;  // global group indices of the next S / PV
+            auto issue_S = [&](const GroupIt& it) {
+                const int h = (int)(it.item / L.windows);
+                const int qb = (int)((n_items - (it.g == 0 ? 0 : 1)) & 1);
+                if (it.g == 0) {
+                    mbar_wait(&sm.q_full[qb], qph[qb]);
+                    qph[qb] ^= 1;
+                    if (h != cur_head) {
+                        mbar_wait(&sm.wg_full, wgph);
+                        wgph ^= 1;
+                        cur_head = h;
+                    }
+                    // G^T = Wg^T . Q^T (hi + lo), into the item's G buffer
+                    const int gb = (int)(n_items & 1);
+                    mbar_wait(&sm.g_empty[gb], gph[gb]);
+                    gph[gb] ^= 1;
+                    tc_fence_after();
+                    const uint32_t gcol = tmem + (gb ? G_COL1 : G_COL0);
+                    for (int part = 0; part < 2; ++part)
+                        for (int ks = 0; ks < 4; ++ks)
+                            mma_bf16(gcol, umma_desc(smem_u32(&sm.wg[part][0]) + ks * 2048, 16, 1024, 2),
+                                     umma_desc(smem_u32(&sm.q[qb][0]) + ks * 32, 16, 1024, 2), id_o,
+                                     (part | ks) != 0);
+                    mma_commit(&sm.wg_empty);
+                    ++n_items;
+                }
+                const int sb = (int)(jS & 1);
+                mbar_wait(&sm.s_empty[sb], sph[sb]);
+                sph[sb] ^= 1;
+                tc_fence_after();
+                const int nw = it.group_windows();
+                const uint32_t scol = tmem + (sb ? S_COL1 : S_COL0);
+                const uint64_t qdesc = umma_desc(smem_u32(&sm.q[qb][0]), 16, 1024, 2);
+                for (int c0 = 0, c = 0; c0 < nw; c0 += 8, ++c) {
+                    mbar_wait(&sm.full[st], fph);
+                    tc_fence_after();
+                    const uint64_t kdesc = umma_desc(smem_u32(&sm.ring[st][0]), 16, 1024, 2);
+                    for (int ks = 0; ks < 4; ++ks)
+                        mma_bf16(scol + 16 * c, kdesc + (uint64_t)(ks * 2), qdesc + (uint64_t)(ks * 2), id_s, ks != 0);
+                    mma_commit(&sm.empty[st]);
+                    if (++st == NS) {
+                        st = 0;
+                        fph ^= 1;
+                    }
+                }
+                mma_commit(&sm.s_full[sb]);
+                if (it.g == it.ng - 1) mma_commit(&sm.q_empty[qb]);
+                ++jS;
+            };
+            auto issue_PV = [&](const GroupIt& it) {
+                const int pb = (int)(jP & 1);
+                mbar_wait(&sm.p_full[pb], pph[pb]);
+                pph[pb] ^= 1;
+                tc_fence_after();
+                const int nw = it.group_windows();
+                const uint32_t ocol = tmem + (pb ? O_COL1 : O_COL0);
+                const uint64_t phi = umma_desc(smem_u32(&sm.p[pb][0][0]), 128, 8192, 0);
+                const uint64_t plo = umma_desc(smem_u32(&sm.p[pb][1][0]), 128, 8192, 0);
+                for (int c0 = 0, c = 0; c0 < nw; c0 += 8, ++c) {
+                    mbar_wait(&sm.full[st], fph);
+                    tc_fence_after();
+                    const uint64_t vdesc = umma_desc(smem_u32(&sm.ring[st][0]), 16, 1024, 2);
+                    // descriptor start addresses are in 16-byte units
+                    for (int ks = 0; ks < 8; ++ks) {
+                        const uint64_t va = vdesc + (uint64_t)(ks * 128);
+                        const uint64_t po = (uint64_t)(c * 128 + ks * 16);
+                        mma_bf16(ocol, va, phi + po, id_o, (c | ks) != 0);
+                        mma_bf16(ocol, va, plo + po, id_o, 1);
+                    }
+                    mma_commit(&sm.empty[st]);
+                    if (++st == NS) {
+                        st = 0;
+                        fph ^= 1;
+                    }
+                }
+                mma_commit(&sm.o_full[pb]);
+                ++jP;
+            };
+            GroupIt kit, vit;
+            kit.start(p);
+            vit.start(p);
+            if (kit.valid(p)) {
+                issue_S(kit);
+                kit.next(p);
+            }
+            while (vit.valid(p)) {
+                if (kit.valid(p)) {
+                    issue_S(kit);
+                    kit.next(p);
+                }
+                issue_PV(vit);
+                vit.next(p);
+            }
+        }
+    } else {
+        // ======================= softmax + epilogue (warps 2..5) ====================
+        // Software-pipelined by one group: softmax(j) runs while the tensor core
+        // computes PV(j-1); then finish(j-1) folds O(j-1) into the accumulator
+        // and, at the end of an item, writes the gated output.
+        const int ws = warp - 2;        // 0..3 (reduction slot)
+        const int qd = warp & 3;        // TMEM lane quadrant this warp may access
+        const int t0 = lane & 3, t1 = lane >> 2;
+        const bool stat_owner = (ws == 0 && t1 == 0);  // 4 threads x 4 query slots = 16 queries
+        float acc[16];
+        uint32_t sph[2] = {0, 0}, oph[2] = {0, 0};
+        int64_t j = 0, n_fin_items = 0;
+        GroupIt it, fin;
+        it.start(p);
+        fin.start(p);
+
+        auto finish = [&](const GroupIt& f, int64_t jf) {
+            const int fb = (int)(jf & 1);
+            mbar_wait(&sm.o_full[fb], oph[fb]);
+            oph[fb] ^= 1;
+            tc_fence_after();
+            uint32_t orr[16];
+            tmem_ld_32x32b_x16(tmem + ((uint32_t)(32 * qd) << 16) + (fb ? O_COL1 : O_COL0), orr);
+            tmem_wait_ld();
+            if (f.g == 0) {
+#pragma unroll
+                for (int q = 0; q < 16; ++q) acc[q] = __uint_as_float(orr[q]);
+            } else {
+#pragma unroll
+                for (int q = 0; q < 16; ++q) acc[q] = fmaf(acc[q], sm.alpha[fb][q], __uint_as_float(orr[q]));
+            }
+            if (f.g != f.ng - 1) return;
+            // ------------------------------- epilogue -------------------------------
+            const int gb = (int)(n_fin_items & 1);
+            uint32_t grr[16];
+            tmem_ld_32x32b_x16(tmem + ((uint32_t)(32 * qd) << 16) + (gb ? G_COL1 : G_COL0), grr);
+            tmem_wait_ld();
+            tc_fence_before();
+            mbar_arrive(&sm.g_empty[gb]);
+            ++n_fin_items;
+            // lanes 0-15 hold feature 16*qd+lane for all 16 queries; lanes 16-31 take
+            // queries 8..15 of lane-16 so every lane writes 8 outputs
+            const int hi_half = lane >> 4;
+            float a8[8], z8[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const float a_hi = __shfl_sync(0xffffffffu, acc[i + 8], lane & 15);
+                const float z_hi = __shfl_sync(0xffffffffu, __uint_as_float(grr[i + 8]), lane & 15);
+                a8[i] = hi_half ? a_hi : acc[i];
+                z8[i] = hi_half ? z_hi : __uint_as_float(grr[i]);
+            }
+            const int h = (int)(f.item / L.windows), w = (int)(f.item - (int64_t)h * L.windows);
+            const int jf_feat = 16 * qd + (lane & 15);
+            const float comp = p.o_comp[((int64_t)h * L.windows + w) * 64 + jf_feat];
+            const int fr = w / L.wins_per_frame, rr = w - fr * L.wins_per_frame;
+            const int wr = rr / L.wins_w, wc = rr - wr * L.wins_w;
+            const int tok0 = fr * L.tokens_per_frame + wr * 4 * L.grid_w + wc * 4;
+            float* outh = p.out + (int64_t)h * p.out_hs;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const int q = i + 8 * hi_half;
+                const int tok = tok0 + (q >> 2) * L.grid_w + (q & 3);
+                const float sel = a8[i] / sm.run_l[fb][q];
+                const float g = 1.0f / (1.0f + __expf(-z8[i]));
+                outh[(int64_t)tok * p.out_rs + jf_feat] = g * comp + (1.0f - g) * sel;
+                if (p.o_sel_ctx || p.gate_ctx) {
+                    const int64_t ti = (int64_t)h * L.image_tokens + tok;
+                    if (p.o_sel_ctx) p.o_sel_ctx[ti * 64 + jf_feat] = sel;
+                    if (p.gate_ctx) p.gate_ctx[ti * 64 + jf_feat] = g;
+                }
+            }
+            if (p.lse && ws == 0 && lane < 16) {
+                const int tok = tok0 + (lane >> 2) * L.grid_w + (lane & 3);
+                p.lse[(int64_t)h * L.image_tokens + tok] = sm.run_m[fb][lane] * p.scale + logf(sm.run_l[fb][lane]);
+            }
+        };
+
+        while (it.valid(p)) {
+            const int sb = (int)(j & 1);
+            const int nkeys = it.group_windows() * 16;
+            mbar_wait(&sm.s_full[sb], sph[sb]);
+            sph[sb] ^= 1;
+            tc_fence_after();
+            float s[4][2][8];
+            const uint32_t scol = tmem + (sb ? S_COL1 : S_COL0);
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+#pragma unroll
+                for (int hf = 0; hf < 2; ++hf) {
+                    uint32_t r[8];
+                    if (c * 128 < nkeys) {
+                        tmem_ld_16x256b_x2(scol + ((uint32_t)(32 * qd + 16 * hf) << 16) + 16 * c, r);
+                    } else {
+#pragma unroll
+                        for (int e = 0; e < 8; ++e) r[e] = 0u;
+                    }
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) s[c][hf][e] = __uint_as_float(r[e]);
+                }
+            tmem_wait_ld();
+            tc_fence_before();
+            mbar_arrive(&sm.s_empty[sb]);
+            // mask keys past the row end; key of s[c][hf][e] = 128c + 32qd + 16hf + t1 + 8*((e>>1)&1)
+            float mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+#pragma unroll
+                for (int hf = 0; hf < 2; ++hf)
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) {
+                        const int key = 128 * c + 32 * qd + 16 * hf + t1 + 8 * ((e >> 1) & 1);
+                        if (key >= nkeys) s[c][hf][e] = -INFINITY;
+                        const int slot = (e & 1) | ((e >> 2) << 1);  // query 2*t0 + (e&1) + 8*(e>>2)
+                        mx[slot] = fmaxf(mx[slot], s[c][hf][e]);
+                    }
+#pragma unroll
+            for (int sl = 0; sl < 4; ++sl) {
+                mx[sl] = fmaxf(mx[sl], __shfl_xor_sync(0xffffffffu, mx[sl], 4));
+                mx[sl] = fmaxf(mx[sl], __shfl_xor_sync(0xffffffffu, mx[sl], 8));
+                mx[sl] = fmaxf(mx[sl], __shfl_xor_sync(0xffffffffu, mx[sl], 16));
+            }
+            if (t1 == 0) {
+#pragma unroll
+                for (int sl = 0; sl < 4; ++sl) sm.red[0][ws][2 * t0 + (sl & 1) + 8 * (sl >> 1)] = mx[sl];
+            }
+            named_bar_sync(1, 128);
+            const int pb = sb;           // this group's statistics / P buffers
+            const int ob = sb ^ 1;       // previous group's
+            float mq[4], al[4];
+#pragma unroll
+            for (int sl = 0; sl < 4; ++sl) {
+                const int q = 2 * t0 + (sl & 1) + 8 * (sl >> 1);
+                const float gm = fmaxf(fmaxf(sm.red[0][0][q], sm.red[0][1][q]), fmaxf(sm.red[0][2][q], sm.red[0][3][q]));
+                const float mold = it.g == 0 ? -INFINITY : sm.run_m[ob][q];
+                const float mnew = fmaxf(mold, gm);
+                al[sl] = mold == -INFINITY ? 0.0f : exp2f((mold - mnew) * p.c2);
+                mq[sl] = mnew * p.c2;
+                if (stat_owner) {
+                    sm.run_m[pb][q] = mnew;
+                    sm.alpha[pb][q] = al[sl];
+                }
+            }
+            float sum[4] = {0.f, 0.f, 0.f, 0.f};
+            // P = exp(scale*(s - m)); stored as bf16 hi + lo through stmatrix.trans
+            const uint32_t pbase_hi = smem_u32(&sm.p[pb][0][0]), pbase_lo = smem_u32(&sm.p[pb][1][0]);
+            const int mi = lane >> 3, rr = lane & 7;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                if (c * 128 >= nkeys) continue;  // (continue keeps the unroll static)
+#pragma unroll
+                for (int hf = 0; hf < 2; ++hf) {
+                    float pv[8];
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) {
+                        const int slot = (e & 1) | ((e >> 2) << 1);
+                        const float x = s[c][hf][e];
+                        pv[e] = x == -INFINITY ? 0.0f : exp2f(fmaf(x, p.c2, -mq[slot]));
+                        sum[slot] += pv[e];
+                    }
+                    uint32_t hi[4], lo[4];
+#pragma unroll
+                    for (int e2 = 0; e2 < 4; ++e2) {
+                        const float a0 = pv[2 * e2], a1 = pv[2 * e2 + 1];
+                        const __nv_bfloat16 h0 = __float2bfloat16_rn(a0), h1 = __float2bfloat16_rn(a1);
+                        hi[e2] = pack_bf16(__bfloat162float(h0), __bfloat162float(h1));
+                        lo[e2] = pack_bf16(a0 - __bfloat162float(h0), a1 - __bfloat162float(h1));
+                    }
+                    // matrix mi: keys +8*(mi&1), queries 8*(mi>>1); memory row rr = query
+                    const int kc = (128 * c + 32 * qd + 16 * hf) / 8 + (mi & 1);
+                    const uint32_t off = (uint32_t)((mi >> 1) * 8192 + kc * 128 + rr * 16);
+                    stmatrix_x4_trans(pbase_hi + off, hi[0], hi[1], hi[2], hi[3]);
+                    stmatrix_x4_trans(pbase_lo + off, lo[0], lo[1], lo[2], lo[3]);
+                }
+            }
+            fence_proxy_async_smem();
+            mbar_arrive(&sm.p_full[pb]);
+#pragma unroll
+            for (int sl = 0; sl < 4; ++sl) {
+                sum[sl] += __shfl_xor_sync(0xffffffffu, sum[sl], 4);
+                sum[sl] += __shfl_xor_sync(0xffffffffu, sum[sl], 8);
+                sum[sl] += __shfl_xor_sync(0xffffffffu, sum[sl], 16);
+            }
+            if (t1 == 0) {
+#pragma unroll
+                for (int sl = 0; sl < 4; ++sl) sm.red[1][ws][2 * t0 + (sl & 1) + 8 * (sl >> 1)] = sum[sl];
+            }
+            named_bar_sync(1, 128);
+            if (stat_owner) {
+#pragma unroll
+                for (int sl = 0; sl < 4; ++sl) {
+                    const int q = 2 * t0 + (sl & 1) + 8 * (sl >> 1);
+                    const float gs = (sm.red[1][0][q] + sm.red[1][1][q]) + (sm.red[1][2][q] + sm.red[1][3][q]);
+                    const float lold = it.g == 0 ? 0.0f : sm.run_l[ob][q];
+                    sm.run_l[pb][q] = lold * al[sl] + gs;
+                }
+            }
+            // fold in the previous group's PV (computed while this softmax ran)
+            if (j > 0) {
+                finish(fin, j - 1);
+                fin.next(p);
+            }
+            ++j;
+            it.next(p);
+        }
+        if (j > 0) {
+            named_bar_sync(1, 128);  // run_l of the last group visible to every finishing thread
+            finish(fin, j - 1);
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc(tmem, TMEM_COLS);
+    }
+}
+
+// W_g f32 [H][64][64] -> bf16 hi / lo, [a][j] rows of 128 B with the 128B swizzle
+// pre-applied (chunk j/8 stored at chunk (j/8) ^ (a%8)), so one bulk copy lands
+// the MN-major UMMA A-operand of G^T = W_g^T . Q^T.
+__global__ void wg_prep_kernel(const float* __restrict__ wg, int heads, uint8_t* out) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;  // over heads*64*64
+    if (i >= heads * 4096) return;
+    const int h = i / 4096, a = (i / 64) % 64, jj = i % 64;
+    const float x = wg[i];
+    const __nv_bfloat16 hi = __float2bfloat16_rn(x);
+    const __nv_bfloat16 lo = __float2bfloat16_rn(x - __bfloat162float(hi));
+    const int byte = a * 128 + ((((jj * 2) >> 4) ^ (a & 7)) << 4) + ((jj * 2) & 15);
+    *reinterpret_cast<__nv_bfloat16*>(out + (size_t)h * 16384 + byte) = hi;
+    *reinterpret_cast<__nv_bfloat16*>(out + (size_t)h * 16384 + 8192 + byte) = lo;
+}
+
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeFn get_encode() {
+    static EncodeFn fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeFn>(p);
+    }
+    return fn;
+}
+
+// window gather map over the image rows of a head-major [H][M][64] bf16 tensor
+bool make_window_map(CUtensorMap* m, const TensorRef& t, int heads, const DevLayout& L) {
+    EncodeFn enc = get_encode();
+    if (!enc) return false;
+    cuuint64_t dims[4] = {64, (cuuint64_t)L.grid_w, (cuuint64_t)L.grid_h * L.num_frames, (cuuint64_t)heads};
+    cuuint64_t strides[3] = {128, (cuuint64_t)L.grid_w * 128, (cuuint64_t)t.hs * 2};
+    cuuint32_t box[4] = {64, 4, 4, 1};
+    cuuint32_t es[4] = {1, 1, 1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(t.data), dims, strides, box, es,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+bool tensor_ok(const TensorRef& t) {
+    return t.dtype == GSA_DTYPE_BF16 && t.rs == 64 && t.hs % 8 == 0 && (reinterpret_cast<uintptr_t>(t.data) & 15) == 0;
+}
+
+}  // namespace
+
+bool tc_select_supported(const gsa_tensor& q, const DevLayout& L, const RowSource&) {
+    return q.dtype == GSA_DTYPE_BF16 && q.dim == 64 && L.s == 4 && get_encode() != nullptr;
+}
+
+size_t tc_select_workspace_bytes(int heads) { return (size_t)heads * 16384; }
+
+cudaError_t tc_select_gate_merge(const SelectArgs& a, cudaStream_t st) {
+    if (!tensor_ok(a.q) || !tensor_ok(a.k) || !tensor_ok(a.v) || a.dim != 64 || a.L.s != 4 || !a.w_g ||
+        !a.o_comp || !a.wg_prep)
+        return cudaErrorNotSupported;
+    CUtensorMap tq, tk, tv;
+    if (!make_window_map(&tq, a.q, a.heads, a.L) || !make_window_map(&tk, a.k, a.heads, a.L) ||
+        !make_window_map(&tv, a.v, a.heads, a.L))
+        return cudaErrorNotSupported;
+    wg_prep_kernel<<<(a.heads * 4096 + 255) / 256, 256, 0, st>>>(a.w_g, a.heads, a.wg_prep);
+    note_launch();
+    SelTcParams p;
+    p.heads = a.heads;
+    p.L = a.L;
+    p.rows = a.rows;
+    p.scale = a.scale;
+    p.c2 = a.scale * 1.4426950408889634f;
+    p.items = (int64_t)a.heads * a.L.windows;
+    p.o_comp = a.o_comp;
+    p.out = a.out;
+    p.out_hs = a.out_hs;
+    p.out_rs = a.out_rs;
+    p.lse = a.lse;
+    p.o_sel_ctx = a.o_sel_ctx;
+    p.gate_ctx = a.gate_ctx;
+    p.wg_prep = a.wg_prep;
+    int dev = 0, nsm = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    const size_t smem = sizeof(SelSmem) + 1024;
+    cudaError_t e = cudaFuncSetAttribute(select_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    const int grid = (int)std::min<int64_t>(nsm, p.items);
+    select_tc_kernel<<<grid, NTHREADS, smem, st>>>(tq, tk, tv, p);
+    note_launch();
+    return cudaGetLastError();
+}
+
+}  // namespace gsa_sm100

@@ -24,6 +24,7 @@ cudaError_t tc_compress_topk(const gsa_tensor& qc, const gsa_tensor& kc, const g
 
 // selection branch + gate + merge
 bool tc_select_supported(const gsa_tensor& q, const DevLayout& L, const RowSource& rows);
+size_t tc_select_workspace_bytes(int heads);
 cudaError_t tc_select_gate_merge(const SelectArgs& a, cudaStream_t st);
 
 }  // namespace gsa_sm100

@@ -44,8 +44,5 @@ cudaError_t tc_compress_topk(const gsa_tensor& qc, const gsa_tensor& kc, const g
     return launch_attn_f32(a, st);
 }
 
-bool tc_select_supported(const gsa_tensor&, const DevLayout&, const RowSource&) { return false; }
-
-cudaError_t tc_select_gate_merge(const SelectArgs&, cudaStream_t) { return cudaErrorNotSupported; }
 
 }  // namespace gsa_sm100
