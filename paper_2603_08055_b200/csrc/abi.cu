@@ -219,12 +219,12 @@ int gsa_upsample_nearest(const gsa_tensor* coarse, const gsa_layout* layout, con
 
 static int dense_attention(const gsa_tensor* q, const gsa_tensor* k, const gsa_tensor* v, float scale,
                            const gsa_tensor* out, float* lse, int q_row_offset, int out_row_offset,
-                           int mq, cudaStream_t st) {
+                           int mq, cudaStream_t st, void* ws = nullptr, size_t ws_bytes = 0) {
     if (mq == 0) return GSA_OK;
     if (k->rows == 0) return fail(GSA_ERR_SHAPE_MISMATCH, "tiled_attention: empty key set");
     if (tc_dense_supported(*q, *k, *v)) {
         GSA_CUDA(tc_dense_attention(*q, *k, *v, scale, q_row_offset, mq, static_cast<float*>(out->data),
-                                    out->head_stride, out->row_stride, out_row_offset, lse, st));
+                                    out->head_stride, out->row_stride, out_row_offset, lse, ws, ws_bytes, st));
         return GSA_OK;
     }
     GSA_TRY(generic_supported(q->dim, 1));
@@ -494,6 +494,8 @@ struct LayerBufs {
     void* compress_ws;
     size_t compress_ws_bytes;
     uint8_t* wg_prep;
+    void* dense_ws;
+    size_t dense_ws_bytes;
 };
 
 size_t carve(const LayerPlan& lp, const gsa_context* ctx, char* base, size_t cap, bool dry, LayerBufs* b) {
@@ -512,6 +514,8 @@ size_t carve(const LayerPlan& lp, const gsa_context* ctx, char* base, size_t cap
     b->compress_ws_bytes = tc_compress_workspace_bytes(lp.heads, lp.W, lp.dim, lp.k_eff);
     b->compress_ws = c.take<char>(b->compress_ws_bytes);
     b->wg_prep = c.take<uint8_t>(tc_select_workspace_bytes(lp.heads));
+    b->dense_ws_bytes = tc_dense_workspace_bytes(lp.heads, lp.Ms, lp.Ms + lp.Mi);
+    b->dense_ws = c.take<char>(b->dense_ws_bytes);
     return c.used + 256;
 }
 
@@ -551,7 +555,7 @@ int gsa_forward(const gsa_tensor* q, const gsa_tensor* k, const gsa_tensor* v, c
 
     // 1. special tokens: dense attention over all M keys (layer.hpp:201-202)
     stage_mark(0, st);
-    GSA_TRY(dense_attention(q, k, v, lp.scale, out, b.lse_spec, 0, 0, lp.Ms, st));
+    GSA_TRY(dense_attention(q, k, v, lp.scale, out, b.lse_spec, 0, 0, lp.Ms, st, b.dense_ws, b.dense_ws_bytes));
     stage_mark(1, st);
 
     // 2. pool Q/K/V image rows (layer.hpp:204-206)

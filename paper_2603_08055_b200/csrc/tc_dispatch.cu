@@ -9,12 +9,6 @@ namespace gsa_sm100 {
 std::atomic<unsigned long long> g_launch_total{0};
 void note_launch(int n) { g_launch_total += (unsigned long long)n; }
 
-bool tc_dense_supported(const gsa_tensor&, const gsa_tensor&, const gsa_tensor&) { return false; }
-
-cudaError_t tc_dense_attention(const gsa_tensor&, const gsa_tensor&, const gsa_tensor&, float, int, int,
-                               float*, int64_t, int64_t, int, float*, cudaStream_t) {
-    return cudaErrorNotSupported;
-}
 
 size_t tc_compress_workspace_bytes(int, int, int, int) { return 0; }
 

@@ -117,6 +117,23 @@ def test_tiled_attention(gsa, orc):
         assert np.abs(host(lse) - l_ref).max() < 1e-3
 
 
+@pytest.mark.parametrize("mq,mk,grow", [(128, 128, False), (200, 1000, False), (77, 4099, True), (1, 300, True)])
+def test_tiled_attention_tc_shapes(gsa, orc, mq, mk, grow):
+    """bf16 / d=64 runs on the tcgen05 kernel: ragged tiles, and keys whose
+    scores grow along the sequence so the lazy O rescale path fires."""
+    rng = np.random.default_rng(mq + mk)
+    q = orc.bf16_round(rng.standard_normal((2, mq, 64)).astype(np.float32))
+    k = rng.standard_normal((2, mk, 64)).astype(np.float32)
+    if grow:
+        k *= np.linspace(0.2, 4.0, mk, dtype=np.float32)[None, :, None]
+    k = orc.bf16_round(k)
+    v = orc.bf16_round(rng.standard_normal((2, mk, 64)).astype(np.float32))
+    o_ref, l_ref = orc.dense_attention(q, k, v, 0.125)
+    out, lse = gsa.tiled_attention(dev(q), dev(k), dev(v), 0.125)
+    assert rel_l2(host(out), o_ref) < 1e-4
+    assert np.abs(host(lse) - l_ref).max() < 1e-3
+
+
 def test_gate_and_upsample(gsa, orc):
     rng = np.random.default_rng(4)
     q = orc.bf16_round(rng.standard_normal((2, 96, 64)).astype(np.float32))
