@@ -558,11 +558,14 @@ int gsa_forward(const gsa_tensor* q, const gsa_tensor* k, const gsa_tensor* v, c
     GSA_TRY(dense_attention(q, k, v, lp.scale, out, b.lse_spec, 0, 0, lp.Ms, st, b.dense_ws, b.dense_ws_bytes));
     stage_mark(1, st);
 
-    // 2. pool Q/K/V image rows (layer.hpp:204-206)
+    // 2. pool Q/K/V image rows (layer.hpp:204-206); on the tensor-core path the
+    // same pass also writes the bf16 hi/lo operands and row norms K2 consumes
+    CompressSplits sp{};
+    const bool have_sp = tc_compress_split_buffers(b.compress_ws, b.compress_ws_bytes, H, lp.W, d, lp.k_eff, &sp);
     PoolJob jobs[3] = {
-        {ref_of(*q, lp.Ms), b.qc, nullptr, nullptr, nullptr},
-        {ref_of(*k, lp.Ms), b.kc, nullptr, nullptr, nullptr},
-        {ref_of(*v, lp.Ms), b.vc, nullptr, nullptr, nullptr},
+        {ref_of(*q, lp.Ms), b.qc, sp.qh, sp.ql, sp.qnorm},
+        {ref_of(*k, lp.Ms), b.kc, sp.kh, sp.kl, sp.knorm},
+        {ref_of(*v, lp.Ms), b.vc, sp.vh, sp.vl, nullptr},
     };
     GSA_CUDA(launch_pool(jobs, 3, H, d, lp.L, 1.0f / (float)(lp.L.s * lp.L.s), st));
     stage_mark(2, st);
@@ -578,8 +581,9 @@ int gsa_forward(const gsa_tensor* q, const gsa_tensor* k, const gsa_tensor* v, c
     gsa_tensor tq{b.qc, GSA_DTYPE_F32, H, lp.W, d, (int64_t)lp.W * d, d};
     gsa_tensor tk{b.kc, GSA_DTYPE_F32, H, lp.W, d, (int64_t)lp.W * d, d};
     gsa_tensor tv{b.vc, GSA_DTYPE_F32, H, lp.W, d, (int64_t)lp.W * d, d};
-    GSA_CUDA(tc_compress_topk(tq, tk, tv, lp.k_eff, lp.scale, excluded, b.o_comp, (int64_t)lp.W * d, d,
-                              b.lse_comp, b.topk, nullptr, b.compress_ws, b.compress_ws_bytes, st));
+    GSA_CUDA(tc_compress_topk_splits(have_sp ? &sp : nullptr, tq, tk, tv, lp.k_eff, lp.scale, excluded, b.o_comp,
+                                     (int64_t)lp.W * d, d, b.lse_comp, b.topk, nullptr, b.compress_ws,
+                                     b.compress_ws_bytes, st));
     stage_mark(3, st);
 
     // 5-7. plan rows = forced ++ top-k (selection.cpp:55-59; the top-k already

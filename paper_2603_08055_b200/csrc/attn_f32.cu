@@ -62,7 +62,14 @@ __global__ void __launch_bounds__(NT) attn_f32_kernel(AttnArgs a, bool vec8) {
     int* lst_i = reinterpret_cast<int*>(lst_s + (TOPK ? BQ * a.k_eff : 0));
     __shared__ int lst_n[BQ];
 
-    const int h = blockIdx.y, q0 = blockIdx.x * BQ;
+    int h = blockIdx.y, q0 = blockIdx.x * BQ;
+    if (a.block_list) {
+        if ((int)blockIdx.x >= *a.block_count) return;
+        const int qtiles = (a.mq + BQ - 1) / BQ;
+        const int blk = a.block_list[blockIdx.x];
+        h = blk / qtiles;
+        q0 = (blk - h * qtiles) * BQ;
+    }
     const int tid = threadIdx.x;
     const int qrows = min(BQ, a.mq - q0);
     const T* qb = reinterpret_cast<const T*>(a.q.data) + (int64_t)h * a.q.hs + (int64_t)q0 * a.q.rs;
@@ -178,13 +185,15 @@ __global__ void __launch_bounds__(NT) attn_f32_kernel(AttnArgs a, bool vec8) {
             }
         }
     }
-    if (r < qrows) {
+    if (r < qrows && !(TOPK && a.topk_only)) {
         const float inv = 1.0f / l;
         float* orow = a.out + (int64_t)h * a.out_hs + (int64_t)(q0 + r) * a.out_rs;
 #pragma unroll
         for (int e = 0; e < DMAX / 4; ++e)
             if (p * (DMAX / 4) + e < dim) orow[p * (DMAX / 4) + e] = acc[e] * inv;
         if (p == 0 && a.lse) a.lse[(int64_t)h * a.mq + q0 + r] = m + logf(l);
+    }
+    if (r < qrows) {
         if (TOPK && p == 0 && a.k_eff > 0) {
             const int64_t base = ((int64_t)h * a.mq + q0 + r) * a.k_eff;
             for (int j = 0; j < a.k_eff; ++j) {
@@ -204,6 +213,7 @@ cudaError_t launch_typed(const AttnArgs& a, bool vec8, cudaStream_t st) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     dim3 grid((a.mq + BQ - 1) / BQ, a.heads);
+    if (a.block_list) grid = dim3(((a.mq + BQ - 1) / BQ) * a.heads, 1);
     { kern<<<grid, NT, smem, st>>>(a, vec8); note_launch(); }
     return cudaGetLastError();
 }

@@ -1,0 +1,697 @@
+// compress_tc.cu — K2: compressed attention with streaming top-k on tcgen05
+// tensor cores (fused_compressed_attention_topk, compression.hpp:180-297),
+// indices bit-exact with the reference by construction.
+//
+// Pooled Qc/Kc/Vc are f32 means (not bf16-representable), so every operand is
+// split x = hi + lo (bf16 each, |x - hi - lo| <= 2^-16 |x|) and
+//   S  = Qh.Kh^T + Qh.Kl^T + Ql.Kh^T            (12 MMAs, M=N=128, per key tile)
+//   O += Ph.Vh + Ph.Vl + Pl.Vh                  (24 MMAs, P from TMEM)
+// give softmax/PV far inside the tolerance. S is only an APPROXIMATION of the
+// reference guide score (scaled_dot: 4 stride-4 f32 lane sums, no FMA), so the
+// top-k runs in two steps:
+//   1. here, per query row (one thread = one TMEM lane): a sorted list of the
+//      k_eff best approximate scores plus a side list of everything within the
+//      margin 2*eps + delta of the running k-th score, where
+//      eps = 2^-11 * ||qc|| * max_j ||kc_j|| bounds |S - exact| (split error
+//      <= 3.1*2^-16 sum|q k|, f32 accumulation << that; Cauchy-Schwarz).
+//      Every true top-k member satisfies S >= tau - 2 eps (tau: k-th largest S),
+//      so the candidate set is a guaranteed superset;
+//   2. rescore_kernel: exact scaled_dot for each candidate, rank by
+//      (score desc, index asc) = topk_better (compression.hpp:67-73).
+// A row whose side list overflows (mass near-ties, e.g. identical keys) is
+// flagged and recomputed by the exact CUDA-core kernel (attn_f32.cu).
+#include <cuda.h>
+
+#include <cstdlib>
+
+#include "tc.h"
+#include "tc_ptx.cuh"
+#include "tma_util.cuh"
+
+namespace gsa_sm100 {
+namespace {
+
+using namespace ptx;
+
+constexpr int NS = 4;
+constexpr int TILE = 16384;       // 128 rows x 64 bf16
+constexpr int STAGE = 2 * TILE;   // hi + lo
+constexpr int NTHREADS = 192;
+constexpr uint32_t TMEM_COLS = 512;
+constexpr uint32_t O_COL = 384;
+constexpr float RESCALE_LOG2 = 8.0f;
+constexpr int KCAP = 32;          // max k_eff on this path
+constexpr int SIDE = 16;
+constexpr int CAND = KCAP + SIDE;
+constexpr float EPS_REL = 0.00048828125f;  // 2^-11
+constexpr float DELTA_REL = 9.5367431640625e-07f;  // 2^-20: collapse of distinct sums under *scale
+
+struct __align__(1024) CompSmem {
+    uint8_t qh[TILE], ql[TILE];
+    uint8_t ring[NS][STAGE];
+    float2 list[128][KCAP + 1];  // per row: (approx score, index bits), sorted desc; padded stride
+    float2 side[128][SIDE + 1];
+    uint64_t full[NS], empty[NS];
+    uint64_t q_full;
+    uint64_t s_full[3], s_free[3];
+    // by tile parity: the softmax runs up to a tile ahead of the MMA, and parity waits are
+    // only unambiguous within one phase of their target
+    uint64_t p_full[2], o_done[2];
+    uint32_t tmem_base;
+};
+
+struct CompParams {
+    int debug;  // bring-up switches (GSA_DEBUG_COMPRESS): 1 = no top-k scan, 2 = 1-term S/PV
+    int heads, W, k_eff;
+    float scale, c2;
+    int kv_tiles;
+    const float* qnorm;      // [H][W]
+    const float* kmax;       // [H]
+    const uint32_t* exbits;  // [ceil(W/32)] or null
+    float* out;
+    int64_t out_hs, out_rs;
+    float* lse;              // [H][W]
+    float2* cand;            // [H*W][CAND]
+    int* cand_n;             // [H*W]
+    uint8_t* flag;           // [H*W]
+};
+
+__device__ __forceinline__ uint32_t s_col(int b) { return (uint32_t)(128 * b); }
+
+// per-row streaming top-k state (kept off the hot path: touched only for candidates)
+struct TopkState {
+    float2* lst;  // sorted desc by approximate score, K entries when full
+    float2* sd;   // side list (near-tie candidates)
+    int n, nside, K;
+    float tau, thr, eps;
+    bool overflow;
+};
+
+__device__ __noinline__ void topk_handle(TopkState& s, float a, int col) {
+    auto set_thr = [&]() { s.thr = s.tau - (2.0f * s.eps + DELTA_REL * fabsf(s.tau)); };
+    auto side_push = [&](float v, int c) {
+        if (s.nside == SIDE) {  // drop what the risen threshold has excluded since
+            int w = 0;
+            for (int i = 0; i < SIDE; ++i)
+                if (s.sd[i].x >= s.thr) s.sd[w++] = s.sd[i];
+            s.nside = w;
+            if (s.nside == SIDE) {
+                s.overflow = true;  // near-tie flood: the exact kernel redoes this row
+                return;
+            }
+        }
+        s.sd[s.nside++] = make_float2(v, __int_as_float(c));
+    };
+    auto insert = [&](float v, int c) {
+        int i = s.n < s.K ? s.n : s.K - 1;
+        while (i > 0 && s.lst[i - 1].x < v) {
+            s.lst[i] = s.lst[i - 1];
+            --i;
+        }
+        s.lst[i] = make_float2(v, __int_as_float(c));
+    };
+    if (s.n < s.K) {
+        insert(a, col);
+        if (++s.n == s.K) {
+            s.tau = s.lst[s.K - 1].x;
+            set_thr();
+        }
+    } else if (a > s.tau) {
+        const float2 ev = s.lst[s.K - 1];
+        insert(a, col);
+        s.tau = s.lst[s.K - 1].x;
+        set_thr();
+        if (ev.x >= s.thr) side_push(ev.x, __float_as_int(ev.y));
+    } else {
+        side_push(a, col);
+    }
+}
+
+// v[e] for a runtime e without local memory: a 5-level select tree
+__device__ __forceinline__ float select32(const uint32_t (&v)[32], int e) {
+    uint32_t a[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) a[i] = (e & 16) ? v[i + 16] : v[i];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) a[i] = (e & 8) ? a[i + 8] : a[i];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) a[i] = (e & 4) ? a[i + 4] : a[i];
+#pragma unroll
+    for (int i = 0; i < 2; ++i) a[i] = (e & 2) ? a[i + 2] : a[i];
+    return __uint_as_float((e & 1) ? a[1] : a[0]);
+}
+
+__global__ void __launch_bounds__(NTHREADS, 1)
+    compress_tc_kernel(const __grid_constant__ CUtensorMap tm_qh, const __grid_constant__ CUtensorMap tm_ql,
+                       const __grid_constant__ CUtensorMap tm_kh, const __grid_constant__ CUtensorMap tm_kl,
+                       const __grid_constant__ CUtensorMap tm_vh, const __grid_constant__ CUtensorMap tm_vl,
+                       const CompParams p) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    CompSmem& sm = *reinterpret_cast<CompSmem*>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
+    const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
+    const int qt = blockIdx.x, h = blockIdx.y;
+    const int T = p.kv_tiles;
+
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < NS; ++i) {
+            mbar_init(&sm.full[i], 1);
+            mbar_init(&sm.empty[i], 1);
+        }
+        for (int i = 0; i < 3; ++i) {
+            mbar_init(&sm.s_full[i], 1);
+            mbar_init(&sm.s_free[i], 1);
+        }
+        mbar_init(&sm.q_full, 1);
+        mbar_init(&sm.p_full[0], 128);
+        mbar_init(&sm.p_full[1], 128);
+        mbar_init(&sm.o_done[0], 1);
+        mbar_init(&sm.o_done[1], 1);
+        fence_barrier_init();
+    }
+    if (warp == 1) tmem_alloc(&sm.tmem_base, TMEM_COLS);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = sm.tmem_base;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            // ================================ TMA ================================
+            mbar_arrive_expect_tx(&sm.q_full, 2 * TILE);
+            tma_load_3d(&sm.qh[0], &tm_qh, &sm.q_full, 0, qt * 128, h);
+            tma_load_3d(&sm.ql[0], &tm_ql, &sm.q_full, 0, qt * 128, h);
+            int st = 0;
+            uint32_t eph = 1;
+            auto load = [&](const CUtensorMap* th, const CUtensorMap* tl, int t) {
+                mbar_wait(&sm.empty[st], eph);
+                mbar_arrive_expect_tx(&sm.full[st], STAGE);
+                tma_load_3d(&sm.ring[st][0], th, &sm.full[st], 0, t * 128, h);
+                tma_load_3d(&sm.ring[st][TILE], tl, &sm.full[st], 0, t * 128, h);
+                if (++st == NS) {
+                    st = 0;
+                    eph ^= 1;
+                }
+            };
+            load(&tm_kh, &tm_kl, 0);
+            for (int t = 0; t < T; ++t) {
+                if (t + 1 < T) load(&tm_kh, &tm_kl, t + 1);
+                load(&tm_vh, &tm_vl, t);
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            // ================================ MMA ================================
+            const uint32_t id_s = idesc_bf16(128, 128, 0, 0);
+            const uint32_t id_o = idesc_bf16(128, 64, 0, 1);
+            int st = 0;
+            uint32_t fph = 0;
+            uint32_t freeph[3] = {1, 1, 1};
+            uint32_t pph[2] = {0, 0};
+            mbar_wait(&sm.q_full, 0);
+            const uint64_t qh = umma_desc(smem_u32(&sm.qh[0]), 16, 1024, 2);
+            const uint64_t ql = umma_desc(smem_u32(&sm.ql[0]), 16, 1024, 2);
+            auto issue_S = [&](int t) {
+                const int b = t % 3;
+                mbar_wait(&sm.s_free[b], freeph[b]);
+                freeph[b] ^= 1;
+                mbar_wait(&sm.full[st], fph);
+                tc_fence_after();
+                const uint64_t kh = umma_desc(smem_u32(&sm.ring[st][0]), 16, 1024, 2);
+                const uint64_t kl = umma_desc(smem_u32(&sm.ring[st][TILE]), 16, 1024, 2);
+                const uint32_t d = tmem + s_col(b);
+                for (int ks = 0; ks < 4; ++ks) mma_bf16(d, qh + 2 * ks, kh + 2 * ks, id_s, ks != 0);
+                if (!(p.debug & 2)) {
+                    for (int ks = 0; ks < 4; ++ks) mma_bf16(d, qh + 2 * ks, kl + 2 * ks, id_s, 1);
+                    for (int ks = 0; ks < 4; ++ks) mma_bf16(d, ql + 2 * ks, kh + 2 * ks, id_s, 1);
+                }
+                mma_commit(&sm.empty[st]);
+                mma_commit(&sm.s_full[b]);
+                if (++st == NS) {
+                    st = 0;
+                    fph ^= 1;
+                }
+            };
+            auto issue_PV = [&](int t) {
+                const int b = t % 3;
+                mbar_wait(&sm.p_full[t & 1], pph[t & 1]);
+                pph[t & 1] ^= 1;
+                mbar_wait(&sm.full[st], fph);
+                tc_fence_after();
+                const uint64_t vh = umma_desc(smem_u32(&sm.ring[st][0]), 16, 1024, 2);
+                const uint64_t vl = umma_desc(smem_u32(&sm.ring[st][TILE]), 16, 1024, 2);
+                for (int ks = 0; ks < 8; ++ks) {
+                    const uint32_t a_hi = tmem + s_col(b) + 32 * (ks >> 1) + 8 * (ks & 1);
+                    mma_bf16_ts(tmem + O_COL, a_hi, vh + 128 * ks, id_o, (t | ks) != 0);
+                    if (!(p.debug & 2)) {
+                        mma_bf16_ts(tmem + O_COL, a_hi, vl + 128 * ks, id_o, 1);
+                        mma_bf16_ts(tmem + O_COL, a_hi + 16, vh + 128 * ks, id_o, 1);
+                    }
+                }
+                mma_commit(&sm.empty[st]);
+                mma_commit(&sm.s_free[b]);
+                mma_commit(&sm.o_done[t & 1]);
+                if (++st == NS) {
+                    st = 0;
+                    fph ^= 1;
+                }
+            };
+            issue_S(0);
+            for (int t = 0; t < T; ++t) {
+                if (t + 1 < T) issue_S(t + 1);
+                issue_PV(t);
+            }
+        }
+    } else {
+        // ===================== softmax + streaming top-k (warps 2..5) =====================
+        const int qd = warp & 3;
+        const int row = 32 * qd + lane;
+        const int grow = qt * 128 + row;
+        const bool row_ok = grow < p.W;
+        const uint32_t lane_base = tmem + ((uint32_t)(32 * qd) << 16);
+        const int K = p.k_eff;
+        const float eps = row_ok ? EPS_REL * p.qnorm[(int64_t)h * p.W + grow] * p.kmax[h] : 0.0f;
+        TopkState ts;
+        ts.lst = &sm.list[row][0];
+        ts.sd = &sm.side[row][0];
+        ts.n = ts.nside = 0;
+        ts.K = K;
+        ts.tau = ts.thr = -INFINITY;
+        ts.eps = eps;
+        ts.overflow = !row_ok;
+        float m_used = -INFINITY, l = 0.0f;
+        uint32_t sph[3] = {0, 0, 0};
+
+        for (int t = 0; t < T; ++t) {
+            const int b = t % 3;
+            mbar_wait(&sm.s_full[b], sph[b]);
+            sph[b] ^= 1;
+            __syncwarp();  // .sync.aligned tcgen05 ops below need a converged warp
+            tc_fence_after();
+            uint32_t sr[4][32];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) tmem_ld_32x32b_x32(lane_base + s_col(b) + 32 * c, sr[c]);
+            tmem_wait_ld();
+            const int valid = p.W - t * 128;
+            float mt = -INFINITY;
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+#pragma unroll
+                for (int e = 0; e < 32; ++e) {
+                    if (32 * c + e >= valid) sr[c][e] = __float_as_uint(-INFINITY);
+                    mt = fmaxf(mt, __uint_as_float(sr[c][e]));
+                }
+            if (t == 0) {
+                m_used = mt;
+            } else {
+                const bool need = (mt - m_used) * p.c2 > RESCALE_LOG2;
+                if (__any_sync(0xffffffffu, need)) {
+                    // PV(t-1) done: completion #((t-1)>>1) of o_done[(t-1)&1]; PV(t-3) is already
+                    // implied by s_full(t) and PV(t+1) cannot have run, so this parity is exact
+                    mbar_wait(&sm.o_done[(t - 1) & 1], (uint32_t)(((t - 1) >> 1) & 1));
+                    __syncwarp();
+                    tc_fence_after();
+                    const float mnew = need ? mt : m_used;
+                    const float f = ex2_approx((m_used - mnew) * p.c2);
+                    uint32_t o[32];
+#pragma unroll
+                    for (int half = 0; half < 2; ++half) {
+                        tmem_ld_32x32b_x32(lane_base + O_COL + 32 * half, o);
+                        tmem_wait_ld();
+#pragma unroll
+                        for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * f);
+                        tmem_st_32x32b_x32(lane_base + O_COL + 32 * half, o);
+                    }
+                    tmem_wait_st();
+                    l *= f;
+                    m_used = mnew;
+                }
+            }
+            const float mc = m_used * p.c2;
+            float ls = 0.0f;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                uint32_t hi[16], lo[16];
+#pragma unroll
+                for (int e2 = 0; e2 < 16; ++e2) {
+                    const float x0 = __uint_as_float(sr[c][2 * e2]), x1 = __uint_as_float(sr[c][2 * e2 + 1]);
+                    const float p0 = ex2_approx(fmaf(x0, p.c2, -mc));
+                    const float p1 = ex2_approx(fmaf(x1, p.c2, -mc));
+                    ls += p0 + p1;
+                    hi[e2] = pack_bf16(p0, p1);
+                    const __nv_bfloat162 hb = *reinterpret_cast<const __nv_bfloat162*>(&hi[e2]);
+                    lo[e2] = pack_bf16(p0 - __low2float(hb), p1 - __high2float(hb));
+                }
+                tmem_st_32x32b_x16(lane_base + s_col(b) + 32 * c, hi);
+                tmem_st_32x32b_x16(lane_base + s_col(b) + 32 * c + 16, lo);
+            }
+            l += ls;
+            tmem_wait_st();
+            tc_fence_before();
+            mbar_arrive(&sm.p_full[t & 1]);
+
+            // ---- streaming top-k over this tile's approximate scores (after P is out)
+            if (K > 0 && !ts.overflow && !(p.debug & 1)) {
+                uint4 ex = make_uint4(0, 0, 0, 0);
+                if (p.exbits) ex = __ldg(reinterpret_cast<const uint4*>(p.exbits) + t);
+                const uint32_t exw[4] = {ex.x, ex.y, ex.z, ex.w};
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    float thr = ts.thr;
+                    uint32_t m = 0;
+#pragma unroll
+                    for (int e = 0; e < 32; ++e)
+                        m |= (__uint_as_float(sr[c][e]) >= thr && 32 * c + e < valid) ? (1u << e) : 0u;
+                    m &= ~exw[c];
+                    while (m) {
+                        const int e = __ffs(m) - 1;
+                        m &= m - 1;
+                        const float a = select32(sr[c], e);
+                        if (p.debug & 4) continue;
+                        if (a >= ts.thr) topk_handle(ts, a, t * 128 + 32 * c + e);
+                    }
+                }
+            }
+            __syncwarp();
+            if (p.debug & 16) ts.overflow = true;
+        }
+        // ------------------------------- epilogue -------------------------------
+        // the commit after PV(T-1) covers every earlier MMA
+        mbar_wait(&sm.o_done[(T - 1) & 1], (uint32_t)(((T - 1) >> 1) & 1));
+        __syncwarp();
+        tc_fence_after();
+        uint32_t o[2][32];
+        tmem_ld_32x32b_x32(lane_base + O_COL, o[0]);
+        tmem_ld_32x32b_x32(lane_base + O_COL + 32, o[1]);
+        tmem_wait_ld();
+        if (row_ok) {
+            const float inv = 1.0f / l;
+            float* dst = p.out + (int64_t)h * p.out_hs + (int64_t)grow * p.out_rs;
+#pragma unroll
+            for (int half = 0; half < 2; ++half)
+#pragma unroll
+                for (int e = 0; e < 32; e += 4)
+                    *reinterpret_cast<float4*>(dst + 32 * half + e) =
+                        make_float4(__uint_as_float(o[half][e]) * inv, __uint_as_float(o[half][e + 1]) * inv,
+                                    __uint_as_float(o[half][e + 2]) * inv, __uint_as_float(o[half][e + 3]) * inv);
+            if (p.lse) p.lse[(int64_t)h * p.W + grow] = m_used * p.scale + logf(l);
+            const int64_t r = (int64_t)h * p.W + grow;
+            if (K > 0) {
+                float2* cd = p.cand + r * CAND;
+                int cnt = 0;
+                for (int i = 0; i < ts.n; ++i) cd[cnt++] = ts.lst[i];
+                for (int i = 0; i < ts.nside; ++i)
+                    if (ts.sd[i].x >= ts.thr) cd[cnt++] = ts.sd[i];
+                p.cand_n[r] = cnt;
+            }
+            p.flag[r] = ts.overflow ? 1 : 0;
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc(tmem, TMEM_COLS);
+    }
+}
+
+// Exact re-score of the candidates and final ordering. One warp per row; lane
+// i owns candidates i and i+32. scaled_dot order (dot.hpp:11-23) without FMA.
+__global__ void rescore_kernel(const float* __restrict__ qc, const float* __restrict__ kc, int heads, int W,
+                               float scale, int k_eff, const float2* __restrict__ cand, const int* __restrict__ cand_n,
+                               const uint8_t* __restrict__ flag, int32_t* topk, float* guide) {
+    const int64_t r = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+    const int lane = threadIdx.x & 31;
+    if (r >= (int64_t)heads * W || flag[r]) return;
+    const int h = (int)(r / W);
+    const float* q = qc + r * 64;
+    const int cnt = cand_n[r];
+    float e[2];
+    int idx[2];
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+        const int i = lane + 32 * s;
+        e[s] = -INFINITY;
+        idx[s] = -1;
+        if (i < cnt) {
+            idx[s] = __float_as_int(cand[r * CAND + i].y);
+            const float* k = kc + ((int64_t)h * W + idx[s]) * 64;
+            ExactDot4 d;
+            d.zero();
+#pragma unroll 4
+            for (int x = 0; x < 64; x += 4) {
+                const float4 qv = __ldg(reinterpret_cast<const float4*>(q + x));
+                const float4 kv = __ldg(reinterpret_cast<const float4*>(k + x));
+                d.step(qv.x, qv.y, qv.z, qv.w, kv.x, kv.y, kv.z, kv.w);
+            }
+            e[s] = d.finish(scale);
+        }
+    }
+    // rank = number of candidates strictly better under topk_better
+    int rank[2] = {0, 0};
+    for (int j = 0; j < cnt; ++j) {
+        const float ej = __shfl_sync(0xffffffffu, e[j >> 5], j & 31);
+        const int ij = __shfl_sync(0xffffffffu, idx[j >> 5], j & 31);
+#pragma unroll
+        for (int s = 0; s < 2; ++s)
+            if (topk_better(ej, ij, e[s], idx[s])) ++rank[s];
+    }
+#pragma unroll
+    for (int s = 0; s < 2; ++s)
+        if (idx[s] >= 0 && rank[s] < k_eff) {
+            topk[r * k_eff + rank[s]] = idx[s];
+            if (guide) guide[r * k_eff + rank[s]] = e[s];
+        }
+}
+
+// f32 [H][W][64] (strided) -> bf16 hi, lo contiguous + row norms
+__global__ void split_kernel(const float* __restrict__ x, int64_t hs, int64_t rs, int heads, int W,
+                             __nv_bfloat16* hi, __nv_bfloat16* lo, float* norm) {
+    const int64_t row = (int64_t)blockIdx.x * (blockDim.x / 8) + threadIdx.x / 8;
+    const int c = threadIdx.x & 7;
+    float sq = 0.0f;
+    if (row < (int64_t)heads * W) {
+        const int h = (int)(row / W), w = (int)(row % W);
+        const float* src = x + (int64_t)h * hs + (int64_t)w * rs + 8 * c;
+        __nv_bfloat16 H8[8], L8[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const float v = src[i];
+            H8[i] = __float2bfloat16_rn(v);
+            L8[i] = __float2bfloat16_rn(v - __bfloat162float(H8[i]));
+            sq = fmaf(v, v, sq);
+        }
+        *reinterpret_cast<uint4*>(hi + row * 64 + 8 * c) = *reinterpret_cast<uint4*>(H8);
+        *reinterpret_cast<uint4*>(lo + row * 64 + 8 * c) = *reinterpret_cast<uint4*>(L8);
+    }
+    sq += __shfl_xor_sync(0xffffffffu, sq, 1);
+    sq += __shfl_xor_sync(0xffffffffu, sq, 2);
+    sq += __shfl_xor_sync(0xffffffffu, sq, 4);
+    if (norm && c == 0 && row < (int64_t)heads * W) norm[row] = sqrtf(sq);
+}
+
+// per-head max of the key-window norms (order-free, deterministic)
+__global__ void rowmax_kernel(const float* __restrict__ norm, int W, float* out) {
+    const int h = blockIdx.x;
+    float m = 0.0f;
+    for (int i = threadIdx.x; i < W; i += blockDim.x) m = fmaxf(m, norm[(int64_t)h * W + i]);
+    __shared__ float red[32];
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x / 32] = m;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        m = threadIdx.x < blockDim.x / 32 ? red[threadIdx.x] : 0.0f;
+        for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+        if (threadIdx.x == 0) out[h] = m;
+    }
+}
+
+__global__ void exbits_kernel(const uint8_t* __restrict__ ex, int W, int words, uint32_t* bits) {
+    const int wd = blockIdx.x * blockDim.x + threadIdx.x;
+    if (wd >= words) return;
+    uint32_t v = 0;
+    for (int b = 0; b < 32; ++b) {
+        const int i = wd * 32 + b;
+        if (i < W && ex[i]) v |= 1u << b;
+    }
+    bits[wd] = v;
+}
+
+// 64-row blocks containing a flagged row -> list for the exact fallback
+__global__ void flag_blocks_kernel(const uint8_t* __restrict__ flag, int heads, int W, int* list, int* count) {
+    const int qtiles = (W + 63) / 64;
+    const int blk = blockIdx.x * blockDim.x + threadIdx.x;
+    if (blk >= heads * qtiles) return;
+    const int h = blk / qtiles, t = blk % qtiles;
+    bool any = false;
+    for (int i = t * 64; i < min(W, t * 64 + 64); ++i) any |= flag[(int64_t)h * W + i] != 0;
+    if (any) list[atomicAdd(count, 1)] = blk;
+}
+
+struct Ws {
+    __nv_bfloat16 *qh, *ql, *kh, *kl, *vh, *vl;
+    float *qn, *kn, *kmax;
+    uint32_t* exbits;
+    float2* cand;
+    int* cand_n;
+    uint8_t* flag;
+    int* blocks;
+    int* nblocks;
+    size_t used;
+};
+
+Ws carve_ws(void* base, int heads, int W, bool dry) {
+    Ws w{};
+    size_t off = 0;
+    auto take = [&](size_t bytes) -> char* {
+        off = (off + 255) & ~size_t(255);
+        char* p = dry ? nullptr : static_cast<char*>(base) + off;
+        off += bytes;
+        return p;
+    };
+    const size_t n = (size_t)heads * W;
+    w.qh = reinterpret_cast<__nv_bfloat16*>(take(n * 128));
+    w.ql = reinterpret_cast<__nv_bfloat16*>(take(n * 128));
+    w.kh = reinterpret_cast<__nv_bfloat16*>(take(n * 128));
+    w.kl = reinterpret_cast<__nv_bfloat16*>(take(n * 128));
+    w.vh = reinterpret_cast<__nv_bfloat16*>(take(n * 128));
+    w.vl = reinterpret_cast<__nv_bfloat16*>(take(n * 128));
+    w.qn = reinterpret_cast<float*>(take(n * 4));
+    w.kn = reinterpret_cast<float*>(take(n * 4));
+    w.kmax = reinterpret_cast<float*>(take((size_t)heads * 4));
+    w.exbits = reinterpret_cast<uint32_t*>(take((size_t)((W + 127) / 128) * 16));
+    w.cand = reinterpret_cast<float2*>(take(n * CAND * 8));
+    w.cand_n = reinterpret_cast<int*>(take(n * 4));
+    w.flag = reinterpret_cast<uint8_t*>(take(n));
+    w.blocks = reinterpret_cast<int*>(take((size_t)heads * ((W + 63) / 64) * 4));
+    w.nblocks = reinterpret_cast<int*>(take(4));
+    w.used = off + 256;
+    return w;
+}
+
+bool contiguous_f32(const gsa_tensor& t) {
+    return t.dtype == GSA_DTYPE_F32 && t.dim == 64 && (reinterpret_cast<uintptr_t>(t.data) & 15) == 0 &&
+           t.row_stride == 64 && t.head_stride == (int64_t)t.rows * 64;
+}
+
+}  // namespace
+
+size_t tc_compress_workspace_bytes(int heads, int windows, int dim, int k_eff) {
+    if (dim != 64 || k_eff > KCAP) return 0;
+    return carve_ws(nullptr, heads, windows, true).used;
+}
+
+bool tc_compress_split_buffers(void* ws, size_t ws_bytes, int heads, int windows, int dim, int k_eff,
+                               CompressSplits* out) {
+    if (dim != 64 || k_eff > KCAP || !ws || ws_bytes < carve_ws(nullptr, heads, windows, true).used) return false;
+    Ws w = carve_ws(ws, heads, windows, false);
+    *out = CompressSplits{w.qh, w.ql, w.kh, w.kl, w.vh, w.vl, w.qn, w.kn};
+    return true;
+}
+
+cudaError_t tc_compress_topk(const gsa_tensor& qc, const gsa_tensor& kc, const gsa_tensor& vc, int k_eff, float scale,
+                             const uint8_t* excluded, float* out, int64_t out_hs, int64_t out_rs, float* lse,
+                             int32_t* topk, float* guide, void* ws, size_t ws_bytes, cudaStream_t st) {
+    return tc_compress_topk_splits(nullptr, qc, kc, vc, k_eff, scale, excluded, out, out_hs, out_rs, lse, topk, guide,
+                                   ws, ws_bytes, st);
+}
+
+cudaError_t tc_compress_topk_splits(const CompressSplits* pre, const gsa_tensor& qc, const gsa_tensor& kc,
+                                    const gsa_tensor& vc, int k_eff, float scale, const uint8_t* excluded,
+                                    float* out, int64_t out_hs, int64_t out_rs, float* lse, int32_t* topk,
+                                    float* guide, void* ws, size_t ws_bytes, cudaStream_t st) {
+    const int H = qc.heads, W = qc.rows;
+    AttnArgs ex{};  // exact CUDA-core kernel (phase-1 path and fallback)
+    ex.q = TensorRef{qc.data, qc.dtype, qc.head_stride, qc.row_stride};
+    ex.k = TensorRef{kc.data, kc.dtype, kc.head_stride, kc.row_stride};
+    ex.v = TensorRef{vc.data, vc.dtype, vc.head_stride, vc.row_stride};
+    ex.heads = H;
+    ex.mq = W;
+    ex.mk = kc.rows;
+    ex.dim = qc.dim;
+    ex.scale = scale;
+    ex.out = out;
+    ex.out_hs = out_hs;
+    ex.out_rs = out_rs;
+    ex.lse = lse;
+    ex.topk = k_eff > 0 ? topk : nullptr;
+    ex.guide = guide;
+    ex.k_eff = k_eff;
+    ex.excluded = excluded;
+    const bool tc_ok = qc.dim == 64 && k_eff <= KCAP && contiguous_f32(qc) && contiguous_f32(kc) &&
+                       contiguous_f32(vc) && tmap_encode_fn() != nullptr && ws &&
+                       ws_bytes >= carve_ws(nullptr, H, W, true).used && W > 0;
+    if (!tc_ok) return launch_attn_f32(ex, st);
+
+    Ws w = carve_ws(ws, H, W, false);
+    const __nv_bfloat16 *qh = w.qh, *ql = w.ql, *kh = w.kh, *kl = w.kl, *vh = w.vh, *vl = w.vl;
+    const float *qn = w.qn, *kn = w.kn;
+    if (pre) {
+        qh = pre->qh; ql = pre->ql; kh = pre->kh; kl = pre->kl; vh = pre->vh; vl = pre->vl;
+        qn = pre->qnorm; kn = pre->knorm;
+    } else {
+        const unsigned blocks = (unsigned)(((int64_t)H * W + 31) / 32);
+        split_kernel<<<blocks, 256, 0, st>>>(static_cast<const float*>(qc.data), qc.head_stride, qc.row_stride, H, W,
+                                              w.qh, w.ql, w.qn);
+        split_kernel<<<blocks, 256, 0, st>>>(static_cast<const float*>(kc.data), kc.head_stride, kc.row_stride, H, W,
+                                              w.kh, w.kl, w.kn);
+        split_kernel<<<blocks, 256, 0, st>>>(static_cast<const float*>(vc.data), vc.head_stride, vc.row_stride, H, W,
+                                              w.vh, w.vl, nullptr);
+        note_launch(3);
+    }
+    rowmax_kernel<<<H, 256, 0, st>>>(kn, W, w.kmax);
+    note_launch();
+    const int tiles = (W + 127) / 128;
+    if (excluded) {
+        exbits_kernel<<<(tiles * 4 + 127) / 128, 128, 0, st>>>(excluded, W, tiles * 4, w.exbits);
+        note_launch();
+    }
+    CUtensorMap tqh, tql, tkh, tkl, tvh, tvl;
+    const int64_t hs = (int64_t)W * 64;
+    if (!make_rows_tmap(&tqh, qh, H, W, hs, 64) || !make_rows_tmap(&tql, ql, H, W, hs, 64) ||
+        !make_rows_tmap(&tkh, kh, H, W, hs, 64) || !make_rows_tmap(&tkl, kl, H, W, hs, 64) ||
+        !make_rows_tmap(&tvh, vh, H, W, hs, 64) || !make_rows_tmap(&tvl, vl, H, W, hs, 64))
+        return launch_attn_f32(ex, st);
+    CompParams p{};
+    if (const char* dbg = getenv("GSA_DEBUG_COMPRESS")) p.debug = atoi(dbg);
+    p.heads = H;
+    p.W = W;
+    p.k_eff = k_eff;
+    p.scale = scale;
+    p.c2 = scale * 1.4426950408889634f;
+    p.kv_tiles = tiles;
+    p.qnorm = qn;
+    p.kmax = w.kmax;
+    p.exbits = excluded ? w.exbits : nullptr;
+    p.out = out;
+    p.out_hs = out_hs;
+    p.out_rs = out_rs;
+    p.lse = lse;
+    p.cand = w.cand;
+    p.cand_n = w.cand_n;
+    p.flag = w.flag;
+    const size_t smem = sizeof(CompSmem) + 1024;
+    cudaError_t e = cudaFuncSetAttribute(compress_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    compress_tc_kernel<<<dim3(tiles, H), NTHREADS, smem, st>>>(tqh, tql, tkh, tkl, tvh, tvl, p);
+    note_launch();
+    if (k_eff > 0) {
+        const int64_t rows = (int64_t)H * W;
+        rescore_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(static_cast<const float*>(qc.data),
+                                                                   static_cast<const float*>(kc.data), H, W, scale,
+                                                                   k_eff, w.cand, w.cand_n, w.flag, topk, guide);
+        note_launch();
+        // rows whose near-tie side list overflowed: exact recompute of their 64-row blocks
+        cudaMemsetAsync(w.nblocks, 0, sizeof(int), st);
+        const int nb = H * ((W + 63) / 64);
+        flag_blocks_kernel<<<(nb + 127) / 128, 128, 0, st>>>(w.flag, H, W, w.blocks, w.nblocks);
+        note_launch();
+        ex.block_list = w.blocks;
+        ex.block_count = w.nblocks;
+        ex.topk_only = true;
+        e = launch_attn_f32(ex, st);
+        if (e != cudaSuccess) return e;
+    }
+    return cudaGetLastError();
+}
+
+}  // namespace gsa_sm100

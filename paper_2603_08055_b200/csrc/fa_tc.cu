@@ -37,7 +37,9 @@ struct __align__(1024) FaSmem {
     uint64_t full[NS], empty[NS];
     uint64_t q_full;
     uint64_t s_full[3], s_free[3];
-    uint64_t p_full, o_done;
+    // by tile parity: the softmax runs up to a tile ahead of the MMA, and parity waits are
+    // only unambiguous within one phase of their target
+    uint64_t p_full[2], o_done[2];
     uint32_t tmem_base;
 };
 
@@ -75,8 +77,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             mbar_init(&sm.s_free[i], 1);
         }
         mbar_init(&sm.q_full, 1);
-        mbar_init(&sm.p_full, 128);
-        mbar_init(&sm.o_done, 1);
+        mbar_init(&sm.p_full[0], 128);
+        mbar_init(&sm.p_full[1], 128);
+        mbar_init(&sm.o_done[0], 1);
+        mbar_init(&sm.o_done[1], 1);
         fence_barrier_init();
         prefetch_tmap(&tm_q);
         prefetch_tmap(&tm_k);
@@ -118,7 +122,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             int st = 0;
             uint32_t fph = 0;
             uint32_t freeph[3] = {1, 1, 1};
-            uint32_t pph = 0;
+            uint32_t pph[2] = {0, 0};
             mbar_wait(&sm.q_full, 0);
             const uint64_t qdesc = umma_desc(smem_u32(&sm.q[0]), 16, 1024, 2);
             auto issue_S = [&](int t) {
@@ -139,8 +143,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             };
             auto issue_PV = [&](int t) {
                 const int b = t % 3;
-                mbar_wait(&sm.p_full, pph);
-                pph ^= 1;
+                mbar_wait(&sm.p_full[t & 1], pph[t & 1]);
+                pph[t & 1] ^= 1;
                 mbar_wait(&sm.full[st], fph);
                 tc_fence_after();
                 const uint64_t vdesc = umma_desc(smem_u32(&sm.ring[st][0]), 16, 1024, 2);
@@ -153,7 +157,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 }
                 mma_commit(&sm.empty[st]);
                 mma_commit(&sm.s_free[b]);
-                mma_commit(&sm.o_done);
+                mma_commit(&sm.o_done[t & 1]);
                 if (++st == NS) {
                     st = 0;
                     fph ^= 1;
@@ -176,6 +180,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             const int b = t % 3;
             mbar_wait(&sm.s_full[b], sph[b]);
             sph[b] ^= 1;
+            __syncwarp();  // .sync.aligned tcgen05 ops below need a converged warp
             tc_fence_after();
             uint32_t sr[4][32];
 #pragma unroll
@@ -195,11 +200,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             } else {
                 const bool need = (mt - m_used) * p.c2 > RESCALE_LOG2;
                 if (__any_sync(0xffffffffu, need)) {
-                    // rescale O (TMEM) and l once PV(t-1) has landed. o_done completes
-                    // once per PV; parity waits are only unambiguous one phase back, so
-                    // step through completion t-2 (already implied by s_full(t)) first.
-                    if (t >= 2) mbar_wait(&sm.o_done, (uint32_t)((t - 2) & 1));
-                    mbar_wait(&sm.o_done, (uint32_t)((t - 1) & 1));
+                    // rescale O (TMEM) and l once PV(t-1) has landed.
+                    // PV(t-1) done: completion #((t-1)>>1) of o_done[(t-1)&1]; PV(t-3) is already
+                    // implied by s_full(t) and PV(t+1) cannot have run, so this parity is exact
+                    mbar_wait(&sm.o_done[(t - 1) & 1], (uint32_t)(((t - 1) >> 1) & 1));
+                    __syncwarp();
                     tc_fence_after();
                     const float mnew = need ? mt : m_used;
                     const float f = ex2_approx((m_used - mnew) * p.c2);
@@ -238,12 +243,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             l += ls;
             tmem_wait_st();
             tc_fence_before();
-            mbar_arrive(&sm.p_full);
+            mbar_arrive(&sm.p_full[t & 1]);
         }
         // ------------------------------- epilogue -------------------------------
-        // PV(T-2) is issued after S(T-1), so o_done may still be two phases back here
-        if (T >= 2) mbar_wait(&sm.o_done, (uint32_t)((T - 2) & 1));
-        mbar_wait(&sm.o_done, (uint32_t)((T - 1) & 1));
+        // the commit after PV(T-1) covers every earlier MMA
+        mbar_wait(&sm.o_done[(T - 1) & 1], (uint32_t)(((T - 1) >> 1) & 1));
+        __syncwarp();
         tc_fence_after();
         uint32_t o[2][32];
         tmem_ld_32x32b_x32(lane_base + O_COL, o[0]);

@@ -42,6 +42,12 @@ struct AttnArgs {
     float* guide;
     int k_eff;
     const uint8_t* excluded;  // [mk] or null
+    // fallback mode for the tensor-core compressed kernel: CTA b recomputes the
+    // 64-row block block_list[b] (= h * ceil(mq/64) + tile) if b < *block_count,
+    // writing only top-k indices / guide scores
+    const int* block_list;
+    const int* block_count;
+    bool topk_only;
 };
 cudaError_t launch_attn_f32(const AttnArgs& a, cudaStream_t st);
 

@@ -349,6 +349,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             const int fb = (int)(jf & 1);
             mbar_wait(&sm.o_full[fb], oph[fb]);
             oph[fb] ^= 1;
+            __syncwarp();
             tc_fence_after();
             uint32_t orr[16];
             tmem_ld_32x32b_x16(tmem + ((uint32_t)(32 * qd) << 16) + (fb ? O_COL1 : O_COL0), orr);
@@ -411,6 +412,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             const int nkeys = it.group_windows() * 16;
             mbar_wait(&sm.s_full[sb], sph[sb]);
             sph[sb] ^= 1;
+            __syncwarp();
             tc_fence_after();
             float s[4][2][8];
             const uint32_t scol = tmem + (sb ? S_COL1 : S_COL0);

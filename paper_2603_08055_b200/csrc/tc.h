@@ -18,6 +18,18 @@ cudaError_t tc_dense_attention(const gsa_tensor& q, const gsa_tensor& k, const g
 // approximate scores + exact re-scoring of the boundary candidates when
 // supported, else the exact CUDA-core kernel. Indices are bit-exact either way.
 size_t tc_compress_workspace_bytes(int heads, int windows, int dim, int k_eff);
+// pre-split operands (bf16 hi/lo of contiguous [H][W][64] Qc/Kc/Vc + row norms),
+// e.g. written by the pooling kernel; carved from the compress workspace
+struct CompressSplits {
+    __nv_bfloat16 *qh, *ql, *kh, *kl, *vh, *vl;
+    float *qnorm, *knorm;
+};
+bool tc_compress_split_buffers(void* ws, size_t ws_bytes, int heads, int windows, int dim, int k_eff,
+                               CompressSplits* out);
+cudaError_t tc_compress_topk_splits(const CompressSplits* pre, const gsa_tensor& qc, const gsa_tensor& kc,
+                                    const gsa_tensor& vc, int k_eff, float scale, const uint8_t* excluded,
+                                    float* out, int64_t out_hs, int64_t out_rs, float* lse, int32_t* topk,
+                                    float* guide, void* ws, size_t ws_bytes, cudaStream_t st);
 cudaError_t tc_compress_topk(const gsa_tensor& qc, const gsa_tensor& kc, const gsa_tensor& vc, int k_eff,
                              float scale, const uint8_t* excluded, float* out, int64_t out_hs,
                              int64_t out_rs, float* lse, int32_t* topk, float* guide, void* ws,

@@ -1,5 +1,4 @@
-// tc_dispatch.cu — routes each stage to its tensor-core kernel when the shape
-// is on the fast path, otherwise to the exact CUDA-core kernel.
+// tc_dispatch.cu — library-wide launch accounting (gsa_launch_count).
 #include "tc.h"
 
 #include <atomic>
@@ -8,35 +7,6 @@ namespace gsa_sm100 {
 
 std::atomic<unsigned long long> g_launch_total{0};
 void note_launch(int n) { g_launch_total += (unsigned long long)n; }
-
-
-size_t tc_compress_workspace_bytes(int, int, int, int) { return 0; }
-
-cudaError_t tc_compress_topk(const gsa_tensor& qc, const gsa_tensor& kc, const gsa_tensor& vc, int k_eff,
-                             float scale, const uint8_t* excluded, float* out, int64_t out_hs,
-                             int64_t out_rs, float* lse, int32_t* topk, float* guide, void*, size_t,
-                             cudaStream_t st) {
-    AttnArgs a{};
-    a.q = TensorRef{qc.data, qc.dtype, qc.head_stride, qc.row_stride};
-    a.k = TensorRef{kc.data, kc.dtype, kc.head_stride, kc.row_stride};
-    a.v = TensorRef{vc.data, vc.dtype, vc.head_stride, vc.row_stride};
-    a.heads = qc.heads;
-    a.mq = qc.rows;
-    a.mk = kc.rows;
-    a.dim = qc.dim;
-    a.scale = scale;
-    a.out = out;
-    a.out_hs = out_hs;
-    a.out_rs = out_rs;
-    a.lse = lse;
-    a.topk = topk;
-    a.guide = guide;
-    a.k_eff = k_eff;
-    a.excluded = excluded;
-    // k_eff == 0 (everything excluded) still needs the softmax half
-    if (k_eff == 0) a.topk = nullptr;
-    return launch_attn_f32(a, st);
-}
 
 
 }  // namespace gsa_sm100

@@ -6,6 +6,7 @@
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <stdint.h>
+#include <cstdio>
 
 namespace gsa_sm100 {
 namespace ptx {
@@ -52,8 +53,17 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     if (mbar_try_wait(bar, parity)) return;
     const uint64_t t0 = globaltimer_ns();
     uint32_t n = 0;
+    bool reported = false;
     while (!mbar_try_wait(bar, parity)) {
-        if ((++n & 1023) == 0 && globaltimer_ns() - t0 > 20000000000ull) __trap();
+        if ((++n & 1023) == 0) {
+            const uint64_t dt = globaltimer_ns() - t0;
+            if (!reported && dt > 4000000000ull) {
+                printf("gsa watchdog: block (%d,%d,%d) thread %d stuck on mbarrier smem+0x%x parity %u\n", blockIdx.x,
+                       blockIdx.y, blockIdx.z, threadIdx.x, smem_u32(bar), parity);
+                reported = true;
+            }
+            if (dt > 10000000000ull) __trap();
+        }
     }
 }
 
