@@ -33,7 +33,7 @@ namespace {
 
 using namespace ptx;
 
-constexpr int NS = 4;
+constexpr int NS = 3;
 constexpr int TILE = 16384;       // 128 rows x 64 bf16
 constexpr int STAGE = 2 * TILE;   // hi + lo
 constexpr int NTHREADS = 192;
@@ -41,16 +41,16 @@ constexpr uint32_t TMEM_COLS = 512;
 constexpr uint32_t O_COL = 384;
 constexpr float RESCALE_LOG2 = 8.0f;
 constexpr int KCAP = 32;          // max k_eff on this path
-constexpr int SIDE = 16;
-constexpr int CAND = KCAP + SIDE;
+constexpr int SCAP = 95;          // per-row candidate stage (odd stride: 2-way banks at most)
+constexpr int FLUSH_AT = SCAP - 32;  // flush before a 32-column chunk could overflow the stage
+constexpr int CAND = 64;          // candidates handed to the exact re-score (2 per lane)
 constexpr float EPS_REL = 0.00048828125f;  // 2^-11
 constexpr float DELTA_REL = 9.5367431640625e-07f;  // 2^-20: collapse of distinct sums under *scale
 
 struct __align__(1024) CompSmem {
     uint8_t qh[TILE], ql[TILE];
     uint8_t ring[NS][STAGE];
-    float2 list[128][KCAP + 1];  // per row: (approx score, index bits), sorted desc; padded stride
-    float2 side[128][SIDE + 1];
+    float2 stage[128][SCAP];     // per row: candidates (approx score, index bits), unsorted
     uint64_t full[NS], empty[NS];
     uint64_t q_full;
     uint64_t s_full[3], s_free[3];
@@ -62,69 +62,68 @@ struct __align__(1024) CompSmem {
 
 struct CompParams {
     int debug;  // bring-up switches (GSA_DEBUG_COMPRESS): 1 = no top-k scan, 2 = 1-term S/PV
-    int heads, W, k_eff;
+    int heads, Wq, Wk, k_eff;  // query rows (windows of this shard) / key rows (all windows)
     float scale, c2;
     int kv_tiles;
-    const float* qnorm;      // [H][W]
+    const float* qnorm;      // [H][Wq]
     const float* kmax;       // [H]
-    const uint32_t* exbits;  // [ceil(W/32)] or null
+    const uint32_t* exbits;  // [ceil(Wk/32)] or null
     float* out;
     int64_t out_hs, out_rs;
-    float* lse;              // [H][W]
-    float2* cand;            // [H*W][CAND]
-    int* cand_n;             // [H*W]
-    uint8_t* flag;           // [H*W]
+    float* lse;              // [H][Wq]
+    float2* cand;            // [H*Wq][CAND]
+    int* cand_n;             // [H*Wq]
+    uint8_t* flag;           // [H*Wq]
 };
 
 __device__ __forceinline__ uint32_t s_col(int b) { return (uint32_t)(128 * b); }
 
-// per-row streaming top-k state (kept off the hot path: touched only for candidates)
-struct TopkState {
-    float2* lst;  // sorted desc by approximate score, K entries when full
-    float2* sd;   // side list (near-tie candidates)
-    int n, nside, K;
-    float tau, thr, eps;
-    bool overflow;
-};
+// order-preserving map float -> uint32 (finite and +-inf); 0 is below every real key
+__device__ __forceinline__ uint32_t fkey(float x) {
+    const uint32_t b = __float_as_uint(x);
+    return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+__device__ __forceinline__ float fkey_inv(uint32_t k) {
+    return __uint_as_float((k & 0x80000000u) ? (k & 0x7fffffffu) : ~k);
+}
 
-__device__ __noinline__ void topk_handle(TopkState& s, float a, int col) {
-    auto set_thr = [&]() { s.thr = s.tau - (2.0f * s.eps + DELTA_REL * fabsf(s.tau)); };
-    auto side_push = [&](float v, int c) {
-        if (s.nside == SIDE) {  // drop what the risen threshold has excluded since
-            int w = 0;
-            for (int i = 0; i < SIDE; ++i)
-                if (s.sd[i].x >= s.thr) s.sd[w++] = s.sd[i];
-            s.nside = w;
-            if (s.nside == SIDE) {
-                s.overflow = true;  // near-tie flood: the exact kernel redoes this row
-                return;
-            }
-        }
-        s.sd[s.nside++] = make_float2(v, __int_as_float(c));
-    };
-    auto insert = [&](float v, int c) {
-        int i = s.n < s.K ? s.n : s.K - 1;
-        while (i > 0 && s.lst[i - 1].x < v) {
-            s.lst[i] = s.lst[i - 1];
-            --i;
-        }
-        s.lst[i] = make_float2(v, __int_as_float(c));
-    };
-    if (s.n < s.K) {
-        insert(a, col);
-        if (++s.n == s.K) {
-            s.tau = s.lst[s.K - 1].x;
-            set_thr();
-        }
-    } else if (a > s.tau) {
-        const float2 ev = s.lst[s.K - 1];
-        insert(a, col);
-        s.tau = s.lst[s.K - 1].x;
-        set_thr();
-        if (ev.x >= s.thr) side_push(ev.x, __float_as_int(ev.y));
-    } else {
-        side_push(a, col);
+__device__ __forceinline__ float topk_threshold(float tau, float eps) {
+    return tau - (2.0f * eps + DELTA_REL * fabsf(tau));
+}
+
+// Warp-cooperative flush of row R's candidate stage (n entries, all >= thr):
+// exact K-th largest approximate score tau by a 32-step radix select over
+// order-preserving keys (3 entries per lane, counts summed with redux.sync),
+// then keep only entries >= the raised threshold. Returns the new count
+// (>= K); the owner lane takes it and the new threshold.
+__device__ __noinline__ int flush_stage(float2* stage, int n, int K, float eps, float& thr, int lane) {
+    float2 e[3];
+    uint32_t key[3];
+#pragma unroll
+    for (int s = 0; s < 3; ++s) {
+        const int i = lane + 32 * s;
+        e[s] = i < n ? stage[i] : make_float2(-INFINITY, 0.0f);
+        key[s] = i < n ? fkey(e[s].x) : 0u;
     }
+    uint32_t res = 0;
+#pragma unroll 1
+    for (int bit = 31; bit >= 0; --bit) {
+        const uint32_t cand = res | (1u << bit);
+        const int c = (key[0] >= cand) + (key[1] >= cand) + (key[2] >= cand);
+        if ((int)__reduce_add_sync(0xffffffffu, (unsigned)c) >= K) res = cand;
+    }
+    thr = fmaxf(thr, topk_threshold(fkey_inv(res), eps));
+    __syncwarp();
+    int base = 0;
+#pragma unroll
+    for (int s = 0; s < 3; ++s) {
+        const bool keep = key[s] != 0u && e[s].x >= thr;
+        const unsigned b = __ballot_sync(0xffffffffu, keep);
+        if (keep) stage[base + __popc(b & ((1u << lane) - 1u))] = e[s];
+        base += __popc(b);
+    }
+    __syncwarp();
+    return base;
 }
 
 // v[e] for a runtime e without local memory: a 5-level select tree
@@ -266,18 +265,13 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         const int qd = warp & 3;
         const int row = 32 * qd + lane;
         const int grow = qt * 128 + row;
-        const bool row_ok = grow < p.W;
+        const bool row_ok = grow < p.Wq;
         const uint32_t lane_base = tmem + ((uint32_t)(32 * qd) << 16);
         const int K = p.k_eff;
-        const float eps = row_ok ? EPS_REL * p.qnorm[(int64_t)h * p.W + grow] * p.kmax[h] : 0.0f;
-        TopkState ts;
-        ts.lst = &sm.list[row][0];
-        ts.sd = &sm.side[row][0];
-        ts.n = ts.nside = 0;
-        ts.K = K;
-        ts.tau = ts.thr = -INFINITY;
-        ts.eps = eps;
-        ts.overflow = !row_ok;
+        const float eps = row_ok ? EPS_REL * p.qnorm[(int64_t)h * p.Wq + grow] * p.kmax[h] : 0.0f;
+        float thr = -INFINITY;  // this row's candidate threshold (monotone lower bound of tau - margin)
+        int cnt = row_ok ? 0 : -1;  // staged candidates; -1 = overflowed / no row (exact fallback)
+        float2* my_stage = sm.stage[row];
         float m_used = -INFINITY, l = 0.0f;
         uint32_t sph[3] = {0, 0, 0};
 
@@ -291,15 +285,29 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 #pragma unroll
             for (int c = 0; c < 4; ++c) tmem_ld_32x32b_x32(lane_base + s_col(b) + 32 * c, sr[c]);
             tmem_wait_ld();
-            const int valid = p.W - t * 128;
-            float mt = -INFINITY;
+            const int valid = p.Wk - t * 128;
+            float cmax[4];
+            if (valid < 128) {  // last key tile only: columns past Wk do not exist
 #pragma unroll
-            for (int c = 0; c < 4; ++c)
+                for (int c = 0; c < 4; ++c)
 #pragma unroll
-                for (int e = 0; e < 32; ++e) {
-                    if (32 * c + e >= valid) sr[c][e] = __float_as_uint(-INFINITY);
-                    mt = fmaxf(mt, __uint_as_float(sr[c][e]));
+                    for (int e = 0; e < 32; ++e)
+                        if (32 * c + e >= valid) sr[c][e] = __float_as_uint(-INFINITY);
+            }
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {  // 4-way tree per chunk (short dependency chains)
+                float a0 = __uint_as_float(sr[c][0]), a1 = __uint_as_float(sr[c][1]);
+                float a2 = __uint_as_float(sr[c][2]), a3 = __uint_as_float(sr[c][3]);
+#pragma unroll
+                for (int e = 4; e < 32; e += 4) {
+                    a0 = fmaxf(a0, __uint_as_float(sr[c][e]));
+                    a1 = fmaxf(a1, __uint_as_float(sr[c][e + 1]));
+                    a2 = fmaxf(a2, __uint_as_float(sr[c][e + 2]));
+                    a3 = fmaxf(a3, __uint_as_float(sr[c][e + 3]));
                 }
+                cmax[c] = fmaxf(fmaxf(a0, a1), fmaxf(a2, a3));
+            }
+            const float mt = fmaxf(fmaxf(cmax[0], cmax[1]), fmaxf(cmax[2], cmax[3]));
             if (t == 0) {
                 m_used = mt;
             } else {
@@ -327,7 +335,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 }
             }
             const float mc = m_used * p.c2;
-            float ls = 0.0f;
+            float lsum[4] = {0.0f, 0.0f, 0.0f, 0.0f};  // independent partial sums
 #pragma unroll
             for (int c = 0; c < 4; ++c) {
                 uint32_t hi[16], lo[16];
@@ -336,7 +344,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     const float x0 = __uint_as_float(sr[c][2 * e2]), x1 = __uint_as_float(sr[c][2 * e2 + 1]);
                     const float p0 = ex2_approx(fmaf(x0, p.c2, -mc));
                     const float p1 = ex2_approx(fmaf(x1, p.c2, -mc));
-                    ls += p0 + p1;
+                    lsum[e2 & 3] += p0 + p1;
                     hi[e2] = pack_bf16(p0, p1);
                     const __nv_bfloat162 hb = *reinterpret_cast<const __nv_bfloat162*>(&hi[e2]);
                     lo[e2] = pack_bf16(p0 - __low2float(hb), p1 - __high2float(hb));
@@ -344,35 +352,94 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 tmem_st_32x32b_x16(lane_base + s_col(b) + 32 * c, hi);
                 tmem_st_32x32b_x16(lane_base + s_col(b) + 32 * c + 16, lo);
             }
-            l += ls;
+            l += (lsum[0] + lsum[1]) + (lsum[2] + lsum[3]);
             tmem_wait_st();
             tc_fence_before();
             mbar_arrive(&sm.p_full[t & 1]);
 
-            // ---- streaming top-k over this tile's approximate scores (after P is out)
-            if (K > 0 && !ts.overflow && !(p.debug & 1)) {
+            // ---- streaming top-k over this tile's approximate scores (after P is out):
+            // append every selectable score >= thr to the row's stage; a full stage is
+            // flushed by the whole warp (radix select of the K-th best, threshold raise)
+            if (K > 0 && !(p.debug & 1)) {
                 uint4 ex = make_uint4(0, 0, 0, 0);
                 if (p.exbits) ex = __ldg(reinterpret_cast<const uint4*>(p.exbits) + t);
                 const uint32_t exw[4] = {ex.x, ex.y, ex.z, ex.w};
+                uint32_t keep[4];
 #pragma unroll
                 for (int c = 0; c < 4; ++c) {
-                    float thr = ts.thr;
-                    uint32_t m = 0;
+                    const int vc = valid - 32 * c;
+                    keep[c] = (vc >= 32 ? 0xffffffffu : (vc <= 0 ? 0u : ((1u << vc) - 1u))) & ~exw[c];
+                }
+                if (t == 0) {
+                    // initial threshold: the largest 16-bit key prefix P with >= K selectable
+                    // keys >= P<<16 bounds the row's K-th largest score from below
 #pragma unroll
-                    for (int e = 0; e < 32; ++e)
-                        m |= (__uint_as_float(sr[c][e]) >= thr && 32 * c + e < valid) ? (1u << e) : 0u;
-                    m &= ~exw[c];
+                    for (int c = 0; c < 4; ++c)
+#pragma unroll
+                        for (int e = 0; e < 32; ++e)
+                            sr[c][e] = ((keep[c] >> e) & 1u) ? fkey(__uint_as_float(sr[c][e])) : 0u;
+                    uint32_t res = 0;
+#pragma unroll 1
+                    for (int bit = 31; bit >= 16; --bit) {
+                        const uint32_t cand = res | (1u << bit);
+                        int n = 0;
+#pragma unroll
+                        for (int c = 0; c < 4; ++c)
+#pragma unroll
+                            for (int e = 0; e < 32; ++e) n += sr[c][e] >= cand ? 1 : 0;
+                        if (n >= K) res = cand;
+                    }
+#pragma unroll
+                    for (int c = 0; c < 4; ++c)
+#pragma unroll
+                        for (int e = 0; e < 32; ++e) sr[c][e] = __float_as_uint(fkey_inv(sr[c][e]));
+                    if (res != 0) thr = topk_threshold(fkey_inv(res), eps);
+                }
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    const float tq = cnt < 0 ? INFINITY : thr;
+                    uint32_t m = 0;
+                    if (__any_sync(0xffffffffu, cmax[c] >= tq)) {
+                        uint32_t mm[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+                        for (int e = 0; e < 32; ++e) mm[e & 3] |= (__uint_as_float(sr[c][e]) >= tq) ? (1u << e) : 0u;
+                        m = ((mm[0] | mm[1]) | (mm[2] | mm[3])) & keep[c];
+                    }
                     while (m) {
                         const int e = __ffs(m) - 1;
                         m &= m - 1;
-                        const float a = select32(sr[c], e);
-                        if (p.debug & 4) continue;
-                        if (a >= ts.thr) topk_handle(ts, a, t * 128 + 32 * c + e);
+                        my_stage[cnt++] = make_float2(select32(sr[c], e), __int_as_float(t * 128 + 32 * c + e));
+                    }
+                    unsigned fl = __ballot_sync(0xffffffffu, cnt > FLUSH_AT);
+                    while (fl) {
+                        const int L = __ffs(fl) - 1;
+                        fl &= fl - 1;
+                        float lt = __shfl_sync(0xffffffffu, thr, L);
+                        const int n2 = flush_stage(sm.stage[32 * qd + L], __shfl_sync(0xffffffffu, cnt, L), K,
+                                                   __shfl_sync(0xffffffffu, eps, L), lt, lane);
+                        if (lane == L) {
+                            thr = lt;
+                            cnt = n2 > FLUSH_AT ? -1 : n2;  // near-tie flood: exact fallback
+                        }
                     }
                 }
             }
             __syncwarp();
-            if (p.debug & 16) ts.overflow = true;
+        }
+        // final flush: tighten every row's threshold with the candidates staged since
+        if (K > 0 && !(p.debug & 1)) {
+            unsigned fl = __ballot_sync(0xffffffffu, cnt > K);
+            while (fl) {
+                const int L = __ffs(fl) - 1;
+                fl &= fl - 1;
+                float lt = __shfl_sync(0xffffffffu, thr, L);
+                const int n2 = flush_stage(sm.stage[32 * qd + L], __shfl_sync(0xffffffffu, cnt, L), K,
+                                           __shfl_sync(0xffffffffu, eps, L), lt, lane);
+                if (lane == L) {
+                    thr = lt;
+                    cnt = n2;
+                }
+            }
         }
         // ------------------------------- epilogue -------------------------------
         // the commit after PV(T-1) covers every earlier MMA
@@ -393,17 +460,24 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     *reinterpret_cast<float4*>(dst + 32 * half + e) =
                         make_float4(__uint_as_float(o[half][e]) * inv, __uint_as_float(o[half][e + 1]) * inv,
                                     __uint_as_float(o[half][e + 2]) * inv, __uint_as_float(o[half][e + 3]) * inv);
-            if (p.lse) p.lse[(int64_t)h * p.W + grow] = m_used * p.scale + logf(l);
-            const int64_t r = (int64_t)h * p.W + grow;
+            if (p.lse) p.lse[(int64_t)h * p.Wq + grow] = m_used * p.scale + logf(l);
+            const int64_t r = (int64_t)h * p.Wq + grow;
             if (K > 0) {
                 float2* cd = p.cand + r * CAND;
-                int cnt = 0;
-                for (int i = 0; i < ts.n; ++i) cd[cnt++] = ts.lst[i];
-                for (int i = 0; i < ts.nside; ++i)
-                    if (ts.sd[i].x >= ts.thr) cd[cnt++] = ts.sd[i];
-                p.cand_n[r] = cnt;
+                int n = 0;
+                for (int i = 0; i < cnt; ++i) {
+                    const float2 c = my_stage[i];
+                    if (c.x >= thr) {
+                        if (n == CAND) {
+                            cnt = -1;  // more near-ties than the re-score takes: exact fallback
+                            break;
+                        }
+                        cd[n++] = c;
+                    }
+                }
+                p.cand_n[r] = cnt < 0 ? 0 : n;
             }
-            p.flag[r] = ts.overflow ? 1 : 0;
+            p.flag[r] = (K > 0 && (cnt < 0 || (p.debug & 16))) ? 1 : 0;
         }
     }
     tc_fence_before();
@@ -416,14 +490,16 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 
 // Exact re-score of the candidates and final ordering. One warp per row; lane
 // i owns candidates i and i+32. scaled_dot order (dot.hpp:11-23) without FMA.
-__global__ void rescore_kernel(const float* __restrict__ qc, const float* __restrict__ kc, int heads, int W,
-                               float scale, int k_eff, const float2* __restrict__ cand, const int* __restrict__ cand_n,
-                               const uint8_t* __restrict__ flag, int32_t* topk, float* guide) {
+// Query rows index [H][Wq], key windows [H][Wk] (Wq < Wk for a view shard).
+__global__ void rescore_kernel(const float* __restrict__ qc, int64_t q_hs, const float* __restrict__ kc, int heads,
+                               int Wq, int Wk, float scale, int k_eff, const float2* __restrict__ cand,
+                               const int* __restrict__ cand_n, const uint8_t* __restrict__ flag, int32_t* topk,
+                               float* guide) {
     const int64_t r = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
     const int lane = threadIdx.x & 31;
-    if (r >= (int64_t)heads * W || flag[r]) return;
-    const int h = (int)(r / W);
-    const float* q = qc + r * 64;
+    if (r >= (int64_t)heads * Wq || flag[r]) return;
+    const int h = (int)(r / Wq);
+    const float* q = qc + (int64_t)h * q_hs + (r - (int64_t)h * Wq) * 64;
     const int cnt = cand_n[r];
     float e[2];
     int idx[2];
@@ -434,7 +510,7 @@ __global__ void rescore_kernel(const float* __restrict__ qc, const float* __rest
         idx[s] = -1;
         if (i < cnt) {
             idx[s] = __float_as_int(cand[r * CAND + i].y);
-            const float* k = kc + ((int64_t)h * W + idx[s]) * 64;
+            const float* k = kc + ((int64_t)h * Wk + idx[s]) * 64;
             ExactDot4 d;
             d.zero();
 #pragma unroll 4
@@ -539,7 +615,7 @@ struct Ws {
     size_t used;
 };
 
-Ws carve_ws(void* base, int heads, int W, bool dry) {
+Ws carve_ws(void* base, int heads, int Wq, int Wk, bool dry) {
     Ws w{};
     size_t off = 0;
     auto take = [&](size_t bytes) -> char* {
@@ -548,21 +624,21 @@ Ws carve_ws(void* base, int heads, int W, bool dry) {
         off += bytes;
         return p;
     };
-    const size_t n = (size_t)heads * W;
-    w.qh = reinterpret_cast<__nv_bfloat16*>(take(n * 128));
-    w.ql = reinterpret_cast<__nv_bfloat16*>(take(n * 128));
-    w.kh = reinterpret_cast<__nv_bfloat16*>(take(n * 128));
-    w.kl = reinterpret_cast<__nv_bfloat16*>(take(n * 128));
-    w.vh = reinterpret_cast<__nv_bfloat16*>(take(n * 128));
-    w.vl = reinterpret_cast<__nv_bfloat16*>(take(n * 128));
-    w.qn = reinterpret_cast<float*>(take(n * 4));
-    w.kn = reinterpret_cast<float*>(take(n * 4));
+    const size_t nq = (size_t)heads * Wq, nk = (size_t)heads * Wk;
+    w.qh = reinterpret_cast<__nv_bfloat16*>(take(nq * 128));
+    w.ql = reinterpret_cast<__nv_bfloat16*>(take(nq * 128));
+    w.kh = reinterpret_cast<__nv_bfloat16*>(take(nk * 128));
+    w.kl = reinterpret_cast<__nv_bfloat16*>(take(nk * 128));
+    w.vh = reinterpret_cast<__nv_bfloat16*>(take(nk * 128));
+    w.vl = reinterpret_cast<__nv_bfloat16*>(take(nk * 128));
+    w.qn = reinterpret_cast<float*>(take(nq * 4));
+    w.kn = reinterpret_cast<float*>(take(nk * 4));
     w.kmax = reinterpret_cast<float*>(take((size_t)heads * 4));
-    w.exbits = reinterpret_cast<uint32_t*>(take((size_t)((W + 127) / 128) * 16));
-    w.cand = reinterpret_cast<float2*>(take(n * CAND * 8));
-    w.cand_n = reinterpret_cast<int*>(take(n * 4));
-    w.flag = reinterpret_cast<uint8_t*>(take(n));
-    w.blocks = reinterpret_cast<int*>(take((size_t)heads * ((W + 63) / 64) * 4));
+    w.exbits = reinterpret_cast<uint32_t*>(take((size_t)((Wk + 127) / 128) * 16));
+    w.cand = reinterpret_cast<float2*>(take(nq * CAND * 8));
+    w.cand_n = reinterpret_cast<int*>(take(nq * 4));
+    w.flag = reinterpret_cast<uint8_t*>(take(nq));
+    w.blocks = reinterpret_cast<int*>(take((size_t)heads * ((Wq + 63) / 64) * 4));
     w.nblocks = reinterpret_cast<int*>(take(4));
     w.used = off + 256;
     return w;
@@ -576,14 +652,19 @@ bool contiguous_f32(const gsa_tensor& t) {
 }  // namespace
 
 size_t tc_compress_workspace_bytes(int heads, int windows, int dim, int k_eff) {
+    return tc_compress_workspace_bytes_qk(heads, windows, windows, dim, k_eff);
+}
+
+size_t tc_compress_workspace_bytes_qk(int heads, int wq, int wk, int dim, int k_eff) {
     if (dim != 64 || k_eff > KCAP) return 0;
-    return carve_ws(nullptr, heads, windows, true).used;
+    return carve_ws(nullptr, heads, wq, wk, true).used;
 }
 
 bool tc_compress_split_buffers(void* ws, size_t ws_bytes, int heads, int windows, int dim, int k_eff,
                                CompressSplits* out) {
-    if (dim != 64 || k_eff > KCAP || !ws || ws_bytes < carve_ws(nullptr, heads, windows, true).used) return false;
-    Ws w = carve_ws(ws, heads, windows, false);
+    if (dim != 64 || k_eff > KCAP || !ws || ws_bytes < carve_ws(nullptr, heads, windows, windows, true).used)
+        return false;
+    Ws w = carve_ws(ws, heads, windows, windows, false);
     *out = CompressSplits{w.qh, w.ql, w.kh, w.kl, w.vh, w.vl, w.qn, w.kn};
     return true;
 }
@@ -599,14 +680,14 @@ cudaError_t tc_compress_topk_splits(const CompressSplits* pre, const gsa_tensor&
                                     const gsa_tensor& vc, int k_eff, float scale, const uint8_t* excluded,
                                     float* out, int64_t out_hs, int64_t out_rs, float* lse, int32_t* topk,
                                     float* guide, void* ws, size_t ws_bytes, cudaStream_t st) {
-    const int H = qc.heads, W = qc.rows;
+    const int H = qc.heads, Wq = qc.rows, Wk = kc.rows;
     AttnArgs ex{};  // exact CUDA-core kernel (phase-1 path and fallback)
     ex.q = TensorRef{qc.data, qc.dtype, qc.head_stride, qc.row_stride};
     ex.k = TensorRef{kc.data, kc.dtype, kc.head_stride, kc.row_stride};
     ex.v = TensorRef{vc.data, vc.dtype, vc.head_stride, vc.row_stride};
     ex.heads = H;
-    ex.mq = W;
-    ex.mk = kc.rows;
+    ex.mq = Wq;
+    ex.mk = Wk;
     ex.dim = qc.dim;
     ex.scale = scale;
     ex.out = out;
@@ -619,42 +700,43 @@ cudaError_t tc_compress_topk_splits(const CompressSplits* pre, const gsa_tensor&
     ex.excluded = excluded;
     const bool tc_ok = qc.dim == 64 && k_eff <= KCAP && contiguous_f32(qc) && contiguous_f32(kc) &&
                        contiguous_f32(vc) && tmap_encode_fn() != nullptr && ws &&
-                       ws_bytes >= carve_ws(nullptr, H, W, true).used && W > 0;
+                       ws_bytes >= carve_ws(nullptr, H, Wq, Wk, true).used && Wq > 0 && Wk > 0;
     if (!tc_ok) return launch_attn_f32(ex, st);
 
-    Ws w = carve_ws(ws, H, W, false);
+    Ws w = carve_ws(ws, H, Wq, Wk, false);
     const __nv_bfloat16 *qh = w.qh, *ql = w.ql, *kh = w.kh, *kl = w.kl, *vh = w.vh, *vl = w.vl;
     const float *qn = w.qn, *kn = w.kn;
     if (pre) {
         qh = pre->qh; ql = pre->ql; kh = pre->kh; kl = pre->kl; vh = pre->vh; vl = pre->vl;
         qn = pre->qnorm; kn = pre->knorm;
     } else {
-        const unsigned blocks = (unsigned)(((int64_t)H * W + 31) / 32);
-        split_kernel<<<blocks, 256, 0, st>>>(static_cast<const float*>(qc.data), qc.head_stride, qc.row_stride, H, W,
-                                              w.qh, w.ql, w.qn);
-        split_kernel<<<blocks, 256, 0, st>>>(static_cast<const float*>(kc.data), kc.head_stride, kc.row_stride, H, W,
-                                              w.kh, w.kl, w.kn);
-        split_kernel<<<blocks, 256, 0, st>>>(static_cast<const float*>(vc.data), vc.head_stride, vc.row_stride, H, W,
-                                              w.vh, w.vl, nullptr);
+        const unsigned qb = (unsigned)(((int64_t)H * Wq + 31) / 32), kb = (unsigned)(((int64_t)H * Wk + 31) / 32);
+        split_kernel<<<qb, 256, 0, st>>>(static_cast<const float*>(qc.data), qc.head_stride, qc.row_stride, H, Wq,
+                                          w.qh, w.ql, w.qn);
+        split_kernel<<<kb, 256, 0, st>>>(static_cast<const float*>(kc.data), kc.head_stride, kc.row_stride, H, Wk,
+                                          w.kh, w.kl, w.kn);
+        split_kernel<<<kb, 256, 0, st>>>(static_cast<const float*>(vc.data), vc.head_stride, vc.row_stride, H, Wk,
+                                          w.vh, w.vl, nullptr);
         note_launch(3);
     }
-    rowmax_kernel<<<H, 256, 0, st>>>(kn, W, w.kmax);
+    rowmax_kernel<<<H, 256, 0, st>>>(kn, Wk, w.kmax);
     note_launch();
-    const int tiles = (W + 127) / 128;
+    const int tiles = (Wk + 127) / 128;
     if (excluded) {
-        exbits_kernel<<<(tiles * 4 + 127) / 128, 128, 0, st>>>(excluded, W, tiles * 4, w.exbits);
+        exbits_kernel<<<(tiles * 4 + 127) / 128, 128, 0, st>>>(excluded, Wk, tiles * 4, w.exbits);
         note_launch();
     }
     CUtensorMap tqh, tql, tkh, tkl, tvh, tvl;
-    const int64_t hs = (int64_t)W * 64;
-    if (!make_rows_tmap(&tqh, qh, H, W, hs, 64) || !make_rows_tmap(&tql, ql, H, W, hs, 64) ||
-        !make_rows_tmap(&tkh, kh, H, W, hs, 64) || !make_rows_tmap(&tkl, kl, H, W, hs, 64) ||
-        !make_rows_tmap(&tvh, vh, H, W, hs, 64) || !make_rows_tmap(&tvl, vl, H, W, hs, 64))
+    const int64_t qhs = (int64_t)Wq * 64, khs = (int64_t)Wk * 64;
+    if (!make_rows_tmap(&tqh, qh, H, Wq, qhs, 64) || !make_rows_tmap(&tql, ql, H, Wq, qhs, 64) ||
+        !make_rows_tmap(&tkh, kh, H, Wk, khs, 64) || !make_rows_tmap(&tkl, kl, H, Wk, khs, 64) ||
+        !make_rows_tmap(&tvh, vh, H, Wk, khs, 64) || !make_rows_tmap(&tvl, vl, H, Wk, khs, 64))
         return launch_attn_f32(ex, st);
     CompParams p{};
     if (const char* dbg = getenv("GSA_DEBUG_COMPRESS")) p.debug = atoi(dbg);
     p.heads = H;
-    p.W = W;
+    p.Wq = Wq;
+    p.Wk = Wk;
     p.k_eff = k_eff;
     p.scale = scale;
     p.c2 = scale * 1.4426950408889634f;
@@ -672,18 +754,18 @@ cudaError_t tc_compress_topk_splits(const CompressSplits* pre, const gsa_tensor&
     const size_t smem = sizeof(CompSmem) + 1024;
     cudaError_t e = cudaFuncSetAttribute(compress_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    compress_tc_kernel<<<dim3(tiles, H), NTHREADS, smem, st>>>(tqh, tql, tkh, tkl, tvh, tvl, p);
+    compress_tc_kernel<<<dim3((Wq + 127) / 128, H), NTHREADS, smem, st>>>(tqh, tql, tkh, tkl, tvh, tvl, p);
     note_launch();
     if (k_eff > 0) {
-        const int64_t rows = (int64_t)H * W;
-        rescore_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(static_cast<const float*>(qc.data),
-                                                                   static_cast<const float*>(kc.data), H, W, scale,
+        const int64_t rows = (int64_t)H * Wq;
+        rescore_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(static_cast<const float*>(qc.data), qc.head_stride,
+                                                                   static_cast<const float*>(kc.data), H, Wq, Wk, scale,
                                                                    k_eff, w.cand, w.cand_n, w.flag, topk, guide);
         note_launch();
         // rows whose near-tie side list overflowed: exact recompute of their 64-row blocks
         cudaMemsetAsync(w.nblocks, 0, sizeof(int), st);
-        const int nb = H * ((W + 63) / 64);
-        flag_blocks_kernel<<<(nb + 127) / 128, 128, 0, st>>>(w.flag, H, W, w.blocks, w.nblocks);
+        const int nb = H * ((Wq + 63) / 64);
+        flag_blocks_kernel<<<(nb + 127) / 128, 128, 0, st>>>(w.flag, H, Wq, w.blocks, w.nblocks);
         note_launch();
         ex.block_list = w.blocks;
         ex.block_count = w.nblocks;

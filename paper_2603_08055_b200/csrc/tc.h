@@ -18,6 +18,8 @@ cudaError_t tc_dense_attention(const gsa_tensor& q, const gsa_tensor& k, const g
 // approximate scores + exact re-scoring of the boundary candidates when
 // supported, else the exact CUDA-core kernel. Indices are bit-exact either way.
 size_t tc_compress_workspace_bytes(int heads, int windows, int dim, int k_eff);
+// query rows wq (a shard's windows) against wk key windows
+size_t tc_compress_workspace_bytes_qk(int heads, int wq, int wk, int dim, int k_eff);
 // pre-split operands (bf16 hi/lo of contiguous [H][W][64] Qc/Kc/Vc + row norms),
 // e.g. written by the pooling kernel; carved from the compress workspace
 struct CompressSplits {
