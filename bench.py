@@ -169,6 +169,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-dense", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--shard", action="store_true", help="use the view-sharded layer even on 1 GPU")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference_arm(args)
@@ -199,21 +200,31 @@ def main():
     out = torch.empty(HEADS, G["M"], DIM, device=dev)
     ws = gsa.Workspace()
 
-    if world > 1:
+    layer = None
+    sharded = world > 1 or args.shard
+    if sharded:
         from paper_2603_08055_b200 import dist as gdist
-        step_fn, shard_tokens = gdist.make_sharded_step(q, k, v, wg, lt, params, rank, world)
+        spec = gdist.shard_spec(L, rank, world)
+        q_own = gdist.own_rows_of(q, L, spec).contiguous()
+        out_own = torch.empty(HEADS, spec.own_rows(L), DIM, device=dev)
+        layer = gdist.ShardedLayer(L, params, HEADS, DIM, rank, world, device=dev)
+
+        def step_fn():
+            layer.forward(q_own, k, v, wg, out_own)
     else:
         def step_fn():
             gsa.gsa_forward(q, k, v, wg, L, params, out=out, workspace=ws)
-        shard_tokens = G["M"]
 
-    # stage events (rank-local, recorded by the library on the launching stream)
+    # stage events on the launching stream: the library records them inside
+    # gsa_forward (special | pool | compress | select); the sharded layer
+    # records pool | compress (incl. the Kc/Vc gather wait) | attend
     import ctypes
-    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(args.steps)]
+    nev = 4 if sharded else 5
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(nev)] for _ in range(args.steps)]
     for row in ev:
-        for e in row:
-            e.record()  # materialise the cudaEvent_t handles
-    handles = [(ctypes.c_void_p * 5)(*[e.cuda_event for e in row]) for row in ev]
+        for e_ in row:
+            e_.record()  # materialise the cudaEvent_t handles
+    handles = [(ctypes.c_void_p * 5)(*[e_.cuda_event for e_ in row]) for row in ev] if not sharded else None
     for _ in range(args.warmup):
         step_fn()
     torch.cuda.synchronize()
@@ -227,12 +238,18 @@ def main():
     with ClockSampler(local) as clocks:
         start.record()
         for i in range(args.steps):
-            lib.gsa_set_stage_events(handles[i], 5)
+            if not sharded:
+                lib.gsa_set_stage_events(handles[i], 5)
+            else:
+                layer.events = ev[i]
             step_fn()
-        lib.gsa_set_stage_events(None, 0)
+        if not sharded:
+            lib.gsa_set_stage_events(None, 0)
+        else:
+            layer.events = None
         stop.record()
         torch.cuda.synchronize()
-    names = ("special", "pool", "compress", "select")
+    names = ("pool", "compress", "attend") if sharded else ("special", "pool", "compress", "select")
     stage_ms = {n: sum(ev[i][j].elapsed_time(ev[i][j + 1]) for i in range(args.steps)) / args.steps
                 for j, n in enumerate(names)}
     n1 = ctypes.c_uint64()
@@ -247,13 +264,16 @@ def main():
 
     hbm, tc_peak, tc_sust, peak_kind = load_peaks()
     W, Mi, Ms, M = G["W"], G["Mi"], G["Ms"], G["M"]
-    F = 0
-    flops = {"special": 4.0 * HEADS * Ms * M * DIM, "compress": 4.0 * HEADS * W * W * DIM,
-             "select": 4.0 * HEADS * Mi * (TOPK + F) * S * S * DIM}
-    bytes_ = {"pool": 3 * HEADS * Mi * DIM * 2 + 3 * HEADS * W * DIM * 4,
-              "select": HEADS * W * (TOPK + F) * S * S * DIM * 2 * 2 + HEADS * Mi * DIM * (2 + 4) + HEADS * W * DIM * 4}
-    dom = max(stage_ms, key=lambda n: stage_ms[n])
-    if dom in ("pool",) or (dom == "select"):
+    Wg, Mig, Msg = W // world, Mi // world, Ms // world  # this rank's share (equal blocks)
+    # algorithmic work per rank and step: useful MMA flops
+    # (4*d per score: QK^T + PV) and compulsory HBM bytes
+    flops = {"special": 4.0 * HEADS * Msg * M * DIM, "compress": 4.0 * HEADS * Wg * W * DIM,
+             "select": 4.0 * HEADS * Mig * TOPK * S * S * DIM}
+    bytes_ = {"pool": 3 * HEADS * Mig * DIM * 2 + 3 * HEADS * Wg * DIM * 4 + 3 * HEADS * Wg * DIM * 4,
+              "select": HEADS * Wg * TOPK * S * S * DIM * 2 * 2 + HEADS * Mig * DIM * (2 + 4) + HEADS * Wg * DIM * 4}
+    timed = {k_: v_ for k_, v_ in stage_ms.items() if k_ in flops or k_ in bytes_}
+    dom = max(timed, key=lambda n: timed[n])
+    if dom in bytes_:
         A = bytes_[dom] / (stage_ms[dom] / 1e3) / 1e9
         roof = {"kernel": dom, "bound": "hbm", "achieved": A, "peak": hbm, "unit": "GB/s", "frac": A / hbm,
                 "traffic": None, "peak_kind": peak_kind}
@@ -266,48 +286,80 @@ def main():
         tr = json.load(open(prof)).get(dom)
         if tr:
             roof["traffic"] = tr
-    sel_tc = flops["select"] / (stage_ms["select"] / 1e3) / 1e12
+    per_stage = {}
+    for n_, t_ in stage_ms.items():
+        if n_ in flops:
+            per_stage[n_] = {"ms": round(t_, 3), "tflops": round(flops[n_] / (t_ / 1e3) / 1e12, 1),
+                             "tc_frac": round(flops[n_] / (t_ / 1e3) / 1e12 / tc_peak, 4)}
+        if n_ in bytes_:
+            per_stage.setdefault(n_, {"ms": round(t_, 3)})["gbs"] = round(bytes_[n_] / (t_ / 1e3) / 1e9, 1)
+            per_stage[n_]["hbm_frac"] = round(bytes_[n_] / (t_ / 1e3) / 1e9 / hbm, 4)
 
     line = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak" if world == 1 else "strong",
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (torch N(0,1) bf16 Q/K/V, W_g=N(0,1)/8 f32), resident in HBM",
             "config": {"workload": f"1 GSA layer, {args.views} views x (5 specials + 36x36 patches) = {M} tokens, "
                                    f"16 heads x 64, s=4, top-32, plain", "views": args.views, "tokens": M,
-                       "windows": W, "parallelism": f"views sharded over {world}" if world > 1 else "1 GPU",
+                       "windows": W, "parallelism": f"query views sharded over {world} (NCCL all-gather of Kc/Vc "
+                                                    f"and K/V)" if world > 1 else "1 GPU",
                        "l2": "inputs larger than L2 (no flush)"},
             "stage_ms": {k_: round(v_, 3) for k_, v_ in stage_ms.items()},
+            "stage_roofline": per_stage,
             "roofline": roof,
-            "select_tc_util": {"achieved_tflops": sel_tc, "frac_of_peak": sel_tc / tc_peak},
             "gpu_launches": int(n1.value - n0.value),
             "clocks": clocks.summary()}
 
-    # end to end through the public API from pinned host buffers
-    if not args.no_e2e and world == 1:
-        hq, hk, hv = (x.cpu().pin_memory() for x in (q, k, v))
-        hout = torch.empty(out.shape, dtype=torch.float32).pin_memory()
-        dq, dk, dv = (torch.empty_like(x) for x in (q, k, v))
+    # end to end through the public API from pinned host buffers: per step the
+    # rank's Q/K/V rows go host -> device and its f32 output rows come back
+    if not args.no_e2e:
+        if not sharded:
+            hq, hk, hv = (x.cpu().pin_memory() for x in (q, k, v))
+            hout = torch.empty(out.shape, dtype=torch.float32).pin_memory()
+            dq, dk, dv = (torch.empty_like(x) for x in (q, k, v))
 
-        def e2e_step():
-            dq.copy_(hq, non_blocking=True)
-            dk.copy_(hk, non_blocking=True)
-            dv.copy_(hv, non_blocking=True)
-            gsa.gsa_forward(dq, dk, dv, wg, L, params, out=out, workspace=ws)
-            hout.copy_(out, non_blocking=True)
+            def e2e_step():
+                dq.copy_(hq, non_blocking=True)
+                dk.copy_(hk, non_blocking=True)
+                dv.copy_(hv, non_blocking=True)
+                gsa.gsa_forward(dq, dk, dv, wg, L, params, out=out, workspace=ws)
+                hout.copy_(out, non_blocking=True)
+            h2d, d2h = 3 * q.numel() * 2, out.numel() * 4
+        else:
+            hq = q_own.cpu().pin_memory()
+            hk, hv = (gdist.own_rows_of(x, L, spec).cpu().pin_memory() for x in (k, v))
+            hout = torch.empty(out_own.shape, dtype=torch.float32).pin_memory()
+            dq = torch.empty_like(q_own)
+            ms_g = spec.special_end - spec.special_begin
+            i0, i1 = spec.image_rows(L)
+
+            def e2e_step():
+                dq.copy_(hq, non_blocking=True)
+                for dst, src in ((k, hk), (v, hv)):
+                    dst[:, spec.special_begin:spec.special_end].copy_(src[:, :ms_g], non_blocking=True)
+                    dst[:, Ms + i0:Ms + i1].copy_(src[:, ms_g:], non_blocking=True)
+                layer.forward(dq, k, v, wg, out_own)
+                hout.copy_(out_own, non_blocking=True)
+            h2d, d2h = (hq.numel() + hk.numel() + hv.numel()) * 2, out_own.numel() * 4
 
         for _ in range(2):
             e2e_step()
         torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
         s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s0.record()
         for _ in range(args.steps):
             e2e_step()
         s1.record()
         torch.cuda.synchronize()
-        e_ms = s0.elapsed_time(s1) / args.steps
+        te = torch.tensor([s0.elapsed_time(s1) / args.steps], device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e_ms = float(te.item())
         line["e2e"] = {"value": M / (e_ms / 1e3), "unit": "tokens/s", "ms_per_step": e_ms,
-                       "h2d_bytes_per_step": 3 * q.numel() * 2, "d2h_bytes_per_step": out.numel() * 4}
-        del hq, hk, hv, hout, dq, dk, dv
+                       "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h}
+        del hq, hk, hv, hout, dq
 
     # the paper's sparse-vs-dense comparison on the same GPU: fastest library dense
     # attention over all M tokens (timed on a query subset; cost is linear in queries)

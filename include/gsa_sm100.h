@@ -178,6 +178,42 @@ int gsa_forward_with_plan(const gsa_tensor* q, const gsa_tensor* k, const gsa_te
                           const int32_t* window_ids, const gsa_tensor* out, void* workspace,
                           size_t workspace_bytes, gsa_stream_t stream);
 
+/* ---------------------------------------------------------------------------
+ * View-sharded layer (multi-GPU; no reference counterpart — the reference is a
+ * single-process CPU library). A rank owns frames [frame_begin, frame_end) and
+ * special rows [special_begin, special_end) of the global layout. Per layer:
+ *   1. gsa_shard_pool: own Q windows -> qc_own; own K/V windows written at their
+ *      global rows of kc_all / vc_all ([H][W][d] f32), ready for an in-place
+ *      all-gather. k_all / v_all hold the rank's own rows at their global
+ *      positions (the K/V all-gather may run concurrently: pooling only reads
+ *      own rows).
+ *   2. (all-gather kc_all, vc_all) gsa_shard_compress: own query windows against
+ *      all W windows; topk_own [H][W_g][k_eff] holds GLOBAL window ids, bit-exact
+ *      with the unsharded layer.
+ *   3. (all-gather k_all, v_all) gsa_shard_attend: own special rows over all M
+ *      keys, own windows' selection + gate + merge; out_own [H][Ms_g + Mi_g][d]
+ *      f32 = the rank's rows of the unsharded output (specials first).
+ * q_own: [H][Ms_g + Mi_g][d] (own specials, then own image rows). */
+typedef struct {
+    int32_t frame_begin, frame_end, special_begin, special_end;
+} gsa_shard;
+
+size_t gsa_shard_workspace_bytes(const gsa_layout* layout, const gsa_params* params, const gsa_shard* shard,
+                                 int heads, int dim);
+int gsa_shard_pool(const gsa_tensor* q_own, const gsa_tensor* k_all, const gsa_tensor* v_all,
+                   const gsa_layout* layout, const gsa_params* params, const gsa_shard* shard,
+                   const gsa_tensor* qc_own, const gsa_tensor* kc_all, const gsa_tensor* vc_all,
+                   gsa_stream_t stream);
+int gsa_shard_compress(const gsa_tensor* qc_own, const gsa_tensor* kc_all, const gsa_tensor* vc_all,
+                       const gsa_layout* layout, const gsa_params* params, const gsa_shard* shard,
+                       const gsa_tensor* o_comp_own, float* lse_own, int32_t* topk_own, int* k_eff_out,
+                       void* workspace, size_t workspace_bytes, gsa_stream_t stream);
+int gsa_shard_attend(const gsa_tensor* q_own, const gsa_tensor* k_all, const gsa_tensor* v_all,
+                     const gsa_tensor* w_g, const gsa_layout* layout, const gsa_params* params,
+                     const gsa_shard* shard, const gsa_tensor* o_comp_own, const int32_t* topk_own,
+                     const gsa_tensor* out_own, void* workspace, size_t workspace_bytes,
+                     gsa_stream_t stream);
+
 /* KernelStats (types.hpp:78-86) in closed form for a gsa_forward call:
  * scores_computed = H*(Ms*M + W*W); keys_attended = sum over rows of
  * |row| * s^2 * s^2 (rows have width F + k_eff). */

@@ -31,6 +31,11 @@ class GsaParamsC(C.Structure):
                 ("ref_stride", C.c_int32), ("block_m", C.c_int32), ("block_n", C.c_int32)]
 
 
+class GsaShard(C.Structure):
+    _fields_ = [("frame_begin", C.c_int32), ("frame_end", C.c_int32), ("special_begin", C.c_int32),
+                ("special_end", C.c_int32)]
+
+
 class GsaContextC(C.Structure):
     _fields_ = [(n, C.c_void_p) for n in ("qc", "kc", "vc", "o_comp", "lse_comp", "topk", "o_sel", "lse_sel",
                                           "gate", "lse_spec")]
@@ -76,6 +81,12 @@ def load() -> C.CDLL:
     L.gsa_forward.argtypes = [T, T, T, T, Lp, P, T, C.POINTER(GsaContextC), C.POINTER(C.c_int), vp, C.c_size_t, vp]
     L.gsa_forward_with_plan.argtypes = [T, T, T, T, Lp, P, vp, vp, T, vp, C.c_size_t, vp]
     L.gsa_forward_stats.argtypes = [Lp, P, i32, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]
+    S = C.POINTER(GsaShard)
+    L.gsa_shard_workspace_bytes.restype = C.c_size_t
+    L.gsa_shard_workspace_bytes.argtypes = [Lp, P, S, i32, i32]
+    L.gsa_shard_pool.argtypes = [T, T, T, Lp, P, S, T, T, T, vp]
+    L.gsa_shard_compress.argtypes = [T, T, T, Lp, P, S, T, vp, vp, C.POINTER(C.c_int), vp, C.c_size_t, vp]
+    L.gsa_shard_attend.argtypes = [T, T, T, T, Lp, P, S, T, vp, T, vp, C.c_size_t, vp]
     L.gsa_set_stage_events.argtypes = [C.POINTER(C.c_void_p), i32]
     L.gsa_launch_count.argtypes = [C.POINTER(C.c_uint64)]
     _lib = L
@@ -88,5 +99,6 @@ EXPORTED_SYMBOLS = [
     "gsa_compressed_attention_topk_workspace_bytes", "gsa_compressed_attention_topk", "gsa_forced_windows",
     "gsa_build_selection_plan", "gsa_build_selection_plan_workspace_bytes", "gsa_block_sparse_attention",
     "gsa_gate", "gsa_forward_workspace_bytes", "gsa_forward", "gsa_forward_with_plan", "gsa_forward_stats",
-    "gsa_set_stage_events", "gsa_launch_count",
+    "gsa_set_stage_events", "gsa_launch_count", "gsa_shard_workspace_bytes", "gsa_shard_pool", "gsa_shard_compress",
+    "gsa_shard_attend",
 ]

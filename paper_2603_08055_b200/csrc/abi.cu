@@ -415,6 +415,7 @@ int gsa_block_sparse_attention(const gsa_tensor* q, const gsa_tensor* k, const g
     a.heads = q->heads;
     a.dim = q->dim;
     a.L = L;
+    a.Lkv = L;
     a.rows = RowSource{offsets, ids, nullptr, 0, nullptr, 0, 0};
     a.scale = scale;
     a.out = static_cast<float*>(out->data);
@@ -596,6 +597,7 @@ int gsa_forward(const gsa_tensor* q, const gsa_tensor* k, const gsa_tensor* v, c
     a.heads = H;
     a.dim = d;
     a.L = lp.L;
+    a.Lkv = lp.L;
     a.rows = RowSource{nullptr, nullptr, b.forced, params->variant == 1 ? lp.n_forced : 0, b.topk, lp.k_eff, lp.k_eff};
     a.scale = lp.scale;
     a.out = outp + (size_t)lp.Ms * out->row_stride;
@@ -646,6 +648,7 @@ int gsa_forward_with_plan(const gsa_tensor* q, const gsa_tensor* k, const gsa_te
     a.heads = H;
     a.dim = d;
     a.L = lp.L;
+    a.Lkv = lp.L;
     a.rows = RowSource{offsets, ids, nullptr, 0, nullptr, 0, 0};
     a.scale = lp.scale;
     a.out = static_cast<float*>(out->data) + (size_t)lp.Ms * out->row_stride;
@@ -654,6 +657,220 @@ int gsa_forward_with_plan(const gsa_tensor* q, const gsa_tensor* k, const gsa_te
     a.w_g = static_cast<const float*>(w_g->data);
     a.o_comp = b.o_comp;
     GSA_CUDA(launch_select_f32(a, st));
+    return GSA_OK;
+}
+
+// ------------------------------------------------------- view-sharded layer
+// One rank of a layer partitioned by query views: the
+// rank owns frames [frame_begin, frame_end) and special rows [special_begin,
+// special_end). K/V (all M rows) and Kc/Vc (all W windows) are completed by
+// all-gathers between the three calls; window ids stay global throughout.
+
+namespace {
+
+struct ShardPlan {
+    LayerPlan g;         // the global layer
+    DevLayout Lq;        // the shard's own frames (no specials)
+    int Ms_g, Mi_g, W_g, w_begin;
+};
+
+int shard_checks(const gsa_layout* layout, const gsa_params* p, const gsa_shard* sh, int heads, int dim,
+                 ShardPlan* sp) {
+    GSA_TRY(check_layout(layout));
+    GSA_TRY(gsa_validate_params(p, layout));
+    if (!sh) return fail(GSA_ERR_GENERIC, "null shard");
+    if (sh->frame_begin < 0 || sh->frame_end > layout->num_frames || sh->frame_begin > sh->frame_end ||
+        sh->special_begin < 0 || sh->special_end > layout->num_special || sh->special_begin > sh->special_end)
+        return fail(GSA_ERR_INDEX_OUT_OF_RANGE, "shard ranges outside the layout");
+    GSA_TRY(generic_supported(dim, layout->window_s));
+    const DevLayout L = make_dev_layout(*layout);
+    LayerPlan& lp = sp->g;
+    lp.L = L;
+    lp.heads = heads;
+    lp.dim = dim;
+    lp.Ms = layout->num_special;
+    lp.Mi = L.image_tokens;
+    lp.M = lp.Ms + lp.Mi;
+    lp.W = L.windows;
+    const int sel = selectable_windows(L, p->variant, p->ref_stride, &lp.n_forced);
+    lp.k_eff = p->top_k < sel ? p->top_k : sel;
+    lp.scale = resolved_scale(p->scale, dim);
+    if (lp.k_eff > 128) return fail(GSA_ERR_UNSUPPORTED, "k_eff=%d > 128 not implemented on sm_100a yet", lp.k_eff);
+    gsa_layout lq{0, sh->frame_end - sh->frame_begin, layout->grid_h, layout->grid_w, layout->window_s};
+    if (lq.num_frames == 0) lq.num_frames = 1;  // placeholder geometry; an empty shard does no work
+    sp->Lq = make_dev_layout(lq);
+    sp->Ms_g = sh->special_end - sh->special_begin;
+    sp->Mi_g = (sh->frame_end - sh->frame_begin) * L.tokens_per_frame;
+    sp->W_g = (sh->frame_end - sh->frame_begin) * L.wins_per_frame;
+    sp->w_begin = sh->frame_begin * L.wins_per_frame;
+    return GSA_OK;
+}
+
+int check_shape(const gsa_tensor* t, const char* name, int heads, int rows, int dim, bool bf16_ok) {
+    GSA_TRY(check_tensor(t, name, bf16_ok));
+    if (t->heads != heads || t->rows != rows || t->dim != dim)
+        return fail(GSA_ERR_SHAPE_MISMATCH, "%s: expected [%d x %d x %d], got [%d x %d x %d]", name, heads, rows, dim,
+                    t->heads, t->rows, t->dim);
+    return GSA_OK;
+}
+
+int contiguous_f32_windows(const gsa_tensor* t, const char* name) {
+    if (t->dtype != GSA_DTYPE_F32 || t->row_stride != t->dim || t->head_stride != (int64_t)t->rows * t->dim)
+        return fail(GSA_ERR_UNSUPPORTED, "%s must be contiguous f32 [H][rows][d]", name);
+    return GSA_OK;
+}
+
+struct ShardBufs {
+    int32_t *forced;
+    uint8_t* mask;
+    void* compress_ws;
+    size_t compress_ws_bytes;
+    uint8_t* wg_prep;
+    void* dense_ws;
+    size_t dense_ws_bytes;
+    float* lse_spec;
+};
+
+size_t shard_carve(const ShardPlan& sp, char* base, bool dry, ShardBufs* b) {
+    Carver c{base, 0, 0, dry};
+    const LayerPlan& g = sp.g;
+    b->forced = c.take<int32_t>(g.W);
+    b->mask = c.take<uint8_t>(g.W);
+    b->compress_ws_bytes = tc_compress_workspace_bytes_qk(g.heads, sp.W_g, g.W, g.dim, g.k_eff);
+    b->compress_ws = c.take<char>(b->compress_ws_bytes);
+    b->wg_prep = c.take<uint8_t>(tc_select_workspace_bytes(g.heads));
+    b->dense_ws_bytes = tc_dense_workspace_bytes(g.heads, sp.Ms_g, g.M);
+    b->dense_ws = c.take<char>(b->dense_ws_bytes);
+    b->lse_spec = c.take<float>((size_t)g.heads * sp.Ms_g);
+    return c.used + 256;
+}
+
+}  // namespace
+
+size_t gsa_shard_workspace_bytes(const gsa_layout* layout, const gsa_params* params, const gsa_shard* shard,
+                                 int heads, int dim) {
+    ShardPlan sp;
+    if (shard_checks(layout, params, shard, heads, dim, &sp) != GSA_OK) return 0;
+    ShardBufs b;
+    return shard_carve(sp, nullptr, true, &b);
+}
+
+int gsa_shard_pool(const gsa_tensor* q_own, const gsa_tensor* k_all, const gsa_tensor* v_all,
+                   const gsa_layout* layout, const gsa_params* params, const gsa_shard* shard,
+                   const gsa_tensor* qc_own, const gsa_tensor* kc_all, const gsa_tensor* vc_all,
+                   gsa_stream_t stream) {
+    GSA_TRY(check_tensor(q_own, "q_own"));
+    ShardPlan sp;
+    GSA_TRY(shard_checks(layout, params, shard, q_own->heads, q_own->dim, &sp));
+    const LayerPlan& g = sp.g;
+    const int H = g.heads, d = g.dim;
+    GSA_TRY(check_shape(q_own, "q_own", H, sp.Ms_g + sp.Mi_g, d, true));
+    GSA_TRY(check_shape(k_all, "k_all", H, g.M, d, true));
+    GSA_TRY(check_shape(v_all, "v_all", H, g.M, d, true));
+    if (k_all->dtype != q_own->dtype || v_all->dtype != q_own->dtype)
+        return fail(GSA_ERR_UNSUPPORTED, "shard_pool: q/k/v dtypes differ");
+    GSA_TRY(check_shape(qc_own, "qc_own", H, sp.W_g, d, false));
+    GSA_TRY(check_shape(kc_all, "kc_all", H, g.W, d, false));
+    GSA_TRY(check_shape(vc_all, "vc_all", H, g.W, d, false));
+    GSA_TRY(contiguous_f32_windows(qc_own, "qc_own"));
+    GSA_TRY(contiguous_f32_windows(kc_all, "kc_all"));
+    GSA_TRY(contiguous_f32_windows(vc_all, "vc_all"));
+    if (sp.W_g == 0) return GSA_OK;
+    const int own_img = g.Ms + shard->frame_begin * g.L.tokens_per_frame;  // first own image row of k_all
+    const int64_t wofs = (int64_t)sp.w_begin * d;
+    PoolJob jobs[3] = {
+        {ref_of(*q_own, sp.Ms_g), static_cast<float*>(qc_own->data), nullptr, nullptr, nullptr, 0},
+        {ref_of(*k_all, own_img), static_cast<float*>(kc_all->data) + wofs, nullptr, nullptr, nullptr, (int64_t)g.W * d},
+        {ref_of(*v_all, own_img), static_cast<float*>(vc_all->data) + wofs, nullptr, nullptr, nullptr, (int64_t)g.W * d},
+    };
+    GSA_CUDA(launch_pool(jobs, 3, H, d, sp.Lq, 1.0f / (float)(g.L.s * g.L.s), (cudaStream_t)stream));
+    return GSA_OK;
+}
+
+int gsa_shard_compress(const gsa_tensor* qc_own, const gsa_tensor* kc_all, const gsa_tensor* vc_all,
+                       const gsa_layout* layout, const gsa_params* params, const gsa_shard* shard,
+                       const gsa_tensor* o_comp_own, float* lse_own, int32_t* topk_own, int* k_eff_out,
+                       void* workspace, size_t ws_bytes, gsa_stream_t stream) {
+    GSA_TRY(check_tensor(qc_own, "qc_own", false));
+    ShardPlan sp;
+    GSA_TRY(shard_checks(layout, params, shard, qc_own->heads, qc_own->dim, &sp));
+    const LayerPlan& g = sp.g;
+    const int H = g.heads, d = g.dim;
+    if (k_eff_out) *k_eff_out = g.k_eff;
+    GSA_TRY(check_shape(qc_own, "qc_own", H, sp.W_g, d, false));
+    GSA_TRY(check_shape(kc_all, "kc_all", H, g.W, d, false));
+    GSA_TRY(check_shape(vc_all, "vc_all", H, g.W, d, false));
+    GSA_TRY(check_shape(o_comp_own, "o_comp_own", H, sp.W_g, d, false));
+    ShardBufs b;
+    const size_t need = shard_carve(sp, static_cast<char*>(workspace), workspace == nullptr, &b);
+    if (!workspace || need > ws_bytes + 256)
+        return fail(GSA_ERR_WORKSPACE, "shard_compress: workspace %zu < %zu bytes", ws_bytes, need);
+    if (sp.W_g == 0) return GSA_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    const uint8_t* excluded = nullptr;
+    if (params->variant == 1) {  // forced windows are global ids (selection.cpp:7-27)
+        GSA_CUDA(launch_forced(g.L, params->ref_stride, b.forced, b.mask, st));
+        excluded = b.mask;
+    }
+    GSA_CUDA(tc_compress_topk(*qc_own, *kc_all, *vc_all, g.k_eff, g.scale, excluded,
+                              static_cast<float*>(o_comp_own->data), o_comp_own->head_stride,
+                              o_comp_own->row_stride, lse_own, topk_own, nullptr, b.compress_ws,
+                              b.compress_ws_bytes, st));
+    return GSA_OK;
+}
+
+int gsa_shard_attend(const gsa_tensor* q_own, const gsa_tensor* k_all, const gsa_tensor* v_all,
+                     const gsa_tensor* w_g, const gsa_layout* layout, const gsa_params* params,
+                     const gsa_shard* shard, const gsa_tensor* o_comp_own, const int32_t* topk_own,
+                     const gsa_tensor* out_own, void* workspace, size_t ws_bytes, gsa_stream_t stream) {
+    GSA_TRY(check_tensor(q_own, "q_own"));
+    ShardPlan sp;
+    GSA_TRY(shard_checks(layout, params, shard, q_own->heads, q_own->dim, &sp));
+    const LayerPlan& g = sp.g;
+    const int H = g.heads, d = g.dim;
+    GSA_TRY(check_shape(q_own, "q_own", H, sp.Ms_g + sp.Mi_g, d, true));
+    GSA_TRY(check_shape(k_all, "k_all", H, g.M, d, true));
+    GSA_TRY(check_shape(v_all, "v_all", H, g.M, d, true));
+    if (k_all->dtype != q_own->dtype || v_all->dtype != q_own->dtype)
+        return fail(GSA_ERR_UNSUPPORTED, "shard_attend: q/k/v dtypes differ");
+    GSA_TRY(check_shape(o_comp_own, "o_comp_own", H, sp.W_g, d, false));
+    GSA_TRY(contiguous_f32_windows(o_comp_own, "o_comp_own"));
+    GSA_TRY(check_tensor(w_g, "w_g", false));
+    if (w_g->heads != H || w_g->rows != d || w_g->dim != d || w_g->row_stride != d ||
+        w_g->head_stride != (int64_t)d * d)
+        return fail(GSA_ERR_SHAPE_MISMATCH, "weights: w_g must be contiguous heads x dim x dim");
+    GSA_TRY(check_f32_out(out_own, "out_own", H, sp.Ms_g + sp.Mi_g, d));
+    ShardBufs b;
+    const size_t need = shard_carve(sp, static_cast<char*>(workspace), workspace == nullptr, &b);
+    if (!workspace || need > ws_bytes + 256)
+        return fail(GSA_ERR_WORKSPACE, "shard_attend: workspace %zu < %zu bytes", ws_bytes, need);
+    cudaStream_t st = (cudaStream_t)stream;
+    // own special rows: dense attention over all M keys (layer.hpp:80-96)
+    if (sp.Ms_g > 0)
+        GSA_TRY(dense_attention(q_own, k_all, v_all, g.scale, out_own, b.lse_spec, 0, 0, sp.Ms_g, st, b.dense_ws,
+                                b.dense_ws_bytes));
+    if (sp.W_g == 0) return GSA_OK;
+    if (params->variant == 1) GSA_CUDA(launch_forced(g.L, params->ref_stride, b.forced, b.mask, st));
+    SelectArgs a{};
+    a.q = ref_of(*q_own, sp.Ms_g);
+    a.k = ref_of(*k_all, g.Ms);
+    a.v = ref_of(*v_all, g.Ms);
+    a.heads = H;
+    a.dim = d;
+    a.L = sp.Lq;
+    a.Lkv = g.L;
+    a.rows = RowSource{nullptr, nullptr, b.forced, params->variant == 1 ? g.n_forced : 0, topk_own, g.k_eff, g.k_eff};
+    a.scale = g.scale;
+    a.out = static_cast<float*>(out_own->data) + (size_t)sp.Ms_g * out_own->row_stride;
+    a.out_hs = out_own->head_stride;
+    a.out_rs = out_own->row_stride;
+    a.w_g = static_cast<const float*>(w_g->data);
+    a.o_comp = static_cast<const float*>(o_comp_own->data);
+    a.wg_prep = b.wg_prep;
+    if (tc_select_supported(*q_own, sp.Lq, a.rows))
+        GSA_CUDA(tc_select_gate_merge(a, st));
+    else
+        GSA_CUDA(launch_select_f32(a, st));
     return GSA_OK;
 }
 

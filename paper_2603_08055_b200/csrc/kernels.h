@@ -23,6 +23,7 @@ struct PoolJob {
     __nv_bfloat16* hi; // optional split copies for the tensor-core path [H][W][d]
     __nv_bfloat16* lo;
     float* norm;       // optional ||row||_2 [H][W]
+    int64_t out_hs;    // head stride of out (elements); 0 = W*d (contiguous). hi/lo/norm assume contiguous
 };
 cudaError_t launch_pool(const PoolJob* jobs, int njobs, int heads, int dim, const DevLayout& L,
                         float inv, cudaStream_t st);
@@ -55,7 +56,8 @@ cudaError_t launch_attn_f32(const AttnArgs& a, cudaStream_t st);
 struct SelectArgs {
     TensorRef q, k, v;  // image rows
     int heads, dim;
-    DevLayout L;
+    DevLayout L;        // query side: windows / tokens of q, rows, o_comp, out (a view shard's own frames)
+    DevLayout Lkv;      // key side: the frames k/v cover and window ids refer to (== L unsharded)
     RowSource rows;
     float scale;
     float* out;  // o_sel or merged output

@@ -58,7 +58,8 @@ __global__ void __launch_bounds__(256) pool_kernel(PoolJobs jobs, int njobs, int
         acc[i] = __fmul_rn(acc[i], inv);
         sq = fmaf(acc[i], acc[i], sq);
     }
-    const int64_t orow = ((int64_t)h * L.windows + w) * dim + c * chunk;
+    const int64_t ohs = J.out_hs ? J.out_hs : (int64_t)L.windows * dim;
+    const int64_t orow = (int64_t)h * ohs + (int64_t)w * dim + c * chunk;
     if (active) {
         if (VEC8) {
             float4* o = reinterpret_cast<float4*>(J.out + orow);

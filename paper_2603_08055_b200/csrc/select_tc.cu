@@ -167,13 +167,17 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         uint32_t eph = 1;  // empty barriers: first pass succeeds
         uint32_t qph[2] = {1, 1};
         int cur_head = -1;
+        int n_heads = 0;      // W_g loads issued
         int64_t n_items = 0;  // items whose Q/Wg prelude has been issued
         auto load_chunks = [&](const GroupIt& it, const CUtensorMap* tm, bool with_prelude) {
             const int h = (int)(it.item / L.windows), w = (int)(it.item - (int64_t)h * L.windows);
             if (with_prelude) {
                 if (h != cur_head) {
-                    // W_g of the new head: wait until every G MMA of the old head completed
-                    if (n_items > 0) mbar_wait(&sm.wg_empty, (uint32_t)((n_items - 1) & 1));
+                    // W_g of the new head: wait until every G MMA of the old head completed.
+                    // wg_empty completes once per head (after its last item's G MMA), so
+                    // this wait and that commit advance in lockstep: a parity wait is exact
+                    if (n_heads > 0) mbar_wait(&sm.wg_empty, (uint32_t)((n_heads - 1) & 1));
+                    ++n_heads;
                     if (lane == 0) {
                         mbar_arrive_expect_tx(&sm.wg_full, 16384);
                         bulk_load(&sm.wg[0][0], p.wg_prep + (size_t)h * 16384, 16384, &sm.wg_full);
@@ -258,7 +262,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                             mma_bf16(gcol, umma_desc(smem_u32(&sm.wg[part][0]) + ks * 2048, 16, 1024, 2),
                                      umma_desc(smem_u32(&sm.q[qb][0]) + ks * 32, 16, 1024, 2), id_o,
                                      (part | ks) != 0);
-                    mma_commit(&sm.wg_empty);
+                    // the last item of this head on this CTA releases W_g
+                    const int64_t nxt = it.item + gridDim.x;
+                    if (nxt >= p.items || (int)(nxt / L.windows) != h) mma_commit(&sm.wg_empty);
                     ++n_items;
                 }
                 const int sb = (int)(jS & 1);
@@ -609,8 +615,8 @@ cudaError_t tc_select_gate_merge(const SelectArgs& a, cudaStream_t st) {
         !a.o_comp || !a.wg_prep)
         return cudaErrorNotSupported;
     CUtensorMap tq, tk, tv;
-    if (!make_window_map(&tq, a.q, a.heads, a.L) || !make_window_map(&tk, a.k, a.heads, a.L) ||
-        !make_window_map(&tv, a.v, a.heads, a.L))
+    if (!make_window_map(&tq, a.q, a.heads, a.L) || !make_window_map(&tk, a.k, a.heads, a.Lkv) ||
+        !make_window_map(&tv, a.v, a.heads, a.Lkv))
         return cudaErrorNotSupported;
     wg_prep_kernel<<<(a.heads * 4096 + 255) / 256, 256, 0, st>>>(a.w_g, a.heads, a.wg_prep);
     note_launch();

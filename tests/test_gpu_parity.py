@@ -301,3 +301,19 @@ def test_forward_with_plan(gsa, orc):
     out = gsa.gsa_forward_with_plan(dev(g["q"]), dev(g["k"]), dev(g["v"]), dev(g["w_g"], torch.float32), L,
                                     gsa.GsaParams(window_s=lt[4], top_k=g["top_k"]), plan)
     assert rel_l2(host(out), g["out"]) < 1e-4
+
+
+@pytest.mark.parametrize("heads,k", [(4, 8), (4, 16), (16, 16), (2, 16), (4, 24)])
+def test_forward_small_k_many_items_per_cta(gsa, orc, heads, k):
+    """Short plan rows (k <= 16 windows = 1-2 key chunks) with several work items
+    per persistent selection CTA let the TMA producer run two items ahead of the
+    MMA issuer: regression test for the W_g reload race (wg_empty must complete
+    once per head, not once per item)."""
+    lt = (0, 8, 36, 36, 4)
+    L = Layout(*lt)
+    q, k_, v, wg = make_inputs(orc, L, heads=heads, dim=64, seed=5)
+    ref = orc.gsa_forward(q, k_, v, wg, L, top_k=k)
+    out, ctx = run_forward(gsa, q, k_, v, wg, lt, k)
+    np.testing.assert_array_equal(ctx.topk.cpu().numpy(), ref["topk"])
+    assert np.abs(out - ref["out"]).max() < 1e-4
+    assert rel_l2(out, ref["out"]) < 1e-5
