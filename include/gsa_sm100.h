@@ -214,6 +214,15 @@ int gsa_shard_attend(const gsa_tensor* q_own, const gsa_tensor* k_all, const gsa
                      const gsa_tensor* out_own, void* workspace, size_t workspace_bytes,
                      gsa_stream_t stream);
 
+/* project_qkv (layer.hpp:48-76): q/k/v[h][t][j] = sum_a x[t][a] * w[h][a][j], a
+ * ascending, products and sums rounded separately (the reference's arithmetic,
+ * so f32 outputs are bit-identical to it). x: device [tokens][model_dim] f32;
+ * w_*: device [heads][model_dim][dim] f32; outputs f32 (exact) or bf16 (RNE of
+ * the exact value). Adjacent to the hot path. */
+int gsa_project_qkv(const float* x, int tokens, int model_dim, const float* w_q, const float* w_k,
+                    const float* w_v, int heads, int dim, const gsa_tensor* q, const gsa_tensor* k,
+                    const gsa_tensor* v, gsa_stream_t stream);
+
 /* KernelStats (types.hpp:78-86) in closed form for a gsa_forward call:
  * scores_computed = H*(Ms*M + W*W); keys_attended = sum over rows of
  * |row| * s^2 * s^2 (rows have width F + k_eff). */

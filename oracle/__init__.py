@@ -451,6 +451,16 @@ class RefLib:
                                                    self._p(out)))
         return out
 
+    def project(self, x, w_q, w_k, w_v):
+        """project_qkv (layer.hpp:48-76): x [tokens][C], w_* [H][C][d] -> q, k, v [H][tokens][d]."""
+        x, w_q, w_k, w_v = (np.ascontiguousarray(a, np.float32) for a in (x, w_q, w_k, w_v))
+        tokens, C_ = x.shape
+        H, _, d = w_q.shape
+        q, k, v = (np.empty((H, tokens, d), np.float32) for _ in range(3))
+        self._check(self.lib.gsa_ref_project(self._p(x), C.c_int(tokens), C.c_int(C_), self._p(w_q), self._p(w_k),
+                                             self._p(w_v), C.c_int(H), C.c_int(d), self._p(q), self._p(k), self._p(v)))
+        return q, k, v
+
     def random_init(self, seed, lt, heads, dim, model_dim, clustered=False):
         M = self.build_layout(*lt)[2] + lt[0]
         q, k, v = (np.empty((heads, M, dim), np.float32) for _ in range(3))

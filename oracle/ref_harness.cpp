@@ -374,4 +374,20 @@ int gsa_ref_random_init(uint64_t seed, int ns, int nf, int gh, int gw, int s, in
     });
 }
 
+// project_qkv (layer.hpp:48-76) on given X [tokens][C] and W_q/W_k/W_v [heads][C][dim].
+int gsa_ref_project(const float* x, int tokens, int model_dim, const float* wq, const float* wk, const float* wv,
+                    int heads, int dim, float* q, float* k, float* v) {
+    return guarded([&] {
+        gsa::LayerWeights<float> w;
+        w.w_q = to_tensor(wq, heads, model_dim, dim);
+        w.w_k = to_tensor(wk, heads, model_dim, dim);
+        w.w_v = to_tensor(wv, heads, model_dim, dim);
+        w.w_g = gsa::Tensor<float>(heads, dim, dim);
+        auto p = gsa::project_qkv(to_tensor(x, 1, tokens, model_dim), w);
+        from_tensor(p.q, q);
+        from_tensor(p.k, k);
+        from_tensor(p.v, v);
+    });
+}
+
 }  // extern "C"

@@ -24,7 +24,7 @@ from .gsa import (  # noqa: E402
     IndexOutOfRange, InvalidStride, InvalidTiling, KernelTiling, NonFiniteInput, SelectionPlan, ShapeMismatch,
     TokenLayout, Unsupported, Workspace, ZeroSizeError, avg_pool_tokens, block_sparse_attention, build_selection_plan,
     build_token_layout, forced_windows_of, forward_stats, fused_compressed_attention_topk, gate, gsa_forward,
-    gsa_forward_with_plan, resolved_scale, special_token_attention, tiled_attention, upsample_nearest,
+    gsa_forward_with_plan, project_qkv, resolved_scale, special_token_attention, tiled_attention, upsample_nearest,
 )
 
 __all__ = [
@@ -32,6 +32,6 @@ __all__ = [
     "GsaError", "GsaParams", "IndexOutOfRange", "InvalidStride", "InvalidTiling", "KernelTiling", "NonFiniteInput",
     "SelectionPlan", "ShapeMismatch", "TokenLayout", "Unsupported", "Workspace", "ZeroSizeError", "avg_pool_tokens",
     "block_sparse_attention", "build_selection_plan", "build_token_layout", "forced_windows_of", "forward_stats",
-    "fused_compressed_attention_topk", "gate", "gsa_forward", "gsa_forward_with_plan", "resolved_scale",
+    "fused_compressed_attention_topk", "gate", "gsa_forward", "gsa_forward_with_plan", "project_qkv", "resolved_scale",
     "special_token_attention", "tiled_attention", "upsample_nearest",
 ]

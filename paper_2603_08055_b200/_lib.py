@@ -87,6 +87,7 @@ def load() -> C.CDLL:
     L.gsa_shard_pool.argtypes = [T, T, T, Lp, P, S, T, T, T, vp]
     L.gsa_shard_compress.argtypes = [T, T, T, Lp, P, S, T, vp, vp, C.POINTER(C.c_int), vp, C.c_size_t, vp]
     L.gsa_shard_attend.argtypes = [T, T, T, T, Lp, P, S, T, vp, T, vp, C.c_size_t, vp]
+    L.gsa_project_qkv.argtypes = [vp, i32, i32, vp, vp, vp, i32, i32, T, T, T, vp]
     L.gsa_set_stage_events.argtypes = [C.POINTER(C.c_void_p), i32]
     L.gsa_launch_count.argtypes = [C.POINTER(C.c_uint64)]
     _lib = L
@@ -100,5 +101,5 @@ EXPORTED_SYMBOLS = [
     "gsa_build_selection_plan", "gsa_build_selection_plan_workspace_bytes", "gsa_block_sparse_attention",
     "gsa_gate", "gsa_forward_workspace_bytes", "gsa_forward", "gsa_forward_with_plan", "gsa_forward_stats",
     "gsa_set_stage_events", "gsa_launch_count", "gsa_shard_workspace_bytes", "gsa_shard_pool", "gsa_shard_compress",
-    "gsa_shard_attend",
+    "gsa_shard_attend", "gsa_project_qkv",
 ]

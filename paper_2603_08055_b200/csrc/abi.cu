@@ -874,6 +874,34 @@ int gsa_shard_attend(const gsa_tensor* q_own, const gsa_tensor* k_all, const gsa
     return GSA_OK;
 }
 
+int gsa_project_qkv(const float* x, int tokens, int model_dim, const float* w_q, const float* w_k,
+                    const float* w_v, int heads, int dim, const gsa_tensor* q, const gsa_tensor* k,
+                    const gsa_tensor* v, gsa_stream_t stream) {
+    // project_qkv (layer.hpp:48-76): X [1 x tokens x C], W [H x C x d]
+    if (tokens < 0 || model_dim < 1 || heads < 0 || dim < 1)
+        return fail(GSA_ERR_SHAPE_MISMATCH, "project_qkv: bad extents");
+    if ((int64_t)tokens * model_dim > 0 && !x) return fail(GSA_ERR_GENERIC, "project_qkv: null x");
+    if (!w_q || !w_k || !w_v) return fail(GSA_ERR_GENERIC, "project_qkv: null weights");
+    const gsa_tensor* outs[3] = {q, k, v};
+    ProjectMats m{};
+    m.w[0] = w_q;
+    m.w[1] = w_k;
+    m.w[2] = w_v;
+    int dtype = -1;
+    for (int i = 0; i < 3; ++i) {
+        GSA_TRY(check_tensor(outs[i], i == 0 ? "q" : (i == 1 ? "k" : "v")));
+        if (outs[i]->heads != heads || outs[i]->rows != tokens || outs[i]->dim != dim)
+            return fail(GSA_ERR_SHAPE_MISMATCH, "project_qkv: output must be [heads x tokens x dim]");
+        if (dtype >= 0 && outs[i]->dtype != dtype) return fail(GSA_ERR_UNSUPPORTED, "project_qkv: output dtypes differ");
+        dtype = outs[i]->dtype;
+        m.out[i] = outs[i]->data;
+        m.out_hs[i] = outs[i]->head_stride;
+        m.out_rs[i] = outs[i]->row_stride;
+    }
+    GSA_CUDA(launch_project(x, tokens, model_dim, m, 3, heads, dim, dtype == GSA_DTYPE_BF16, (cudaStream_t)stream));
+    return GSA_OK;
+}
+
 int gsa_forward_stats(const gsa_layout* layout, const gsa_params* p, int heads, uint64_t* scores,
                       uint64_t* keys) {
     GSA_TRY(check_layout(layout));

@@ -72,6 +72,15 @@ struct SelectArgs {
 };
 cudaError_t launch_select_f32(const SelectArgs& a, cudaStream_t st);
 
+// ---- exact per-head projection (project.cu) ------------------------------
+struct ProjectMats {
+    const float* w[3];  // [H][C][d] f32
+    void* out[3];       // [H][tokens][d] (f32 or bf16)
+    int64_t out_hs[3], out_rs[3];
+};
+cudaError_t launch_project(const float* x, int tokens, int C, const ProjectMats& mats, int nmats, int heads, int dim,
+                           bool bf16_out, cudaStream_t st);
+
 // ---- gate, upsample, plan helpers (misc.cu) -----------------------------
 cudaError_t launch_gate(const TensorRef& q, int heads, int rows, int dim, const float* w_g,
                         float* g, int64_t g_hs, int64_t g_rs, cudaStream_t st);

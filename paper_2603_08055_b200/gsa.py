@@ -439,3 +439,22 @@ def forward_stats(layout: TokenLayout, params: GsaParams, heads: int) -> tuple[i
     a, b = C.c_uint64(), C.c_uint64()
     _check(_lib.load().gsa_forward_stats(C.byref(layout.c()), C.byref(params.c()), heads, C.byref(a), C.byref(b)))
     return a.value, b.value
+
+
+def project_qkv(x: torch.Tensor, w_q: torch.Tensor, w_k: torch.Tensor, w_v: torch.Tensor,
+                dtype: torch.dtype = torch.float32):
+    """project_qkv (layer.hpp:48-76): x [tokens, C] f32, w_* [H, C, d] f32 ->
+    (q, k, v) [H, tokens, d]. f32 outputs are bit-identical to the reference
+    (ascending-a accumulation, no FMA); bf16 outputs are their RNE rounding."""
+    L = _lib.load()
+    x, w_q, w_k, w_v = (t.contiguous() for t in (x, w_q, w_k, w_v))
+    if x.dim() == 3:
+        x = x.reshape(x.shape[-2], x.shape[-1])
+    T, Cm = x.shape
+    H, C2, d = w_q.shape
+    if C2 != Cm or w_k.shape != w_q.shape or w_v.shape != w_q.shape:
+        raise ShapeMismatch("project_qkv: X must be [tokens x model_dim] and weights [heads x model_dim x dim]")
+    outs = [_empty(H, T, d, dtype=dtype, device=x.device) for _ in range(3)]
+    _check(L.gsa_project_qkv(_ptr(x), T, Cm, _ptr(w_q), _ptr(w_k), _ptr(w_v), H, d, C.byref(_desc(outs[0])),
+                             C.byref(_desc(outs[1])), C.byref(_desc(outs[2])), _stream()))
+    return tuple(outs)

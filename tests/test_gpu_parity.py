@@ -317,3 +317,23 @@ def test_forward_small_k_many_items_per_cta(gsa, orc, heads, k):
     np.testing.assert_array_equal(ctx.topk.cpu().numpy(), ref["topk"])
     assert np.abs(out - ref["out"]).max() < 1e-4
     assert rel_l2(out, ref["out"]) < 1e-5
+
+
+@pytest.mark.parametrize("tokens,C,H", [(130, 1024, 2), (1000, 96, 3), (7, 33, 1)])
+def test_project_qkv_bitexact_vs_reference(gsa, ref, tokens, C, H):
+    """project_qkv (layer.hpp:48-76) on the device reproduces the reference's
+    f32 arithmetic bit for bit (ascending reduction, no FMA)."""
+    rng = np.random.default_rng(tokens + C)
+    x = (rng.standard_normal((tokens, C)) / np.sqrt(C)).astype(np.float32)
+    w = [(rng.standard_normal((H, C, 64)) / np.sqrt(C)).astype(np.float32) for _ in range(3)]
+    rq, rk, rv = ref.project(x, *w)
+    q, k, v = gsa.project_qkv(dev(x, torch.float32), *(dev(t, torch.float32) for t in w))
+    for got, want in ((q, rq), (k, rk), (v, rv)):
+        np.testing.assert_array_equal(host(got).view(np.uint32), want.view(np.uint32))
+    qb, _, _ = gsa.project_qkv(dev(x, torch.float32), *(dev(t, torch.float32) for t in w), dtype=torch.bfloat16)
+    np.testing.assert_array_equal(host(qb), orc_bf16(rq))
+
+
+def orc_bf16(x):
+    from oracle import Oracle
+    return Oracle().bf16_round(x)
