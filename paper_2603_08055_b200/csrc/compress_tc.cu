@@ -33,50 +33,49 @@ namespace {
 
 using namespace ptx;
 
-constexpr int NS = 3;
-constexpr int TILE = 16384;       // 128 rows x 64 bf16
-constexpr int STAGE = 2 * TILE;   // hi + lo
-constexpr int NTHREADS = 192;
+constexpr int NS = 4;                   // K/V ring stages
+constexpr int TILE = 16384;             // 128 rows x 64 bf16
+constexpr int STAGE = 2 * TILE;         // hi + lo
+constexpr int NTHREADS = 384;           // warps 0-3 / 4-7: softmax WG0 / WG1, 8: TMA, 9: MMA, 10-11 idle
+constexpr int NWG = 2;                  // query tiles (softmax warpgroups) per CTA
+constexpr int NSB = 3;                  // S/P buffers in TMEM, rotating over the S(n) sequence
 constexpr uint32_t TMEM_COLS = 512;
-constexpr uint32_t O_COL = 384;
+constexpr uint32_t O_COL0 = 384;        // O of WG w: [384 + 64 w, +64); S/P buffer b: [128 b, +128)
 constexpr float RESCALE_LOG2 = 8.0f;
-constexpr int KCAP = 32;          // max k_eff on this path
-constexpr int SCAP = 95;          // per-row candidate stage (odd stride: 2-way banks at most)
-constexpr int FLUSH_AT = SCAP - 32;  // flush before a 32-column chunk could overflow the stage
-constexpr int CAND = 64;          // candidates handed to the exact re-score (2 per lane)
-constexpr float EPS_REL = 0.00048828125f;  // 2^-11
+constexpr int KCAP = 32;                // max k_eff on this path
+constexpr int CCAP = 512;               // candidates a row may stream out (more: exact fallback)
+constexpr int CAND = 64;                // candidates handed to the exact re-score (2 per lane)
+constexpr int NBIN = 8;                 // threshold histogram bins (8-bit saturating counters)
+constexpr float EPS_REL = 0.00048828125f;          // 2^-11
 constexpr float DELTA_REL = 9.5367431640625e-07f;  // 2^-20: collapse of distinct sums under *scale
 
 struct __align__(1024) CompSmem {
-    uint8_t qh[TILE], ql[TILE];
-    uint8_t ring[NS][STAGE];
-    float2 stage[128][SCAP];     // per row: candidates (approx score, index bits), unsorted
+    uint8_t q[NWG][2][TILE];  // the CTA's two query tiles, bf16 hi / lo
+    uint8_t ring[NS][STAGE];  // K / V tiles, bf16 hi / lo
     uint64_t full[NS], empty[NS];
     uint64_t q_full;
-    uint64_t s_full[3], s_free[3];
-    // by tile parity: the softmax runs up to a tile ahead of the MMA, and parity waits are
-    // only unambiguous within one phase of their target
-    uint64_t p_full[2], o_done[2];
+    uint64_t s_full[NSB];
+    uint64_t p_full[NWG][2];  // by tile parity: a WG may run one tile ahead of the MMA's P wait
+    uint64_t o_done[NWG];     // every PV of the WG (lazy O rescale waits on it)
+    uint64_t o_final[NWG];    // the WG's last PV
     uint32_t tmem_base;
 };
 
 struct CompParams {
-    int debug;  // bring-up switches (GSA_DEBUG_COMPRESS): 1 = no top-k scan, 2 = 1-term S/PV
+    int debug;  // bring-up switches (GSA_DEBUG_COMPRESS): 1 = no top-k scan, 16 = flag every row
     int heads, Wq, Wk, k_eff;  // query rows (windows of this shard) / key rows (all windows)
     float scale, c2;
     int kv_tiles;
-    const float* qnorm;      // [H][Wq]
-    const float* kmax;       // [H]
-    const uint32_t* exbits;  // [ceil(Wk/32)] or null
+    const float* qnorm;       // [H][Wq]
+    const float* kmax;        // [H]
+    const uint32_t* exbits;   // [ceil(Wk/32)] or null
     float* out;
     int64_t out_hs, out_rs;
-    float* lse;              // [H][Wq]
-    float2* cand;            // [H*Wq][CAND]
-    int* cand_n;             // [H*Wq]
-    uint8_t* flag;           // [H*Wq]
+    float* lse;               // [H][Wq]
+    float2* cand;             // [H*Wq][CCAP] (approx score, window id)
+    int* cand_n;              // [H*Wq]
+    uint8_t* flag;            // [H*Wq]
 };
-
-__device__ __forceinline__ uint32_t s_col(int b) { return (uint32_t)(128 * b); }
 
 // order-preserving map float -> uint32 (finite and +-inf); 0 is below every real key
 __device__ __forceinline__ uint32_t fkey(float x) {
@@ -91,40 +90,8 @@ __device__ __forceinline__ float topk_threshold(float tau, float eps) {
     return tau - (2.0f * eps + DELTA_REL * fabsf(tau));
 }
 
-// Warp-cooperative flush of row R's candidate stage (n entries, all >= thr):
-// exact K-th largest approximate score tau by a 32-step radix select over
-// order-preserving keys (3 entries per lane, counts summed with redux.sync),
-// then keep only entries >= the raised threshold. Returns the new count
-// (>= K); the owner lane takes it and the new threshold.
-__device__ __noinline__ int flush_stage(float2* stage, int n, int K, float eps, float& thr, int lane) {
-    float2 e[3];
-    uint32_t key[3];
-#pragma unroll
-    for (int s = 0; s < 3; ++s) {
-        const int i = lane + 32 * s;
-        e[s] = i < n ? stage[i] : make_float2(-INFINITY, 0.0f);
-        key[s] = i < n ? fkey(e[s].x) : 0u;
-    }
-    uint32_t res = 0;
-#pragma unroll 1
-    for (int bit = 31; bit >= 0; --bit) {
-        const uint32_t cand = res | (1u << bit);
-        const int c = (key[0] >= cand) + (key[1] >= cand) + (key[2] >= cand);
-        if ((int)__reduce_add_sync(0xffffffffu, (unsigned)c) >= K) res = cand;
-    }
-    thr = fmaxf(thr, topk_threshold(fkey_inv(res), eps));
-    __syncwarp();
-    int base = 0;
-#pragma unroll
-    for (int s = 0; s < 3; ++s) {
-        const bool keep = key[s] != 0u && e[s].x >= thr;
-        const unsigned b = __ballot_sync(0xffffffffu, keep);
-        if (keep) stage[base + __popc(b & ((1u << lane) - 1u))] = e[s];
-        base += __popc(b);
-    }
-    __syncwarp();
-    return base;
-}
+__device__ __forceinline__ void setmaxnreg_inc() { asm volatile("setmaxnreg.inc.sync.aligned.u32 224;\n" ::: "memory"); }
+__device__ __forceinline__ void setmaxnreg_dec() { asm volatile("setmaxnreg.dec.sync.aligned.u32 56;\n" ::: "memory"); }
 
 // v[e] for a runtime e without local memory: a 5-level select tree
 __device__ __forceinline__ float select32(const uint32_t (&v)[32], int e) {
@@ -140,6 +107,57 @@ __device__ __forceinline__ float select32(const uint32_t (&v)[32], int e) {
     return __uint_as_float((e & 1) ? a[1] : a[0]);
 }
 
+// Per-row streaming top-k, run by the thread that owns the row. The row keeps a
+// lower bound LB of its K-th best approximate score and streams every
+// selectable score >= LB - margin into its global candidate list. LB rises via
+// a histogram of the candidates above it (8 bins of width `delta`, saturating
+// byte counters): once >= K candidates sit at or above bin j, LB += j*delta is
+// still a lower bound. No sorting or shared state on the hot path; the exact
+// K-th best and the final candidate set are resolved by the re-score kernel.
+struct RowTopk {
+    float lb, thr, delta, inv_delta, eps;
+    uint32_t hist[2];  // bytes: bins 0..7 relative to lb (bin 7 open-ended)
+    int cnt;           // candidates streamed; -1 = none (invalid row) / overflow
+    float2* dst;
+
+    __device__ __forceinline__ void add(float v, int col) {
+        if (cnt < 0) return;
+        if (cnt == CCAP) {
+            cnt = -1;  // more candidates than the list holds: exact fallback for this row
+            return;
+        }
+        dst[cnt++] = make_float2(v, __int_as_float(col));
+        if (v >= lb) {
+            const int b = min(NBIN - 1, (int)((v - lb) * inv_delta));
+            const uint32_t inc = 1u << (8 * (b & 3));
+            if (b < 4) hist[0] = __vaddus4(hist[0], inc);
+            else hist[1] = __vaddus4(hist[1], inc);
+        }
+    }
+    // after each tile: raise LB by the largest j with >= K counted at or above bin j
+    __device__ __forceinline__ void raise(int K) {
+        int suffix = 0, j = 0;
+#pragma unroll
+        for (int b = NBIN - 1; b >= 1; --b) {
+            suffix += (int)((hist[b >> 2] >> (8 * (b & 3))) & 0xffu);
+            if (j == 0 && suffix >= K) j = b;
+        }
+        if (j == 0) return;
+        lb += (float)j * delta;
+        thr = fmaxf(thr, topk_threshold(lb, eps));
+        const uint64_t h = ((uint64_t)hist[1] << 32) | hist[0];
+        const uint64_t s = h >> (8 * j);
+        hist[0] = (uint32_t)s;
+        hist[1] = (uint32_t)(s >> 32);
+    }
+};
+
+// Position of K(t) / V(t) in the TMA load sequence K0 K1 V0 K2 V1 K3 V2 ...
+// K(T-1) V(T-2) V(T-1) (the MMA issuer's first-use order); ring slot = seq % NS,
+// fill phase = seq / NS.
+__device__ __forceinline__ int seq_k(int t) { return t == 0 ? 0 : 2 * t - 1; }
+__device__ __forceinline__ int seq_v(int t, int T) { return t == T - 1 ? 2 * T - 1 : 2 * t + 2; }
+
 __global__ void __launch_bounds__(NTHREADS, 1)
     compress_tc_kernel(const __grid_constant__ CUtensorMap tm_qh, const __grid_constant__ CUtensorMap tm_ql,
                        const __grid_constant__ CUtensorMap tm_kh, const __grid_constant__ CUtensorMap tm_kl,
@@ -148,145 +166,158 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     CompSmem& sm = *reinterpret_cast<CompSmem*>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
     const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
-    const int qt = blockIdx.x, h = blockIdx.y;
+    const int h = blockIdx.y;
     const int T = p.kv_tiles;
+    const int N = NWG * T;  // S(n), n = 2t + w: WG w's scores against key tile t
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < NS; ++i) {
             mbar_init(&sm.full[i], 1);
             mbar_init(&sm.empty[i], 1);
         }
-        for (int i = 0; i < 3; ++i) {
-            mbar_init(&sm.s_full[i], 1);
-            mbar_init(&sm.s_free[i], 1);
-        }
         mbar_init(&sm.q_full, 1);
-        mbar_init(&sm.p_full[0], 128);
-        mbar_init(&sm.p_full[1], 128);
-        mbar_init(&sm.o_done[0], 1);
-        mbar_init(&sm.o_done[1], 1);
+        for (int b = 0; b < NSB; ++b) mbar_init(&sm.s_full[b], 1);
+        for (int w = 0; w < NWG; ++w) {
+            mbar_init(&sm.p_full[w][0], 128);
+            mbar_init(&sm.p_full[w][1], 128);
+            mbar_init(&sm.o_done[w], 1);
+            mbar_init(&sm.o_final[w], 1);
+        }
         fence_barrier_init();
     }
-    if (warp == 1) tmem_alloc(&sm.tmem_base, TMEM_COLS);
+    if (warp == 9) tmem_alloc(&sm.tmem_base, TMEM_COLS);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = sm.tmem_base;
 
-    if (warp == 0) {
-        if (lane == 0) {
+    if (warp >= 8) {
+        setmaxnreg_dec();
+        if (warp == 8) {
             // ================================ TMA ================================
-            mbar_arrive_expect_tx(&sm.q_full, 2 * TILE);
-            tma_load_3d(&sm.qh[0], &tm_qh, &sm.q_full, 0, qt * 128, h);
-            tma_load_3d(&sm.ql[0], &tm_ql, &sm.q_full, 0, qt * 128, h);
-            int st = 0;
-            uint32_t eph = 1;
-            auto load = [&](const CUtensorMap* th, const CUtensorMap* tl, int t) {
-                mbar_wait(&sm.empty[st], eph);
-                mbar_arrive_expect_tx(&sm.full[st], STAGE);
-                tma_load_3d(&sm.ring[st][0], th, &sm.full[st], 0, t * 128, h);
-                tma_load_3d(&sm.ring[st][TILE], tl, &sm.full[st], 0, t * 128, h);
-                if (++st == NS) {
-                    st = 0;
-                    eph ^= 1;
+            if (elect_one()) {
+                mbar_arrive_expect_tx(&sm.q_full, NWG * 2 * TILE);
+                for (int w = 0; w < NWG; ++w) {
+                    tma_load_3d(&sm.q[w][0][0], &tm_qh, &sm.q_full, 0, (blockIdx.x * NWG + w) * 128, h);
+                    tma_load_3d(&sm.q[w][1][0], &tm_ql, &sm.q_full, 0, (blockIdx.x * NWG + w) * 128, h);
                 }
+            }
+            __syncwarp();
+            int seq = 0;
+            auto load = [&](const CUtensorMap* th, const CUtensorMap* tl, int t) {
+                const int st = seq % NS;
+                mbar_wait(&sm.empty[st], (uint32_t)(((seq / NS) & 1) ^ 1));
+                if (elect_one()) {
+                    mbar_arrive_expect_tx(&sm.full[st], STAGE);
+                    tma_load_3d(&sm.ring[st][0], th, &sm.full[st], 0, t * 128, h);
+                    tma_load_3d(&sm.ring[st][TILE], tl, &sm.full[st], 0, t * 128, h);
+                }
+                __syncwarp();
+                ++seq;
             };
             load(&tm_kh, &tm_kl, 0);
+            if (T > 1) load(&tm_kh, &tm_kl, 1);
             for (int t = 0; t < T; ++t) {
-                if (t + 1 < T) load(&tm_kh, &tm_kl, t + 1);
                 load(&tm_vh, &tm_vl, t);
+                if (t + 2 < T) load(&tm_kh, &tm_kl, t + 2);
             }
-        }
-    } else if (warp == 1) {
-        if (lane == 0) {
+        } else if (warp == 9) {
             // ================================ MMA ================================
+            // S(n) = Q_w . K(t)^T  (Qh.Kh + Qh.Kl + Ql.Kh)          -> S/P buffer n % 3
+            // O_w += P(n) . V(t)    (Ph.Vh + Ph.Vl + Pl.Vh; P in TMEM)  n = 2t + w
+            // Issue order: S(0) S(1) S(2) | PV(n) S(n+3) | ... S(n+3) reuses PV(n)'s
+            // buffer (in-order execution) and is issued BEFORE the P waits of n+1, n+2,
+            // so every WG always has its next S computing while it runs a softmax.
             const uint32_t id_s = idesc_bf16(128, 128, 0, 0);
             const uint32_t id_o = idesc_bf16(128, 64, 0, 1);
-            int st = 0;
-            uint32_t fph = 0;
-            uint32_t freeph[3] = {1, 1, 1};
-            uint32_t pph[2] = {0, 0};
-            mbar_wait(&sm.q_full, 0);
-            const uint64_t qh = umma_desc(smem_u32(&sm.qh[0]), 16, 1024, 2);
-            const uint64_t ql = umma_desc(smem_u32(&sm.ql[0]), 16, 1024, 2);
-            auto issue_S = [&](int t) {
-                const int b = t % 3;
-                mbar_wait(&sm.s_free[b], freeph[b]);
-                freeph[b] ^= 1;
-                mbar_wait(&sm.full[st], fph);
+            auto wait_tile = [&](int s) {
+                mbar_wait(&sm.full[s % NS], (uint32_t)((s / NS) & 1));
                 tc_fence_after();
-                const uint64_t kh = umma_desc(smem_u32(&sm.ring[st][0]), 16, 1024, 2);
-                const uint64_t kl = umma_desc(smem_u32(&sm.ring[st][TILE]), 16, 1024, 2);
-                const uint32_t d = tmem + s_col(b);
-                for (int ks = 0; ks < 4; ++ks) mma_bf16(d, qh + 2 * ks, kh + 2 * ks, id_s, ks != 0);
-                if (!(p.debug & 2)) {
-                    for (int ks = 0; ks < 4; ++ks) mma_bf16(d, qh + 2 * ks, kl + 2 * ks, id_s, 1);
-                    for (int ks = 0; ks < 4; ++ks) mma_bf16(d, ql + 2 * ks, kh + 2 * ks, id_s, 1);
-                }
-                mma_commit(&sm.empty[st]);
-                mma_commit(&sm.s_full[b]);
-                if (++st == NS) {
-                    st = 0;
-                    fph ^= 1;
-                }
             };
-            auto issue_PV = [&](int t) {
-                const int b = t % 3;
-                mbar_wait(&sm.p_full[t & 1], pph[t & 1]);
-                pph[t & 1] ^= 1;
-                mbar_wait(&sm.full[st], fph);
-                tc_fence_after();
-                const uint64_t vh = umma_desc(smem_u32(&sm.ring[st][0]), 16, 1024, 2);
-                const uint64_t vl = umma_desc(smem_u32(&sm.ring[st][TILE]), 16, 1024, 2);
-                for (int ks = 0; ks < 8; ++ks) {
-                    const uint32_t a_hi = tmem + s_col(b) + 32 * (ks >> 1) + 8 * (ks & 1);
-                    mma_bf16_ts(tmem + O_COL, a_hi, vh + 128 * ks, id_o, (t | ks) != 0);
-                    if (!(p.debug & 2)) {
-                        mma_bf16_ts(tmem + O_COL, a_hi, vl + 128 * ks, id_o, 1);
-                        mma_bf16_ts(tmem + O_COL, a_hi + 16, vh + 128 * ks, id_o, 1);
+            auto issue_S = [&](int n) {
+                const int w = n & 1, t = n >> 1;
+                const int s = seq_k(t);
+                if (w == 0) wait_tile(s);
+                const uint64_t kh = umma_desc(smem_u32(&sm.ring[s % NS][0]), 16, 1024, 2);
+                const uint64_t kl = umma_desc(smem_u32(&sm.ring[s % NS][TILE]), 16, 1024, 2);
+                const uint64_t qh = umma_desc(smem_u32(&sm.q[w][0][0]), 16, 1024, 2);
+                const uint64_t ql = umma_desc(smem_u32(&sm.q[w][1][0]), 16, 1024, 2);
+                const uint32_t d = tmem + 128 * (n % NSB);
+                if (elect_one()) {
+                    for (int ks = 0; ks < 4; ++ks) {
+                        mma_bf16(d, qh + 2 * ks, kh + 2 * ks, id_s, ks != 0);
+                        mma_bf16(d, qh + 2 * ks, kl + 2 * ks, id_s, 1);
+                        mma_bf16(d, ql + 2 * ks, kh + 2 * ks, id_s, 1);
                     }
+                    mma_commit(&sm.s_full[n % NSB]);
+                    if (w == 1) mma_commit(&sm.empty[s % NS]);  // K(t) fully used
                 }
-                mma_commit(&sm.empty[st]);
-                mma_commit(&sm.s_free[b]);
-                mma_commit(&sm.o_done[t & 1]);
-                if (++st == NS) {
-                    st = 0;
-                    fph ^= 1;
-                }
+                __syncwarp();
             };
-            issue_S(0);
-            for (int t = 0; t < T; ++t) {
-                if (t + 1 < T) issue_S(t + 1);
-                issue_PV(t);
+            auto issue_PV = [&](int n) {
+                const int w = n & 1, t = n >> 1;
+                const int s = seq_v(t, T);
+                if (w == 0) wait_tile(s);
+                mbar_wait(&sm.p_full[w][t & 1], (uint32_t)((t >> 1) & 1));
+                tc_fence_after();
+                const uint64_t vh = umma_desc(smem_u32(&sm.ring[s % NS][0]), 16, 1024, 2);
+                const uint64_t vl = umma_desc(smem_u32(&sm.ring[s % NS][TILE]), 16, 1024, 2);
+                const uint32_t o = tmem + O_COL0 + 64 * w, pb = tmem + 128 * (n % NSB);
+                if (elect_one()) {
+                    for (int ks = 0; ks < 8; ++ks) {
+                        const uint32_t a_hi = pb + 32 * (ks >> 1) + 8 * (ks & 1);
+                        mma_bf16_ts(o, a_hi, vh + 128 * ks, id_o, (t | ks) != 0);
+                        mma_bf16_ts(o, a_hi, vl + 128 * ks, id_o, 1);
+                        mma_bf16_ts(o, a_hi + 16, vh + 128 * ks, id_o, 1);
+                    }
+                    mma_commit(&sm.o_done[w]);
+                    if (t == T - 1) mma_commit(&sm.o_final[w]);
+                    if (w == 1) mma_commit(&sm.empty[s % NS]);  // V(t) fully used
+                }
+                __syncwarp();
+            };
+            mbar_wait(&sm.q_full, 0);
+            tc_fence_after();
+            for (int n = 0; n < min(NSB, N); ++n) issue_S(n);
+            for (int n = 0; n < N; ++n) {
+                issue_PV(n);
+                if (n + NSB < N) issue_S(n + NSB);
             }
         }
     } else {
-        // ===================== softmax + streaming top-k (warps 2..5) =====================
-        const int qd = warp & 3;
+        // ===================== softmax + streaming top-k (warps 0..7) =====================
+        setmaxnreg_inc();
+        const int w = warp >> 2;           // warpgroup = query tile of this CTA
+        const int qd = warp & 3;           // TMEM lane quadrant
         const int row = 32 * qd + lane;
-        const int grow = qt * 128 + row;
+        const int grow = (blockIdx.x * NWG + w) * 128 + row;
         const bool row_ok = grow < p.Wq;
         const uint32_t lane_base = tmem + ((uint32_t)(32 * qd) << 16);
+        const uint32_t o_base = lane_base + O_COL0 + 64 * w;
         const int K = p.k_eff;
-        const float eps = row_ok ? EPS_REL * p.qnorm[(int64_t)h * p.Wq + grow] * p.kmax[h] : 0.0f;
-        float thr = -INFINITY;  // this row's candidate threshold (monotone lower bound of tau - margin)
-        int cnt = row_ok ? 0 : -1;  // staged candidates; -1 = overflowed / no row (exact fallback)
-        float2* my_stage = sm.stage[row];
+        const int64_t r = (int64_t)h * p.Wq + grow;
+        RowTopk tk;
+        tk.lb = -INFINITY;
+        tk.thr = -INFINITY;
+        tk.delta = 1.0f;
+        tk.inv_delta = 1.0f;
+        tk.eps = row_ok ? EPS_REL * p.qnorm[r] * p.kmax[h] : 0.0f;
+        tk.hist[0] = tk.hist[1] = 0u;
+        tk.cnt = (row_ok && K > 0) ? 0 : -1;
+        tk.dst = p.cand + r * CCAP;
         float m_used = -INFINITY, l = 0.0f;
-        uint32_t sph[3] = {0, 0, 0};
 
         for (int t = 0; t < T; ++t) {
-            const int b = t % 3;
-            mbar_wait(&sm.s_full[b], sph[b]);
-            sph[b] ^= 1;
+            const int n = 2 * t + w, b = n % NSB;
+            const uint32_t s_base = lane_base + 128 * b;
+            mbar_wait(&sm.s_full[b], (uint32_t)((n / NSB) & 1));
             __syncwarp();  // .sync.aligned tcgen05 ops below need a converged warp
             tc_fence_after();
             uint32_t sr[4][32];
 #pragma unroll
-            for (int c = 0; c < 4; ++c) tmem_ld_32x32b_x32(lane_base + s_col(b) + 32 * c, sr[c]);
+            for (int c = 0; c < 4; ++c) tmem_ld_32x32b_x32(s_base + 32 * c, sr[c]);
             tmem_wait_ld();
             const int valid = p.Wk - t * 128;
-            float cmax[4];
             if (valid < 128) {  // last key tile only: columns past Wk do not exist
 #pragma unroll
                 for (int c = 0; c < 4; ++c)
@@ -294,8 +325,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     for (int e = 0; e < 32; ++e)
                         if (32 * c + e >= valid) sr[c][e] = __float_as_uint(-INFINITY);
             }
+            float cmax[4];
 #pragma unroll
-            for (int c = 0; c < 4; ++c) {  // 4-way tree per chunk (short dependency chains)
+            for (int c = 0; c < 4; ++c) {  // 4-way trees (short dependency chains)
                 float a0 = __uint_as_float(sr[c][0]), a1 = __uint_as_float(sr[c][1]);
                 float a2 = __uint_as_float(sr[c][2]), a3 = __uint_as_float(sr[c][3]);
 #pragma unroll
@@ -313,9 +345,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             } else {
                 const bool need = (mt - m_used) * p.c2 > RESCALE_LOG2;
                 if (__any_sync(0xffffffffu, need)) {
-                    // PV(t-1) done: completion #((t-1)>>1) of o_done[(t-1)&1]; PV(t-3) is already
-                    // implied by s_full(t) and PV(t+1) cannot have run, so this parity is exact
-                    mbar_wait(&sm.o_done[(t - 1) & 1], (uint32_t)(((t - 1) >> 1) & 1));
+                    // O must hold every tile < t: PV_w(t-1) done = o_done[w] phase t-1
+                    mbar_wait(&sm.o_done[w], (uint32_t)((t - 1) & 1));
                     __syncwarp();
                     tc_fence_after();
                     const float mnew = need ? mt : m_used;
@@ -323,11 +354,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     uint32_t o[32];
 #pragma unroll
                     for (int half = 0; half < 2; ++half) {
-                        tmem_ld_32x32b_x32(lane_base + O_COL + 32 * half, o);
+                        tmem_ld_32x32b_x32(o_base + 32 * half, o);
                         tmem_wait_ld();
 #pragma unroll
                         for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * f);
-                        tmem_st_32x32b_x32(lane_base + O_COL + 32 * half, o);
+                        tmem_st_32x32b_x32(o_base + 32 * half, o);
                     }
                     tmem_wait_st();
                     l *= f;
@@ -335,7 +366,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 }
             }
             const float mc = m_used * p.c2;
-            float lsum[4] = {0.0f, 0.0f, 0.0f, 0.0f};  // independent partial sums
+            float lsum[4] = {0.0f, 0.0f, 0.0f, 0.0f};
 #pragma unroll
             for (int c = 0; c < 4; ++c) {
                 uint32_t hi[16], lo[16];
@@ -349,17 +380,15 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     const __nv_bfloat162 hb = *reinterpret_cast<const __nv_bfloat162*>(&hi[e2]);
                     lo[e2] = pack_bf16(p0 - __low2float(hb), p1 - __high2float(hb));
                 }
-                tmem_st_32x32b_x16(lane_base + s_col(b) + 32 * c, hi);
-                tmem_st_32x32b_x16(lane_base + s_col(b) + 32 * c + 16, lo);
+                tmem_st_32x32b_x16(s_base + 32 * c, hi);
+                tmem_st_32x32b_x16(s_base + 32 * c + 16, lo);
             }
             l += (lsum[0] + lsum[1]) + (lsum[2] + lsum[3]);
             tmem_wait_st();
             tc_fence_before();
-            mbar_arrive(&sm.p_full[t & 1]);
+            mbar_arrive(&sm.p_full[w][t & 1]);
 
-            // ---- streaming top-k over this tile's approximate scores (after P is out):
-            // append every selectable score >= thr to the row's stage; a full stage is
-            // flushed by the whole warp (radix select of the K-th best, threshold raise)
+            // ---- streaming top-k over this tile's approximate scores (overlaps the MMAs)
             if (K > 0 && !(p.debug & 1)) {
                 uint4 ex = make_uint4(0, 0, 0, 0);
                 if (p.exbits) ex = __ldg(reinterpret_cast<const uint4*>(p.exbits) + t);
@@ -371,8 +400,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     keep[c] = (vc >= 32 ? 0xffffffffu : (vc <= 0 ? 0u : ((1u << vc) - 1u))) & ~exw[c];
                 }
                 if (t == 0) {
-                    // initial threshold: the largest 16-bit key prefix P with >= K selectable
-                    // keys >= P<<16 bounds the row's K-th largest score from below
+                    // initial LB: the largest 16-bit key prefix P with >= K selectable keys
+                    // >= P<<16 bounds the row's K-th best from below; bins span [LB, max]
 #pragma unroll
                     for (int c = 0; c < 4; ++c)
 #pragma unroll
@@ -382,73 +411,51 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 #pragma unroll 1
                     for (int bit = 31; bit >= 16; --bit) {
                         const uint32_t cand = res | (1u << bit);
-                        int n = 0;
+                        int cnt = 0;
 #pragma unroll
                         for (int c = 0; c < 4; ++c)
 #pragma unroll
-                            for (int e = 0; e < 32; ++e) n += sr[c][e] >= cand ? 1 : 0;
-                        if (n >= K) res = cand;
+                            for (int e = 0; e < 32; ++e) cnt += sr[c][e] >= cand ? 1 : 0;
+                        if (cnt >= K) res = cand;
                     }
+                    // back to scores; excluded / out-of-range columns become NaN (never >= thr)
 #pragma unroll
                     for (int c = 0; c < 4; ++c)
 #pragma unroll
                         for (int e = 0; e < 32; ++e) sr[c][e] = __float_as_uint(fkey_inv(sr[c][e]));
-                    if (res != 0) thr = topk_threshold(fkey_inv(res), eps);
+                    if (res != 0) {
+                        tk.lb = fkey_inv(res);
+                        tk.thr = topk_threshold(tk.lb, tk.eps);
+                        const float span = mt - tk.lb;
+                        tk.delta = span > 0.0f ? span * (1.0f / NBIN) : fmaxf(fabsf(tk.lb) * 0.0009765625f, 1e-30f);
+                        tk.inv_delta = 1.0f / tk.delta;
+                    }
                 }
+                const float tq = tk.cnt < 0 ? INFINITY : tk.thr;
 #pragma unroll
                 for (int c = 0; c < 4; ++c) {
-                    const float tq = cnt < 0 ? INFINITY : thr;
-                    uint32_t m = 0;
-                    if (__any_sync(0xffffffffu, cmax[c] >= tq)) {
-                        uint32_t mm[4] = {0u, 0u, 0u, 0u};
+                    if (!__any_sync(0xffffffffu, cmax[c] >= tq)) continue;
+                    uint32_t mm[4] = {0u, 0u, 0u, 0u};
 #pragma unroll
-                        for (int e = 0; e < 32; ++e) mm[e & 3] |= (__uint_as_float(sr[c][e]) >= tq) ? (1u << e) : 0u;
-                        m = ((mm[0] | mm[1]) | (mm[2] | mm[3])) & keep[c];
-                    }
+                    for (int e = 0; e < 32; ++e) mm[e & 3] |= (__uint_as_float(sr[c][e]) >= tq) ? (1u << e) : 0u;
+                    uint32_t m = ((mm[0] | mm[1]) | (mm[2] | mm[3])) & keep[c];
                     while (m) {
                         const int e = __ffs(m) - 1;
                         m &= m - 1;
-                        my_stage[cnt++] = make_float2(select32(sr[c], e), __int_as_float(t * 128 + 32 * c + e));
-                    }
-                    unsigned fl = __ballot_sync(0xffffffffu, cnt > FLUSH_AT);
-                    while (fl) {
-                        const int L = __ffs(fl) - 1;
-                        fl &= fl - 1;
-                        float lt = __shfl_sync(0xffffffffu, thr, L);
-                        const int n2 = flush_stage(sm.stage[32 * qd + L], __shfl_sync(0xffffffffu, cnt, L), K,
-                                                   __shfl_sync(0xffffffffu, eps, L), lt, lane);
-                        if (lane == L) {
-                            thr = lt;
-                            cnt = n2 > FLUSH_AT ? -1 : n2;  // near-tie flood: exact fallback
-                        }
+                        tk.add(select32(sr[c], e), t * 128 + 32 * c + e);
                     }
                 }
+                if (tk.cnt > 0) tk.raise(K);
             }
             __syncwarp();
         }
-        // final flush: tighten every row's threshold with the candidates staged since
-        if (K > 0 && !(p.debug & 1)) {
-            unsigned fl = __ballot_sync(0xffffffffu, cnt > K);
-            while (fl) {
-                const int L = __ffs(fl) - 1;
-                fl &= fl - 1;
-                float lt = __shfl_sync(0xffffffffu, thr, L);
-                const int n2 = flush_stage(sm.stage[32 * qd + L], __shfl_sync(0xffffffffu, cnt, L), K,
-                                           __shfl_sync(0xffffffffu, eps, L), lt, lane);
-                if (lane == L) {
-                    thr = lt;
-                    cnt = n2;
-                }
-            }
-        }
         // ------------------------------- epilogue -------------------------------
-        // the commit after PV(T-1) covers every earlier MMA
-        mbar_wait(&sm.o_done[(T - 1) & 1], (uint32_t)(((T - 1) >> 1) & 1));
+        mbar_wait(&sm.o_final[w], 0);
         __syncwarp();
         tc_fence_after();
         uint32_t o[2][32];
-        tmem_ld_32x32b_x32(lane_base + O_COL, o[0]);
-        tmem_ld_32x32b_x32(lane_base + O_COL + 32, o[1]);
+        tmem_ld_32x32b_x32(o_base, o[0]);
+        tmem_ld_32x32b_x32(o_base + 32, o[1]);
         tmem_wait_ld();
         if (row_ok) {
             const float inv = 1.0f / l;
@@ -460,56 +467,91 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     *reinterpret_cast<float4*>(dst + 32 * half + e) =
                         make_float4(__uint_as_float(o[half][e]) * inv, __uint_as_float(o[half][e + 1]) * inv,
                                     __uint_as_float(o[half][e + 2]) * inv, __uint_as_float(o[half][e + 3]) * inv);
-            if (p.lse) p.lse[(int64_t)h * p.Wq + grow] = m_used * p.scale + logf(l);
-            const int64_t r = (int64_t)h * p.Wq + grow;
+            if (p.lse) p.lse[r] = m_used * p.scale + logf(l);
             if (K > 0) {
-                float2* cd = p.cand + r * CAND;
-                int n = 0;
-                for (int i = 0; i < cnt; ++i) {
-                    const float2 c = my_stage[i];
-                    if (c.x >= thr) {
-                        if (n == CAND) {
-                            cnt = -1;  // more near-ties than the re-score takes: exact fallback
-                            break;
-                        }
-                        cd[n++] = c;
-                    }
-                }
-                p.cand_n[r] = cnt < 0 ? 0 : n;
+                p.cand_n[r] = tk.cnt < 0 ? 0 : tk.cnt;
+                p.flag[r] = (tk.cnt < 0 || (p.debug & 16)) ? 1 : 0;
             }
-            p.flag[r] = (K > 0 && (cnt < 0 || (p.debug & 16))) ? 1 : 0;
         }
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == 1) {
+    if (warp == 9) {
         tc_fence_after();
         tmem_dealloc(tmem, TMEM_COLS);
     }
 }
 
-// Exact re-score of the candidates and final ordering. One warp per row; lane
-// i owns candidates i and i+32. scaled_dot order (dot.hpp:11-23) without FMA.
+// Exact top-k of one row from its streamed candidates. One warp per row:
+//  1. the K-th best APPROXIMATE score tau_a by a 32-step radix select over the
+//     candidates' order-preserving keys (<= CCAP, 16 per lane);
+//  2. the candidates within the error margin of tau_a (a superset of the true
+//     top-k: |approx - exact| <= eps) — at most CAND, else the row is flagged
+//     for the exact CUDA-core recompute;
+//  3. exact scaled_dot (dot.hpp:11-23 order, no FMA) for those, rank by
+//     (score desc, index asc) = topk_better (compression.hpp:67-73).
 // Query rows index [H][Wq], key windows [H][Wk] (Wq < Wk for a view shard).
-__global__ void rescore_kernel(const float* __restrict__ qc, int64_t q_hs, const float* __restrict__ kc, int heads,
-                               int Wq, int Wk, float scale, int k_eff, const float2* __restrict__ cand,
-                               const int* __restrict__ cand_n, const uint8_t* __restrict__ flag, int32_t* topk,
-                               float* guide) {
+__global__ void __launch_bounds__(256) rescore_kernel(const float* __restrict__ qc, int64_t q_hs,
+                                                      const float* __restrict__ kc, int heads, int Wq, int Wk,
+                                                      float scale, int k_eff, const float* __restrict__ qnorm,
+                                                      const float* __restrict__ kmax, const float2* __restrict__ cand,
+                                                      const int* __restrict__ cand_n, uint8_t* flag, int32_t* topk,
+                                                      float* guide) {
+    constexpr int PER = CCAP / 32;
     const int64_t r = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
     const int lane = threadIdx.x & 31;
     if (r >= (int64_t)heads * Wq || flag[r]) return;
     const int h = (int)(r / Wq);
-    const float* q = qc + (int64_t)h * q_hs + (r - (int64_t)h * Wq) * 64;
-    const int cnt = cand_n[r];
-    float e[2];
-    int idx[2];
+    const int n = min(cand_n[r], CCAP);
+    const float2* cr = cand + r * CCAP;
+    float2 cv[PER];
+    uint32_t key[PER];
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+        const int j = lane + 32 * i;
+        cv[i] = j < n ? cr[j] : make_float2(-INFINITY, __int_as_float(-1));
+        key[i] = j < n ? fkey(cv[i].x) : 0u;
+    }
+    uint32_t res = 0;
+#pragma unroll 1
+    for (int bit = 31; bit >= 0; --bit) {
+        const uint32_t c = res | (1u << bit);
+        int cnt = 0;
+#pragma unroll
+        for (int i = 0; i < PER; ++i) cnt += key[i] >= c ? 1 : 0;
+        if ((int)__reduce_add_sync(0xffffffffu, (unsigned)cnt) >= k_eff) res = c;
+    }
+    const float eps = EPS_REL * qnorm[r] * kmax[h];
+    const float thr = topk_threshold(fkey_inv(res), eps);
+    // compact the survivors (through shared memory) into two slots per lane
+    __shared__ float2 surv[8][CAND];
+    float2* sv = surv[threadIdx.x / 32];
+    int total = 0;
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+        const bool keep = key[i] != 0u && cv[i].x >= thr;
+        const unsigned b = __ballot_sync(0xffffffffu, keep);
+        const int pos = total + __popc(b & ((1u << lane) - 1u));
+        if (keep && pos < CAND) sv[pos] = cv[i];
+        total += __popc(b);
+    }
+    __syncwarp();
+    float e[2] = {-INFINITY, -INFINITY};
+    int idx[2] = {-1, -1};
 #pragma unroll
     for (int s = 0; s < 2; ++s) {
-        const int i = lane + 32 * s;
-        e[s] = -INFINITY;
-        idx[s] = -1;
-        if (i < cnt) {
-            idx[s] = __float_as_int(cand[r * CAND + i].y);
+        const int j = lane + 32 * s;
+        if (j < total && j < CAND) idx[s] = __float_as_int(sv[j].y);
+    }
+    if (total > CAND) {
+        if (lane == 0) flag[r] = 1;  // near-tie flood: the exact kernel redoes this row
+        return;
+    }
+    // exact re-score of the survivors
+    const float* q = qc + (int64_t)h * q_hs + (r - (int64_t)h * Wq) * 64;
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+        if (idx[s] >= 0) {
             const float* k = kc + ((int64_t)h * Wk + idx[s]) * 64;
             ExactDot4 d;
             d.zero();
@@ -522,9 +564,9 @@ __global__ void rescore_kernel(const float* __restrict__ qc, int64_t q_hs, const
             e[s] = d.finish(scale);
         }
     }
-    // rank = number of candidates strictly better under topk_better
+    // rank = number of survivors strictly better under topk_better
     int rank[2] = {0, 0};
-    for (int j = 0; j < cnt; ++j) {
+    for (int j = 0; j < total; ++j) {
         const float ej = __shfl_sync(0xffffffffu, e[j >> 5], j & 31);
         const int ij = __shfl_sync(0xffffffffu, idx[j >> 5], j & 31);
 #pragma unroll
@@ -635,7 +677,7 @@ Ws carve_ws(void* base, int heads, int Wq, int Wk, bool dry) {
     w.kn = reinterpret_cast<float*>(take(nk * 4));
     w.kmax = reinterpret_cast<float*>(take((size_t)heads * 4));
     w.exbits = reinterpret_cast<uint32_t*>(take((size_t)((Wk + 127) / 128) * 16));
-    w.cand = reinterpret_cast<float2*>(take(nq * CAND * 8));
+    w.cand = reinterpret_cast<float2*>(take(nq * CCAP * 8));
     w.cand_n = reinterpret_cast<int*>(take(nq * 4));
     w.flag = reinterpret_cast<uint8_t*>(take(nq));
     w.blocks = reinterpret_cast<int*>(take((size_t)heads * ((Wq + 63) / 64) * 4));
@@ -754,13 +796,14 @@ cudaError_t tc_compress_topk_splits(const CompressSplits* pre, const gsa_tensor&
     const size_t smem = sizeof(CompSmem) + 1024;
     cudaError_t e = cudaFuncSetAttribute(compress_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    compress_tc_kernel<<<dim3((Wq + 127) / 128, H), NTHREADS, smem, st>>>(tqh, tql, tkh, tkl, tvh, tvl, p);
+    compress_tc_kernel<<<dim3((Wq + 128 * NWG - 1) / (128 * NWG), H), NTHREADS, smem, st>>>(tqh, tql, tkh, tkl, tvh, tvl, p);
     note_launch();
     if (k_eff > 0) {
         const int64_t rows = (int64_t)H * Wq;
         rescore_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(static_cast<const float*>(qc.data), qc.head_stride,
                                                                    static_cast<const float*>(kc.data), H, Wq, Wk, scale,
-                                                                   k_eff, w.cand, w.cand_n, w.flag, topk, guide);
+                                                                   k_eff, qn, w.kmax, w.cand, w.cand_n, w.flag, topk,
+                                                                   guide);
         note_launch();
         // rows whose near-tie side list overflowed: exact recompute of their 64-row blocks
         cudaMemsetAsync(w.nblocks, 0, sizeof(int), st);
