@@ -22,7 +22,9 @@
 // flagged and recomputed by the exact CUDA-core kernel (attn_f32.cu).
 #include <cuda.h>
 
+#include <cstdio>
 #include <cstdlib>
+#include <vector>
 
 #include "tc.h"
 #include "tc_ptx.cuh"
@@ -149,6 +151,16 @@ struct RowTopk {
         const uint64_t s = h >> (8 * j);
         hist[0] = (uint32_t)s;
         hist[1] = (uint32_t)(s >> 32);
+        if (j == NBIN - 1) {
+            // LB climbed the whole histogram in one tile: the bins are too fine. Double
+            // them; merged counts stay lower bounds (new bin b holds old bins 2b, 2b+1,
+            // all >= lb + b * 2 delta; the open-ended old bin 7 lands in new bin 3)
+            const uint32_t ev = __byte_perm(hist[0], hist[1], 0x6420), od = __byte_perm(hist[0], hist[1], 0x7531);
+            hist[0] = __vaddus4(ev, od);
+            hist[1] = 0u;
+            delta *= 2.0f;
+            inv_delta *= 0.5f;
+        }
     }
 };
 
@@ -366,24 +378,32 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 }
             }
             const float mc = m_used * p.c2;
-            float lsum[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+            // P = exp2(S*c2 - m*c2), split P = hi + lo with hi = P truncated to bf16
+            // (one PRMT packs two his; lo = P - hi is exact in f32, then rounded:
+            // |P - hi - lo| <= 2^-15 |P|); paired f32 ops (FFMA2/FADD2) halve the ALU work
+            const float2 c2v = make_float2(p.c2, p.c2), nmc = make_float2(-mc, -mc);
+            const float2 neg1 = make_float2(-1.0f, -1.0f);
+            float2 lsum2[2] = {make_float2(0.0f, 0.0f), make_float2(0.0f, 0.0f)};
 #pragma unroll
             for (int c = 0; c < 4; ++c) {
                 uint32_t hi[16], lo[16];
 #pragma unroll
                 for (int e2 = 0; e2 < 16; ++e2) {
-                    const float x0 = __uint_as_float(sr[c][2 * e2]), x1 = __uint_as_float(sr[c][2 * e2 + 1]);
-                    const float p0 = ex2_approx(fmaf(x0, p.c2, -mc));
-                    const float p1 = ex2_approx(fmaf(x1, p.c2, -mc));
-                    lsum[e2 & 3] += p0 + p1;
-                    hi[e2] = pack_bf16(p0, p1);
-                    const __nv_bfloat162 hb = *reinterpret_cast<const __nv_bfloat162*>(&hi[e2]);
-                    lo[e2] = pack_bf16(p0 - __low2float(hb), p1 - __high2float(hb));
+                    const float2 x = make_float2(__uint_as_float(sr[c][2 * e2]), __uint_as_float(sr[c][2 * e2 + 1]));
+                    const float2 a = __ffma2_rn(x, c2v, nmc);
+                    const float2 pv = make_float2(ex2_approx(a.x), ex2_approx(a.y));
+                    lsum2[e2 & 1] = __fadd2_rn(lsum2[e2 & 1], pv);
+                    const uint32_t u0 = __float_as_uint(pv.x), u1 = __float_as_uint(pv.y);
+                    hi[e2] = __byte_perm(u0, u1, 0x7632);
+                    const float2 hf = make_float2(__uint_as_float(u0 & 0xffff0000u), __uint_as_float(u1 & 0xffff0000u));
+                    const float2 lf = __ffma2_rn(hf, neg1, pv);
+                    lo[e2] = pack_bf16(lf.x, lf.y);
                 }
                 tmem_st_32x32b_x16(s_base + 32 * c, hi);
                 tmem_st_32x32b_x16(s_base + 32 * c + 16, lo);
             }
-            l += (lsum[0] + lsum[1]) + (lsum[2] + lsum[3]);
+            const float2 ls = __fadd2_rn(lsum2[0], lsum2[1]);
+            l += ls.x + ls.y;
             tmem_wait_st();
             tc_fence_before();
             mbar_arrive(&sm.p_full[w][t & 1]);
@@ -424,10 +444,22 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 #pragma unroll
                         for (int e = 0; e < 32; ++e) sr[c][e] = __float_as_uint(fkey_inv(sr[c][e]));
                     if (res != 0) {
+                        // bin width = (std of the row's first 128 scores) / 8: fine enough
+                        // that LB trails the running K-th best by a fraction of the spread
+                        float s1 = 0.0f, s2 = 0.0f;
+#pragma unroll
+                        for (int c = 0; c < 4; ++c)
+#pragma unroll
+                            for (int e = 0; e < 32; ++e) {
+                                const float x = ((keep[c] >> e) & 1u) ? __uint_as_float(sr[c][e]) : 0.0f;
+                                s1 += x;
+                                s2 = fmaf(x, x, s2);
+                            }
+                        const float nk = (float)(__popc(keep[0]) + __popc(keep[1]) + __popc(keep[2]) + __popc(keep[3]));
+                        const float mean = s1 / nk, var = fmaxf(s2 / nk - mean * mean, 0.0f);
                         tk.lb = fkey_inv(res);
                         tk.thr = topk_threshold(tk.lb, tk.eps);
-                        const float span = mt - tk.lb;
-                        tk.delta = span > 0.0f ? span * (1.0f / NBIN) : fmaxf(fabsf(tk.lb) * 0.0009765625f, 1e-30f);
+                        tk.delta = var > 0.0f ? sqrtf(var) * (1.0f / NBIN) : fmaxf(fabsf(tk.lb) * 0.0009765625f, 1e-30f);
                         tk.inv_delta = 1.0f / tk.delta;
                     }
                 }
@@ -435,10 +467,23 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 #pragma unroll
                 for (int c = 0; c < 4; ++c) {
                     if (!__any_sync(0xffffffffu, cmax[c] >= tq)) continue;
-                    uint32_t mm[4] = {0u, 0u, 0u, 0u};
+                    // bit e = (S[e] >= tq): the sign of S - tq (FADD2), gathered by funnel shifts
+                    // from e = 31 down; two interleaved chains of 16
+                    uint32_t mh = 0u, ml = 0u;
+                    const float2 ntq = make_float2(-tq, -tq);
 #pragma unroll
-                    for (int e = 0; e < 32; ++e) mm[e & 3] |= (__uint_as_float(sr[c][e]) >= tq) ? (1u << e) : 0u;
-                    uint32_t m = ((mm[0] | mm[1]) | (mm[2] | mm[3])) & keep[c];
+                    for (int e2 = 15; e2 >= 0; --e2) {
+                        const float2 dd = __fadd2_rn(make_float2(__uint_as_float(sr[c][2 * e2]),
+                                                                 __uint_as_float(sr[c][2 * e2 + 1])), ntq);
+                        if (e2 >= 8) {
+                            mh = __funnelshift_l(__float_as_uint(dd.y), mh, 1);
+                            mh = __funnelshift_l(__float_as_uint(dd.x), mh, 1);
+                        } else {
+                            ml = __funnelshift_l(__float_as_uint(dd.y), ml, 1);
+                            ml = __funnelshift_l(__float_as_uint(dd.x), ml, 1);
+                        }
+                    }
+                    uint32_t m = ~((mh << 16) | (ml & 0xffffu)) & keep[c];
                     while (m) {
                         const int e = __ffs(m) - 1;
                         m &= m - 1;
@@ -634,15 +679,106 @@ __global__ void exbits_kernel(const uint8_t* __restrict__ ex, int W, int words, 
     bits[wd] = v;
 }
 
-// 64-row blocks containing a flagged row -> list for the exact fallback
-__global__ void flag_blocks_kernel(const uint8_t* __restrict__ flag, int heads, int W, int* list, int* count) {
-    const int qtiles = (W + 63) / 64;
-    const int blk = blockIdx.x * blockDim.x + threadIdx.x;
-    if (blk >= heads * qtiles) return;
-    const int h = blk / qtiles, t = blk % qtiles;
-    bool any = false;
-    for (int i = t * 64; i < min(W, t * 64 + 64); ++i) any |= flag[(int64_t)h * W + i] != 0;
-    if (any) list[atomicAdd(count, 1)] = blk;
+// flagged rows (candidate list overflow / near-tie flood) -> list for the exact per-row path
+__global__ void flag_rows_kernel(const uint8_t* __restrict__ flag, int64_t rows, int* list, int* count) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < rows && flag[i]) list[atomicAdd(count, 1)] = (int)i;
+}
+
+constexpr int XR_THREADS = 256;
+constexpr int XR_CTAS = 296;
+
+__device__ __forceinline__ int block_sum(int v, int* red) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x / 32] = v;
+    __syncthreads();
+    int s = 0;
+#pragma unroll
+    for (int i = 0; i < XR_THREADS / 32; ++i) s += red[i];
+    return s;
+}
+
+// Exact top-k of a flagged row from scratch (fused_compressed_attention_topk's
+// contract, compression.hpp:259-275): every guide score in the scaled_dot
+// order (dot.hpp:11-23, no FMA), the exact K-th largest by a radix select over
+// order-preserving keys, then all scores above it plus the lowest-index ties
+// at it (topk_better: equal scores go to the lower index), ranked. Persistent
+// CTAs over the flagged-row list; the row's keys live in a per-CTA scratch.
+__global__ void __launch_bounds__(XR_THREADS) exact_row_kernel(const float* __restrict__ qc, int64_t q_hs,
+                                                               const float* __restrict__ kc, int Wq, int Wk,
+                                                               float scale, int k_eff, const uint32_t* __restrict__ exbits,
+                                                               const int* __restrict__ list, const int* __restrict__ count,
+                                                               uint32_t* scratch, int32_t* topk, float* guide) {
+    __shared__ float qs[64];
+    __shared__ int red[XR_THREADS / 32];
+    __shared__ float sel_s[128];
+    __shared__ int sel_i[128];
+    __shared__ int nsel;
+    uint32_t* keys = scratch + (size_t)blockIdx.x * Wk;
+    const int n_rows = *count;
+    for (int li = blockIdx.x; li < n_rows; li += gridDim.x) {
+        const int64_t r = list[li];
+        const int h = (int)(r / Wq);
+        const float* q = qc + (int64_t)h * q_hs + (r - (int64_t)h * Wq) * 64;
+        __syncthreads();
+        if (threadIdx.x < 64) qs[threadIdx.x] = q[threadIdx.x];
+        if (threadIdx.x == 0) nsel = 0;
+        __syncthreads();
+        for (int j = threadIdx.x; j < Wk; j += XR_THREADS) {
+            const bool ex = exbits && ((exbits[j >> 5] >> (j & 31)) & 1u);
+            keys[j] = ex ? 0u : fkey(exact_scaled_dot(qs, kc + ((int64_t)h * Wk + j) * 64, 64, scale));
+        }
+        __syncthreads();
+        uint32_t res = 0;
+        for (int bit = 31; bit >= 0; --bit) {
+            const uint32_t cand = res | (1u << bit);
+            int c = 0;
+            for (int j = threadIdx.x; j < Wk; j += XR_THREADS) c += keys[j] >= cand ? 1 : 0;
+            if (block_sum(c, red) >= k_eff) res = cand;
+        }
+        int gt = 0;
+        for (int j = threadIdx.x; j < Wk; j += XR_THREADS) gt += keys[j] > res ? 1 : 0;
+        const int need_eq = k_eff - block_sum(gt, red);
+        // everything above the K-th, then the lowest-index ties at it, in index order
+        int taken_eq = 0;
+        for (int j0 = 0; j0 < Wk; j0 += XR_THREADS) {
+            const int j = j0 + threadIdx.x;
+            const uint32_t kj = j < Wk ? keys[j] : 0u;
+            const bool eq = j < Wk && kj == res && res != 0u;
+            const unsigned b = __ballot_sync(0xffffffffu, eq);
+            __syncthreads();
+            if ((threadIdx.x & 31) == 0) red[threadIdx.x / 32] = __popc(b);
+            __syncthreads();
+            int before = 0, tot = 0;
+            for (int i = 0; i < XR_THREADS / 32; ++i) {
+                before += i < (int)(threadIdx.x / 32) ? red[i] : 0;
+                tot += red[i];
+            }
+            const int rank_eq = taken_eq + before + __popc(b & ((1u << (threadIdx.x & 31)) - 1u));
+            if ((j < Wk && kj > res) || (eq && rank_eq < need_eq)) {
+                const int slot = atomicAdd(&nsel, 1);
+                if (slot < 128) {
+                    sel_s[slot] = fkey_inv(kj);
+                    sel_i[slot] = j;
+                }
+            }
+            taken_eq += tot;
+        }
+        __syncthreads();
+        const int ns = min(nsel, 128);
+        if ((int)threadIdx.x < ns) {
+            const float s = sel_s[threadIdx.x];
+            const int idx = sel_i[threadIdx.x];
+            int rank = 0;
+            for (int i = 0; i < ns; ++i) rank += topk_better(sel_s[i], sel_i[i], s, idx) ? 1 : 0;
+            if (rank < k_eff) {
+                topk[r * k_eff + rank] = idx;
+                if (guide) guide[r * k_eff + rank] = s;
+            }
+        }
+    }
 }
 
 struct Ws {
@@ -654,6 +790,7 @@ struct Ws {
     uint8_t* flag;
     int* blocks;
     int* nblocks;
+    uint32_t* scratch;
     size_t used;
 };
 
@@ -680,8 +817,9 @@ Ws carve_ws(void* base, int heads, int Wq, int Wk, bool dry) {
     w.cand = reinterpret_cast<float2*>(take(nq * CCAP * 8));
     w.cand_n = reinterpret_cast<int*>(take(nq * 4));
     w.flag = reinterpret_cast<uint8_t*>(take(nq));
-    w.blocks = reinterpret_cast<int*>(take((size_t)heads * ((Wq + 63) / 64) * 4));
+    w.blocks = reinterpret_cast<int*>(take(nq * 4));  // flagged rows
     w.nblocks = reinterpret_cast<int*>(take(4));
+    w.scratch = reinterpret_cast<uint32_t*>(take((size_t)XR_CTAS * Wk * 4));
     w.used = off + 256;
     return w;
 }
@@ -805,16 +943,39 @@ cudaError_t tc_compress_topk_splits(const CompressSplits* pre, const gsa_tensor&
                                                                    k_eff, qn, w.kmax, w.cand, w.cand_n, w.flag, topk,
                                                                    guide);
         note_launch();
-        // rows whose near-tie side list overflowed: exact recompute of their 64-row blocks
+        // rows whose candidate list overflowed (near-tie floods): exact recompute per row
         cudaMemsetAsync(w.nblocks, 0, sizeof(int), st);
-        const int nb = H * ((Wq + 63) / 64);
-        flag_blocks_kernel<<<(nb + 127) / 128, 128, 0, st>>>(w.flag, H, Wq, w.blocks, w.nblocks);
-        note_launch();
-        ex.block_list = w.blocks;
-        ex.block_count = w.nblocks;
-        ex.topk_only = true;
-        e = launch_attn_f32(ex, st);
-        if (e != cudaSuccess) return e;
+        flag_rows_kernel<<<(unsigned)((rows + 255) / 256), 256, 0, st>>>(w.flag, rows, w.blocks, w.nblocks);
+        exact_row_kernel<<<XR_CTAS, XR_THREADS, 0, st>>>(static_cast<const float*>(qc.data), qc.head_stride,
+                                                          static_cast<const float*>(kc.data), Wq, Wk, scale, k_eff,
+                                                          excluded ? w.exbits : nullptr, w.blocks, w.nblocks,
+                                                          w.scratch, topk, guide);
+        note_launch(2);
+        if (getenv("GSA_DEBUG_STATS")) {  // bring-up: candidate statistics (synchronises)
+            const int64_t rows = (int64_t)H * Wq;
+            std::vector<int> cn(rows);
+            std::vector<uint8_t> fl(rows);
+            int nblk = 0;
+            cudaMemcpyAsync(cn.data(), w.cand_n, rows * 4, cudaMemcpyDeviceToHost, st);
+            cudaMemcpyAsync(fl.data(), w.flag, rows, cudaMemcpyDeviceToHost, st);
+            cudaMemcpyAsync(&nblk, w.nblocks, 4, cudaMemcpyDeviceToHost, st);
+            cudaStreamSynchronize(st);
+            int64_t sum = 0, mx = 0, nfl = 0, nzero = 0;
+            for (int64_t i = 0; i < rows; ++i) {
+                sum += cn[i];
+                mx = cn[i] > mx ? cn[i] : mx;
+                nfl += fl[i] ? 1 : 0;
+                nzero += cn[i] == 0 ? 1 : 0;
+            }
+            fprintf(stderr, "compress stats: rows %lld mean cand %.1f max %lld flagged %lld zero %lld blocks %d\n",
+                    (long long)rows, (double)sum / rows, (long long)mx, (long long)nfl, (long long)nzero, nblk);
+            int shown = 0;
+            for (int64_t i = 0; i < rows && shown < 8; ++i)
+                if (fl[i]) {
+                    fprintf(stderr, "  flagged row %lld (h %lld, w %lld)\n", (long long)i, (long long)(i / Wq), (long long)(i % Wq));
+                    ++shown;
+                }
+        }
     }
     return cudaGetLastError();
 }
