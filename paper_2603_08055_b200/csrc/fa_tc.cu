@@ -24,22 +24,24 @@ namespace {
 
 using namespace ptx;
 
-constexpr int NS = 6;
-constexpr int TILE = 16384;  // 128 rows x 64 bf16
-constexpr int NTHREADS = 192;
+constexpr int NS = 8;                // K / V ring stages (16 KB each)
+constexpr int TILE = 16384;          // 128 rows x 64 bf16
+constexpr int NTHREADS = 384;        // warps 0-3 / 4-7: softmax WG0 / WG1, 8: TMA, 9: MMA, 10-11 idle
+constexpr int NWG = 2;               // query tiles (softmax warpgroups) per CTA
+constexpr int NSB = 3;               // S/P buffers in TMEM, rotating over the S(n) sequence
 constexpr uint32_t TMEM_COLS = 512;
-constexpr uint32_t O_COL = 384;
+constexpr uint32_t O_COL0 = 384;     // O of WG w: [384 + 64 w, +64); S/P buffer b: [128 b, +128)
 constexpr float RESCALE_LOG2 = 8.0f;
 
 struct __align__(1024) FaSmem {
-    uint8_t q[TILE];
+    uint8_t q[NWG][TILE];
     uint8_t ring[NS][TILE];
     uint64_t full[NS], empty[NS];
     uint64_t q_full;
-    uint64_t s_full[3], s_free[3];
-    // by tile parity: the softmax runs up to a tile ahead of the MMA, and parity waits are
-    // only unambiguous within one phase of their target
-    uint64_t p_full[2], o_done[2];
+    uint64_t s_full[NSB];
+    uint64_t p_full[NWG][2];  // by tile parity: a WG may run one tile ahead of the MMA's P wait
+    uint64_t o_done[NWG];     // every PV of the WG (lazy O rescale waits on it)
+    uint64_t o_final[NWG];
     uint32_t tmem_base;
 };
 
@@ -54,156 +56,175 @@ struct FaParams {
     float* part_lse;  // [splits][H][mq]
 };
 
-__device__ __forceinline__ uint32_t s_col(int b) { return (uint32_t)(128 * b); }
+__device__ __forceinline__ void setmaxnreg_inc() { asm volatile("setmaxnreg.inc.sync.aligned.u32 224;\n" ::: "memory"); }
+__device__ __forceinline__ void setmaxnreg_dec() { asm volatile("setmaxnreg.dec.sync.aligned.u32 56;\n" ::: "memory"); }
 
+// load order = the MMA issuer's first-use order: K0 K1 V0 K2 V1 ... K(T-1) V(T-2) V(T-1)
+__device__ __forceinline__ int seq_k(int t) { return t == 0 ? 0 : 2 * t - 1; }
+__device__ __forceinline__ int seq_v(int t, int T) { return t == T - 1 ? 2 * T - 1 : 2 * t + 2; }
+
+// Dense flash attention, two 128-query tiles per CTA (one softmax warpgroup
+// each) sharing every K/V tile of the CTA's key split:
+//   S(n) = Q_w K(t)^T (bf16, 1 term)             -> TMEM S/P buffer n % 3, n = 2t + w
+//   O_w += P(n) V(t) (P = hi + lo bf16, from TMEM) -> TMEM O_w
+// S(n+3) is issued right after PV(n), ahead of the next P waits, so a warpgroup
+// always has its next scores computing while it runs a softmax.
 __global__ void __launch_bounds__(NTHREADS, 1)
     fa_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                  const __grid_constant__ CUtensorMap tm_v, const FaParams p) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     FaSmem& sm = *reinterpret_cast<FaSmem*>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
     const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
-    const int qt = blockIdx.x, split = blockIdx.y, h = blockIdx.z;
+    const int qp = blockIdx.x, split = blockIdx.y, h = blockIdx.z;
     const int t_begin = split * p.tiles_per_split;
     const int t_end = min(p.kv_tiles, t_begin + p.tiles_per_split);
     const int T = t_end - t_begin;
+    const int N = NWG * T;
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < NS; ++i) {
             mbar_init(&sm.full[i], 1);
             mbar_init(&sm.empty[i], 1);
         }
-        for (int i = 0; i < 3; ++i) {
-            mbar_init(&sm.s_full[i], 1);
-            mbar_init(&sm.s_free[i], 1);
-        }
         mbar_init(&sm.q_full, 1);
-        mbar_init(&sm.p_full[0], 128);
-        mbar_init(&sm.p_full[1], 128);
-        mbar_init(&sm.o_done[0], 1);
-        mbar_init(&sm.o_done[1], 1);
+        for (int b = 0; b < NSB; ++b) mbar_init(&sm.s_full[b], 1);
+        for (int w = 0; w < NWG; ++w) {
+            mbar_init(&sm.p_full[w][0], 128);
+            mbar_init(&sm.p_full[w][1], 128);
+            mbar_init(&sm.o_done[w], 1);
+            mbar_init(&sm.o_final[w], 1);
+        }
         fence_barrier_init();
         prefetch_tmap(&tm_q);
         prefetch_tmap(&tm_k);
         prefetch_tmap(&tm_v);
     }
-    if (warp == 1) tmem_alloc(&sm.tmem_base, TMEM_COLS);
+    if (warp == 9) tmem_alloc(&sm.tmem_base, TMEM_COLS);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = sm.tmem_base;
 
-    if (warp == 0) {
-        if (lane == 0 && T > 0) {
+    if (warp >= 8) {
+        setmaxnreg_dec();
+        if (warp == 8 && T > 0) {
             // ================================ TMA ================================
-            mbar_arrive_expect_tx(&sm.q_full, TILE);
-            tma_load_3d(&sm.q[0], &tm_q, &sm.q_full, 0, qt * 128, h);
-            int st = 0;
-            uint32_t eph = 1;
+            if (elect_one()) {
+                mbar_arrive_expect_tx(&sm.q_full, NWG * TILE);
+                for (int w = 0; w < NWG; ++w) tma_load_3d(&sm.q[w][0], &tm_q, &sm.q_full, 0, (qp * NWG + w) * 128, h);
+            }
+            __syncwarp();
+            int seq = 0;
             auto load = [&](const CUtensorMap* tm, int t) {
-                mbar_wait(&sm.empty[st], eph);
-                mbar_arrive_expect_tx(&sm.full[st], TILE);
-                tma_load_3d(&sm.ring[st][0], tm, &sm.full[st], 0, (t_begin + t) * 128, h);
-                if (++st == NS) {
-                    st = 0;
-                    eph ^= 1;
+                const int st = seq % NS;
+                mbar_wait(&sm.empty[st], (uint32_t)(((seq / NS) & 1) ^ 1));
+                if (elect_one()) {
+                    mbar_arrive_expect_tx(&sm.full[st], TILE);
+                    tma_load_3d(&sm.ring[st][0], tm, &sm.full[st], 0, (t_begin + t) * 128, h);
                 }
+                __syncwarp();
+                ++seq;
             };
             load(&tm_k, 0);
+            if (T > 1) load(&tm_k, 1);
             for (int t = 0; t < T; ++t) {
-                if (t + 1 < T) load(&tm_k, t + 1);
                 load(&tm_v, t);
+                if (t + 2 < T) load(&tm_k, t + 2);
             }
-        }
-    } else if (warp == 1) {
-        if (lane == 0 && T > 0) {
+        } else if (warp == 9 && T > 0) {
             // ================================ MMA ================================
             const uint32_t id_s = idesc_bf16(128, 128, 0, 0);
             const uint32_t id_o = idesc_bf16(128, 64, 0, 1);
-            int st = 0;
-            uint32_t fph = 0;
-            uint32_t freeph[3] = {1, 1, 1};
-            uint32_t pph[2] = {0, 0};
+            auto wait_tile = [&](int s) {
+                mbar_wait(&sm.full[s % NS], (uint32_t)((s / NS) & 1));
+                tc_fence_after();
+            };
+            auto issue_S = [&](int n) {
+                const int w = n & 1, t = n >> 1;
+                const int s = seq_k(t);
+                if (w == 0) wait_tile(s);
+                const uint64_t kd = umma_desc(smem_u32(&sm.ring[s % NS][0]), 16, 1024, 2);
+                const uint64_t qd = umma_desc(smem_u32(&sm.q[w][0]), 16, 1024, 2);
+                const uint32_t d = tmem + 128 * (n % NSB);
+                if (elect_one()) {
+                    for (int ks = 0; ks < 4; ++ks) mma_bf16(d, qd + 2 * ks, kd + 2 * ks, id_s, ks != 0);
+                    mma_commit(&sm.s_full[n % NSB]);
+                    if (w == 1) mma_commit(&sm.empty[s % NS]);
+                }
+                __syncwarp();
+            };
+            auto issue_PV = [&](int n) {
+                const int w = n & 1, t = n >> 1;
+                const int s = seq_v(t, T);
+                if (w == 0) wait_tile(s);
+                mbar_wait(&sm.p_full[w][t & 1], (uint32_t)((t >> 1) & 1));
+                tc_fence_after();
+                const uint64_t vd = umma_desc(smem_u32(&sm.ring[s % NS][0]), 16, 1024, 2);
+                const uint32_t o = tmem + O_COL0 + 64 * w, pb = tmem + 128 * (n % NSB);
+                if (elect_one()) {
+                    for (int ks = 0; ks < 8; ++ks) {
+                        // P hi of keys 16ks..16ks+15: cols 32*(ks/2) + 8*(ks%2); lo 16 columns later
+                        const uint32_t a_hi = pb + 32 * (ks >> 1) + 8 * (ks & 1);
+                        mma_bf16_ts(o, a_hi, vd + 128 * ks, id_o, (t | ks) != 0);
+                        mma_bf16_ts(o, a_hi + 16, vd + 128 * ks, id_o, 1);
+                    }
+                    mma_commit(&sm.o_done[w]);
+                    if (t == T - 1) mma_commit(&sm.o_final[w]);
+                    if (w == 1) mma_commit(&sm.empty[s % NS]);
+                }
+                __syncwarp();
+            };
             mbar_wait(&sm.q_full, 0);
-            const uint64_t qdesc = umma_desc(smem_u32(&sm.q[0]), 16, 1024, 2);
-            auto issue_S = [&](int t) {
-                const int b = t % 3;
-                mbar_wait(&sm.s_free[b], freeph[b]);
-                freeph[b] ^= 1;
-                mbar_wait(&sm.full[st], fph);
-                tc_fence_after();
-                const uint64_t kdesc = umma_desc(smem_u32(&sm.ring[st][0]), 16, 1024, 2);
-                for (int ks = 0; ks < 4; ++ks)
-                    mma_bf16(tmem + s_col(b), qdesc + (uint64_t)(2 * ks), kdesc + (uint64_t)(2 * ks), id_s, ks != 0);
-                mma_commit(&sm.empty[st]);
-                mma_commit(&sm.s_full[b]);
-                if (++st == NS) {
-                    st = 0;
-                    fph ^= 1;
-                }
-            };
-            auto issue_PV = [&](int t) {
-                const int b = t % 3;
-                mbar_wait(&sm.p_full[t & 1], pph[t & 1]);
-                pph[t & 1] ^= 1;
-                mbar_wait(&sm.full[st], fph);
-                tc_fence_after();
-                const uint64_t vdesc = umma_desc(smem_u32(&sm.ring[st][0]), 16, 1024, 2);
-                for (int ks = 0; ks < 8; ++ks) {
-                    // P hi of keys 16ks..16ks+15: TMEM cols 32*(ks/2) + 8*(ks%2); lo 16 columns later
-                    const uint32_t a_hi = tmem + s_col(b) + 32 * (ks >> 1) + 8 * (ks & 1);
-                    const uint64_t vb = vdesc + (uint64_t)(128 * ks);
-                    mma_bf16_ts(tmem + O_COL, a_hi, vb, id_o, (t | ks) != 0);
-                    mma_bf16_ts(tmem + O_COL, a_hi + 16, vb, id_o, 1);
-                }
-                mma_commit(&sm.empty[st]);
-                mma_commit(&sm.s_free[b]);
-                mma_commit(&sm.o_done[t & 1]);
-                if (++st == NS) {
-                    st = 0;
-                    fph ^= 1;
-                }
-            };
-            issue_S(0);
-            for (int t = 0; t < T; ++t) {
-                if (t + 1 < T) issue_S(t + 1);
-                issue_PV(t);
+            tc_fence_after();
+            for (int n = 0; n < min(NSB, N); ++n) issue_S(n);
+            for (int n = 0; n < N; ++n) {
+                issue_PV(n);
+                if (n + NSB < N) issue_S(n + NSB);
             }
         }
     } else if (T > 0) {
-        // ============================ softmax (warps 2..5) ============================
-        const int qd = warp & 3;
+        // ============================ softmax (warps 0..7) ============================
+        setmaxnreg_inc();
+        const int w = warp >> 2, qd = warp & 3;
         const int row = 32 * qd + lane;
         const uint32_t lane_base = tmem + ((uint32_t)(32 * qd) << 16);
+        const uint32_t o_base = lane_base + O_COL0 + 64 * w;
         float m_used = -INFINITY, l = 0.0f;
-        uint32_t sph[3] = {0, 0, 0};
         for (int t = 0; t < T; ++t) {
-            const int b = t % 3;
-            mbar_wait(&sm.s_full[b], sph[b]);
-            sph[b] ^= 1;
+            const int n = 2 * t + w, b = n % NSB;
+            const uint32_t s_base = lane_base + 128 * b;
+            mbar_wait(&sm.s_full[b], (uint32_t)((n / NSB) & 1));
             __syncwarp();  // .sync.aligned tcgen05 ops below need a converged warp
             tc_fence_after();
             uint32_t sr[4][32];
 #pragma unroll
-            for (int c = 0; c < 4; ++c) tmem_ld_32x32b_x32(lane_base + s_col(b) + 32 * c, sr[c]);
+            for (int c = 0; c < 4; ++c) tmem_ld_32x32b_x32(s_base + 32 * c, sr[c]);
             tmem_wait_ld();
             const int valid = p.mk - (t_begin + t) * 128;  // keys of this tile that exist
-            float mt = -INFINITY;
+            if (valid < 128) {
 #pragma unroll
-            for (int c = 0; c < 4; ++c)
+                for (int c = 0; c < 4; ++c)
 #pragma unroll
-                for (int e = 0; e < 32; ++e) {
-                    if (32 * c + e >= valid) sr[c][e] = __float_as_uint(-INFINITY);
-                    mt = fmaxf(mt, __uint_as_float(sr[c][e]));
-                }
+                    for (int e = 0; e < 32; ++e)
+                        if (32 * c + e >= valid) sr[c][e] = __float_as_uint(-INFINITY);
+            }
+            float a0 = __uint_as_float(sr[0][0]), a1 = __uint_as_float(sr[1][0]);
+            float a2 = __uint_as_float(sr[2][0]), a3 = __uint_as_float(sr[3][0]);
+#pragma unroll
+            for (int e = 1; e < 32; ++e) {
+                a0 = fmaxf(a0, __uint_as_float(sr[0][e]));
+                a1 = fmaxf(a1, __uint_as_float(sr[1][e]));
+                a2 = fmaxf(a2, __uint_as_float(sr[2][e]));
+                a3 = fmaxf(a3, __uint_as_float(sr[3][e]));
+            }
+            const float mt = fmaxf(fmaxf(a0, a1), fmaxf(a2, a3));
             if (t == 0) {
                 m_used = mt;
             } else {
                 const bool need = (mt - m_used) * p.c2 > RESCALE_LOG2;
                 if (__any_sync(0xffffffffu, need)) {
-                    // rescale O (TMEM) and l once PV(t-1) has landed.
-                    // PV(t-1) done: completion #((t-1)>>1) of o_done[(t-1)&1]; PV(t-3) is already
-                    // implied by s_full(t) and PV(t+1) cannot have run, so this parity is exact
-                    mbar_wait(&sm.o_done[(t - 1) & 1], (uint32_t)(((t - 1) >> 1) & 1));
+                    // O must hold every tile < t: PV_w(t-1) done = o_done[w] phase t-1
+                    mbar_wait(&sm.o_done[w], (uint32_t)((t - 1) & 1));
                     __syncwarp();
                     tc_fence_after();
                     const float mnew = need ? mt : m_used;
@@ -211,11 +232,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     uint32_t o[32];
 #pragma unroll
                     for (int half = 0; half < 2; ++half) {
-                        tmem_ld_32x32b_x32(lane_base + O_COL + 32 * half, o);
+                        tmem_ld_32x32b_x32(o_base + 32 * half, o);
                         tmem_wait_ld();
 #pragma unroll
                         for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * f);
-                        tmem_st_32x32b_x32(lane_base + O_COL + 32 * half, o);
+                        tmem_st_32x32b_x32(o_base + 32 * half, o);
                     }
                     tmem_wait_st();
                     l *= f;
@@ -223,38 +244,43 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 }
             }
             const float mc = m_used * p.c2;
-            float ls = 0.0f;
+            // P = hi + lo with hi = P truncated to bf16 (PRMT packs two), lo = P - hi rounded
+            const float2 c2v = make_float2(p.c2, p.c2), nmc = make_float2(-mc, -mc);
+            const float2 neg1 = make_float2(-1.0f, -1.0f);
+            float2 lsum2[2] = {make_float2(0.0f, 0.0f), make_float2(0.0f, 0.0f)};
 #pragma unroll
             for (int c = 0; c < 4; ++c) {
                 uint32_t hi[16], lo[16];
 #pragma unroll
                 for (int e2 = 0; e2 < 16; ++e2) {
-                    const float x0 = __uint_as_float(sr[c][2 * e2]), x1 = __uint_as_float(sr[c][2 * e2 + 1]);
-                    const float p0 = ex2_approx(fmaf(x0, p.c2, -mc));
-                    const float p1 = ex2_approx(fmaf(x1, p.c2, -mc));
-                    ls += p0 + p1;
-                    hi[e2] = pack_bf16(p0, p1);
-                    const __nv_bfloat162 hb = *reinterpret_cast<const __nv_bfloat162*>(&hi[e2]);
-                    lo[e2] = pack_bf16(p0 - __low2float(hb), p1 - __high2float(hb));
+                    const float2 x = make_float2(__uint_as_float(sr[c][2 * e2]), __uint_as_float(sr[c][2 * e2 + 1]));
+                    const float2 a = __ffma2_rn(x, c2v, nmc);
+                    const float2 pv = make_float2(ex2_approx(a.x), ex2_approx(a.y));
+                    lsum2[e2 & 1] = __fadd2_rn(lsum2[e2 & 1], pv);
+                    const uint32_t u0 = __float_as_uint(pv.x), u1 = __float_as_uint(pv.y);
+                    hi[e2] = __byte_perm(u0, u1, 0x7632);
+                    const float2 hf = make_float2(__uint_as_float(u0 & 0xffff0000u), __uint_as_float(u1 & 0xffff0000u));
+                    const float2 lf = __ffma2_rn(hf, neg1, pv);
+                    lo[e2] = pack_bf16(lf.x, lf.y);
                 }
-                tmem_st_32x32b_x16(lane_base + s_col(b) + 32 * c, hi);
-                tmem_st_32x32b_x16(lane_base + s_col(b) + 32 * c + 16, lo);
+                tmem_st_32x32b_x16(s_base + 32 * c, hi);
+                tmem_st_32x32b_x16(s_base + 32 * c + 16, lo);
             }
-            l += ls;
+            const float2 ls = __fadd2_rn(lsum2[0], lsum2[1]);
+            l += ls.x + ls.y;
             tmem_wait_st();
             tc_fence_before();
-            mbar_arrive(&sm.p_full[t & 1]);
+            mbar_arrive(&sm.p_full[w][t & 1]);
         }
         // ------------------------------- epilogue -------------------------------
-        // the commit after PV(T-1) covers every earlier MMA
-        mbar_wait(&sm.o_done[(T - 1) & 1], (uint32_t)(((T - 1) >> 1) & 1));
+        mbar_wait(&sm.o_final[w], 0);
         __syncwarp();
         tc_fence_after();
         uint32_t o[2][32];
-        tmem_ld_32x32b_x32(lane_base + O_COL, o[0]);
-        tmem_ld_32x32b_x32(lane_base + O_COL + 32, o[1]);
+        tmem_ld_32x32b_x32(o_base, o[0]);
+        tmem_ld_32x32b_x32(o_base + 32, o[1]);
         tmem_wait_ld();
-        const int qrow = qt * 128 + row;
+        const int qrow = (qp * NWG + w) * 128 + row;
         if (qrow < p.mq) {
             const float inv = 1.0f / l;
             const float lse = m_used * p.scale + logf(l);
@@ -278,7 +304,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == 1) {
+    if (warp == 9) {
         tc_fence_after();
         tmem_dealloc(tmem, TMEM_COLS);
     }
@@ -354,10 +380,16 @@ bool tc_dense_supported(const gsa_tensor& q, const gsa_tensor& k, const gsa_tens
     return rows_ok(q) && rows_ok(k) && rows_ok(v) && encode_fn() != nullptr;
 }
 
-size_t tc_dense_workspace_bytes(int heads, int mq, int mk) {
-    const int qtiles = (mq + 127) / 128, kv_tiles = (mk + 127) / 128;
+// key splits: enough CTAs for ~8 waves of 148 SMs while each split keeps >= 16 key tiles
+int fa_splits(int qpairs, int heads, int kv_tiles) {
     int splits = 1;
-    while (qtiles * heads * splits < 2 * 148 && kv_tiles / (splits * 2) >= 4) splits *= 2;
+    while (qpairs * heads * splits < 8 * 148 && kv_tiles / (splits * 2) >= 16) splits *= 2;
+    return splits;
+}
+
+size_t tc_dense_workspace_bytes(int heads, int mq, int mk) {
+    const int qpairs = (mq + 255) / 256, kv_tiles = (mk + 127) / 128;
+    const int splits = fa_splits(qpairs, heads, kv_tiles);
     if (splits == 1) return 0;
     return (size_t)splits * heads * mq * 65 * sizeof(float) + 256;
 }
@@ -379,9 +411,8 @@ cudaError_t tc_dense_attention(const gsa_tensor& q, const gsa_tensor& k, const g
     p.scale = scale;
     p.c2 = scale * 1.4426950408889634f;
     p.kv_tiles = (k.rows + 127) / 128;
-    const int qtiles = (mq + 127) / 128;
-    int splits = 1;
-    while (qtiles * q.heads * splits < 2 * 148 && p.kv_tiles / (splits * 2) >= 4) splits *= 2;
+    const int qpairs = (mq + 255) / 256;
+    int splits = fa_splits(qpairs, q.heads, p.kv_tiles);
     // split-KV needs caller workspace for the partials; without it run unsplit
     if (splits > 1 && (!ws || ws_bytes < (size_t)splits * q.heads * mq * 65 * sizeof(float))) splits = 1;
     p.tiles_per_split = (p.kv_tiles + splits - 1) / splits;
@@ -397,7 +428,7 @@ cudaError_t tc_dense_attention(const gsa_tensor& q, const gsa_tensor& k, const g
     const size_t smem = sizeof(FaSmem) + 1024;
     cudaError_t e = cudaFuncSetAttribute(fa_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    dim3 grid(qtiles, p.splits, q.heads);
+    dim3 grid(qpairs, p.splits, q.heads);
     fa_tc_kernel<<<grid, NTHREADS, smem, st>>>(tq, tk, tv, p);
     note_launch();
     if (p.splits > 1) {
