@@ -44,7 +44,8 @@ constexpr int WIN = 2048;                // 16 tokens x 64 bf16
 constexpr int NTHREADS = 192;
 constexpr uint32_t TMEM_COLS = 256;
 constexpr uint32_t S_COL0 = 0, S_COL1 = 64, O_COL0 = 128, O_COL1 = 144, G_COL0 = 160, G_COL1 = 176;
-constexpr int GROUP_WIN = 32;            // windows per softmax group (512 keys)
+constexpr int GROUP_WIN = 32;
+constexpr int PREFETCH_AHEAD = 0;   // items of L2 prefetch ahead of the gathers (2 measured slower: 54 -> 71 ms)            // windows per softmax group (512 keys)
 
 struct __align__(1024) SelSmem {
     uint8_t ring[NS][STAGE];
@@ -199,6 +200,21 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             const int my_wid = lane < nw ? p.rows.window(it.item, (int64_t)it.g * GROUP_WIN + lane) : 0;
             int c1, c2;
             window_coords(L, my_wid, c1, c2);
+            if (PREFETCH_AHEAD > 0 && tm == &tm_k && it.g == 0) {
+                // warm L2 with the K and V windows of the item PREFETCH_AHEAD items ahead: the
+                // ring holds about one item, so without this every item pays a DRAM round trip
+                const int64_t pi = it.item + (int64_t)PREFETCH_AHEAD * gridDim.x;
+                if (pi < p.items) {
+                    const int ph = (int)(pi / L.windows);
+                    const int64_t pn = p.rows.size(pi);
+                    for (int64_t j = lane; j < pn; j += 32) {
+                        int d1, d2;
+                        window_coords(L, p.rows.window(pi, j), d1, d2);
+                        tma_prefetch_4d(&tm_k, 0, d1, d2, ph);
+                        tma_prefetch_4d(&tm_v, 0, d1, d2, ph);
+                    }
+                }
+            }
             for (int c0 = 0; c0 < nw; c0 += 8) {
                 const int nc = min(8, nw - c0);
                 mbar_wait(&sm.empty[st], eph);
@@ -229,8 +245,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         }
     } else if (warp == 1) {
         // ================================ MMA issuer ===============================
-        // Stream order: S(0); then per group j: S(j+1) (look-ahead), PV(j).
-        if (lane == 0) {
+        // Stream order: S(0); then per group j: S(j+1) (look-ahead), PV(j). The whole
+        // warp walks the stream (uniform descriptors); one elected lane issues.
+        {
             const uint32_t id_s = idesc_bf16(128, 16, 0, 0);
             const uint32_t id_o = idesc_bf16(64, 16, 1, 0);
             int st = 0;
@@ -257,14 +274,18 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     gph[gb] ^= 1;
                     tc_fence_after();
                     const uint32_t gcol = tmem + (gb ? G_COL1 : G_COL0);
-                    for (int part = 0; part < 2; ++part)
-                        for (int ks = 0; ks < 4; ++ks)
-                            mma_bf16(gcol, umma_desc(smem_u32(&sm.wg[part][0]) + ks * 2048, 16, 1024, 2),
-                                     umma_desc(smem_u32(&sm.q[qb][0]) + ks * 32, 16, 1024, 2), id_o,
-                                     (part | ks) != 0);
                     // the last item of this head on this CTA releases W_g
                     const int64_t nxt = it.item + gridDim.x;
-                    if (nxt >= p.items || (int)(nxt / L.windows) != h) mma_commit(&sm.wg_empty);
+                    const bool last_of_head = nxt >= p.items || (int)(nxt / L.windows) != h;
+                    if (elect_one()) {
+                        for (int part = 0; part < 2; ++part)
+                            for (int ks = 0; ks < 4; ++ks)
+                                mma_bf16(gcol, umma_desc(smem_u32(&sm.wg[part][0]) + ks * 2048, 16, 1024, 2),
+                                         umma_desc(smem_u32(&sm.q[qb][0]) + ks * 32, 16, 1024, 2), id_o,
+                                         (part | ks) != 0);
+                        if (last_of_head) mma_commit(&sm.wg_empty);
+                    }
+                    __syncwarp();
                     ++n_items;
                 }
                 const int sb = (int)(jS & 1);
@@ -278,16 +299,23 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     mbar_wait(&sm.full[st], fph);
                     tc_fence_after();
                     const uint64_t kdesc = umma_desc(smem_u32(&sm.ring[st][0]), 16, 1024, 2);
-                    for (int ks = 0; ks < 4; ++ks)
-                        mma_bf16(scol + 16 * c, kdesc + (uint64_t)(ks * 2), qdesc + (uint64_t)(ks * 2), id_s, ks != 0);
-                    mma_commit(&sm.empty[st]);
+                    if (elect_one()) {
+                        for (int ks = 0; ks < 4; ++ks)
+                            mma_bf16(scol + 16 * c, kdesc + (uint64_t)(ks * 2), qdesc + (uint64_t)(ks * 2), id_s,
+                                     ks != 0);
+                        mma_commit(&sm.empty[st]);
+                    }
+                    __syncwarp();
                     if (++st == NS) {
                         st = 0;
                         fph ^= 1;
                     }
                 }
-                mma_commit(&sm.s_full[sb]);
-                if (it.g == it.ng - 1) mma_commit(&sm.q_empty[qb]);
+                if (elect_one()) {
+                    mma_commit(&sm.s_full[sb]);
+                    if (it.g == it.ng - 1) mma_commit(&sm.q_empty[qb]);
+                }
+                __syncwarp();
                 ++jS;
             };
             auto issue_PV = [&](const GroupIt& it) {
@@ -304,19 +332,23 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     tc_fence_after();
                     const uint64_t vdesc = umma_desc(smem_u32(&sm.ring[st][0]), 16, 1024, 2);
                     // descriptor start addresses are in 16-byte units
-                    for (int ks = 0; ks < 8; ++ks) {
-                        const uint64_t va = vdesc + (uint64_t)(ks * 128);
-                        const uint64_t po = (uint64_t)(c * 128 + ks * 16);
-                        mma_bf16(ocol, va, phi + po, id_o, (c | ks) != 0);
-                        mma_bf16(ocol, va, plo + po, id_o, 1);
+                    if (elect_one()) {
+                        for (int ks = 0; ks < 8; ++ks) {
+                            const uint64_t va = vdesc + (uint64_t)(ks * 128);
+                            const uint64_t po = (uint64_t)(c * 128 + ks * 16);
+                            mma_bf16(ocol, va, phi + po, id_o, (c | ks) != 0);
+                            mma_bf16(ocol, va, plo + po, id_o, 1);
+                        }
+                        mma_commit(&sm.empty[st]);
                     }
-                    mma_commit(&sm.empty[st]);
+                    __syncwarp();
                     if (++st == NS) {
                         st = 0;
                         fph ^= 1;
                     }
                 }
-                mma_commit(&sm.o_full[pb]);
+                if (elect_one()) mma_commit(&sm.o_full[pb]);
+                __syncwarp();
                 ++jP;
             };
             GroupIt kit, vit;
