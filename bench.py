@@ -318,12 +318,14 @@ def main():
             hout = torch.empty(out.shape, dtype=torch.float32).pin_memory()
             dq, dk, dv = (torch.empty_like(x) for x in (q, k, v))
 
+            del dq, dk, dv
+            dq = dk = dv = None
+            # host -> host through the public API, pipelined over head groups
+            # (H2D of group g+1 and D2H of group g-1 overlap the layer on group g)
+            pipe = gsa.HostPipeline(heads_per_group=4, device=dev)
+
             def e2e_step():
-                dq.copy_(hq, non_blocking=True)
-                dk.copy_(hk, non_blocking=True)
-                dv.copy_(hv, non_blocking=True)
-                gsa.gsa_forward(dq, dk, dv, wg, L, params, out=out, workspace=ws)
-                hout.copy_(out, non_blocking=True)
+                pipe.forward(hq, hk, hv, wg, L, params, hout)
             h2d, d2h = 3 * q.numel() * 2, out.numel() * 4
         else:
             hq = q_own.cpu().pin_memory()

@@ -20,7 +20,7 @@ def build(jobs: int = 8) -> str:
 
 
 from .gsa import (  # noqa: E402
-    HYBRID, PLAIN, CompressedResult, DivisibilityError, EmptySelection, ForwardContext, GsaError, GsaParams,
+    HostPipeline, HYBRID, PLAIN, CompressedResult, DivisibilityError, EmptySelection, ForwardContext, GsaError, GsaParams,
     IndexOutOfRange, InvalidStride, InvalidTiling, KernelTiling, NonFiniteInput, SelectionPlan, ShapeMismatch,
     TokenLayout, Unsupported, Workspace, ZeroSizeError, avg_pool_tokens, block_sparse_attention, build_selection_plan,
     build_token_layout, forced_windows_of, forward_stats, fused_compressed_attention_topk, gate, gsa_forward,
@@ -28,7 +28,7 @@ from .gsa import (  # noqa: E402
 )
 
 __all__ = [
-    "build", "HYBRID", "PLAIN", "CompressedResult", "DivisibilityError", "EmptySelection", "ForwardContext",
+    "build", "HostPipeline", "HYBRID", "PLAIN", "CompressedResult", "DivisibilityError", "EmptySelection", "ForwardContext",
     "GsaError", "GsaParams", "IndexOutOfRange", "InvalidStride", "InvalidTiling", "KernelTiling", "NonFiniteInput",
     "SelectionPlan", "ShapeMismatch", "TokenLayout", "Unsupported", "Workspace", "ZeroSizeError", "avg_pool_tokens",
     "block_sparse_attention", "build_selection_plan", "build_token_layout", "forced_windows_of", "forward_stats",

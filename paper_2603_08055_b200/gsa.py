@@ -458,3 +458,74 @@ def project_qkv(x: torch.Tensor, w_q: torch.Tensor, w_k: torch.Tensor, w_v: torc
     _check(L.gsa_project_qkv(_ptr(x), T, Cm, _ptr(w_q), _ptr(w_k), _ptr(w_v), H, d, C.byref(_desc(outs[0])),
                              C.byref(_desc(outs[1])), C.byref(_desc(outs[2])), _stream()))
     return tuple(outs)
+
+
+class HostPipeline:
+    """gsa_forward from HOST (pinned) Q/K/V to a HOST output, pipelined over head
+    groups. Every stage of the layer is independent per head (the top-k, the plan
+    and all softmaxes are per head: types.hpp:27-48, compression.hpp:213-215), so
+    head group g is computed on the compute stream while group g+1 is copied in
+    and group g-1 is copied out on two copy streams: PCIe and HBM/tensor work
+    overlap instead of adding up. Results are bitwise those of one gsa_forward
+    over all heads (same kernels, same per-head arithmetic).
+
+    Device buffers are allocated once per (shape, dtype) and reused.
+    """
+
+    def __init__(self, heads_per_group: int = 4, device="cuda"):
+        self.g = heads_per_group
+        self.device = torch.device(device)
+        self.s_in = torch.cuda.Stream(self.device)
+        self.s_comp = torch.cuda.Stream(self.device)
+        self.s_out = torch.cuda.Stream(self.device)
+        self._bufs = None
+        self._key = None
+        self.ws = [Workspace(), Workspace()]
+
+    def _alloc(self, q, out_dtype=torch.float32):
+        H, M, d = q.shape
+        key = (H, M, d, q.dtype)
+        if self._key != key:
+            g = min(self.g, H)
+            mk = lambda dt: torch.empty(g, M, d, dtype=dt, device=self.device)  # noqa: E731
+            # double-buffered device slots per head group
+            self._bufs = [dict(q=mk(q.dtype), k=mk(q.dtype), v=mk(q.dtype), out=mk(out_dtype)) for _ in range(2)]
+            self._key = key
+        return self._bufs
+
+    def forward(self, q_host, k_host, v_host, w_g, layout: TokenLayout, params: GsaParams, out_host):
+        """q/k/v_host: pinned [H, M, d] (bf16 or f32); w_g: device f32 [H, d, d];
+        out_host: pinned f32 [H, M, d]. Returns out_host once the copies are done."""
+        H = q_host.shape[0]
+        bufs = self._alloc(q_host)
+        g = min(self.g, H)
+        groups = [(h0, min(H, h0 + g)) for h0 in range(0, H, g)]
+        ev_in = [torch.cuda.Event() for _ in groups]
+        ev_comp = [torch.cuda.Event() for _ in groups]
+        ev_out = [torch.cuda.Event() for _ in groups]
+        cur = torch.cuda.current_stream(self.device)
+        for s in (self.s_in, self.s_comp, self.s_out):
+            s.wait_stream(cur)
+        for i, (h0, h1) in enumerate(groups):
+            b = bufs[i & 1]
+            n = h1 - h0
+            with torch.cuda.stream(self.s_in):
+                if i >= 2:  # the slot's previous compute must be done reading it
+                    self.s_in.wait_event(ev_comp[i - 2])
+                b["q"][:n].copy_(q_host[h0:h1], non_blocking=True)
+                b["k"][:n].copy_(k_host[h0:h1], non_blocking=True)
+                b["v"][:n].copy_(v_host[h0:h1], non_blocking=True)
+                ev_in[i].record(self.s_in)
+            with torch.cuda.stream(self.s_comp):
+                self.s_comp.wait_event(ev_in[i])
+                if i >= 2:  # the slot's previous output must be copied out
+                    self.s_comp.wait_event(ev_out[i - 2])
+                gsa_forward(b["q"][:n], b["k"][:n], b["v"][:n], w_g[h0:h1], layout, params,
+                            out=b["out"][:n], workspace=self.ws[i & 1])
+                ev_comp[i].record(self.s_comp)
+            with torch.cuda.stream(self.s_out):
+                self.s_out.wait_event(ev_comp[i])
+                out_host[h0:h1].copy_(b["out"][:n], non_blocking=True)
+                ev_out[i].record(self.s_out)
+        cur.wait_stream(self.s_out)
+        return out_host

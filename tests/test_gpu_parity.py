@@ -337,3 +337,24 @@ def test_project_qkv_bitexact_vs_reference(gsa, ref, tokens, C, H):
 def orc_bf16(x):
     from oracle import Oracle
     return Oracle().bf16_round(x)
+
+
+@pytest.mark.parametrize("group", [3, 8])
+def test_host_pipeline_matches_forward(gsa, orc, group):
+    """HostPipeline (host -> host, head groups pipelined over copy/compute
+    streams) returns exactly what one device gsa_forward returns."""
+    lt = (10, 4, 16, 16, 4)
+    L = Layout(*lt)
+    q, k, v, wg = make_inputs(orc, L, heads=8, dim=64, seed=9)
+    layout = gsa.build_token_layout(*lt)
+    params = gsa.GsaParams(window_s=4, top_k=12)
+    hq, hk, hv = (torch.from_numpy(x).to(torch.bfloat16).pin_memory() for x in (q, k, v))
+    twg = dev(wg, torch.float32)
+    ref = gsa.gsa_forward(hq.cuda(), hk.cuda(), hv.cuda(), twg, layout, params)
+    hout = torch.empty(ref.shape, dtype=torch.float32).pin_memory()
+    pipe = gsa.HostPipeline(heads_per_group=group)
+    for _ in range(2):  # reuse of the device slots
+        hout.zero_()
+        pipe.forward(hq, hk, hv, twg, layout, params, hout)
+        torch.cuda.synchronize()
+        assert torch.equal(hout, ref.cpu())
