@@ -30,6 +30,9 @@
 // 65536 MACs (16 flop/B), see DESIGN.md.
 #include <cuda.h>
 
+#include <cstdio>
+#include <cstdlib>
+
 #include "tc.h"
 #include "tc_ptx.cuh"
 
@@ -273,6 +276,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     mbar_wait(&sm.g_empty[gb], gph[gb]);
                     gph[gb] ^= 1;
                     tc_fence_after();
+
                     const uint32_t gcol = tmem + (gb ? G_COL1 : G_COL0);
                     // the last item of this head on this CTA releases W_g
                     const int64_t nxt = it.item + gridDim.x;
@@ -385,6 +389,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 
         auto finish = [&](const GroupIt& f, int64_t jf) {
             const int fb = (int)(jf & 1);
+            // the compressed-branch row this item merges with: issued before the PV wait
+            // so its global-load latency overlaps it
+            const int fh = (int)(f.item / L.windows), fw = (int)(f.item - (int64_t)fh * L.windows);
+            const float comp_pre = f.g == f.ng - 1 ? __ldg(p.o_comp + ((int64_t)fh * L.windows + fw) * 64 + 16 * qd + (lane & 15)) : 0.0f;
             mbar_wait(&sm.o_full[fb], oph[fb]);
             oph[fb] ^= 1;
             __syncwarp();
@@ -421,7 +429,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             }
             const int h = (int)(f.item / L.windows), w = (int)(f.item - (int64_t)h * L.windows);
             const int jf_feat = 16 * qd + (lane & 15);
-            const float comp = p.o_comp[((int64_t)h * L.windows + w) * 64 + jf_feat];
+            const float comp = comp_pre;
             const int fr = w / L.wins_per_frame, rr = w - fr * L.wins_per_frame;
             const int wr = rr / L.wins_w, wc = rr - wr * L.wins_w;
             const int tok0 = fr * L.tokens_per_frame + wr * 4 * L.grid_w + wc * 4;
@@ -525,7 +533,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     for (int e = 0; e < 8; ++e) {
                         const int slot = (e & 1) | ((e >> 2) << 1);
                         const float x = s[c][hf][e];
-                        pv[e] = x == -INFINITY ? 0.0f : exp2f(fmaf(x, p.c2, -mq[slot]));
+                        pv[e] = x == -INFINITY ? 0.0f : ex2_approx(fmaf(x, p.c2, -mq[slot]));
                         sum[slot] += pv[e];
                     }
                     uint32_t hi[4], lo[4];
