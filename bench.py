@@ -29,12 +29,13 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-HEADS, DIM, S, TOPK, SPECIAL_PER_VIEW, GRID = 16, 64, 4, 32, 5, 36
+HEADS, DIM, S = 16, 64, 4
+TOPK, SPECIAL_PER_VIEW, GRID_H, GRID_W = 32, 5, 36, 36  # defaults: VGGT-shaped (BASELINE configs[1..2])
 METRIC = "sparse global-attn layer ms & tokens/s at 1000 views; speedup vs dense; TC util"
 
 
 def layout_for(views: int):
-    return (SPECIAL_PER_VIEW * views, views, GRID, GRID, S)
+    return (SPECIAL_PER_VIEW * views, views, GRID_H, GRID_W, S)
 
 
 def geometry(views: int):
@@ -149,8 +150,9 @@ def run_reference_arm(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": geometry(args.views)["M"] / v * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (seeded N(0,1) bf16-representable Q/K/V)",
-            "config": {"workload": f"1 GSA layer, {args.views} views x (5 specials + 36x36 patches), 16 heads x 64, "
-                                   f"s=4, top-32, plain", "views": args.views, "tokens": geometry(args.views)["M"]},
+            "config": {"workload": f"1 GSA layer, {args.views} views x ({SPECIAL_PER_VIEW} specials + {GRID_H}x{GRID_W} "
+                                   f"patches), 16 heads x 64, s=4, top-{TOPK}, plain", "views": args.views,
+                       "tokens": geometry(args.views)["M"]},
             "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": last["cores"], "kind": last["kind"],
                              "sample": last["sample"]},
             "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -170,7 +172,13 @@ def main():
     ap.add_argument("--no-dense", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--shard", action="store_true", help="use the view-sharded layer even on 1 GPU")
+    ap.add_argument("--grid", default="36x36", help="patch grid per view (pi3 518x1036: 36x76)")
+    ap.add_argument("--specials-per-view", type=int, default=5, help="VGGT: 5, pi3: 0")
+    ap.add_argument("--topk", type=int, default=32)
     args = ap.parse_args()
+    global TOPK, SPECIAL_PER_VIEW, GRID_H, GRID_W
+    GRID_H, GRID_W = (int(x) for x in args.grid.split("x"))
+    SPECIAL_PER_VIEW, TOPK = args.specials_per_view, args.topk
     if args.impl == "reference":
         return run_reference_arm(args)
 
@@ -193,6 +201,7 @@ def main():
     lt = layout_for(args.views)
     L = gsa.build_token_layout(*lt)
     params = gsa.GsaParams(window_s=S, top_k=TOPK)
+    geometry_default = (GRID_H, GRID_W, SPECIAL_PER_VIEW, TOPK) == (36, 36, 5, 32)
     gen = torch.Generator(device=dev).manual_seed(7)
     q, k, v = (torch.randn(HEADS, G["M"], DIM, generator=gen, device=dev, dtype=torch.float32).to(torch.bfloat16)
                for _ in range(3))
@@ -282,10 +291,11 @@ def main():
         roof = {"kernel": dom, "bound": "tensor", "achieved": A, "peak": tc_peak, "unit": "TFLOP/s",
                 "frac": A / tc_peak, "traffic": None, "peak_kind": peak_kind}
     prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(prof):
+    if os.path.exists(prof) and world == 1 and geometry_default:
         tr = json.load(open(prof)).get(dom)
-        if tr:
-            roof["traffic"] = tr
+        if tr:  # DRAM bytes (read + write) per launch of the stage's kernel, from one ncu --set full capture
+            roof["traffic"] = tr["dram_gbytes_per_launch"] * 1e9
+            roof["traffic_source"] = "profiles/" + tr["source"]
     per_stage = {}
     for n_, t_ in stage_ms.items():
         if n_ in flops:
@@ -299,8 +309,9 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (torch N(0,1) bf16 Q/K/V, W_g=N(0,1)/8 f32), resident in HBM",
-            "config": {"workload": f"1 GSA layer, {args.views} views x (5 specials + 36x36 patches) = {M} tokens, "
-                                   f"16 heads x 64, s=4, top-32, plain", "views": args.views, "tokens": M,
+            "config": {"workload": f"1 GSA layer, {args.views} views x ({SPECIAL_PER_VIEW} specials + {GRID_H}x{GRID_W} "
+                                   f"patches) = {M} tokens, 16 heads x 64, s=4, top-{TOPK}, plain", "views": args.views,
+                       "tokens": M,
                        "windows": W, "parallelism": f"query views sharded over {world} (NCCL all-gather of Kc/Vc "
                                                     f"and K/V)" if world > 1 else "1 GPU",
                        "l2": "inputs larger than L2 (no flush)"},

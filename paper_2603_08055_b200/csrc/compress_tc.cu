@@ -44,9 +44,12 @@ constexpr int NSB = 3;                  // S/P buffers in TMEM, rotating over th
 constexpr uint32_t TMEM_COLS = 512;
 constexpr uint32_t O_COL0 = 384;        // O of WG w: [384 + 64 w, +64); S/P buffer b: [128 b, +128)
 constexpr float RESCALE_LOG2 = 8.0f;
-constexpr int KCAP = 32;                // max k_eff on this path
-constexpr int CCAP = 512;               // candidates a row may stream out (more: exact fallback)
-constexpr int CAND = 64;                // candidates handed to the exact re-score (2 per lane)
+constexpr int KCAP = 128;               // max k_eff on this path
+// candidates a row may stream out (more: exact per-row fallback) and survivors
+// of the approximate radix select handed to the exact re-score: sized by k
+// (the streamed count grows like k (1 + ln(W / k)))
+__host__ __device__ constexpr int ccap_for(int k) { return k <= 32 ? 512 : 2048; }
+__host__ __device__ constexpr int surv_for(int k) { return k <= 32 ? 64 : 256; }
 constexpr int NBIN = 8;                 // threshold histogram bins (8-bit saturating counters)
 constexpr float EPS_REL = 0.00048828125f;          // 2^-11
 constexpr float DELTA_REL = 9.5367431640625e-07f;  // 2^-20: collapse of distinct sums under *scale
@@ -74,7 +77,8 @@ struct CompParams {
     float* out;
     int64_t out_hs, out_rs;
     float* lse;               // [H][Wq]
-    float2* cand;             // [H*Wq][CCAP] (approx score, window id)
+    float2* cand;             // [H*Wq][ccap] (approx score, window id)
+    int ccap;
     int* cand_n;              // [H*Wq]
     uint8_t* flag;            // [H*Wq]
 };
@@ -120,11 +124,12 @@ struct RowTopk {
     float lb, thr, delta, inv_delta, eps;
     uint32_t hist[2];  // bytes: bins 0..7 relative to lb (bin 7 open-ended)
     int cnt;           // candidates streamed; -1 = none (invalid row) / overflow
+    int ccap;
     float2* dst;
 
     __device__ __forceinline__ void add(float v, int col) {
         if (cnt < 0) return;
-        if (cnt == CCAP) {
+        if (cnt == ccap) {
             cnt = -1;  // more candidates than the list holds: exact fallback for this row
             return;
         }
@@ -316,7 +321,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         tk.eps = row_ok ? EPS_REL * p.qnorm[r] * p.kmax[h] : 0.0f;
         tk.hist[0] = tk.hist[1] = 0u;
         tk.cnt = (row_ok && K > 0) ? 0 : -1;
-        tk.dst = p.cand + r * CCAP;
+        tk.ccap = p.ccap;
+        tk.dst = p.cand + r * p.ccap;
         float m_used = -INFINITY, l = 0.0f;
 
         for (int t = 0; t < T; ++t) {
@@ -536,19 +542,21 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 //  3. exact scaled_dot (dot.hpp:11-23 order, no FMA) for those, rank by
 //     (score desc, index asc) = topk_better (compression.hpp:67-73).
 // Query rows index [H][Wq], key windows [H][Wk] (Wq < Wk for a view shard).
+template <int PER, int SLOTS>
 __global__ void __launch_bounds__(256) rescore_kernel(const float* __restrict__ qc, int64_t q_hs,
                                                       const float* __restrict__ kc, int heads, int Wq, int Wk,
                                                       float scale, int k_eff, const float* __restrict__ qnorm,
                                                       const float* __restrict__ kmax, const float2* __restrict__ cand,
                                                       const int* __restrict__ cand_n, uint8_t* flag, int32_t* topk,
                                                       float* guide) {
-    constexpr int PER = CCAP / 32;
+    constexpr int CC = PER * 32, SV = SLOTS * 32;  // candidate capacity / survivor capacity
+    extern __shared__ float2 surv_all[];           // [8 warps][SV]
     const int64_t r = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
     const int lane = threadIdx.x & 31;
     if (r >= (int64_t)heads * Wq || flag[r]) return;
     const int h = (int)(r / Wq);
-    const int n = min(cand_n[r], CCAP);
-    const float2* cr = cand + r * CCAP;
+    const int n = min(cand_n[r], CC);
+    const float2* cr = cand + r * CC;
     float2 cv[PER];
     uint32_t key[PER];
 #pragma unroll
@@ -568,35 +576,31 @@ __global__ void __launch_bounds__(256) rescore_kernel(const float* __restrict__ 
     }
     const float eps = EPS_REL * qnorm[r] * kmax[h];
     const float thr = topk_threshold(fkey_inv(res), eps);
-    // compact the survivors (through shared memory) into two slots per lane
-    __shared__ float2 surv[8][CAND];
-    float2* sv = surv[threadIdx.x / 32];
+    // compact the survivors (through shared memory) into SLOTS slots per lane
+    float2* sv = surv_all + (threadIdx.x / 32) * SV;
     int total = 0;
 #pragma unroll
     for (int i = 0; i < PER; ++i) {
         const bool keep = key[i] != 0u && cv[i].x >= thr;
         const unsigned b = __ballot_sync(0xffffffffu, keep);
         const int pos = total + __popc(b & ((1u << lane) - 1u));
-        if (keep && pos < CAND) sv[pos] = cv[i];
+        if (keep && pos < SV) sv[pos] = cv[i];
         total += __popc(b);
     }
     __syncwarp();
-    float e[2] = {-INFINITY, -INFINITY};
-    int idx[2] = {-1, -1};
-#pragma unroll
-    for (int s = 0; s < 2; ++s) {
-        const int j = lane + 32 * s;
-        if (j < total && j < CAND) idx[s] = __float_as_int(sv[j].y);
-    }
-    if (total > CAND) {
-        if (lane == 0) flag[r] = 1;  // near-tie flood: the exact kernel redoes this row
+    if (total > SV) {
+        if (lane == 0) flag[r] = 1;  // near-tie flood: the exact per-row kernel redoes this row
         return;
     }
-    // exact re-score of the survivors
+    float e[SLOTS];
+    int idx[SLOTS];
     const float* q = qc + (int64_t)h * q_hs + (r - (int64_t)h * Wq) * 64;
 #pragma unroll
-    for (int s = 0; s < 2; ++s) {
-        if (idx[s] >= 0) {
+    for (int s = 0; s < SLOTS; ++s) {
+        const int j = lane + 32 * s;
+        e[s] = -INFINITY;
+        idx[s] = j < total ? __float_as_int(sv[j].y) : -1;
+        if (idx[s] >= 0) {  // exact scaled_dot (dot.hpp:11-23 order)
             const float* k = kc + ((int64_t)h * Wk + idx[s]) * 64;
             ExactDot4 d;
             d.zero();
@@ -609,17 +613,27 @@ __global__ void __launch_bounds__(256) rescore_kernel(const float* __restrict__ 
             e[s] = d.finish(scale);
         }
     }
-    // rank = number of survivors strictly better under topk_better
-    int rank[2] = {0, 0};
-    for (int j = 0; j < total; ++j) {
-        const float ej = __shfl_sync(0xffffffffu, e[j >> 5], j & 31);
-        const int ij = __shfl_sync(0xffffffffu, idx[j >> 5], j & 31);
+    // rank = number of survivors strictly better under topk_better (compression.hpp:67-73)
+    int rank[SLOTS];
 #pragma unroll
-        for (int s = 0; s < 2; ++s)
+    for (int s = 0; s < SLOTS; ++s) rank[s] = 0;
+    for (int j = 0; j < total; ++j) {
+        float ej = e[0];
+        int ij = idx[0];
+#pragma unroll
+        for (int s = 1; s < SLOTS; ++s)
+            if ((j >> 5) == s) {
+                ej = e[s];
+                ij = idx[s];
+            }
+        ej = __shfl_sync(0xffffffffu, ej, j & 31);
+        ij = __shfl_sync(0xffffffffu, ij, j & 31);
+#pragma unroll
+        for (int s = 0; s < SLOTS; ++s)
             if (topk_better(ej, ij, e[s], idx[s])) ++rank[s];
     }
 #pragma unroll
-    for (int s = 0; s < 2; ++s)
+    for (int s = 0; s < SLOTS; ++s)
         if (idx[s] >= 0 && rank[s] < k_eff) {
             topk[r * k_eff + rank[s]] = idx[s];
             if (guide) guide[r * k_eff + rank[s]] = e[s];
@@ -794,7 +808,7 @@ struct Ws {
     size_t used;
 };
 
-Ws carve_ws(void* base, int heads, int Wq, int Wk, bool dry) {
+Ws carve_ws(void* base, int heads, int Wq, int Wk, int k_eff, bool dry) {
     Ws w{};
     size_t off = 0;
     auto take = [&](size_t bytes) -> char* {
@@ -814,7 +828,7 @@ Ws carve_ws(void* base, int heads, int Wq, int Wk, bool dry) {
     w.kn = reinterpret_cast<float*>(take(nk * 4));
     w.kmax = reinterpret_cast<float*>(take((size_t)heads * 4));
     w.exbits = reinterpret_cast<uint32_t*>(take((size_t)((Wk + 127) / 128) * 16));
-    w.cand = reinterpret_cast<float2*>(take(nq * CCAP * 8));
+    w.cand = reinterpret_cast<float2*>(take(nq * (size_t)ccap_for(k_eff) * 8));
     w.cand_n = reinterpret_cast<int*>(take(nq * 4));
     w.flag = reinterpret_cast<uint8_t*>(take(nq));
     w.blocks = reinterpret_cast<int*>(take(nq * 4));  // flagged rows
@@ -837,14 +851,14 @@ size_t tc_compress_workspace_bytes(int heads, int windows, int dim, int k_eff) {
 
 size_t tc_compress_workspace_bytes_qk(int heads, int wq, int wk, int dim, int k_eff) {
     if (dim != 64 || k_eff > KCAP) return 0;
-    return carve_ws(nullptr, heads, wq, wk, true).used;
+    return carve_ws(nullptr, heads, wq, wk, k_eff, true).used;
 }
 
 bool tc_compress_split_buffers(void* ws, size_t ws_bytes, int heads, int windows, int dim, int k_eff,
                                CompressSplits* out) {
-    if (dim != 64 || k_eff > KCAP || !ws || ws_bytes < carve_ws(nullptr, heads, windows, windows, true).used)
+    if (dim != 64 || k_eff > KCAP || !ws || ws_bytes < carve_ws(nullptr, heads, windows, windows, k_eff, true).used)
         return false;
-    Ws w = carve_ws(ws, heads, windows, windows, false);
+    Ws w = carve_ws(ws, heads, windows, windows, k_eff, false);
     *out = CompressSplits{w.qh, w.ql, w.kh, w.kl, w.vh, w.vl, w.qn, w.kn};
     return true;
 }
@@ -880,10 +894,10 @@ cudaError_t tc_compress_topk_splits(const CompressSplits* pre, const gsa_tensor&
     ex.excluded = excluded;
     const bool tc_ok = qc.dim == 64 && k_eff <= KCAP && contiguous_f32(qc) && contiguous_f32(kc) &&
                        contiguous_f32(vc) && tmap_encode_fn() != nullptr && ws &&
-                       ws_bytes >= carve_ws(nullptr, H, Wq, Wk, true).used && Wq > 0 && Wk > 0;
+                       ws_bytes >= carve_ws(nullptr, H, Wq, Wk, k_eff, true).used && Wq > 0 && Wk > 0;
     if (!tc_ok) return launch_attn_f32(ex, st);
 
-    Ws w = carve_ws(ws, H, Wq, Wk, false);
+    Ws w = carve_ws(ws, H, Wq, Wk, k_eff, false);
     const __nv_bfloat16 *qh = w.qh, *ql = w.ql, *kh = w.kh, *kl = w.kl, *vh = w.vh, *vl = w.vl;
     const float *qn = w.qn, *kn = w.kn;
     if (pre) {
@@ -929,6 +943,7 @@ cudaError_t tc_compress_topk_splits(const CompressSplits* pre, const gsa_tensor&
     p.out_rs = out_rs;
     p.lse = lse;
     p.cand = w.cand;
+    p.ccap = ccap_for(k_eff);
     p.cand_n = w.cand_n;
     p.flag = w.flag;
     const size_t smem = sizeof(CompSmem) + 1024;
@@ -938,10 +953,17 @@ cudaError_t tc_compress_topk_splits(const CompressSplits* pre, const gsa_tensor&
     note_launch();
     if (k_eff > 0) {
         const int64_t rows = (int64_t)H * Wq;
-        rescore_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(static_cast<const float*>(qc.data), qc.head_stride,
-                                                                   static_cast<const float*>(kc.data), H, Wq, Wk, scale,
-                                                                   k_eff, qn, w.kmax, w.cand, w.cand_n, w.flag, topk,
-                                                                   guide);
+        const float* qcp = static_cast<const float*>(qc.data);
+        const float* kcp = static_cast<const float*>(kc.data);
+        if (k_eff <= 32) {
+            static_assert(ccap_for(32) == 16 * 32 && surv_for(32) == 2 * 32, "rescore instance");
+            rescore_kernel<16, 2><<<(unsigned)((rows + 7) / 8), 256, 8 * 64 * sizeof(float2), st>>>(
+                qcp, qc.head_stride, kcp, H, Wq, Wk, scale, k_eff, qn, w.kmax, w.cand, w.cand_n, w.flag, topk, guide);
+        } else {
+            static_assert(ccap_for(128) == 64 * 32 && surv_for(128) == 8 * 32, "rescore instance");
+            rescore_kernel<64, 8><<<(unsigned)((rows + 7) / 8), 256, 8 * 256 * sizeof(float2), st>>>(
+                qcp, qc.head_stride, kcp, H, Wq, Wk, scale, k_eff, qn, w.kmax, w.cand, w.cand_n, w.flag, topk, guide);
+        }
         note_launch();
         // rows whose candidate list overflowed (near-tie floods): exact recompute per row
         cudaMemsetAsync(w.nblocks, 0, sizeof(int), st);

@@ -358,3 +358,29 @@ def test_host_pipeline_matches_forward(gsa, orc, group):
         pipe.forward(hq, hk, hv, twg, layout, params, hout)
         torch.cuda.synchronize()
         assert torch.equal(hout, ref.cpu())
+
+
+@pytest.mark.parametrize("kind,W,k", [("normal", 3000, 64), ("normal", 5000, 128), ("sharp", 2000, 96),
+                                      ("ties", 700, 128), ("pooled_bf16", 4000, 128)])
+def test_compress_topk_tc_large_k(gsa, orc, kind, W, k):
+    """k in (32, 128] on the tensor-core path (the paper's top-64/128 ablation,
+    PAPER.md:487-491): larger candidate lists and survivor sets, same bit-exact
+    contract."""
+    rng = np.random.default_rng(W + k)
+    H = 2
+    if kind == "ties":
+        qc, kc, vc = (rng.integers(-2, 3, size=(H, W, 64)).astype(np.float32) for _ in range(3))
+    elif kind == "normal":
+        qc, kc, vc = (rng.standard_normal((H, W, 64)).astype(np.float32) for _ in range(3))
+    elif kind == "sharp":
+        qc, kc, vc = (rng.standard_normal((H, W, 64)).astype(np.float32) * 6 for _ in range(3))
+    else:
+        L = Layout(0, W // 81, 36, 36, 4)
+        x = [orc.bf16_round(rng.standard_normal((H, L.image_tokens, 64)).astype(np.float32)) for _ in range(3)]
+        qc, kc, vc = (orc.pool(t, L) for t in x)
+    o_ref, l_ref, i_ref, g_ref = orc.compress_topk(qc, kc, vc, k, 0.125, guide=True)
+    r = gsa.fused_compressed_attention_topk(dev(qc, torch.float32), dev(kc, torch.float32), dev(vc, torch.float32),
+                                            k, 0.125, keep_guide_scores=True)
+    np.testing.assert_array_equal(host(r.indices).astype(np.int32), i_ref)
+    np.testing.assert_array_equal(host(r.guide_scores), g_ref.reshape(host(r.guide_scores).shape))
+    assert rel_l2(host(r.out), o_ref) < 1e-4
