@@ -81,6 +81,7 @@ struct CompParams {
     int ccap;
     int* cand_n;              // [H*Wq]
     uint8_t* flag;            // [H*Wq]
+    unsigned long long* prof; // COMPRESS_PROF builds: per-phase cycles of one softmax warp
 };
 
 // order-preserving map float -> uint32 (finite and +-inf); 0 is below every real key
@@ -325,16 +326,26 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         tk.dst = p.cand + r * p.ccap;
         float m_used = -INFINITY, l = 0.0f;
 
+#ifdef COMPRESS_PROF
+        const bool prof_on = p.prof && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0;
+        unsigned long long pt[6] = {0, 0, 0, 0, 0, 0}, c0 = clock64(), c1;
+#endif
         for (int t = 0; t < T; ++t) {
             const int n = 2 * t + w, b = n % NSB;
             const uint32_t s_base = lane_base + 128 * b;
             mbar_wait(&sm.s_full[b], (uint32_t)((n / NSB) & 1));
+#ifdef COMPRESS_PROF
+            if (prof_on) { c1 = clock64(); pt[0] += c1 - c0; c0 = c1; }
+#endif
             __syncwarp();  // .sync.aligned tcgen05 ops below need a converged warp
             tc_fence_after();
             uint32_t sr[4][32];
 #pragma unroll
             for (int c = 0; c < 4; ++c) tmem_ld_32x32b_x32(s_base + 32 * c, sr[c]);
             tmem_wait_ld();
+#ifdef COMPRESS_PROF
+            if (prof_on) { c1 = clock64(); pt[1] += c1 - c0; c0 = c1; }
+#endif
             const int valid = p.Wk - t * 128;
             if (valid < 128) {  // last key tile only: columns past Wk do not exist
 #pragma unroll
@@ -413,6 +424,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             tmem_wait_st();
             tc_fence_before();
             mbar_arrive(&sm.p_full[w][t & 1]);
+#ifdef COMPRESS_PROF
+            if (prof_on) { c1 = clock64(); pt[3] += c1 - c0; c0 = c1; }
+#endif
 
             // ---- streaming top-k over this tile's approximate scores (overlaps the MMAs)
             if (K > 0 && !(p.debug & 1)) {
@@ -497,9 +511,15 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     }
                 }
                 if (tk.cnt > 0) tk.raise(K);
+#ifdef COMPRESS_PROF
+            if (prof_on) { c1 = clock64(); pt[4] += c1 - c0; c0 = c1; pt[5] += 1; }
+#endif
             }
             __syncwarp();
         }
+#ifdef COMPRESS_PROF
+        if (prof_on) { for (int i = 0; i < 6; ++i) p.prof[i] = pt[i]; }
+#endif
         // ------------------------------- epilogue -------------------------------
         mbar_wait(&sm.o_final[w], 0);
         __syncwarp();
@@ -943,6 +963,11 @@ cudaError_t tc_compress_topk_splits(const CompressSplits* pre, const gsa_tensor&
     p.out_rs = out_rs;
     p.lse = lse;
     p.cand = w.cand;
+#ifdef COMPRESS_PROF
+    static unsigned long long* prof_buf = nullptr;
+    if (!prof_buf) cudaMalloc(&prof_buf, 64);
+    p.prof = prof_buf;
+#endif
     p.ccap = ccap_for(k_eff);
     p.cand_n = w.cand_n;
     p.flag = w.flag;
@@ -951,6 +976,15 @@ cudaError_t tc_compress_topk_splits(const CompressSplits* pre, const gsa_tensor&
     if (e != cudaSuccess) return e;
     compress_tc_kernel<<<dim3((Wq + 128 * NWG - 1) / (128 * NWG), H), NTHREADS, smem, st>>>(tqh, tql, tkh, tkl, tvh, tvl, p);
     note_launch();
+#ifdef COMPRESS_PROF
+    {
+        unsigned long long hp[6];
+        cudaMemcpyAsync(hp, p.prof, sizeof(hp), cudaMemcpyDeviceToHost, st);
+        cudaStreamSynchronize(st);
+        fprintf(stderr, "compress prof (CTA0 warp0): tiles %llu  wait_S %.0f  ldtm %.0f  softmax+P %.0f  topk %.0f cyc/tile\n", hp[5],
+                (double)hp[0] / hp[5], (double)hp[1] / hp[5], (double)hp[3] / hp[5], (double)hp[4] / hp[5]);
+    }
+#endif
     if (k_eff > 0) {
         const int64_t rows = (int64_t)H * Wq;
         const float* qcp = static_cast<const float*>(qc.data);
