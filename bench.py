@@ -146,13 +146,16 @@ def run_reference_arm(args):
     vals = [r["value"] for r in steps]
     v = statistics.median(vals)
     last = steps[-1]
+    G = geometry(args.views)
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "tokens/s", "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": geometry(args.views)["M"] / v * 1e3,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": G["M"] / v * 1e3,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (seeded N(0,1) bf16-representable Q/K/V)",
             "config": {"workload": f"1 GSA layer, {args.views} views x ({SPECIAL_PER_VIEW} specials + {GRID_H}x{GRID_W} "
-                                   f"patches), 16 heads x 64, s=4, top-{TOPK}, plain", "views": args.views,
-                       "tokens": geometry(args.views)["M"]},
+                                   f"patches) = {G['M']} tokens, 16 heads x 64, s=4, top-{TOPK}, plain",
+                       "views": args.views, "tokens": G["M"], "windows": G["W"],
+                       "parallelism": f"CPU reference, {last['cores']} host threads (rank 0 only)",
+                       "l2": "n/a (CPU)"},
             "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": last["cores"], "kind": last["kind"],
                              "sample": last["sample"]},
             "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
