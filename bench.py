@@ -178,6 +178,8 @@ def main():
     ap.add_argument("--grid", default="36x36", help="patch grid per view (pi3 518x1036: 36x76)")
     ap.add_argument("--specials-per-view", type=int, default=5, help="VGGT: 5, pi3: 0")
     ap.add_argument("--topk", type=int, default=32)
+    ap.add_argument("--hybrid", type=int, default=0, metavar="REF_STRIDE",
+                    help="hybrid selection with reference frames every REF_STRIDE views (0 = plain)")
     args = ap.parse_args()
     global TOPK, SPECIAL_PER_VIEW, GRID_H, GRID_W
     GRID_H, GRID_W = (int(x) for x in args.grid.split("x"))
@@ -203,8 +205,9 @@ def main():
     G = geometry(args.views)
     lt = layout_for(args.views)
     L = gsa.build_token_layout(*lt)
-    params = gsa.GsaParams(window_s=S, top_k=TOPK)
-    geometry_default = (GRID_H, GRID_W, SPECIAL_PER_VIEW, TOPK) == (36, 36, 5, 32)
+    params = gsa.GsaParams(window_s=S, top_k=TOPK, variant=1 if args.hybrid else 0,
+                           ref_stride=args.hybrid if args.hybrid else 100)
+    geometry_default = (GRID_H, GRID_W, SPECIAL_PER_VIEW, TOPK, args.hybrid) == (36, 36, 5, 32, 0)
     gen = torch.Generator(device=dev).manual_seed(7)
     q, k, v = (torch.randn(HEADS, G["M"], DIM, generator=gen, device=dev, dtype=torch.float32).to(torch.bfloat16)
                for _ in range(3))
@@ -279,10 +282,12 @@ def main():
     Wg, Mig, Msg = W // world, Mi // world, Ms // world  # this rank's share (equal blocks)
     # algorithmic work per rank and step: useful MMA flops
     # (4*d per score: QK^T + PV) and compulsory HBM bytes
+    # selected windows per plan row: top-k (+ every window of the reference frames, hybrid)
+    row_w = TOPK + (len(range(0, args.views, args.hybrid)) * (GRID_H // S) * (GRID_W // S) if args.hybrid else 0)
     flops = {"special": 4.0 * HEADS * Msg * M * DIM, "compress": 4.0 * HEADS * Wg * W * DIM,
-             "select": 4.0 * HEADS * Mig * TOPK * S * S * DIM}
+             "select": 4.0 * HEADS * Mig * row_w * S * S * DIM}
     bytes_ = {"pool": 3 * HEADS * Mig * DIM * 2 + 3 * HEADS * Wg * DIM * 4 + 3 * HEADS * Wg * DIM * 4,
-              "select": HEADS * Wg * TOPK * S * S * DIM * 2 * 2 + HEADS * Mig * DIM * (2 + 4) + HEADS * Wg * DIM * 4}
+              "select": HEADS * Wg * row_w * S * S * DIM * 2 * 2 + HEADS * Mig * DIM * (2 + 4) + HEADS * Wg * DIM * 4}
     timed = {k_: v_ for k_, v_ in stage_ms.items() if k_ in flops or k_ in bytes_}
     dom = max(timed, key=lambda n: timed[n])
     if dom in bytes_:
@@ -313,7 +318,9 @@ def main():
             "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (torch N(0,1) bf16 Q/K/V, W_g=N(0,1)/8 f32), resident in HBM",
             "config": {"workload": f"1 GSA layer, {args.views} views x ({SPECIAL_PER_VIEW} specials + {GRID_H}x{GRID_W} "
-                                   f"patches) = {M} tokens, 16 heads x 64, s=4, top-{TOPK}, plain", "views": args.views,
+                                   f"patches) = {M} tokens, 16 heads x 64, s=4, top-{TOPK}, "
+                                   f"{'hybrid (reference frames every %d views)' % args.hybrid if args.hybrid else 'plain'}",
+                       "views": args.views,
                        "tokens": M,
                        "windows": W, "parallelism": f"query views sharded over {world} (NCCL all-gather of Kc/Vc "
                                                     f"and K/V)" if world > 1 else "1 GPU",

@@ -48,7 +48,8 @@ constexpr int KCAP = 128;               // max k_eff on this path
 // candidates a row may stream out (more: exact per-row fallback) and survivors
 // of the approximate radix select handed to the exact re-score: sized by k
 // (the streamed count grows like k (1 + ln(W / k)))
-__host__ __device__ constexpr int ccap_for(int k) { return k <= 32 ? 512 : 2048; }
+// hybrid rows (excluded reference windows) start from a weaker first-tile bound: more candidates
+__host__ __device__ constexpr int ccap_for(int k, bool excl = false) { return k <= 32 ? (excl ? 1024 : 512) : 2048; }
 __host__ __device__ constexpr int surv_for(int k) { return k <= 32 ? 64 : 256; }
 constexpr int NBIN = 8;                 // threshold histogram bins (8-bit saturating counters)
 constexpr float EPS_REL = 0.00048828125f;          // 2^-11
@@ -848,7 +849,7 @@ Ws carve_ws(void* base, int heads, int Wq, int Wk, int k_eff, bool dry) {
     w.kn = reinterpret_cast<float*>(take(nk * 4));
     w.kmax = reinterpret_cast<float*>(take((size_t)heads * 4));
     w.exbits = reinterpret_cast<uint32_t*>(take((size_t)((Wk + 127) / 128) * 16));
-    w.cand = reinterpret_cast<float2*>(take(nq * (size_t)ccap_for(k_eff) * 8));
+    w.cand = reinterpret_cast<float2*>(take(nq * (size_t)ccap_for(k_eff, true) * 8));
     w.cand_n = reinterpret_cast<int*>(take(nq * 4));
     w.flag = reinterpret_cast<uint8_t*>(take(nq));
     w.blocks = reinterpret_cast<int*>(take(nq * 4));  // flagged rows
@@ -968,7 +969,7 @@ cudaError_t tc_compress_topk_splits(const CompressSplits* pre, const gsa_tensor&
     if (!prof_buf) cudaMalloc(&prof_buf, 64);
     p.prof = prof_buf;
 #endif
-    p.ccap = ccap_for(k_eff);
+    p.ccap = ccap_for(k_eff, excluded != nullptr);
     p.cand_n = w.cand_n;
     p.flag = w.flag;
     const size_t smem = sizeof(CompSmem) + 1024;
@@ -989,12 +990,16 @@ cudaError_t tc_compress_topk_splits(const CompressSplits* pre, const gsa_tensor&
         const int64_t rows = (int64_t)H * Wq;
         const float* qcp = static_cast<const float*>(qc.data);
         const float* kcp = static_cast<const float*>(kc.data);
-        if (k_eff <= 32) {
+        if (k_eff <= 32 && !excluded) {
             static_assert(ccap_for(32) == 16 * 32 && surv_for(32) == 2 * 32, "rescore instance");
             rescore_kernel<16, 2><<<(unsigned)((rows + 7) / 8), 256, 8 * 64 * sizeof(float2), st>>>(
                 qcp, qc.head_stride, kcp, H, Wq, Wk, scale, k_eff, qn, w.kmax, w.cand, w.cand_n, w.flag, topk, guide);
+        } else if (k_eff <= 32) {
+            static_assert(ccap_for(32, true) == 32 * 32, "rescore instance");
+            rescore_kernel<32, 2><<<(unsigned)((rows + 7) / 8), 256, 8 * 64 * sizeof(float2), st>>>(
+                qcp, qc.head_stride, kcp, H, Wq, Wk, scale, k_eff, qn, w.kmax, w.cand, w.cand_n, w.flag, topk, guide);
         } else {
-            static_assert(ccap_for(128) == 64 * 32 && surv_for(128) == 8 * 32, "rescore instance");
+            static_assert(ccap_for(128) == 64 * 32 && ccap_for(128, true) == 64 * 32 && surv_for(128) == 8 * 32, "rescore instance");
             rescore_kernel<64, 8><<<(unsigned)((rows + 7) / 8), 256, 8 * 256 * sizeof(float2), st>>>(
                 qcp, qc.head_stride, kcp, H, Wq, Wk, scale, k_eff, qn, w.kmax, w.cand, w.cand_n, w.flag, topk, guide);
         }
