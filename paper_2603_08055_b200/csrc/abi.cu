@@ -490,6 +490,12 @@ int layer_checks(const gsa_tensor* q, const gsa_tensor* k, const gsa_tensor* v, 
 
 struct LayerBufs {
     float *qc, *kc, *vc, *o_comp, *lse_comp, *lse_spec;
+    // hybrid fast path: reference-frame K/V rows gathered contiguously, their dense
+    // softmax (normalised output + LSE per image token) and the dense pass's workspace
+    __nv_bfloat16 *kf, *vf;
+    float *prior_o, *prior_lse;
+    void* fa_ws;
+    size_t fa_ws_bytes;
     int32_t *topk, *forced;
     uint8_t* mask;
     void* compress_ws;
@@ -517,6 +523,19 @@ size_t carve(const LayerPlan& lp, const gsa_context* ctx, char* base, size_t cap
     b->wg_prep = c.take<uint8_t>(tc_select_workspace_bytes(lp.heads));
     b->dense_ws_bytes = tc_dense_workspace_bytes(lp.heads, lp.Ms, lp.Ms + lp.Mi);
     b->dense_ws = c.take<char>(b->dense_ws_bytes);
+    b->kf = b->vf = nullptr;
+    b->prior_o = b->prior_lse = nullptr;
+    b->fa_ws = nullptr;
+    b->fa_ws_bytes = 0;
+    if (lp.n_forced > 0) {  // sized whenever the plan is hybrid; used only on the tensor-core path
+        const int fk = lp.n_forced / lp.L.wins_per_frame * lp.L.tokens_per_frame;  // reference-frame keys
+        b->kf = c.take<__nv_bfloat16>((size_t)lp.heads * fk * lp.dim);
+        b->vf = c.take<__nv_bfloat16>((size_t)lp.heads * fk * lp.dim);
+        b->prior_o = c.take<float>((size_t)lp.heads * lp.Mi * lp.dim);
+        b->prior_lse = c.take<float>((size_t)lp.heads * lp.Mi);
+        b->fa_ws_bytes = tc_dense_workspace_bytes(lp.heads, lp.Mi, fk);
+        b->fa_ws = c.take<char>(b->fa_ws_bytes);
+    }
     return c.used + 256;
 }
 
@@ -533,6 +552,7 @@ size_t gsa_forward_workspace_bytes(const gsa_layout* layout, const gsa_params* p
     lp.W = lp.L.windows;
     int nf = 0;
     const int sel = selectable_windows(lp.L, params->variant, params->ref_stride > 0 ? params->ref_stride : 1, &nf);
+    lp.n_forced = nf;
     lp.k_eff = params->top_k < sel ? params->top_k : sel;
     if (lp.k_eff < 0) lp.k_eff = 0;
     LayerBufs b;
@@ -609,7 +629,36 @@ int gsa_forward(const gsa_tensor* q, const gsa_tensor* k, const gsa_tensor* v, c
     a.o_sel_ctx = ctx ? ctx->o_sel : nullptr;
     a.gate_ctx = ctx ? ctx->gate : nullptr;
     a.wg_prep = b.wg_prep;
-    if (tc_select_supported(*q, lp.L, a.rows))
+    const bool tc_sel = tc_select_supported(*q, lp.L, a.rows);
+    if (tc_sel && params->variant == 1 && lp.n_forced > 0 && lp.k_eff > 0 && b.kf && q->dim == 64 && k->row_stride == 64 &&
+        v->row_stride == 64 && tc_dense_supported(*q, *k, *v)) {
+        // Hybrid fast path. Every query attends ALL reference-frame keys (selection.cpp:55-59:
+        // forced windows lead every plan row), so that part of the softmax is a dense
+        // attention of all image queries over the reference frames' keys (one tcgen05 FA
+        // pass instead of gathering the same 810 windows once per query window), merged
+        // in the selection epilogue with the dynamic top-k windows' partial softmax by
+        // log-sum-exp: identical to one softmax over forced ++ top-k up to f32 rounding.
+        const int tpf = lp.L.tokens_per_frame, nff = lp.n_forced / lp.L.wins_per_frame, fk = nff * tpf;
+        for (int fi = 0; fi < nff; ++fi) {
+            const int f = fi * params->ref_stride;  // forced frames 0, r, 2r, ... (selection.cpp:7-12)
+            const size_t src_row = (size_t)lp.Ms + (size_t)f * tpf;
+            GSA_CUDA(cudaMemcpy2DAsync(b.kf + (size_t)fi * tpf * 64, (size_t)fk * 64 * 2,
+                                       static_cast<const __nv_bfloat16*>(k->data) + src_row * 64,
+                                       (size_t)k->head_stride * 2, (size_t)tpf * 64 * 2, H, cudaMemcpyDeviceToDevice, st));
+            GSA_CUDA(cudaMemcpy2DAsync(b.vf + (size_t)fi * tpf * 64, (size_t)fk * 64 * 2,
+                                       static_cast<const __nv_bfloat16*>(v->data) + src_row * 64,
+                                       (size_t)v->head_stride * 2, (size_t)tpf * 64 * 2, H, cudaMemcpyDeviceToDevice, st));
+        }
+        gsa_tensor tkf{b.kf, GSA_DTYPE_BF16, H, fk, 64, (int64_t)fk * 64, 64};
+        gsa_tensor tvf{b.vf, GSA_DTYPE_BF16, H, fk, 64, (int64_t)fk * 64, 64};
+        gsa_tensor tpo{b.prior_o, GSA_DTYPE_F32, H, lp.Mi, 64, (int64_t)lp.Mi * 64, 64};
+        GSA_TRY(dense_attention(q, &tkf, &tvf, lp.scale, &tpo, b.prior_lse, lp.Ms, 0, lp.Mi, st, b.fa_ws,
+                                b.fa_ws_bytes));
+        a.rows = RowSource{nullptr, nullptr, b.forced, 0, b.topk, lp.k_eff, lp.k_eff};
+        a.prior_o = b.prior_o;
+        a.prior_lse = b.prior_lse;
+    }
+    if (tc_sel)
         GSA_CUDA(tc_select_gate_merge(a, st));
     else
         GSA_CUDA(launch_select_f32(a, st));

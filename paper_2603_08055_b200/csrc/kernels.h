@@ -69,6 +69,11 @@ struct SelectArgs {
     float* o_sel_ctx;     // optional materialised o_sel [H][Mi][d]
     float* gate_ctx;      // optional materialised gate [H][Mi][d]
     uint8_t* wg_prep;     // tensor-core path scratch: W_g hi/lo split, H * 16 KB
+    // hybrid fast path: softmax already taken over the reference-frame keys by a dense
+    // pass (normalised output and natural-log LSE per image token); the plan rows then
+    // hold only the dynamic windows and the epilogue merges the two partial softmaxes
+    const float* prior_o;    // [H][Mi][d] f32 or null
+    const float* prior_lse;  // [H][Mi]
 };
 cudaError_t launch_select_f32(const SelectArgs& a, cudaStream_t st);
 

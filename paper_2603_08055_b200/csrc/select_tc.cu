@@ -80,6 +80,8 @@ struct SelTcParams {
     float* lse;
     float* o_sel_ctx;
     float* gate_ctx;
+    const float* prior_o;     // hybrid fast path: reference-frame softmax, merged by LSE (or null)
+    const float* prior_lse;
     const uint8_t* wg_prep;  // [H][2][8192] bytes
 };
 
@@ -438,7 +440,15 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             for (int i = 0; i < 8; ++i) {
                 const int q = i + 8 * hi_half;
                 const int tok = tok0 + (q >> 2) * L.grid_w + (q & 3);
-                const float sel = a8[i] / sm.run_l[fb][q];
+                float sel = a8[i] / sm.run_l[fb][q];
+                if (p.prior_o) {  // merge with the reference-frame partial softmax (LSE weights)
+                    const int64_t ti = (int64_t)h * L.image_tokens + tok;
+                    const float l1 = p.prior_lse[ti];
+                    const float l2 = sm.run_m[fb][q] * p.scale + logf(sm.run_l[fb][q]);
+                    const float mm = fmaxf(l1, l2);
+                    const float w1 = __expf(l1 - mm), w2 = __expf(l2 - mm);
+                    sel = (w1 * p.prior_o[ti * 64 + jf_feat] + w2 * sel) / (w1 + w2);
+                }
                 const float g = 1.0f / (1.0f + __expf(-z8[i]));
                 outh[(int64_t)tok * p.out_rs + jf_feat] = g * comp + (1.0f - g) * sel;
                 if (p.o_sel_ctx || p.gate_ctx) {
@@ -449,7 +459,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             }
             if (p.lse && ws == 0 && lane < 16) {
                 const int tok = tok0 + (lane >> 2) * L.grid_w + (lane & 3);
-                p.lse[(int64_t)h * L.image_tokens + tok] = sm.run_m[fb][lane] * p.scale + logf(sm.run_l[fb][lane]);
+                float lse = sm.run_m[fb][lane] * p.scale + logf(sm.run_l[fb][lane]);
+                if (p.prior_o) {
+                    const float l1 = p.prior_lse[(int64_t)h * L.image_tokens + tok], mm = fmaxf(l1, lse);
+                    lse = mm + logf(__expf(l1 - mm) + __expf(lse - mm));
+                }
+                p.lse[(int64_t)h * L.image_tokens + tok] = lse;
             }
         };
 
@@ -673,6 +688,8 @@ cudaError_t tc_select_gate_merge(const SelectArgs& a, cudaStream_t st) {
     p.out_rs = a.out_rs;
     p.lse = a.lse;
     p.o_sel_ctx = a.o_sel_ctx;
+    p.prior_o = a.prior_o;
+    p.prior_lse = a.prior_lse;
     p.gate_ctx = a.gate_ctx;
     p.wg_prep = a.wg_prep;
     int dev = 0, nsm = 148;

@@ -384,3 +384,20 @@ def test_compress_topk_tc_large_k(gsa, orc, kind, W, k):
     np.testing.assert_array_equal(host(r.indices).astype(np.int32), i_ref)
     np.testing.assert_array_equal(host(r.guide_scores), g_ref.reshape(host(r.guide_scores).shape))
     assert rel_l2(host(r.out), o_ref) < 1e-4
+
+
+@pytest.mark.parametrize("lt,ref_stride,k", [((10, 12, 16, 16, 4), 4, 6), ((40, 9, 36, 36, 4), 3, 32)])
+def test_hybrid_fast_path_matches_reference(gsa, ref, lt, ref_stride, k):
+    """Hybrid rows = every reference-frame window ++ dynamic top-k (selection.cpp:55-59).
+    The tensor-core path takes the reference-frame part as one dense attention and
+    merges it into the selection epilogue by log-sum-exp; selection output, its LSE
+    and the layer output must match the reference's single softmax over the row."""
+    L = Layout(*lt)
+    from oracle import Oracle
+    q, k_, v, wg = make_inputs(Oracle(), L, heads=4, dim=64, seed=13)
+    rf = ref.forward(q, k_, v, wg, lt, top_k=k, variant=1, ref_stride=ref_stride)
+    out, ctx = run_forward(gsa, q, k_, v, wg, lt, k, variant=1, ref_stride=ref_stride)
+    np.testing.assert_array_equal(ctx.topk.cpu().numpy(), rf["topk"])
+    assert np.abs(out - rf["out"]).max() < 1e-4 and rel_l2(out, rf["out"]) < 1e-5
+    assert np.abs(host(ctx.o_sel) - rf["o_sel"]).max() < 1e-4
+    assert np.abs(host(ctx.lse_sel) - rf["lse_sel"]).max() < 1e-4
