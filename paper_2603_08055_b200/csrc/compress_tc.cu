@@ -129,19 +129,16 @@ struct RowTopk {
     int ccap;
     float2* dst;
 
+    // branch-free: predicated store, select-based count and bin updates
     __device__ __forceinline__ void add(float v, int col) {
-        if (cnt < 0) return;
-        if (cnt == ccap) {
-            cnt = -1;  // more candidates than the list holds: exact fallback for this row
-            return;
-        }
-        dst[cnt++] = make_float2(v, __int_as_float(col));
-        if (v >= lb) {
-            const int b = min(NBIN - 1, (int)((v - lb) * inv_delta));
-            const uint32_t inc = 1u << (8 * (b & 3));
-            if (b < 4) hist[0] = __vaddus4(hist[0], inc);
-            else hist[1] = __vaddus4(hist[1], inc);
-        }
+        const bool ok = (unsigned)cnt < (unsigned)ccap;  // cnt < 0 (no row / overflowed) is huge unsigned
+        if (ok) dst[cnt] = make_float2(v, __int_as_float(col));
+        cnt = ok ? cnt + 1 : -1;  // reaching ccap overflows the row: exact fallback
+        const float rel = (v - lb) * inv_delta;
+        const int b = min(NBIN - 1, (int)fmaxf(rel, 0.0f));
+        const uint32_t inc = (ok && v >= lb) ? 1u << (8 * (b & 3)) : 0u;
+        hist[0] = __vaddus4(hist[0], b < 4 ? inc : 0u);
+        hist[1] = __vaddus4(hist[1], b < 4 ? 0u : inc);
     }
     // after each tile: raise LB by the largest j with >= K counted at or above bin j
     __device__ __forceinline__ void raise(int K) {
@@ -487,7 +484,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 const float tq = tk.cnt < 0 ? INFINITY : tk.thr;
 #pragma unroll
                 for (int c = 0; c < 4; ++c) {
-                    if (!__any_sync(0xffffffffu, cmax[c] >= tq)) continue;
+                    if (!__any_sync(0xffffffffu, cmax[c] >= tq) || (p.debug & 256)) continue;
                     // bit e = (S[e] >= tq): the sign of S - tq (FADD2), gathered by funnel shifts
                     // from e = 31 down; two interleaved chains of 16
                     uint32_t mh = 0u, ml = 0u;
@@ -505,6 +502,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                         }
                     }
                     uint32_t m = ~((mh << 16) | (ml & 0xffffu)) & keep[c];
+                    if (p.debug & 128) m = 0;  // bring-up: timing without candidate extraction
                     while (m) {
                         const int e = __ffs(m) - 1;
                         m &= m - 1;
