@@ -251,6 +251,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     } else if (warp == 1) {
         // ================================ MMA issuer ===============================
         // Stream order: S(0); then per group j: S(j+1) (look-ahead), PV(j). The whole
+        // (must match the TMA producer's load order K0, K1, V0, K2, V1, ...).
         // warp walks the stream (uniform descriptors); one elected lane issues.
         {
             const uint32_t id_s = idesc_bf16(128, 16, 0, 0);
@@ -384,19 +385,25 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         const bool stat_owner = (ws == 0 && t1 == 0);  // 4 threads x 4 query slots = 16 queries
         float acc[16];
         uint32_t sph[2] = {0, 0}, oph[2] = {0, 0};
-        int64_t j = 0, n_fin_items = 0;
+        int64_t j = 0, n_fin_items = 0, n_started = 0;
+        float comp_pf0 = 0.0f, comp_pf1 = 0.0f;  // o_comp rows of the items in flight, loaded when an item starts
         GroupIt it, fin;
         it.start(p);
         fin.start(p);
 
+#ifdef SELECT_PROF
+        const bool prof_on = blockIdx.x == 0 && threadIdx.x == 64;
+        unsigned long long pt[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0}, c0 = clock64(), c1;
+#endif
         auto finish = [&](const GroupIt& f, int64_t jf) {
             const int fb = (int)(jf & 1);
             // the compressed-branch row this item merges with: issued before the PV wait
             // so its global-load latency overlaps it
-            const int fh = (int)(f.item / L.windows), fw = (int)(f.item - (int64_t)fh * L.windows);
-            const float comp_pre = f.g == f.ng - 1 ? __ldg(p.o_comp + ((int64_t)fh * L.windows + fw) * 64 + 16 * qd + (lane & 15)) : 0.0f;
             mbar_wait(&sm.o_full[fb], oph[fb]);
             oph[fb] ^= 1;
+#ifdef SELECT_PROF
+            if (prof_on) { c1 = clock64(); pt[9] += c1 - c0; c0 = c1; }
+#endif
             __syncwarp();
             tc_fence_after();
             uint32_t orr[16];
@@ -431,7 +438,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             }
             const int h = (int)(f.item / L.windows), w = (int)(f.item - (int64_t)h * L.windows);
             const int jf_feat = 16 * qd + (lane & 15);
-            const float comp = comp_pre;
+            const float comp = ((n_fin_items - 1) & 1) ? comp_pf1 : comp_pf0;
             const int fr = w / L.wins_per_frame, rr = w - fr * L.wins_per_frame;
             const int wr = rr / L.wins_w, wc = rr - wr * L.wins_w;
             const int tok0 = fr * L.tokens_per_frame + wr * 4 * L.grid_w + wc * 4;
@@ -440,7 +447,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             for (int i = 0; i < 8; ++i) {
                 const int q = i + 8 * hi_half;
                 const int tok = tok0 + (q >> 2) * L.grid_w + (q & 3);
-                float sel = a8[i] / sm.run_l[fb][q];
+                float sel = a8[i] * __frcp_rn(sm.run_l[fb][q]);
                 if (p.prior_o) {  // merge with the reference-frame partial softmax (LSE weights)
                     const int64_t ti = (int64_t)h * L.image_tokens + tok;
                     const float l1 = p.prior_lse[ti];
@@ -449,7 +456,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     const float w1 = __expf(l1 - mm), w2 = __expf(l2 - mm);
                     sel = (w1 * p.prior_o[ti * 64 + jf_feat] + w2 * sel) / (w1 + w2);
                 }
-                const float g = 1.0f / (1.0f + __expf(-z8[i]));
+                const float g = __frcp_rn(1.0f + __expf(-z8[i]));
                 outh[(int64_t)tok * p.out_rs + jf_feat] = g * comp + (1.0f - g) * sel;
                 if (p.o_sel_ctx || p.gate_ctx) {
                     const int64_t ti = (int64_t)h * L.image_tokens + tok;
@@ -471,7 +478,17 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         while (it.valid(p)) {
             const int sb = (int)(j & 1);
             const int nkeys = it.group_windows() * 16;
+            if (it.g == 0) {  // the compressed-branch row this item merges with, a full item ahead
+                const int ih = (int)(it.item / L.windows), iw = (int)(it.item - (int64_t)ih * L.windows);
+                const float cv = __ldg(p.o_comp + ((int64_t)ih * L.windows + iw) * 64 + 16 * qd + (lane & 15));
+                if (n_started & 1) comp_pf1 = cv;
+                else comp_pf0 = cv;
+                ++n_started;
+            }
             mbar_wait(&sm.s_full[sb], sph[sb]);
+#ifdef SELECT_PROF
+            if (prof_on) { c1 = clock64(); pt[0] += c1 - c0; c0 = c1; }
+#endif
             sph[sb] ^= 1;
             __syncwarp();
             tc_fence_after();
@@ -492,6 +509,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     for (int e = 0; e < 8; ++e) s[c][hf][e] = __uint_as_float(r[e]);
                 }
             tmem_wait_ld();
+#ifdef SELECT_PROF
+            if (prof_on) { c1 = clock64(); pt[1] += c1 - c0; c0 = c1; }
+#endif
             tc_fence_before();
             mbar_arrive(&sm.s_empty[sb]);
             // mask keys past the row end; key of s[c][hf][e] = 128c + 32qd + 16hf + t1 + 8*((e>>1)&1)
@@ -518,6 +538,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 for (int sl = 0; sl < 4; ++sl) sm.red[0][ws][2 * t0 + (sl & 1) + 8 * (sl >> 1)] = mx[sl];
             }
             named_bar_sync(1, 128);
+#ifdef SELECT_PROF
+            if (prof_on) { c1 = clock64(); pt[2] += c1 - c0; c0 = c1; }
+#endif
             const int pb = sb;           // this group's statistics / P buffers
             const int ob = sb ^ 1;       // previous group's
             float mq[4], al[4];
@@ -547,17 +570,18 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 #pragma unroll
                     for (int e = 0; e < 8; ++e) {
                         const int slot = (e & 1) | ((e >> 2) << 1);
-                        const float x = s[c][hf][e];
-                        pv[e] = x == -INFINITY ? 0.0f : ex2_approx(fmaf(x, p.c2, -mq[slot]));
+                        // masked keys are -inf: ex2(-inf) = +0
+                        pv[e] = ex2_approx(fmaf(s[c][hf][e], p.c2, -mq[slot]));
                         sum[slot] += pv[e];
                     }
+                    // P = hi + lo: hi = P truncated to bf16 (one PRMT per pair), lo = P - hi rounded
                     uint32_t hi[4], lo[4];
 #pragma unroll
                     for (int e2 = 0; e2 < 4; ++e2) {
-                        const float a0 = pv[2 * e2], a1 = pv[2 * e2 + 1];
-                        const __nv_bfloat16 h0 = __float2bfloat16_rn(a0), h1 = __float2bfloat16_rn(a1);
-                        hi[e2] = pack_bf16(__bfloat162float(h0), __bfloat162float(h1));
-                        lo[e2] = pack_bf16(a0 - __bfloat162float(h0), a1 - __bfloat162float(h1));
+                        const uint32_t u0 = __float_as_uint(pv[2 * e2]), u1 = __float_as_uint(pv[2 * e2 + 1]);
+                        hi[e2] = __byte_perm(u0, u1, 0x7632);
+                        lo[e2] = pack_bf16(pv[2 * e2] - __uint_as_float(u0 & 0xffff0000u),
+                                           pv[2 * e2 + 1] - __uint_as_float(u1 & 0xffff0000u));
                     }
                     // matrix mi: keys +8*(mi&1), queries 8*(mi>>1); memory row rr = query
                     const int kc = (128 * c + 32 * qd + 16 * hf) / 8 + (mi & 1);
@@ -566,8 +590,14 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     stmatrix_x4_trans(pbase_lo + off, lo[0], lo[1], lo[2], lo[3]);
                 }
             }
+#ifdef SELECT_PROF
+            if (prof_on) { c1 = clock64(); pt[3] += c1 - c0; c0 = c1; }
+#endif
             fence_proxy_async_smem();
             mbar_arrive(&sm.p_full[pb]);
+#ifdef SELECT_PROF
+            if (prof_on) { c1 = clock64(); pt[4] += c1 - c0; c0 = c1; }
+#endif
 #pragma unroll
             for (int sl = 0; sl < 4; ++sl) {
                 sum[sl] += __shfl_xor_sync(0xffffffffu, sum[sl], 4);
@@ -579,6 +609,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 for (int sl = 0; sl < 4; ++sl) sm.red[1][ws][2 * t0 + (sl & 1) + 8 * (sl >> 1)] = sum[sl];
             }
             named_bar_sync(1, 128);
+#ifdef SELECT_PROF
+            if (prof_on) { c1 = clock64(); pt[5] += c1 - c0; c0 = c1; }
+#endif
             if (stat_owner) {
 #pragma unroll
                 for (int sl = 0; sl < 4; ++sl) {
@@ -591,15 +624,30 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             // fold in the previous group's PV (computed while this softmax ran)
             if (j > 0) {
                 finish(fin, j - 1);
+#ifdef SELECT_PROF
+            if (prof_on) { c1 = clock64(); pt[6] += c1 - c0; c0 = c1; }
+#endif
                 fin.next(p);
             }
             ++j;
             it.next(p);
+#ifdef SELECT_PROF
+            if (prof_on) { c1 = clock64(); pt[7] += c1 - c0; c0 = c1; }
+#endif
+#ifdef SELECT_PROF
+            if (prof_on) pt[8] += 1;
+#endif
         }
         if (j > 0) {
             named_bar_sync(1, 128);  // run_l of the last group visible to every finishing thread
             finish(fin, j - 1);
         }
+#ifdef SELECT_PROF
+        if (prof_on)
+            printf("select prof CTA0 warp2 per item (%llu items): wait_S %llu ldS %llu max+bar %llu exp+P %llu fence+arrive %llu sum+bar %llu finish %llu (o_wait %llu) tail %llu\n",
+                   pt[8], pt[0] / pt[8], pt[1] / pt[8], pt[2] / pt[8], pt[3] / pt[8], pt[4] / pt[8], pt[5] / pt[8],
+                   pt[6] / pt[8], pt[9] / pt[8], pt[7] / pt[8]);
+#endif
     }
     tc_fence_before();
     __syncthreads();
