@@ -46,9 +46,10 @@ constexpr int STAGE = 16384;             // 8 windows x 2 KB
 constexpr int WIN = 2048;                // 16 tokens x 64 bf16
 constexpr int NTHREADS = 192;
 constexpr uint32_t TMEM_COLS = 256;
-constexpr uint32_t S_COL0 = 0, S_COL1 = 64, O_COL0 = 128, O_COL1 = 144, G_COL0 = 160, G_COL1 = 176;
-constexpr int GROUP_WIN = 32;
-constexpr int PREFETCH_AHEAD = 0;   // items of L2 prefetch ahead of the gathers (2 measured slower: 54 -> 71 ms)            // windows per softmax group (512 keys)
+constexpr uint32_t S_COL0 = 0, S_COL1 = 64, O_COL0 = 128, O_COL1 = 144, G_COL0 = 160;  // G buffer b at G_COL0 + 16 b
+constexpr int NGB = 3;  // G^T buffers: item j+1's G MMA must not wait for item j-1's epilogue
+constexpr int GROUP_WIN = 32;       // windows per softmax group (512 keys)
+constexpr int PREFETCH_AHEAD = 0;   // items of L2 prefetch ahead of the gathers (2 measured slower: 54 -> 71 ms)
 
 struct __align__(1024) SelSmem {
     uint8_t ring[NS][STAGE];
@@ -64,7 +65,7 @@ struct __align__(1024) SelSmem {
     uint64_t wg_full, wg_empty;
     uint64_t s_full[2], s_empty[2];
     uint64_t p_full[2], o_full[2];
-    uint64_t g_empty[2];
+    uint64_t g_empty[NGB];
     uint32_t tmem_base;
 };
 
@@ -83,6 +84,7 @@ struct SelTcParams {
     const float* prior_o;     // hybrid fast path: reference-frame softmax, merged by LSE (or null)
     const float* prior_lse;
     const uint8_t* wg_prep;  // [H][2][8192] bytes
+    int debug;               // bring-up switches (GSA_DEBUG_SELECT): 1 = no P-lo MMAs (timing only)
 };
 
 // Iterates this CTA's (item, group) sequence.
@@ -145,12 +147,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             mbar_init(&sm.q_empty[i], 1);
             mbar_init(&sm.s_full[i], 1);
             mbar_init(&sm.s_empty[i], 128);
-            mbar_init(&sm.g_empty[i], 128);
             mbar_init(&sm.p_full[i], 128);
             mbar_init(&sm.o_full[i], 1);
         }
         mbar_init(&sm.wg_full, 1);
         mbar_init(&sm.wg_empty, 1);
+        for (int i = 0; i < NGB; ++i) mbar_init(&sm.g_empty[i], 128);
         fence_barrier_init();
         prefetch_tmap(&tm_q);
         prefetch_tmap(&tm_k);
@@ -175,7 +177,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         int cur_head = -1;
         int n_heads = 0;      // W_g loads issued
         int64_t n_items = 0;  // items whose Q/Wg prelude has been issued
-        auto load_chunks = [&](const GroupIt& it, const CUtensorMap* tm, bool with_prelude) {
+        auto load_chunks = [&](const GroupIt& it, const CUtensorMap* tm, bool with_prelude, int my_wid) {
             const int h = (int)(it.item / L.windows), w = (int)(it.item - (int64_t)h * L.windows);
             if (with_prelude) {
                 if (h != cur_head) {
@@ -202,7 +204,6 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 ++n_items;
             }
             const int nw = it.group_windows();
-            const int my_wid = lane < nw ? p.rows.window(it.item, (int64_t)it.g * GROUP_WIN + lane) : 0;
             int c1, c2;
             window_coords(L, my_wid, c1, c2);
             if (PREFETCH_AHEAD > 0 && tm == &tm_k && it.g == 0) {
@@ -233,19 +234,40 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 }
             }
         };
-        GroupIt kit, vit;
+        // window ids run two groups ahead of the K loads (one lane per window of the
+        // group): the index loads' round trip overlaps the gathers instead of preceding them
+        GroupIt kit, vit, pit;
         kit.start(p);
         vit.start(p);
+        pit.start(p);
+        auto ids_of = [&](const GroupIt& g) {
+            return (g.valid(p) && lane < g.group_windows()) ? p.rows.window(g.item, (int64_t)g.g * GROUP_WIN + lane) : 0;
+        };
+        int wid_k = ids_of(pit);  // ids of kit's group
+        if (pit.valid(p)) pit.next(p);
+        int wid_n = ids_of(pit);  // ids of the group after kit's
+        if (pit.valid(p)) pit.next(p);
+        auto advance_k = [&]() {
+            wid_k = wid_n;
+            wid_n = ids_of(pit);
+            if (pit.valid(p)) pit.next(p);
+        };
+        int wid_vq = wid_k;  // ids of vit's current group
         if (kit.valid(p)) {
-            load_chunks(kit, &tm_k, true);
+            load_chunks(kit, &tm_k, true, wid_k);
             kit.next(p);
+            wid_vq = wid_k;
+            advance_k();
         }
         while (vit.valid(p)) {
+            const int wv = wid_vq;
             if (kit.valid(p)) {
-                load_chunks(kit, &tm_k, kit.g == 0);
+                load_chunks(kit, &tm_k, kit.g == 0, wid_k);
                 kit.next(p);
+                wid_vq = wid_k;
+                advance_k();
             }
-            load_chunks(vit, &tm_v, false);
+            load_chunks(vit, &tm_v, false, wv);
             vit.next(p);
         }
     } else if (warp == 1) {
@@ -258,7 +280,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             const uint32_t id_o = idesc_bf16(64, 16, 1, 0);
             int st = 0;
             uint32_t fph = 0;
-            uint32_t qph[2] = {0, 0}, sph[2] = {1, 1}, gph[2] = {1, 1}, pph[2] = {0, 0};
+            uint32_t qph[2] = {0, 0}, sph[2] = {1, 1}, pph[2] = {0, 0};
+            uint32_t gphase = (1u << NGB) - 1u;  // bit b: parity to wait on g_empty[b] (first use passes)
             uint32_t wgph = 0;
             int cur_head = -1;
             int64_t n_items = 0;
@@ -275,12 +298,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                         cur_head = h;
                     }
                     // G^T = Wg^T . Q^T (hi + lo), into the item's G buffer
-                    const int gb = (int)(n_items & 1);
-                    mbar_wait(&sm.g_empty[gb], gph[gb]);
-                    gph[gb] ^= 1;
+                    const int gb = (int)(n_items % NGB);
+                    mbar_wait(&sm.g_empty[gb], (gphase >> gb) & 1u);
+                    gphase ^= 1u << gb;
                     tc_fence_after();
 
-                    const uint32_t gcol = tmem + (gb ? G_COL1 : G_COL0);
+                    const uint32_t gcol = tmem + G_COL0 + 16u * (uint32_t)gb;
                     // the last item of this head on this CTA releases W_g
                     const int64_t nxt = it.item + gridDim.x;
                     const bool last_of_head = nxt >= p.items || (int)(nxt / L.windows) != h;
@@ -344,7 +367,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                             const uint64_t va = vdesc + (uint64_t)(ks * 128);
                             const uint64_t po = (uint64_t)(c * 128 + ks * 16);
                             mma_bf16(ocol, va, phi + po, id_o, (c | ks) != 0);
-                            mma_bf16(ocol, va, plo + po, id_o, 1);
+                            if (!(p.debug & 1)) mma_bf16(ocol, va, plo + po, id_o, 1);
                         }
                         mma_commit(&sm.empty[st]);
                     }
@@ -418,9 +441,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             }
             if (f.g != f.ng - 1) return;
             // ------------------------------- epilogue -------------------------------
-            const int gb = (int)(n_fin_items & 1);
+            const int gb = (int)(n_fin_items % NGB);
             uint32_t grr[16];
-            tmem_ld_32x32b_x16(tmem + ((uint32_t)(32 * qd) << 16) + (gb ? G_COL1 : G_COL0), grr);
+            tmem_ld_32x32b_x16(tmem + ((uint32_t)(32 * qd) << 16) + G_COL0 + 16u * (uint32_t)gb, grr);
             tmem_wait_ld();
             tc_fence_before();
             mbar_arrive(&sm.g_empty[gb]);
@@ -740,6 +763,8 @@ cudaError_t tc_select_gate_merge(const SelectArgs& a, cudaStream_t st) {
     p.prior_lse = a.prior_lse;
     p.gate_ctx = a.gate_ctx;
     p.wg_prep = a.wg_prep;
+    p.debug = 0;
+    if (const char* dbg = getenv("GSA_DEBUG_SELECT")) p.debug = atoi(dbg);
     int dev = 0, nsm = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
