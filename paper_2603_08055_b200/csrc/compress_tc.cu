@@ -39,6 +39,7 @@ constexpr int NS = 4;                   // K/V ring stages
 constexpr int TILE = 16384;             // 128 rows x 64 bf16
 constexpr int STAGE = 2 * TILE;         // hi + lo
 constexpr int NTHREADS = 384;           // warps 0-3 / 4-7: softmax WG0 / WG1, 8: TMA, 9: MMA, 10-11 idle
+// (registers are split per SM sub-partition: 3 warps each; setmaxnreg moves 2 x 224 + 56 per SMSP)
 constexpr int NWG = 2;                  // query tiles (softmax warpgroups) per CTA
 constexpr int NSB = 3;                  // S/P buffers in TMEM, rotating over the S(n) sequence
 constexpr uint32_t TMEM_COLS = 512;
@@ -115,6 +116,32 @@ __device__ __forceinline__ float select32(const uint32_t (&v)[32], int e) {
     return __uint_as_float((e & 1) ? a[1] : a[0]);
 }
 
+// The lowest set bit of m (m != 0): its index e and v[e], by a binary search over m's
+// halves fused with a 5-level select tree. Integer/select ALU ops only: __ffs (FLO) and
+// friends issue on the XU pipe, which queues behind the softmax warps' MUFU.EX2 traffic.
+__device__ __forceinline__ float lowest_candidate(const uint32_t (&v)[32], uint32_t m, int& e) {
+    uint32_t a[16];
+    const bool b4 = (m & 0xffffu) == 0u;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) a[i] = b4 ? v[i + 16] : v[i];
+    m = b4 ? m >> 16 : m;
+    const bool b3 = (m & 0xffu) == 0u;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) a[i] = b3 ? a[i + 8] : a[i];
+    m = b3 ? m >> 8 : m;
+    const bool b2 = (m & 0xfu) == 0u;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) a[i] = b2 ? a[i + 4] : a[i];
+    m = b2 ? m >> 4 : m;
+    const bool b1 = (m & 0x3u) == 0u;
+#pragma unroll
+    for (int i = 0; i < 2; ++i) a[i] = b1 ? a[i + 2] : a[i];
+    m = b1 ? m >> 2 : m;
+    const bool b0 = (m & 0x1u) == 0u;
+    e = (b4 ? 16 : 0) | (b3 ? 8 : 0) | (b2 ? 4 : 0) | (b1 ? 2 : 0) | (b0 ? 1 : 0);
+    return __uint_as_float(b0 ? a[1] : a[0]);
+}
+
 // Per-row streaming top-k, run by the thread that owns the row. The row keeps a
 // lower bound LB of its K-th best approximate score and streams every
 // selectable score >= LB - margin into its global candidate list. LB rises via
@@ -128,14 +155,24 @@ struct RowTopk {
     int cnt;           // candidates streamed; -1 = none (invalid row) / overflow
     int ccap;
     float2* dst;
+#ifdef COMPRESS_PROF
+    int dbg;
+#endif
 
     // branch-free: predicated store, select-based count and bin updates
     __device__ __forceinline__ void add(float v, int col) {
         const bool ok = (unsigned)cnt < (unsigned)ccap;  // cnt < 0 (no row / overflowed) is huge unsigned
+#ifdef COMPRESS_PROF
+        if (ok && !(dbg & 512)) dst[cnt] = make_float2(v, __int_as_float(col));
+        if (dbg & 1024) { cnt = ok ? cnt + 1 : -1; return; }
+#else
         if (ok) dst[cnt] = make_float2(v, __int_as_float(col));
+#endif
         cnt = ok ? cnt + 1 : -1;  // reaching ccap overflows the row: exact fallback
-        const float rel = (v - lb) * inv_delta;
-        const int b = min(NBIN - 1, (int)fmaxf(rel, 0.0f));
+        // bin = floor(clamp(rel, 0, 7)) without F2I (XU pipe): a round-down add of 2^23
+        // leaves floor(x) in the mantissa bits
+        const float rel = fminf(fmaxf((v - lb) * inv_delta, 0.0f), (float)(NBIN - 1));
+        const int b = __float_as_int(__fadd_rd(rel, 8388608.0f)) - 0x4B000000;
         const uint32_t inc = (ok && v >= lb) ? 1u << (8 * (b & 3)) : 0u;
         hist[0] = __vaddus4(hist[0], b < 4 ? inc : 0u);
         hist[1] = __vaddus4(hist[1], b < 4 ? 0u : inc);
@@ -143,13 +180,17 @@ struct RowTopk {
     // after each tile: raise LB by the largest j with >= K counted at or above bin j
     __device__ __forceinline__ void raise(int K) {
         int suffix = 0, j = 0;
+        float jf = 0.0f;  // (float)j without I2F (XU pipe)
 #pragma unroll
         for (int b = NBIN - 1; b >= 1; --b) {
             suffix += (int)((hist[b >> 2] >> (8 * (b & 3))) & 0xffu);
-            if (j == 0 && suffix >= K) j = b;
+            if (j == 0 && suffix >= K) {
+                j = b;
+                jf = (float)b;
+            }
         }
         if (j == 0) return;
-        lb += (float)j * delta;
+        lb += jf * delta;
         thr = fmaxf(thr, topk_threshold(lb, eps));
         const uint64_t h = ((uint64_t)hist[1] << 32) | hist[0];
         const uint64_t s = h >> (8 * j);
@@ -246,8 +287,19 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             // so every WG always has its next S computing while it runs a softmax.
             const uint32_t id_s = idesc_bf16(128, 128, 0, 0);
             const uint32_t id_o = idesc_bf16(128, 64, 0, 1);
+#ifdef COMPRESS_PROF
+            const bool mprof = p.prof && blockIdx.x == 0 && blockIdx.y == 0 && lane == 0;
+            unsigned long long mw_full = 0, mw_p = 0, m_t0 = clock64(), m_c;
+#define MPROF_T(acc) if (mprof) { m_c = clock64(); acc += m_c - m_t0; m_t0 = m_c; }
+#define MPROF_MARK() if (mprof) m_t0 = clock64();
+#else
+#define MPROF_T(acc)
+#define MPROF_MARK()
+#endif
             auto wait_tile = [&](int s) {
+                MPROF_MARK();
                 mbar_wait(&sm.full[s % NS], (uint32_t)((s / NS) & 1));
+                MPROF_T(mw_full);
                 tc_fence_after();
             };
             auto issue_S = [&](int n) {
@@ -274,7 +326,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 const int w = n & 1, t = n >> 1;
                 const int s = seq_v(t, T);
                 if (w == 0) wait_tile(s);
+                MPROF_MARK();
                 mbar_wait(&sm.p_full[w][t & 1], (uint32_t)((t >> 1) & 1));
+                MPROF_T(mw_p);
                 tc_fence_after();
                 const uint64_t vh = umma_desc(smem_u32(&sm.ring[s % NS][0]), 16, 1024, 2);
                 const uint64_t vl = umma_desc(smem_u32(&sm.ring[s % NS][TILE]), 16, 1024, 2);
@@ -295,10 +349,22 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             mbar_wait(&sm.q_full, 0);
             tc_fence_after();
             for (int n = 0; n < min(NSB, N); ++n) issue_S(n);
+#ifdef COMPRESS_PROF
+            const unsigned long long m_start = clock64();
+#endif
             for (int n = 0; n < N; ++n) {
                 issue_PV(n);
                 if (n + NSB < N) issue_S(n + NSB);
             }
+#ifdef COMPRESS_PROF
+            if (mprof) {
+                p.prof[6] = mw_full;
+                p.prof[7] = mw_p;
+                p.prof[8] = clock64() - m_start;
+            }
+#endif
+#undef MPROF_T
+#undef MPROF_MARK
         }
     } else {
         // ===================== softmax + streaming top-k (warps 0..7) =====================
@@ -322,12 +388,74 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         tk.cnt = (row_ok && K > 0) ? 0 : -1;
         tk.ccap = p.ccap;
         tk.dst = p.cand + r * p.ccap;
+#ifdef COMPRESS_PROF
+        tk.dbg = p.debug;
+#endif
         float m_used = -INFINITY, l = 0.0f;
 
 #ifdef COMPRESS_PROF
         const bool prof_on = p.prof && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0;
-        unsigned long long pt[6] = {0, 0, 0, 0, 0, 0}, c0 = clock64(), c1;
+        unsigned long long pt[8] = {0, 0, 0, 0, 0, 0, 0, 0}, pb[5] = {0, 0, 0, 0, 0}, c0 = clock64(), c1;
 #endif
+        const bool do_topk = K > 0 && !(p.debug & 1);
+        if (do_topk) {
+            // ---- top-k seed from key tile 0 (its own register scope: peeled off the loop)
+            // initial LB: the largest 16-bit key prefix P with >= K selectable keys >= P<<16
+            // bounds the row's K-th best from below; bins span [LB, max]
+            mbar_wait(&sm.s_full[w], 0u);  // S(n = w) lives in buffer w, first fill
+            __syncwarp();
+            tc_fence_after();
+            uint32_t sr[4][32];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) tmem_ld_32x32b_x32(lane_base + 128 * w + 32 * c, sr[c]);
+            tmem_wait_ld();
+            uint32_t keep[4];
+            {
+                uint4 ex = make_uint4(0, 0, 0, 0);
+                if (p.exbits) ex = __ldg(reinterpret_cast<const uint4*>(p.exbits));
+                const uint32_t exw[4] = {ex.x, ex.y, ex.z, ex.w};
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    const int vc = p.Wk - 32 * c;
+                    keep[c] = (vc >= 32 ? 0xffffffffu : (vc <= 0 ? 0u : ((1u << vc) - 1u))) & ~exw[c];
+                }
+            }
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+#pragma unroll
+                for (int e = 0; e < 32; ++e)
+                    sr[c][e] = ((keep[c] >> e) & 1u) ? fkey(__uint_as_float(sr[c][e])) : 0u;
+            uint32_t res = 0;
+#pragma unroll 1
+            for (int bit = 31; bit >= 16; --bit) {
+                const uint32_t cand = res | (1u << bit);
+                int cnt = 0;
+#pragma unroll
+                for (int c = 0; c < 4; ++c)
+#pragma unroll
+                    for (int e = 0; e < 32; ++e) cnt += sr[c][e] >= cand ? 1 : 0;
+                if (cnt >= K) res = cand;
+            }
+            if (res != 0) {
+                // bin width = (std of the row's first 128 scores) / 8: fine enough
+                // that LB trails the running K-th best by a fraction of the spread
+                float s1 = 0.0f, s2 = 0.0f;
+#pragma unroll
+                for (int c = 0; c < 4; ++c)
+#pragma unroll
+                    for (int e = 0; e < 32; ++e) {
+                        const float x = ((keep[c] >> e) & 1u) ? fkey_inv(sr[c][e]) : 0.0f;
+                        s1 += x;
+                        s2 = fmaf(x, x, s2);
+                    }
+                const float nk = (float)(__popc(keep[0]) + __popc(keep[1]) + __popc(keep[2]) + __popc(keep[3]));
+                const float mean = s1 / nk, var = fmaxf(s2 / nk - mean * mean, 0.0f);
+                tk.lb = fkey_inv(res);
+                tk.thr = topk_threshold(tk.lb, tk.eps);
+                tk.delta = var > 0.0f ? sqrtf(var) * (1.0f / NBIN) : fmaxf(fabsf(tk.lb) * 0.0009765625f, 1e-30f);
+                tk.inv_delta = 1.0f / tk.delta;
+            }
+        }
         for (int t = 0; t < T; ++t) {
             const int n = 2 * t + w, b = n % NSB;
             const uint32_t s_base = lane_base + 128 * b;
@@ -337,36 +465,81 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 #endif
             __syncwarp();  // .sync.aligned tcgen05 ops below need a converged warp
             tc_fence_after();
-            uint32_t sr[4][32];
+            const int valid = p.Wk - t * 128;  // < 128 on the last key tile only
+            uint32_t keep[4];                  // selectable columns (in range, not excluded)
+            {
+                uint4 ex = make_uint4(0, 0, 0, 0);
+                if (do_topk && p.exbits) ex = __ldg(reinterpret_cast<const uint4*>(p.exbits) + t);
+                const uint32_t exw[4] = {ex.x, ex.y, ex.z, ex.w};
 #pragma unroll
-            for (int c = 0; c < 4; ++c) tmem_ld_32x32b_x32(s_base + 32 * c, sr[c]);
-            tmem_wait_ld();
+                for (int c = 0; c < 4; ++c) {
+                    const int vc = valid - 32 * c;
+                    keep[c] = (vc >= 32 ? 0xffffffffu : (vc <= 0 ? 0u : ((1u << vc) - 1u))) & ~exw[c];
+                }
+            }
+            // ---- pass A: chunk maxima of S and the top-k candidate masks. The
+            // 128 scores are live only here; pass B re-reads them from TMEM one chunk at a
+            // time, so the softmax and the top-k run with ~100 registers instead of 200+.
+            float cmax[4];
+            uint32_t cmask[4] = {0u, 0u, 0u, 0u};  // top-k candidate columns per chunk
+            {
+                uint32_t sr[4][32];
+#pragma unroll
+                for (int c = 0; c < 4; ++c) tmem_ld_32x32b_x32(s_base + 32 * c, sr[c]);
+                tmem_wait_ld();
+                if (valid < 128) {
+                    // last key tile: columns past Wk do not exist. -inf goes back to TMEM too,
+                    // so pass B needs no masking code (P = exp2(-inf) = 0)
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) {
+#pragma unroll
+                        for (int e = 0; e < 32; ++e)
+                            if (32 * c + e >= valid) sr[c][e] = __float_as_uint(-INFINITY);
+                        tmem_st_32x32b_x32(s_base + 32 * c, sr[c]);
+                    }
+                    tmem_wait_st();
+                }
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {  // 3-input max trees (short dependency chains)
+                    float a0 = __uint_as_float(sr[c][0]), a1 = __uint_as_float(sr[c][1]);
+                    float a2 = __uint_as_float(sr[c][2]), a3 = __uint_as_float(sr[c][3]);
+#pragma unroll
+                    for (int e = 4; e < 32; e += 4) {
+                        a0 = fmaxf(a0, __uint_as_float(sr[c][e]));
+                        a1 = fmaxf(a1, __uint_as_float(sr[c][e + 1]));
+                        a2 = fmaxf(a2, __uint_as_float(sr[c][e + 2]));
+                        a3 = fmaxf(a3, __uint_as_float(sr[c][e + 3]));
+                    }
+                    cmax[c] = fmaxf(fmaxf(a0, a1), fmaxf(a2, a3));
+                }
+                if (do_topk && !(p.debug & 256)) {
+                    // candidate masks: bit e = (S[e] >= tq) = NOT sign(S - tq) (FADD2), gathered by
+                    // funnel shifts into four independent 8-bit chains per chunk
+                    const float tq = tk.cnt < 0 ? INFINITY : tk.thr;
+                    const float2 ntq = make_float2(-tq, -tq);
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) {
+                        // most chunks hold no candidate of any of the warp's 32 rows late in the row
+                        if (!__any_sync(0xffffffffu, cmax[c] >= tq)) continue;
+                        uint32_t ch[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+                        for (int i = 3; i >= 0; --i)  // element pair 2i, 2i+1 of every 8-element group
+#pragma unroll
+                            for (int j = 0; j < 4; ++j) {
+                                const int e = 8 * j + 2 * i;
+                                const float2 dd = __fadd2_rn(make_float2(__uint_as_float(sr[c][e]), __uint_as_float(sr[c][e + 1])), ntq);
+                                ch[j] = __funnelshift_l(__float_as_uint(dd.y), ch[j], 1);
+                                ch[j] = __funnelshift_l(__float_as_uint(dd.x), ch[j], 1);
+                            }
+                        cmask[c] = ~(ch[0] | (ch[1] << 8) | (ch[2] << 16) | (ch[3] << 24)) & keep[c];
+                    }
+                    if (p.debug & 128) cmask[0] = cmask[1] = cmask[2] = cmask[3] = 0u;  // bring-up: no extraction
+                }
+            }
+            const float mt = fmaxf(fmaxf(cmax[0], cmax[1]), fmaxf(cmax[2], cmax[3]));
 #ifdef COMPRESS_PROF
             if (prof_on) { c1 = clock64(); pt[1] += c1 - c0; c0 = c1; }
 #endif
-            const int valid = p.Wk - t * 128;
-            if (valid < 128) {  // last key tile only: columns past Wk do not exist
-#pragma unroll
-                for (int c = 0; c < 4; ++c)
-#pragma unroll
-                    for (int e = 0; e < 32; ++e)
-                        if (32 * c + e >= valid) sr[c][e] = __float_as_uint(-INFINITY);
-            }
-            float cmax[4];
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {  // 4-way trees (short dependency chains)
-                float a0 = __uint_as_float(sr[c][0]), a1 = __uint_as_float(sr[c][1]);
-                float a2 = __uint_as_float(sr[c][2]), a3 = __uint_as_float(sr[c][3]);
-#pragma unroll
-                for (int e = 4; e < 32; e += 4) {
-                    a0 = fmaxf(a0, __uint_as_float(sr[c][e]));
-                    a1 = fmaxf(a1, __uint_as_float(sr[c][e + 1]));
-                    a2 = fmaxf(a2, __uint_as_float(sr[c][e + 2]));
-                    a3 = fmaxf(a3, __uint_as_float(sr[c][e + 3]));
-                }
-                cmax[c] = fmaxf(fmaxf(a0, a1), fmaxf(a2, a3));
-            }
-            const float mt = fmaxf(fmaxf(cmax[0], cmax[1]), fmaxf(cmax[2], cmax[3]));
             if (t == 0) {
                 m_used = mt;
             } else {
@@ -392,132 +565,109 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     m_used = mnew;
                 }
             }
+            // ---- pass B, per 32-key chunk: P = exp2(S*c2 - m*c2) split P = hi + lo with hi =
+            // P truncated to bf16 (one PRMT packs two his; lo = P - hi is exact in f32, then
+            // rounded: |P - hi - lo| <= 2^-15 |P|) written over the chunk's S; then the
+            // chunk's top-k candidates. The P barrier is released after the last chunk's
+            // stores, before its top-k.
             const float mc = m_used * p.c2;
-            // P = exp2(S*c2 - m*c2), split P = hi + lo with hi = P truncated to bf16
-            // (one PRMT packs two his; lo = P - hi is exact in f32, then rounded:
-            // |P - hi - lo| <= 2^-15 |P|); paired f32 ops (FFMA2/FADD2) halve the ALU work
             const float2 c2v = make_float2(p.c2, p.c2), nmc = make_float2(-mc, -mc);
             const float2 neg1 = make_float2(-1.0f, -1.0f);
             float2 lsum2[2] = {make_float2(0.0f, 0.0f), make_float2(0.0f, 0.0f)};
-#pragma unroll
+            // not unrolled: one copy of the chunk body keeps the hot loop inside the
+            // instruction cache (the unrolled loop measured 20-50% no_instruction stalls)
+            uint32_t mrot = cmask[0], mq1 = cmask[1], mq2 = cmask[2], mq3 = cmask[3];
+#pragma unroll 1
             for (int c = 0; c < 4; ++c) {
-                uint32_t hi[16], lo[16];
+                uint32_t v[32];
+#ifdef COMPRESS_PROF
+                if (prof_on) { c1 = clock64(); pt[3] += c1 - c0; c0 = c1; }
+#endif
+                const uint32_t cb = s_base + 32 * c;
+                tmem_ld_32x32b_x32(cb, v);
+                tmem_wait_ld();
+#ifdef COMPRESS_PROF
+                if (prof_on) { c1 = clock64(); pb[0] += c1 - c0; c0 = c1; }
+#endif
+                {
+                    uint32_t hi[16], lo[16];
 #pragma unroll
-                for (int e2 = 0; e2 < 16; ++e2) {
-                    const float2 x = make_float2(__uint_as_float(sr[c][2 * e2]), __uint_as_float(sr[c][2 * e2 + 1]));
-                    const float2 a = __ffma2_rn(x, c2v, nmc);
-                    const float2 pv = make_float2(ex2_approx(a.x), ex2_approx(a.y));
-                    lsum2[e2 & 1] = __fadd2_rn(lsum2[e2 & 1], pv);
-                    const uint32_t u0 = __float_as_uint(pv.x), u1 = __float_as_uint(pv.y);
-                    hi[e2] = __byte_perm(u0, u1, 0x7632);
-                    const float2 hf = make_float2(__uint_as_float(u0 & 0xffff0000u), __uint_as_float(u1 & 0xffff0000u));
-                    const float2 lf = __ffma2_rn(hf, neg1, pv);
-                    lo[e2] = pack_bf16(lf.x, lf.y);
+                    for (int e2 = 0; e2 < 16; ++e2) {
+                        const float2 x = make_float2(__uint_as_float(v[2 * e2]), __uint_as_float(v[2 * e2 + 1]));
+                        const float2 a = __ffma2_rn(x, c2v, nmc);
+                        const float2 pv = make_float2(ex2_approx(a.x), ex2_approx(a.y));
+                        lsum2[e2 & 1] = __fadd2_rn(lsum2[e2 & 1], pv);
+                        const uint32_t u0 = __float_as_uint(pv.x), u1 = __float_as_uint(pv.y);
+                        hi[e2] = __byte_perm(u0, u1, 0x7632);
+                        const float2 hf = make_float2(__uint_as_float(u0 & 0xffff0000u), __uint_as_float(u1 & 0xffff0000u));
+                        const float2 lf = __ffma2_rn(hf, neg1, pv);
+                        lo[e2] = pack_bf16(lf.x, lf.y);
+                    }
+                    tmem_st_32x32b_x16(cb, hi);
+                    tmem_st_32x32b_x16(cb + 16, lo);
                 }
-                tmem_st_32x32b_x16(s_base + 32 * c, hi);
-                tmem_st_32x32b_x16(s_base + 32 * c + 16, lo);
+#ifdef COMPRESS_PROF
+                if (prof_on) { c1 = clock64(); pb[1] += c1 - c0; c0 = c1; }
+#endif
+                if (c == 3) {
+                    tmem_wait_st();
+                    tc_fence_before();
+                    mbar_arrive(&sm.p_full[w][t & 1]);
+#ifdef COMPRESS_PROF
+                    if (prof_on) { c1 = clock64(); pb[2] += c1 - c0; c0 = c1; }
+#endif
+                }
+                // this chunk's candidates (overlaps the MMAs)
+                uint32_t m = mrot;
+                mrot = mq1;
+                mq1 = mq2;
+                mq2 = mq3;
+#ifdef COMPRESS_PROF
+                {
+                    const unsigned mx = __reduce_max_sync(0xffffffffu, (unsigned)__popc(m));
+                    const unsigned sm_ = __reduce_add_sync(0xffffffffu, (unsigned)__popc(m));
+                    if (prof_on) { pt[2] += mx; pt[6] += sm_; pt[7] += mx ? 1 : 0; }
+                }
+#endif
+                const int col0 = t * 128 + 32 * c;
+#ifdef COMPRESS_PROF
+                if (prof_on) { c1 = clock64(); pb[3] += c1 - c0; c0 = c1; }
+#endif
+                while (m) {
+                    int e;
+                    const float x = lowest_candidate(v, m, e);
+                    m &= m - 1;
+                    tk.add(x, col0 + e);
+                }
+#ifdef COMPRESS_PROF
+                if (prof_on) { c1 = clock64(); pb[4] += c1 - c0; c0 = c1; }
+#endif
             }
-            const float2 ls = __fadd2_rn(lsum2[0], lsum2[1]);
-            l += ls.x + ls.y;
-            tmem_wait_st();
-            tc_fence_before();
-            mbar_arrive(&sm.p_full[w][t & 1]);
+            {
+                const float2 ls = __fadd2_rn(lsum2[0], lsum2[1]);
+                l += ls.x + ls.y;
+            }
 #ifdef COMPRESS_PROF
             if (prof_on) { c1 = clock64(); pt[3] += c1 - c0; c0 = c1; }
 #endif
-
-            // ---- streaming top-k over this tile's approximate scores (overlaps the MMAs)
-            if (K > 0 && !(p.debug & 1)) {
-                uint4 ex = make_uint4(0, 0, 0, 0);
-                if (p.exbits) ex = __ldg(reinterpret_cast<const uint4*>(p.exbits) + t);
-                const uint32_t exw[4] = {ex.x, ex.y, ex.z, ex.w};
-                uint32_t keep[4];
-#pragma unroll
-                for (int c = 0; c < 4; ++c) {
-                    const int vc = valid - 32 * c;
-                    keep[c] = (vc >= 32 ? 0xffffffffu : (vc <= 0 ? 0u : ((1u << vc) - 1u))) & ~exw[c];
-                }
-                if (t == 0) {
-                    // initial LB: the largest 16-bit key prefix P with >= K selectable keys
-                    // >= P<<16 bounds the row's K-th best from below; bins span [LB, max]
-#pragma unroll
-                    for (int c = 0; c < 4; ++c)
-#pragma unroll
-                        for (int e = 0; e < 32; ++e)
-                            sr[c][e] = ((keep[c] >> e) & 1u) ? fkey(__uint_as_float(sr[c][e])) : 0u;
-                    uint32_t res = 0;
-#pragma unroll 1
-                    for (int bit = 31; bit >= 16; --bit) {
-                        const uint32_t cand = res | (1u << bit);
-                        int cnt = 0;
-#pragma unroll
-                        for (int c = 0; c < 4; ++c)
-#pragma unroll
-                            for (int e = 0; e < 32; ++e) cnt += sr[c][e] >= cand ? 1 : 0;
-                        if (cnt >= K) res = cand;
-                    }
-                    // back to scores; excluded / out-of-range columns become NaN (never >= thr)
-#pragma unroll
-                    for (int c = 0; c < 4; ++c)
-#pragma unroll
-                        for (int e = 0; e < 32; ++e) sr[c][e] = __float_as_uint(fkey_inv(sr[c][e]));
-                    if (res != 0) {
-                        // bin width = (std of the row's first 128 scores) / 8: fine enough
-                        // that LB trails the running K-th best by a fraction of the spread
-                        float s1 = 0.0f, s2 = 0.0f;
-#pragma unroll
-                        for (int c = 0; c < 4; ++c)
-#pragma unroll
-                            for (int e = 0; e < 32; ++e) {
-                                const float x = ((keep[c] >> e) & 1u) ? __uint_as_float(sr[c][e]) : 0.0f;
-                                s1 += x;
-                                s2 = fmaf(x, x, s2);
-                            }
-                        const float nk = (float)(__popc(keep[0]) + __popc(keep[1]) + __popc(keep[2]) + __popc(keep[3]));
-                        const float mean = s1 / nk, var = fmaxf(s2 / nk - mean * mean, 0.0f);
-                        tk.lb = fkey_inv(res);
-                        tk.thr = topk_threshold(tk.lb, tk.eps);
-                        tk.delta = var > 0.0f ? sqrtf(var) * (1.0f / NBIN) : fmaxf(fabsf(tk.lb) * 0.0009765625f, 1e-30f);
-                        tk.inv_delta = 1.0f / tk.delta;
-                    }
-                }
-                const float tq = tk.cnt < 0 ? INFINITY : tk.thr;
-#pragma unroll
-                for (int c = 0; c < 4; ++c) {
-                    if (!__any_sync(0xffffffffu, cmax[c] >= tq) || (p.debug & 256)) continue;
-                    // bit e = (S[e] >= tq): the sign of S - tq (FADD2), gathered by funnel shifts
-                    // from e = 31 down; two interleaved chains of 16
-                    uint32_t mh = 0u, ml = 0u;
-                    const float2 ntq = make_float2(-tq, -tq);
-#pragma unroll
-                    for (int e2 = 15; e2 >= 0; --e2) {
-                        const float2 dd = __fadd2_rn(make_float2(__uint_as_float(sr[c][2 * e2]),
-                                                                 __uint_as_float(sr[c][2 * e2 + 1])), ntq);
-                        if (e2 >= 8) {
-                            mh = __funnelshift_l(__float_as_uint(dd.y), mh, 1);
-                            mh = __funnelshift_l(__float_as_uint(dd.x), mh, 1);
-                        } else {
-                            ml = __funnelshift_l(__float_as_uint(dd.y), ml, 1);
-                            ml = __funnelshift_l(__float_as_uint(dd.x), ml, 1);
-                        }
-                    }
-                    uint32_t m = ~((mh << 16) | (ml & 0xffffu)) & keep[c];
-                    if (p.debug & 128) m = 0;  // bring-up: timing without candidate extraction
-                    while (m) {
-                        const int e = __ffs(m) - 1;
-                        m &= m - 1;
-                        tk.add(select32(sr[c], e), t * 128 + 32 * c + e);
-                    }
-                }
-                if (tk.cnt > 0) tk.raise(K);
+            if (do_topk && tk.cnt > 0) tk.raise(K);
 #ifdef COMPRESS_PROF
             if (prof_on) { c1 = clock64(); pt[4] += c1 - c0; c0 = c1; pt[5] += 1; }
 #endif
-            }
             __syncwarp();
         }
 #ifdef COMPRESS_PROF
-        if (prof_on) { for (int i = 0; i < 6; ++i) p.prof[i] = pt[i]; }
+        if (prof_on) {
+            for (int i = 0; i < 6; ++i) p.prof[i] = pt[i];
+            p.prof[9] = pt[2];   // warp extraction iterations (max over lanes, summed over chunks)
+            p.prof[10] = pt[6];  // candidates of the warp's 32 rows
+            p.prof[11] = pt[7];  // chunks with a mask pass
+            p.prof[12] = pb[0];  // pass B: TMEM load + wait
+            p.prof[13] = pb[1];  // pass B: exp2 + P split + TMEM stores
+            p.prof[14] = pb[2];  // pass B: wait_st + arrive
+            p.prof[15] = pb[3];  // pass B: before the extraction loops
+            p.prof[16] = pb[4];  // pass B: extraction loops
+        }
 #endif
         // ------------------------------- epilogue -------------------------------
         mbar_wait(&sm.o_final[w], 0);
@@ -964,7 +1114,7 @@ cudaError_t tc_compress_topk_splits(const CompressSplits* pre, const gsa_tensor&
     p.cand = w.cand;
 #ifdef COMPRESS_PROF
     static unsigned long long* prof_buf = nullptr;
-    if (!prof_buf) cudaMalloc(&prof_buf, 64);
+    if (!prof_buf) cudaMalloc(&prof_buf, 256);
     p.prof = prof_buf;
 #endif
     p.ccap = ccap_for(k_eff, excluded != nullptr);
@@ -977,11 +1127,19 @@ cudaError_t tc_compress_topk_splits(const CompressSplits* pre, const gsa_tensor&
     note_launch();
 #ifdef COMPRESS_PROF
     {
-        unsigned long long hp[6];
+        unsigned long long hp[17];
         cudaMemcpyAsync(hp, p.prof, sizeof(hp), cudaMemcpyDeviceToHost, st);
         cudaStreamSynchronize(st);
-        fprintf(stderr, "compress prof (CTA0 warp0): tiles %llu  wait_S %.0f  ldtm %.0f  softmax+P %.0f  topk %.0f cyc/tile\n", hp[5],
+        fprintf(stderr, "compress prof (CTA0 warp0): tiles %llu  wait_S %.0f  pass A %.0f  pass B (softmax+P+topk) %.0f  raise %.0f cyc/tile\n", hp[5],
                 (double)hp[0] / hp[5], (double)hp[1] / hp[5], (double)hp[3] / hp[5], (double)hp[4] / hp[5]);
+        fprintf(stderr, "compress prof (CTA0 MMA warp): per key tile  wait TMA %.0f  wait P %.0f  total %.0f cyc\n",
+                (double)hp[6] / hp[5], (double)hp[7] / hp[5], (double)hp[8] / hp[5]);
+        fprintf(stderr, "compress prof (CTA0 warp0): extraction iterations %llu  candidates/row %.1f  masked chunks %llu of %llu\n",
+                hp[9], (double)hp[10] / 32.0, hp[11], 4 * hp[5]);
+        fprintf(stderr, "compress prof (CTA0 warp0): pass B per tile: ld %.0f  softmax %.0f  wait_st+arrive %.0f  (rest = top-k)\n",
+                (double)hp[12] / hp[5], (double)hp[13] / hp[5], (double)hp[14] / hp[5]);
+        fprintf(stderr, "compress prof (CTA0 warp0): pass B per tile: pre-extraction %.0f  extraction %.0f\n",
+                (double)hp[15] / hp[5], (double)hp[16] / hp[5]);
     }
 #endif
     if (k_eff > 0) {
