@@ -5,15 +5,15 @@
 // (layer.hpp:99-119), assemble_image_output (layer.hpp:154-170).
 //
 // One work item = (head h, query window w): its 16 queries attend the 16 keys
-// of every window in the plan row (forced ++ top-k). Persistent CTAs (one per
+// of every window in the plan row (forced ++ top-k). Persistent CTAs (two per
 // SM) walk the items head-major; inside a CTA the items' key windows form one
-// global stream of "groups" (<= 32 windows = 512 keys each):
+// global stream of "groups" (<= GROUP_WIN = 16 windows = 256 keys each):
 //
 //   warp 0 (TMA)   : gathers each selected window of K and V straight from the
 //                    head-major [H][M][64] bf16 tensors with a 4-D tensor map
 //                    (box 64 x 4 x 4 = one 2 KB window, 128B-swizzled), 8
 //                    windows per 16 KB ring stage; Q tile per item; W_g (hi/lo
-//                    bf16 split, pre-swizzled) per head.
+//                    bf16 split, pre-swizzled) per head. Two CTAs per SM.
 //   warp 1 (MMA)   : S^T[128 keys x 16 q] = K_chunk . Q^T   (M=128, N=16, K=64)
 //                    G^T[64 x 16]        = W_g^T . Q^T       (hi + lo, M=64)
 //                    O^T[64 x 16]       += V_chunk^T . P^T   (P hi + lo, M=64, K=16/step)
@@ -41,21 +41,37 @@ namespace {
 
 using namespace ptx;
 
-constexpr int NS = 8;                    // ring stages
+// Two CTAs per SM (SEL_CTAS): the per-item chain (gather -> S -> softmax -> PV ->
+// epilogue) is latency-bound with one consumer warpgroup, so a second CTA hides it.
+// That caps shared memory at ~113 KB per CTA: 256-key groups (SEL_GROUP_WIN 16, so
+// P^T buffers are 32 KB) and a 3-stage ring. Measured at V=1000 (select stage):
+// 1 CTA, 512-key groups, 8 stages 53 ms; 2 CTAs, 16-window groups, 3 stages 33 ms;
+// 2 CTAs with 8-window groups 42 ms.
+#ifndef SEL_NS
+#define SEL_NS 3
+#endif
+#ifndef SEL_CTAS
+#define SEL_CTAS 2
+#endif
+#ifndef SEL_GROUP_WIN
+#define SEL_GROUP_WIN 16
+#endif
+constexpr int NS = SEL_NS;               // ring stages
 constexpr int STAGE = 16384;             // 8 windows x 2 KB
 constexpr int WIN = 2048;                // 16 tokens x 64 bf16
 constexpr int NTHREADS = 192;
 constexpr uint32_t TMEM_COLS = 256;
 constexpr uint32_t S_COL0 = 0, S_COL1 = 64, O_COL0 = 128, O_COL1 = 144, G_COL0 = 160;  // G buffer b at G_COL0 + 16 b
 constexpr int NGB = 3;  // G^T buffers: item j+1's G MMA must not wait for item j-1's epilogue
-constexpr int GROUP_WIN = 32;       // windows per softmax group (512 keys)
+constexpr int GROUP_WIN = SEL_GROUP_WIN;  // windows per softmax group (<= 32, 16 keys each)
+constexpr int P_QSTRIDE = GROUP_WIN * 256; // bytes per 8-query half of a P^T buffer
 constexpr int PREFETCH_AHEAD = 0;   // items of L2 prefetch ahead of the gathers (2 measured slower: 54 -> 71 ms)
 
 struct __align__(1024) SelSmem {
     uint8_t ring[NS][STAGE];
     uint8_t q[2][WIN];
     uint8_t wg[2][8192];      // W_g hi / lo, [a][j] 128B-swizzled
-    uint8_t p[2][2][16384];   // [group parity][hi/lo] P^T: [q-group 2][key-chunk 64][8 rows][16 B]
+    uint8_t p[2][2][2 * P_QSTRIDE];  // [group parity][hi/lo] P^T: [q-group 2][key-chunk][8 rows][16 B]
     float red[2][4][16];      // cross-warp max / sum partials
     float run_m[2][16];       // [group parity] running row max (raw score units)
     float run_l[2][16];       // [group parity] running denominator
@@ -122,7 +138,7 @@ __device__ __forceinline__ void window_coords(const DevLayout& L, int wid, int& 
     c2 = f * L.grid_h + wr * 4;
 }
 
-__global__ void __launch_bounds__(NTHREADS, 1)
+__global__ void __launch_bounds__(NTHREADS, SEL_CTAS)
     select_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                      const __grid_constant__ CUtensorMap tm_v, const SelTcParams p) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -355,8 +371,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 tc_fence_after();
                 const int nw = it.group_windows();
                 const uint32_t ocol = tmem + (pb ? O_COL1 : O_COL0);
-                const uint64_t phi = umma_desc(smem_u32(&sm.p[pb][0][0]), 128, 8192, 0);
-                const uint64_t plo = umma_desc(smem_u32(&sm.p[pb][1][0]), 128, 8192, 0);
+                const uint64_t phi = umma_desc(smem_u32(&sm.p[pb][0][0]), 128, P_QSTRIDE, 0);
+                const uint64_t plo = umma_desc(smem_u32(&sm.p[pb][1][0]), 128, P_QSTRIDE, 0);
                 for (int c0 = 0, c = 0; c0 < nw; c0 += 8, ++c) {
                     mbar_wait(&sm.full[st], fph);
                     tc_fence_after();
@@ -608,7 +624,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     }
                     // matrix mi: keys +8*(mi&1), queries 8*(mi>>1); memory row rr = query
                     const int kc = (128 * c + 32 * qd + 16 * hf) / 8 + (mi & 1);
-                    const uint32_t off = (uint32_t)((mi >> 1) * 8192 + kc * 128 + rr * 16);
+                    const uint32_t off = (uint32_t)((mi >> 1) * P_QSTRIDE + kc * 128 + rr * 16);
                     stmatrix_x4_trans(pbase_hi + off, hi[0], hi[1], hi[2], hi[3]);
                     stmatrix_x4_trans(pbase_lo + off, lo[0], lo[1], lo[2], lo[3]);
                 }
@@ -771,7 +787,7 @@ cudaError_t tc_select_gate_merge(const SelectArgs& a, cudaStream_t st) {
     const size_t smem = sizeof(SelSmem) + 1024;
     cudaError_t e = cudaFuncSetAttribute(select_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    const int grid = (int)std::min<int64_t>(nsm, p.items);
+    const int grid = (int)std::min<int64_t>((int64_t)nsm * SEL_CTAS, p.items);
     select_tc_kernel<<<grid, NTHREADS, smem, st>>>(tq, tk, tv, p);
     note_launch();
     return cudaGetLastError();
