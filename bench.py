@@ -301,7 +301,7 @@ def main():
     prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(prof) and world == 1 and geometry_default:
         tr = json.load(open(prof)).get(dom)
-        if tr:  # DRAM bytes (read + write) per launch of the stage's kernel, from one ncu --set full capture
+        if tr and tr.get("views") == args.views:  # DRAM bytes (read + write) per launch of the stage's kernel, from one ncu --set full capture of this workload
             roof["traffic"] = tr["dram_gbytes_per_launch"] * 1e9
             roof["traffic_source"] = "profiles/" + tr["source"]
     per_stage = {}

@@ -8,6 +8,7 @@ import subprocess
 import sys
 
 rep, out = sys.argv[1], sys.argv[2]
+VIEWS = int(sys.argv[4]) if len(sys.argv) > 4 else 1000  # workload of the capture (bench --views)
 rows = list(csv.reader(subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
                                       text=True).stdout.splitlines()))
 h, units = rows[0], rows[1]
@@ -46,7 +47,7 @@ for d in res:
             r, w = gbytes(d["metrics"], "dram__bytes_read.sum"), gbytes(d["metrics"], "dram__bytes_write.sum")
             if r is not None and w is not None:
                 traffic[st] = {"dram_gbytes_per_launch": round(r + w, 3), "read_gb": round(r, 3), "write_gb": round(w, 3),
-                               "source": rep.split("/")[-1]}
+                               "source": rep.split("/")[-1], "views": VIEWS}
 if len(sys.argv) > 3:
     json.dump(traffic, open(sys.argv[3], "w"), indent=1)
 for d in res:
