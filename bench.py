@@ -163,6 +163,82 @@ def run_reference_arm(args):
 
 
 # ------------------------------------------------------------- GPU arm
+def run_stack(args):
+    """BASELINE configs[2] on one GPU: an L-layer global-attention stack. One step
+    = L x (X . W_qkv on cuBLAS bf16 -> GSA layer on strided head views -> head
+    concat to bf16 X), paper_2603_08055_b200.stack. Stage times and the roofline
+    come from layer 0 of each timed step (library CUDA events)."""
+    import ctypes
+
+    import torch
+
+    import paper_2603_08055_b200 as gsa
+    from paper_2603_08055_b200 import _lib
+    from paper_2603_08055_b200.stack import GsaStack
+
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    lib = _lib.load()
+    G = geometry(args.views)
+    L = gsa.build_token_layout(*layout_for(args.views))
+    params = gsa.GsaParams(window_s=S, top_k=TOPK, variant=1 if args.hybrid else 0,
+                           ref_stride=args.hybrid if args.hybrid else 100)
+    st = GsaStack(L, params, args.layers, HEADS, DIM, device=dev, seed=7)
+    x0 = torch.randn(G["M"], HEADS * DIM, generator=torch.Generator(device=dev).manual_seed(7), device=dev,
+                     dtype=torch.float32).to(torch.bfloat16)
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(args.steps)]
+    for row in ev:
+        for e_ in row:
+            e_.record()
+    handles = [(ctypes.c_void_p * 5)(*[e_.cuda_event for e_ in row]) for row in ev]
+    for _ in range(args.warmup):
+        st.forward(x0)
+    torch.cuda.synchronize()
+    n0 = ctypes.c_uint64()
+    lib.gsa_launch_count(ctypes.byref(n0))
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(0) as clocks:
+        start.record()
+        for i in range(args.steps):
+            x = x0
+            for l in range(args.layers):
+                lib.gsa_set_stage_events(handles[i] if l == 0 else None, 5 if l == 0 else 0)
+                x = st.layer(x, l)
+            lib.gsa_set_stage_events(None, 0)
+        stop.record()
+        torch.cuda.synchronize()
+    n1 = ctypes.c_uint64()
+    lib.gsa_launch_count(ctypes.byref(n1))
+    ms = start.elapsed_time(stop) / args.steps
+    names = ("special", "pool", "compress", "select")
+    stage_ms = {n: sum(ev[i][j].elapsed_time(ev[i][j + 1]) for i in range(args.steps)) / args.steps
+                for j, n in enumerate(names)}
+    hbm, tc_peak, _, peak_kind = load_peaks()
+    W, Mi, Ms, M = G["W"], G["Mi"], G["Ms"], G["M"]
+    flops = 4.0 * HEADS * W * W * DIM
+    A = flops / (stage_ms["compress"] / 1e3) / 1e12
+    layer_ms = sum(stage_ms.values())
+    line = {
+        "metric": METRIC, "value": M / (ms / 1e3), "unit": "tokens/s", "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "bf16", "data": "synthetic (torch N(0,1) bf16 X, random-init N(0,1/C) bf16 W_qkv, W_g=N(0,1)/8 f32)",
+        "config": {"workload": f"{args.layers}-layer GSA stack, {args.views} views x ({SPECIAL_PER_VIEW} specials + "
+                               f"{GRID_H}x{GRID_W} patches) = {M} tokens, 16 heads x 64, s=4, top-{TOPK}; per layer "
+                               "QKV GEMM (cuBLAS bf16) + GSA layer + residual", "views": args.views, "layers": args.layers,
+                   "tokens": M, "parallelism": "1 GPU", "l2": "inputs larger than L2 (no flush)"},
+        "ms_per_layer": ms / args.layers,
+        "stage_ms_layer0": {k_: round(v_, 3) for k_, v_ in stage_ms.items()},
+        "projection_and_concat_ms_per_layer": ms / args.layers - layer_ms,
+        "roofline": {"kernel": "compress", "bound": "tensor", "achieved": A, "peak": tc_peak, "unit": "TFLOP/s",
+                     "frac": A / tc_peak, "traffic": None, "peak_kind": peak_kind},
+        "gpu_launches": int((n1.value - n0.value)),
+        "clocks": clocks.summary(),
+        "e2e": None, "cpu_baseline": None,
+    }
+    print(json.dumps(line))
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -178,6 +254,8 @@ def main():
     ap.add_argument("--grid", default="36x36", help="patch grid per view (pi3 518x1036: 36x76)")
     ap.add_argument("--specials-per-view", type=int, default=5, help="VGGT: 5, pi3: 0")
     ap.add_argument("--topk", type=int, default=32)
+    ap.add_argument("--layers", type=int, default=1,
+                    help="L > 1: an L-layer stack (BASELINE configs[2]); each layer = fused QKV GEMM + GSA layer")
     ap.add_argument("--hybrid", type=int, default=0, metavar="REF_STRIDE",
                     help="hybrid selection with reference frames every REF_STRIDE views (0 = plain)")
     args = ap.parse_args()
@@ -186,6 +264,8 @@ def main():
     SPECIAL_PER_VIEW, TOPK = args.specials_per_view, args.topk
     if args.impl == "reference":
         return run_reference_arm(args)
+    if args.layers > 1:
+        return run_stack(args)
 
     import torch
     import torch.distributed as dist

@@ -630,8 +630,8 @@ int gsa_forward(const gsa_tensor* q, const gsa_tensor* k, const gsa_tensor* v, c
     a.gate_ctx = ctx ? ctx->gate : nullptr;
     a.wg_prep = b.wg_prep;
     const bool tc_sel = tc_select_supported(*q, lp.L, a.rows);
-    if (tc_sel && params->variant == 1 && lp.n_forced > 0 && lp.k_eff > 0 && b.kf && q->dim == 64 && k->row_stride == 64 &&
-        v->row_stride == 64 && tc_dense_supported(*q, *k, *v)) {
+    if (tc_sel && params->variant == 1 && lp.n_forced > 0 && lp.k_eff > 0 && b.kf && q->dim == 64 &&
+        tc_dense_supported(*q, *k, *v)) {
         // Hybrid fast path. Every query attends ALL reference-frame keys (selection.cpp:55-59:
         // forced windows lead every plan row), so that part of the softmax is a dense
         // attention of all image queries over the reference frames' keys (one tcgen05 FA
@@ -642,12 +642,19 @@ int gsa_forward(const gsa_tensor* q, const gsa_tensor* k, const gsa_tensor* v, c
         for (int fi = 0; fi < nff; ++fi) {
             const int f = fi * params->ref_stride;  // forced frames 0, r, 2r, ... (selection.cpp:7-12)
             const size_t src_row = (size_t)lp.Ms + (size_t)f * tpf;
-            GSA_CUDA(cudaMemcpy2DAsync(b.kf + (size_t)fi * tpf * 64, (size_t)fk * 64 * 2,
-                                       static_cast<const __nv_bfloat16*>(k->data) + src_row * 64,
-                                       (size_t)k->head_stride * 2, (size_t)tpf * 64 * 2, H, cudaMemcpyDeviceToDevice, st));
-            GSA_CUDA(cudaMemcpy2DAsync(b.vf + (size_t)fi * tpf * 64, (size_t)fk * 64 * 2,
-                                       static_cast<const __nv_bfloat16*>(v->data) + src_row * 64,
-                                       (size_t)v->head_stride * 2, (size_t)tpf * 64 * 2, H, cudaMemcpyDeviceToDevice, st));
+            for (int kv = 0; kv < 2; ++kv) {
+                const gsa_tensor* t = kv ? v : k;
+                __nv_bfloat16* dst = (kv ? b.vf : b.kf) + (size_t)fi * tpf * 64;
+                const __nv_bfloat16* src = static_cast<const __nv_bfloat16*>(t->data) + src_row * t->row_stride;
+                if (t->row_stride == 64) {  // contiguous rows: one 2-D copy over heads
+                    GSA_CUDA(cudaMemcpy2DAsync(dst, (size_t)fk * 64 * 2, src, (size_t)t->head_stride * 2,
+                                               (size_t)tpf * 64 * 2, H, cudaMemcpyDeviceToDevice, st));
+                } else {  // strided rows (e.g. views of a fused QKV projection): one 2-D copy per head
+                    for (int hh = 0; hh < H; ++hh)
+                        GSA_CUDA(cudaMemcpy2DAsync(dst + (size_t)hh * fk * 64, 64 * 2, src + (size_t)hh * t->head_stride,
+                                                   (size_t)t->row_stride * 2, 64 * 2, tpf, cudaMemcpyDeviceToDevice, st));
+                }
+            }
         }
         gsa_tensor tkf{b.kf, GSA_DTYPE_BF16, H, fk, 64, (int64_t)fk * 64, 64};
         gsa_tensor tvf{b.vf, GSA_DTYPE_BF16, H, fk, 64, (int64_t)fk * 64, 64};

@@ -732,7 +732,9 @@ bool make_window_map(CUtensorMap* m, const TensorRef& t, int heads, const DevLay
     EncodeFn enc = get_encode();
     if (!enc) return false;
     cuuint64_t dims[4] = {64, (cuuint64_t)L.grid_w, (cuuint64_t)L.grid_h * L.num_frames, (cuuint64_t)heads};
-    cuuint64_t strides[3] = {128, (cuuint64_t)L.grid_w * 128, (cuuint64_t)t.hs * 2};
+    // rows of rs elements: head-major [H][M][64] (rs = 64) or strided views such as the
+    // token-major [M][3][H][64] output of a fused QKV projection (rs = 3 * H * 64)
+    cuuint64_t strides[3] = {(cuuint64_t)t.rs * 2, (cuuint64_t)L.grid_w * t.rs * 2, (cuuint64_t)t.hs * 2};
     cuuint32_t box[4] = {64, 4, 4, 1};
     cuuint32_t es[4] = {1, 1, 1, 1};
     return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(t.data), dims, strides, box, es,
@@ -741,7 +743,8 @@ bool make_window_map(CUtensorMap* m, const TensorRef& t, int heads, const DevLay
 }
 
 bool tensor_ok(const TensorRef& t) {
-    return t.dtype == GSA_DTYPE_BF16 && t.rs == 64 && t.hs % 8 == 0 && (reinterpret_cast<uintptr_t>(t.data) & 15) == 0;
+    return t.dtype == GSA_DTYPE_BF16 && t.rs >= 64 && t.rs % 8 == 0 && t.hs % 8 == 0 &&
+           (reinterpret_cast<uintptr_t>(t.data) & 15) == 0;
 }
 
 }  // namespace
