@@ -35,7 +35,10 @@ namespace {
 
 using namespace ptx;
 
-constexpr int NS = 4;                   // K/V ring stages
+#ifndef COMP_NS
+#define COMP_NS 4
+#endif
+constexpr int NS = COMP_NS;             // K/V ring stages
 constexpr int TILE = 16384;             // 128 rows x 64 bf16
 constexpr int STAGE = 2 * TILE;         // hi + lo
 constexpr int NTHREADS = 384;           // warps 0-3 / 4-7: softmax WG0 / WG1, 8: TMA, 9: MMA, 10-11 idle
@@ -53,7 +56,8 @@ constexpr int KCAP = 128;               // max k_eff on this path
 __host__ __device__ constexpr int ccap_for(int k, bool excl = false) { return k <= 32 ? (excl ? 1024 : 512) : 2048; }
 __host__ __device__ constexpr int surv_for(int k) { return k <= 32 ? 64 : 256; }
 constexpr int NBIN = 8;                 // threshold histogram bins (8-bit saturating counters)
-constexpr float EPS_REL = 0.00048828125f;          // 2^-11
+constexpr float EPS_REL = 0.00048828125f;          // 2^-11: split + accumulation error, x |q| max|kc - kbar|
+constexpr float EPS_REF = 7.62939453125e-06f;      // 2^-17: the reference's own f32 rounding, x |q| max|kc|
 constexpr float DELTA_REL = 9.5367431640625e-07f;  // 2^-20: collapse of distinct sums under *scale
 
 struct __align__(1024) CompSmem {
@@ -74,7 +78,11 @@ struct CompParams {
     float scale, c2;
     int kv_tiles;
     const float* qnorm;       // [H][Wq]
-    const float* kmax;        // [H]
+    const float* kmax;        // [H] max |kc|
+    const float* cmax;        // [H] max |kc - kbar| (the scores are computed on centred keys)
+    const float* kbar;        // [H][64] per-head mean key: S' = q.(kc - kbar) = S - q.kbar
+    const float* qc;          // [H][Wq][64] f32 (lse correction q.kbar)
+    int64_t qc_hs;
     const uint32_t* exbits;   // [ceil(Wk/32)] or null
     float* out;
     int64_t out_hs, out_rs;
@@ -383,7 +391,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         tk.thr = -INFINITY;
         tk.delta = 1.0f;
         tk.inv_delta = 1.0f;
-        tk.eps = row_ok ? EPS_REL * p.qnorm[r] * p.kmax[h] : 0.0f;
+        tk.eps = row_ok ? EPS_REL * p.qnorm[r] * p.cmax[h] + EPS_REF * p.qnorm[r] * p.kmax[h] : 0.0f;
         tk.hist[0] = tk.hist[1] = 0u;
         tk.cnt = (row_ok && K > 0) ? 0 : -1;
         tk.ccap = p.ccap;
@@ -687,7 +695,15 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     *reinterpret_cast<float4*>(dst + 32 * half + e) =
                         make_float4(__uint_as_float(o[half][e]) * inv, __uint_as_float(o[half][e + 1]) * inv,
                                     __uint_as_float(o[half][e + 2]) * inv, __uint_as_float(o[half][e + 3]) * inv);
-            if (p.lse) p.lse[r] = m_used * p.scale + logf(l);
+            if (p.lse) {
+                // the softmax ran on S' = S - q.kbar (a per-row shift): add it back to the lse
+                const float* qrow = p.qc + (int64_t)h * p.qc_hs + (int64_t)grow * 64;
+                const float* kb = p.kbar + h * 64;
+                float qk = 0.0f;
+#pragma unroll 8
+                for (int j = 0; j < 64; ++j) qk = fmaf(__ldg(qrow + j), __ldg(kb + j), qk);
+                p.lse[r] = m_used * p.scale + logf(l) + qk * p.scale;
+            }
             if (K > 0) {
                 p.cand_n[r] = tk.cnt < 0 ? 0 : tk.cnt;
                 p.flag[r] = (tk.cnt < 0 || (p.debug & 16)) ? 1 : 0;
@@ -715,7 +731,8 @@ template <int PER, int SLOTS>
 __global__ void __launch_bounds__(256) rescore_kernel(const float* __restrict__ qc, int64_t q_hs,
                                                       const float* __restrict__ kc, int heads, int Wq, int Wk,
                                                       float scale, int k_eff, const float* __restrict__ qnorm,
-                                                      const float* __restrict__ kmax, const float2* __restrict__ cand,
+                                                      const float* __restrict__ kmax, const float* __restrict__ cmax,
+                                                      const float2* __restrict__ cand,
                                                       const int* __restrict__ cand_n, uint8_t* flag, int32_t* topk,
                                                       float* guide) {
     constexpr int CC = PER * 32, SV = SLOTS * 32;  // candidate capacity / survivor capacity
@@ -743,7 +760,7 @@ __global__ void __launch_bounds__(256) rescore_kernel(const float* __restrict__ 
         for (int i = 0; i < PER; ++i) cnt += key[i] >= c ? 1 : 0;
         if ((int)__reduce_add_sync(0xffffffffu, (unsigned)cnt) >= k_eff) res = c;
     }
-    const float eps = EPS_REL * qnorm[r] * kmax[h];
+    const float eps = EPS_REL * qnorm[r] * cmax[h] + EPS_REF * qnorm[r] * kmax[h];  // as in the main kernel
     const float thr = topk_threshold(fkey_inv(res), eps);
     // compact the survivors (through shared memory) into SLOTS slots per lane
     float2* sv = surv_all + (threadIdx.x / 32) * SV;
@@ -835,11 +852,72 @@ __global__ void split_kernel(const float* __restrict__ x, int64_t hs, int64_t rs
     if (norm && c == 0 && row < (int64_t)heads * W) norm[row] = sqrtf(sq);
 }
 
+// per-head mean key kbar[h] = sum_w kc[h][w] / Wk (fixed summation order: deterministic).
+// Any fixed vector would do -- the scores are shifted by q.kbar per row, which changes
+// neither the softmax nor the ranking -- the mean makes |kc - kbar| small when the
+// key windows share a large common component (over-smoothed activations), which is
+// what keeps the top-k error margin narrower than the spread of the scores.
+constexpr int KMEAN_CHUNKS = 64;  // row chunks per head (grid H x 64): the 20 MB/head read is spread over the GPU
+__global__ void kmean_partial_kernel(const float* __restrict__ x, int64_t hs, int64_t rs, int W, float* part_out) {
+    const int h = blockIdx.y, ch = blockIdx.x, j = threadIdx.x & 63, part = threadIdx.x >> 6;
+    const int w0 = (int)((int64_t)W * ch / KMEAN_CHUNKS), w1 = (int)((int64_t)W * (ch + 1) / KMEAN_CHUNKS);
+    float acc = 0.0f;
+    for (int w = w0 + part; w < w1; w += 4) acc += x[(int64_t)h * hs + (int64_t)w * rs + j];
+    __shared__ float red[4][64];
+    red[part][j] = acc;
+    __syncthreads();
+    if (part == 0) part_out[((int64_t)h * KMEAN_CHUNKS + ch) * 64 + j] = (red[0][j] + red[1][j]) + (red[2][j] + red[3][j]);
+}
+__global__ void kmean_final_kernel(const float* __restrict__ part_in, int W, float* kbar) {
+    const int h = blockIdx.x, j = threadIdx.x;
+    float acc = 0.0f;
+    for (int ch = 0; ch < KMEAN_CHUNKS; ++ch) acc += part_in[((int64_t)h * KMEAN_CHUNKS + ch) * 64 + j];
+    kbar[h * 64 + j] = acc / (float)W;
+}
+
+// c = kc - kbar (f32) -> bf16 hi, lo + norms |c| and |kc|
+__global__ void center_split_kernel(const float* __restrict__ x, int64_t hs, int64_t rs, int heads, int W,
+                                    const float* __restrict__ kbar, __nv_bfloat16* hi, __nv_bfloat16* lo,
+                                    float* cnorm, float* knorm) {
+    const int64_t row = (int64_t)blockIdx.x * (blockDim.x / 8) + threadIdx.x / 8;
+    const int c = threadIdx.x & 7;
+    float sq = 0.0f, sk = 0.0f;
+    if (row < (int64_t)heads * W) {
+        const int h = (int)(row / W), w = (int)(row % W);
+        const float* src = x + (int64_t)h * hs + (int64_t)w * rs + 8 * c;
+        __nv_bfloat16 H8[8], L8[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const float k = src[i];
+            const float v = k - kbar[h * 64 + 8 * c + i];
+            H8[i] = __float2bfloat16_rn(v);
+            L8[i] = __float2bfloat16_rn(v - __bfloat162float(H8[i]));
+            sq = fmaf(v, v, sq);
+            sk = fmaf(k, k, sk);
+        }
+        *reinterpret_cast<uint4*>(hi + row * 64 + 8 * c) = *reinterpret_cast<uint4*>(H8);
+        *reinterpret_cast<uint4*>(lo + row * 64 + 8 * c) = *reinterpret_cast<uint4*>(L8);
+    }
+#pragma unroll
+    for (int o = 1; o < 8; o <<= 1) {
+        sq += __shfl_xor_sync(0xffffffffu, sq, o);
+        sk += __shfl_xor_sync(0xffffffffu, sk, o);
+    }
+    if (c == 0 && row < (int64_t)heads * W) {
+        // 1 ulp of headroom: the norms bound error terms, they must not round low
+        cnorm[row] = sqrtf(sq) * 1.0000002f;
+        knorm[row] = sqrtf(sk) * 1.0000002f;
+    }
+}
+
 // per-head max of the key-window norms (order-free, deterministic)
+// grid (chunks, H); out[h] zeroed beforehand; norms are >= 0, so the f32 bit patterns
+// order like the values and an integer atomicMax merges the chunks (order-free)
 __global__ void rowmax_kernel(const float* __restrict__ norm, int W, float* out) {
-    const int h = blockIdx.x;
+    const int h = blockIdx.y;
+    const int i0 = (int)((int64_t)W * blockIdx.x / gridDim.x), i1 = (int)((int64_t)W * (blockIdx.x + 1) / gridDim.x);
     float m = 0.0f;
-    for (int i = threadIdx.x; i < W; i += blockDim.x) m = fmaxf(m, norm[(int64_t)h * W + i]);
+    for (int i = i0 + threadIdx.x; i < i1; i += blockDim.x) m = fmaxf(m, norm[(int64_t)h * W + i]);
     __shared__ float red[32];
     for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
     if ((threadIdx.x & 31) == 0) red[threadIdx.x / 32] = m;
@@ -847,7 +925,7 @@ __global__ void rowmax_kernel(const float* __restrict__ norm, int W, float* out)
     if (threadIdx.x < 32) {
         m = threadIdx.x < blockDim.x / 32 ? red[threadIdx.x] : 0.0f;
         for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-        if (threadIdx.x == 0) out[h] = m;
+        if (threadIdx.x == 0) atomicMax(reinterpret_cast<int*>(out) + h, __float_as_int(m));
     }
 }
 
@@ -967,6 +1045,7 @@ __global__ void __launch_bounds__(XR_THREADS) exact_row_kernel(const float* __re
 struct Ws {
     __nv_bfloat16 *qh, *ql, *kh, *kl, *vh, *vl;
     float *qn, *kn, *kmax;
+    float *cn, *cmax, *kbar, *kpart;
     uint32_t* exbits;
     float2* cand;
     int* cand_n;
@@ -996,6 +1075,10 @@ Ws carve_ws(void* base, int heads, int Wq, int Wk, int k_eff, bool dry) {
     w.qn = reinterpret_cast<float*>(take(nq * 4));
     w.kn = reinterpret_cast<float*>(take(nk * 4));
     w.kmax = reinterpret_cast<float*>(take((size_t)heads * 4));
+    w.cn = reinterpret_cast<float*>(take(nk * 4));
+    w.cmax = reinterpret_cast<float*>(take((size_t)heads * 4));
+    w.kbar = reinterpret_cast<float*>(take((size_t)heads * 64 * 4));
+    w.kpart = reinterpret_cast<float*>(take((size_t)heads * KMEAN_CHUNKS * 64 * 4));
     w.exbits = reinterpret_cast<uint32_t*>(take((size_t)((Wk + 127) / 128) * 16));
     w.cand = reinterpret_cast<float2*>(take(nq * (size_t)ccap_for(k_eff, true) * 8));
     w.cand_n = reinterpret_cast<int*>(take(nq * 4));
@@ -1076,14 +1159,24 @@ cudaError_t tc_compress_topk_splits(const CompressSplits* pre, const gsa_tensor&
         const unsigned qb = (unsigned)(((int64_t)H * Wq + 31) / 32), kb = (unsigned)(((int64_t)H * Wk + 31) / 32);
         split_kernel<<<qb, 256, 0, st>>>(static_cast<const float*>(qc.data), qc.head_stride, qc.row_stride, H, Wq,
                                           w.qh, w.ql, w.qn);
-        split_kernel<<<kb, 256, 0, st>>>(static_cast<const float*>(kc.data), kc.head_stride, kc.row_stride, H, Wk,
-                                          w.kh, w.kl, w.kn);
         split_kernel<<<kb, 256, 0, st>>>(static_cast<const float*>(vc.data), vc.head_stride, vc.row_stride, H, Wk,
                                           w.vh, w.vl, nullptr);
-        note_launch(3);
+        note_launch(2);
     }
-    rowmax_kernel<<<H, 256, 0, st>>>(kn, Wk, w.kmax);
-    note_launch();
+    // centred keys for the scores (kc - kbar), written over the K splits
+    kmean_partial_kernel<<<dim3(KMEAN_CHUNKS, H), 256, 0, st>>>(static_cast<const float*>(kc.data), kc.head_stride,
+                                                                 kc.row_stride, Wk, w.kpart);
+    kmean_final_kernel<<<H, 64, 0, st>>>(w.kpart, Wk, w.kbar);
+    center_split_kernel<<<(unsigned)(((int64_t)H * Wk + 31) / 32), 256, 0, st>>>(
+        static_cast<const float*>(kc.data), kc.head_stride, kc.row_stride, H, Wk, w.kbar, w.kh, w.kl, w.cn, w.kn);
+    kh = w.kh;
+    kl = w.kl;
+    kn = w.kn;
+    cudaMemsetAsync(w.kmax, 0, (size_t)H * 4, st);
+    cudaMemsetAsync(w.cmax, 0, (size_t)H * 4, st);
+    rowmax_kernel<<<dim3(32, H), 256, 0, st>>>(kn, Wk, w.kmax);
+    rowmax_kernel<<<dim3(32, H), 256, 0, st>>>(w.cn, Wk, w.cmax);
+    note_launch(5);
     const int tiles = (Wk + 127) / 128;
     if (excluded) {
         exbits_kernel<<<(tiles * 4 + 127) / 128, 128, 0, st>>>(excluded, Wk, tiles * 4, w.exbits);
@@ -1106,6 +1199,10 @@ cudaError_t tc_compress_topk_splits(const CompressSplits* pre, const gsa_tensor&
     p.kv_tiles = tiles;
     p.qnorm = qn;
     p.kmax = w.kmax;
+    p.cmax = w.cmax;
+    p.kbar = w.kbar;
+    p.qc = static_cast<const float*>(qc.data);
+    p.qc_hs = qc.head_stride;
     p.exbits = excluded ? w.exbits : nullptr;
     p.out = out;
     p.out_hs = out_hs;
@@ -1149,15 +1246,15 @@ cudaError_t tc_compress_topk_splits(const CompressSplits* pre, const gsa_tensor&
         if (k_eff <= 32 && !excluded) {
             static_assert(ccap_for(32) == 16 * 32 && surv_for(32) == 2 * 32, "rescore instance");
             rescore_kernel<16, 2><<<(unsigned)((rows + 7) / 8), 256, 8 * 64 * sizeof(float2), st>>>(
-                qcp, qc.head_stride, kcp, H, Wq, Wk, scale, k_eff, qn, w.kmax, w.cand, w.cand_n, w.flag, topk, guide);
+                qcp, qc.head_stride, kcp, H, Wq, Wk, scale, k_eff, qn, w.kmax, w.cmax, w.cand, w.cand_n, w.flag, topk, guide);
         } else if (k_eff <= 32) {
             static_assert(ccap_for(32, true) == 32 * 32, "rescore instance");
             rescore_kernel<32, 2><<<(unsigned)((rows + 7) / 8), 256, 8 * 64 * sizeof(float2), st>>>(
-                qcp, qc.head_stride, kcp, H, Wq, Wk, scale, k_eff, qn, w.kmax, w.cand, w.cand_n, w.flag, topk, guide);
+                qcp, qc.head_stride, kcp, H, Wq, Wk, scale, k_eff, qn, w.kmax, w.cmax, w.cand, w.cand_n, w.flag, topk, guide);
         } else {
             static_assert(ccap_for(128) == 64 * 32 && ccap_for(128, true) == 64 * 32 && surv_for(128) == 8 * 32, "rescore instance");
             rescore_kernel<64, 8><<<(unsigned)((rows + 7) / 8), 256, 8 * 256 * sizeof(float2), st>>>(
-                qcp, qc.head_stride, kcp, H, Wq, Wk, scale, k_eff, qn, w.kmax, w.cand, w.cand_n, w.flag, topk, guide);
+                qcp, qc.head_stride, kcp, H, Wq, Wk, scale, k_eff, qn, w.kmax, w.cmax, w.cand, w.cand_n, w.flag, topk, guide);
         }
         note_launch();
         // rows whose candidate list overflowed (near-tie floods): exact recompute per row

@@ -401,3 +401,29 @@ def test_hybrid_fast_path_matches_reference(gsa, ref, lt, ref_stride, k):
     assert np.abs(out - rf["out"]).max() < 1e-4 and rel_l2(out, rf["out"]) < 1e-5
     assert np.abs(host(ctx.o_sel) - rf["o_sel"]).max() < 1e-4
     assert np.abs(host(ctx.lse_sel) - rf["lse_sel"]).max() < 1e-4
+
+
+@pytest.mark.parametrize("eps", [0.2, 0.02])
+def test_oversmoothed_keys_bitexact(gsa, ref, eps):
+    """Keys sharing a large common component (deep-layer, over-smoothed activations):
+    |kc| >> spread of the scores. The scores run on centred keys (kc - kbar), so the
+    top-k error margin scales with |kc - kbar|; indices stay bit-exact and the lse
+    (shift added back) within 1e-4 of the reference."""
+    lt = (40, 8, 36, 36, 4)
+    L = gsa.build_token_layout(*lt)
+    M = L.total_tokens
+    g = torch.Generator(device="cuda").manual_seed(4)
+    q = torch.randn(4, M, 64, generator=g, device="cuda").to(torch.bfloat16)
+    base = 2.0 * torch.randn(4, 1, 64, generator=g, device="cuda")
+    k = (base + eps * torch.randn(4, M, 64, generator=g, device="cuda")).to(torch.bfloat16)
+    v = torch.randn(4, M, 64, generator=g, device="cuda").to(torch.bfloat16)
+    wg = torch.randn(4, 64, 64, generator=g, device="cuda") / 8
+    p = gsa.GsaParams(window_s=4, top_k=32)
+    out, ctx = gsa.gsa_forward(q, k, v, wg, L, p, context=True)
+    f = lambda t: t.float().cpu().numpy()
+    rf = ref.forward(f(q), f(k), f(v), f(wg), lt, top_k=32, variant=0, ref_stride=2)
+    np.testing.assert_array_equal(ctx.topk.cpu().numpy(), rf["topk"])
+    o = host(out)
+    assert np.abs(o - rf["out"]).max() < 1e-4 and rel_l2(o, rf["out"]) < 1e-5
+    if "lse_comp" in rf:
+        assert np.abs(host(ctx.lse_comp) - rf["lse_comp"]).max() < 1e-4
