@@ -254,6 +254,8 @@ def main():
     ap.add_argument("--grid", default="36x36", help="patch grid per view (pi3 518x1036: 36x76)")
     ap.add_argument("--specials-per-view", type=int, default=5, help="VGGT: 5, pi3: 0")
     ap.add_argument("--topk", type=int, default=32)
+    ap.add_argument("--e2e-heads-per-group", type=int, default=2,
+                    help="e2e host pipeline granularity: heads per H2D / compute / D2H group")
     ap.add_argument("--layers", type=int, default=1,
                     help="L > 1: an L-layer stack (BASELINE configs[2]); each layer = fused QKV GEMM + GSA layer")
     ap.add_argument("--hybrid", type=int, default=0, metavar="REF_STRIDE",
@@ -423,7 +425,7 @@ def main():
             dq = dk = dv = None
             # host -> host through the public API, pipelined over head groups
             # (H2D of group g+1 and D2H of group g-1 overlap the layer on group g)
-            pipe = gsa.HostPipeline(heads_per_group=4, device=dev)
+            pipe = gsa.HostPipeline(heads_per_group=args.e2e_heads_per_group, device=dev)
 
             def e2e_step():
                 pipe.forward(hq, hk, hv, wg, L, params, hout)

@@ -472,7 +472,7 @@ class HostPipeline:
     Device buffers are allocated once per (shape, dtype) and reused.
     """
 
-    def __init__(self, heads_per_group: int = 4, device="cuda"):
+    def __init__(self, heads_per_group: int = 2, device="cuda"):
         self.g = heads_per_group
         self.device = torch.device(device)
         self.s_in = torch.cuda.Stream(self.device)
