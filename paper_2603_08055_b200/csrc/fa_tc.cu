@@ -34,6 +34,9 @@ constexpr int NSB = 3;               // S/P buffers in TMEM, rotating over the S
 constexpr uint32_t TMEM_COLS = 512;
 constexpr uint32_t O_COL0 = 384;     // O of WG w: [384 + 64 w, +64); S/P buffer b: [128 b, +128)
 constexpr float RESCALE_LOG2 = 8.0f;
+#ifndef FA_PF
+#define FA_PF 24  // measured: special 41.3 -> 40.8 ms at V=1000
+#endif
 
 struct __align__(1024) FaSmem {
     uint8_t q[NWG][TILE];
@@ -133,6 +136,13 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             for (int t = 0; t < T; ++t) {
                 load(&tm_v, t);
                 if (t + 2 < T) load(&tm_k, t + 2);
+                // warm L2 FA_PF tiles ahead of the ring: the CTA that first touches a K/V tile
+                // of its (head, split) group otherwise waits on DRAM (followers hit L2)
+                if (FA_PF > 0 && t + 2 + FA_PF < T && elect_one()) {
+                    tma_prefetch_3d(&tm_k, 0, (t_begin + t + 2 + FA_PF) * 128, h);
+                    tma_prefetch_3d(&tm_v, 0, (t_begin + t + 2 + FA_PF) * 128, h);
+                }
+                __syncwarp();
             }
         } else if (warp == 9 && T > 0) {
             // ================================ MMA ================================
