@@ -48,6 +48,15 @@ constexpr int NSB = 3;                  // S/P buffers in TMEM, rotating over th
 constexpr uint32_t TMEM_COLS = 512;
 constexpr uint32_t O_COL0 = 384;        // O of WG w: [384 + 64 w, +64); S/P buffer b: [128 b, +128)
 constexpr float RESCALE_LOG2 = 8.0f;
+#ifndef COMP_SM_REGS
+#define COMP_SM_REGS 224
+#define COMP_PROD_REGS 56
+#endif
+#ifndef COMP_PB_UNROLL
+#define COMP_PB_UNROLL 2
+#endif
+constexpr int SM_REGS = COMP_SM_REGS, PROD_REGS = COMP_PROD_REGS;  // 8 x 32 x SM + 4 x 32 x PROD <= 384 x 168
+constexpr int PB_UNROLL = COMP_PB_UNROLL;
 constexpr int KCAP = 128;               // max k_eff on this path
 // candidates a row may stream out (more: exact per-row fallback) and survivors
 // of the approximate radix select handed to the exact re-score: sized by k
@@ -107,8 +116,8 @@ __device__ __forceinline__ float topk_threshold(float tau, float eps) {
     return tau - (2.0f * eps + DELTA_REL * fabsf(tau));
 }
 
-__device__ __forceinline__ void setmaxnreg_inc() { asm volatile("setmaxnreg.inc.sync.aligned.u32 224;\n" ::: "memory"); }
-__device__ __forceinline__ void setmaxnreg_dec() { asm volatile("setmaxnreg.dec.sync.aligned.u32 56;\n" ::: "memory"); }
+__device__ __forceinline__ void setmaxnreg_inc() { asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(SM_REGS) : "memory"); }
+__device__ __forceinline__ void setmaxnreg_dec() { asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(PROD_REGS) : "memory"); }
 
 // v[e] for a runtime e without local memory: a 5-level select tree
 __device__ __forceinline__ float select32(const uint32_t (&v)[32], int e) {
@@ -582,10 +591,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             const float2 c2v = make_float2(p.c2, p.c2), nmc = make_float2(-mc, -mc);
             const float2 neg1 = make_float2(-1.0f, -1.0f);
             float2 lsum2[2] = {make_float2(0.0f, 0.0f), make_float2(0.0f, 0.0f)};
-            // not unrolled: one copy of the chunk body keeps the hot loop inside the
-            // instruction cache (the unrolled loop measured 20-50% no_instruction stalls)
+            // unrolled by 2 only: the fully unrolled loop did not fit the instruction cache
+            // (20-50 % no_instruction stalls); measured at V=1000: x1 82.2 ms, x2 76-78 ms, x4 85 ms
             uint32_t mrot = cmask[0], mq1 = cmask[1], mq2 = cmask[2], mq3 = cmask[3];
-#pragma unroll 1
+#pragma unroll PB_UNROLL
             for (int c = 0; c < 4; ++c) {
                 uint32_t v[32];
 #ifdef COMPRESS_PROF
