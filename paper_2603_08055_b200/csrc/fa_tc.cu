@@ -34,6 +34,13 @@ constexpr int NSB = 3;               // S/P buffers in TMEM, rotating over the S
 constexpr uint32_t TMEM_COLS = 512;
 constexpr uint32_t O_COL0 = 384;     // O of WG w: [384 + 64 w, +64); S/P buffer b: [128 b, +128)
 constexpr float RESCALE_LOG2 = 8.0f;
+#ifndef FA_TWO_PASS
+#define FA_TWO_PASS 1
+#endif
+#ifndef FA_PB_UNROLL
+#define FA_PB_UNROLL 4  // measured (special, V=1000): single pass 41.0 ms; two-pass x1 44.5, x2 41.8, x4 39.1-39.7
+#endif
+constexpr int PB_UNROLL = FA_PB_UNROLL;
 #ifndef FA_PF
 #define FA_PF 24  // measured: special 41.3 -> 40.8 ms at V=1000
 #endif
@@ -216,10 +223,13 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             const int valid = p.mk - (t_begin + t) * 128;  // keys of this tile that exist
             if (valid < 128) {
 #pragma unroll
-                for (int c = 0; c < 4; ++c)
+                for (int c = 0; c < 4; ++c) {
 #pragma unroll
                     for (int e = 0; e < 32; ++e)
                         if (32 * c + e >= valid) sr[c][e] = __float_as_uint(-INFINITY);
+                    if (FA_TWO_PASS) tmem_st_32x32b_x32(s_base + 32 * c, sr[c]);  // pass B re-reads TMEM
+                }
+                if (FA_TWO_PASS) tmem_wait_st();
             }
             float a0 = __uint_as_float(sr[0][0]), a1 = __uint_as_float(sr[1][0]);
             float a2 = __uint_as_float(sr[2][0]), a3 = __uint_as_float(sr[3][0]);
@@ -261,12 +271,22 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             const float2 c2v = make_float2(p.c2, p.c2), nmc = make_float2(-mc, -mc);
             const float2 neg1 = make_float2(-1.0f, -1.0f);
             float2 lsum2[2] = {make_float2(0.0f, 0.0f), make_float2(0.0f, 0.0f)};
-#pragma unroll
+            // FA_TWO_PASS: the 128 scores are live only through the max; the P pass re-reads
+            // one 32-key chunk at a time from TMEM (fewer live registers, a chunk loop
+            // unrolled by PB_UNROLL instead of a fully unrolled tile)
+#pragma unroll PB_UNROLL
             for (int c = 0; c < 4; ++c) {
                 uint32_t hi[16], lo[16];
+                uint32_t vv[32];
+                if (FA_TWO_PASS) {
+                    tmem_ld_32x32b_x32(s_base + 32 * c, vv);
+                    tmem_wait_ld();
+                }
 #pragma unroll
                 for (int e2 = 0; e2 < 16; ++e2) {
-                    const float2 x = make_float2(__uint_as_float(sr[c][2 * e2]), __uint_as_float(sr[c][2 * e2 + 1]));
+                    const uint32_t s0 = FA_TWO_PASS ? vv[2 * e2] : sr[c & 3][2 * e2];
+                    const uint32_t s1 = FA_TWO_PASS ? vv[2 * e2 + 1] : sr[c & 3][2 * e2 + 1];
+                    const float2 x = make_float2(__uint_as_float(s0), __uint_as_float(s1));
                     const float2 a = __ffma2_rn(x, c2v, nmc);
                     const float2 pv = (p.debug & 2) ? __ffma2_rn(a, c2v, c2v) : make_float2(ex2_approx(a.x), ex2_approx(a.y));
                     lsum2[e2 & 1] = __fadd2_rn(lsum2[e2 & 1], pv);
