@@ -119,20 +119,6 @@ __device__ __forceinline__ float topk_threshold(float tau, float eps) {
 __device__ __forceinline__ void setmaxnreg_inc() { asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(SM_REGS) : "memory"); }
 __device__ __forceinline__ void setmaxnreg_dec() { asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(PROD_REGS) : "memory"); }
 
-// v[e] for a runtime e without local memory: a 5-level select tree
-__device__ __forceinline__ float select32(const uint32_t (&v)[32], int e) {
-    uint32_t a[16];
-#pragma unroll
-    for (int i = 0; i < 16; ++i) a[i] = (e & 16) ? v[i + 16] : v[i];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) a[i] = (e & 8) ? a[i + 8] : a[i];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) a[i] = (e & 4) ? a[i + 4] : a[i];
-#pragma unroll
-    for (int i = 0; i < 2; ++i) a[i] = (e & 2) ? a[i + 2] : a[i];
-    return __uint_as_float((e & 1) ? a[1] : a[0]);
-}
-
 // The lowest set bit of m (m != 0): its index e and v[e], by a binary search over m's
 // halves fused with a 5-level select tree. Integer/select ALU ops only: __ffs (FLO) and
 // friends issue on the XU pipe, which queues behind the softmax warps' MUFU.EX2 traffic.
