@@ -10,3 +10,4 @@
 #include "gsa/selection.hpp"
 #include "gsa/tensor.hpp"
 #include "gsa/types.hpp"
+#include "gsa/workload.hpp"

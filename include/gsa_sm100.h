@@ -229,6 +229,12 @@ int gsa_project_qkv(const float* x, int tokens, int model_dim, const float* w_q,
 int gsa_forward_stats(const gsa_layout* layout, const gsa_params* params, int heads,
                       uint64_t* scores_computed, uint64_t* keys_attended);
 
+/* selection_sparsity (declared at the reference's proj/include/gsa/workload.hpp:112 but
+ * never defined there): 1 - attended fine keys per image query /
+ * image_tokens, attended = (|forced windows| + k_eff) * s^2 with k_eff = min(k,
+ * selectable windows) (plain: min(k, num_windows) * s^2). Host arithmetic only. */
+int gsa_selection_sparsity(const gsa_layout* layout, const gsa_params* params, double* sparsity);
+
 /* Instrumentation (bench.py, profiling). gsa_set_stage_events: when n >= 5,
  * subsequent gsa_forward calls on this thread record cudaEvent_t events[0..4]
  * on `stream` at: start, after the special path, after pooling, after the

@@ -81,6 +81,7 @@ def load() -> C.CDLL:
     L.gsa_forward.argtypes = [T, T, T, T, Lp, P, T, C.POINTER(GsaContextC), C.POINTER(C.c_int), vp, C.c_size_t, vp]
     L.gsa_forward_with_plan.argtypes = [T, T, T, T, Lp, P, vp, vp, T, vp, C.c_size_t, vp]
     L.gsa_forward_stats.argtypes = [Lp, P, i32, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]
+    L.gsa_selection_sparsity.argtypes = [Lp, P, C.POINTER(C.c_double)]
     S = C.POINTER(GsaShard)
     L.gsa_shard_workspace_bytes.restype = C.c_size_t
     L.gsa_shard_workspace_bytes.argtypes = [Lp, P, S, i32, i32]
@@ -99,7 +100,7 @@ EXPORTED_SYMBOLS = [
     "gsa_avg_pool_tokens", "gsa_upsample_nearest", "gsa_tiled_attention", "gsa_special_token_attention",
     "gsa_compressed_attention_topk_workspace_bytes", "gsa_compressed_attention_topk", "gsa_forced_windows",
     "gsa_build_selection_plan", "gsa_build_selection_plan_workspace_bytes", "gsa_block_sparse_attention",
-    "gsa_gate", "gsa_forward_workspace_bytes", "gsa_forward", "gsa_forward_with_plan", "gsa_forward_stats",
+    "gsa_gate", "gsa_forward_workspace_bytes", "gsa_forward", "gsa_forward_with_plan", "gsa_forward_stats", "gsa_selection_sparsity",
     "gsa_set_stage_events", "gsa_launch_count", "gsa_shard_workspace_bytes", "gsa_shard_pool", "gsa_shard_compress",
     "gsa_shard_attend", "gsa_project_qkv",
 ]

@@ -976,6 +976,19 @@ int gsa_forward_stats(const gsa_layout* layout, const gsa_params* p, int heads, 
     return GSA_OK;
 }
 
+int gsa_selection_sparsity(const gsa_layout* layout, const gsa_params* p, double* sparsity) {
+    GSA_TRY(check_layout(layout));
+    GSA_TRY(gsa_validate_params(p, layout));
+    if (!sparsity) return fail(GSA_ERR_GENERIC, "gsa_selection_sparsity: null output");
+    const DevLayout L = make_dev_layout(*layout);
+    int nf = 0;
+    const int sel = selectable_windows(L, p->variant, p->ref_stride, &nf);
+    const int k_eff = p->top_k < sel ? p->top_k : sel;
+    const double attended = (double)(nf + k_eff) * L.s * L.s;  // forced ++ dynamic, deduplicated
+    *sparsity = L.image_tokens > 0 ? 1.0 - attended / (double)L.image_tokens : 0.0;
+    return GSA_OK;
+}
+
 int gsa_set_stage_events(void* const* events, int n) {
     if (n < 5 || !events) {
         g_n_stage_events = 0;

@@ -441,6 +441,14 @@ def forward_stats(layout: TokenLayout, params: GsaParams, heads: int) -> tuple[i
     return a.value, b.value
 
 
+def selection_sparsity(layout: TokenLayout, params: GsaParams) -> float:
+    """selection_sparsity (declared at workload.hpp:112, undefined in the
+    reference): 1 - attended fine keys per image query / image_tokens."""
+    out = C.c_double()
+    _check(_lib.load().gsa_selection_sparsity(C.byref(layout.c()), C.byref(params.c()), C.byref(out)))
+    return out.value
+
+
 def project_qkv(x: torch.Tensor, w_q: torch.Tensor, w_k: torch.Tensor, w_v: torch.Tensor,
                 dtype: torch.dtype = torch.float32):
     """project_qkv (layer.hpp:48-76): x [tokens, C] f32, w_* [H, C, d] f32 ->
