@@ -34,6 +34,13 @@ constexpr int NSB = 3;               // S/P buffers in TMEM, rotating over the S
 constexpr uint32_t TMEM_COLS = 512;
 constexpr uint32_t O_COL0 = 384;     // O of WG w: [384 + 64 w, +64); S/P buffer b: [128 b, +128)
 constexpr float RESCALE_LOG2 = 8.0f;
+#ifndef FA_MIN_WAVES
+#define FA_MIN_WAVES 8  // key splits: enough CTAs for this many waves of 148 SMs
+#endif
+#ifndef FA_SM_REGS
+#define FA_SM_REGS 224
+#define FA_PROD_REGS 56
+#endif
 #ifndef FA_TWO_PASS
 #define FA_TWO_PASS 1
 #endif
@@ -69,8 +76,8 @@ struct FaParams {
     int debug;        // bring-up switches (GSA_DEBUG_FA, timing only): 1 = no Pl.V MMA, 2 = FFMA instead of ex2
 };
 
-__device__ __forceinline__ void setmaxnreg_inc() { asm volatile("setmaxnreg.inc.sync.aligned.u32 224;\n" ::: "memory"); }
-__device__ __forceinline__ void setmaxnreg_dec() { asm volatile("setmaxnreg.dec.sync.aligned.u32 56;\n" ::: "memory"); }
+__device__ __forceinline__ void setmaxnreg_inc() { asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(FA_SM_REGS) : "memory"); }
+__device__ __forceinline__ void setmaxnreg_dec() { asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(FA_PROD_REGS) : "memory"); }
 
 // load order = the MMA issuer's first-use order: K0 K1 V0 K2 V1 ... K(T-1) V(T-2) V(T-1)
 __device__ __forceinline__ int seq_k(int t) { return t == 0 ? 0 : 2 * t - 1; }
@@ -416,7 +423,7 @@ bool tc_dense_supported(const gsa_tensor& q, const gsa_tensor& k, const gsa_tens
 // key splits: enough CTAs for ~8 waves of 148 SMs while each split keeps >= 16 key tiles
 int fa_splits(int qpairs, int heads, int kv_tiles) {
     int splits = 1;
-    while (qpairs * heads * splits < 8 * 148 && kv_tiles / (splits * 2) >= 16) splits *= 2;
+    while (qpairs * heads * splits < FA_MIN_WAVES * 148 && kv_tiles / (splits * 2) >= 16) splits *= 2;
     return splits;
 }
 
