@@ -52,6 +52,9 @@ constexpr float RESCALE_LOG2 = 8.0f;
 #define COMP_SM_REGS 224
 #define COMP_PROD_REGS 56
 #endif
+#ifndef COMP_MASK_VOTE
+#define COMP_MASK_VOTE 1
+#endif
 #ifndef COMP_PB_UNROLL
 #define COMP_PB_UNROLL 2
 #endif
@@ -523,7 +526,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 #pragma unroll
                     for (int c = 0; c < 4; ++c) {
                         // most chunks hold no candidate of any of the warp's 32 rows late in the row
-                        if (!__any_sync(0xffffffffu, cmax[c] >= tq)) continue;
+                        if (COMP_MASK_VOTE && !__any_sync(0xffffffffu, cmax[c] >= tq)) continue;
                         uint32_t ch[4] = {0u, 0u, 0u, 0u};
 #pragma unroll
                         for (int i = 3; i >= 0; --i)  // element pair 2i, 2i+1 of every 8-element group
