@@ -300,8 +300,8 @@ int gsa_compressed_attention_topk(const gsa_tensor* qc, const gsa_tensor* kc, co
     if (k_eff_out) *k_eff_out = k_eff;
     if (W == 0) return GSA_OK;
     GSA_TRY(generic_supported(qc->dim, 1));
-    if (k_eff > 128)
-        return fail(GSA_ERR_UNSUPPORTED, "fused_compressed_attention_topk: k_eff=%d > 128 not implemented on sm_100a yet", k_eff);
+    if (k_eff > 2048)
+        return fail(GSA_ERR_UNSUPPORTED, "fused_compressed_attention_topk: k_eff=%d > 2048 not implemented on sm_100a yet", k_eff);
     GSA_CUDA(tc_compress_topk(*qc, *kc, *vc, k_eff, scale, excluded, static_cast<float*>(out->data),
                               out->head_stride, out->row_stride, lse, indices, guide, workspace, ws_bytes,
                               (cudaStream_t)stream));
@@ -483,8 +483,8 @@ int layer_checks(const gsa_tensor* q, const gsa_tensor* k, const gsa_tensor* v, 
     const int sel = selectable_windows(L, p->variant, p->ref_stride, &lp->n_forced);
     lp->k_eff = p->top_k < sel ? p->top_k : sel;
     lp->scale = resolved_scale(p->scale, q->dim);
-    if (lp->k_eff > 128)
-        return fail(GSA_ERR_UNSUPPORTED, "gsa_forward: k_eff=%d > 128 not implemented on sm_100a yet", lp->k_eff);
+    if (lp->k_eff > 2048)
+        return fail(GSA_ERR_UNSUPPORTED, "gsa_forward: k_eff=%d > 2048 not implemented on sm_100a yet", lp->k_eff);
     return GSA_OK;
 }
 
@@ -751,7 +751,7 @@ int shard_checks(const gsa_layout* layout, const gsa_params* p, const gsa_shard*
     const int sel = selectable_windows(L, p->variant, p->ref_stride, &lp.n_forced);
     lp.k_eff = p->top_k < sel ? p->top_k : sel;
     lp.scale = resolved_scale(p->scale, dim);
-    if (lp.k_eff > 128) return fail(GSA_ERR_UNSUPPORTED, "k_eff=%d > 128 not implemented on sm_100a yet", lp.k_eff);
+    if (lp.k_eff > 2048) return fail(GSA_ERR_UNSUPPORTED, "k_eff=%d > 2048 not implemented on sm_100a yet", lp.k_eff);
     gsa_layout lq{0, sh->frame_end - sh->frame_begin, layout->grid_h, layout->grid_w, layout->window_s};
     if (lq.num_frames == 0) lq.num_frames = 1;  // placeholder geometry; an empty shard does no work
     sp->Lq = make_dev_layout(lq);

@@ -1040,6 +1040,203 @@ __global__ void __launch_bounds__(XR_THREADS) exact_row_kernel(const float* __re
     }
 }
 
+// ---------------------------------------------------------------------------------------
+// Large budgets (KCAP < k_eff <= LK_KMAX; the 2-5 % points of the budget sweep, SURVEY
+// §8(f) #2). The streaming candidate lists of the main kernel would need ~k(1+ln(W/k))
+// entries per row, so the softmax kernel runs without top-k and this kernel selects
+// from EXACT scores: a CTA takes LK_ROWS query rows of one head, streams Kc tiles
+// through shared memory (each tile serves all LK_ROWS rows), writes the rows'
+// order-preserving score keys to its scratch, then per row (all 256 threads): a 4-pass
+// 8-bit radix select for the k-th key T, the keys > T plus the lowest-index keys == T,
+// a bitonic sort by (score desc, index asc) = topk_better (compression.hpp:67-73).
+// ---------------------------------------------------------------------------------------
+#ifndef LK_CTAS_N
+#define LK_CTAS_N 296
+#endif
+constexpr int LK_ROWS = 32, LK_THREADS = 256, LK_KT = 64, LK_CTAS = LK_CTAS_N;
+constexpr int LK_KMAX = 2048;
+constexpr int LK_QS = 68;  // padded row strides (floats) of the shared q / k tiles: no bank conflicts
+constexpr size_t LK_SMEM = (size_t)(LK_ROWS + LK_KT) * LK_QS * 4 + (size_t)LK_KMAX * 8 + (size_t)LK_ROWS * 256 * 4;
+
+__global__ void __launch_bounds__(LK_THREADS) largek_topk_kernel(
+    const float* __restrict__ qc, int64_t q_hs, const float* __restrict__ kc, int heads, int Wq, int Wk, float scale,
+    int k_eff, const uint32_t* __restrict__ exbits, uint32_t* scratch, int32_t* topk, float* guide) {
+    extern __shared__ __align__(16) uint8_t lk_smem[];
+    float* qs = reinterpret_cast<float*>(lk_smem);                           // [LK_ROWS][LK_QS]
+    float* ks = qs + LK_ROWS * LK_QS;                                        // [LK_KT][LK_QS]
+    unsigned long long* sb = reinterpret_cast<unsigned long long*>(ks + LK_KT * LK_QS);  // [LK_KMAX] sort buffer
+    int* rhist = reinterpret_cast<int*>(sb + LK_KMAX);                       // [LK_ROWS][256] pass-0 histograms
+    __shared__ int hist[256];
+    __shared__ int sh_digit, sh_above, sh_cnt_gt, sh_eq_taken;
+    __shared__ int warp_cnt[LK_THREADS / 32];
+    uint32_t* sk = scratch + (size_t)blockIdx.x * LK_ROWS * Wk;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int blocks_per_head = (Wq + LK_ROWS - 1) / LK_ROWS;
+    const int nblocks = heads * blocks_per_head;
+    for (int blk = blockIdx.x; blk < nblocks; blk += gridDim.x) {
+        const int h = blk / blocks_per_head, w0 = (blk - h * blocks_per_head) * LK_ROWS;
+        const int nr = min(LK_ROWS, Wq - w0);
+        __syncthreads();
+        for (int i = tid; i < LK_ROWS * 256; i += LK_THREADS) rhist[i] = 0;
+        for (int i = tid; i < LK_ROWS * 64; i += LK_THREADS)
+            qs[(i / 64) * LK_QS + (i & 63)] = (i / 64) < nr ? qc[(int64_t)h * q_hs + (int64_t)(w0 + i / 64) * 64 + (i & 63)] : 0.0f;
+        // ---- exact scores of the block's rows against every key window
+        for (int kt0 = 0; kt0 < Wk; kt0 += LK_KT) {
+            __syncthreads();
+            for (int i = tid; i < LK_KT * 16; i += LK_THREADS) {
+                const int j = kt0 + i / 16;
+                const float4 v = j < Wk ? reinterpret_cast<const float4*>(kc + ((int64_t)h * Wk + j) * 64)[i & 15]
+                                        : make_float4(0.f, 0.f, 0.f, 0.f);
+                *reinterpret_cast<float4*>(ks + (i / 16) * LK_QS + 4 * (i & 15)) = v;
+            }
+            __syncthreads();
+            const int r = tid >> 3;  // row of this thread; 8 threads per row, keys jj, jj+8, ...
+            if (r < nr) {
+                for (int jj = tid & 7; jj < LK_KT; jj += 8) {
+                    const int j = kt0 + jj;
+                    if (j >= Wk) break;
+                    // dot.hpp:11-23 order (scalar __fmul_rn/__fadd_rn: the paired FMUL2/FADD2
+                    // forms get contracted into FFMA2 and measured 54 index mismatches in 1.8 M)
+                    ExactDot4 d;
+                    d.zero();
+                    const float4* a = reinterpret_cast<const float4*>(qs + r * LK_QS);
+                    const float4* b = reinterpret_cast<const float4*>(ks + jj * LK_QS);
+#pragma unroll
+                    for (int x = 0; x < 16; ++x) {
+                        const float4 av = a[x], bv = b[x];
+                        d.step(av.x, av.y, av.z, av.w, bv.x, bv.y, bv.z, bv.w);
+                    }
+                    const float sc = d.finish(scale);
+                    const bool ex = exbits && ((exbits[j >> 5] >> (j & 31)) & 1u);
+                    // +0.0f folds -0 into +0: the keys order like topk_better's float compare
+                    const uint32_t key = ex ? 0u : fkey(sc + 0.0f);
+                    sk[(size_t)r * Wk + j] = key;
+                    atomicAdd(&rhist[r * 256 + (key >> 24)], 1);  // radix pass 0, fused
+                }
+            }
+        }
+        __syncthreads();
+        // ---- per row: radix select, collect, sort, write
+        for (int r = 0; r < nr; ++r) {
+            const uint32_t* rk = sk + (size_t)r * Wk;
+            uint32_t prefix = 0;
+            int need = k_eff;  // still to take at or below the current prefix
+            for (int pass = 0; pass < 4; ++pass) {
+                const int shift = 24 - 8 * pass;
+                if (pass == 0) {  // accumulated while the scores were written
+                    for (int i = tid; i < 256; i += LK_THREADS) hist[i] = rhist[r * 256 + i];
+                    __syncthreads();
+                } else {
+                    for (int i = tid; i < 256; i += LK_THREADS) hist[i] = 0;
+                    __syncthreads();
+                    for (int j = tid; j < Wk; j += LK_THREADS) {
+                        const uint32_t key = rk[j];
+                        if ((key >> (shift + 8)) == prefix) atomicAdd(&hist[(key >> shift) & 255u], 1);
+                    }
+                    __syncthreads();
+                }
+                if (warp == 0) {
+                    // suffix sums over 256 bins: lane l owns bins 8l..8l+7
+                    int c[8], tot = 0;
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                        c[i] = hist[8 * lane + i];
+                        tot += c[i];
+                    }
+                    int incl = tot;  // suffix scan over lanes: bins of lanes >= this one
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const int v = __shfl_down_sync(0xffffffffu, incl, o);
+                        if (lane + o < 32) incl += v;
+                    }
+                    const int above = incl - tot;  // count in the bins of higher lanes
+                    // digit d: suffix(d+1) < need <= suffix(d)
+                    int suf = above, found = -1, above_d = 0;
+#pragma unroll
+                    for (int i = 7; i >= 0; --i) {
+                        if (found < 0 && suf + c[i] >= need) {
+                            found = 8 * lane + i;
+                            above_d = suf;
+                        }
+                        suf += c[i];
+                    }
+                    const unsigned b = __ballot_sync(0xffffffffu, found >= 0);
+                    const int src = 31 - __clz(b);  // the highest lane holding the digit
+                    const int d = __shfl_sync(0xffffffffu, found, src);
+                    const int ab = __shfl_sync(0xffffffffu, above_d, src);
+                    if (lane == 0) {
+                        sh_digit = d;
+                        sh_above = ab;
+                    }
+                }
+                __syncthreads();
+                prefix = (prefix << 8) | (uint32_t)sh_digit;
+                need -= sh_above;
+            }
+            const uint32_t T = prefix;  // the k-th largest key; `need` keys equal to T are taken
+            // collect: keys > T (their count is k_eff - need) in any order, then the `need`
+            // lowest-index keys == T, in index order
+            if (tid == 0) {
+                sh_cnt_gt = 0;
+                sh_eq_taken = 0;
+            }
+            __syncthreads();
+            for (int j0 = 0; j0 < Wk; j0 += LK_THREADS) {
+                const int j = j0 + tid;
+                const uint32_t key = j < Wk ? rk[j] : 0u;
+                const bool gt = j < Wk && key > T;
+                const bool eq = j < Wk && key == T;
+                if (gt) {
+                    const int slot = atomicAdd(&sh_cnt_gt, 1);
+                    sb[slot] = ((unsigned long long)key << 32) | (0xffffffffu - (uint32_t)j);
+                }
+                // ties in index order: block-wide exclusive prefix of eq
+                const unsigned be = __ballot_sync(0xffffffffu, eq);
+                if (lane == 0) warp_cnt[warp] = __popc(be);
+                __syncthreads();
+                int before = 0, tot = 0;
+                for (int i = 0; i < LK_THREADS / 32; ++i) {
+                    before += i < warp ? warp_cnt[i] : 0;
+                    tot += warp_cnt[i];
+                }
+                const int rank = sh_eq_taken + before + __popc(be & ((1u << lane) - 1u));
+                if (eq && rank < need)
+                    sb[(k_eff - need) + rank] = ((unsigned long long)key << 32) | (0xffffffffu - (uint32_t)j);
+                __syncthreads();
+                if (tid == 0) sh_eq_taken += tot;
+            }
+            __syncthreads();
+            // bitonic sort of sb[0..n2) descending (pad with 0 = below every real entry)
+            int n2 = 1;
+            while (n2 < k_eff) n2 <<= 1;
+            for (int i = k_eff + tid; i < n2; i += LK_THREADS) sb[i] = 0ull;
+            __syncthreads();
+            for (int size = 2; size <= n2; size <<= 1) {
+                for (int stride = size >> 1; stride > 0; stride >>= 1) {
+                    for (int i = tid; i < n2 / 2; i += LK_THREADS) {
+                        const int lo = 2 * i - (i & (stride - 1));
+                        const int hi = lo + stride;
+                        const bool desc = (lo & size) == 0;
+                        const unsigned long long a = sb[lo], b = sb[hi];
+                        if ((a < b) == desc) {
+                            sb[lo] = b;
+                            sb[hi] = a;
+                        }
+                    }
+                    __syncthreads();
+                }
+            }
+            const int64_t row = (int64_t)h * Wq + w0 + r;
+            for (int i = tid; i < k_eff; i += LK_THREADS) {
+                const unsigned long long e = sb[i];
+                topk[row * k_eff + i] = (int32_t)(0xffffffffu - (uint32_t)(e & 0xffffffffu));
+                if (guide) guide[row * k_eff + i] = fkey_inv((uint32_t)(e >> 32));
+            }
+            __syncthreads();
+        }
+    }
+}
+
 struct Ws {
     __nv_bfloat16 *qh, *ql, *kh, *kl, *vh, *vl;
     float *qn, *kn, *kmax;
@@ -1078,12 +1275,13 @@ Ws carve_ws(void* base, int heads, int Wq, int Wk, int k_eff, bool dry) {
     w.kbar = reinterpret_cast<float*>(take((size_t)heads * 64 * 4));
     w.kpart = reinterpret_cast<float*>(take((size_t)heads * KMEAN_CHUNKS * 64 * 4));
     w.exbits = reinterpret_cast<uint32_t*>(take((size_t)((Wk + 127) / 128) * 16));
-    w.cand = reinterpret_cast<float2*>(take(nq * (size_t)ccap_for(k_eff, true) * 8));
+    const bool large_k = k_eff > KCAP;  // exact large-budget selection: no candidate lists
+    w.cand = reinterpret_cast<float2*>(take(large_k ? 8 : nq * (size_t)ccap_for(k_eff, true) * 8));
     w.cand_n = reinterpret_cast<int*>(take(nq * 4));
     w.flag = reinterpret_cast<uint8_t*>(take(nq));
     w.blocks = reinterpret_cast<int*>(take(nq * 4));  // flagged rows
     w.nblocks = reinterpret_cast<int*>(take(4));
-    w.scratch = reinterpret_cast<uint32_t*>(take((size_t)XR_CTAS * Wk * 4));
+    w.scratch = reinterpret_cast<uint32_t*>(take((size_t)(large_k ? LK_CTAS * LK_ROWS : XR_CTAS) * Wk * 4));
     w.used = off + 256;
     return w;
 }
@@ -1100,13 +1298,13 @@ size_t tc_compress_workspace_bytes(int heads, int windows, int dim, int k_eff) {
 }
 
 size_t tc_compress_workspace_bytes_qk(int heads, int wq, int wk, int dim, int k_eff) {
-    if (dim != 64 || k_eff > KCAP) return 0;
+    if (dim != 64 || k_eff > LK_KMAX) return 0;
     return carve_ws(nullptr, heads, wq, wk, k_eff, true).used;
 }
 
 bool tc_compress_split_buffers(void* ws, size_t ws_bytes, int heads, int windows, int dim, int k_eff,
                                CompressSplits* out) {
-    if (dim != 64 || k_eff > KCAP || !ws || ws_bytes < carve_ws(nullptr, heads, windows, windows, k_eff, true).used)
+    if (dim != 64 || k_eff > LK_KMAX || !ws || ws_bytes < carve_ws(nullptr, heads, windows, windows, k_eff, true).used)
         return false;
     Ws w = carve_ws(ws, heads, windows, windows, k_eff, false);
     *out = CompressSplits{w.qh, w.ql, w.kh, w.kl, w.vh, w.vl, w.qn, w.kn};
@@ -1142,7 +1340,7 @@ cudaError_t tc_compress_topk_splits(const CompressSplits* pre, const gsa_tensor&
     ex.guide = guide;
     ex.k_eff = k_eff;
     ex.excluded = excluded;
-    const bool tc_ok = qc.dim == 64 && k_eff <= KCAP && contiguous_f32(qc) && contiguous_f32(kc) &&
+    const bool tc_ok = qc.dim == 64 && k_eff <= LK_KMAX && contiguous_f32(qc) && contiguous_f32(kc) &&
                        contiguous_f32(vc) && tmap_encode_fn() != nullptr && ws &&
                        ws_bytes >= carve_ws(nullptr, H, Wq, Wk, k_eff, true).used && Wq > 0 && Wk > 0;
     if (!tc_ok) return launch_attn_f32(ex, st);
@@ -1191,7 +1389,7 @@ cudaError_t tc_compress_topk_splits(const CompressSplits* pre, const gsa_tensor&
     p.heads = H;
     p.Wq = Wq;
     p.Wk = Wk;
-    p.k_eff = k_eff;
+    p.k_eff = k_eff > KCAP ? 0 : k_eff;  // large budgets: softmax only here, exact selection below
     p.scale = scale;
     p.c2 = scale * 1.4426950408889634f;
     p.kv_tiles = tiles;
@@ -1237,6 +1435,17 @@ cudaError_t tc_compress_topk_splits(const CompressSplits* pre, const gsa_tensor&
                 (double)hp[15] / hp[5], (double)hp[16] / hp[5]);
     }
 #endif
+    if (k_eff > KCAP) {
+        const size_t lk_smem = LK_SMEM;
+        cudaError_t e2 = cudaFuncSetAttribute(largek_topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lk_smem);
+        if (e2 != cudaSuccess) return e2;
+        largek_topk_kernel<<<LK_CTAS, LK_THREADS, lk_smem, st>>>(static_cast<const float*>(qc.data), qc.head_stride,
+                                                                  static_cast<const float*>(kc.data), H, Wq, Wk, scale,
+                                                                  k_eff, excluded ? w.exbits : nullptr, w.scratch, topk,
+                                                                  guide);
+        note_launch();
+        return cudaGetLastError();
+    }
     if (k_eff > 0) {
         const int64_t rows = (int64_t)H * Wq;
         const float* qcp = static_cast<const float*>(qc.data);

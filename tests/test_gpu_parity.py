@@ -115,12 +115,63 @@ def test_compress_topk_tc_adversarial(gsa, orc, kind, W, k):
     assert (np.abs(host(r.lse) - l_ref) / np.maximum(1.0, np.abs(l_ref))).max() < 1e-4
 
 
-def test_compress_large_k_is_reported_unsupported(gsa):
-    # k_eff > 128 (the 2-25% budget sweep) is not implemented yet:
-    # it must fail loudly, never silently truncate
-    x = torch.zeros(1, 300, 64, device="cuda")
+def test_compress_k_beyond_2048_is_reported_unsupported(gsa):
+    # budgets beyond 2048 windows per row (the 10-25 % sweep points) are not implemented:
+    # they must fail loudly, never silently truncate
+    x = torch.zeros(1, 3000, 64, device="cuda")
     with pytest.raises(gsa.Unsupported):
-        gsa.fused_compressed_attention_topk(x, x, x, 200, 0.125)
+        gsa.fused_compressed_attention_topk(x, x, x, 2100, 0.125)
+
+
+@pytest.mark.parametrize("kind,W,k,excl", [("normal", 3000, 300, False), ("ties", 700, 200, False),
+                                           ("sharp", 2000, 1024, False), ("normal", 1500, 2048, False),
+                                           ("normal", 2500, 500, True), ("pooled_bf16", 3240, 810, False)])
+def test_compress_large_k_exact(gsa, orc, kind, W, k, excl):
+    """k in (128, 2048] (the 2-5 % budget-sweep points): exact scores,
+    radix select and a sort by (score desc, index asc) -- indices and guide scores
+    bit-exact with the reference order, incl. mass ties and hybrid exclusion."""
+    rng = np.random.default_rng(W + k)
+    H = 2
+    if kind == "ties":
+        qc, kc, vc = (rng.integers(-2, 3, size=(H, W, 64)).astype(np.float32) for _ in range(3))
+    elif kind == "sharp":
+        qc, kc, vc = (rng.standard_normal((H, W, 64)).astype(np.float32) * 6 for _ in range(3))
+    elif kind == "pooled_bf16":
+        L = Layout(0, W // 81, 36, 36, 4)
+        W = L.num_windows
+        x = [orc.bf16_round(rng.standard_normal((H, L.image_tokens, 64)).astype(np.float32)) for _ in range(3)]
+        qc, kc, vc = (orc.pool(t, L) for t in x)
+    else:
+        qc, kc, vc = (rng.standard_normal((H, W, 64)).astype(np.float32) for _ in range(3))
+    ex = None
+    if excl:
+        ex = np.zeros(W, np.uint8)
+        ex[rng.choice(W, W // 5, replace=False)] = 1
+    o_ref, l_ref, i_ref, g_ref = orc.compress_topk(qc, kc, vc, k, 0.125, excluded=ex, guide=True)
+    r = gsa.fused_compressed_attention_topk(dev(qc, torch.float32), dev(kc, torch.float32), dev(vc, torch.float32),
+                                            k, 0.125, excluded=None if ex is None else torch.from_numpy(ex).cuda(),
+                                            keep_guide_scores=True)
+    np.testing.assert_array_equal(host(r.indices).astype(np.int32), i_ref)
+    np.testing.assert_array_equal(host(r.guide_scores), g_ref.reshape(host(r.guide_scores).shape))
+    assert rel_l2(host(r.out), o_ref) < 1e-4
+
+
+@pytest.mark.parametrize("variant,k", [(0, 256), (1, 300)])
+def test_layer_large_k_matches_reference(gsa, ref, variant, k):
+    """The whole layer with a 2-5 % style budget (k > 128) vs the reference fused CPU layer."""
+    lt = (40, 8, 36, 36, 4)
+    L = gsa.build_token_layout(*lt)
+    M = L.total_tokens
+    g = torch.Generator(device="cuda").manual_seed(9)
+    q, k_, v = (torch.randn(2, M, 64, generator=g, device="cuda").to(torch.bfloat16) for _ in range(3))
+    wg = torch.randn(2, 64, 64, generator=g, device="cuda") / 8
+    p = gsa.GsaParams(window_s=4, top_k=k, variant=variant, ref_stride=4)
+    out, ctx = gsa.gsa_forward(q, k_, v, wg, L, p, context=True)
+    f = lambda t: t.float().cpu().numpy()
+    rf = ref.forward(f(q), f(k_), f(v), f(wg), lt, top_k=k, variant=variant, ref_stride=4)
+    np.testing.assert_array_equal(ctx.topk.cpu().numpy(), rf["topk"])
+    o = host(out)
+    assert np.abs(o - rf["out"]).max() < 1e-4 and rel_l2(o, rf["out"]) < 1e-5
 
 
 def test_compress_all_ties(gsa, orc):

@@ -5,7 +5,7 @@ mkdir -p gpurun_out
 TAG=${1:-x}
 OUT=gpurun_out/configs_$TAG.jsonl; : > $OUT
 timeout 300 python bench.py --views 200 --grid 36x76 --specials-per-view 0 --steps 3 --warmup 3 --no-cpu-baseline --no-e2e 2>/dev/null | tail -1 >> $OUT
-for K in 8 16 32 64 128; do
+for K in 8 16 32 64 128 810 2025; do
   timeout 600 python bench.py --views 500 --topk $K --steps 3 --warmup 3 --no-cpu-baseline --no-e2e --no-dense 2>/dev/null | tail -1 >> $OUT
 done
 python - <<PY
