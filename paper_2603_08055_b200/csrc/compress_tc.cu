@@ -1056,7 +1056,43 @@ __global__ void __launch_bounds__(XR_THREADS) exact_row_kernel(const float* __re
 constexpr int LK_ROWS = 32, LK_THREADS = 256, LK_KT = 64, LK_CTAS = LK_CTAS_N;
 constexpr int LK_KMAX = 2048;
 constexpr int LK_QS = 68;  // padded row strides (floats) of the shared q / k tiles: no bank conflicts
-constexpr size_t LK_SMEM = (size_t)(LK_ROWS + LK_KT) * LK_QS * 4 + (size_t)LK_KMAX * 8 + (size_t)LK_ROWS * 256 * 4;
+constexpr int LK_CL = 4096;  // keys sharing the k-th key's top 16 bits, kept in shared memory (fast path)
+constexpr size_t LK_SMEM = (size_t)(LK_ROWS + LK_KT) * LK_QS * 4 + (size_t)LK_KMAX * 8 + (size_t)LK_ROWS * 256 * 4 +
+                           (size_t)LK_CL * 8;
+
+// Radix digit search by warp 0 over a 256-bin histogram: the largest digit d with
+// (count of digits >= d) >= need; writes d and the count strictly above it.
+__device__ __forceinline__ void lk_find_digit(const int* hist, int need, int lane, int* out_digit, int* out_above) {
+    int c[8], tot = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        c[i] = hist[8 * lane + i];
+        tot += c[i];
+    }
+    int incl = tot;  // suffix scan over lanes: bins of lanes >= this one
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_down_sync(0xffffffffu, incl, o);
+        if (lane + o < 32) incl += v;
+    }
+    int suf = incl - tot, found = -1, above_d = 0;
+#pragma unroll
+    for (int i = 7; i >= 0; --i) {
+        if (found < 0 && suf + c[i] >= need) {
+            found = 8 * lane + i;
+            above_d = suf;
+        }
+        suf += c[i];
+    }
+    const unsigned b = __ballot_sync(0xffffffffu, found >= 0);
+    const int src = 31 - __clz(b);
+    const int d = __shfl_sync(0xffffffffu, found, src);
+    const int ab = __shfl_sync(0xffffffffu, above_d, src);
+    if (lane == 0) {
+        *out_digit = d;
+        *out_above = ab;
+    }
+}
 
 __global__ void __launch_bounds__(LK_THREADS) largek_topk_kernel(
     const float* __restrict__ qc, int64_t q_hs, const float* __restrict__ kc, int heads, int Wq, int Wk, float scale,
@@ -1066,8 +1102,9 @@ __global__ void __launch_bounds__(LK_THREADS) largek_topk_kernel(
     float* ks = qs + LK_ROWS * LK_QS;                                        // [LK_KT][LK_QS]
     unsigned long long* sb = reinterpret_cast<unsigned long long*>(ks + LK_KT * LK_QS);  // [LK_KMAX] sort buffer
     int* rhist = reinterpret_cast<int*>(sb + LK_KMAX);                       // [LK_ROWS][256] pass-0 histograms
+    unsigned long long* cl = reinterpret_cast<unsigned long long*>(rhist + LK_ROWS * 256);  // [LK_CL] bin list
     __shared__ int hist[256];
-    __shared__ int sh_digit, sh_above, sh_cnt_gt, sh_eq_taken;
+    __shared__ int sh_digit, sh_above, sh_cnt_gt, sh_eq_taken, sh_cl, sh_fast;
     __shared__ int warp_cnt[LK_THREADS / 32];
     uint32_t* sk = scratch + (size_t)blockIdx.x * LK_ROWS * Wk;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -1090,35 +1127,114 @@ __global__ void __launch_bounds__(LK_THREADS) largek_topk_kernel(
                 *reinterpret_cast<float4*>(ks + (i / 16) * LK_QS + 4 * (i & 15)) = v;
             }
             __syncthreads();
-            const int r = tid >> 3;  // row of this thread; 8 threads per row, keys jj, jj+8, ...
+            const int r = tid >> 3;  // row of this thread; 8 threads per row, keys jj0 + 8 i
+            const int jj0 = tid & 7;
             if (r < nr) {
-                for (int jj = tid & 7; jj < LK_KT; jj += 8) {
-                    const int j = kt0 + jj;
-                    if (j >= Wk) break;
-                    // dot.hpp:11-23 order (scalar __fmul_rn/__fadd_rn: the paired FMUL2/FADD2
-                    // forms get contracted into FFMA2 and measured 54 index mismatches in 1.8 M)
-                    ExactDot4 d;
-                    d.zero();
-                    const float4* a = reinterpret_cast<const float4*>(qs + r * LK_QS);
-                    const float4* b = reinterpret_cast<const float4*>(ks + jj * LK_QS);
+                // 8 independent dots per thread (32 add chains in flight), dot.hpp:11-23 order
+                ExactDot4 d[LK_KT / 8];
 #pragma unroll
-                    for (int x = 0; x < 16; ++x) {
-                        const float4 av = a[x], bv = b[x];
-                        d.step(av.x, av.y, av.z, av.w, bv.x, bv.y, bv.z, bv.w);
+                for (int i = 0; i < LK_KT / 8; ++i) d[i].zero();
+                const float4* a = reinterpret_cast<const float4*>(qs + r * LK_QS);
+#pragma unroll 4
+                for (int x = 0; x < 16; ++x) {
+                    const float4 av = a[x];
+#pragma unroll
+                    for (int i = 0; i < LK_KT / 8; ++i) {
+                        const float4 bv = reinterpret_cast<const float4*>(ks + (jj0 + 8 * i) * LK_QS)[x];
+                        d[i].step(av.x, av.y, av.z, av.w, bv.x, bv.y, bv.z, bv.w);
                     }
-                    const float sc = d.finish(scale);
-                    const bool ex = exbits && ((exbits[j >> 5] >> (j & 31)) & 1u);
-                    // +0.0f folds -0 into +0: the keys order like topk_better's float compare
-                    const uint32_t key = ex ? 0u : fkey(sc + 0.0f);
-                    sk[(size_t)r * Wk + j] = key;
-                    atomicAdd(&rhist[r * 256 + (key >> 24)], 1);  // radix pass 0, fused
+                }
+#pragma unroll
+                for (int i = 0; i < LK_KT / 8; ++i) {
+                    const int j = kt0 + jj0 + 8 * i;
+                    if (j < Wk) {
+                        const bool ex = exbits && ((exbits[j >> 5] >> (j & 31)) & 1u);
+                        // +0.0f folds -0 into +0: the keys order like topk_better's float compare
+                        const uint32_t key = ex ? 0u : fkey(d[i].finish(scale) + 0.0f);
+                        sk[(size_t)r * Wk + j] = key;
+                        atomicAdd(&rhist[r * 256 + (key >> 24)], 1);  // radix pass 0, fused
+                    }
                 }
             }
         }
         __syncthreads();
         // ---- per row: radix select, collect, sort, write
+#ifdef LK_SKIP_SELECT
+        continue;
+#endif
         for (int r = 0; r < nr; ++r) {
             const uint32_t* rk = sk + (size_t)r * Wk;
+            // ---- fast path: digits 0 (fused histogram) and 1 (one scan); then ONE scan sends
+            // the keys above the 16-bit prefix bin straight to the sort buffer and the bin's
+            // keys to a shared list, where digits 2 and 3 are resolved
+            {
+                for (int i = tid; i < 256; i += LK_THREADS) hist[i] = rhist[r * 256 + i];
+                __syncthreads();
+                if (warp == 0) lk_find_digit(hist, k_eff, lane, &sh_digit, &sh_above);
+                __syncthreads();
+                const uint32_t d0 = (uint32_t)sh_digit;
+                int need = k_eff - sh_above;
+                for (int i = tid; i < 256; i += LK_THREADS) hist[i] = 0;
+                __syncthreads();
+                for (int j = tid; j < Wk; j += LK_THREADS) {
+                    const uint32_t key = rk[j];
+                    if ((key >> 24) == d0) atomicAdd(&hist[(key >> 16) & 255u], 1);
+                }
+                __syncthreads();
+                if (warp == 0) lk_find_digit(hist, need, lane, &sh_digit, &sh_above);
+                __syncthreads();
+                const uint32_t p16 = (d0 << 8) | (uint32_t)sh_digit;
+                const int bin_n = hist[sh_digit];
+                need -= sh_above;
+                __syncthreads();
+                if (tid == 0) {
+                    sh_cnt_gt = 0;
+                    sh_cl = 0;
+                    sh_fast = bin_n <= LK_CL;
+                }
+                __syncthreads();
+                if (sh_fast) {
+                    for (int j = tid; j < Wk; j += LK_THREADS) {
+                        const uint32_t key = rk[j];
+                        const uint32_t t16 = key >> 16;
+                        const unsigned long long e = ((unsigned long long)key << 32) | (0xffffffffu - (uint32_t)j);
+                        if (t16 > p16) sb[atomicAdd(&sh_cnt_gt, 1)] = e;
+                        else if (t16 == p16) cl[atomicAdd(&sh_cl, 1)] = e;
+                    }
+                    __syncthreads();
+                    const int m = sh_cl;
+                    uint32_t prefix = p16;
+                    int cnt_eq = 0;
+                    for (int pass = 2; pass < 4; ++pass) {
+                        const int shift = 24 - 8 * pass;
+                        for (int i = tid; i < 256; i += LK_THREADS) hist[i] = 0;
+                        __syncthreads();
+                        for (int i = tid; i < m; i += LK_THREADS) {
+                            const uint32_t key = (uint32_t)(cl[i] >> 32);
+                            if ((key >> (shift + 8)) == prefix) atomicAdd(&hist[(key >> shift) & 255u], 1);
+                        }
+                        __syncthreads();
+                        if (warp == 0) lk_find_digit(hist, need, lane, &sh_digit, &sh_above);
+                        __syncthreads();
+                        prefix = (prefix << 8) | (uint32_t)sh_digit;
+                        need -= sh_above;
+                        cnt_eq = hist[sh_digit];
+                        __syncthreads();
+                    }
+                    const uint32_t T = prefix;
+                    if (cnt_eq == need) {  // every key equal to T is taken: no tie ordering needed
+                        for (int i = tid; i < m; i += LK_THREADS) {
+                            const unsigned long long e = cl[i];
+                            if ((uint32_t)(e >> 32) >= T) sb[atomicAdd(&sh_cnt_gt, 1)] = e;
+                        }
+                        __syncthreads();
+                    } else {
+                        if (tid == 0) sh_fast = 0;  // ties straddle the k-th place: ordered path
+                        __syncthreads();
+                    }
+                }
+            }
+            if (!sh_fast) {
             uint32_t prefix = 0;
             int need = k_eff;  // still to take at or below the current prefix
             for (int pass = 0; pass < 4; ++pass) {
@@ -1206,7 +1322,12 @@ __global__ void __launch_bounds__(LK_THREADS) largek_topk_kernel(
                 if (tid == 0) sh_eq_taken += tot;
             }
             __syncthreads();
+            }  // ordered (slow) path
+            __syncthreads();
             // bitonic sort of sb[0..n2) descending (pad with 0 = below every real entry)
+#ifdef LK_SKIP_SORT
+            continue;
+#endif
             int n2 = 1;
             while (n2 < k_eff) n2 <<= 1;
             for (int i = k_eff + tid; i < n2; i += LK_THREADS) sb[i] = 0ull;
