@@ -437,7 +437,8 @@ def test_compress_topk_tc_large_k(gsa, orc, kind, W, k):
     assert rel_l2(host(r.out), o_ref) < 1e-4
 
 
-@pytest.mark.parametrize("lt,ref_stride,k", [((10, 12, 16, 16, 4), 4, 6), ((40, 9, 36, 36, 4), 3, 32)])
+@pytest.mark.parametrize("lt,ref_stride,k", [((10, 12, 16, 16, 4), 4, 6), ((40, 9, 36, 36, 4), 3, 32),
+                                           ((10, 4, 16, 16, 4), 1, 6), ((10, 5, 16, 16, 4), 9, 40)])
 def test_hybrid_fast_path_matches_reference(gsa, ref, lt, ref_stride, k):
     """Hybrid rows = every reference-frame window ++ dynamic top-k (selection.cpp:55-59).
     The tensor-core path takes the reference-frame part as one dense attention and
