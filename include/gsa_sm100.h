@@ -122,7 +122,9 @@ int gsa_special_token_attention(const gsa_tensor* q_spec, const gsa_tensor* k, c
 /* fused_compressed_attention_topk (compression.hpp:180-297). qc/kc/vc f32
  * [H][W][d]; excluded: device byte mask [W] or NULL; out f32 [H][W][d]; lse
  * [H][W]; indices [H][W][k_eff]; guide_scores (nullable) [H][W][k_eff] f32.
- * *k_eff_out (host) = min(k, selectable). Indices are bit-exact. */
+ * *k_eff_out (host) = min(k, selectable). Indices are bit-exact; k_eff up to
+ * 2048 (above 128 the selection runs on exact CUDA-core scores). With an
+ * exclusion mask the call synchronises `stream` (k_eff needs the mask's count). */
 size_t gsa_compressed_attention_topk_workspace_bytes(int heads, int windows, int dim, int k);
 int gsa_compressed_attention_topk(const gsa_tensor* qc, const gsa_tensor* kc, const gsa_tensor* vc,
                                   int k, float scale, int block_m, int block_n,
@@ -148,7 +150,9 @@ size_t gsa_build_selection_plan_workspace_bytes(int heads, int rows, int k,
                                                 const gsa_layout* layout, int ref_stride);
 
 /* block_sparse_attention (selection.hpp:63-136) over a device CSR plan.
- * Validates that no row is empty (synchronises `stream`; EmptySelection).
+ * Validates that no row is empty (synchronises `stream`; EmptySelection; the
+ * 4-byte flag for it is a stream-ordered cudaMallocAsync, the one allocation in
+ * the library -- gsa_forward checks its own plan without it).
  * out f32 [H][Mi][d], lse [H][Mi]. */
 int gsa_block_sparse_attention(const gsa_tensor* q_img, const gsa_tensor* k_img,
                                const gsa_tensor* v_img, const int64_t* offsets,
