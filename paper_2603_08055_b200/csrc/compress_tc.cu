@@ -1056,9 +1056,19 @@ __global__ void __launch_bounds__(XR_THREADS) exact_row_kernel(const float* __re
 constexpr int LK_ROWS = 32, LK_THREADS = 256, LK_KT = 64, LK_CTAS = LK_CTAS_N;
 constexpr int LK_KMAX = 2048;
 constexpr int LK_QS = 68;  // padded row strides (floats) of the shared q / k tiles: no bank conflicts
-constexpr int LK_CL = 4096;  // keys sharing the k-th key's top 16 bits, kept in shared memory (fast path)
-constexpr size_t LK_SMEM = (size_t)(LK_ROWS + LK_KT) * LK_QS * 4 + (size_t)LK_KMAX * 8 + (size_t)LK_ROWS * 256 * 4 +
-                           (size_t)LK_CL * 8;
+constexpr int LK_CL = 2048;  // keys sharing the k-th key's top 16 bits, kept in shared memory (fast path)
+constexpr size_t LK_SMEM = (size_t)(LK_ROWS + 2 * LK_KT) * LK_QS * 4 + (size_t)LK_KMAX * 8 + (size_t)LK_ROWS * 256 * 4 +
+                           (size_t)LK_CL * 8;  // ~107 KB: two CTAs per SM
+
+// 16-byte global -> shared copies that bypass registers (LDGSTS); src_bytes 0 zero-fills
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src, int src_bytes) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(smem_dst)), "l"(gmem_src),
+                 "r"(src_bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
 // Radix digit search by warp 0 over a 256-bin histogram: the largest digit d with
 // (count of digits >= d) >= need; writes d and the count strictly above it.
@@ -1099,8 +1109,8 @@ __global__ void __launch_bounds__(LK_THREADS) largek_topk_kernel(
     int k_eff, const uint32_t* __restrict__ exbits, uint32_t* scratch, int32_t* topk, float* guide) {
     extern __shared__ __align__(16) uint8_t lk_smem[];
     float* qs = reinterpret_cast<float*>(lk_smem);                           // [LK_ROWS][LK_QS]
-    float* ks = qs + LK_ROWS * LK_QS;                                        // [LK_KT][LK_QS]
-    unsigned long long* sb = reinterpret_cast<unsigned long long*>(ks + LK_KT * LK_QS);  // [LK_KMAX] sort buffer
+    float* ks2 = qs + LK_ROWS * LK_QS;                                       // [2][LK_KT][LK_QS] (double buffer)
+    unsigned long long* sb = reinterpret_cast<unsigned long long*>(ks2 + 2 * LK_KT * LK_QS);  // [LK_KMAX] sort buffer
     int* rhist = reinterpret_cast<int*>(sb + LK_KMAX);                       // [LK_ROWS][256] pass-0 histograms
     unsigned long long* cl = reinterpret_cast<unsigned long long*>(rhist + LK_ROWS * 256);  // [LK_CL] bin list
     __shared__ int hist[256];
@@ -1117,14 +1127,25 @@ __global__ void __launch_bounds__(LK_THREADS) largek_topk_kernel(
         for (int i = tid; i < LK_ROWS * 256; i += LK_THREADS) rhist[i] = 0;
         for (int i = tid; i < LK_ROWS * 64; i += LK_THREADS)
             qs[(i / 64) * LK_QS + (i & 63)] = (i / 64) < nr ? qc[(int64_t)h * q_hs + (int64_t)(w0 + i / 64) * 64 + (i & 63)] : 0.0f;
-        // ---- exact scores of the block's rows against every key window
-        for (int kt0 = 0; kt0 < Wk; kt0 += LK_KT) {
-            __syncthreads();
+        // ---- exact scores of the block's rows against every key window; the next Kc
+        // tile streams into the other buffer (cp.async) while this one is scored
+        auto load_tile = [&](int kt0, float* dst) {
             for (int i = tid; i < LK_KT * 16; i += LK_THREADS) {
                 const int j = kt0 + i / 16;
-                const float4 v = j < Wk ? reinterpret_cast<const float4*>(kc + ((int64_t)h * Wk + j) * 64)[i & 15]
-                                        : make_float4(0.f, 0.f, 0.f, 0.f);
-                *reinterpret_cast<float4*>(ks + (i / 16) * LK_QS + 4 * (i & 15)) = v;
+                const float* src = kc + ((int64_t)h * Wk + (j < Wk ? j : 0)) * 64 + 4 * (i & 15);
+                cp_async16(dst + (i / 16) * LK_QS + 4 * (i & 15), src, j < Wk ? 16 : 0);
+            }
+            cp_async_commit();
+        };
+        __syncthreads();
+        load_tile(0, ks2);
+        for (int kt0 = 0, tb = 0; kt0 < Wk; kt0 += LK_KT, tb ^= 1) {
+            float* ks = ks2 + tb * LK_KT * LK_QS;
+            if (kt0 + LK_KT < Wk) {
+                load_tile(kt0 + LK_KT, ks2 + (tb ^ 1) * LK_KT * LK_QS);
+                cp_async_wait<1>();
+            } else {
+                cp_async_wait<0>();
             }
             __syncthreads();
             const int r = tid >> 3;  // row of this thread; 8 threads per row, keys jj0 + 8 i
@@ -1156,6 +1177,7 @@ __global__ void __launch_bounds__(LK_THREADS) largek_topk_kernel(
                     }
                 }
             }
+            __syncthreads();  // this buffer is refilled by the prefetch of the next iteration
         }
         __syncthreads();
         // ---- per row: radix select, collect, sort, write
