@@ -239,3 +239,23 @@ def test_virtual_shards_match_unsharded_gpu(G, lt, variant):
     np.testing.assert_array_equal(ctx.topk.cpu().numpy(), orc.gsa_forward(q, k, v, wg, L, top_k=16, variant=variant,
                                                                          ref_stride=3)["topk"])
     assert (got - full_out).abs().max().item() < 1e-5
+
+
+@pytest.mark.gpu
+def test_sharded_layer_two_processes_one_gpu():
+    """The view-sharded layer across two real processes (torchrun, gloo group, both on
+    cuda:0, the sm_100a kernels): gathered K/V exact, top-k bit-exact and outputs equal
+    to the unsharded gsa_forward, plain and hybrid (tools/diag_shard_mp.py)."""
+    import subprocess
+    import sys
+
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                        "--master-addr", "127.0.0.1", "--master-port", "29547",
+                        os.path.join(root, "tools", "diag_shard_mp.py")],
+                       capture_output=True, text=True, timeout=600, cwd=root)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    assert r.stdout.count("topk bit-exact True, gathered K/V exact True") == 4, r.stdout
