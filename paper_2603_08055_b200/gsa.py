@@ -507,7 +507,17 @@ class HostPipeline:
         H = q_host.shape[0]
         bufs = self._alloc(q_host)
         g = min(self.g, H)
-        groups = [(h0, min(H, h0 + g)) for h0 in range(0, H, g)]
+        # single-head first and last groups: the pipeline fill (first H2D) and drain
+        # (last D2H) are the only copies that do not overlap compute
+        if H > 2 and g > 1:
+            mid = H - 2
+            sizes = [1] + [g] * (mid // g) + ([mid % g] if mid % g else []) + [1]
+        else:
+            sizes = [g] * (H // g) + ([H % g] if H % g else [])
+        groups, h0 = [], 0
+        for n in sizes:
+            groups.append((h0, h0 + n))
+            h0 += n
         ev_in = [torch.cuda.Event() for _ in groups]
         ev_comp = [torch.cuda.Event() for _ in groups]
         ev_out = [torch.cuda.Event() for _ in groups]
