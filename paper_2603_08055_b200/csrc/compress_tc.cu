@@ -797,31 +797,53 @@ __global__ void __launch_bounds__(256) rescore_kernel(const float* __restrict__ 
             e[s] = d.finish(scale);
         }
     }
-    // rank = number of survivors strictly better under topk_better (compression.hpp:67-73)
-    int rank[SLOTS];
-#pragma unroll
-    for (int s = 0; s < SLOTS; ++s) rank[s] = 0;
-    for (int j = 0; j < total; ++j) {
-        float ej = e[0];
-        int ij = idx[0];
-#pragma unroll
-        for (int s = 1; s < SLOTS; ++s)
-            if ((j >> 5) == s) {
-                ej = e[s];
-                ij = idx[s];
-            }
-        ej = __shfl_sync(0xffffffffu, ej, j & 31);
-        ij = __shfl_sync(0xffffffffu, ij, j & 31);
-#pragma unroll
-        for (int s = 0; s < SLOTS; ++s)
-            if (topk_better(ej, ij, e[s], idx[s])) ++rank[s];
-    }
+    // order by topk_better (compression.hpp:67-73) = descending 64-bit keys
+    // (fkey(score) << 32 | ~index): a warp bitonic sort over SLOTS x 32 entries, element
+    // i = 32 s + lane; position p of the sorted sequence is rank p. (Exact scores are never
+    // -0: the lane sums start at +0, so +0 + x never yields -0 -- fkey orders them as floats.)
+    unsigned long long skey[SLOTS];
 #pragma unroll
     for (int s = 0; s < SLOTS; ++s)
-        if (idx[s] >= 0 && rank[s] < k_eff) {
-            topk[r * k_eff + rank[s]] = idx[s];
-            if (guide) guide[r * k_eff + rank[s]] = e[s];
+        skey[s] = idx[s] >= 0 ? ((unsigned long long)fkey(e[s]) << 32) | (0xffffffffu - (uint32_t)idx[s]) : 0ull;
+#pragma unroll
+    for (int size = 2; size <= SLOTS * 32; size <<= 1) {
+#pragma unroll
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            if (stride >= 32) {  // partner in another slot of the same lane
+#pragma unroll
+                for (int s = 0; s < SLOTS; ++s) {
+                    const int so = s ^ (stride >> 5);
+                    if (so > s) {
+                        const int i = 32 * s + lane;
+                        const bool desc = (i & size) == 0;  // keep the larger at the lower index
+                        const unsigned long long a = skey[s], b = skey[so];
+                        const bool sw = desc ? (a < b) : (a > b);
+                        skey[s] = sw ? b : a;
+                        skey[so] = sw ? a : b;
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int s = 0; s < SLOTS; ++s) {
+                    const int i = 32 * s + lane;
+                    const unsigned long long o = __shfl_xor_sync(0xffffffffu, skey[s], stride);
+                    const bool lower = (lane & stride) == 0;
+                    const bool desc = (i & size) == 0;
+                    // lower index keeps max when desc, min otherwise; the upper the opposite
+                    const bool take_max = lower == desc;
+                    skey[s] = take_max ? (skey[s] > o ? skey[s] : o) : (skey[s] < o ? skey[s] : o);
+                }
+            }
         }
+    }
+#pragma unroll
+    for (int s = 0; s < SLOTS; ++s) {
+        const int p = 32 * s + lane;
+        if (p < k_eff && skey[s] != 0ull) {
+            topk[r * k_eff + p] = (int32_t)(0xffffffffu - (uint32_t)(skey[s] & 0xffffffffu));
+            if (guide) guide[r * k_eff + p] = fkey_inv((uint32_t)(skey[s] >> 32));
+        }
+    }
 }
 
 // f32 [H][W][64] (strided) -> bf16 hi, lo contiguous + row norms
