@@ -256,6 +256,8 @@ def main():
     ap.add_argument("--topk", type=int, default=32)
     ap.add_argument("--e2e-heads-per-group", type=int, default=2,
                     help="e2e host pipeline granularity: heads per H2D / compute / D2H group")
+    ap.add_argument("--data", default="normal", choices=["normal", "clustered"],
+                    help="synthetic Q/K/V: iid N(0,1) (worst case for selection locality) or per-view clusters")
     ap.add_argument("--layers", type=int, default=1,
                     help="L > 1: an L-layer stack (BASELINE configs[2]); each layer = fused QKV GEMM + GSA layer")
     ap.add_argument("--hybrid", type=int, default=0, metavar="REF_STRIDE",
@@ -291,8 +293,18 @@ def main():
                            ref_stride=args.hybrid if args.hybrid else 100)
     geometry_default = (GRID_H, GRID_W, SPECIAL_PER_VIEW, TOPK, args.hybrid) == (36, 36, 5, 32, 0)
     gen = torch.Generator(device=dev).manual_seed(7)
-    q, k, v = (torch.randn(HEADS, G["M"], DIM, generator=gen, device=dev, dtype=torch.float32).to(torch.bfloat16)
-               for _ in range(3))
+    def synth():
+        x = torch.randn(HEADS, G["M"], DIM, generator=gen, device=dev, dtype=torch.float32)
+        if args.data == "clustered":
+            # the reference's kClustered recipe (workload.hpp:78-90): x = centroid(frame) + 0.5 x,
+            # one centroid per (head, view) shared by the view's specials and patches
+            cen = torch.randn(HEADS, args.views, DIM, generator=gen, device=dev, dtype=torch.float32)
+            ms = SPECIAL_PER_VIEW * args.views
+            view_of = torch.cat([torch.arange(ms, device=dev) // max(1, SPECIAL_PER_VIEW),
+                                 torch.arange(G["M"] - ms, device=dev) // (GRID_H * GRID_W)])
+            x = cen[:, view_of] + 0.5 * x
+        return x.to(torch.bfloat16)
+    q, k, v = (synth() for _ in range(3))
     wg = torch.randn(HEADS, DIM, DIM, generator=gen, device=dev) / 8.0
     out = torch.empty(HEADS, G["M"], DIM, device=dev)
     ws = gsa.Workspace()
@@ -398,7 +410,8 @@ def main():
     line = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "bf16",
-            "data": "synthetic (torch N(0,1) bf16 Q/K/V, W_g=N(0,1)/8 f32), resident in HBM",
+            "data": ("synthetic (torch N(0,1) bf16 Q/K/V, W_g=N(0,1)/8 f32), resident in HBM" if args.data == "normal" else
+                     "synthetic clustered (per-view centroid + 0.5 N(0,1), workload.hpp:78-90) bf16 Q/K/V, resident in HBM"),
             "config": {"workload": f"1 GSA layer, {args.views} views x ({SPECIAL_PER_VIEW} specials + {GRID_H}x{GRID_W} "
                                    f"patches) = {M} tokens, 16 heads x 64, s=4, top-{TOPK}, "
                                    f"{'hybrid (reference frames every %d views)' % args.hybrid if args.hybrid else 'plain'}",
