@@ -961,105 +961,52 @@ __global__ void exbits_kernel(const uint8_t* __restrict__ ex, int W, int words, 
 }
 
 // flagged rows (candidate list overflow / near-tie flood) -> list for the exact per-row path
-__global__ void flag_rows_kernel(const uint8_t* __restrict__ flag, int64_t rows, int* list, int* count) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < rows && flag[i]) list[atomicAdd(count, 1)] = (int)i;
+
+// Ordered compaction of the flagged rows (ascending row ids: the fallback's blocks of 32
+// then share a head). Three tiny passes: per-block counts, one-block scan, scatter.
+constexpr int FL_BLOCK = 1024;
+__global__ void flag_count_kernel(const uint8_t* __restrict__ flag, int64_t rows, int* block_counts) {
+    const int64_t i = (int64_t)blockIdx.x * FL_BLOCK + threadIdx.x;
+    const int f = (i < rows && flag[i]) ? 1 : 0;
+    const int c = __syncthreads_count(f);
+    if (threadIdx.x == 0) block_counts[blockIdx.x] = c;
 }
-
-constexpr int XR_THREADS = 256;
-constexpr int XR_CTAS = 296;
-
-__device__ __forceinline__ int block_sum(int v, int* red) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+__global__ void flag_scan_kernel(int* block_counts, int nb, int* total) {
+    // single block, sequential chunks of blockDim.x with a shared running offset
+    __shared__ int carry;
+    __shared__ int wsum[32];
+    if (threadIdx.x == 0) carry = 0;
     __syncthreads();
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x / 32] = v;
-    __syncthreads();
-    int s = 0;
-#pragma unroll
-    for (int i = 0; i < XR_THREADS / 32; ++i) s += red[i];
-    return s;
-}
-
-// Exact top-k of a flagged row from scratch (fused_compressed_attention_topk's
-// contract, compression.hpp:259-275): every guide score in the scaled_dot
-// order (dot.hpp:11-23, no FMA), the exact K-th largest by a radix select over
-// order-preserving keys, then all scores above it plus the lowest-index ties
-// at it (topk_better: equal scores go to the lower index), ranked. Persistent
-// CTAs over the flagged-row list; the row's keys live in a per-CTA scratch.
-__global__ void __launch_bounds__(XR_THREADS) exact_row_kernel(const float* __restrict__ qc, int64_t q_hs,
-                                                               const float* __restrict__ kc, int Wq, int Wk,
-                                                               float scale, int k_eff, const uint32_t* __restrict__ exbits,
-                                                               const int* __restrict__ list, const int* __restrict__ count,
-                                                               uint32_t* scratch, int32_t* topk, float* guide) {
-    __shared__ float qs[64];
-    __shared__ int red[XR_THREADS / 32];
-    __shared__ float sel_s[128];
-    __shared__ int sel_i[128];
-    __shared__ int nsel;
-    uint32_t* keys = scratch + (size_t)blockIdx.x * Wk;
-    const int n_rows = *count;
-    for (int li = blockIdx.x; li < n_rows; li += gridDim.x) {
-        const int64_t r = list[li];
-        const int h = (int)(r / Wq);
-        const float* q = qc + (int64_t)h * q_hs + (r - (int64_t)h * Wq) * 64;
-        __syncthreads();
-        if (threadIdx.x < 64) qs[threadIdx.x] = q[threadIdx.x];
-        if (threadIdx.x == 0) nsel = 0;
-        __syncthreads();
-        for (int j = threadIdx.x; j < Wk; j += XR_THREADS) {
-            const bool ex = exbits && ((exbits[j >> 5] >> (j & 31)) & 1u);
-            keys[j] = ex ? 0u : fkey(exact_scaled_dot(qs, kc + ((int64_t)h * Wk + j) * 64, 64, scale));
+    for (int base = 0; base < nb; base += blockDim.x) {
+        const int i = base + threadIdx.x;
+        const int v = i < nb ? block_counts[i] : 0;
+        int x = v;  // inclusive warp scan
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, x, o);
+            if ((threadIdx.x & 31) >= o) x += y;
         }
+        if ((threadIdx.x & 31) == 31) wsum[threadIdx.x >> 5] = x;
         __syncthreads();
-        uint32_t res = 0;
-        for (int bit = 31; bit >= 0; --bit) {
-            const uint32_t cand = res | (1u << bit);
-            int c = 0;
-            for (int j = threadIdx.x; j < Wk; j += XR_THREADS) c += keys[j] >= cand ? 1 : 0;
-            if (block_sum(c, red) >= k_eff) res = cand;
-        }
-        int gt = 0;
-        for (int j = threadIdx.x; j < Wk; j += XR_THREADS) gt += keys[j] > res ? 1 : 0;
-        const int need_eq = k_eff - block_sum(gt, red);
-        // everything above the K-th, then the lowest-index ties at it, in index order
-        int taken_eq = 0;
-        for (int j0 = 0; j0 < Wk; j0 += XR_THREADS) {
-            const int j = j0 + threadIdx.x;
-            const uint32_t kj = j < Wk ? keys[j] : 0u;
-            const bool eq = j < Wk && kj == res && res != 0u;
-            const unsigned b = __ballot_sync(0xffffffffu, eq);
-            __syncthreads();
-            if ((threadIdx.x & 31) == 0) red[threadIdx.x / 32] = __popc(b);
-            __syncthreads();
-            int before = 0, tot = 0;
-            for (int i = 0; i < XR_THREADS / 32; ++i) {
-                before += i < (int)(threadIdx.x / 32) ? red[i] : 0;
-                tot += red[i];
-            }
-            const int rank_eq = taken_eq + before + __popc(b & ((1u << (threadIdx.x & 31)) - 1u));
-            if ((j < Wk && kj > res) || (eq && rank_eq < need_eq)) {
-                const int slot = atomicAdd(&nsel, 1);
-                if (slot < 128) {
-                    sel_s[slot] = fkey_inv(kj);
-                    sel_i[slot] = j;
-                }
-            }
-            taken_eq += tot;
-        }
+        int woff = 0;
+        for (int w = 0; w < (int)(threadIdx.x >> 5); ++w) woff += wsum[w];
+        if (i < nb) block_counts[i] = carry + woff + x - v;  // exclusive offset
         __syncthreads();
-        const int ns = min(nsel, 128);
-        if ((int)threadIdx.x < ns) {
-            const float s = sel_s[threadIdx.x];
-            const int idx = sel_i[threadIdx.x];
-            int rank = 0;
-            for (int i = 0; i < ns; ++i) rank += topk_better(sel_s[i], sel_i[i], s, idx) ? 1 : 0;
-            if (rank < k_eff) {
-                topk[r * k_eff + rank] = idx;
-                if (guide) guide[r * k_eff + rank] = s;
-            }
-        }
+        if (threadIdx.x == blockDim.x - 1) carry += woff + x;
+        __syncthreads();
     }
+    if (threadIdx.x == 0) *total = carry;
+}
+__global__ void flag_scatter_kernel(const uint8_t* __restrict__ flag, int64_t rows, const int* __restrict__ offsets,
+                                    int* list) {
+    __shared__ int wcnt[FL_BLOCK / 32];
+    const int64_t i = (int64_t)blockIdx.x * FL_BLOCK + threadIdx.x;
+    const bool f = i < rows && flag[i];
+    const unsigned b = __ballot_sync(0xffffffffu, f);
+    if ((threadIdx.x & 31) == 0) wcnt[threadIdx.x >> 5] = __popc(b);
+    __syncthreads();
+    int off = offsets[blockIdx.x];
+    for (int w = 0; w < (int)(threadIdx.x >> 5); ++w) off += wcnt[w];
+    if (f) list[off + __popc(b & ((1u << (threadIdx.x & 31)) - 1u))] = (int)i;
 }
 
 // ---------------------------------------------------------------------------------------
@@ -1128,7 +1075,10 @@ __device__ __forceinline__ void lk_find_digit(const int* hist, int need, int lan
 
 __global__ void __launch_bounds__(LK_THREADS) largek_topk_kernel(
     const float* __restrict__ qc, int64_t q_hs, const float* __restrict__ kc, int heads, int Wq, int Wk, float scale,
-    int k_eff, const uint32_t* __restrict__ exbits, uint32_t* scratch, int32_t* topk, float* guide) {
+    int k_eff, const uint32_t* __restrict__ exbits, uint32_t* scratch, int32_t* topk, float* guide,
+    const int* __restrict__ row_list = nullptr, const int* __restrict__ row_count = nullptr) {
+    // row_list mode (the exact fallback of the main path): the rows are the listed ones
+    // (ascending, so mostly one head per block of 32); otherwise every row of every head
     extern __shared__ __align__(16) uint8_t lk_smem[];
     float* qs = reinterpret_cast<float*>(lk_smem);                           // [LK_ROWS][LK_QS]
     float* ks2 = qs + LK_ROWS * LK_QS;                                       // [2][LK_KT][LK_QS] (double buffer)
@@ -1138,17 +1088,41 @@ __global__ void __launch_bounds__(LK_THREADS) largek_topk_kernel(
     __shared__ int hist[256];
     __shared__ int sh_digit, sh_above, sh_cnt_gt, sh_eq_taken, sh_cl, sh_fast;
     __shared__ int warp_cnt[LK_THREADS / 32];
+    __shared__ int row_id[LK_ROWS], row_h[LK_ROWS];
     uint32_t* sk = scratch + (size_t)blockIdx.x * LK_ROWS * Wk;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int blocks_per_head = (Wq + LK_ROWS - 1) / LK_ROWS;
-    const int nblocks = heads * blocks_per_head;
+    const int n_list = row_list ? *row_count : 0;
+    const int nblocks = row_list ? (n_list + LK_ROWS - 1) / LK_ROWS : heads * blocks_per_head;
     for (int blk = blockIdx.x; blk < nblocks; blk += gridDim.x) {
-        const int h = blk / blocks_per_head, w0 = (blk - h * blocks_per_head) * LK_ROWS;
-        const int nr = min(LK_ROWS, Wq - w0);
+        int nr;
         __syncthreads();
+        if (row_list) {
+            nr = min(LK_ROWS, n_list - blk * LK_ROWS);
+            if (tid < nr) {
+                row_id[tid] = row_list[blk * LK_ROWS + tid];
+                row_h[tid] = row_id[tid] / Wq;
+            }
+        } else {
+            const int hb = blk / blocks_per_head, w0 = (blk - hb * blocks_per_head) * LK_ROWS;
+            nr = min(LK_ROWS, Wq - w0);
+            if (tid < nr) {
+                row_id[tid] = hb * Wq + w0 + tid;
+                row_h[tid] = hb;
+            }
+        }
         for (int i = tid; i < LK_ROWS * 256; i += LK_THREADS) rhist[i] = 0;
-        for (int i = tid; i < LK_ROWS * 64; i += LK_THREADS)
-            qs[(i / 64) * LK_QS + (i & 63)] = (i / 64) < nr ? qc[(int64_t)h * q_hs + (int64_t)(w0 + i / 64) * 64 + (i & 63)] : 0.0f;
+        __syncthreads();
+        // one pass over the keys per distinct head among the block's rows
+        for (int done = 0; done < nr;) {
+        const int h = row_h[done];
+        int span = done;
+        while (span < nr && row_h[span] == h) ++span;  // rows [done, span) share head h (list ascending)
+        for (int i = tid; i < LK_ROWS * 64; i += LK_THREADS) {
+            const int rr = i / 64;
+            qs[rr * LK_QS + (i & 63)] =
+                (rr >= done && rr < span) ? qc[(int64_t)h * q_hs + (int64_t)(row_id[rr] - h * Wq) * 64 + (i & 63)] : 0.0f;
+        }
         // ---- exact scores of the block's rows against every key window; the next Kc
         // tile streams into the other buffer (cp.async) while this one is scored
         auto load_tile = [&](int kt0, float* dst) {
@@ -1172,7 +1146,7 @@ __global__ void __launch_bounds__(LK_THREADS) largek_topk_kernel(
             __syncthreads();
             const int r = tid >> 3;  // row of this thread; 8 threads per row, keys jj0 + 8 i
             const int jj0 = tid & 7;
-            if (r < nr) {
+            if (r >= done && r < span) {
                 // 8 independent dots per thread (32 add chains in flight), dot.hpp:11-23 order
                 ExactDot4 d[LK_KT / 8];
 #pragma unroll
@@ -1202,6 +1176,8 @@ __global__ void __launch_bounds__(LK_THREADS) largek_topk_kernel(
             __syncthreads();  // this buffer is refilled by the prefetch of the next iteration
         }
         __syncthreads();
+        done = span;
+        }
         // ---- per row: radix select, collect, sort, write
 #ifdef LK_SKIP_SELECT
         continue;
@@ -1391,7 +1367,7 @@ __global__ void __launch_bounds__(LK_THREADS) largek_topk_kernel(
                     __syncthreads();
                 }
             }
-            const int64_t row = (int64_t)h * Wq + w0 + r;
+            const int64_t row = row_id[r];
             for (int i = tid; i < k_eff; i += LK_THREADS) {
                 const unsigned long long e = sb[i];
                 topk[row * k_eff + i] = (int32_t)(0xffffffffu - (uint32_t)(e & 0xffffffffu));
@@ -1444,9 +1420,9 @@ Ws carve_ws(void* base, int heads, int Wq, int Wk, int k_eff, bool dry) {
     w.cand = reinterpret_cast<float2*>(take(large_k ? 8 : nq * (size_t)ccap_for(k_eff, true) * 8));
     w.cand_n = reinterpret_cast<int*>(take(nq * 4));
     w.flag = reinterpret_cast<uint8_t*>(take(nq));
-    w.blocks = reinterpret_cast<int*>(take(nq * 4));  // flagged rows
+    w.blocks = reinterpret_cast<int*>(take(nq * 4 + ((nq + 1023) / 1024 + 1) * 4));  // flagged rows + block counts
     w.nblocks = reinterpret_cast<int*>(take(4));
-    w.scratch = reinterpret_cast<uint32_t*>(take((size_t)(large_k ? LK_CTAS * LK_ROWS : XR_CTAS) * Wk * 4));
+    w.scratch = reinterpret_cast<uint32_t*>(take((size_t)LK_CTAS * LK_ROWS * Wk * 4));  // large-k / fallback scores
     w.used = off + 256;
     return w;
 }
@@ -1629,14 +1605,22 @@ cudaError_t tc_compress_topk_splits(const CompressSplits* pre, const gsa_tensor&
                 qcp, qc.head_stride, kcp, H, Wq, Wk, scale, k_eff, qn, w.kmax, w.cmax, w.cand, w.cand_n, w.flag, topk, guide);
         }
         note_launch();
-        // rows whose candidate list overflowed (near-tie floods): exact recompute per row
-        cudaMemsetAsync(w.nblocks, 0, sizeof(int), st);
-        flag_rows_kernel<<<(unsigned)((rows + 255) / 256), 256, 0, st>>>(w.flag, rows, w.blocks, w.nblocks);
-        exact_row_kernel<<<XR_CTAS, XR_THREADS, 0, st>>>(static_cast<const float*>(qc.data), qc.head_stride,
-                                                          static_cast<const float*>(kc.data), Wq, Wk, scale, k_eff,
-                                                          excluded ? w.exbits : nullptr, w.blocks, w.nblocks,
-                                                          w.scratch, topk, guide);
-        note_launch(2);
+        // rows whose candidate list overflowed (near-tie floods, clumps of near-equal keys):
+        // exact recompute of just those rows by the large-k kernel in row-list mode (exact
+        // scores tiled over blocks of 32 listed rows, radix select, lowest-index ties, sort)
+        const unsigned nfb = (unsigned)((rows + FL_BLOCK - 1) / FL_BLOCK);
+        int* fl_counts = w.blocks + rows;  // carve_ws reserves rows + nfb ints
+        flag_count_kernel<<<nfb, FL_BLOCK, 0, st>>>(w.flag, rows, fl_counts);
+        flag_scan_kernel<<<1, 1024, 0, st>>>(fl_counts, (int)nfb, w.nblocks);
+        flag_scatter_kernel<<<nfb, FL_BLOCK, 0, st>>>(w.flag, rows, fl_counts, w.blocks);
+        const size_t lk_smem = LK_SMEM;
+        cudaError_t e3 = cudaFuncSetAttribute(largek_topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lk_smem);
+        if (e3 != cudaSuccess) return e3;
+        largek_topk_kernel<<<LK_CTAS, LK_THREADS, lk_smem, st>>>(static_cast<const float*>(qc.data), qc.head_stride,
+                                                                  static_cast<const float*>(kc.data), H, Wq, Wk, scale,
+                                                                  k_eff, excluded ? w.exbits : nullptr, w.scratch, topk,
+                                                                  guide, w.blocks, w.nblocks);
+        note_launch(4);
         if (getenv("GSA_DEBUG_STATS")) {  // bring-up: candidate statistics (synchronises)
             const int64_t rows = (int64_t)H * Wq;
             std::vector<int> cn(rows);
