@@ -65,7 +65,15 @@ constexpr int KCAP = 128;               // max k_eff on this path
 // of the approximate radix select handed to the exact re-score: sized by k
 // (the streamed count grows like k (1 + ln(W / k)))
 // hybrid rows (excluded reference windows) start from a weaker first-tile bound: more candidates
-__host__ __device__ constexpr int ccap_for(int k, bool excl = false) { return k <= 32 ? (excl ? 1024 : 512) : 2048; }
+#ifndef COMP_PLAIN_CCAP
+#define COMP_PLAIN_CCAP 1024
+#endif
+__host__ __device__ constexpr int ccap_for(int k, bool excl = false) {
+    return k <= 32 ? (excl ? 1024 : COMP_PLAIN_CCAP) : 2048;
+}
+// (a row's candidate count is typically ~k(1 + ln(W/k)), ~330 at k = 32, W = 81000; the
+// larger list absorbs clumps of near-equal keys -- clustered activations -- and the
+// re-score splits rows by count so the common case keeps the 512-entry register tile)
 __host__ __device__ constexpr int surv_for(int k) { return k <= 32 ? 64 : 256; }
 constexpr int NBIN = 8;                 // threshold histogram bins (8-bit saturating counters)
 constexpr float EPS_REL = 0.00048828125f;          // 2^-11: split + accumulation error, x |q| max|kc - kbar|
@@ -730,7 +738,7 @@ __global__ void __launch_bounds__(256) rescore_kernel(const float* __restrict__ 
                                                       const float* __restrict__ kc, int heads, int Wq, int Wk,
                                                       float scale, int k_eff, const float* __restrict__ qnorm,
                                                       const float* __restrict__ kmax, const float* __restrict__ cmax,
-                                                      const float2* __restrict__ cand,
+                                                      const float2* __restrict__ cand, int cstride, int n_lo, int n_hi,
                                                       const int* __restrict__ cand_n, uint8_t* flag, int32_t* topk,
                                                       float* guide) {
     constexpr int CC = PER * 32, SV = SLOTS * 32;  // candidate capacity / survivor capacity
@@ -738,9 +746,11 @@ __global__ void __launch_bounds__(256) rescore_kernel(const float* __restrict__ 
     const int64_t r = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
     const int lane = threadIdx.x & 31;
     if (r >= (int64_t)heads * Wq || flag[r]) return;
+    // this instance takes the rows with n_lo < candidates <= n_hi (register capacity CC)
+    if (cand_n[r] <= n_lo || cand_n[r] > n_hi) return;
     const int h = (int)(r / Wq);
     const int n = min(cand_n[r], CC);
-    const float2* cr = cand + r * CC;
+    const float2* cr = cand + r * cstride;
     float2 cv[PER];
     uint32_t key[PER];
 #pragma unroll
@@ -1591,18 +1601,22 @@ cudaError_t tc_compress_topk_splits(const CompressSplits* pre, const gsa_tensor&
         const int64_t rows = (int64_t)H * Wq;
         const float* qcp = static_cast<const float*>(qc.data);
         const float* kcp = static_cast<const float*>(kc.data);
-        if (k_eff <= 32 && !excluded) {
-            static_assert(ccap_for(32) == 16 * 32 && surv_for(32) == 2 * 32, "rescore instance");
-            rescore_kernel<16, 2><<<(unsigned)((rows + 7) / 8), 256, 8 * 64 * sizeof(float2), st>>>(
-                qcp, qc.head_stride, kcp, H, Wq, Wk, scale, k_eff, qn, w.kmax, w.cmax, w.cand, w.cand_n, w.flag, topk, guide);
-        } else if (k_eff <= 32) {
-            static_assert(ccap_for(32, true) == 32 * 32, "rescore instance");
-            rescore_kernel<32, 2><<<(unsigned)((rows + 7) / 8), 256, 8 * 64 * sizeof(float2), st>>>(
-                qcp, qc.head_stride, kcp, H, Wq, Wk, scale, k_eff, qn, w.kmax, w.cmax, w.cand, w.cand_n, w.flag, topk, guide);
+        const unsigned rb = (unsigned)((rows + 7) / 8);
+        const int cs = ccap_for(k_eff, excluded != nullptr);
+        if (k_eff <= 32) {
+            static_assert(ccap_for(32) == 1024 && ccap_for(32, true) == 1024 && surv_for(32) == 2 * 32, "rescore instances");
+            rescore_kernel<16, 2><<<rb, 256, 8 * 64 * sizeof(float2), st>>>(
+                qcp, qc.head_stride, kcp, H, Wq, Wk, scale, k_eff, qn, w.kmax, w.cmax, w.cand, cs, -1, 512, w.cand_n,
+                w.flag, topk, guide);
+            rescore_kernel<32, 2><<<rb, 256, 8 * 64 * sizeof(float2), st>>>(
+                qcp, qc.head_stride, kcp, H, Wq, Wk, scale, k_eff, qn, w.kmax, w.cmax, w.cand, cs, 512, 1024, w.cand_n,
+                w.flag, topk, guide);
+            note_launch();
         } else {
             static_assert(ccap_for(128) == 64 * 32 && ccap_for(128, true) == 64 * 32 && surv_for(128) == 8 * 32, "rescore instance");
-            rescore_kernel<64, 8><<<(unsigned)((rows + 7) / 8), 256, 8 * 256 * sizeof(float2), st>>>(
-                qcp, qc.head_stride, kcp, H, Wq, Wk, scale, k_eff, qn, w.kmax, w.cmax, w.cand, w.cand_n, w.flag, topk, guide);
+            rescore_kernel<64, 8><<<rb, 256, 8 * 256 * sizeof(float2), st>>>(
+                qcp, qc.head_stride, kcp, H, Wq, Wk, scale, k_eff, qn, w.kmax, w.cmax, w.cand, cs, -1, 2048, w.cand_n,
+                w.flag, topk, guide);
         }
         note_launch();
         // rows whose candidate list overflowed (near-tie floods, clumps of near-equal keys):
