@@ -479,3 +479,29 @@ def test_oversmoothed_keys_bitexact(gsa, ref, eps):
     assert np.abs(o - rf["out"]).max() < 1e-4 and rel_l2(o, rf["out"]) < 1e-5
     if "lse_comp" in rf:
         assert np.abs(host(ctx.lse_comp) - rf["lse_comp"]).max() < 1e-4
+
+
+def test_clustered_views_bitexact(gsa, ref):
+    """Clustered activations (the reference's kClustered recipe, workload.hpp:78-90: a
+    per-view centroid + 0.5 N(0,1)): a view's windows arrive as a clump of near-equal
+    scores, so candidate lists fill in bursts (and may take the exact overflow path);
+    indices must stay bit-exact and the output within tolerance of the reference."""
+    lt = (80, 16, 36, 36, 4)
+    L = gsa.build_token_layout(*lt)
+    M, H = L.total_tokens, 2
+    g = torch.Generator(device="cuda").manual_seed(21)
+    view_of = torch.cat([torch.arange(80, device="cuda") // 5, torch.arange(M - 80, device="cuda") // 1296])
+
+    def synth():
+        cen = torch.randn(H, 16, 64, generator=g, device="cuda")
+        return (cen[:, view_of] + 0.5 * torch.randn(H, M, 64, generator=g, device="cuda")).to(torch.bfloat16)
+
+    q, k, v = synth(), synth(), synth()
+    wg = torch.randn(H, 64, 64, generator=g, device="cuda") / 8
+    p = gsa.GsaParams(window_s=4, top_k=32)
+    out, ctx = gsa.gsa_forward(q, k, v, wg, L, p, context=True)
+    f = lambda t: t.float().cpu().numpy()
+    rf = ref.forward(f(q), f(k), f(v), f(wg), lt, top_k=32, variant=0, ref_stride=2)
+    np.testing.assert_array_equal(ctx.topk.cpu().numpy(), rf["topk"])
+    o = host(out)
+    assert np.abs(o - rf["out"]).max() < 1e-4 and rel_l2(o, rf["out"]) < 1e-5

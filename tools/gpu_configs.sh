@@ -17,6 +17,8 @@ for l in open("$OUT"):
     except Exception as e:
         print("bad line", l[:200])
 PY
+# clustered activations (the reference's kClustered recipe) at 1000 views
+timeout 600 python bench.py --views 1000 --data clustered --steps 2 --warmup 3 --no-cpu-baseline --no-e2e --no-dense 2>/dev/null | tail -1 >> $OUT
 # hybrid (VGGT reference frames every 100 views) at 1000 views
 timeout 600 python bench.py --views 1000 --hybrid 100 --steps 2 --warmup 3 --no-cpu-baseline --no-e2e --no-dense 2>/dev/null | tail -1 >> $OUT
 tail -1 $OUT | cut -c1-600
