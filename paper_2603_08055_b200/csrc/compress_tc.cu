@@ -6,20 +6,24 @@
 // split x = hi + lo (bf16 each, |x - hi - lo| <= 2^-16 |x|) and
 //   S  = Qh.Kh^T + Qh.Kl^T + Ql.Kh^T            (12 MMAs, M=N=128, per key tile)
 //   O += Ph.Vh + Ph.Vl + Pl.Vh                  (24 MMAs, P from TMEM)
-// give softmax/PV far inside the tolerance. S is only an APPROXIMATION of the
-// reference guide score (scaled_dot: 4 stride-4 f32 lane sums, no FMA), so the
-// top-k runs in two steps:
-//   1. here, per query row (one thread = one TMEM lane): a sorted list of the
-//      k_eff best approximate scores plus a side list of everything within the
-//      margin 2*eps + delta of the running k-th score, where
-//      eps = 2^-11 * ||qc|| * max_j ||kc_j|| bounds |S - exact| (split error
-//      <= 3.1*2^-16 sum|q k|, f32 accumulation << that; Cauchy-Schwarz).
+// give softmax/PV far inside the tolerance. The scores run on centred keys
+// kc - kbar (kbar = per-head mean key: a per-row shift, invisible to the softmax and
+// the ranking, added back to the lse). S is only an APPROXIMATION of the reference
+// guide score (scaled_dot: 4 stride-4 f32 lane sums, no FMA), so the top-k runs in
+// two steps:
+//   1. here, per query row (one thread = one TMEM lane): a lower bound LB of the
+//      row's k-th best approximate score (seeded from key tile 0, raised by an
+//      8-bin histogram of the streamed candidates) and a candidate list in global
+//      memory of every selectable score >= LB - margin, margin = 2 eps + 2^-20 |LB|,
+//      eps = 2^-11 ||qc|| max ||kc - kbar|| + 2^-17 ||qc|| max ||kc|| >= |S' - exact'|.
 //      Every true top-k member satisfies S >= tau - 2 eps (tau: k-th largest S),
 //      so the candidate set is a guaranteed superset;
-//   2. rescore_kernel: exact scaled_dot for each candidate, rank by
-//      (score desc, index asc) = topk_better (compression.hpp:67-73).
-// A row whose side list overflows (mass near-ties, e.g. identical keys) is
-// flagged and recomputed by the exact CUDA-core kernel (attn_f32.cu).
+//   2. rescore_kernel: the k-th best approximate score by radix select, the
+//      survivors within the margin, exact scaled_dot for each, a warp bitonic sort
+//      by (score desc, index asc) = topk_better (compression.hpp:67-73).
+// Rows whose list overflows (mass near-ties, clumps of near-equal keys) are
+// re-selected exactly by largek_topk_kernel in row-list mode; k_eff > 128 (budget
+// sweep) runs the softmax here and the whole selection in largek_topk_kernel.
 #include <cuda.h>
 
 #include <cstdio>
