@@ -56,6 +56,9 @@ constexpr float RESCALE_LOG2 = 8.0f;
 #define COMP_SM_REGS 224
 #define COMP_PROD_REGS 56
 #endif
+#ifndef COMP_SMALL_K_BIN_DIV
+#define COMP_SMALL_K_BIN_DIV 8  // histogram bin width std/div for k <= 32
+#endif
 #ifndef COMP_LARGE_K_BIN_DIV
 #define COMP_LARGE_K_BIN_DIV 4  // histogram bin width std/div for k > 32 (k=128 @500 views: 8 -> 49.4 ms, 4 -> 45.6 ms)
 #endif
@@ -473,7 +476,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 const float mean = s1 / nk, var = fmaxf(s2 / nk - mean * mean, 0.0f);
                 tk.lb = fkey_inv(res);
                 tk.thr = topk_threshold(tk.lb, tk.eps);
-                const float bin_div = K <= 32 ? (float)NBIN : (float)COMP_LARGE_K_BIN_DIV;
+                const float bin_div = K <= 32 ? (float)COMP_SMALL_K_BIN_DIV : (float)COMP_LARGE_K_BIN_DIV;
                 tk.delta = var > 0.0f ? sqrtf(var) / bin_div : fmaxf(fabsf(tk.lb) * 0.0009765625f, 1e-30f);
                 tk.inv_delta = 1.0f / tk.delta;
             }
