@@ -60,11 +60,13 @@ constexpr int NS = SEL_NS;               // ring stages
 constexpr int STAGE = 16384;             // 8 windows x 2 KB
 constexpr int WIN = 2048;                // 16 tokens x 64 bf16
 constexpr int NTHREADS = 192;
-constexpr uint32_t TMEM_COLS = 256;
-constexpr uint32_t S_COL0 = 0, S_COL1 = 64, O_COL0 = 128, O_COL1 = 144, G_COL0 = 160;  // G buffer b at G_COL0 + 16 b
 constexpr int NGB = 3;  // G^T buffers: item j+1's G MMA must not wait for item j-1's epilogue
 constexpr int GROUP_WIN = SEL_GROUP_WIN;  // windows per softmax group (<= 32, 16 keys each)
 constexpr int P_QSTRIDE = GROUP_WIN * 256; // bytes per 8-query half of a P^T buffer
+// TMEM: two S^T buffers (16 columns per 8-window chunk of the group), two O^T, NGB G^T
+constexpr uint32_t S_COLS = (GROUP_WIN / 8) * 16;
+constexpr uint32_t S_COL0 = 0, S_COL1 = S_COLS, O_COL0 = 2 * S_COLS, O_COL1 = O_COL0 + 16, G_COL0 = O_COL1 + 16;
+constexpr uint32_t TMEM_COLS = (G_COL0 + 16 * NGB <= 128) ? 128 : 256;  // power of two >= the layout
 constexpr int PREFETCH_AHEAD = 0;   // items of L2 prefetch ahead of the gathers (2 measured slower: 54 -> 71 ms)
 
 struct __align__(1024) SelSmem {
