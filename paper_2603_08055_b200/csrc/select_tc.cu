@@ -67,7 +67,10 @@ constexpr int P_QSTRIDE = GROUP_WIN * 256; // bytes per 8-query half of a P^T bu
 constexpr uint32_t S_COLS = (GROUP_WIN / 8) * 16;
 constexpr uint32_t S_COL0 = 0, S_COL1 = S_COLS, O_COL0 = 2 * S_COLS, O_COL1 = O_COL0 + 16, G_COL0 = O_COL1 + 16;
 constexpr uint32_t TMEM_COLS = (G_COL0 + 16 * NGB <= 128) ? 128 : 256;  // power of two >= the layout
-constexpr int PREFETCH_AHEAD = 0;   // items of L2 prefetch ahead of the gathers (2 measured slower: 54 -> 71 ms)
+#ifndef SEL_PF
+#define SEL_PF 0
+#endif
+constexpr int PREFETCH_AHEAD = SEL_PF;  // items of L2 prefetch ahead of the gathers (measured slower: 1 CTA/SM 54 -> 71 ms; 2 CTAs/SM 34 -> 47 ms)
 
 struct __align__(1024) SelSmem {
     uint8_t ring[NS][STAGE];
