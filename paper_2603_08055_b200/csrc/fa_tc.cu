@@ -2,16 +2,18 @@
 // special-token path (special_token_attention / tiled_attention,
 // layer.hpp:80-96, compression.hpp:99-165) and the dense baseline.
 //
-// CTA = 128 query rows x one head x one key split. Warp roles:
-//   warp 0  TMA: Q tile once, then K(t+1), V(t) tiles of 128 keys (16 KB each,
-//           128B-swizzled) through a 6-stage ring.
-//   warp 1  MMA: S(t) = Q.K(t)^T  (M=128, N=128, K=64, both K-major, into TMEM,
-//           3 rotating S buffers), O += P(t).V(t) with P read from TMEM
+// CTA = two 128-query tiles x one head x one key split. Warp roles:
+//   warp 8  TMA: both Q tiles once, then K / V tiles of 128 keys (16 KB each,
+//           128B-swizzled) through a 12-stage ring in the MMA's first-use order,
+//           plus L2 prefetches FA_PF tiles ahead.
+//   warp 9  MMA: S(n) = Q_w.K(t)^T  (M=128, N=128, K=64, into TMEM, 3 rotating
+//           S/P buffers, n = 2t + w), O_w += P(n).V(t) with P read from TMEM
 //           (A-from-TMEM form, P as bf16 hi + lo: 2 MMAs per 16-key step).
-//   warps 2-5  softmax, one thread per query row = one TMEM lane: row max,
-//           lazy rescale (only when the max grows by > 2^8; O is then rescaled
-//           in TMEM), P = exp2 via MUFU, written back over S in TMEM as
-//           bf16 hi/lo pairs; epilogue O/l and lse.
+//   warps 0-7  softmax, one warpgroup per query tile, one thread per query row =
+//           one TMEM lane: two passes per tile (row max over the loaded scores,
+//           then P chunk by chunk from a TMEM re-read), lazy rescale (only when
+//           the max grows by > 2^8; O is then rescaled in TMEM), P = exp2 via
+//           MUFU written back over S as bf16 hi/lo pairs; epilogue O/l and lse.
 // Split-KV (few query tiles, e.g. 5 specials/view) writes normalised partials
 // + lse that gsa_fa_combine merges.
 #include <cuda.h>
