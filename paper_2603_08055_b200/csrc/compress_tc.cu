@@ -1615,7 +1615,7 @@ cudaError_t tc_compress_topk_splits(const CompressSplits* pre, const gsa_tensor&
         const unsigned rb = (unsigned)((rows + 7) / 8);
         const int cs = ccap_for(k_eff, excluded != nullptr);
         if (k_eff <= 32) {
-            static_assert(ccap_for(32) == 1024 && ccap_for(32, true) == 1024 && surv_for(32) == 2 * 32, "rescore instances");
+            static_assert(ccap_for(32) <= 1024 && ccap_for(32, true) <= 1024 && surv_for(32) == 2 * 32, "rescore instances");
             rescore_kernel<16, 2><<<rb, 256, 8 * 64 * sizeof(float2), st>>>(
                 qcp, qc.head_stride, kcp, H, Wq, Wk, scale, k_eff, qn, w.kmax, w.cmax, w.cand, cs, -1, 512, w.cand_n,
                 w.flag, topk, guide);
