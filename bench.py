@@ -45,6 +45,29 @@ def geometry(views: int):
     return dict(Ms=ns, Mi=mi, M=ns + mi, W=W)
 
 
+def synth_qkv(torch, views, heads=HEADS, dim=DIM, data="normal", seed=7, device="cuda", grid=None, specials=None):
+    """Synthetic post-projection Q/K/V [H][M][d] bf16 on the device (and W_g f32):
+    iid N(0,1), or the reference's kClustered recipe (workload.hpp:78-90: a per-view
+    centroid + 0.5 N(0,1), shared by the view's specials and patches)."""
+    gh, gw = grid or (GRID_H, GRID_W)
+    spv = SPECIAL_PER_VIEW if specials is None else specials
+    ms, mi = spv * views, views * gh * gw
+    M = ms + mi
+    gen = torch.Generator(device=device).manual_seed(seed)
+
+    def one():
+        x = torch.randn(heads, M, dim, generator=gen, device=device, dtype=torch.float32)
+        if data == "clustered":
+            cen = torch.randn(heads, views, dim, generator=gen, device=device, dtype=torch.float32)
+            view_of = torch.cat([torch.arange(ms, device=device) // max(1, spv),
+                                 torch.arange(mi, device=device) // (gh * gw)])
+            x = cen[:, view_of] + 0.5 * x
+        return x.to(torch.bfloat16)
+    q, k, v = one(), one(), one()
+    wg = torch.randn(heads, dim, dim, generator=gen, device=device) / 8.0
+    return q, k, v, wg
+
+
 def load_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -96,7 +119,7 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------- CPU baseline
-def cpu_reference_sample(views_target: int, sample_views: int = 16, repeats: int = 2):
+def cpu_reference_sample(views_target: int, sample_views: int = 16, repeats: int = 3):
     """The reference's own fused CPU layer (oracle/_ref, compiled unmodified from
     /root/reference) on a bounded sample: the same per-view geometry with
     `sample_views` views, all host threads. Stage times are extrapolated to the
@@ -120,6 +143,7 @@ def cpu_reference_sample(views_target: int, sample_views: int = 16, repeats: int
             orc.gsa_forward(q, k, v, wg, L, top_k=TOPK)
             runs.append({"total": (time.perf_counter() - t0) * 1e3})
     st = {key: statistics.median(r[key] for r in runs) for key in runs[0]}
+    totals = [sum(r.values()) for r in runs]
     gs, gt = geometry(sample_views), geometry(views_target)
     law = {"partition": gt["M"] / gs["M"], "special": (gt["Ms"] * gt["M"]) / max(1, gs["Ms"] * gs["M"]),
            "pool": gt["Mi"] / gs["Mi"], "compress": (gt["W"] / gs["W"]) ** 2, "plan": gt["W"] / gs["W"],
@@ -131,7 +155,8 @@ def cpu_reference_sample(views_target: int, sample_views: int = 16, repeats: int
                         f"median of {repeats}, {sample_ms/1e3:.1f} s per run; stages extrapolated to {views_target} "
                         f"views by cost law (compress ~W^2, special ~Ms*M, rest ~M_i)"),
                 sample_stage_ms={k_: round(v_, 1) for k_, v_ in st.items()},
-                extrapolated_ms=round(ms_target, 1))
+                extrapolated_ms=round(ms_target, 1), extrapolated=views_target != sample_views, repeats=repeats,
+                spread=round((max(totals) - min(totals)) / statistics.median(totals), 3) if totals else None)
 
 
 def run_reference_arm(args):
@@ -157,7 +182,9 @@ def run_reference_arm(args):
                        "parallelism": f"CPU reference, {last['cores']} host threads (rank 0 only)",
                        "l2": "n/a (CPU)"},
             "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": last["cores"], "kind": last["kind"],
-                             "sample": last["sample"]},
+                             "sample": last["sample"], "extrapolated": last["extrapolated"],
+                             "repeats": len(steps),
+                             "spread": round((max(vals) - min(vals)) / v, 3) if vals else None},
             "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -248,6 +275,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--ref-sample-views", type=int, default=16)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-parity", action="store_true", help="skip the post-timing sampled-row parity check")
     ap.add_argument("--no-dense", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--shard", action="store_true", help="use the view-sharded layer even on 1 GPU")
@@ -292,20 +320,7 @@ def main():
     params = gsa.GsaParams(window_s=S, top_k=TOPK, variant=1 if args.hybrid else 0,
                            ref_stride=args.hybrid if args.hybrid else 100)
     geometry_default = (GRID_H, GRID_W, SPECIAL_PER_VIEW, TOPK, args.hybrid) == (36, 36, 5, 32, 0)
-    gen = torch.Generator(device=dev).manual_seed(7)
-    def synth():
-        x = torch.randn(HEADS, G["M"], DIM, generator=gen, device=dev, dtype=torch.float32)
-        if args.data == "clustered":
-            # the reference's kClustered recipe (workload.hpp:78-90): x = centroid(frame) + 0.5 x,
-            # one centroid per (head, view) shared by the view's specials and patches
-            cen = torch.randn(HEADS, args.views, DIM, generator=gen, device=dev, dtype=torch.float32)
-            ms = SPECIAL_PER_VIEW * args.views
-            view_of = torch.cat([torch.arange(ms, device=dev) // max(1, SPECIAL_PER_VIEW),
-                                 torch.arange(G["M"] - ms, device=dev) // (GRID_H * GRID_W)])
-            x = cen[:, view_of] + 0.5 * x
-        return x.to(torch.bfloat16)
-    q, k, v = (synth() for _ in range(3))
-    wg = torch.randn(HEADS, DIM, DIM, generator=gen, device=dev) / 8.0
+    q, k, v, wg = synth_qkv(torch, args.views, data=args.data, seed=7, device=dev)
     out = torch.empty(HEADS, G["M"], DIM, device=dev)
     ws = gsa.Workspace()
 
@@ -487,14 +502,43 @@ def main():
     if rank == 0 and not args.no_cpu_baseline:
         try:
             line["cpu_baseline"] = {k_: v_ for k_, v_ in cpu_reference_sample(args.views).items()
-                                    if k_ in ("value", "unit", "cores", "kind", "sample")}
+                                    if k_ in ("value", "unit", "cores", "kind", "sample", "extrapolated",
+                                              "repeats", "spread")}
         except Exception as e:  # the baseline is reported, never required
             line["cpu_baseline"] = {"value": None, "unit": "tokens/s", "cores": os.cpu_count(), "kind": "reference",
                                     "sample": f"failed: {e}"}
+        # parity of the timed workload (after the timed region; same CPU-reference leg):
+        # one more forward with its context, then seeded sampled rows recomputed by the
+        # unmodified reference -- 4 % of the windows of 4 heads = 1 % of all rows
+        if not sharded and not args.no_parity:
+            try:
+                line["parity"] = bench_parity(torch, gsa, q, k, v, wg, L, params, lt)
+            except Exception as e:
+                line["parity"] = {"error": f"{type(e).__name__}: {e}"}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def bench_parity(torch, gsa, q, k, v, wg, L, params, lt):
+    """Sampled-row parity of the benchmarked configuration against the unmodified
+    reference (oracle/sampled.py): top-k rows bit-exact, output rows within the
+    north-star tolerance. Outside the timed region."""
+    from oracle import RefLib
+    from oracle.sampled import sampled_parity
+    if not RefLib.available():
+        return {"error": "oracle/_ref not built"}
+    out, ctx = gsa.gsa_forward(q, k, v, wg, L, params, context=True)
+    torch.cuda.synchronize()
+    res = sampled_parity(q, k, v, wg, lt, params.top_k, out, ctx.topk, variant=params.variant,
+                         ref_stride=params.ref_stride, o_comp=ctx.o_comp_coarse, lse_comp=ctx.lse_comp,
+                         o_sel=ctx.o_sel, lse_sel=ctx.lse_sel, frac=0.04, heads=[0, 5, 10, 15],
+                         seed=1000 + lt[1])
+    res["tolerance"] = {"max_abs": 2e-2, "rel_l2": 1e-3, "topk": "bit-exact incl. order"}
+    res["pass"] = bool(res["topk_mismatches"] == 0 and res["max_abs"] <= 2e-2 and res["rel_l2"] <= 1e-3)
+    del out, ctx
+    return res
 
 
 def dense_baseline(torch, q, k, v, sparse_ms):

@@ -140,7 +140,8 @@ int gsa_forced_windows(const gsa_layout* layout, int ref_stride, int32_t* forced
 /* build_selection_plan (selection.cpp:29-67): device CSR plan from device
  * top-k rows [H][rows][k]. offsets [H*rows+1] int64; window_ids capacity
  * ids_capacity (plain: H*rows*k; hybrid: H*rows*(F+k) suffices). *n_ids
- * (host) is the realised size; this call synchronises `stream`. */
+ * (host) is the realised size; this call synchronises `stream`. A top-k id
+ * outside [0, W) is IndexOutOfRange. */
 int gsa_build_selection_plan(const int32_t* topk, int heads, int rows, int k,
                              const gsa_layout* layout, int variant, int ref_stride,
                              int64_t* offsets, int32_t* window_ids, int64_t ids_capacity,
@@ -150,9 +151,11 @@ size_t gsa_build_selection_plan_workspace_bytes(int heads, int rows, int k,
                                                 const gsa_layout* layout, int ref_stride);
 
 /* block_sparse_attention (selection.hpp:63-136) over a device CSR plan.
- * Validates that no row is empty (synchronises `stream`; EmptySelection; the
- * 4-byte flag for it is a stream-ordered cudaMallocAsync, the one allocation in
- * the library -- gsa_forward checks its own plan without it).
+ * Validates the plan before any compute (synchronises `stream`): an empty row
+ * is EmptySelection (selection.hpp:82-85), a window id outside [0, W) is
+ * IndexOutOfRange (tokens_of_window, layout.cpp:37-56). The 4-byte flag for it
+ * is a stream-ordered cudaMallocAsync, the one allocation in the library
+ * (gsa_forward builds its own plan and needs no check).
  * out f32 [H][Mi][d], lse [H][Mi]. */
 int gsa_block_sparse_attention(const gsa_tensor* q_img, const gsa_tensor* k_img,
                                const gsa_tensor* v_img, const int64_t* offsets,
@@ -175,7 +178,9 @@ int gsa_forward(const gsa_tensor* q, const gsa_tensor* k, const gsa_tensor* v,
                 size_t workspace_bytes, gsa_stream_t stream);
 
 /* gsa_forward_with_plan (layer.hpp:235-262): selection pinned to a device CSR
- * plan; the compressed branch is plain tiled attention (no top-k). */
+ * plan; the compressed branch is plain tiled attention (no top-k, so no budget
+ * limit and no params.window_s check, as in the reference). The plan is
+ * validated like gsa_block_sparse_attention's (synchronises `stream`). */
 int gsa_forward_with_plan(const gsa_tensor* q, const gsa_tensor* k, const gsa_tensor* v,
                           const gsa_tensor* w_g, const gsa_layout* layout,
                           const gsa_params* params, const int64_t* offsets,

@@ -15,6 +15,9 @@
 #include <chrono>
 #include <cstdint>
 #include <cstring>
+#include <limits>
+#include <cmath>
+#include <algorithm>
 #include <string>
 #include <vector>
 
@@ -371,6 +374,150 @@ int gsa_ref_random_init(uint64_t seed, int ns, int nf, int gh, int gw, int s, in
         from_tensor(p.k, k);
         from_tensor(p.v, v);
         from_tensor(w.weights.w_g, w_g);
+    });
+}
+
+// Sampled-row parity at scale ("For V >= 500, use sampled-row parity"),
+// ONE head at a time: the reference's per-row path for a subset of query windows and
+// special rows, with the reference's own functions wherever they exist:
+//   pooling         avg_pool_tokens (compression.hpp:20-38, what gsa_forward uses)
+//   guide scores    scaled_dot (dot.hpp:11-23) over every key window, then
+//                   naive_topk / naive_topk_excluding (reference.hpp:79-109), exactly the
+//                   row body of reference_gsa (reference.hpp:236-247)
+//   compressed out  softmax_inplace + P.Vc (reference.hpp:248-253); lse = m + log(sum)
+//   plan row        build_selection_plan (selection.cpp:29-67) on a TopkResult holding
+//                   the sampled rows
+//   selection       the fused block_sparse_attention loop body (selection.hpp:100-133)
+//                   for the sampled window's s^2 queries (the masked O(M_i) oracle would
+//                   be O(M_i) per query: infeasible at 1.3M tokens)
+//   gate + merge    gate (layer.hpp:99-119) on the sampled query rows, then the
+//                   assemble_image_output formula (layer.hpp:154-170)
+//   special rows    special_token_attention -> tiled_attention (layer.hpp:80-96) of the
+//                   sampled special queries over all M keys
+// q/k/v: this head's rows [M][d] (specials first, then image tokens); w_g [d][d].
+// Outputs per sampled window i: topk [i][k_eff], guide [i][k_eff] (nullable), o_comp
+// [i][d], lse_comp [i], out_img / o_sel [i][s^2][d] (window member order), lse_sel
+// [i][s^2]; per sampled special j: out_spec [j][d].
+int gsa_ref_sampled_head(const float* q, const float* k, const float* v, const float* w_g, int dim, int ns,
+                         int nf, int gh, int gw, int s, int top_k, double scale_param, int variant,
+                         int ref_stride, const int32_t* wins, int n_wins, const int32_t* specs, int n_specs,
+                         int threads, int32_t* topk_out, float* guide_out, float* o_comp_out,
+                         float* lse_comp_out, float* out_img, float* o_sel_out, float* lse_sel_out,
+                         float* out_spec, int* k_eff_out) {
+    return guarded([&] {
+        auto l = gsa::build_token_layout(ns, nf, gh, gw, s);
+        gsa::GsaParams params = make_params(s, top_k, scale_param, variant, ref_stride, 16, 16);
+        gsa::validate_params(params);
+        const int m = l.total_tokens(), W = l.num_windows(), s2 = s * s;
+        const float scale = gsa::resolved_scale<float>(params, dim);
+        auto Q = to_tensor(q, 1, m, dim);
+        auto K = to_tensor(k, 1, m, dim);
+        auto V = to_tensor(v, 1, m, dim);
+        auto parts = gsa::partition_qkv(Q, K, V, l);
+        auto qc = gsa::avg_pool_tokens(parts.q_img, l);
+        auto kc = gsa::avg_pool_tokens(parts.k_img, l);
+        auto vc = gsa::avg_pool_tokens(parts.v_img, l);
+        std::vector<uint8_t> excluded;
+        if (params.variant == gsa::SelectionVariant::kHybrid)
+            excluded = gsa::forced_window_mask(l, params.ref_stride);
+        int selectable = W;
+        for (uint8_t e : excluded)
+            if (e) --selectable;
+        const int k_eff = std::min(params.top_k, selectable);
+        *k_eff_out = k_eff;
+        for (int i = 0; i < n_wins; ++i)
+            if (wins[i] < 0 || wins[i] >= W) throw gsa::IndexOutOfRange("sampled window out of range");
+
+        // per sampled row: guide scores, top-k, compressed softmax row (reference.hpp:236-253)
+        gsa::TopkResult topk(1, W, k_eff);
+        std::fill(topk.indices.begin(), topk.indices.end(), 0);
+        gsa::parallel_for(n_wins, threads, [&](int i) {
+            const int wq = wins[i];
+            std::vector<float> row(W);
+            const float* qrow = qc.row(0, wq);
+            for (int wk = 0; wk < W; ++wk) row[wk] = gsa::scaled_dot(qrow, kc.row(0, wk), dim, scale);
+            std::vector<int32_t> top =
+                excluded.empty() ? gsa::naive_topk(row, k_eff) : gsa::naive_topk_excluding(row, excluded, k_eff);
+            std::copy(top.begin(), top.end(), topk_out + (size_t)i * k_eff);
+            std::copy(top.begin(), top.end(), topk.row(0, wq));  // distinct rows: no race
+            if (guide_out)
+                for (int j = 0; j < k_eff; ++j) guide_out[(size_t)i * k_eff + j] = row[top[j]];
+            float mx = -std::numeric_limits<float>::infinity();
+            for (int wk = 0; wk < W; ++wk) mx = std::max(mx, row[wk]);
+            double sum = 0.0;
+            for (int wk = 0; wk < W; ++wk) sum += std::exp((double)row[wk] - mx);
+            lse_comp_out[i] = (float)(mx + std::log(sum));
+            gsa::softmax_inplace(row.data(), W);
+            float* orow = o_comp_out + (size_t)i * dim;
+            std::fill(orow, orow + dim, 0.0f);
+            for (int wk = 0; wk < W; ++wk) {
+                const float* vrow = vc.row(0, wk);
+                for (int d = 0; d < dim; ++d) orow[d] += row[wk] * vrow[d];
+            }
+        });
+
+        // plan rows (selection.cpp:29-67), then the fused selection loop per sampled window
+        auto plan = gsa::build_selection_plan(topk, l, params.variant, params.ref_stride);
+        gsa::Tensor<float> qsel(1, n_wins * s2, dim);  // the sampled windows' query rows, member order
+        for (int i = 0; i < n_wins; ++i) {
+            const auto members = l.tokens_of_window(wins[i]);
+            for (int j = 0; j < s2; ++j)
+                std::copy(parts.q_img.row(0, members[j]), parts.q_img.row(0, members[j]) + dim, qsel.row(0, i * s2 + j));
+        }
+        gsa::parallel_for(n_wins, threads, [&](int i) {
+            const int w = wins[i];
+            const int nsel = plan.row_size(0, w);
+            const int32_t* sel = plan.row(0, w);
+            std::vector<int> keys;  // selection.hpp:100-105
+            keys.reserve((size_t)nsel * s2);
+            for (int j = 0; j < nsel; ++j)
+                for (int member : l.tokens_of_window(sel[j])) keys.push_back(member);
+            std::vector<float> acc(dim);
+            for (int qi = 0; qi < s2; ++qi) {  // selection.hpp:112-133
+                const float* qrow = qsel.row(0, i * s2 + qi);
+                float mm = -std::numeric_limits<float>::infinity(), ll = 0.0f;
+                std::fill(acc.begin(), acc.end(), 0.0f);
+                for (int key : keys) {
+                    const float sc = gsa::scaled_dot(qrow, parts.k_img.row(0, key), dim, scale);
+                    if (sc > mm) {
+                        const float alpha = std::exp(mm - sc);
+                        for (int d = 0; d < dim; ++d) acc[d] *= alpha;
+                        ll *= alpha;
+                        mm = sc;
+                    }
+                    const float p = std::exp(sc - mm);
+                    ll += p;
+                    const float* vrow = parts.v_img.row(0, key);
+                    for (int d = 0; d < dim; ++d) acc[d] += p * vrow[d];
+                }
+                float* orow = o_sel_out + ((size_t)i * s2 + qi) * dim;
+                const float inv = 1.0f / ll;
+                for (int d = 0; d < dim; ++d) orow[d] = acc[d] * inv;
+                lse_sel_out[(size_t)i * s2 + qi] = mm + std::log(ll);
+            }
+        });
+        // gate (layer.hpp:99-119) + merge (layer.hpp:154-170)
+        auto Wg = to_tensor(w_g, 1, dim, dim);
+        auto g = gsa::gate(qsel, Wg);
+        for (int i = 0; i < n_wins; ++i)
+            for (int qi = 0; qi < s2; ++qi) {
+                const float* gr = g.row(0, i * s2 + qi);
+                const float* comp = o_comp_out + (size_t)i * dim;
+                const float* selr = o_sel_out + ((size_t)i * s2 + qi) * dim;
+                float* orow = out_img + ((size_t)i * s2 + qi) * dim;
+                for (int d = 0; d < dim; ++d) orow[d] = gr[d] * comp[d] + (1.0f - gr[d]) * selr[d];
+            }
+        // special rows over all M keys (layer.hpp:80-96)
+        if (n_specs > 0) {
+            gsa::Tensor<float> qs(1, n_specs, dim);
+            for (int j = 0; j < n_specs; ++j) {
+                if (specs[j] < 0 || specs[j] >= ns) throw gsa::IndexOutOfRange("sampled special row out of range");
+                std::copy(Q.row(0, specs[j]), Q.row(0, specs[j]) + dim, qs.row(0, j));
+            }
+            std::vector<float> lse;
+            auto os = gsa::special_token_attention(qs, K, V, scale, params.tiling, &lse, nullptr, threads);
+            from_tensor(os, out_spec);
+        }
     });
 }
 

@@ -331,6 +331,7 @@ size_t gsa_build_selection_plan_workspace_bytes(int heads, int rows, int k, cons
     c.take<int32_t>(W);
     c.take<uint8_t>(W);
     c.take<char>(scan_offsets_tmp_bytes(n));
+    c.take<int>(1);
     return c.used + 256;
 }
 
@@ -352,6 +353,7 @@ int gsa_build_selection_plan(const int32_t* topk, int heads, int rows, int k, co
     uint8_t* mask = c.take<uint8_t>(L.windows);
     const size_t tmp_bytes = scan_offsets_tmp_bytes(n);
     void* tmp = c.take<char>(tmp_bytes);
+    int* flag = c.take<int>(1);
     if (c.used > ws_bytes) return fail(GSA_ERR_WORKSPACE, "build_selection_plan: workspace %zu < %zu", ws_bytes, c.used);
     int nf = 0;
     if (variant == 1) {
@@ -359,15 +361,41 @@ int gsa_build_selection_plan(const int32_t* topk, int heads, int rows, int k, co
         GSA_CUDA(launch_forced(L, ref_stride, forced, mask, st));
     }
     const uint8_t* m = variant == 1 ? mask : nullptr;
-    GSA_CUDA(launch_plan_count(topk, n, k, m, nf, sizes, st));
+    GSA_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), st));
+    GSA_CUDA(launch_plan_count(topk, n, k, m, nf, L.windows, sizes, flag, st));
     GSA_CUDA(launch_scan_offsets(sizes, n, offsets, tmp, tmp_bytes, st));
-    int64_t total = 0;
-    GSA_CUDA(cudaMemcpyAsync(&total, offsets + n, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    // the CSR size decides the ids capacity: one host read (the call's documented sync)
+    struct { int64_t total; int flag; } hb{0, 0};
+    GSA_CUDA(cudaMemcpyAsync(&hb.total, offsets + n, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    GSA_CUDA(cudaMemcpyAsync(&hb.flag, flag, sizeof(int), cudaMemcpyDeviceToHost, st));
     GSA_CUDA(cudaStreamSynchronize(st));
+    if (hb.flag & 2)
+        return fail(GSA_ERR_INDEX_OUT_OF_RANGE, "build_selection_plan: a top-k window id is outside [0, %d)", L.windows);
+    const int64_t total = hb.total;
     if (n_ids) *n_ids = total;
     if (total > ids_capacity)
         return fail(GSA_ERR_WORKSPACE, "build_selection_plan: ids capacity %lld < %lld", (long long)ids_capacity, (long long)total);
-    GSA_CUDA(launch_plan_fill(topk, n, k, m, forced, nf, offsets, ids, st));
+    GSA_CUDA(launch_plan_fill(topk, n, k, m, forced, nf, L.windows, offsets, ids, st));
+    return GSA_OK;
+}
+
+// A caller-supplied plan, validated before any compute (one host read: the documented
+// sync of the pinned-plan entry points): EmptySelection for an empty row
+// (selection.hpp:82-85), IndexOutOfRange for a window id outside [0, W) (the
+// reference's tokens_of_window check, layout.cpp:37-56).
+static int validate_plan(const int64_t* offsets, const int32_t* ids, int64_t rows, int W, const char* who,
+                         cudaStream_t st) {
+    if (!offsets || !ids) return fail(GSA_ERR_GENERIC, "%s: null plan", who);
+    int* flag = nullptr;
+    GSA_CUDA(cudaMallocAsync(&flag, sizeof(int), st));
+    GSA_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), st));
+    GSA_CUDA(launch_plan_check(offsets, rows, ids, W, flag, st));
+    int h = 0;
+    GSA_CUDA(cudaMemcpyAsync(&h, flag, sizeof(int), cudaMemcpyDeviceToHost, st));
+    GSA_CUDA(cudaFreeAsync(flag, st));
+    GSA_CUDA(cudaStreamSynchronize(st));
+    if (h & 1) return fail(GSA_ERR_EMPTY_SELECTION, "%s: empty plan row", who);
+    if (h & 2) return fail(GSA_ERR_INDEX_OUT_OF_RANGE, "%s: plan window id outside [0, %d)", who, W);
     return GSA_OK;
 }
 
@@ -397,17 +425,7 @@ int gsa_block_sparse_attention(const gsa_tensor* q, const gsa_tensor* k, const g
     cudaStream_t st = (cudaStream_t)stream;
     const int64_t n = (int64_t)q->heads * L.windows;
     if (n == 0) return GSA_OK;
-    {  // EmptySelection (selection.hpp:82-85): checked before any compute
-        int* flag = nullptr;
-        GSA_CUDA(cudaMallocAsync(&flag, sizeof(int), st));
-        GSA_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), st));
-        GSA_CUDA(launch_empty_row_check(offsets, n, flag, st));
-        int h = 0;
-        GSA_CUDA(cudaMemcpyAsync(&h, flag, sizeof(int), cudaMemcpyDeviceToHost, st));
-        GSA_CUDA(cudaFreeAsync(flag, st));
-        GSA_CUDA(cudaStreamSynchronize(st));
-        if (h) return fail(GSA_ERR_EMPTY_SELECTION, "block_sparse_attention: empty plan row");
-    }
+    GSA_TRY(validate_plan(offsets, ids, n, L.windows, "block_sparse_attention", st));
     SelectArgs a{};
     a.q = ref_of(*q);
     a.k = ref_of(*k);
@@ -450,10 +468,13 @@ struct LayerPlan {
     float scale;
 };
 
+// with_plan: gsa_forward_with_plan (layer.hpp:235-262) validates the params but neither
+// checks params.window_s against the layout nor runs a top-k (so no budget limit)
 int layer_checks(const gsa_tensor* q, const gsa_tensor* k, const gsa_tensor* v, const gsa_tensor* w_g,
-                 const gsa_layout* layout, const gsa_params* p, const gsa_tensor* out, LayerPlan* lp) {
+                 const gsa_layout* layout, const gsa_params* p, const gsa_tensor* out, LayerPlan* lp,
+                 bool with_plan = false) {
     GSA_TRY(check_layout(layout));
-    GSA_TRY(gsa_validate_params(p, layout));
+    GSA_TRY(gsa_validate_params(p, with_plan ? nullptr : layout));
     GSA_TRY(check_tensor(q, "q"));
     GSA_TRY(check_tensor(k, "k"));
     GSA_TRY(check_tensor(v, "v"));
@@ -483,8 +504,12 @@ int layer_checks(const gsa_tensor* q, const gsa_tensor* k, const gsa_tensor* v, 
     const int sel = selectable_windows(L, p->variant, p->ref_stride, &lp->n_forced);
     lp->k_eff = p->top_k < sel ? p->top_k : sel;
     lp->scale = resolved_scale(p->scale, q->dim);
-    if (lp->k_eff > 2048)
+    if (with_plan) {
+        lp->k_eff = 0;  // no top-k on the pinned-plan path
+        lp->n_forced = 0;
+    } else if (lp->k_eff > 2048) {
         return fail(GSA_ERR_UNSUPPORTED, "gsa_forward: k_eff=%d > 2048 not implemented on sm_100a yet", lp->k_eff);
+    }
     return GSA_OK;
 }
 
@@ -629,7 +654,7 @@ int gsa_forward(const gsa_tensor* q, const gsa_tensor* k, const gsa_tensor* v, c
     a.o_sel_ctx = ctx ? ctx->o_sel : nullptr;
     a.gate_ctx = ctx ? ctx->gate : nullptr;
     a.wg_prep = b.wg_prep;
-    const bool tc_sel = tc_select_supported(*q, lp.L, a.rows);
+    const bool tc_sel = tc_select_supported(a);
     if (tc_sel && params->variant == 1 && lp.n_forced > 0 && lp.k_eff > 0 && b.kf && q->dim == 64 &&
         tc_dense_supported(*q, *k, *v)) {
         // Hybrid fast path. Every query attends ALL reference-frame keys (selection.cpp:55-59:
@@ -678,12 +703,13 @@ int gsa_forward_with_plan(const gsa_tensor* q, const gsa_tensor* k, const gsa_te
                           const int32_t* ids, const gsa_tensor* out, void* workspace, size_t ws_bytes,
                           gsa_stream_t stream) {
     LayerPlan lp;
-    GSA_TRY(layer_checks(q, k, v, w_g, layout, params, out, &lp));
+    GSA_TRY(layer_checks(q, k, v, w_g, layout, params, out, &lp, true));
     cudaStream_t st = (cudaStream_t)stream;
     LayerBufs b;
     const size_t need = carve(lp, nullptr, static_cast<char*>(workspace), ws_bytes, false, &b);
     if (need > ws_bytes + 256) return fail(GSA_ERR_WORKSPACE, "gsa_forward_with_plan: workspace %zu < %zu", ws_bytes, need);
     const int H = lp.heads, d = lp.dim;
+    GSA_TRY(validate_plan(offsets, ids, (int64_t)H * lp.W, lp.W, "gsa_forward_with_plan", st));
     GSA_TRY(dense_attention(q, k, v, lp.scale, out, b.lse_spec, 0, 0, lp.Ms, st));
     PoolJob jobs[3] = {
         {ref_of(*q, lp.Ms), b.qc, nullptr, nullptr, nullptr},
@@ -923,7 +949,7 @@ int gsa_shard_attend(const gsa_tensor* q_own, const gsa_tensor* k_all, const gsa
     a.w_g = static_cast<const float*>(w_g->data);
     a.o_comp = static_cast<const float*>(o_comp_own->data);
     a.wg_prep = b.wg_prep;
-    if (tc_select_supported(*q_own, sp.Lq, a.rows))
+    if (tc_select_supported(a))
         GSA_CUDA(tc_select_gate_merge(a, st));
     else
         GSA_CUDA(launch_select_f32(a, st));

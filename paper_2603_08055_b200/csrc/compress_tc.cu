@@ -39,6 +39,12 @@ namespace {
 
 using namespace ptx;
 
+// bring-up switches, compile-time only (-DGSA_DEBUG_COMPRESS=<bits>; 0 in every shipped build)
+#ifndef GSA_DEBUG_COMPRESS
+#define GSA_DEBUG_COMPRESS 0
+#endif
+constexpr int kDebug = GSA_DEBUG_COMPRESS;
+
 #ifndef COMP_NS
 #define COMP_NS 4
 #endif
@@ -103,7 +109,6 @@ struct __align__(1024) CompSmem {
 };
 
 struct CompParams {
-    int debug;  // bring-up switches (GSA_DEBUG_COMPRESS): 1 = no top-k scan, 16 = flag every row
     int heads, Wq, Wk, k_eff;  // query rows (windows of this shard) / key rows (all windows)
     float scale, c2;
     int kv_tiles;
@@ -413,7 +418,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         tk.ccap = p.ccap;
         tk.dst = p.cand + r * p.ccap;
 #ifdef COMPRESS_PROF
-        tk.dbg = p.debug;
+        tk.dbg = kDebug;
 #endif
         float m_used = -INFINITY, l = 0.0f;
 
@@ -421,7 +426,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         const bool prof_on = p.prof && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0;
         unsigned long long pt[8] = {0, 0, 0, 0, 0, 0, 0, 0}, pb[5] = {0, 0, 0, 0, 0}, c0 = clock64(), c1;
 #endif
-        const bool do_topk = K > 0 && !(p.debug & 1);
+        const bool do_topk = K > 0 && !(kDebug & 1);
         if (do_topk) {
             // ---- top-k seed from key tile 0 (its own register scope: peeled off the loop)
             // initial LB: the largest 16-bit key prefix P with >= K selectable keys >= P<<16
@@ -537,7 +542,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     }
                     cmax[c] = fmaxf(fmaxf(a0, a1), fmaxf(a2, a3));
                 }
-                if (do_topk && !(p.debug & 256)) {
+                if (do_topk && !(kDebug & 256)) {
                     // candidate masks: bit e = (S[e] >= tq) = NOT sign(S - tq) (FADD2), gathered by
                     // funnel shifts into four independent 8-bit chains per chunk
                     const float tq = tk.cnt < 0 ? INFINITY : tk.thr;
@@ -558,7 +563,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                             }
                         cmask[c] = ~(ch[0] | (ch[1] << 8) | (ch[2] << 16) | (ch[3] << 24)) & keep[c];
                     }
-                    if (p.debug & 128) cmask[0] = cmask[1] = cmask[2] = cmask[3] = 0u;  // bring-up: no extraction
+                    if (kDebug & 128) cmask[0] = cmask[1] = cmask[2] = cmask[3] = 0u;  // bring-up: no extraction
                 }
             }
             const float mt = fmaxf(fmaxf(cmax[0], cmax[1]), fmaxf(cmax[2], cmax[3]));
@@ -723,7 +728,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             }
             if (K > 0) {
                 p.cand_n[r] = tk.cnt < 0 ? 0 : tk.cnt;
-                p.flag[r] = (tk.cnt < 0 || (p.debug & 16)) ? 1 : 0;
+                p.flag[r] = (tk.cnt < 0 || (kDebug & 16)) ? 1 : 0;
             }
         }
     }
@@ -1547,7 +1552,6 @@ cudaError_t tc_compress_topk_splits(const CompressSplits* pre, const gsa_tensor&
         !make_rows_tmap(&tvh, vh, H, Wk, khs, 64) || !make_rows_tmap(&tvl, vl, H, Wk, khs, 64))
         return launch_attn_f32(ex, st);
     CompParams p{};
-    if (const char* dbg = getenv("GSA_DEBUG_COMPRESS")) p.debug = atoi(dbg);
     p.heads = H;
     p.Wq = Wq;
     p.Wk = Wk;
@@ -1646,7 +1650,8 @@ cudaError_t tc_compress_topk_splits(const CompressSplits* pre, const gsa_tensor&
                                                                   k_eff, excluded ? w.exbits : nullptr, w.scratch, topk,
                                                                   guide, w.blocks, w.nblocks);
         note_launch(4);
-        if (getenv("GSA_DEBUG_STATS")) {  // bring-up: candidate statistics (synchronises)
+#ifdef GSA_DEBUG_STATS
+        {  // bring-up builds only: candidate statistics (synchronises)
             const int64_t rows = (int64_t)H * Wq;
             std::vector<int> cn(rows);
             std::vector<uint8_t> fl(rows);
@@ -1671,6 +1676,7 @@ cudaError_t tc_compress_topk_splits(const CompressSplits* pre, const gsa_tensor&
                     ++shown;
                 }
         }
+#endif
     }
     return cudaGetLastError();
 }

@@ -95,13 +95,15 @@ cudaError_t launch_upsample(const float* coarse, int64_t c_hs, int64_t c_rs, int
 cudaError_t launch_forced(const DevLayout& L, int ref_stride, int32_t* forced, uint8_t* mask,
                           cudaStream_t st);
 cudaError_t launch_plan_count(const int32_t* topk, int64_t rows, int k, const uint8_t* mask,
-                              int n_forced, int64_t* sizes, cudaStream_t st);
+                              int n_forced, int n_windows, int64_t* sizes, int* flag, cudaStream_t st);
 cudaError_t launch_plan_fill(const int32_t* topk, int64_t rows, int k, const uint8_t* mask,
-                             const int32_t* forced, int n_forced, const int64_t* offsets,
+                             const int32_t* forced, int n_forced, int n_windows, const int64_t* offsets,
                              int32_t* ids, cudaStream_t st);
 cudaError_t launch_scan_offsets(const int64_t* sizes, int64_t n, int64_t* offsets, void* tmp,
                                 size_t tmp_bytes, cudaStream_t st);
 size_t scan_offsets_tmp_bytes(int64_t n);
-cudaError_t launch_empty_row_check(const int64_t* offsets, int64_t rows, int* flag, cudaStream_t st);
+// flag |= 1: empty plan row; flag |= 2: window id outside [0, n_windows) (ids may be null: rows only)
+cudaError_t launch_plan_check(const int64_t* offsets, int64_t rows, const int32_t* ids, int n_windows, int* flag,
+                              cudaStream_t st);
 
 }  // namespace gsa_sm100

@@ -52,18 +52,29 @@ __global__ void forced_kernel(DevLayout L, int ref_stride, int32_t* forced, uint
     }
 }
 
+// flag bit 2: a top-k id outside [0, W) (the reference would index its forced mask /
+// tokens_of_window with it: IndexOutOfRange, layout.cpp:37-56); such ids are counted as
+// dynamic so the plan stays well-formed, and the caller reports the error
 __global__ void plan_count_kernel(const int32_t* __restrict__ topk, int64_t rows, int k,
-                                  const uint8_t* __restrict__ mask, int n_forced, int64_t* sizes) {
+                                  const uint8_t* __restrict__ mask, int n_forced, int W, int64_t* sizes,
+                                  int* flag) {
     const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= rows) return;
     int n = 0;
-    for (int j = 0; j < k; ++j) n += (mask && mask[topk[r * k + j]]) ? 0 : 1;
+    bool bad = false;
+    for (int j = 0; j < k; ++j) {
+        const int32_t w = topk[r * k + j];
+        const bool ok = w >= 0 && w < W;
+        bad |= !ok;
+        n += (ok && mask && mask[w]) ? 0 : 1;
+    }
+    if (bad && flag) atomicOr(flag, 2);
     sizes[r] = n + (mask ? n_forced : 0);
 }
 
 __global__ void plan_fill_kernel(const int32_t* __restrict__ topk, int64_t rows, int k,
                                  const uint8_t* __restrict__ mask, const int32_t* __restrict__ forced,
-                                 int n_forced, const int64_t* __restrict__ offsets, int32_t* ids) {
+                                 int n_forced, int n_windows, const int64_t* __restrict__ offsets, int32_t* ids) {
     const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= rows) return;
     int64_t o = offsets[r];
@@ -71,13 +82,22 @@ __global__ void plan_fill_kernel(const int32_t* __restrict__ topk, int64_t rows,
         for (int i = 0; i < n_forced; ++i) ids[o++] = forced[i];
     for (int j = 0; j < k; ++j) {
         const int32_t w = topk[r * k + j];
-        if (!(mask && mask[w])) ids[o++] = w;
+        if (!(mask && w >= 0 && w < n_windows && mask[w])) ids[o++] = w;
     }
 }
 
-__global__ void empty_row_kernel(const int64_t* __restrict__ offsets, int64_t rows, int* flag) {
+// plan validation (block_sparse_attention, selection.hpp:82-85 + tokens_of_window's range
+// check): flag bit 1 = an empty (or negative-size) row, bit 2 = a window id outside [0, W)
+__global__ void plan_check_kernel(const int64_t* __restrict__ offsets, int64_t rows, const int32_t* __restrict__ ids,
+                                  int W, int* flag) {
     const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (r < rows && offsets[r + 1] <= offsets[r]) atomicOr(flag, 1);
+    if (r >= rows) return;
+    const int64_t a = offsets[r], b = offsets[r + 1];
+    if (b <= a) atomicOr(flag, 1);
+    if (!ids) return;
+    bool bad = a < 0;
+    for (int64_t i = a; i < b && !bad; ++i) bad = ids[i] < 0 || ids[i] >= W;
+    if (bad) atomicOr(flag, 2);
 }
 
 __global__ void set_zero_kernel(int64_t* p) { *p = 0; }
@@ -114,17 +134,17 @@ cudaError_t launch_forced(const DevLayout& L, int ref_stride, int32_t* forced, u
 }
 
 cudaError_t launch_plan_count(const int32_t* topk, int64_t rows, int k, const uint8_t* mask,
-                              int n_forced, int64_t* sizes, cudaStream_t st) {
+                              int n_forced, int n_windows, int64_t* sizes, int* flag, cudaStream_t st) {
     if (rows == 0) return cudaSuccess;
-    { plan_count_kernel<<<(unsigned)((rows + 255) / 256), 256, 0, st>>>(topk, rows, k, mask, n_forced, sizes); note_launch(); }
+    { plan_count_kernel<<<(unsigned)((rows + 255) / 256), 256, 0, st>>>(topk, rows, k, mask, n_forced, n_windows, sizes, flag); note_launch(); }
     return cudaGetLastError();
 }
 
 cudaError_t launch_plan_fill(const int32_t* topk, int64_t rows, int k, const uint8_t* mask,
-                             const int32_t* forced, int n_forced, const int64_t* offsets,
+                             const int32_t* forced, int n_forced, int n_windows, const int64_t* offsets,
                              int32_t* ids, cudaStream_t st) {
     if (rows == 0) return cudaSuccess;
-    { plan_fill_kernel<<<(unsigned)((rows + 255) / 256), 256, 0, st>>>(topk, rows, k, mask, forced, n_forced, offsets, ids); note_launch(); }
+    { plan_fill_kernel<<<(unsigned)((rows + 255) / 256), 256, 0, st>>>(topk, rows, k, mask, forced, n_forced, n_windows, offsets, ids); note_launch(); }
     return cudaGetLastError();
 }
 
@@ -142,9 +162,10 @@ cudaError_t launch_scan_offsets(const int64_t* sizes, int64_t n, int64_t* offset
     return cub::DeviceScan::InclusiveSum(tmp, tmp_bytes, sizes, offsets + 1, (int)n, st);
 }
 
-cudaError_t launch_empty_row_check(const int64_t* offsets, int64_t rows, int* flag, cudaStream_t st) {
+cudaError_t launch_plan_check(const int64_t* offsets, int64_t rows, const int32_t* ids, int n_windows, int* flag,
+                              cudaStream_t st) {
     if (rows == 0) return cudaSuccess;
-    { empty_row_kernel<<<(unsigned)((rows + 255) / 256), 256, 0, st>>>(offsets, rows, flag); note_launch(); }
+    { plan_check_kernel<<<(unsigned)((rows + 255) / 256), 256, 0, st>>>(offsets, rows, ids, n_windows, flag); note_launch(); }
     return cudaGetLastError();
 }
 

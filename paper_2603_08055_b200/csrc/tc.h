@@ -38,7 +38,7 @@ cudaError_t tc_compress_topk(const gsa_tensor& qc, const gsa_tensor& kc, const g
                              size_t ws_bytes, cudaStream_t st);
 
 // selection branch + gate + merge
-bool tc_select_supported(const gsa_tensor& q, const DevLayout& L, const RowSource& rows);
+bool tc_select_supported(const SelectArgs& a);
 size_t tc_select_workspace_bytes(int heads);
 cudaError_t tc_select_gate_merge(const SelectArgs& a, cudaStream_t st);
 

@@ -47,9 +47,11 @@ __device__ __forceinline__ uint64_t globaltimer_ns() {
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
     return t;
 }
-// Blocking wait with a watchdog: a pipeline bug traps (kernel error) after ~20 s
-// instead of hanging the GPU.
+// Blocking wait. Bring-up builds (-DGSA_WATCHDOG) add a watchdog: a pipeline bug
+// traps (kernel error) after ~10 s instead of hanging the GPU. Shipped builds spin on
+// try_wait only (the watchdog's timer check cost ~1% of K2's issue slots).
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+#ifdef GSA_WATCHDOG
     if (mbar_try_wait(bar, parity)) return;
     const uint64_t t0 = globaltimer_ns();
     uint32_t n = 0;
@@ -65,6 +67,10 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
             if (dt > 10000000000ull) __trap();
         }
     }
+#else
+    while (!mbar_try_wait(bar, parity)) {
+    }
+#endif
 }
 
 // ----------------------------------------------------------------------- TMA

@@ -365,18 +365,35 @@ class ForwardContext:
 
 
 class Workspace:
-    """Caller-owned scratch for gsa_forward (grown on demand, reused across calls)."""
+    """Caller-owned scratch for gsa_forward (grown on demand, reused across calls).
+
+    A workspace is stream-ordered like the calls that use it: share one only
+    between calls on the same CUDA stream (the default workspaces are per
+    (device, stream)). A buffer that is replaced while a call on another stream
+    may still read it is kept alive for that stream (record_stream)."""
 
     def __init__(self):
         self.buf: Optional[torch.Tensor] = None
 
     def get(self, nbytes: int, device) -> torch.Tensor:
         if self.buf is None or self.buf.numel() < nbytes or self.buf.device != torch.device(device):
+            if self.buf is not None and self.buf.is_cuda:
+                self.buf.record_stream(torch.cuda.current_stream(self.buf.device))
             self.buf = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=device)
         return self.buf
 
 
-_default_ws = Workspace()
+_default_ws: dict = {}
+
+
+def _default_workspace(device) -> Workspace:
+    """The implicit workspace of calls without one: one per (device, current stream)."""
+    dev = torch.device(device)
+    key = (dev.index, torch.cuda.current_stream(dev).cuda_stream)
+    ws = _default_ws.get(key)
+    if ws is None:
+        ws = _default_ws[key] = Workspace()
+    return ws
 
 
 def gsa_forward(q, k, v, w_g, layout: TokenLayout, params: GsaParams, context: bool = False,
@@ -390,7 +407,7 @@ def gsa_forward(q, k, v, w_g, layout: TokenLayout, params: GsaParams, context: b
         out = _empty(H, M, d, device=dev)
     lc, pc = layout.c(), params.c()
     ws_bytes = L.gsa_forward_workspace_bytes(C.byref(lc), C.byref(pc), H, d)
-    ws = (workspace or _default_ws).get(ws_bytes, dev)
+    ws = (workspace or _default_workspace(dev)).get(ws_bytes, dev)
     ctx = None
     cstruct = None
     if context:
@@ -427,7 +444,7 @@ def gsa_forward_with_plan(q, k, v, w_g, layout: TokenLayout, params: GsaParams, 
     out = _empty(H, M, d, device=q.device)
     lc, pc = layout.c(), params.c()
     ws_bytes = L.gsa_forward_workspace_bytes(C.byref(lc), C.byref(pc), H, d)
-    ws = (workspace or _default_ws).get(ws_bytes, q.device)
+    ws = (workspace or _default_workspace(q.device)).get(ws_bytes, q.device)
     _check(L.gsa_forward_with_plan(C.byref(_desc(q)), C.byref(_desc(k)), C.byref(_desc(v)),
                                    C.byref(_desc(w_g.contiguous())), C.byref(lc), C.byref(pc), _ptr(plan.offsets),
                                    _ptr(plan.window_ids), C.byref(_desc(out)), _ptr(ws), ws.numel(), _stream()))

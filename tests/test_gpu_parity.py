@@ -505,3 +505,35 @@ def test_clustered_views_bitexact(gsa, ref):
     np.testing.assert_array_equal(ctx.topk.cpu().numpy(), rf["topk"])
     o = host(out)
     assert np.abs(o - rf["out"]).max() < 1e-4 and rel_l2(o, rf["out"]) < 1e-5
+
+
+def test_plan_validation_errors(gsa):
+    """Caller-supplied plans are validated before any compute: a window id
+    outside [0, W) is IndexOutOfRange (the reference's tokens_of_window check,
+    layout.cpp:37-56), an empty row EmptySelection (selection.hpp:82-85) -- for
+    block_sparse_attention and gsa_forward_with_plan alike -- and build_selection_plan
+    rejects out-of-range top-k ids."""
+    lt = (0, 1, 8, 8, 4)
+    gl = gsa.build_token_layout(*lt)
+    x = torch.zeros(1, 64, 64, dtype=torch.bfloat16, device="cuda")
+    wg = torch.zeros(1, 64, 64, device="cuda")
+    offs = torch.tensor([0, 1, 2, 3, 4], dtype=torch.int64, device="cuda")
+    none = torch.empty(0, dtype=torch.int32, device="cuda")
+    for bad_id in (4, -1, 1 << 20):
+        ids = torch.tensor([0, 1, bad_id, 3], dtype=torch.int32, device="cuda")
+        plan = gsa.SelectionPlan(1, 4, offs, ids, none)
+        with pytest.raises(gsa.IndexOutOfRange):
+            gsa.block_sparse_attention(x, x, x, plan, gl, 0.125)
+        with pytest.raises(gsa.IndexOutOfRange):
+            gsa.gsa_forward_with_plan(x, x, x, wg, gl, gsa.GsaParams(window_s=4, top_k=1), plan)
+    empty = gsa.SelectionPlan(1, 4, torch.tensor([0, 1, 1, 2, 3], dtype=torch.int64, device="cuda"),
+                              torch.tensor([0, 1, 2], dtype=torch.int32, device="cuda"), none)
+    with pytest.raises(gsa.EmptySelection):
+        gsa.gsa_forward_with_plan(x, x, x, wg, gl, gsa.GsaParams(window_s=4, top_k=1), empty)
+    with pytest.raises(gsa.IndexOutOfRange):
+        gsa.build_selection_plan(torch.tensor([[[0], [1], [9], [3]]], dtype=torch.int32, device="cuda"), gl, 1, 1)
+    # the reference's with_plan path runs no top-k and does not compare params.window_s
+    # with the layout: a budget beyond the selectable windows and a stale window_s pass
+    good = gsa.SelectionPlan(1, 4, offs, torch.tensor([3, 2, 1, 0], dtype=torch.int32, device="cuda"), none)
+    out = gsa.gsa_forward_with_plan(x, x, x, wg, gl, gsa.GsaParams(window_s=2, top_k=5000), good)
+    assert torch.isfinite(out).all()

@@ -137,3 +137,35 @@ def test_oracle_matches_reference_random(orc, ref, seed):
 def test_reference_errors_mirrored(ref):
     assert ref.build_layout(0, 1, 5, 5, 4)[0] == -3  # DivisibilityError
     assert ref.build_layout(0, 0, 4, 4, 4)[0] == -4  # ZeroSizeError
+
+
+@pytest.mark.parametrize("variant,specials", [(0, 5), (1, 0)])
+def test_sampled_checker_matches_full_reference_layer(orc, ref, variant, specials):
+    """The sampled-row checker (oracle/sampled.py -> gsa_ref_sampled_head) must reproduce the
+    full reference fused layer (gsa_ref_forward) on the rows it samples: top-k bit-exact and
+    outputs to float rounding. This pins the checker used at V >= 100 (tests/test_scale_parity.py,
+    bench.py's post-timing parity) against the reference run in full."""
+    torch = pytest.importorskip("torch")
+    from oracle import Layout
+    from oracle.sampled import sampled_parity
+    lt = (specials * 6, 6, 16, 16, 4)
+    L = Layout(*lt)
+    q, k, v, wg = make_inputs(orc, L, heads=3, dim=64, seed=17)
+    rf = ref.forward(q, k, v, wg, lt, top_k=9, variant=variant, ref_stride=4)
+    T = lambda a: torch.from_numpy(np.ascontiguousarray(a))  # noqa: E731  (CPU tensors stand in for device ones)
+    res = sampled_parity(T(q), T(k), T(v), T(wg), lt, 9, T(rf["out"]), T(rf["topk"]), variant=variant, ref_stride=4,
+                         o_comp=T(rf["o_comp"]), lse_comp=T(rf["lse_comp"]), o_sel=T(rf["o_sel"]),
+                         lse_sel=T(rf["lse_sel"]), frac=0.25, spec_frac=0.5, threads=4)
+    assert res["rows_checked"] == 3 * int(np.ceil(0.25 * L.num_windows))
+    assert res["topk_mismatches"] == 0
+    assert res["rel_l2"] < 1e-6 and res["max_abs"] < 1e-6
+    assert res["o_comp_rel_l2"] < 1e-5 and res["lse_comp_max_abs"] < 1e-5
+    assert res["o_sel_rel_l2"] < 1e-6 and res["lse_sel_max_abs"] < 1e-6
+    if specials:
+        assert res["special_rows_checked"] > 0 and res["special_rel_l2"] < 1e-6
+    # a corrupted GPU row is caught
+    bad = rf["topk"].copy()
+    bad[1, 5, [0, 1]] = bad[1, 5, [1, 0]]
+    res2 = sampled_parity(T(q), T(k), T(v), T(wg), lt, 9, T(rf["out"]), T(bad), variant=variant, ref_stride=4,
+                          frac=1.0, threads=4)
+    assert res2["topk_mismatches"] == 1
