@@ -385,6 +385,19 @@ class RefLib:
                                                   self._p(out), self._p(lse)))
         return out, lse
 
+    def masked_attention(self, q_img, k_img, v_img, lt, offsets, ids, scale):
+        """masked_image_attention (reference.hpp:120-170) -> (out, denominators f64)."""
+        q_img, k_img, v_img = f32(q_img), f32(k_img), f32(v_img)
+        H, Mi, d = q_img.shape
+        offsets = np.ascontiguousarray(offsets, np.int64)
+        ids = np.ascontiguousarray(ids, np.int32)
+        out = np.empty((H, Mi, d), np.float32)
+        den = np.empty((H, Mi), np.float64)
+        self._check(self.lib.gsa_ref_masked_attention(self._p(q_img), self._p(k_img), self._p(v_img), C.c_int(H),
+                                                      C.c_int(d), *[C.c_int(x) for x in lt], self._p(offsets),
+                                                      self._p(ids), C.c_float(scale), self._p(out), self._p(den)))
+        return out, den
+
     def tiled_attention(self, q, k, v, scale, bm=16, bn=16, threads=8):
         q, k, v = f32(q), f32(k), f32(v)
         H, mq, d = q.shape

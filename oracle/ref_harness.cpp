@@ -230,6 +230,27 @@ int gsa_ref_block_sparse(const float* q_img, const float* k_img, const float* v_
     });
 }
 
+// masked_image_attention (reference.hpp:120-170): the -inf-masked dense selection oracle,
+// with the per-query denominators sum_j exp(score_j) (SPEC.md:576 gather/mask equivalence).
+int gsa_ref_masked_attention(const float* q_img, const float* k_img, const float* v_img, int heads, int dim,
+                             int ns, int nf, int gh, int gw, int s, const int64_t* offsets, const int32_t* ids,
+                             float scale, float* out, double* denominators) {
+    return guarded([&] {
+        auto l = gsa::build_token_layout(ns, nf, gh, gw, s);
+        gsa::SelectionPlan p;
+        p.heads = heads;
+        p.rows = l.num_windows();
+        const size_t nr = static_cast<size_t>(heads) * p.rows;
+        p.offsets.assign(offsets, offsets + nr + 1);
+        p.window_ids.assign(ids, ids + offsets[nr]);
+        const int mi = l.image_tokens();
+        auto r = gsa::masked_image_attention(to_tensor(q_img, heads, mi, dim), to_tensor(k_img, heads, mi, dim),
+                                             to_tensor(v_img, heads, mi, dim), p, l, scale);
+        from_tensor(r.out, out);
+        if (denominators) std::copy(r.denominators.begin(), r.denominators.end(), denominators);
+    });
+}
+
 int gsa_ref_tiled_attention(const float* q, const float* k, const float* v, int heads, int mq,
                             int mk, int dim, float scale, int bm, int bn, int threads, float* out,
                             float* lse) {

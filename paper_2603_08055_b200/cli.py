@@ -1,0 +1,242 @@
+"""Benchmark / verification CLI of the GSA layer on the B200 (the reference's
+bench_cli module, which the reference specifies but never
+implements). Times dense vs GSA layers across frame counts on the GPU, fits the
+scaling exponents and writes SPEC's CSV schema:
+
+    mode,frames,image_tokens,window_s,top_k,variant,repeats,median_s,mean_s,stddev_s
+
+    python -m paper_2603_08055_b200.cli --mode gsa --frames 8,16,32,64 --grid 36x36 \
+        --topk 32 --repeats 5 --csv out.csv [--verify all]
+
+Modes: dense (tiled_attention over all M tokens), gsa (gsa_forward),
+compress-only (pooling + fused compressed attention / top-k), select-only
+(block_sparse_attention over the layer's own plan). Timings are CUDA events on
+the launching stream after >= 1 warm-up per size; the workload of each size is
+seeded by seed' = hash(seed, frames). --precision f32|bf16 (f64 is
+rejected: there is no f64 path on the tensor cores). --threads and GSA_THREADS are
+accepted and ignored (the kernels are grids, results do not depend on them).
+--backward is out of scope (the layer is inference-only).
+
+--verify runs the self-contained identities of SPEC.md:545-549 on the GPU path:
+dense degeneration (s=1, k=W, no specials == dense attention), tiling invariance
+and scale invariance of the top-k indices, the closed-form work counters. The
+reference-equivalence suites (fused vs the unmodified reference) are the test
+suite's job (tests/test_spec_properties.py): this tool never links the oracle.
+"""
+from __future__ import annotations
+
+import argparse
+import csv
+import hashlib
+import math
+import os
+import statistics
+import sys
+
+CSV_COLUMNS = ["mode", "frames", "image_tokens", "window_s", "top_k", "variant", "repeats", "median_s", "mean_s",
+               "stddev_s"]
+
+
+class DegenerateInput(ValueError):
+    pass
+
+
+def fit_scaling_exponent(points):
+    """Least-squares slope of log(seconds) on log(tokens)."""
+    pts = list(points)
+    if len(pts) < 3:
+        raise DegenerateInput("fit_scaling_exponent: need >= 3 points")
+    xs, ys = [], []
+    prev = None
+    for n, t in pts:
+        if n <= 0 or t <= 0:
+            raise DegenerateInput("fit_scaling_exponent: tokens and times must be positive")
+        if prev is not None and n <= prev:
+            raise DegenerateInput("fit_scaling_exponent: token counts must increase strictly")
+        prev = n
+        xs.append(math.log(n))
+        ys.append(math.log(t))
+    mx, my = sum(xs) / len(xs), sum(ys) / len(ys)
+    sxx = sum((x - mx) ** 2 for x in xs)
+    return sum((x - mx) * (y - my) for x, y in zip(xs, ys)) / sxx
+
+
+def size_seed(seed: int, frames: int) -> int:
+    """seed' = hash(seed, size), stable across runs and machines."""
+    h = hashlib.sha256(f"{seed}:{frames}".encode()).digest()
+    return int.from_bytes(h[:8], "little") & ((1 << 63) - 1)
+
+
+def _inputs(torch, lt, heads, dim, dtype, seed):
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    M = lt[0] + lt[1] * lt[2] * lt[3]
+    q, k, v = (torch.randn(heads, M, dim, generator=g, device="cuda").to(dtype) for _ in range(3))
+    wg = torch.randn(heads, dim, dim, generator=g, device="cuda") / math.sqrt(dim)
+    return q, k, v, wg
+
+
+def _time(torch, fn, repeats):
+    fn()
+    torch.cuda.synchronize()
+    out = []
+    for _ in range(repeats):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        fn()
+        b.record()
+        torch.cuda.synchronize()
+        out.append(a.elapsed_time(b) / 1e3)
+    return out
+
+
+def run_benchmark(mode, frames_list, grid, s, k, variant, ref_stride, heads, dim, precision, seed, repeats,
+                  specials_per_frame=0):
+    """One row per frame count; an out-of-memory size is a row with
+    empty timing columns, not a crash."""
+    import torch
+
+    import paper_2603_08055_b200 as gsa
+    if repeats < 3:
+        raise ValueError("repeats must be >= 3 (SPEC.md:504)")
+    dtype = {"f32": torch.float32, "bf16": torch.bfloat16}.get(precision)
+    if dtype is None:
+        raise gsa.Unsupported(f"precision {precision}: the sm_100a path computes in bf16 or f32")
+    rows = []
+    for nf in frames_list:
+        lt = (specials_per_frame * nf, nf, grid[0], grid[1], s)
+        L = gsa.build_token_layout(*lt)
+        p = gsa.GsaParams(window_s=s, top_k=k, variant=variant, ref_stride=ref_stride)
+        row = {"mode": mode, "frames": nf, "image_tokens": L.image_tokens, "window_s": s, "top_k": k,
+               "variant": "hybrid" if variant else "plain", "repeats": repeats}
+        try:
+            q, kk, v, wg = _inputs(torch, lt, heads, dim, dtype, size_seed(seed, nf))
+            scale = gsa.resolved_scale(p, dim)
+            if mode == "dense":
+                fn = lambda: gsa.tiled_attention(q, kk, v, scale)  # noqa: E731
+            elif mode == "gsa":
+                fn = lambda: gsa.gsa_forward(q, kk, v, wg, L, p)  # noqa: E731
+            elif mode == "compress-only":
+                ms = lt[0]
+
+                def fn():
+                    qc, kc, vc = (gsa.avg_pool_tokens(t[:, ms:], L) for t in (q, kk, v))
+                    ex = None
+                    if variant:
+                        ex = torch.zeros(L.num_windows, dtype=torch.uint8, device="cuda")
+                        ex[gsa.forced_windows_of(L, ref_stride).long()] = 1
+                    gsa.fused_compressed_attention_topk(qc, kc, vc, k, scale, excluded=ex)
+            elif mode == "select-only":
+                _, ctx = gsa.gsa_forward(q, kk, v, wg, L, p, context=True)
+                plan = gsa.build_selection_plan(ctx.topk, L, variant, ref_stride)
+                ms = lt[0]
+                fn = lambda: gsa.block_sparse_attention(q[:, ms:], kk[:, ms:], v[:, ms:], plan, L, scale)  # noqa: E731
+            else:
+                raise ValueError(f"unknown mode {mode}")
+            ts = _time(torch, fn, repeats)
+            row.update(median_s=statistics.median(ts), mean_s=statistics.mean(ts),
+                       stddev_s=statistics.stdev(ts) if len(ts) > 1 else 0.0)
+        except torch.cuda.OutOfMemoryError:
+            row.update(median_s="", mean_s="", stddev_s="")
+            torch.cuda.empty_cache()
+        rows.append(row)
+    return rows
+
+
+def run_verification(suite, seed, heads=2, dim=64):
+    """GPU-path identities: returns [(name, ok, worst)]."""
+    import torch
+
+    import paper_2603_08055_b200 as gsa
+    results = []
+    if suite in ("oracle", "all"):
+        worst = 0.0
+        for i in range(8):
+            nf = 1 + i % 3
+            lt = (0, nf, 8, 4 + 4 * (i % 3), 1)
+            L = gsa.build_token_layout(*lt)
+            q, k, v, wg = _inputs(torch, lt, heads, dim, torch.float32, size_seed(seed, 100 + i))
+            out = gsa.gsa_forward(q, k, v, wg, L, gsa.GsaParams(window_s=1, top_k=L.num_windows))
+            dense, _ = gsa.tiled_attention(q, k, v, 1.0 / math.sqrt(dim))
+            worst = max(worst, float((out - dense).abs().max()))
+        results.append(("dense_degeneration", worst <= 1e-4, worst))
+    if suite in ("topk", "all"):
+        lt = (10, 6, 16, 16, 4)
+        L = gsa.build_token_layout(*lt)
+        q, k, v, wg = _inputs(torch, lt, heads, dim, torch.bfloat16, size_seed(seed, 7))
+        _, c0 = gsa.gsa_forward(q, k, v, wg, L, gsa.GsaParams(top_k=12), context=True)
+        mism = 0
+        for bm, bn in ((8, 8), (16, 64), (64, 32)):
+            _, c1 = gsa.gsa_forward(q, k, v, wg, L, gsa.GsaParams(top_k=12, tiling=gsa.KernelTiling(bm, bn)),
+                                    context=True)
+            mism += int((c1.topk != c0.topk).any(-1).sum())
+        _, c2 = gsa.gsa_forward(q, k, v, wg, L, gsa.GsaParams(top_k=12, scale=0.37), context=True)
+        mism += int((c2.topk != c0.topk).any(-1).sum())
+        results.append(("topk_tiling_and_scale_invariance", mism == 0, mism))
+        sc, ka = gsa.forward_stats(L, gsa.GsaParams(top_k=12), heads)
+        W, M = L.num_windows, L.total_tokens
+        ok = sc == heads * (lt[0] * M + W * W) and ka == heads * W * 12 * 16 * 16
+        results.append(("work_counters_closed_form", ok, 0))
+    return results
+
+
+def main(argv=None):
+    ap = argparse.ArgumentParser(description=__doc__.split("\n\n")[0])
+    ap.add_argument("--config", help="key=value file (frames, grid, window, topk, variant, ref_stride, heads, dim, "
+                                     "precision, seed, repeats)")
+    ap.add_argument("--mode", default="gsa", choices=["dense", "gsa", "compress-only", "select-only"])
+    ap.add_argument("--frames", default="8,16,32,64")
+    ap.add_argument("--grid", default="36x36")
+    ap.add_argument("--window", type=int, default=4)
+    ap.add_argument("--topk", type=int, default=32)
+    ap.add_argument("--variant", default="plain", choices=["plain", "hybrid"])
+    ap.add_argument("--ref-stride", type=int, default=100)
+    ap.add_argument("--heads", type=int, default=16)
+    ap.add_argument("--dim", type=int, default=64)
+    ap.add_argument("--specials-per-frame", type=int, default=0)
+    ap.add_argument("--precision", default="bf16", choices=["f32", "bf16", "f64"])
+    ap.add_argument("--seed", type=int, default=7)
+    ap.add_argument("--repeats", type=int, default=5)
+    ap.add_argument("--threads", type=int, default=int(os.environ.get("GSA_THREADS", "1")))
+    ap.add_argument("--csv")
+    ap.add_argument("--verify", choices=["oracle", "topk", "all"])
+    ap.add_argument("--backward", action="store_true")
+    a = ap.parse_args(argv)
+    if a.config:
+        for line in open(a.config):
+            line = line.split("#")[0].strip()
+            if not line:
+                continue
+            if "=" not in line:
+                raise SystemExit(f"ConfigParseError: {line!r}")
+            key, val = (x.strip() for x in line.split("=", 1))
+            attr = key.replace("-", "_")
+            if not hasattr(a, attr):
+                raise SystemExit(f"ConfigParseError: unknown key {key!r}")
+            cur = getattr(a, attr)
+            setattr(a, attr, type(cur)(val) if cur is not None and not isinstance(cur, bool) else val)
+    if a.backward:
+        raise SystemExit("--backward: the sm_100a layer is inference-only (DESIGN.md §8)")
+    if a.verify:
+        ok_all = True
+        for name, ok, worst in run_verification(a.verify, a.seed):
+            print(f"CHECK {name} {'PASS' if ok else 'FAIL'} worst={worst}")
+            ok_all &= ok
+        return 0 if ok_all else 1
+    gh, gw = (int(x) for x in a.grid.split("x"))
+    frames = [int(x) for x in a.frames.split(",") if x]
+    rows = run_benchmark(a.mode, frames, (gh, gw), a.window, a.topk, 1 if a.variant == "hybrid" else 0,
+                         a.ref_stride, a.heads, a.dim, a.precision, a.seed, a.repeats, a.specials_per_frame)
+    out = open(a.csv, "w", newline="") if a.csv else sys.stdout
+    w = csv.DictWriter(out, fieldnames=CSV_COLUMNS)
+    w.writeheader()
+    for r in rows:
+        w.writerow(r)
+    pts = [(r["image_tokens"], r["median_s"]) for r in rows if r["median_s"] != ""]
+    if len(pts) >= 3:
+        print(f"# fitted exponent ({a.mode}): {fit_scaling_exponent(pts[-3:]):.3f} over the top three sizes",
+              file=sys.stderr)
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -385,7 +385,7 @@ int gsa_build_selection_plan(const int32_t* topk, int heads, int rows, int k, co
 // reference's tokens_of_window check, layout.cpp:37-56).
 static int validate_plan(const int64_t* offsets, const int32_t* ids, int64_t rows, int W, const char* who,
                          cudaStream_t st) {
-    if (!offsets || !ids) return fail(GSA_ERR_GENERIC, "%s: null plan", who);
+    if (!offsets) return fail(GSA_ERR_GENERIC, "%s: null plan offsets", who);
     int* flag = nullptr;
     GSA_CUDA(cudaMallocAsync(&flag, sizeof(int), st));
     GSA_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), st));
@@ -395,6 +395,7 @@ static int validate_plan(const int64_t* offsets, const int32_t* ids, int64_t row
     GSA_CUDA(cudaFreeAsync(flag, st));
     GSA_CUDA(cudaStreamSynchronize(st));
     if (h & 1) return fail(GSA_ERR_EMPTY_SELECTION, "%s: empty plan row", who);
+    if (h & 4) return fail(GSA_ERR_GENERIC, "%s: null plan window ids", who);
     if (h & 2) return fail(GSA_ERR_INDEX_OUT_OF_RANGE, "%s: plan window id outside [0, %d)", who, W);
     return GSA_OK;
 }

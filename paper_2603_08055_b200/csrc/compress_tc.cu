@@ -799,7 +799,7 @@ __global__ void __launch_bounds__(256) rescore_kernel(const float* __restrict__ 
     }
     __syncwarp();
     if (total > SV) {
-        if (lane == 0) flag[r] = 1;  // near-tie flood: the exact per-row kernel redoes this row
+        if (lane == 0) flag[r] = 2;  // near-tie flood: the exact per-row kernel redoes this row
         return;
     }
     float e[SLOTS];
@@ -1660,15 +1660,19 @@ cudaError_t tc_compress_topk_splits(const CompressSplits* pre, const gsa_tensor&
             cudaMemcpyAsync(fl.data(), w.flag, rows, cudaMemcpyDeviceToHost, st);
             cudaMemcpyAsync(&nblk, w.nblocks, 4, cudaMemcpyDeviceToHost, st);
             cudaStreamSynchronize(st);
-            int64_t sum = 0, mx = 0, nfl = 0, nzero = 0;
+            int64_t sum = 0, mx = 0, nfl = 0, nzero = 0, nover = 0, nflood = 0;
             for (int64_t i = 0; i < rows; ++i) {
                 sum += cn[i];
                 mx = cn[i] > mx ? cn[i] : mx;
                 nfl += fl[i] ? 1 : 0;
+                nover += fl[i] == 1 ? 1 : 0;
+                nflood += fl[i] == 2 ? 1 : 0;
                 nzero += cn[i] == 0 ? 1 : 0;
             }
-            fprintf(stderr, "compress stats: rows %lld mean cand %.1f max %lld flagged %lld zero %lld blocks %d\n",
-                    (long long)rows, (double)sum / rows, (long long)mx, (long long)nfl, (long long)nzero, nblk);
+            fprintf(stderr, "compress stats: rows %lld mean cand %.1f max %lld flagged %lld (list overflow %lld, "
+                    "survivor flood %lld) zero %lld blocks %d\n",
+                    (long long)rows, (double)sum / rows, (long long)mx, (long long)nfl, (long long)nover,
+                    (long long)nflood, (long long)nzero, nblk);
             int shown = 0;
             for (int64_t i = 0; i < rows && shown < 8; ++i)
                 if (fl[i]) {

@@ -94,7 +94,10 @@ __global__ void plan_check_kernel(const int64_t* __restrict__ offsets, int64_t r
     if (r >= rows) return;
     const int64_t a = offsets[r], b = offsets[r + 1];
     if (b <= a) atomicOr(flag, 1);
-    if (!ids) return;
+    if (!ids) {
+        if (b > a) atomicOr(flag, 4);  // non-empty rows but no id array
+        return;
+    }
     bool bad = a < 0;
     for (int64_t i = a; i < b && !bad; ++i) bad = ids[i] < 0 || ids[i] >= W;
     if (bad) atomicOr(flag, 2);

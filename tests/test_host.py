@@ -1,6 +1,8 @@
 """Host-side pieces of the C ABI that need no GPU."""
 from __future__ import annotations
 
+import pytest
+
 
 def test_selection_sparsity_spec_examples():
     """selection_sparsity (declared, never defined, in the reference's
@@ -21,3 +23,30 @@ def test_selection_sparsity_spec_examples():
         a = gsa.selection_sparsity(gsa.build_token_layout(0, frames, 36, 36, 4), gsa.GsaParams(window_s=4, top_k=32))
         b = gsa.selection_sparsity(gsa.build_token_layout(0, frames * 2, 36, 36, 4), gsa.GsaParams(window_s=4, top_k=32))
         assert b >= a
+
+
+def test_bench_cli_exponent_fit_and_seeds():
+    """SPEC.md:522-529 known answers of fit_scaling_exponent; seed' = hash(seed, size) is
+    stable and size-dependent (SPEC.md:509)."""
+    from paper_2603_08055_b200.cli import DegenerateInput, fit_scaling_exponent, size_seed
+    ns = [1000, 2000, 4000, 8000]
+    assert abs(fit_scaling_exponent([(n, 3e-9 * n * n) for n in ns]) - 2.0) < 1e-9
+    assert abs(fit_scaling_exponent([(n, 5e-6 * n) for n in ns]) - 1.0) < 1e-9
+    for bad in ([(1, 1.0), (2, 2.0)], [(1, 1.0), (2, 2.0), (2, 3.0)], [(1, 1.0), (2, -2.0), (3, 3.0)]):
+        with pytest.raises(DegenerateInput):
+            fit_scaling_exponent(bad)
+    assert size_seed(7, 8) == size_seed(7, 8) and size_seed(7, 8) != size_seed(7, 16) != size_seed(8, 16)
+
+
+def test_bench_cli_csv_schema_and_flags(tmp_path):
+    """The CSV header is SPEC's exact column order; f64 / --backward are
+    rejected loudly rather than silently downgraded."""
+    from paper_2603_08055_b200 import cli
+    assert cli.CSV_COLUMNS == ["mode", "frames", "image_tokens", "window_s", "top_k", "variant", "repeats",
+                               "median_s", "mean_s", "stddev_s"]
+    with pytest.raises(SystemExit):
+        cli.main(["--backward"])
+    cfg = tmp_path / "c.cfg"
+    cfg.write_text("bogus_key = 3\n")
+    with pytest.raises(SystemExit):
+        cli.main(["--config", str(cfg)])
