@@ -308,6 +308,11 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1 or args.shard:
+        # communicator set-up lines (ranks, NVLS/P2P transport) on stderr: the scaling
+        # record can be checked against them
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -331,7 +336,9 @@ def main():
         spec = gdist.shard_spec(L, rank, world)
         q_own = gdist.own_rows_of(q, L, spec).contiguous()
         out_own = torch.empty(HEADS, spec.own_rows(L), DIM, device=dev)
-        layer = gdist.ShardedLayer(L, params, HEADS, DIM, rank, world, device=dev)
+        # the C-level sharded layer: NCCL communicator + gsa_shard_forward (the K/V-row
+        # all-gather overlaps the compressed branch on the communicator's stream)
+        layer = gdist.NcclShardedLayer(L, params, HEADS, DIM, rank, world, device=dev)
 
         def step_fn():
             layer.forward(q_own, k, v, wg, out_own)
@@ -339,16 +346,15 @@ def main():
         def step_fn():
             gsa.gsa_forward(q, k, v, wg, L, params, out=out, workspace=ws)
 
-    # stage events on the launching stream: the library records them inside
-    # gsa_forward (special | pool | compress | select); the sharded layer
-    # records pool | compress (incl. the Kc/Vc gather wait) | attend
+    # stage events on the launching stream, recorded by the library inside gsa_forward
+    # (special | pool | compress | select) or gsa_shard_forward (pool | Kc/Vc gather wait |
+    # compress | attend)
     import ctypes
-    nev = 4 if sharded else 5
-    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(nev)] for _ in range(args.steps)]
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(args.steps)]
     for row in ev:
         for e_ in row:
             e_.record()  # materialise the cudaEvent_t handles
-    handles = [(ctypes.c_void_p * 5)(*[e_.cuda_event for e_ in row]) for row in ev] if not sharded else None
+    handles = [(ctypes.c_void_p * 5)(*[e_.cuda_event for e_ in row]) for row in ev]
     for _ in range(args.warmup):
         step_fn()
     torch.cuda.synchronize()
@@ -362,18 +368,12 @@ def main():
     with ClockSampler(local) as clocks:
         start.record()
         for i in range(args.steps):
-            if not sharded:
-                lib.gsa_set_stage_events(handles[i], 5)
-            else:
-                layer.events = ev[i]
+            lib.gsa_set_stage_events(handles[i], 5)
             step_fn()
-        if not sharded:
-            lib.gsa_set_stage_events(None, 0)
-        else:
-            layer.events = None
+        lib.gsa_set_stage_events(None, 0)
         stop.record()
         torch.cuda.synchronize()
-    names = ("pool", "compress", "attend") if sharded else ("special", "pool", "compress", "select")
+    names = ("pool", "gather_kc", "compress", "attend") if sharded else ("special", "pool", "compress", "select")
     stage_ms = {n: sum(ev[i][j].elapsed_time(ev[i][j + 1]) for i in range(args.steps)) / args.steps
                 for j, n in enumerate(names)}
     n1 = ctypes.c_uint64()

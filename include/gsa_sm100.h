@@ -51,7 +51,7 @@ typedef enum {
     GSA_ERR_UNSUPPORTED = 10,       /* shape outside what the sm_100a kernels implement */
     GSA_ERR_CUDA = 11,              /* CUDA runtime / launch failure */
     GSA_ERR_WORKSPACE = 12,         /* workspace too small or misaligned */
-    GSA_ERR_NCCL = 13               /* reserved for the sharded layer */
+    GSA_ERR_NCCL = 13               /* NCCL failure in the multi-GPU layer (gsa_comm_*, gsa_shard_forward) */
 } gsa_status;
 
 typedef enum { GSA_DTYPE_F32 = 0, GSA_DTYPE_BF16 = 1 } gsa_dtype;
@@ -223,6 +223,54 @@ int gsa_shard_attend(const gsa_tensor* q_own, const gsa_tensor* k_all, const gsa
                      const gsa_tensor* out_own, void* workspace, size_t workspace_bytes,
                      gsa_stream_t stream);
 
+/* ---------------------------------------------------------------------------
+ * Multi-GPU layer at the C level (one process per GPU, NCCL over NVLink/NVSwitch).
+ *
+ * gsa_shard_of_rank: the rank's shard -- equal contiguous blocks of views and of
+ * special rows (num_frames and num_special must divide by nranks: every gather is
+ * then a plain equal-count all-gather).
+ *
+ * gsa_shard_gather_plan: the in-place all-gathers that complete a rank's buffers,
+ * identical on every rank. Op i gathers `count` elements per rank into buffer
+ * `buffer` at element offset `offset` (rank r's block at offset + r * count); buffers
+ * 0/1 = kc_all/vc_all (f32 [H][W][d]), 2/3 = k_all/v_all ([H][M][d], rows contiguous,
+ * head stride kv_head_stride elements). phase 0 (Kc/Vc) gates gsa_shard_compress,
+ * phase 1 (K/V rows) gates gsa_shard_attend. torch.distributed callers (dist.py)
+ * and gsa_shard_forward run the same plan.
+ *
+ * gsa_comm_*: an NCCL communicator. libnccl.so.2 is resolved at run time (inside a
+ * PyTorch process that is the library torch already loaded); the id is
+ * NCCL_UNIQUE_ID_BYTES = 128 bytes, made by rank 0 and broadcast by the caller.
+ * The communicator binds to the device current at gsa_comm_init. Failures are
+ * GSA_ERR_NCCL.
+ *
+ * gsa_shard_forward: the whole view-sharded layer on this rank: pool own windows ->
+ * Kc/Vc all-gather -> compressed attention + top-k of own windows vs all W (global
+ * ids) -> own specials + selection + gate + merge, with the K/V-row all-gather on
+ * the communicator's own stream overlapping the compressed branch (event-ordered,
+ * no host sync). q_own [H][Ms_g + Mi_g][d] (own specials, then own image rows);
+ * k_all / v_all [H][M][d] hold the rank's own rows, the rest is filled in place;
+ * out_own f32 = the rank's rows of the unsharded output; topk_own (nullable, device,
+ * [H][W_g][k_eff]) receives the rank's top-k rows. Bit-exact top-k with gsa_forward. */
+typedef struct {
+    int32_t buffer, phase;
+    int64_t offset, count;
+} gsa_gather_op;
+typedef struct gsa_comm_st* gsa_comm;
+
+int gsa_shard_of_rank(const gsa_layout* layout, int nranks, int rank, gsa_shard* out);
+int gsa_shard_gather_plan(const gsa_layout* layout, int nranks, int heads, int dim, int64_t kv_head_stride,
+                          gsa_gather_op* ops, int capacity, int* n_ops);
+int gsa_comm_get_unique_id(void* id /* 128 bytes */);
+int gsa_comm_init(gsa_comm* comm, const void* id /* 128 bytes */, int nranks, int rank);
+int gsa_comm_destroy(gsa_comm comm);
+size_t gsa_shard_forward_workspace_bytes(const gsa_layout* layout, const gsa_params* params, int nranks, int rank,
+                                         int heads, int dim);
+int gsa_shard_forward(gsa_comm comm, const gsa_tensor* q_own, const gsa_tensor* k_all, const gsa_tensor* v_all,
+                      const gsa_tensor* w_g, const gsa_layout* layout, const gsa_params* params,
+                      const gsa_tensor* out_own, int32_t* topk_own, void* workspace, size_t workspace_bytes,
+                      gsa_stream_t stream);
+
 /* project_qkv (layer.hpp:48-76): q/k/v[h][t][j] = sum_a x[t][a] * w[h][a][j], a
  * ascending, products and sums rounded separately (the reference's arithmetic,
  * so f32 outputs are bit-identical to it). x: device [tokens][model_dim] f32;
@@ -247,7 +295,9 @@ int gsa_selection_sparsity(const gsa_layout* layout, const gsa_params* params, d
 /* Instrumentation (bench.py, profiling). gsa_set_stage_events: when n >= 5,
  * subsequent gsa_forward calls on this thread record cudaEvent_t events[0..4]
  * on `stream` at: start, after the special path, after pooling, after the
- * compressed attention + top-k, after selection/gate/merge. n = 0 disables.
+ * compressed attention + top-k, after selection/gate/merge (gsa_shard_forward: start,
+ * after pooling, after the Kc/Vc gather, after the compressed branch, done). n = 0
+ * disables.
  * gsa_launch_count: kernels this library has launched since it was loaded. */
 int gsa_set_stage_events(void* const* events, int n);
 int gsa_launch_count(uint64_t* count);

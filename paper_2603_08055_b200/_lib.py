@@ -36,6 +36,10 @@ class GsaShard(C.Structure):
                 ("special_end", C.c_int32)]
 
 
+class GsaGatherOp(C.Structure):
+    _fields_ = [("buffer", C.c_int32), ("phase", C.c_int32), ("offset", C.c_int64), ("count", C.c_int64)]
+
+
 class GsaContextC(C.Structure):
     _fields_ = [(n, C.c_void_p) for n in ("qc", "kc", "vc", "o_comp", "lse_comp", "topk", "o_sel", "lse_sel",
                                           "gate", "lse_spec")]
@@ -89,6 +93,14 @@ def load() -> C.CDLL:
     L.gsa_shard_compress.argtypes = [T, T, T, Lp, P, S, T, vp, vp, C.POINTER(C.c_int), vp, C.c_size_t, vp]
     L.gsa_shard_attend.argtypes = [T, T, T, T, Lp, P, S, T, vp, T, vp, C.c_size_t, vp]
     L.gsa_project_qkv.argtypes = [vp, i32, i32, vp, vp, vp, i32, i32, T, T, T, vp]
+    L.gsa_shard_of_rank.argtypes = [Lp, i32, i32, S]
+    L.gsa_shard_gather_plan.argtypes = [Lp, i32, i32, i32, i64, C.POINTER(GsaGatherOp), i32, C.POINTER(C.c_int)]
+    L.gsa_comm_get_unique_id.argtypes = [vp]
+    L.gsa_comm_init.argtypes = [C.POINTER(C.c_void_p), vp, i32, i32]
+    L.gsa_comm_destroy.argtypes = [vp]
+    L.gsa_shard_forward_workspace_bytes.restype = C.c_size_t
+    L.gsa_shard_forward_workspace_bytes.argtypes = [Lp, P, i32, i32, i32, i32]
+    L.gsa_shard_forward.argtypes = [vp, T, T, T, T, Lp, P, T, vp, vp, C.c_size_t, vp]
     L.gsa_set_stage_events.argtypes = [C.POINTER(C.c_void_p), i32]
     L.gsa_launch_count.argtypes = [C.POINTER(C.c_uint64)]
     _lib = L
@@ -102,5 +114,6 @@ EXPORTED_SYMBOLS = [
     "gsa_build_selection_plan", "gsa_build_selection_plan_workspace_bytes", "gsa_block_sparse_attention",
     "gsa_gate", "gsa_forward_workspace_bytes", "gsa_forward", "gsa_forward_with_plan", "gsa_forward_stats", "gsa_selection_sparsity",
     "gsa_set_stage_events", "gsa_launch_count", "gsa_shard_workspace_bytes", "gsa_shard_pool", "gsa_shard_compress",
-    "gsa_shard_attend", "gsa_project_qkv",
+    "gsa_shard_attend", "gsa_project_qkv", "gsa_shard_of_rank", "gsa_shard_gather_plan", "gsa_comm_get_unique_id",
+    "gsa_comm_init", "gsa_comm_destroy", "gsa_shard_forward_workspace_bytes", "gsa_shard_forward",
 ]

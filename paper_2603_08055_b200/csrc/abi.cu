@@ -24,9 +24,6 @@ thread_local std::string g_msg;
 thread_local cudaEvent_t g_stage_events[5];
 thread_local int g_n_stage_events = 0;
 
-void stage_mark(int i, cudaStream_t st) {
-    if (g_n_stage_events >= 5) cudaEventRecord(g_stage_events[i], st);
-}
 
 int fail(int status, const char* fmt, ...) {
     char buf[512];
@@ -134,6 +131,19 @@ int selectable_windows(const DevLayout& L, int variant, int ref_stride, int* n_f
 }
 
 }  // namespace
+
+namespace gsa_sm100 {
+// the calling thread's gsa_last_error_message() (for entry points defined in other
+// translation units, e.g. comm.cu)
+int report_error(int status, const char* msg) {
+    g_msg = msg;
+    return status;
+}
+// gsa_set_stage_events instrumentation: record event i on `st` when enabled
+void stage_mark(int i, cudaStream_t st) {
+    if (g_n_stage_events >= 5) cudaEventRecord(g_stage_events[i], st);
+}
+}  // namespace gsa_sm100
 
 extern "C" {
 
@@ -565,6 +575,41 @@ size_t carve(const LayerPlan& lp, const gsa_context* ctx, char* base, size_t cap
     return c.used + 256;
 }
 
+
+// Hybrid fast path (selection.cpp:55-59: the forced windows lead every plan row, i.e.
+// every query attends ALL reference-frame keys). That part of each softmax is a dense
+// attention of the queries over the reference frames' keys: one tcgen05 FA pass over a
+// contiguous copy of those rows instead of gathering the same windows once per query
+// window. The selection epilogue merges it with the dynamic top-k windows' partial
+// softmax by log-sum-exp (identical to one softmax over forced ++ top-k up to f32
+// rounding). q rows [q_row0, q_row0 + mq) are image queries; k/v image rows start at
+// kv_img_row0; kf/vf [H][fk][64] bf16, prior_o [H][mq][64] f32, prior_lse [H][mq].
+int hybrid_prior(const gsa_tensor* q, int q_row0, int mq, const gsa_tensor* k, const gsa_tensor* v, int kv_img_row0,
+                 const DevLayout& L, int ref_stride, int n_forced, float scale, int H, __nv_bfloat16* kf,
+                 __nv_bfloat16* vf, float* prior_o, float* prior_lse, void* fa_ws, size_t fa_ws_bytes, cudaStream_t st) {
+    const int tpf = L.tokens_per_frame, nff = n_forced / L.wins_per_frame, fk = nff * tpf;
+    for (int fi = 0; fi < nff; ++fi) {
+        const int f = fi * ref_stride;  // forced frames 0, r, 2r, ... (selection.cpp:7-12)
+        const size_t src_row = (size_t)kv_img_row0 + (size_t)f * tpf;
+        for (int kv = 0; kv < 2; ++kv) {
+            const gsa_tensor* t = kv ? v : k;
+            __nv_bfloat16* dst = (kv ? vf : kf) + (size_t)fi * tpf * 64;
+            const __nv_bfloat16* src = static_cast<const __nv_bfloat16*>(t->data) + src_row * t->row_stride;
+            if (t->row_stride == 64) {  // contiguous rows: one 2-D copy over heads
+                GSA_CUDA(cudaMemcpy2DAsync(dst, (size_t)fk * 64 * 2, src, (size_t)t->head_stride * 2,
+                                           (size_t)tpf * 64 * 2, H, cudaMemcpyDeviceToDevice, st));
+            } else {  // strided rows (e.g. views of a fused QKV projection): one 2-D copy per head
+                for (int hh = 0; hh < H; ++hh)
+                    GSA_CUDA(cudaMemcpy2DAsync(dst + (size_t)hh * fk * 64, 64 * 2, src + (size_t)hh * t->head_stride,
+                                               (size_t)t->row_stride * 2, 64 * 2, tpf, cudaMemcpyDeviceToDevice, st));
+            }
+        }
+    }
+    gsa_tensor tkf{kf, GSA_DTYPE_BF16, H, fk, 64, (int64_t)fk * 64, 64};
+    gsa_tensor tvf{vf, GSA_DTYPE_BF16, H, fk, 64, (int64_t)fk * 64, 64};
+    gsa_tensor tpo{prior_o, GSA_DTYPE_F32, H, mq, 64, (int64_t)mq * 64, 64};
+    return dense_attention(q, &tkf, &tvf, scale, &tpo, prior_lse, q_row0, 0, mq, st, fa_ws, fa_ws_bytes);
+}
 }  // namespace
 
 size_t gsa_forward_workspace_bytes(const gsa_layout* layout, const gsa_params* params, int heads, int dim) {
@@ -658,35 +703,8 @@ int gsa_forward(const gsa_tensor* q, const gsa_tensor* k, const gsa_tensor* v, c
     const bool tc_sel = tc_select_supported(a);
     if (tc_sel && params->variant == 1 && lp.n_forced > 0 && lp.k_eff > 0 && b.kf && q->dim == 64 &&
         tc_dense_supported(*q, *k, *v)) {
-        // Hybrid fast path. Every query attends ALL reference-frame keys (selection.cpp:55-59:
-        // forced windows lead every plan row), so that part of the softmax is a dense
-        // attention of all image queries over the reference frames' keys (one tcgen05 FA
-        // pass instead of gathering the same 810 windows once per query window), merged
-        // in the selection epilogue with the dynamic top-k windows' partial softmax by
-        // log-sum-exp: identical to one softmax over forced ++ top-k up to f32 rounding.
-        const int tpf = lp.L.tokens_per_frame, nff = lp.n_forced / lp.L.wins_per_frame, fk = nff * tpf;
-        for (int fi = 0; fi < nff; ++fi) {
-            const int f = fi * params->ref_stride;  // forced frames 0, r, 2r, ... (selection.cpp:7-12)
-            const size_t src_row = (size_t)lp.Ms + (size_t)f * tpf;
-            for (int kv = 0; kv < 2; ++kv) {
-                const gsa_tensor* t = kv ? v : k;
-                __nv_bfloat16* dst = (kv ? b.vf : b.kf) + (size_t)fi * tpf * 64;
-                const __nv_bfloat16* src = static_cast<const __nv_bfloat16*>(t->data) + src_row * t->row_stride;
-                if (t->row_stride == 64) {  // contiguous rows: one 2-D copy over heads
-                    GSA_CUDA(cudaMemcpy2DAsync(dst, (size_t)fk * 64 * 2, src, (size_t)t->head_stride * 2,
-                                               (size_t)tpf * 64 * 2, H, cudaMemcpyDeviceToDevice, st));
-                } else {  // strided rows (e.g. views of a fused QKV projection): one 2-D copy per head
-                    for (int hh = 0; hh < H; ++hh)
-                        GSA_CUDA(cudaMemcpy2DAsync(dst + (size_t)hh * fk * 64, 64 * 2, src + (size_t)hh * t->head_stride,
-                                                   (size_t)t->row_stride * 2, 64 * 2, tpf, cudaMemcpyDeviceToDevice, st));
-                }
-            }
-        }
-        gsa_tensor tkf{b.kf, GSA_DTYPE_BF16, H, fk, 64, (int64_t)fk * 64, 64};
-        gsa_tensor tvf{b.vf, GSA_DTYPE_BF16, H, fk, 64, (int64_t)fk * 64, 64};
-        gsa_tensor tpo{b.prior_o, GSA_DTYPE_F32, H, lp.Mi, 64, (int64_t)lp.Mi * 64, 64};
-        GSA_TRY(dense_attention(q, &tkf, &tvf, lp.scale, &tpo, b.prior_lse, lp.Ms, 0, lp.Mi, st, b.fa_ws,
-                                b.fa_ws_bytes));
+        GSA_TRY(hybrid_prior(q, lp.Ms, lp.Mi, k, v, lp.Ms, lp.L, params->ref_stride, lp.n_forced, lp.scale, H, b.kf,
+                             b.vf, b.prior_o, b.prior_lse, b.fa_ws, b.fa_ws_bytes, st));
         a.rows = RowSource{nullptr, nullptr, b.forced, 0, b.topk, lp.k_eff, lp.k_eff};
         a.prior_o = b.prior_o;
         a.prior_lse = b.prior_lse;
@@ -812,6 +830,11 @@ struct ShardBufs {
     void* dense_ws;
     size_t dense_ws_bytes;
     float* lse_spec;
+    // hybrid fast path (hybrid_prior): reference-frame K/V copies, their dense softmax
+    __nv_bfloat16 *kf, *vf;
+    float *prior_o, *prior_lse;
+    void* fa_ws;
+    size_t fa_ws_bytes;
 };
 
 size_t shard_carve(const ShardPlan& sp, char* base, bool dry, ShardBufs* b) {
@@ -825,6 +848,19 @@ size_t shard_carve(const ShardPlan& sp, char* base, bool dry, ShardBufs* b) {
     b->dense_ws_bytes = tc_dense_workspace_bytes(g.heads, sp.Ms_g, g.M);
     b->dense_ws = c.take<char>(b->dense_ws_bytes);
     b->lse_spec = c.take<float>((size_t)g.heads * sp.Ms_g);
+    b->kf = b->vf = nullptr;
+    b->prior_o = b->prior_lse = nullptr;
+    b->fa_ws = nullptr;
+    b->fa_ws_bytes = 0;
+    if (g.n_forced > 0 && sp.Mi_g > 0) {
+        const int fk = g.n_forced / g.L.wins_per_frame * g.L.tokens_per_frame;  // reference-frame keys
+        b->kf = c.take<__nv_bfloat16>((size_t)g.heads * fk * g.dim);
+        b->vf = c.take<__nv_bfloat16>((size_t)g.heads * fk * g.dim);
+        b->prior_o = c.take<float>((size_t)g.heads * sp.Mi_g * g.dim);
+        b->prior_lse = c.take<float>((size_t)g.heads * sp.Mi_g);
+        b->fa_ws_bytes = tc_dense_workspace_bytes(g.heads, sp.Mi_g, fk);
+        b->fa_ws = c.take<char>(b->fa_ws_bytes);
+    }
     return c.used + 256;
 }
 
@@ -950,7 +986,18 @@ int gsa_shard_attend(const gsa_tensor* q_own, const gsa_tensor* k_all, const gsa
     a.w_g = static_cast<const float*>(w_g->data);
     a.o_comp = static_cast<const float*>(o_comp_own->data);
     a.wg_prep = b.wg_prep;
-    if (tc_select_supported(a))
+    const bool tc_sel = tc_select_supported(a);
+    if (tc_sel && params->variant == 1 && g.n_forced > 0 && g.k_eff > 0 && b.kf && d == 64 &&
+        tc_dense_supported(*q_own, *k_all, *v_all)) {
+        // the hybrid fast path of gsa_forward on the rank's own image queries (forced
+        // frames are global: their K/V rows are complete after the K/V all-gather)
+        GSA_TRY(hybrid_prior(q_own, sp.Ms_g, sp.Mi_g, k_all, v_all, g.Ms, g.L, params->ref_stride, g.n_forced,
+                             g.scale, H, b.kf, b.vf, b.prior_o, b.prior_lse, b.fa_ws, b.fa_ws_bytes, st));
+        a.rows = RowSource{nullptr, nullptr, b.forced, 0, topk_own, g.k_eff, g.k_eff};
+        a.prior_o = b.prior_o;
+        a.prior_lse = b.prior_lse;
+    }
+    if (tc_sel)
         GSA_CUDA(tc_select_gate_merge(a, st));
     else
         GSA_CUDA(launch_select_f32(a, st));

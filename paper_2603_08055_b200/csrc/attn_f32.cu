@@ -70,6 +70,11 @@ __global__ void __launch_bounds__(NT) attn_f32_kernel(AttnArgs a, bool vec8) {
         h = blk / qtiles;
         q0 = (blk - h * qtiles) * BQ;
     }
+    if (TOPK && a.glist_s) {  // k_eff too large for shared memory: per-CTA lists in global scratch
+        const int64_t cta = (int64_t)h * ((a.mq + BQ - 1) / BQ) + q0 / BQ;
+        lst_s = a.glist_s + cta * BQ * a.k_eff;
+        lst_i = a.glist_i + cta * BQ * a.k_eff;
+    }
     const int tid = threadIdx.x;
     const int qrows = min(BQ, a.mq - q0);
     const T* qb = reinterpret_cast<const T*>(a.q.data) + (int64_t)h * a.q.hs + (int64_t)q0 * a.q.rs;
@@ -208,14 +213,32 @@ template <typename T, int DMAX, bool TOPK>
 cudaError_t launch_typed(const AttnArgs& a, bool vec8, cudaStream_t st) {
     const int dp = ((a.dim + 3) & ~3) + 4;
     size_t smem = sizeof(float) * ((size_t)(BQ + 2 * BK) * dp + BQ * (BK + 1));
-    if (TOPK) smem += (size_t)BQ * a.k_eff * (sizeof(float) + sizeof(int));
+    const size_t list_bytes = TOPK ? (size_t)BQ * a.k_eff * (sizeof(float) + sizeof(int)) : 0;
+    AttnArgs b = a;
+    b.glist_s = nullptr;
+    b.glist_i = nullptr;
+    void* glist = nullptr;
+    if (smem + list_bytes <= 200 * 1024) {
+        smem += list_bytes;
+    } else {
+        // large budgets on this generic (head dim != 64) path: the sorted per-row lists
+        // go to stream-ordered global scratch instead of shared memory
+        const size_t n = (size_t)a.heads * ((a.mq + BQ - 1) / BQ) * list_bytes;
+        cudaError_t e = cudaMallocAsync(&glist, n, st);
+        if (e != cudaSuccess) return e;
+        b.glist_s = static_cast<float*>(glist);
+        b.glist_i = reinterpret_cast<int*>(static_cast<char*>(glist) + n / 2);
+        // per CTA: [BQ][k] floats in the first half, [BQ][k] ints in the second
+    }
     auto kern = attn_f32_kernel<T, DMAX, TOPK>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     dim3 grid((a.mq + BQ - 1) / BQ, a.heads);
     if (a.block_list) grid = dim3(((a.mq + BQ - 1) / BQ) * a.heads, 1);
-    { kern<<<grid, NT, smem, st>>>(a, vec8); note_launch(); }
-    return cudaGetLastError();
+    { kern<<<grid, NT, smem, st>>>(b, vec8); note_launch(); }
+    e = cudaGetLastError();
+    if (glist) cudaFreeAsync(glist, st);
+    return e;
 }
 
 template <typename T>

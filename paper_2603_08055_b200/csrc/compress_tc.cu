@@ -564,6 +564,52 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                         cmask[c] = ~(ch[0] | (ch[1] << 8) | (ch[2] << 16) | (ch[3] << 24)) & keep[c];
                     }
                     if (kDebug & 128) cmask[0] = cmask[1] = cmask[2] = cmask[3] = 0u;  // bring-up: no extraction
+                    // Re-seed on a clump: when >= K selectable scores of THIS tile clear the
+                    // threshold (the query's own view arriving in clustered activations: 81
+                    // near-equal windows; or the first tiles of any row), this tile's K-th best
+                    // approximate score bounds the row's K-th best from below. Raise LB to it
+                    // right away (16-bit radix search over the tile's 128 scores, as the tile-0
+                    // seed) instead of letting the histogram climb bin by bin while the later
+                    // tiles flood the candidate list.
+                    const int nc = __popc(cmask[0]) + __popc(cmask[1]) + __popc(cmask[2]) + __popc(cmask[3]);
+                    const bool reseed = t > 0 && tk.cnt >= 0 && nc >= K;
+                    if (__any_sync(0xffffffffu, reseed)) {
+                        if (reseed) {
+                            // sr is dead after pass A: turn it into order-preserving keys in
+                            // place (0 = not selectable, below every key)
+#pragma unroll
+                            for (int c = 0; c < 4; ++c)
+#pragma unroll
+                                for (int e = 0; e < 32; ++e)
+                                    sr[c][e] = ((keep[c] >> e) & 1u) ? fkey(__uint_as_float(sr[c][e])) : 0u;
+                            uint32_t res = 0;
+#pragma unroll 1
+                            for (int bit = 31; bit >= 16; --bit) {
+                                const uint32_t cand = res | (1u << bit);
+                                int cnt = 0;
+#pragma unroll
+                                for (int c = 0; c < 4; ++c)
+#pragma unroll
+                                    for (int e = 0; e < 32; ++e) cnt += sr[c][e] >= cand ? 1 : 0;
+                                if (cnt >= K) res = cand;
+                            }
+                            const float lbt = fkey_inv(res);
+                            if (res != 0u && lbt > tk.lb) {
+                                tk.lb = lbt;
+                                tk.thr = fmaxf(tk.thr, topk_threshold(lbt, tk.eps));
+                                tk.hist[0] = tk.hist[1] = 0u;  // counts were relative to the old LB
+                                const uint32_t kthr = fkey(tk.thr);
+#pragma unroll
+                                for (int c = 0; c < 4; ++c) {
+                                    uint32_t m = 0u;
+#pragma unroll
+                                    for (int e = 0; e < 32; ++e) m |= (sr[c][e] >= kthr ? 1u : 0u) << e;
+                                    cmask[c] &= m;
+                                }
+                            }
+                        }
+                        __syncwarp();
+                    }
                 }
             }
             const float mt = fmaxf(fmaxf(cmax[0], cmax[1]), fmaxf(cmax[2], cmax[3]));

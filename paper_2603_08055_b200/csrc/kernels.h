@@ -9,6 +9,10 @@ namespace gsa_sm100 {
 
 // kernels launched by this library (gsa_launch_count); bumped by every launcher
 void note_launch(int n = 1);
+// sets the calling thread's gsa_last_error_message() and returns status
+int report_error(int status, const char* msg);
+// gsa_set_stage_events: records stage event i (0..4) on st when enabled on this thread
+void stage_mark(int i, cudaStream_t st);
 
 struct TensorRef {  // device view, element strides
     const void* data;
@@ -49,6 +53,9 @@ struct AttnArgs {
     const int* block_list;
     const int* block_count;
     bool topk_only;
+    // set by the launcher when the per-row top-k lists do not fit in shared memory
+    float* glist_s;
+    int* glist_i;
 };
 cudaError_t launch_attn_f32(const AttnArgs& a, cudaStream_t st);
 

@@ -67,16 +67,27 @@ class ShardSpec:
 
 
 def shard_spec(layout: TokenLayout, rank: int, world: int) -> ShardSpec:
-    """Contiguous equal blocks of views and specials. Equal blocks keep every
-    all-gather a plain ncclAllGather (equal counts), so the view and special
+    """Contiguous equal blocks of views and specials (gsa_shard_of_rank). Equal blocks
+    keep every all-gather a plain ncclAllGather (equal counts), so the view and special
     counts must divide by the world size."""
     if world < 1 or not 0 <= rank < world:
         raise ShapeMismatch(f"rank {rank} outside world {world}")
-    if layout.num_frames % world or layout.num_special % world:
-        raise ShapeMismatch(f"view sharding needs num_frames ({layout.num_frames}) and num_special "
-                            f"({layout.num_special}) divisible by the world size {world}")
-    fv, fs = layout.num_frames // world, layout.num_special // world
-    return ShardSpec(rank * fv, (rank + 1) * fv, rank * fs, (rank + 1) * fs)
+    out = _lib.GsaShard()
+    _check(_lib.load().gsa_shard_of_rank(C.byref(layout.c()), world, rank, C.byref(out)))
+    return ShardSpec(out.frame_begin, out.frame_end, out.special_begin, out.special_end)
+
+
+def gather_plan(layout: TokenLayout, world: int, heads: int, dim: int, kv_head_stride: int):
+    """The in-place all-gathers of one sharded layer (gsa_shard_gather_plan; identical on
+    every rank): [(buffer, phase, offset, count)], buffer 0/1 = kc_all/vc_all, 2/3 =
+    k_all/v_all (flat element offsets; rank r's block at offset + r * count)."""
+    L = _lib.load()
+    n = C.c_int()
+    _check(L.gsa_shard_gather_plan(C.byref(layout.c()), world, heads, dim, kv_head_stride, None, 0, C.byref(n)))
+    ops = (_lib.GsaGatherOp * max(1, n.value))()
+    _check(L.gsa_shard_gather_plan(C.byref(layout.c()), world, heads, dim, kv_head_stride, ops, n.value,
+                                   C.byref(n)))
+    return [(o.buffer, o.phase, o.offset, o.count) for o in ops[: n.value]]
 
 
 def own_rows_of(x: torch.Tensor, layout: TokenLayout, spec: ShardSpec) -> torch.Tensor:
@@ -127,20 +138,17 @@ class DeviceOps:
 
 
 # ---------------------------------------------------------------- collectives
-def _gather_segments(bufs, segments, rank: int, world: int, group, coalesce: bool):
-    """In-place all-gather of row segments of head-major [H][rows][d] buffers.
-    segments: (begin_row, rows_per_rank) per buffer segment; rank r's rows sit
-    at begin + r*rows_per_rank. Returns a handle whose wait() orders the
-    current stream after the gathers."""
+def _run_gathers(bufs, plan, phase: int, rank: int, world: int, group, coalesce: bool):
+    """In-place all-gathers of the C plan's ops of one phase over flat views of the
+    (contiguous) buffers. Returns a handle whose wait() orders the current stream
+    after the gathers."""
     calls = []
-    for buf in bufs:
-        for begin, per in segments[id(buf)]:
-            if per == 0:
-                continue
-            for h in range(buf.shape[0]):
-                out = buf[h, begin:begin + world * per]
-                inp = out[rank * per:(rank + 1) * per]
-                calls.append((out, inp))
+    for b, ph, off, cnt in plan:
+        if ph != phase or cnt == 0:
+            continue
+        flat = bufs[b].view(-1)
+        out = flat[off:off + world * cnt]
+        calls.append((out, out[rank * cnt:(rank + 1) * cnt]))
     if coalesce:
         with dist._coalescing_manager(group, calls[0][0].device if calls else None, async_ops=True) as cm:
             for out, inp in calls:
@@ -204,14 +212,15 @@ class ShardedLayer:
         self.ops.pool(q_own, k_all, v_all, self.qc_own, self.kc_all, self.vc_all)
         self._mark(1)
         if self.world > 1:
-            # 2. Kc/Vc first (gates the compressed branch), then K/V rows (gates step 4);
-            #    both queue on the group's NCCL stream, so the K/V transfer overlaps step 3
-            segs = {id(self.kc_all): [(0, self.W_g)], id(self.vc_all): [(0, self.W_g)]}
-            h_c = _gather_segments([self.kc_all, self.vc_all], segs, self.rank, self.world, self.group, self.coalesce)
-            ms_g = spec.special_end - spec.special_begin
-            mi_g = (spec.frame_end - spec.frame_begin) * L.tokens_per_frame
-            segs_kv = {id(k_all): [(0, ms_g), (L.num_special, mi_g)], id(v_all): [(0, ms_g), (L.num_special, mi_g)]}
-            h_kv = _gather_segments([k_all, v_all], segs_kv, self.rank, self.world, self.group, self.coalesce)
+            # 2. the C plan's gathers (gsa_shard_gather_plan): Kc/Vc first (gates the
+            #    compressed branch), then K/V rows (gates step 4); both queue on the group's
+            #    NCCL stream, so the K/V transfer overlaps step 3
+            if not (k_all.is_contiguous() and v_all.is_contiguous()):
+                raise ShapeMismatch("sharded layer: k_all / v_all must be contiguous [H][M][d]")
+            plan = gather_plan(L, self.world, self.heads, self.dim, k_all.stride(0))
+            bufs = [self.kc_all, self.vc_all, k_all, v_all]
+            h_c = _run_gathers(bufs, plan, 0, self.rank, self.world, self.group, self.coalesce)
+            h_kv = _run_gathers(bufs, plan, 1, self.rank, self.world, self.group, self.coalesce)
             h_c.wait()
         # 3. compressed attention + top-k: own query windows vs all windows
         ke = self.ops.compress(self.qc_own, self.kc_all, self.vc_all, self.o_comp_own, self.lse_own, self.topk_own)
@@ -227,3 +236,68 @@ class ShardedLayer:
     @property
     def ctx_topk(self):
         return self.topk_own[:, :, :self.k_eff]
+
+
+class NcclShardedLayer:
+    """The view-sharded layer at the C level: one NCCL communicator (gsa_comm_init,
+    libnccl resolved by the library) and gsa_shard_forward, which runs pool -> Kc/Vc
+    all-gather -> compress -> selection with the K/V-row all-gather overlapping the
+    compressed branch on the communicator's stream (include/gsa_sm100.h). The id is
+    exchanged through the caller's torch.distributed group (or passed in)."""
+
+    def __init__(self, layout: TokenLayout, params: GsaParams, heads: int, dim: int, rank: int, world: int,
+                 group=None, device=None, unique_id: Optional[bytes] = None):
+        self.L = _lib.load()
+        self.layout, self.params, self.heads, self.dim = layout, params, heads, dim
+        self.rank, self.world = rank, world
+        self.spec = shard_spec(layout, rank, world)
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        if unique_id is None:
+            buf = (C.c_char * 128)()
+            if rank == 0:
+                _check(self.L.gsa_comm_get_unique_id(buf))
+            obj = [bytes(buf)]
+            if world > 1:
+                dist.broadcast_object_list(obj, src=0, group=group)
+            unique_id = obj[0]
+        idb = (C.c_char * 128).from_buffer_copy(unique_id)
+        self.comm = C.c_void_p()
+        with torch.cuda.device(self.device):
+            _check(self.L.gsa_comm_init(C.byref(self.comm), idb, world, rank))
+        self.lc, self.pc = layout.c(), params.c()
+        nbytes = self.L.gsa_shard_forward_workspace_bytes(C.byref(self.lc), C.byref(self.pc), world, rank, heads, dim)
+        if nbytes == 0:
+            raise ShapeMismatch("gsa_shard_forward_workspace_bytes rejected the layout / params")
+        self.ws = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+        W = layout.num_windows
+        nf = 0
+        if params.variant == 1 and params.ref_stride >= 1:
+            nf = len(range(0, layout.num_frames, params.ref_stride)) * layout.windows_per_frame
+        self.k_eff = max(0, min(params.top_k, W - nf))
+        w0, w1 = self.spec.windows(layout)
+        self.topk_own = torch.empty(heads, w1 - w0, max(1, self.k_eff), dtype=torch.int32, device=self.device)
+
+    def forward(self, q_own, k_all, v_all, w_g, out_own: Optional[torch.Tensor] = None):
+        if out_own is None:
+            out_own = torch.empty(self.heads, self.spec.own_rows(self.layout), self.dim, dtype=torch.float32,
+                                  device=self.device)
+        _check(self.L.gsa_shard_forward(self.comm, C.byref(_desc(q_own)), C.byref(_desc(k_all)),
+                                        C.byref(_desc(v_all)), C.byref(_desc(w_g.contiguous())), C.byref(self.lc),
+                                        C.byref(self.pc), C.byref(_desc(out_own)), _ptr(self.topk_own),
+                                        _ptr(self.ws), self.ws.numel(), _stream()))
+        return out_own
+
+    @property
+    def ctx_topk(self):
+        return self.topk_own[:, :, :self.k_eff]
+
+    def close(self):
+        if self.comm:
+            _check(self.L.gsa_comm_destroy(self.comm))
+            self.comm = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

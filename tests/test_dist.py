@@ -259,3 +259,73 @@ def test_sharded_layer_two_processes_one_gpu():
                        capture_output=True, text=True, timeout=600, cwd=root)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
     assert r.stdout.count("topk bit-exact True, gathered K/V exact True") == 4, r.stdout
+
+
+def test_shard_of_rank_and_gather_plan_cover_every_row():
+    """The C plan (gsa_shard_gather_plan) run by both gsa_shard_forward (NCCL) and the
+    torch.distributed path: over all ranks its blocks tile every Kc/Vc row and every K/V
+    row of every head exactly once, and gsa_shard_of_rank matches the equal-block split."""
+    import paper_2603_08055_b200 as gsa
+    from paper_2603_08055_b200.dist import gather_plan, shard_spec
+    for lt, world in (((40, 8, 36, 36, 4), 4), ((0, 6, 8, 12, 4), 3), ((6, 2, 8, 8, 2), 2), ((5, 5, 4, 4, 4), 5)):
+        L = gsa.build_token_layout(*lt)
+        H, d = 3, 64
+        M, W = L.total_tokens, L.num_windows
+        for r in range(world):
+            s = shard_spec(L, r, world)
+            assert (s.frame_begin, s.frame_end) == (r * lt[1] // world, (r + 1) * lt[1] // world)
+            assert (s.special_begin, s.special_end) == (r * lt[0] // world, (r + 1) * lt[0] // world)
+        kv_hs = M * d + 64  # a padded head stride is allowed
+        plan = gather_plan(L, world, H, d, kv_hs)
+        cover = {0: np.zeros(H * W * d, np.int32), 1: np.zeros(H * W * d, np.int32),
+                 2: np.zeros(H * kv_hs, np.int32), 3: np.zeros(H * kv_hs, np.int32)}
+        for b, phase, off, cnt in plan:
+            assert phase == (0 if b < 2 else 1)
+            cover[b][off:off + world * cnt] += 1
+        for b in (0, 1):
+            assert (cover[b] == 1).all()
+        for b in (2, 3):
+            c = cover[b].reshape(H, kv_hs)
+            assert (c[:, :M * d] == 1).all() and (c[:, M * d:] == 0).all()
+    with pytest.raises(gsa.ShapeMismatch):
+        shard_spec(gsa.build_token_layout(5, 5, 4, 4, 4), 0, 2)
+
+
+def test_comm_init_fails_cleanly_without_a_gpu():
+    """gsa_comm_* report status codes (NcclError / CudaError), never crash, when the
+    process has no usable GPU (this CPU box)."""
+    import ctypes as C
+    torch = pytest.importorskip("torch")
+    if torch.cuda.is_available():
+        pytest.skip("needs a GPU-less process")
+    from paper_2603_08055_b200 import _lib
+    L = _lib.load()
+    comm = C.c_void_p()
+    rc = L.gsa_comm_init(C.byref(comm), (C.c_char * 128)(), 1, 0)
+    assert rc in (11, 13), rc  # GSA_ERR_CUDA / GSA_ERR_NCCL
+    assert L.gsa_comm_destroy(None) == 0
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("variant", [0, 1])
+def test_nccl_sharded_layer_single_rank_matches_forward(variant):
+    """gsa_shard_forward through a real NCCL communicator (one rank: the only GPU this
+    box has) equals gsa_forward: top-k bit-exact, output to f32 rounding."""
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2603_08055_b200 as gsa
+    from paper_2603_08055_b200.dist import NcclShardedLayer
+    lt = (40, 8, 36, 36, 4)
+    L = gsa.build_token_layout(*lt)
+    g = torch.Generator(device="cuda").manual_seed(3)
+    q, k, v = (torch.randn(4, L.total_tokens, 64, generator=g, device="cuda").to(torch.bfloat16) for _ in range(3))
+    wg = torch.randn(4, 64, 64, generator=g, device="cuda") / 8
+    p = gsa.GsaParams(window_s=4, top_k=16, variant=variant, ref_stride=3)
+    ref, ctx = gsa.gsa_forward(q, k, v, wg, L, p, context=True)
+    layer = NcclShardedLayer(L, p, 4, 64, 0, 1)
+    out = layer.forward(q, k.clone(), v.clone(), wg)
+    torch.cuda.synchronize()
+    assert torch.equal(layer.ctx_topk, ctx.topk)
+    assert float((out - ref).abs().max()) < 1e-5
+    layer.close()
