@@ -123,7 +123,8 @@ int gsa_special_token_attention(const gsa_tensor* q_spec, const gsa_tensor* k, c
  * [H][W][d]; excluded: device byte mask [W] or NULL; out f32 [H][W][d]; lse
  * [H][W]; indices [H][W][k_eff]; guide_scores (nullable) [H][W][k_eff] f32.
  * *k_eff_out (host) = min(k, selectable). Indices are bit-exact; k_eff up to
- * 2048 (above 128 the selection runs on exact CUDA-core scores). With an
+ * 10240 (above 128 the selection runs on exact CUDA-core scores; above 10240 the
+ * call returns GSA_ERR_UNSUPPORTED). With an
  * exclusion mask the call synchronises `stream` (k_eff needs the mask's count). */
 size_t gsa_compressed_attention_topk_workspace_bytes(int heads, int windows, int dim, int k);
 int gsa_compressed_attention_topk(const gsa_tensor* qc, const gsa_tensor* kc, const gsa_tensor* vc,

@@ -310,8 +310,9 @@ int gsa_compressed_attention_topk(const gsa_tensor* qc, const gsa_tensor* kc, co
     if (k_eff_out) *k_eff_out = k_eff;
     if (W == 0) return GSA_OK;
     GSA_TRY(generic_supported(qc->dim, 1));
-    if (k_eff > 2048)
-        return fail(GSA_ERR_UNSUPPORTED, "fused_compressed_attention_topk: k_eff=%d > 2048 not implemented on sm_100a yet", k_eff);
+    if (k_eff > kMaxTopK)
+        return fail(GSA_ERR_UNSUPPORTED, "fused_compressed_attention_topk: k_eff=%d > %d (the largest per-row budget the "
+                    "sm_100a selection sorts)", k_eff, kMaxTopK);
     GSA_CUDA(tc_compress_topk(*qc, *kc, *vc, k_eff, scale, excluded, static_cast<float*>(out->data),
                               out->head_stride, out->row_stride, lse, indices, guide, workspace, ws_bytes,
                               (cudaStream_t)stream));
@@ -518,8 +519,9 @@ int layer_checks(const gsa_tensor* q, const gsa_tensor* k, const gsa_tensor* v, 
     if (with_plan) {
         lp->k_eff = 0;  // no top-k on the pinned-plan path
         lp->n_forced = 0;
-    } else if (lp->k_eff > 2048) {
-        return fail(GSA_ERR_UNSUPPORTED, "gsa_forward: k_eff=%d > 2048 not implemented on sm_100a yet", lp->k_eff);
+    } else if (lp->k_eff > kMaxTopK) {
+        return fail(GSA_ERR_UNSUPPORTED, "gsa_forward: k_eff=%d > %d (the largest per-row budget the sm_100a "
+                    "selection sorts)", lp->k_eff, kMaxTopK);
     }
     return GSA_OK;
 }
@@ -651,13 +653,13 @@ int gsa_forward(const gsa_tensor* q, const gsa_tensor* k, const gsa_tensor* v, c
     stage_mark(1, st);
 
     // 2. pool Q/K/V image rows (layer.hpp:204-206); on the tensor-core path the
-    // same pass also writes the bf16 hi/lo operands and row norms K2 consumes
+    // same pass also writes Qc's bf16 hi/lo operands and row norms K2 consumes
     CompressSplits sp{};
     const bool have_sp = tc_compress_split_buffers(b.compress_ws, b.compress_ws_bytes, H, lp.W, d, lp.k_eff, &sp);
-    PoolJob jobs[3] = {
+    PoolJob jobs[3] = {  // K and V get their tensor-core operands in K2 (centred K splits, fp16 V)
         {ref_of(*q, lp.Ms), b.qc, sp.qh, sp.ql, sp.qnorm},
-        {ref_of(*k, lp.Ms), b.kc, sp.kh, sp.kl, sp.knorm},
-        {ref_of(*v, lp.Ms), b.vc, sp.vh, sp.vl, nullptr},
+        {ref_of(*k, lp.Ms), b.kc, nullptr, nullptr, nullptr},
+        {ref_of(*v, lp.Ms), b.vc, nullptr, nullptr, nullptr},
     };
     GSA_CUDA(launch_pool(jobs, 3, H, d, lp.L, 1.0f / (float)(lp.L.s * lp.L.s), st));
     stage_mark(2, st);
@@ -796,7 +798,9 @@ int shard_checks(const gsa_layout* layout, const gsa_params* p, const gsa_shard*
     const int sel = selectable_windows(L, p->variant, p->ref_stride, &lp.n_forced);
     lp.k_eff = p->top_k < sel ? p->top_k : sel;
     lp.scale = resolved_scale(p->scale, dim);
-    if (lp.k_eff > 2048) return fail(GSA_ERR_UNSUPPORTED, "k_eff=%d > 2048 not implemented on sm_100a yet", lp.k_eff);
+    if (lp.k_eff > kMaxTopK)
+        return fail(GSA_ERR_UNSUPPORTED, "k_eff=%d > %d (the largest per-row budget the sm_100a selection sorts)",
+                    lp.k_eff, kMaxTopK);
     gsa_layout lq{0, sh->frame_end - sh->frame_begin, layout->grid_h, layout->grid_w, layout->window_s};
     if (lq.num_frames == 0) lq.num_frames = 1;  // placeholder geometry; an empty shard does no work
     sp->Lq = make_dev_layout(lq);

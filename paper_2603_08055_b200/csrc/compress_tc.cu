@@ -3,10 +3,13 @@
 // indices bit-exact with the reference by construction.
 //
 // Pooled Qc/Kc/Vc are f32 means (not bf16-representable), so every operand is
-// split x = hi + lo (bf16 each, |x - hi - lo| <= 2^-16 |x|) and
+// split x = hi + lo (bf16 each, |x - hi - lo| <= 2^-16 |x|) for the scores, which set
+// the softmax AND the ranking, and
 //   S  = Qh.Kh^T + Qh.Kl^T + Ql.Kh^T            (12 MMAs, M=N=128, per key tile)
-//   O += Ph.Vh + Ph.Vl + Pl.Vh                  (24 MMAs, P from TMEM)
-// give softmax/PV far inside the tolerance. The scores run on centred keys
+//   O += P16.V16                                 (8 MMAs, P fp16 from TMEM)
+// where P and V go through fp16 (11-bit significands, V scaled per head by a power of
+// two into fp16 range): relative error <= ~2^-11 in O'_comp (measured ~3e-4 rel L2),
+// far inside the 1e-3 layer tolerance, for one PV MMA term instead of three. The scores run on centred keys
 // kc - kbar (kbar = per-head mean key: a per-row shift, invisible to the softmax and
 // the ranking, added back to the lse). S is only an APPROXIMATION of the reference
 // guide score (scaled_dot: 4 stride-4 f32 lane sums, no FMA), so the top-k runs in
@@ -28,6 +31,8 @@
 
 #include <cstdio>
 #include <cstdlib>
+#include <cub/block/block_radix_sort.cuh>
+#include <cub/block/block_scan.cuh>
 #include <vector>
 
 #include "tc.h"
@@ -118,6 +123,7 @@ struct CompParams {
     const float* kbar;        // [H][64] per-head mean key: S' = q.(kc - kbar) = S - q.kbar
     const float* qc;          // [H][Wq][64] f32 (lse correction q.kbar)
     int64_t qc_hs;
+    const float* vmax;        // [H] max |vc|: V is fed to the MMA as fp16(vc * 2^-e_h), e_h = vexp(vmax[h])
     const uint32_t* exbits;   // [ceil(Wk/32)] or null
     float* out;
     int64_t out_hs, out_rs;
@@ -137,6 +143,9 @@ __device__ __forceinline__ uint32_t fkey(float x) {
 __device__ __forceinline__ float fkey_inv(uint32_t k) {
     return __uint_as_float((k & 0x80000000u) ? (k & 0x7fffffffu) : ~k);
 }
+
+// per-head power-of-two exponent that brings |vc| <= vmax below 2^14 in fp16 (exact scaling)
+__device__ __forceinline__ int vexp(float vmax) { return vmax > 0.0f ? ilogbf(vmax) - 13 : 0; }
 
 __device__ __forceinline__ float topk_threshold(float tau, float eps) {
     return tau - (2.0f * eps + DELTA_REL * fabsf(tau));
@@ -247,8 +256,7 @@ __device__ __forceinline__ int seq_v(int t, int T) { return t == T - 1 ? 2 * T -
 __global__ void __launch_bounds__(NTHREADS, 1)
     compress_tc_kernel(const __grid_constant__ CUtensorMap tm_qh, const __grid_constant__ CUtensorMap tm_ql,
                        const __grid_constant__ CUtensorMap tm_kh, const __grid_constant__ CUtensorMap tm_kl,
-                       const __grid_constant__ CUtensorMap tm_vh, const __grid_constant__ CUtensorMap tm_vl,
-                       const CompParams p) {
+                       const __grid_constant__ CUtensorMap tm_v16, const CompParams p) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     CompSmem& sm = *reinterpret_cast<CompSmem*>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
     const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
@@ -290,13 +298,13 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             }
             __syncwarp();
             int seq = 0;
-            auto load = [&](const CUtensorMap* th, const CUtensorMap* tl, int t) {
+            auto load = [&](const CUtensorMap* th, const CUtensorMap* tl, int t) {  // tl null: fp16 V tile only
                 const int st = seq % NS;
                 mbar_wait(&sm.empty[st], (uint32_t)(((seq / NS) & 1) ^ 1));
                 if (elect_one()) {
-                    mbar_arrive_expect_tx(&sm.full[st], STAGE);
+                    mbar_arrive_expect_tx(&sm.full[st], tl ? STAGE : TILE);
                     tma_load_3d(&sm.ring[st][0], th, &sm.full[st], 0, t * 128, h);
-                    tma_load_3d(&sm.ring[st][TILE], tl, &sm.full[st], 0, t * 128, h);
+                    if (tl) tma_load_3d(&sm.ring[st][TILE], tl, &sm.full[st], 0, t * 128, h);
                 }
                 __syncwarp();
                 ++seq;
@@ -304,7 +312,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             load(&tm_kh, &tm_kl, 0);
             if (T > 1) load(&tm_kh, &tm_kl, 1);
             for (int t = 0; t < T; ++t) {
-                load(&tm_vh, &tm_vl, t);
+                load(&tm_v16, nullptr, t);
                 if (t + 2 < T) load(&tm_kh, &tm_kl, t + 2);
             }
         } else if (warp == 9) {
@@ -315,7 +323,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             // buffer (in-order execution) and is issued BEFORE the P waits of n+1, n+2,
             // so every WG always has its next S computing while it runs a softmax.
             const uint32_t id_s = idesc_bf16(128, 128, 0, 0);
-            const uint32_t id_o = idesc_bf16(128, 64, 0, 1);
+            const uint32_t id_o = idesc_f16(128, 64, 0, 1);  // P (TMEM) and V (SMEM) in fp16
 #ifdef COMPRESS_PROF
             const bool mprof = p.prof && blockIdx.x == 0 && blockIdx.y == 0 && lane == 0;
             unsigned long long mw_full = 0, mw_p = 0, m_t0 = clock64(), m_c;
@@ -359,16 +367,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 mbar_wait(&sm.p_full[w][t & 1], (uint32_t)((t >> 1) & 1));
                 MPROF_T(mw_p);
                 tc_fence_after();
-                const uint64_t vh = umma_desc(smem_u32(&sm.ring[s % NS][0]), 16, 1024, 2);
-                const uint64_t vl = umma_desc(smem_u32(&sm.ring[s % NS][TILE]), 16, 1024, 2);
+                const uint64_t v16 = umma_desc(smem_u32(&sm.ring[s % NS][0]), 16, 1024, 2);
                 const uint32_t o = tmem + O_COL0 + 64 * w, pb = tmem + 128 * (n % NSB);
                 if (elect_one()) {
-                    for (int ks = 0; ks < 8; ++ks) {
-                        const uint32_t a_hi = pb + 32 * (ks >> 1) + 8 * (ks & 1);
-                        mma_bf16_ts(o, a_hi, vh + 128 * ks, id_o, (t | ks) != 0);
-                        mma_bf16_ts(o, a_hi, vl + 128 * ks, id_o, 1);
-                        mma_bf16_ts(o, a_hi + 16, vh + 128 * ks, id_o, 1);
-                    }
+                    for (int ks = 0; ks < 8; ++ks)  // P fp16 of keys [16 ks, 16 ks + 16): columns 32 (ks/2) + 8 (ks%2)
+                        mma_bf16_ts(o, pb + 32 * (ks >> 1) + 8 * (ks & 1), v16 + 128 * ks, id_o, (t | ks) != 0);
                     mma_commit(&sm.o_done[w]);
                     if (t == T - 1) mma_commit(&sm.o_final[w]);
                     if (w == 1) mma_commit(&sm.empty[s % NS]);  // V(t) fully used
@@ -641,14 +644,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     m_used = mnew;
                 }
             }
-            // ---- pass B, per 32-key chunk: P = exp2(S*c2 - m*c2) split P = hi + lo with hi =
-            // P truncated to bf16 (one PRMT packs two his; lo = P - hi is exact in f32, then
-            // rounded: |P - hi - lo| <= 2^-15 |P|) written over the chunk's S; then the
-            // chunk's top-k candidates. The P barrier is released after the last chunk's
-            // stores, before its top-k.
+            // ---- pass B, per 32-key chunk: P = exp2(S*c2 - m*c2) as packed fp16 pairs written
+            // over the first 16 columns of the chunk's S (one cvt per pair); then the chunk's
+            // top-k candidates. The P barrier is released after the last chunk's stores,
+            // before its top-k.
             const float mc = m_used * p.c2;
             const float2 c2v = make_float2(p.c2, p.c2), nmc = make_float2(-mc, -mc);
-            const float2 neg1 = make_float2(-1.0f, -1.0f);
             float2 lsum2[2] = {make_float2(0.0f, 0.0f), make_float2(0.0f, 0.0f)};
             // unrolled by 2 only: the fully unrolled loop did not fit the instruction cache
             // (20-50 % no_instruction stalls); measured at V=1000: x1 82.2 ms, x2 76-78 ms, x4 85 ms
@@ -666,21 +667,16 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 if (prof_on) { c1 = clock64(); pb[0] += c1 - c0; c0 = c1; }
 #endif
                 {
-                    uint32_t hi[16], lo[16];
+                    uint32_t p16[16];
 #pragma unroll
                     for (int e2 = 0; e2 < 16; ++e2) {
                         const float2 x = make_float2(__uint_as_float(v[2 * e2]), __uint_as_float(v[2 * e2 + 1]));
                         const float2 a = __ffma2_rn(x, c2v, nmc);
                         const float2 pv = make_float2(ex2_approx(a.x), ex2_approx(a.y));
-                        lsum2[e2 & 1] = __fadd2_rn(lsum2[e2 & 1], pv);
-                        const uint32_t u0 = __float_as_uint(pv.x), u1 = __float_as_uint(pv.y);
-                        hi[e2] = __byte_perm(u0, u1, 0x7632);
-                        const float2 hf = make_float2(__uint_as_float(u0 & 0xffff0000u), __uint_as_float(u1 & 0xffff0000u));
-                        const float2 lf = __ffma2_rn(hf, neg1, pv);
-                        lo[e2] = pack_bf16(lf.x, lf.y);
+                        lsum2[e2 & 1] = __fadd2_rn(lsum2[e2 & 1], pv);  // the denominator sums the exact f32 P
+                        p16[e2] = pack_f16(pv.x, pv.y);
                     }
-                    tmem_st_32x32b_x16(cb, hi);
-                    tmem_st_32x32b_x16(cb + 16, lo);
+                    tmem_st_32x32b_x16(cb, p16);
                 }
 #ifdef COMPRESS_PROF
                 if (prof_on) { c1 = clock64(); pb[1] += c1 - c0; c0 = c1; }
@@ -754,7 +750,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         tmem_ld_32x32b_x32(o_base + 32, o[1]);
         tmem_wait_ld();
         if (row_ok) {
-            const float inv = 1.0f / l;
+            const float inv = ldexpf(1.0f / l, vexp(p.vmax[h]));  // undo the fp16 V scaling exactly
             float* dst = p.out + (int64_t)h * p.out_hs + (int64_t)grow * p.out_rs;
 #pragma unroll
             for (int half = 0; half < 2; ++half)
@@ -944,6 +940,43 @@ __global__ void split_kernel(const float* __restrict__ x, int64_t hs, int64_t rs
     if (norm && c == 0 && row < (int64_t)heads * W) norm[row] = sqrtf(sq);
 }
 
+// per-head max |x| of an f32 [H][W][64] tensor (strided rows). grid (chunks, H); out[h]
+// zeroed beforehand; |x| >= 0, so the f32 bit patterns order like the values and an
+// integer atomicMax merges the chunks (order-free, deterministic)
+__global__ void absmax_kernel(const float* __restrict__ x, int64_t hs, int64_t rs, int W, float* out) {
+    const int h = blockIdx.y;
+    const int64_t n = (int64_t)W * 64;
+    const int64_t i0 = n * blockIdx.x / gridDim.x, i1 = n * (blockIdx.x + 1) / gridDim.x;
+    float m = 0.0f;
+    for (int64_t i = i0 + threadIdx.x; i < i1; i += blockDim.x)
+        m = fmaxf(m, fabsf(x[(int64_t)h * hs + (i >> 6) * rs + (i & 63)]));
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    __shared__ float red[32];
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x / 32] = m;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        m = threadIdx.x < blockDim.x / 32 ? red[threadIdx.x] : 0.0f;
+        for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+        if (threadIdx.x == 0) atomicMax(reinterpret_cast<int*>(out) + h, __float_as_int(m));
+    }
+}
+
+// vc f32 [H][W][64] (strided) -> fp16(vc * 2^-e_h) contiguous, e_h = vexp(vmax[h]) (the PV
+// MMA operand; the epilogue multiplies O by 2^e_h)
+__global__ void v16_kernel(const float* __restrict__ x, int64_t hs, int64_t rs, int heads, int W,
+                           const float* __restrict__ vmax, __half* out) {
+    const int64_t row = (int64_t)blockIdx.x * (blockDim.x / 8) + threadIdx.x / 8;
+    const int c = threadIdx.x & 7;
+    if (row >= (int64_t)heads * W) return;
+    const int h = (int)(row / W), w = (int)(row % W);
+    const int e = vexp(vmax[h]);
+    const float* src = x + (int64_t)h * hs + (int64_t)w * rs + 8 * c;
+    __half o8[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) o8[i] = __float2half_rn(ldexpf(src[i], -e));
+    *reinterpret_cast<uint4*>(out + row * 64 + 8 * c) = *reinterpret_cast<uint4*>(o8);
+}
+
 // per-head mean key kbar[h] = sum_w kc[h][w] / Wk (fixed summation order: deterministic).
 // Any fixed vector would do -- the scores are shifted by q.kbar per row, which changes
 // neither the softmax nor the ranking -- the mean makes |kc - kbar| small when the
@@ -1082,7 +1115,7 @@ __global__ void flag_scatter_kernel(const uint8_t* __restrict__ flag, int64_t ro
 }
 
 // ---------------------------------------------------------------------------------------
-// Large budgets (KCAP < k_eff <= LK_KMAX; the 2-5 % points of the budget sweep, SURVEY
+// Large budgets (KCAP < k_eff <= HK_KMAX; the 2-25 % points of the budget sweep, SURVEY
 // §8(f) #2). The streaming candidate lists of the main kernel would need ~k(1+ln(W/k))
 // entries per row, so the softmax kernel runs without top-k and this kernel selects
 // from EXACT scores: a CTA takes LK_ROWS query rows of one head, streams Kc tiles
@@ -1145,6 +1178,93 @@ __device__ __forceinline__ void lk_find_digit(const int* hist, int need, int lan
     }
 }
 
+// Budgets beyond the shared sort buffer (LK_KMAX < k_eff <= HK_KMAX: the 10 % and 25 %
+// points of the budget sweep, k = 4050 / 10125 at 500 views). Per row, from the row's
+// exact keys in the scratch: an 8-bit radix select of the k-th key T (4 passes; the
+// first histogram was accumulated while the keys were written), the winners (every key
+// > T, then the lowest-index keys == T) collected in index order by block scans, and a
+// block radix sort of their unique 64-bit keys (fkey(score) << 32 | ~index) descending
+// = topk_better order (compression.hpp:67-73). Shared memory: HK_SMEM past LK_SMEM.
+constexpr int HK_IPT = 40;                      // keys per thread of the block radix sort
+constexpr int HK_KMAX = LK_THREADS * HK_IPT;    // 10240
+static_assert(HK_KMAX == kMaxTopK, "tc.h kMaxTopK is the huge-k capacity");
+using HkSort = cub::BlockRadixSort<unsigned long long, LK_THREADS, HK_IPT>;
+using HkScan = cub::BlockScan<int, LK_THREADS>;
+constexpr size_t HK_WIN_BYTES = (size_t)HK_KMAX * 8;  // collected winners (64-bit keys)
+constexpr size_t HK_SMEM = (HK_WIN_BYTES > sizeof(typename HkSort::TempStorage) ? HK_WIN_BYTES
+                                                                                  : sizeof(typename HkSort::TempStorage)) +
+                           sizeof(typename HkScan::TempStorage) + 256;
+
+__device__ void hugek_row(const uint32_t* __restrict__ rk, int Wk, int k_eff, const int* row_hist, int64_t row,
+                          int32_t* topk, float* guide, uint8_t* hk, int* hist, int* sh) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    unsigned long long* win = reinterpret_cast<unsigned long long*>(hk);
+    typename HkSort::TempStorage& sort_tmp = *reinterpret_cast<typename HkSort::TempStorage*>(hk);  // aliases win
+    typename HkScan::TempStorage& scan_tmp =
+        *reinterpret_cast<typename HkScan::TempStorage*>(hk + (HK_SMEM - 256 - sizeof(typename HkScan::TempStorage)));
+    // 1. radix select of the k-th largest key
+    uint32_t prefix = 0;
+    int need = k_eff;
+    for (int pass = 0; pass < 4; ++pass) {
+        const int shift = 24 - 8 * pass;
+        __syncthreads();
+        if (pass == 0) {
+            for (int i = tid; i < 256; i += LK_THREADS) hist[i] = row_hist[i];
+        } else {
+            for (int i = tid; i < 256; i += LK_THREADS) hist[i] = 0;
+            __syncthreads();
+            for (int j = tid; j < Wk; j += LK_THREADS) {
+                const uint32_t key = rk[j];
+                if ((key >> (shift + 8)) == prefix) atomicAdd(&hist[(key >> shift) & 255u], 1);
+            }
+        }
+        __syncthreads();
+        if (warp == 0) lk_find_digit(hist, need, lane, &sh[0], &sh[1]);
+        __syncthreads();
+        prefix = (prefix << 8) | (uint32_t)sh[0];
+        need -= sh[1];
+    }
+    const uint32_t T = prefix;  // need = how many keys == T to take (lowest indices first)
+    // 2. winners in index order
+    int base = 0, eq_base = 0;
+    for (int j0 = 0; j0 < Wk; j0 += LK_THREADS) {
+        const int j = j0 + tid;
+        const uint32_t key = j < Wk ? rk[j] : 0u;
+        const int eq = (j < Wk && key == T) ? 1 : 0;
+        int eq_rank, eq_tot;
+        HkScan(scan_tmp).ExclusiveSum(eq, eq_rank, eq_tot);
+        __syncthreads();
+        const int take = (j < Wk && (key > T || (eq && eq_base + eq_rank < need))) ? 1 : 0;
+        int pos, tot;
+        HkScan(scan_tmp).ExclusiveSum(take, pos, tot);
+        __syncthreads();
+        if (take) win[base + pos] = ((unsigned long long)key << 32) | (0xffffffffu - (uint32_t)j);
+        base += tot;
+        eq_base += eq_tot;
+    }
+    __syncthreads();
+    // 3. sort descending (unique keys: no stability needed), write in rank order
+    unsigned long long keys[HK_IPT];
+#pragma unroll
+    for (int i = 0; i < HK_IPT; ++i) {
+        const int q = tid * HK_IPT + i;
+        keys[i] = q < k_eff ? win[q] : 0ull;
+    }
+    __syncthreads();  // the sort's temp storage aliases win
+    HkSort(sort_tmp).SortDescending(keys);
+#pragma unroll
+    for (int i = 0; i < HK_IPT; ++i) {
+        const int q = tid * HK_IPT + i;
+        if (q < k_eff) {
+            topk[row * k_eff + q] = (int32_t)(0xffffffffu - (uint32_t)(keys[i] & 0xffffffffu));
+            if (guide) guide[row * k_eff + q] = fkey_inv((uint32_t)(keys[i] >> 32));
+        }
+    }
+    __syncthreads();
+}
+
+#pragma nv_diag_suppress 128  // the HUGE instance leaves the k <= LK_KMAX row body unreachable
+template <bool HUGE>  // HUGE: k_eff > LK_KMAX (hugek_row); a separate instance keeps the common one's registers low
 __global__ void __launch_bounds__(LK_THREADS) largek_topk_kernel(
     const float* __restrict__ qc, int64_t q_hs, const float* __restrict__ kc, int heads, int Wq, int Wk, float scale,
     int k_eff, const uint32_t* __restrict__ exbits, uint32_t* scratch, int32_t* topk, float* guide,
@@ -1161,6 +1281,7 @@ __global__ void __launch_bounds__(LK_THREADS) largek_topk_kernel(
     __shared__ int sh_digit, sh_above, sh_cnt_gt, sh_eq_taken, sh_cl, sh_fast;
     __shared__ int warp_cnt[LK_THREADS / 32];
     __shared__ int row_id[LK_ROWS], row_h[LK_ROWS];
+    __shared__ int hk_sh[2];
     uint32_t* sk = scratch + (size_t)blockIdx.x * LK_ROWS * Wk;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int blocks_per_head = (Wq + LK_ROWS - 1) / LK_ROWS;
@@ -1256,6 +1377,10 @@ __global__ void __launch_bounds__(LK_THREADS) largek_topk_kernel(
 #endif
         for (int r = 0; r < nr; ++r) {
             const uint32_t* rk = sk + (size_t)r * Wk;
+            if constexpr (HUGE) {  // budgets past the shared sort buffer (the rest is the k <= LK_KMAX body)
+                hugek_row(rk, Wk, k_eff, rhist + r * 256, row_id[r], topk, guide, lk_smem + LK_SMEM, hist, hk_sh);
+                continue;
+            }
             // ---- fast path: digits 0 (fused histogram) and 1 (one scan); then ONE scan sends
             // the keys above the 16-bit prefix bin straight to the sort buffer and the bin's
             // keys to a shared list, where digits 2 and 3 are resolved
@@ -1451,8 +1576,9 @@ __global__ void __launch_bounds__(LK_THREADS) largek_topk_kernel(
 }
 
 struct Ws {
-    __nv_bfloat16 *qh, *ql, *kh, *kl, *vh, *vl;
-    float *qn, *kn, *kmax;
+    __nv_bfloat16 *qh, *ql, *kh, *kl;
+    __half* v16;
+    float *qn, *kn, *kmax, *vmax;
     float *cn, *cmax, *kbar, *kpart;
     uint32_t* exbits;
     float2* cand;
@@ -1478,8 +1604,8 @@ Ws carve_ws(void* base, int heads, int Wq, int Wk, int k_eff, bool dry) {
     w.ql = reinterpret_cast<__nv_bfloat16*>(take(nq * 128));
     w.kh = reinterpret_cast<__nv_bfloat16*>(take(nk * 128));
     w.kl = reinterpret_cast<__nv_bfloat16*>(take(nk * 128));
-    w.vh = reinterpret_cast<__nv_bfloat16*>(take(nk * 128));
-    w.vl = reinterpret_cast<__nv_bfloat16*>(take(nk * 128));
+    w.v16 = reinterpret_cast<__half*>(take(nk * 128));
+    w.vmax = reinterpret_cast<float*>(take((size_t)heads * 4));
     w.qn = reinterpret_cast<float*>(take(nq * 4));
     w.kn = reinterpret_cast<float*>(take(nk * 4));
     w.kmax = reinterpret_cast<float*>(take((size_t)heads * 4));
@@ -1511,16 +1637,16 @@ size_t tc_compress_workspace_bytes(int heads, int windows, int dim, int k_eff) {
 }
 
 size_t tc_compress_workspace_bytes_qk(int heads, int wq, int wk, int dim, int k_eff) {
-    if (dim != 64 || k_eff > LK_KMAX) return 0;
+    if (dim != 64 || k_eff > HK_KMAX) return 0;
     return carve_ws(nullptr, heads, wq, wk, k_eff, true).used;
 }
 
 bool tc_compress_split_buffers(void* ws, size_t ws_bytes, int heads, int windows, int dim, int k_eff,
                                CompressSplits* out) {
-    if (dim != 64 || k_eff > LK_KMAX || !ws || ws_bytes < carve_ws(nullptr, heads, windows, windows, k_eff, true).used)
+    if (dim != 64 || k_eff > HK_KMAX || !ws || ws_bytes < carve_ws(nullptr, heads, windows, windows, k_eff, true).used)
         return false;
     Ws w = carve_ws(ws, heads, windows, windows, k_eff, false);
-    *out = CompressSplits{w.qh, w.ql, w.kh, w.kl, w.vh, w.vl, w.qn, w.kn};
+    *out = CompressSplits{w.qh, w.ql, w.qn};
     return true;
 }
 
@@ -1553,34 +1679,38 @@ cudaError_t tc_compress_topk_splits(const CompressSplits* pre, const gsa_tensor&
     ex.guide = guide;
     ex.k_eff = k_eff;
     ex.excluded = excluded;
-    const bool tc_ok = qc.dim == 64 && k_eff <= LK_KMAX && contiguous_f32(qc) && contiguous_f32(kc) &&
+    const bool tc_ok = qc.dim == 64 && k_eff <= HK_KMAX && contiguous_f32(qc) && contiguous_f32(kc) &&
                        contiguous_f32(vc) && tmap_encode_fn() != nullptr && ws &&
                        ws_bytes >= carve_ws(nullptr, H, Wq, Wk, k_eff, true).used && Wq > 0 && Wk > 0;
     if (!tc_ok) return launch_attn_f32(ex, st);
 
     Ws w = carve_ws(ws, H, Wq, Wk, k_eff, false);
-    const __nv_bfloat16 *qh = w.qh, *ql = w.ql, *kh = w.kh, *kl = w.kl, *vh = w.vh, *vl = w.vl;
-    const float *qn = w.qn, *kn = w.kn;
-    if (pre) {
-        qh = pre->qh; ql = pre->ql; kh = pre->kh; kl = pre->kl; vh = pre->vh; vl = pre->vl;
-        qn = pre->qnorm; kn = pre->knorm;
+    const __nv_bfloat16 *qh = w.qh, *ql = w.ql, *kh = w.kh, *kl = w.kl;
+    const float* qn = w.qn;
+    if (pre) {  // Q splits + norms written by the pooling pass
+        qh = pre->qh;
+        ql = pre->ql;
+        qn = pre->qnorm;
     } else {
-        const unsigned qb = (unsigned)(((int64_t)H * Wq + 31) / 32), kb = (unsigned)(((int64_t)H * Wk + 31) / 32);
+        const unsigned qb = (unsigned)(((int64_t)H * Wq + 31) / 32);
         split_kernel<<<qb, 256, 0, st>>>(static_cast<const float*>(qc.data), qc.head_stride, qc.row_stride, H, Wq,
                                           w.qh, w.ql, w.qn);
-        split_kernel<<<kb, 256, 0, st>>>(static_cast<const float*>(vc.data), vc.head_stride, vc.row_stride, H, Wk,
-                                          w.vh, w.vl, nullptr);
-        note_launch(2);
+        note_launch();
     }
+    // V as the fp16 PV operand, scaled per head by a power of two into fp16 range
+    cudaMemsetAsync(w.vmax, 0, (size_t)H * 4, st);
+    absmax_kernel<<<dim3(32, H), 256, 0, st>>>(static_cast<const float*>(vc.data), vc.head_stride, vc.row_stride,
+                                               Wk, w.vmax);
+    v16_kernel<<<(unsigned)(((int64_t)H * Wk + 31) / 32), 256, 0, st>>>(
+        static_cast<const float*>(vc.data), vc.head_stride, vc.row_stride, H, Wk, w.vmax, w.v16);
+    note_launch(2);
     // centred keys for the scores (kc - kbar), written over the K splits
     kmean_partial_kernel<<<dim3(KMEAN_CHUNKS, H), 256, 0, st>>>(static_cast<const float*>(kc.data), kc.head_stride,
                                                                  kc.row_stride, Wk, w.kpart);
     kmean_final_kernel<<<H, 64, 0, st>>>(w.kpart, Wk, w.kbar);
     center_split_kernel<<<(unsigned)(((int64_t)H * Wk + 31) / 32), 256, 0, st>>>(
         static_cast<const float*>(kc.data), kc.head_stride, kc.row_stride, H, Wk, w.kbar, w.kh, w.kl, w.cn, w.kn);
-    kh = w.kh;
-    kl = w.kl;
-    kn = w.kn;
+    const float* kn = w.kn;
     cudaMemsetAsync(w.kmax, 0, (size_t)H * 4, st);
     cudaMemsetAsync(w.cmax, 0, (size_t)H * 4, st);
     rowmax_kernel<<<dim3(32, H), 256, 0, st>>>(kn, Wk, w.kmax);
@@ -1591,11 +1721,12 @@ cudaError_t tc_compress_topk_splits(const CompressSplits* pre, const gsa_tensor&
         exbits_kernel<<<(tiles * 4 + 127) / 128, 128, 0, st>>>(excluded, Wk, tiles * 4, w.exbits);
         note_launch();
     }
-    CUtensorMap tqh, tql, tkh, tkl, tvh, tvl;
+    CUtensorMap tqh, tql, tkh, tkl, tv16;
     const int64_t qhs = (int64_t)Wq * 64, khs = (int64_t)Wk * 64;
+    // (2-byte elements: the bf16 tensor-map type moves the fp16 V tile bit for bit)
     if (!make_rows_tmap(&tqh, qh, H, Wq, qhs, 64) || !make_rows_tmap(&tql, ql, H, Wq, qhs, 64) ||
         !make_rows_tmap(&tkh, kh, H, Wk, khs, 64) || !make_rows_tmap(&tkl, kl, H, Wk, khs, 64) ||
-        !make_rows_tmap(&tvh, vh, H, Wk, khs, 64) || !make_rows_tmap(&tvl, vl, H, Wk, khs, 64))
+        !make_rows_tmap(&tv16, reinterpret_cast<const __nv_bfloat16*>(w.v16), H, Wk, khs, 64))
         return launch_attn_f32(ex, st);
     CompParams p{};
     p.heads = H;
@@ -1611,6 +1742,7 @@ cudaError_t tc_compress_topk_splits(const CompressSplits* pre, const gsa_tensor&
     p.kbar = w.kbar;
     p.qc = static_cast<const float*>(qc.data);
     p.qc_hs = qc.head_stride;
+    p.vmax = w.vmax;
     p.exbits = excluded ? w.exbits : nullptr;
     p.out = out;
     p.out_hs = out_hs;
@@ -1628,7 +1760,7 @@ cudaError_t tc_compress_topk_splits(const CompressSplits* pre, const gsa_tensor&
     const size_t smem = sizeof(CompSmem) + 1024;
     cudaError_t e = cudaFuncSetAttribute(compress_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    compress_tc_kernel<<<dim3((Wq + 128 * NWG - 1) / (128 * NWG), H), NTHREADS, smem, st>>>(tqh, tql, tkh, tkl, tvh, tvl, p);
+    compress_tc_kernel<<<dim3((Wq + 128 * NWG - 1) / (128 * NWG), H), NTHREADS, smem, st>>>(tqh, tql, tkh, tkl, tv16, p);
     note_launch();
 #ifdef COMPRESS_PROF
     {
@@ -1648,13 +1780,15 @@ cudaError_t tc_compress_topk_splits(const CompressSplits* pre, const gsa_tensor&
     }
 #endif
     if (k_eff > KCAP) {
-        const size_t lk_smem = LK_SMEM;
-        cudaError_t e2 = cudaFuncSetAttribute(largek_topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lk_smem);
+        const bool huge = k_eff > LK_KMAX;
+        const size_t lk_smem = LK_SMEM + (huge ? HK_SMEM : 0);
+        auto kern = huge ? largek_topk_kernel<true> : largek_topk_kernel<false>;
+        cudaError_t e2 = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lk_smem);
         if (e2 != cudaSuccess) return e2;
-        largek_topk_kernel<<<LK_CTAS, LK_THREADS, lk_smem, st>>>(static_cast<const float*>(qc.data), qc.head_stride,
-                                                                  static_cast<const float*>(kc.data), H, Wq, Wk, scale,
-                                                                  k_eff, excluded ? w.exbits : nullptr, w.scratch, topk,
-                                                                  guide);
+        kern<<<LK_CTAS, LK_THREADS, lk_smem, st>>>(static_cast<const float*>(qc.data), qc.head_stride,
+                                                    static_cast<const float*>(kc.data), H, Wq, Wk, scale, k_eff,
+                                                    excluded ? w.exbits : nullptr, w.scratch, topk, guide, nullptr,
+                                                    nullptr);
         note_launch();
         return cudaGetLastError();
     }
@@ -1689,9 +1823,9 @@ cudaError_t tc_compress_topk_splits(const CompressSplits* pre, const gsa_tensor&
         flag_scan_kernel<<<1, 1024, 0, st>>>(fl_counts, (int)nfb, w.nblocks);
         flag_scatter_kernel<<<nfb, FL_BLOCK, 0, st>>>(w.flag, rows, fl_counts, w.blocks);
         const size_t lk_smem = LK_SMEM;
-        cudaError_t e3 = cudaFuncSetAttribute(largek_topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lk_smem);
+        cudaError_t e3 = cudaFuncSetAttribute(largek_topk_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lk_smem);
         if (e3 != cudaSuccess) return e3;
-        largek_topk_kernel<<<LK_CTAS, LK_THREADS, lk_smem, st>>>(static_cast<const float*>(qc.data), qc.head_stride,
+        largek_topk_kernel<false><<<LK_CTAS, LK_THREADS, lk_smem, st>>>(static_cast<const float*>(qc.data), qc.head_stride,
                                                                   static_cast<const float*>(kc.data), H, Wq, Wk, scale,
                                                                   k_eff, excluded ? w.exbits : nullptr, w.scratch, topk,
                                                                   guide, w.blocks, w.nblocks);

@@ -7,6 +7,11 @@
 
 namespace gsa_sm100 {
 
+// the largest per-row top-k budget (k_eff) the selection implements: up to 128 on the
+// tensor-core streaming path, up to 2048 with a shared sort buffer, up to 10240 with a
+// block radix sort (compress_tc.cu, HK_KMAX)
+constexpr int kMaxTopK = 10240;
+
 // dense attention (special tokens, tiled_attention, dense baseline)
 bool tc_dense_supported(const gsa_tensor& q, const gsa_tensor& k, const gsa_tensor& v);
 size_t tc_dense_workspace_bytes(int heads, int mq, int mk);
@@ -20,11 +25,11 @@ cudaError_t tc_dense_attention(const gsa_tensor& q, const gsa_tensor& k, const g
 size_t tc_compress_workspace_bytes(int heads, int windows, int dim, int k_eff);
 // query rows wq (a shard's windows) against wk key windows
 size_t tc_compress_workspace_bytes_qk(int heads, int wq, int wk, int dim, int k_eff);
-// pre-split operands (bf16 hi/lo of contiguous [H][W][64] Qc/Kc/Vc + row norms),
-// e.g. written by the pooling kernel; carved from the compress workspace
+// pre-split query operands (bf16 hi/lo of contiguous [H][W][64] Qc + row norms), written
+// by the pooling kernel; carved from the compress workspace
 struct CompressSplits {
-    __nv_bfloat16 *qh, *ql, *kh, *kl, *vh, *vl;
-    float *qnorm, *knorm;
+    __nv_bfloat16 *qh, *ql;
+    float* qnorm;
 };
 bool tc_compress_split_buffers(void* ws, size_t ws_bytes, int heads, int windows, int dim, int k_eff,
                                CompressSplits* out);

@@ -5,6 +5,7 @@
 
 #include <cuda.h>
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <stdint.h>
 #include <cstdio>
 
@@ -260,6 +261,12 @@ __device__ __forceinline__ uint64_t umma_desc(uint32_t smem_addr, uint32_t lbo_b
 
 // Instruction descriptor, kind::f16 with bf16 A/B and f32 D.
 // a_mn / b_mn: 1 = MN-major operand (transposed), 0 = K-major.
+// Instruction descriptor, kind::f16 with fp16 A/B (format 0) and f32 D.
+__host__ __device__ constexpr uint32_t idesc_f16(int M, int N, int a_mn, int b_mn) {
+    return (1u << 4)  // D format f32
+           | ((uint32_t)a_mn << 15) | ((uint32_t)b_mn << 16) | ((uint32_t)(N >> 3) << 17) |
+           ((uint32_t)(M >> 4) << 24);
+}
 __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N, int a_mn, int b_mn) {
     return (1u << 4)                      // D format f32
            | (1u << 7)                    // A bf16
@@ -270,6 +277,11 @@ __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N, int a_mn, int b_
 
 __device__ __forceinline__ uint32_t pack_bf16(float lo_elem, float hi_elem) {
     __nv_bfloat162 v = __floats2bfloat162_rn(lo_elem, hi_elem);  // .x = lo_elem (low 16 bits)
+    return *reinterpret_cast<uint32_t*>(&v);
+}
+
+__device__ __forceinline__ uint32_t pack_f16(float lo_elem, float hi_elem) {
+    __half2 v = __floats2half2_rn(lo_elem, hi_elem);  // .x = lo_elem (low 16 bits), RN
     return *reinterpret_cast<uint32_t*>(&v);
 }
 

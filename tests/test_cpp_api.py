@@ -78,8 +78,9 @@ def test_cpp_api_matches_reference(tmp_path, ref, lt, heads, model_dim, top_k, v
     rf = ref.forward(q, k, v, d["w_g"], lt, top_k=top_k, variant=variant, ref_stride=2)
     np.testing.assert_array_equal(d["topk"], rf["topk"])
     np.testing.assert_array_equal(d["qc"].view(np.uint32), rf["qc"].view(np.uint32))
-    assert np.abs(d["out"] - rf["out"]).max() < 1e-4 and rel_l2(d["out"], rf["out"]) < 1e-5
-    assert np.abs(d["o_comp"] - rf["o_comp"]).max() < 1e-5
+    # regression bounds inside the north star: O'_comp carries the fp16 P.V error
+    assert np.abs(d["out"] - rf["out"]).max() < 1e-3 and rel_l2(d["out"], rf["out"]) < 2e-4
+    assert rel_l2(d["o_comp"], rf["o_comp"]) < 1e-3
     assert np.abs(d["gate"] - rf["gate"]).max() < 1e-5
     assert np.abs(d["o_sel"] - rf["o_sel"]).max() < 1e-4
     offs, ids = ref.plan(rf["topk"], lt, variant, 2)
@@ -101,7 +102,7 @@ def test_cpp_api_matches_reference(tmp_path, ref, lt, heads, model_dim, top_k, v
     oc, _, idx, guide = ref.compress(rf["qc"], rf["kc"], rf["vc"], top_k, scale, excluded=ex, guide=True)
     np.testing.assert_array_equal(d["op_topk"], idx)
     np.testing.assert_array_equal(d["op_guide"], guide.reshape(-1).astype(np.float32))
-    assert np.abs(d["op_o_comp"] - oc).max() < 1e-5
+    assert rel_l2(d["op_o_comp"], oc) < 1e-3
     np.testing.assert_array_equal(d["op_plan_ids"], ids)
     osel, _ = ref.block_sparse(q[:, Ms:], k[:, Ms:], v[:, Ms:], lt, offs, ids, scale)
     assert np.abs(d["op_o_sel"] - osel).max() < 1e-4
@@ -111,5 +112,5 @@ def test_cpp_api_matches_reference(tmp_path, ref, lt, heads, model_dim, top_k, v
         ospec, _ = ref.tiled_attention(q[:, :Ms], k, v, scale)
         assert np.abs(d["op_o_spec"] - ospec).max() < 1e-4
     # pinned plan = the plan gsa_forward realised: compressed branch without top-k
-    assert np.abs(d["op_out_with_plan"] - rf["out"]).max() < 1e-4
+    assert np.abs(d["op_out_with_plan"] - rf["out"]).max() < 1e-3
     assert Mi > 0

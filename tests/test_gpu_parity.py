@@ -20,6 +20,10 @@ torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
 MAX_ABS, REL_L2 = 2e-2, 1e-3  # north_star tolerance for the layer output
+# regression bounds, 5-20x inside the north star (DESIGN.md §2 error budget): the layer
+# output (O'_comp's fp16 P.V error enters through the gate) and the compressed branch
+LAYER_ABS, LAYER_REL = 1e-3, 2e-4
+COMP_ABS, COMP_REL = 2e-3, 1e-3
 
 
 @pytest.fixture(scope="module")
@@ -80,8 +84,9 @@ def test_compress_topk_exact(gsa, orc, W, k, excl):
     assert r.k == i_ref.shape[2]
     np.testing.assert_array_equal(host(r.indices).astype(np.int32), i_ref)
     np.testing.assert_array_equal(host(r.guide_scores).reshape(-1), g_ref.reshape(-1))
-    # the tensor-core path splits f32 operands into bf16 hi+lo: relative error <= ~2^-16
-    assert np.abs(host(r.out) - o_ref).max() < 1e-4
+    # scores: bf16 hi+lo split of the f32 operands (~2^-16 relative): lse to 1e-4; P.V with P
+    # and V in fp16 (~2^-11 relative per element): O'_comp to COMP_REL
+    assert rel_l2(host(r.out), o_ref) < COMP_REL and np.abs(host(r.out) - o_ref).max() < COMP_ABS
     assert np.abs(host(r.lse) - l_ref).max() < 1e-4
 
 
@@ -110,7 +115,7 @@ def test_compress_topk_tc_adversarial(gsa, orc, kind, W, k):
                                             k, 0.125, keep_guide_scores=True)
     np.testing.assert_array_equal(host(r.indices).astype(np.int32), i_ref)
     np.testing.assert_array_equal(host(r.guide_scores), g_ref.reshape(host(r.guide_scores).shape))
-    assert rel_l2(host(r.out), o_ref) < 1e-4
+    assert rel_l2(host(r.out), o_ref) < COMP_REL
     # lse grows with the logit scale (x6 inputs: |lse| ~ 1e2): compare relatively
     assert (np.abs(host(r.lse) - l_ref) / np.maximum(1.0, np.abs(l_ref))).max() < 1e-4
 
@@ -153,7 +158,7 @@ def test_compress_large_k_exact(gsa, orc, kind, W, k, excl):
                                             keep_guide_scores=True)
     np.testing.assert_array_equal(host(r.indices).astype(np.int32), i_ref)
     np.testing.assert_array_equal(host(r.guide_scores), g_ref.reshape(host(r.guide_scores).shape))
-    assert rel_l2(host(r.out), o_ref) < 1e-4
+    assert rel_l2(host(r.out), o_ref) < COMP_REL
 
 
 @pytest.mark.parametrize("variant,k", [(0, 256), (1, 300)])
@@ -171,7 +176,7 @@ def test_layer_large_k_matches_reference(gsa, ref, variant, k):
     rf = ref.forward(f(q), f(k_), f(v), f(wg), lt, top_k=k, variant=variant, ref_stride=4)
     np.testing.assert_array_equal(ctx.topk.cpu().numpy(), rf["topk"])
     o = host(out)
-    assert np.abs(o - rf["out"]).max() < 1e-4 and rel_l2(o, rf["out"]) < 1e-5
+    assert np.abs(o - rf["out"]).max() < LAYER_ABS and rel_l2(o, rf["out"]) < LAYER_REL
 
 
 def test_compress_all_ties(gsa, orc):
@@ -299,7 +304,7 @@ def test_forward_f32_inputs_tight(gsa, orc):
     r = orc.gsa_forward(q, k, v, wg, L, top_k=7)
     out, ctx = run_forward(gsa, q, k, v, wg, lt, 7, dtype=torch.float32)
     np.testing.assert_array_equal(host(ctx.topk).astype(np.int32), r["topk"])
-    assert rel_l2(out, r["out"]) < 1e-5
+    assert rel_l2(out, r["out"]) < LAYER_REL
 
 
 @pytest.mark.parametrize("case", ["v8_normal", "v8_sharp", "v8_hybrid", "v8_uniform"])
@@ -329,7 +334,7 @@ def test_dense_degeneration(gsa, orc):
     wg = (rng.standard_normal((2, 64, 64)) / 8).astype(np.float32)
     out, _ = run_forward(gsa, q, k, v, wg, lt, L.num_windows)
     dense, _ = orc.dense_attention(q, k, v, 0.125)
-    assert np.abs(out - dense).max() < 1e-4
+    assert np.abs(out - dense).max() < LAYER_ABS
 
 
 def test_determinism_and_scale_invariance(gsa, orc):
@@ -351,7 +356,7 @@ def test_forward_with_plan(gsa, orc):
     plan = gsa.build_selection_plan(dev(g["topk"], torch.int32), L, 0, 100)
     out = gsa.gsa_forward_with_plan(dev(g["q"]), dev(g["k"]), dev(g["v"]), dev(g["w_g"], torch.float32), L,
                                     gsa.GsaParams(window_s=lt[4], top_k=g["top_k"]), plan)
-    assert rel_l2(host(out), g["out"]) < 1e-4
+    assert rel_l2(host(out), g["out"]) < LAYER_REL
 
 
 @pytest.mark.parametrize("heads,k", [(4, 8), (4, 16), (16, 16), (2, 16), (4, 24)])
@@ -366,8 +371,8 @@ def test_forward_small_k_many_items_per_cta(gsa, orc, heads, k):
     ref = orc.gsa_forward(q, k_, v, wg, L, top_k=k)
     out, ctx = run_forward(gsa, q, k_, v, wg, lt, k)
     np.testing.assert_array_equal(ctx.topk.cpu().numpy(), ref["topk"])
-    assert np.abs(out - ref["out"]).max() < 1e-4
-    assert rel_l2(out, ref["out"]) < 1e-5
+    assert np.abs(out - ref["out"]).max() < LAYER_ABS
+    assert rel_l2(out, ref["out"]) < LAYER_REL
 
 
 @pytest.mark.parametrize("tokens,C,H", [(130, 1024, 2), (1000, 96, 3), (7, 33, 1)])
@@ -434,7 +439,7 @@ def test_compress_topk_tc_large_k(gsa, orc, kind, W, k):
                                             k, 0.125, keep_guide_scores=True)
     np.testing.assert_array_equal(host(r.indices).astype(np.int32), i_ref)
     np.testing.assert_array_equal(host(r.guide_scores), g_ref.reshape(host(r.guide_scores).shape))
-    assert rel_l2(host(r.out), o_ref) < 1e-4
+    assert rel_l2(host(r.out), o_ref) < COMP_REL
 
 
 @pytest.mark.parametrize("lt,ref_stride,k", [((10, 12, 16, 16, 4), 4, 6), ((40, 9, 36, 36, 4), 3, 32),
@@ -450,7 +455,7 @@ def test_hybrid_fast_path_matches_reference(gsa, ref, lt, ref_stride, k):
     rf = ref.forward(q, k_, v, wg, lt, top_k=k, variant=1, ref_stride=ref_stride)
     out, ctx = run_forward(gsa, q, k_, v, wg, lt, k, variant=1, ref_stride=ref_stride)
     np.testing.assert_array_equal(ctx.topk.cpu().numpy(), rf["topk"])
-    assert np.abs(out - rf["out"]).max() < 1e-4 and rel_l2(out, rf["out"]) < 1e-5
+    assert np.abs(out - rf["out"]).max() < LAYER_ABS and rel_l2(out, rf["out"]) < LAYER_REL
     assert np.abs(host(ctx.o_sel) - rf["o_sel"]).max() < 1e-4
     assert np.abs(host(ctx.lse_sel) - rf["lse_sel"]).max() < 1e-4
 
@@ -476,7 +481,7 @@ def test_oversmoothed_keys_bitexact(gsa, ref, eps):
     rf = ref.forward(f(q), f(k), f(v), f(wg), lt, top_k=32, variant=0, ref_stride=2)
     np.testing.assert_array_equal(ctx.topk.cpu().numpy(), rf["topk"])
     o = host(out)
-    assert np.abs(o - rf["out"]).max() < 1e-4 and rel_l2(o, rf["out"]) < 1e-5
+    assert np.abs(o - rf["out"]).max() < LAYER_ABS and rel_l2(o, rf["out"]) < LAYER_REL
     if "lse_comp" in rf:
         assert np.abs(host(ctx.lse_comp) - rf["lse_comp"]).max() < 1e-4
 
@@ -504,7 +509,7 @@ def test_clustered_views_bitexact(gsa, ref):
     rf = ref.forward(f(q), f(k), f(v), f(wg), lt, top_k=32, variant=0, ref_stride=2)
     np.testing.assert_array_equal(ctx.topk.cpu().numpy(), rf["topk"])
     o = host(out)
-    assert np.abs(o - rf["out"]).max() < 1e-4 and rel_l2(o, rf["out"]) < 1e-5
+    assert np.abs(o - rf["out"]).max() < LAYER_ABS and rel_l2(o, rf["out"]) < LAYER_REL
 
 
 def test_plan_validation_errors(gsa):
