@@ -192,7 +192,7 @@ def run_reference_arm(args):
 # ------------------------------------------------------------- GPU arm
 def run_stack(args):
     """BASELINE configs[2] on one GPU: an L-layer global-attention stack. One step
-    = L x (X . W_qkv on cuBLAS bf16 -> GSA layer on strided head views -> head
+    = L x (X . W_qkv on the library tcgen05 GEMM -> GSA layer on strided head views -> head
     concat to bf16 X), paper_2603_08055_b200.stack. Stage times and the roofline
     come from layer 0 of each timed step (library CUDA events)."""
     import ctypes
@@ -251,7 +251,7 @@ def run_stack(args):
         "dtype": "bf16", "data": "synthetic (torch N(0,1) bf16 X, random-init N(0,1/C) bf16 W_qkv, W_g=N(0,1)/8 f32)",
         "config": {"workload": f"{args.layers}-layer GSA stack, {args.views} views x ({SPECIAL_PER_VIEW} specials + "
                                f"{GRID_H}x{GRID_W} patches) = {M} tokens, 16 heads x 64, s=4, top-{TOPK}; per layer "
-                               "QKV GEMM (cuBLAS bf16) + GSA layer + residual", "views": args.views, "layers": args.layers,
+                               "QKV GEMM (tcgen05, gsa_project_qkv_bf16) + GSA layer + residual (gsa_residual_bf16)", "views": args.views, "layers": args.layers,
                    "tokens": M, "parallelism": "1 GPU", "l2": "inputs larger than L2 (no flush)"},
         "ms_per_layer": ms / args.layers,
         "stage_ms_layer0": {k_: round(v_, 3) for k_, v_ in stage_ms.items()},

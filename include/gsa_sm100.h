@@ -281,6 +281,18 @@ int gsa_project_qkv(const float* x, int tokens, int model_dim, const float* w_q,
                     const float* w_v, int heads, int dim, const gsa_tensor* q, const gsa_tensor* k,
                     const gsa_tensor* v, gsa_stream_t stream);
 
+/* The L-layer stack driver's per-layer maps (BASELINE configs[2]), on
+ * tensor cores. gsa_project_qkv_bf16: qkv[t][n] = sum_a x[t][a] * W[a][n] with bf16
+ * x [tokens][model_dim] (row stride ldx), the weight given TRANSPOSED w_qkv_t
+ * [n_out][model_dim] (K-major, stored once per layer), f32 accumulation, bf16 qkv
+ * [tokens][n_out] (row stride ld_qkv) -- e.g. n_out = 3 * heads * dim for a fused
+ * [Q | K | V] projection whose head views feed gsa_forward as strided tensors.
+ * n_out % 256 == 0, model_dim % 64 == 0. gsa_residual_bf16: y = bf16(x + o) over n
+ * elements (x, y bf16; o f32), the residual connection between stacked layers. */
+int gsa_project_qkv_bf16(const void* x, int tokens, int model_dim, int64_t ldx, const void* w_qkv_t, int n_out,
+                         void* qkv, int64_t ld_qkv, gsa_stream_t stream);
+int gsa_residual_bf16(const void* x, const float* o, void* y, int64_t n, gsa_stream_t stream);
+
 /* KernelStats (types.hpp:78-86) in closed form for a gsa_forward call:
  * scores_computed = H*(Ms*M + W*W); keys_attended = sum over rows of
  * |row| * s^2 * s^2 (rows have width F + k_eff). */

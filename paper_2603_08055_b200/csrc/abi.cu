@@ -1008,6 +1008,33 @@ int gsa_shard_attend(const gsa_tensor* q_own, const gsa_tensor* k_all, const gsa
     return GSA_OK;
 }
 
+int gsa_project_qkv_bf16(const void* x, int tokens, int model_dim, int64_t ldx, const void* w_qkv_t,
+                         int n_out, void* qkv, int64_t ld_qkv, gsa_stream_t stream) {
+    // the stack driver's projection on tensor cores (X . W_qkv with W_qkv stored transposed)
+    if (!x || !w_qkv_t || !qkv) return fail(GSA_ERR_GENERIC, "project_qkv_bf16: null pointer");
+    if (tokens < 0 || model_dim < 1 || n_out < 1) return fail(GSA_ERR_ZERO_SIZE, "project_qkv_bf16: empty shape");
+    if (tokens == 0) return GSA_OK;
+    if (!tc_gemm_supported(tokens, n_out, model_dim) || ldx % 8 || ld_qkv % 8 ||
+        (reinterpret_cast<uintptr_t>(x) & 15) || (reinterpret_cast<uintptr_t>(w_qkv_t) & 15) ||
+        (reinterpret_cast<uintptr_t>(qkv) & 15))
+        return fail(GSA_ERR_UNSUPPORTED, "project_qkv_bf16: needs n_out %% 256 == 0, model_dim %% 64 == 0, 16-byte "
+                    "aligned rows");
+    GSA_CUDA(tc_gemm_bf16(static_cast<const __nv_bfloat16*>(x), ldx, static_cast<const __nv_bfloat16*>(w_qkv_t),
+                          model_dim, static_cast<__nv_bfloat16*>(qkv), ld_qkv, tokens, n_out, model_dim,
+                          (cudaStream_t)stream));
+    return GSA_OK;
+}
+
+int gsa_residual_bf16(const void* x, const float* o, void* y, int64_t n, gsa_stream_t stream) {
+    if (n < 0 || (n && (!x || !o || !y))) return fail(GSA_ERR_GENERIC, "residual_bf16: null pointer");
+    if (n % 8 || (reinterpret_cast<uintptr_t>(x) & 15) || (reinterpret_cast<uintptr_t>(o) & 15) ||
+        (reinterpret_cast<uintptr_t>(y) & 15))
+        return fail(GSA_ERR_UNSUPPORTED, "residual_bf16: n %% 8 == 0 and 16-byte aligned buffers");
+    GSA_CUDA(launch_residual_bf16(static_cast<const __nv_bfloat16*>(x), o, static_cast<__nv_bfloat16*>(y), n,
+                                  (cudaStream_t)stream));
+    return GSA_OK;
+}
+
 int gsa_project_qkv(const float* x, int tokens, int model_dim, const float* w_q, const float* w_k,
                     const float* w_v, int heads, int dim, const gsa_tensor* q, const gsa_tensor* k,
                     const gsa_tensor* v, gsa_stream_t stream) {

@@ -47,4 +47,11 @@ bool tc_select_supported(const SelectArgs& a);
 size_t tc_select_workspace_bytes(int heads);
 cudaError_t tc_select_gate_merge(const SelectArgs& a, cudaStream_t st);
 
+// dense projection of the stack driver: C[M][N] bf16 = A[M][K] . Bt[N][K]^T (gemm.cu);
+// N % 256 == 0, K % 64 == 0; and the stack's residual y = bf16(x + o)
+bool tc_gemm_supported(int M, int N, int K);
+cudaError_t tc_gemm_bf16(const __nv_bfloat16* a, int64_t lda, const __nv_bfloat16* bt, int64_t ldb, __nv_bfloat16* c,
+                         int64_t ldc, int M, int N, int K, cudaStream_t st);
+cudaError_t launch_residual_bf16(const __nv_bfloat16* x, const float* o, __nv_bfloat16* y, int64_t n, cudaStream_t st);
+
 }  // namespace gsa_sm100

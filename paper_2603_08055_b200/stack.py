@@ -14,19 +14,23 @@ Per layer (the reference's layer contract, layer.hpp:48-76 and 177-230):
           compressed scores collapse into near-ties and the exact top-k fallback
           takes over (measured: a 24-layer stack without residual did not finish)
 
-The projection is a plain dense GEMM and runs on cuBLAS (bf16 in, f32
-accumulate, bf16 out); parity is defined at the post-projection boundary
-(SURVEY §8(c)): the layer tests compare the GSA layer against the reference
-on the same bf16 Q/K/V, and the exact f32 `project_qkv` (layer.hpp:48-76)
-remains available for bit-parity of the projection itself.
+The projection runs on the library's tcgen05 GEMM (gsa_project_qkv_bf16: bf16
+in, f32 accumulate in TMEM, bf16 out; W_qkv stored transposed once per layer)
+and the residual on gsa_residual_bf16, so a stacked forward launches only this
+library's kernels. Parity is defined at the post-projection boundary (SURVEY
+§8(c)): the layer tests compare the GSA layer against the reference on the same
+bf16 Q/K/V, and the exact f32 `project_qkv` (layer.hpp:48-76) remains available
+for bit-parity of the projection itself.
 """
 from __future__ import annotations
 
+import ctypes as C
 from typing import Optional
 
 import torch
 
-from .gsa import GsaParams, TokenLayout, Workspace, gsa_forward
+from . import _lib
+from .gsa import GsaParams, TokenLayout, Workspace, _check, _stream, gsa_forward
 
 
 class GsaStack:
@@ -42,8 +46,12 @@ class GsaStack:
             (torch.randn(C, 3 * C, generator=gen, device=device) / C ** 0.5).to(torch.bfloat16) for _ in range(layers)]
         self.w_g = w_g if w_g is not None else [
             torch.randn(heads, dim, dim, generator=gen, device=device) / 8.0 for _ in range(layers)]
+        # K-major copies for the tensor-core GEMM (static weights: transposed once)
+        self.w_qkv_t = [w.t().contiguous() for w in self.w_qkv]
         self.ws = Workspace()
         self._out = None
+        self._qkv = None
+        self._lib = _lib.load()
 
     def heads_of(self, qkv: torch.Tensor):
         """[M, 3C] -> three [H, M, d] strided views (head stride d, row stride 3C)."""
@@ -51,17 +59,33 @@ class GsaStack:
         v = qkv.view(M, 3, self.heads, self.dim)
         return tuple(v[:, i].permute(1, 0, 2) for i in range(3))
 
+    def project(self, x: torch.Tensor, l: int, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+        """x [M, C] bf16 -> X . W_qkv[l] [M, 3C] bf16 (tcgen05 GEMM, f32 accumulation)."""
+        M, Cm = x.shape
+        if out is None:
+            out = torch.empty(M, 3 * Cm, dtype=torch.bfloat16, device=x.device)
+        _check(self._lib.gsa_project_qkv_bf16(C.c_void_p(x.data_ptr()), M, Cm, x.stride(0),
+                                              C.c_void_p(self.w_qkv_t[l].data_ptr()), 3 * Cm,
+                                              C.c_void_p(out.data_ptr()), out.stride(0), _stream()))
+        return out
+
+    def residual(self, x: torch.Tensor, o: torch.Tensor) -> torch.Tensor:
+        """bf16(x + o): x [M, C] bf16, o [M, C] f32."""
+        y = torch.empty_like(x)
+        _check(self._lib.gsa_residual_bf16(C.c_void_p(x.data_ptr()), C.c_void_p(o.data_ptr()),
+                                           C.c_void_p(y.data_ptr()), x.numel(), _stream()))
+        return y
+
     def layer(self, x: torch.Tensor, l: int) -> torch.Tensor:
         M = x.shape[0]
         if self._out is None or self._out.shape[0] != M or self._out.device != x.device:
             self._out = torch.empty(M, self.heads, self.dim, device=x.device)
-        qkv = x @ self.w_qkv[l]
+            self._qkv = torch.empty(M, 3 * self.model_dim, dtype=torch.bfloat16, device=x.device)
+        qkv = self.project(x, l, self._qkv)
         q, k, v = self.heads_of(qkv)
         gsa_forward(q, k, v, self.w_g[l], self.layout, self.params, out=self._out.permute(1, 0, 2),
                     workspace=self.ws)
-        o = self._out.view(M, self.model_dim)
-        o.add_(x)  # residual in f32, in place (no f32 copy of X)
-        return o.to(torch.bfloat16)
+        return self.residual(x, self._out.view(M, self.model_dim))
 
     def forward(self, x: torch.Tensor) -> torch.Tensor:
         """x [M, C] bf16 -> X_L [M, C] bf16."""

@@ -120,12 +120,47 @@ def test_compress_topk_tc_adversarial(gsa, orc, kind, W, k):
     assert (np.abs(host(r.lse) - l_ref) / np.maximum(1.0, np.abs(l_ref))).max() < 1e-4
 
 
-def test_compress_k_beyond_2048_is_reported_unsupported(gsa):
-    # budgets beyond 2048 windows per row (the 10-25 % sweep points) are not implemented:
-    # they must fail loudly, never silently truncate
-    x = torch.zeros(1, 3000, 64, device="cuda")
+def test_compress_k_beyond_10240_is_reported_unsupported(gsa):
+    # budgets beyond the largest per-row sort (kMaxTopK = 10240) must fail loudly, never
+    # silently truncate
+    x = torch.zeros(1, 10300, 64, device="cuda")
     with pytest.raises(gsa.Unsupported):
-        gsa.fused_compressed_attention_topk(x, x, x, 2100, 0.125)
+        gsa.fused_compressed_attention_topk(x, x, x, 10241, 0.125)
+
+
+@pytest.mark.parametrize("kind,W,k,excl", [("normal", 6000, 2500, False), ("pooled_bf16", 6480, 4050, False),
+                                           ("ties", 3000, 2049, False), ("normal", 5000, 5000, True),
+                                           ("sharp", 10300, 10240, False)])
+def test_compress_huge_k_exact(gsa, orc, kind, W, k, excl):
+    """k in (2048, 10240] (the 10 % / 25 % budget-sweep points): exact scores,
+    radix select, winners collected in index order and block-radix-sorted by (score desc,
+    index asc) -- indices and guide scores bit-exact, incl. mass ties, k == selectable and
+    exclusion."""
+    rng = np.random.default_rng(W + k)
+    H = 1
+    if kind == "ties":
+        qc, kc, vc = (rng.integers(-2, 3, size=(H, W, 64)).astype(np.float32) for _ in range(3))
+    elif kind == "sharp":
+        qc, kc, vc = (rng.standard_normal((H, W, 64)).astype(np.float32) * 4 for _ in range(3))
+    elif kind == "pooled_bf16":
+        L = Layout(0, W // 81, 36, 36, 4)
+        W = L.num_windows
+        x = [orc.bf16_round(rng.standard_normal((H, L.image_tokens, 64)).astype(np.float32)) for _ in range(3)]
+        qc, kc, vc = (orc.pool(t, L) for t in x)
+    else:
+        qc, kc, vc = (rng.standard_normal((H, W, 64)).astype(np.float32) for _ in range(3))
+    ex = None
+    if excl:
+        ex = np.zeros(W, np.uint8)
+        ex[rng.choice(W, W // 5, replace=False)] = 1
+    o_ref, l_ref, i_ref, g_ref = orc.compress_topk(qc, kc, vc, k, 0.125, excluded=ex, guide=True)
+    r = gsa.fused_compressed_attention_topk(dev(qc, torch.float32), dev(kc, torch.float32), dev(vc, torch.float32),
+                                            k, 0.125, excluded=None if ex is None else torch.from_numpy(ex).cuda(),
+                                            keep_guide_scores=True)
+    assert r.k == i_ref.shape[2]
+    np.testing.assert_array_equal(host(r.indices).astype(np.int32), i_ref)
+    np.testing.assert_array_equal(host(r.guide_scores), g_ref.reshape(host(r.guide_scores).shape))
+    assert rel_l2(host(r.out), o_ref) < COMP_REL
 
 
 @pytest.mark.parametrize("kind,W,k,excl", [("normal", 3000, 300, False), ("ties", 700, 200, False),

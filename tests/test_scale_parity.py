@@ -88,7 +88,12 @@ SCALE_CASES = {
     "v500_k128": (500, (36, 36), 5, 128, 0, 100, "normal"),
     "v500_k810": (500, (36, 36), 5, 810, 0, 100, "normal"),
     "v500_k2025": (500, (36, 36), 5, 2025, 0, 100, "normal"),
+    "v500_k4050": (500, (36, 36), 5, 4050, 0, 100, "normal"),
+    "v500_k10125": (500, (36, 36), 5, 10125, 0, 100, "normal"),
 }
+# the 10 % / 25 % budgets attend 65k / 162k keys per query: the reference recomputes a
+# 0.25 % row sample (1 % of 4 heads' windows) instead of 1 %
+SAMPLE_FRAC = {"v500_k4050": 0.01, "v500_k10125": 0.01}
 
 
 @pytest.mark.parametrize("name", list(SCALE_CASES))
@@ -101,9 +106,10 @@ def test_sampled_rows_at_scale(gsa, ref, name):
     out, ctx = _forward(gsa, q, k, v, wg, lt, top_k, variant, ref_stride)
     res = sampled_parity(q, k, v, wg, lt, top_k, out, ctx.topk, variant=variant, ref_stride=ref_stride,
                          o_comp=ctx.o_comp_coarse, lse_comp=ctx.lse_comp, o_sel=ctx.o_sel, lse_sel=ctx.lse_sel,
-                         frac=0.04, heads=[0, 5, 10, 15], seed=1000 + views)
+                         frac=SAMPLE_FRAC.get(name, 0.04), heads=[0, 5, 10, 15], seed=1000 + views)
     _log(name, res)
-    assert res["rows_checked"] >= 0.01 * 16 * views * (grid[0] // 4) * (grid[1] // 4)  # >= 1 % of all rows
+    frac_all = SAMPLE_FRAC.get(name, 0.04) / 4  # 4 of 16 heads
+    assert res["rows_checked"] >= frac_all * 16 * views * (grid[0] // 4) * (grid[1] // 4)  # >= 1 % (0.25 %) of all rows
     assert res["topk_mismatches"] == 0, res.get("first_mismatch")
     assert res["max_abs"] <= MAX_ABS and res["rel_l2"] <= REL_L2
     assert res["o_comp_rel_l2"] <= REL_L2 and res["o_sel_rel_l2"] <= REL_L2

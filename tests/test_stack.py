@@ -34,12 +34,44 @@ def test_stack_strided_views_match_contiguous_layers(gsa, lt, heads, topk, varia
 
     x = x0
     for l in range(3):
-        qkv = x @ st.w_qkv[l]
+        qkv = st.project(x, l)
         q, k, v = (t.contiguous() for t in st.heads_of(qkv))
         out = gsa.gsa_forward(q, k, v, st.w_g[l], L, p)
         x = (x.float() + out.permute(1, 0, 2).reshape(M, C)).to(torch.bfloat16)
     torch.cuda.synchronize()
     assert torch.equal(got.view(torch.int16), x.view(torch.int16))
+
+
+@pytest.mark.parametrize("M,Cm,N", [(1000, 1024, 3072), (300, 128, 256), (129, 64, 512), (4096, 512, 1536)])
+def test_projection_gemm_tc(gsa, M, Cm, N):
+    """The stack's tcgen05 GEMM (gsa_project_qkv_bf16) against an f32 reference of the same
+    bf16 inputs: the bf16 output differs from the rounded exact product by at most a
+    couple of ulps (f32 accumulation order), and ragged M (TMA zero fill) is handled."""
+    import ctypes as C
+    from paper_2603_08055_b200 import _lib
+    L = _lib.load()
+    g = torch.Generator(device="cuda").manual_seed(M + N)
+    x = torch.randn(M, Cm, generator=g, device="cuda").to(torch.bfloat16)
+    w = (torch.randn(Cm, N, generator=g, device="cuda") / Cm ** 0.5).to(torch.bfloat16)
+    wt = w.t().contiguous()
+    out = torch.full((M, N), float("nan"), dtype=torch.bfloat16, device="cuda")
+    rc = L.gsa_project_qkv_bf16(C.c_void_p(x.data_ptr()), M, Cm, Cm, C.c_void_p(wt.data_ptr()), N,
+                                C.c_void_p(out.data_ptr()), N, C.c_void_p(torch.cuda.current_stream().cuda_stream))
+    assert rc == 0
+    ref = x.double() @ w.double()
+    err = (out.double() - ref).abs()
+    tol = 2 ** -7 * ref.abs() + 1e-6 * (x.double().abs() @ w.double().abs())  # <= ~1 bf16 ulp + f32 accumulation
+    assert torch.isfinite(out.float()).all()
+    assert (err <= tol).all(), float((err / tol.clamp_min(1e-30)).max())
+
+
+def test_residual_bf16_matches_torch(gsa):
+    from paper_2603_08055_b200.stack import GsaStack
+    L = gsa.build_token_layout(0, 1, 8, 8, 4)
+    st = GsaStack(L, gsa.GsaParams(window_s=4, top_k=2), layers=1, heads=2, dim=64, seed=1)
+    x = torch.randn(333, 128, device="cuda").to(torch.bfloat16)
+    o = torch.randn(333, 128, device="cuda")
+    assert torch.equal(st.residual(x, o).view(torch.int16), (x.float() + o).to(torch.bfloat16).view(torch.int16))
 
 
 def test_stack_layer_within_tolerance_of_reference(gsa, ref):
