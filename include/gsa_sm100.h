@@ -287,7 +287,7 @@ int gsa_project_qkv(const float* x, int tokens, int model_dim, const float* w_q,
  * [n_out][model_dim] (K-major, stored once per layer), f32 accumulation, bf16 qkv
  * [tokens][n_out] (row stride ld_qkv) -- e.g. n_out = 3 * heads * dim for a fused
  * [Q | K | V] projection whose head views feed gsa_forward as strided tensors.
- * n_out % 256 == 0, model_dim % 64 == 0. gsa_residual_bf16: y = bf16(x + o) over n
+ * n_out % 32 == 0, model_dim % 64 == 0. gsa_residual_bf16: y = bf16(x + o) over n
  * elements (x, y bf16; o f32), the residual connection between stacked layers. */
 int gsa_project_qkv_bf16(const void* x, int tokens, int model_dim, int64_t ldx, const void* w_qkv_t, int n_out,
                          void* qkv, int64_t ld_qkv, gsa_stream_t stream);

@@ -237,6 +237,13 @@ static int dense_attention(const gsa_tensor* q, const gsa_tensor* k, const gsa_t
                                     out->head_stride, out->row_stride, out_row_offset, lse, ws, ws_bytes, st));
         return GSA_OK;
     }
+    if (q->dim == 64 && q->dtype == GSA_DTYPE_F32 && k->dtype == GSA_DTYPE_F32 && v->dtype == GSA_DTYPE_F32) {
+        // f32 Q/K/V: the same tensor cores through bf16 hi/lo score splits and fp16 P.V
+        GSA_CUDA(tc_dense_f32(*q, q_row_offset, mq, *k, *v, scale,
+                              static_cast<float*>(out->data) + (size_t)out_row_offset * out->row_stride,
+                              out->head_stride, out->row_stride, lse, ws, ws_bytes, st));
+        return GSA_OK;
+    }
     GSA_TRY(generic_supported(q->dim, 1));
     AttnArgs a{};
     a.q = ref_of(*q, q_row_offset);
@@ -1017,7 +1024,7 @@ int gsa_project_qkv_bf16(const void* x, int tokens, int model_dim, int64_t ldx, 
     if (!tc_gemm_supported(tokens, n_out, model_dim) || ldx % 8 || ld_qkv % 8 ||
         (reinterpret_cast<uintptr_t>(x) & 15) || (reinterpret_cast<uintptr_t>(w_qkv_t) & 15) ||
         (reinterpret_cast<uintptr_t>(qkv) & 15))
-        return fail(GSA_ERR_UNSUPPORTED, "project_qkv_bf16: needs n_out %% 256 == 0, model_dim %% 64 == 0, 16-byte "
+        return fail(GSA_ERR_UNSUPPORTED, "project_qkv_bf16: needs n_out %% 32 == 0, model_dim %% 64 == 0, 16-byte "
                     "aligned rows");
     GSA_CUDA(tc_gemm_bf16(static_cast<const __nv_bfloat16*>(x), ldx, static_cast<const __nv_bfloat16*>(w_qkv_t),
                           model_dim, static_cast<__nv_bfloat16*>(qkv), ld_qkv, tokens, n_out, model_dim,

@@ -122,7 +122,7 @@ struct CompParams {
     const float* cmax;        // [H] max |kc - kbar| (the scores are computed on centred keys)
     const float* kbar;        // [H][64] per-head mean key: S' = q.(kc - kbar) = S - q.kbar
     const float* qc;          // [H][Wq][64] f32 (lse correction q.kbar)
-    int64_t qc_hs;
+    int64_t qc_hs, qc_rs;
     const float* vmax;        // [H] max |vc|: V is fed to the MMA as fp16(vc * 2^-e_h), e_h = vexp(vmax[h])
     const uint32_t* exbits;   // [ceil(Wk/32)] or null
     float* out;
@@ -761,7 +761,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                                     __uint_as_float(o[half][e + 2]) * inv, __uint_as_float(o[half][e + 3]) * inv);
             if (p.lse) {
                 // the softmax ran on S' = S - q.kbar (a per-row shift): add it back to the lse
-                const float* qrow = p.qc + (int64_t)h * p.qc_hs + (int64_t)grow * 64;
+                const float* qrow = p.qc + (int64_t)h * p.qc_hs + (int64_t)grow * p.qc_rs;
                 const float* kb = p.kbar + h * 64;
                 float qk = 0.0f;
 #pragma unroll 8
@@ -1590,7 +1590,8 @@ struct Ws {
     size_t used;
 };
 
-Ws carve_ws(void* base, int heads, int Wq, int Wk, int k_eff, bool dry) {
+// dense: softmax-only use (tc_dense_f32: no top-k, so no candidate lists / scratch)
+Ws carve_ws(void* base, int heads, int Wq, int Wk, int k_eff, bool dry, bool dense = false) {
     Ws w{};
     size_t off = 0;
     auto take = [&](size_t bytes) -> char* {
@@ -1615,12 +1616,13 @@ Ws carve_ws(void* base, int heads, int Wq, int Wk, int k_eff, bool dry) {
     w.kpart = reinterpret_cast<float*>(take((size_t)heads * KMEAN_CHUNKS * 64 * 4));
     w.exbits = reinterpret_cast<uint32_t*>(take((size_t)((Wk + 127) / 128) * 16));
     const bool large_k = k_eff > KCAP;  // exact large-budget selection: no candidate lists
-    w.cand = reinterpret_cast<float2*>(take(large_k ? 8 : nq * (size_t)ccap_for(k_eff, true) * 8));
-    w.cand_n = reinterpret_cast<int*>(take(nq * 4));
-    w.flag = reinterpret_cast<uint8_t*>(take(nq));
-    w.blocks = reinterpret_cast<int*>(take(nq * 4 + ((nq + 1023) / 1024 + 1) * 4));  // flagged rows + block counts
+    const size_t nl = dense ? 1 : nq;
+    w.cand = reinterpret_cast<float2*>(take(large_k || dense ? 8 : nq * (size_t)ccap_for(k_eff, true) * 8));
+    w.cand_n = reinterpret_cast<int*>(take(nl * 4));
+    w.flag = reinterpret_cast<uint8_t*>(take(nl));
+    w.blocks = reinterpret_cast<int*>(take(nl * 4 + ((nl + 1023) / 1024 + 1) * 4));  // flagged rows + block counts
     w.nblocks = reinterpret_cast<int*>(take(4));
-    w.scratch = reinterpret_cast<uint32_t*>(take((size_t)LK_CTAS * LK_ROWS * Wk * 4));  // large-k / fallback scores
+    w.scratch = reinterpret_cast<uint32_t*>(take(dense ? 4 : (size_t)LK_CTAS * LK_ROWS * Wk * 4));  // large-k / fallback scores
     w.used = off + 256;
     return w;
 }
@@ -1742,6 +1744,7 @@ cudaError_t tc_compress_topk_splits(const CompressSplits* pre, const gsa_tensor&
     p.kbar = w.kbar;
     p.qc = static_cast<const float*>(qc.data);
     p.qc_hs = qc.head_stride;
+    p.qc_rs = qc.row_stride;
     p.vmax = w.vmax;
     p.exbits = excluded ? w.exbits : nullptr;
     p.out = out;
@@ -1863,6 +1866,92 @@ cudaError_t tc_compress_topk_splits(const CompressSplits* pre, const gsa_tensor&
 #endif
     }
     return cudaGetLastError();
+}
+
+size_t tc_dense_f32_workspace_bytes(int heads, int mq, int mk) {
+    return carve_ws(nullptr, heads, mq, mk, 0, true, true).used;
+}
+
+// Dense attention of f32 Q/K/V on the tensor cores: the compressed-branch kernel in
+// softmax-only mode (no top-k). Scores from the bf16 hi/lo split of Q and of the
+// centred keys (S = Qh.Kh + Qh.Kl + Ql.Kh, ~2^-16 relative), P.V in fp16 with V
+// scaled per head (~2^-11 relative in O), lse exact to the split. q rows
+// [q_row_offset, + mq) of q; out rows written at out + h*out_hs + r*out_rs.
+cudaError_t tc_dense_f32(const gsa_tensor& q, int q_row_offset, int mq, const gsa_tensor& k, const gsa_tensor& v,
+                         float scale, float* out, int64_t out_hs, int64_t out_rs, float* lse, void* ws,
+                         size_t ws_bytes, cudaStream_t st) {
+    const int H = q.heads, Wk = k.rows;
+    if (mq == 0) return cudaSuccess;
+    if (q.dtype != GSA_DTYPE_F32 || k.dtype != GSA_DTYPE_F32 || v.dtype != GSA_DTYPE_F32 || q.dim != 64 || Wk == 0 ||
+        !tmap_encode_fn())
+        return cudaErrorNotSupported;
+    void* own = nullptr;
+    const size_t need = tc_dense_f32_workspace_bytes(H, mq, Wk);
+    if (!ws || ws_bytes < need) {  // operator entry points without a workspace argument
+        cudaError_t e = cudaMallocAsync(&own, need, st);
+        if (e != cudaSuccess) return e;
+        ws = own;
+    }
+    Ws w = carve_ws(ws, H, mq, Wk, 0, false, true);
+    const float* qb = static_cast<const float*>(q.data) + (int64_t)q_row_offset * q.row_stride;
+    split_kernel<<<(unsigned)(((int64_t)H * mq + 31) / 32), 256, 0, st>>>(qb, q.head_stride, q.row_stride, H, mq,
+                                                                          w.qh, w.ql, w.qn);
+    cudaMemsetAsync(w.vmax, 0, (size_t)H * 4, st);
+    cudaMemsetAsync(w.kmax, 0, (size_t)H * 4, st);  // (top-k margins: unused without a top-k)
+    cudaMemsetAsync(w.cmax, 0, (size_t)H * 4, st);
+    absmax_kernel<<<dim3(32, H), 256, 0, st>>>(static_cast<const float*>(v.data), v.head_stride, v.row_stride, Wk,
+                                               w.vmax);
+    v16_kernel<<<(unsigned)(((int64_t)H * Wk + 31) / 32), 256, 0, st>>>(
+        static_cast<const float*>(v.data), v.head_stride, v.row_stride, H, Wk, w.vmax, w.v16);
+    kmean_partial_kernel<<<dim3(KMEAN_CHUNKS, H), 256, 0, st>>>(static_cast<const float*>(k.data), k.head_stride,
+                                                                 k.row_stride, Wk, w.kpart);
+    kmean_final_kernel<<<H, 64, 0, st>>>(w.kpart, Wk, w.kbar);
+    center_split_kernel<<<(unsigned)(((int64_t)H * Wk + 31) / 32), 256, 0, st>>>(
+        static_cast<const float*>(k.data), k.head_stride, k.row_stride, H, Wk, w.kbar, w.kh, w.kl, w.cn, w.kn);
+    note_launch(6);
+    CUtensorMap tqh, tql, tkh, tkl, tv16;
+    const int64_t qhs = (int64_t)mq * 64, khs = (int64_t)Wk * 64;
+    cudaError_t e = cudaSuccess;
+    if (!make_rows_tmap(&tqh, w.qh, H, mq, qhs, 64) || !make_rows_tmap(&tql, w.ql, H, mq, qhs, 64) ||
+        !make_rows_tmap(&tkh, w.kh, H, Wk, khs, 64) || !make_rows_tmap(&tkl, w.kl, H, Wk, khs, 64) ||
+        !make_rows_tmap(&tv16, reinterpret_cast<const __nv_bfloat16*>(w.v16), H, Wk, khs, 64))
+        e = cudaErrorNotSupported;
+    if (e == cudaSuccess) {
+        CompParams p{};
+        p.heads = H;
+        p.Wq = mq;
+        p.Wk = Wk;
+        p.k_eff = 0;
+        p.scale = scale;
+        p.c2 = scale * 1.4426950408889634f;
+        p.kv_tiles = (Wk + 127) / 128;
+        p.qnorm = w.qn;
+        p.kmax = w.kmax;
+        p.cmax = w.cmax;
+        p.kbar = w.kbar;
+        p.qc = qb;
+        p.qc_hs = q.head_stride;
+        p.qc_rs = q.row_stride;
+        p.vmax = w.vmax;
+        p.out = out;
+        p.out_hs = out_hs;
+        p.out_rs = out_rs;
+        p.lse = lse;
+        p.cand = w.cand;
+        p.ccap = 1;
+        p.cand_n = w.cand_n;
+        p.flag = w.flag;
+        const size_t smem = sizeof(CompSmem) + 1024;
+        e = cudaFuncSetAttribute(compress_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e == cudaSuccess) {
+            compress_tc_kernel<<<dim3((mq + 128 * NWG - 1) / (128 * NWG), H), NTHREADS, smem, st>>>(tqh, tql, tkh, tkl,
+                                                                                                 tv16, p);
+            note_launch();
+            e = cudaGetLastError();
+        }
+    }
+    if (own) cudaFreeAsync(own, st);
+    return e;
 }
 
 }  // namespace gsa_sm100

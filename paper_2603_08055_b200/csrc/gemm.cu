@@ -1,6 +1,7 @@
 // gemm.cu — the stack driver's dense projection on tcgen05 tensor cores (sm_100a):
 // QKV[M][N] (bf16) = X[M][K] (bf16) . W[K][N] with W given transposed (Wt[N][K],
 // K-major, the layout a static weight is stored in once), f32 accumulation in TMEM.
+// N % 32 == 0 (a ragged last N tile reads zero rows of Wt), K % 64 == 0, any M.
 // This is the per-layer X -> Q/K/V projection of the L-layer stack (BASELINE
 // configs[2]; the reference's project_qkv, layer.hpp:48-76, does the same map in
 // exact f32 on the CPU). Plus the residual X_{l+1} = bf16(X_l + O_l) of the stack.
@@ -135,7 +136,7 @@ __global__ void __launch_bounds__(G_THREADS, 1)
                 uint32_t pk[16];
 #pragma unroll
                 for (int e = 0; e < 16; ++e) pk[e] = pack_bf16(__uint_as_float(v[2 * e]), __uint_as_float(v[2 * e + 1]));
-                if (grow < p.M) {
+                if (grow < p.M && n * GN + 32 * c < p.N) {  // ragged last N tile: its columns past N are zeros
                     uint4* o = reinterpret_cast<uint4*>(dst + 32 * c);
 #pragma unroll
                     for (int q = 0; q < 4; ++q) o[q] = make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
@@ -186,14 +187,14 @@ __global__ void residual_bf16_kernel(const __nv_bfloat16* __restrict__ x, const 
 
 }  // namespace
 
-bool tc_gemm_supported(int M, int N, int K) { return M > 0 && N % GN == 0 && K % GK == 0 && tmap_encode_fn(); }
+bool tc_gemm_supported(int M, int N, int K) { return M > 0 && N > 0 && N % 32 == 0 && K % GK == 0 && tmap_encode_fn(); }
 
 cudaError_t tc_gemm_bf16(const __nv_bfloat16* a, int64_t lda, const __nv_bfloat16* bt, int64_t ldb, __nv_bfloat16* c,
                          int64_t ldc, int M, int N, int K, cudaStream_t st) {
     if (!tc_gemm_supported(M, N, K)) return cudaErrorNotSupported;
     CUtensorMap ta, tb;
     if (!make_2d_tmap(&ta, a, M, K, lda, GM) || !make_2d_tmap(&tb, bt, N, K, ldb, GN)) return cudaErrorNotSupported;
-    GemmParams p{M, N, K, (M + GM - 1) / GM, N / GN, c, ldc};
+    GemmParams p{M, N, K, (M + GM - 1) / GM, (N + GN - 1) / GN, c, ldc};
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);

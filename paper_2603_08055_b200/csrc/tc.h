@@ -42,13 +42,21 @@ cudaError_t tc_compress_topk(const gsa_tensor& qc, const gsa_tensor& kc, const g
                              int64_t out_rs, float* lse, int32_t* topk, float* guide, void* ws,
                              size_t ws_bytes, cudaStream_t st);
 
+// dense attention of f32 Q/K/V on tensor cores (the compressed-branch kernel without a
+// top-k): the f32 special path, tiled_attention and the pinned-plan compressed branch.
+// Without a large enough workspace the scratch is allocated stream-ordered.
+size_t tc_dense_f32_workspace_bytes(int heads, int mq, int mk);
+cudaError_t tc_dense_f32(const gsa_tensor& q, int q_row_offset, int mq, const gsa_tensor& k, const gsa_tensor& v,
+                         float scale, float* out, int64_t out_hs, int64_t out_rs, float* lse, void* ws,
+                         size_t ws_bytes, cudaStream_t st);
+
 // selection branch + gate + merge
 bool tc_select_supported(const SelectArgs& a);
 size_t tc_select_workspace_bytes(int heads);
 cudaError_t tc_select_gate_merge(const SelectArgs& a, cudaStream_t st);
 
 // dense projection of the stack driver: C[M][N] bf16 = A[M][K] . Bt[N][K]^T (gemm.cu);
-// N % 256 == 0, K % 64 == 0; and the stack's residual y = bf16(x + o)
+// N % 32 == 0, K % 64 == 0; and the stack's residual y = bf16(x + o)
 bool tc_gemm_supported(int M, int N, int K);
 cudaError_t tc_gemm_bf16(const __nv_bfloat16* a, int64_t lda, const __nv_bfloat16* bt, int64_t ldb, __nv_bfloat16* c,
                          int64_t ldc, int M, int N, int K, cudaStream_t st);

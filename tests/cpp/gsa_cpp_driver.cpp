@@ -5,7 +5,12 @@
 // reference would call it: build a layout, make weights and X, call
 // gsa_forward / the per-branch operators, catch gsa:: exceptions.
 //
-//   gsa_cpp_driver <out_dir> <num_special> <frames> <grid_h> <grid_w> <s> <heads> <model_dim> <top_k> <variant>
+//   gsa_cpp_driver <out_dir> <num_special> <frames> <grid_h> <grid_w> <s> <heads> <model_dim> <top_k> <variant> [f32|bf16]
+//   gsa_cpp_driver --time <views> <iters> [f32|bf16]
+//       times gsa::gsa_forward(Tensor<float> X, ...) host -> host (upload, projection, layer,
+//       context download: everything the reference API returns) at V views of 5 specials +
+//       36x36 patches, 16 heads, C = 1024, top-32; prints one JSON line
+#include <chrono>
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
@@ -70,9 +75,45 @@ void expect_throw(const char* what, F&& f) {
     std::exit(3);
 }
 
+int time_forward(int views, int iters, bool bf16) {
+    gsa::device::compute_precision() = bf16 ? gsa::device::Precision::kBf16 : gsa::device::Precision::kF32;
+    const int heads = 16, dim = 64, model_dim = heads * dim;
+    const gsa::TokenLayout layout = gsa::build_token_layout(5 * views, views, 36, 36, 4);
+    gsa::LayerWeights<float> w;
+    const float wscale = 1.0f / std::sqrt(static_cast<float>(model_dim));
+    w.w_q = random_tensor(heads, model_dim, dim, wscale, 2);
+    w.w_k = random_tensor(heads, model_dim, dim, wscale, 3);
+    w.w_v = random_tensor(heads, model_dim, dim, wscale, 4);
+    w.w_g = random_tensor(heads, dim, dim, 1.0f / 8.0f, 5);
+    const gsa::Tensor<float> x = random_tensor(1, layout.total_tokens(), model_dim, 1.0f, 1);
+    gsa::GsaParams p;
+    { auto warm = gsa::gsa_forward(x, layout, p, w); }
+    double best = 1e30, sum = 0.0;
+    for (int i = 0; i < iters; ++i) {
+        const auto t0 = std::chrono::steady_clock::now();
+        auto r = gsa::gsa_forward(x, layout, p, w);
+        const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+        best = std::min(best, ms);
+        sum += ms;
+    }
+    std::printf("{\"views\": %d, \"tokens\": %d, \"precision\": \"%s\", \"iters\": %d, \"ms_mean\": %.3f, "
+                "\"ms_best\": %.3f, \"tokens_per_s\": %.1f}\n",
+                views, layout.total_tokens(), bf16 ? "bf16" : "f32", iters, sum / iters, best,
+                layout.total_tokens() / (sum / iters / 1e3));
+    return 0;
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
+    if (argc >= 4 && std::string(argv[1]) == "--time") {
+        try {
+            return time_forward(std::atoi(argv[2]), std::atoi(argv[3]), argc >= 5 && std::string(argv[4]) == "bf16");
+        } catch (const gsa::GsaError& e) {
+            std::fprintf(stderr, "gsa error: %s\n", e.what());
+            return 1;
+        }
+    }
     if (argc < 11) {
         std::fprintf(stderr, "usage: %s out_dir ns frames gh gw s heads model_dim top_k variant\n", argv[0]);
         return 2;
@@ -81,6 +122,8 @@ int main(int argc, char** argv) {
     const int ns = std::atoi(argv[2]), nf = std::atoi(argv[3]), gh = std::atoi(argv[4]), gw = std::atoi(argv[5]);
     const int s = std::atoi(argv[6]), heads = std::atoi(argv[7]), model_dim = std::atoi(argv[8]);
     const int top_k = std::atoi(argv[9]), variant = std::atoi(argv[10]);
+    const bool bf16 = argc >= 12 && std::string(argv[11]) == "bf16";
+    gsa::device::compute_precision() = bf16 ? gsa::device::Precision::kBf16 : gsa::device::Precision::kF32;
     const int dim = 64;
     g_manifest.open(g_dir + "/manifest.txt");
     try {

@@ -51,26 +51,33 @@ def _load(d):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("precision", ["f32", "bf16"])
 @pytest.mark.parametrize("lt,heads,model_dim,top_k,variant", [
     ((10, 2, 16, 16, 4), 2, 128, 8, 0),
     ((40, 8, 36, 36, 4), 4, 256, 32, 0),
     ((12, 6, 16, 16, 4), 2, 64, 6, 1),
 ])
-def test_cpp_api_matches_reference(tmp_path, ref, lt, heads, model_dim, top_k, variant):
+def test_cpp_api_matches_reference(tmp_path, ref, lt, heads, model_dim, top_k, variant, precision):
+    """precision f32: the caller's values as they are; bf16 (gsa::device::Precision::kBf16):
+    Q/K/V rounded to bf16 after the exact projection -- the reference then runs on those
+    same rounded values (the driver dumps the Q/K/V the layer consumed)."""
     import torch
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     exe = _build()
-    r = subprocess.run([exe, str(tmp_path), *map(str, lt), str(heads), str(model_dim), str(top_k), str(variant)],
-                       capture_output=True, text=True, timeout=600)
+    r = subprocess.run([exe, str(tmp_path), *map(str, lt), str(heads), str(model_dim), str(top_k), str(variant),
+                        precision], capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr
     d = _load(str(tmp_path))
     assert "done" in d["_checks"]
     for name in ("divisibility", "tiling", "double", "empty_selection", "forward_rows", "nonfinite"):
         assert f"ok {name}" in d["_checks"], name
 
-    # project_qkv: the reference's f32 arithmetic, bit for bit
+    # project_qkv: the reference's f32 arithmetic, bit for bit (then RNE to bf16 in bf16 mode)
     q, k, v = ref.project(d["x"][0], d["w_q"], d["w_k"], d["w_v"])
+    if precision == "bf16":
+        import torch as _t
+        q, k, v = (_t.from_numpy(a).to(_t.bfloat16).float().numpy() for a in (q, k, v))
     for got, want in ((d["q"], q), (d["k"], k), (d["v"], v)):
         np.testing.assert_array_equal(got.view(np.uint32), want.view(np.uint32))
 

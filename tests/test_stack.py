@@ -42,7 +42,7 @@ def test_stack_strided_views_match_contiguous_layers(gsa, lt, heads, topk, varia
     assert torch.equal(got.view(torch.int16), x.view(torch.int16))
 
 
-@pytest.mark.parametrize("M,Cm,N", [(1000, 1024, 3072), (300, 128, 256), (129, 64, 512), (4096, 512, 1536)])
+@pytest.mark.parametrize("M,Cm,N", [(1000, 1024, 3072), (300, 128, 384), (129, 64, 512), (4096, 512, 1536), (77, 192, 96)])
 def test_projection_gemm_tc(gsa, M, Cm, N):
     """The stack's tcgen05 GEMM (gsa_project_qkv_bf16) against an f32 reference of the same
     bf16 inputs: the bf16 output differs from the rounded exact product by at most a
