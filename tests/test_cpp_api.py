@@ -117,7 +117,9 @@ def test_cpp_api_matches_reference(tmp_path, ref, lt, heads, model_dim, top_k, v
     np.testing.assert_array_equal(d["op_up"], ref.upsample(d["op_o_comp"], lt))
     if Ms:
         ospec, _ = ref.tiled_attention(q[:, :Ms], k, v, scale)
-        assert np.abs(d["op_o_spec"] - ospec).max() < 1e-4
+        # f32 operands: S on tensor cores from a 3-term bf16 split, P.V with P and V in fp16
+        # (the compressed-branch kernel in softmax-only mode): ~2^-11 relative in the output
+        assert np.abs(d["op_o_spec"] - ospec).max() < 5e-4 and rel_l2(d["op_o_spec"], ospec) < 1e-3
     # pinned plan = the plan gsa_forward realised: compressed branch without top-k
     assert np.abs(d["op_out_with_plan"] - rf["out"]).max() < 1e-3
     assert Mi > 0
