@@ -433,6 +433,60 @@ static int select_checks(const gsa_tensor* q, const gsa_tensor* k, const gsa_ten
     return GSA_OK;
 }
 
+// The selection branch (block_sparse_attention, selection.hpp:63-136; with the gate and
+// the gated merge fused when a.w_g is set). The tensor-core kernel's window geometry
+// (d = 64, s = 4) takes every dtype: bf16 rows are TMA-gathered where they lie; f32 rows
+// (and bf16 views whose strides a tensor map cannot express) are first packed into
+// contiguous bf16 hi(/lo) planes allocated stream-ordered (no host sync), and the kernel
+// runs 3-term products on them. Geometries outside that tile (s in {1, 2, 8}, d != 64),
+// which the reference API also accepts, run the exact CUDA-core kernel.
+static bool tma_rows_ok(const TensorRef& t) {
+    return t.dtype == GSA_DTYPE_BF16 && t.rs >= 64 && t.rs % 8 == 0 && t.hs % 8 == 0 &&
+           (reinterpret_cast<uintptr_t>(t.data) & 15) == 0;
+}
+
+static int run_select(SelectArgs a, cudaStream_t st) {
+    if (!(a.dim == 64 && a.L.s == 4 && a.Lkv.s == 4)) {
+        GSA_CUDA(launch_select_f32(a, st));
+        return GSA_OK;
+    }
+    void* mem = nullptr;
+    if (!tma_rows_ok(a.q) || !tma_rows_ok(a.k) || !tma_rows_ok(a.v)) {
+        const bool split = a.q.dtype == GSA_DTYPE_F32;
+        const int rq = a.L.image_tokens, rkv = a.Lkv.image_tokens, H = a.heads;
+        const size_t plane_q = (size_t)H * rq * 64, plane_kv = (size_t)H * rkv * 64;
+        const size_t elems = (plane_q + 2 * plane_kv) * (split ? 2 : 1);
+        GSA_CUDA(cudaMallocAsync(&mem, elems * sizeof(__nv_bfloat16), st));
+        __nv_bfloat16* base = static_cast<__nv_bfloat16*>(mem);
+        __nv_bfloat16* hq = base;
+        __nv_bfloat16* hk = hq + plane_q;
+        __nv_bfloat16* hv = hk + plane_kv;
+        __nv_bfloat16* lq = split ? hv + plane_kv : nullptr;
+        __nv_bfloat16* lk = split ? lq + plane_q : nullptr;
+        __nv_bfloat16* lv = split ? lk + plane_kv : nullptr;
+        GSA_CUDA(launch_pack_rows(a.q, H, rq, hq, lq, st));
+        GSA_CUDA(launch_pack_rows(a.k, H, rkv, hk, lk, st));
+        GSA_CUDA(launch_pack_rows(a.v, H, rkv, hv, lv, st));
+        auto plane = [](const __nv_bfloat16* p, int rows) {
+            return TensorRef{p, GSA_DTYPE_BF16, (int64_t)rows * 64, 64};
+        };
+        a.q = plane(hq, rq);
+        a.k = plane(hk, rkv);
+        a.v = plane(hv, rkv);
+        if (split) {
+            a.ql = plane(lq, rq);
+            a.kl = plane(lk, rkv);
+            a.vl = plane(lv, rkv);
+        }
+    }
+    const cudaError_t e = tc_select(a, st);
+    if (mem) cudaFreeAsync(mem, st);
+    if (e == cudaErrorNotSupported)
+        return fail(GSA_ERR_UNSUPPORTED, "block_sparse_attention: tensor-core selection rejected the operands");
+    GSA_CUDA(e);
+    return GSA_OK;
+}
+
 int gsa_block_sparse_attention(const gsa_tensor* q, const gsa_tensor* k, const gsa_tensor* v,
                                const int64_t* offsets, const int32_t* ids, const gsa_layout* layout,
                                float scale, const gsa_tensor* out, float* lse, gsa_stream_t stream) {
@@ -459,8 +513,7 @@ int gsa_block_sparse_attention(const gsa_tensor* q, const gsa_tensor* k, const g
     a.out_hs = out->head_stride;
     a.out_rs = out->row_stride;
     a.lse = lse;
-    GSA_CUDA(launch_select_f32(a, st));
-    return GSA_OK;
+    return run_select(a, st);
 }
 
 int gsa_gate(const gsa_tensor* q, const gsa_tensor* w_g, const gsa_tensor* g, gsa_stream_t stream) {
@@ -718,10 +771,7 @@ int gsa_forward(const gsa_tensor* q, const gsa_tensor* k, const gsa_tensor* v, c
         a.prior_o = b.prior_o;
         a.prior_lse = b.prior_lse;
     }
-    if (tc_sel)
-        GSA_CUDA(tc_select_gate_merge(a, st));
-    else
-        GSA_CUDA(launch_select_f32(a, st));
+    GSA_TRY(run_select(a, st));
     stage_mark(4, st);
     return GSA_OK;
 }
@@ -766,8 +816,8 @@ int gsa_forward_with_plan(const gsa_tensor* q, const gsa_tensor* k, const gsa_te
     a.out_rs = out->row_stride;
     a.w_g = static_cast<const float*>(w_g->data);
     a.o_comp = b.o_comp;
-    GSA_CUDA(launch_select_f32(a, st));
-    return GSA_OK;
+    a.wg_prep = b.wg_prep;
+    return run_select(a, st);
 }
 
 // ------------------------------------------------------- view-sharded layer
@@ -1008,11 +1058,7 @@ int gsa_shard_attend(const gsa_tensor* q_own, const gsa_tensor* k_all, const gsa
         a.prior_o = b.prior_o;
         a.prior_lse = b.prior_lse;
     }
-    if (tc_sel)
-        GSA_CUDA(tc_select_gate_merge(a, st));
-    else
-        GSA_CUDA(launch_select_f32(a, st));
-    return GSA_OK;
+    return run_select(a, st);
 }
 
 int gsa_project_qkv_bf16(const void* x, int tokens, int model_dim, int64_t ldx, const void* w_qkv_t,

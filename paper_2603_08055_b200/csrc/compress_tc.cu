@@ -104,6 +104,10 @@ constexpr float DELTA_REL = 9.5367431640625e-07f;  // 2^-20: collapse of distinc
 struct __align__(1024) CompSmem {
     uint8_t q[NWG][2][TILE];  // the CTA's two query tiles, bf16 hi / lo
     uint8_t ring[NS][STAGE];  // K / V tiles, bf16 hi / lo
+    // per softmax thread: the scores of the 32-key chunk it is extracting candidates from,
+    // so a candidate's score is one indexed shared load instead of a register select tree
+    // (16-byte groups XOR-swizzled by lane so a warp's row writes spread over the banks)
+    float cstage[256][32];
     uint64_t full[NS], empty[NS];
     uint64_t q_full;
     uint64_t s_full[NSB];
@@ -154,9 +158,11 @@ __device__ __forceinline__ float topk_threshold(float tau, float eps) {
 __device__ __forceinline__ void setmaxnreg_inc() { asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(SM_REGS) : "memory"); }
 __device__ __forceinline__ void setmaxnreg_dec() { asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(PROD_REGS) : "memory"); }
 
+#ifndef COMP_STAGE
+#define COMP_STAGE 1  // candidates read back from a shared staging row (else a register select tree)
+#endif
 // The lowest set bit of m (m != 0): its index e and v[e], by a binary search over m's
-// halves fused with a 5-level select tree. Integer/select ALU ops only: __ffs (FLO) and
-// friends issue on the XU pipe, which queues behind the softmax warps' MUFU.EX2 traffic.
+// halves fused with a 5-level select tree (COMP_STAGE 0).
 __device__ __forceinline__ float lowest_candidate(const uint32_t (&v)[32], uint32_t m, int& e) {
     uint32_t a[16];
     const bool b4 = (m & 0xffffu) == 0u;
@@ -189,7 +195,11 @@ __device__ __forceinline__ float lowest_candidate(const uint32_t (&v)[32], uint3
 // K-th best and the final candidate set are resolved by the re-score kernel.
 struct RowTopk {
     float lb, thr, delta, inv_delta, eps;
-    uint32_t hist[2];  // bytes: bins 0..7 relative to lb (bin 7 open-ended)
+    // byte b = candidates in bin b >= 1 relative to lb (bin 7 open-ended). Bin 0 is never
+    // counted (raise() only reads bins >= 1), so no byte overflows without saturation: before
+    // a tile every suffix from bin 1 up is < K (else raise() had lifted LB), and one tile
+    // adds at most 128: a byte stays <= K - 1 + 128 <= 255 for K <= KCAP
+    uint64_t hist;
     int cnt;           // candidates streamed; -1 = none (invalid row) / overflow
     int ccap;
     float2* dst;
@@ -211,9 +221,7 @@ struct RowTopk {
         // leaves floor(x) in the mantissa bits
         const float rel = fminf(fmaxf((v - lb) * inv_delta, 0.0f), (float)(NBIN - 1));
         const int b = __float_as_int(__fadd_rd(rel, 8388608.0f)) - 0x4B000000;
-        const uint32_t inc = (ok && v >= lb) ? 1u << (8 * (b & 3)) : 0u;
-        hist[0] = __vaddus4(hist[0], b < 4 ? inc : 0u);
-        hist[1] = __vaddus4(hist[1], b < 4 ? 0u : inc);
+        hist += (ok && b > 0) ? 1ull << (8 * b) : 0ull;
     }
     // after each tile: raise LB by the largest j with >= K counted at or above bin j
     __device__ __forceinline__ void raise(int K) {
@@ -221,7 +229,7 @@ struct RowTopk {
         float jf = 0.0f;  // (float)j without I2F (XU pipe)
 #pragma unroll
         for (int b = NBIN - 1; b >= 1; --b) {
-            suffix += (int)((hist[b >> 2] >> (8 * (b & 3))) & 0xffu);
+            suffix += (int)((hist >> (8 * b)) & 0xffu);
             if (j == 0 && suffix >= K) {
                 j = b;
                 jf = (float)b;
@@ -230,17 +238,13 @@ struct RowTopk {
         if (j == 0) return;
         lb += jf * delta;
         thr = fmaxf(thr, topk_threshold(lb, eps));
-        const uint64_t h = ((uint64_t)hist[1] << 32) | hist[0];
-        const uint64_t s = h >> (8 * j);
-        hist[0] = (uint32_t)s;
-        hist[1] = (uint32_t)(s >> 32);
+        hist >>= 8 * j;
         if (j == NBIN - 1) {
             // LB climbed the whole histogram in one tile: the bins are too fine. Double
             // them; merged counts stay lower bounds (new bin b holds old bins 2b, 2b+1,
             // all >= lb + b * 2 delta; the open-ended old bin 7 lands in new bin 3)
-            const uint32_t ev = __byte_perm(hist[0], hist[1], 0x6420), od = __byte_perm(hist[0], hist[1], 0x7531);
-            hist[0] = __vaddus4(ev, od);
-            hist[1] = 0u;
+            const uint32_t h0 = (uint32_t)hist, h1 = (uint32_t)(hist >> 32);
+            hist = __vaddus4(__byte_perm(h0, h1, 0x6420), __byte_perm(h0, h1, 0x7531));
             delta *= 2.0f;
             inv_delta *= 0.5f;
         }
@@ -416,7 +420,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         tk.delta = 1.0f;
         tk.inv_delta = 1.0f;
         tk.eps = row_ok ? EPS_REL * p.qnorm[r] * p.cmax[h] + EPS_REF * p.qnorm[r] * p.kmax[h] : 0.0f;
-        tk.hist[0] = tk.hist[1] = 0u;
+        tk.hist = 0ull;
         tk.cnt = (row_ok && K > 0) ? 0 : -1;
         tk.ccap = p.ccap;
         tk.dst = p.cand + r * p.ccap;
@@ -499,8 +503,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             __syncwarp();  // .sync.aligned tcgen05 ops below need a converged warp
             tc_fence_after();
             const int valid = p.Wk - t * 128;  // < 128 on the last key tile only
-            uint32_t keep[4];                  // selectable columns (in range, not excluded)
-            {
+            uint32_t keep[4] = {~0u, ~0u, ~0u, ~0u};  // selectable columns (in range, not excluded)
+            if (valid < 128 || (do_topk && p.exbits)) {
                 uint4 ex = make_uint4(0, 0, 0, 0);
                 if (do_topk && p.exbits) ex = __ldg(reinterpret_cast<const uint4*>(p.exbits) + t);
                 const uint32_t exw[4] = {ex.x, ex.y, ex.z, ex.w};
@@ -600,7 +604,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                             if (res != 0u && lbt > tk.lb) {
                                 tk.lb = lbt;
                                 tk.thr = fmaxf(tk.thr, topk_threshold(lbt, tk.eps));
-                                tk.hist[0] = tk.hist[1] = 0u;  // counts were relative to the old LB
+                                tk.hist = 0ull;  // counts were relative to the old LB
                                 const uint32_t kthr = fkey(tk.thr);
 #pragma unroll
                                 for (int c = 0; c < 4; ++c) {
@@ -705,12 +709,28 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 #ifdef COMPRESS_PROF
                 if (prof_on) { c1 = clock64(); pb[3] += c1 - c0; c0 = c1; }
 #endif
+#if COMP_STAGE
+                if (__any_sync(0xffffffffu, m != 0u)) {
+                    float4* srow = reinterpret_cast<float4*>(&sm.cstage[threadIdx.x][0]);
+#pragma unroll
+                    for (int j = 0; j < 8; ++j)
+                        srow[j ^ (lane & 7)] = make_float4(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]),
+                                                           __uint_as_float(v[4 * j + 2]), __uint_as_float(v[4 * j + 3]));
+                    const float* sf = &sm.cstage[threadIdx.x][0];  // the thread's own row: no barrier
+                    while (m) {
+                        const int e = __ffs(m) - 1;
+                        m &= m - 1;
+                        tk.add(sf[(((e >> 2) ^ (lane & 7)) << 2) | (e & 3)], col0 + e);
+                    }
+                }
+#else
                 while (m) {
                     int e;
                     const float x = lowest_candidate(v, m, e);
                     m &= m - 1;
                     tk.add(x, col0 + e);
                 }
+#endif
 #ifdef COMPRESS_PROF
                 if (prof_on) { c1 = clock64(); pb[4] += c1 - c0; c0 = c1; }
 #endif

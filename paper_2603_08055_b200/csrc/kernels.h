@@ -62,6 +62,7 @@ cudaError_t launch_attn_f32(const AttnArgs& a, cudaStream_t st);
 // ---- selection branch on CUDA cores (select_f32.cu) ---------------------
 struct SelectArgs {
     TensorRef q, k, v;  // image rows
+    TensorRef ql, kl, vl;  // tensor-core path, f32 inputs: bf16 lo planes (q/k/v then hold the hi planes)
     int heads, dim;
     DevLayout L;        // query side: windows / tokens of q, rows, o_comp, out (a view shard's own frames)
     DevLayout Lkv;      // key side: the frames k/v cover and window ids refer to (== L unsharded)
@@ -94,6 +95,9 @@ cudaError_t launch_project(const float* x, int tokens, int C, const ProjectMats&
                            bool bf16_out, cudaStream_t st);
 
 // ---- gate, upsample, plan helpers (misc.cu) -----------------------------
+// [H][rows][64] rows (f32 or bf16, any strides) -> contiguous bf16 hi (+ lo for f32) planes
+cudaError_t launch_pack_rows(const TensorRef& in, int heads, int rows, __nv_bfloat16* hi, __nv_bfloat16* lo,
+                             cudaStream_t st);
 cudaError_t launch_gate(const TensorRef& q, int heads, int rows, int dim, const float* w_g,
                         float* g, int64_t g_hs, int64_t g_rs, cudaStream_t st);
 cudaError_t launch_upsample(const float* coarse, int64_t c_hs, int64_t c_rs, int heads, int dim,

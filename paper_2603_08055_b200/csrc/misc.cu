@@ -28,6 +28,29 @@ __global__ void gate_kernel(TensorRef q, int heads, int rows, int dim, const flo
     }
 }
 
+// rows of a [H][rows][64] tensor (any strides; f32 or bf16) -> contiguous bf16 planes
+// [H][rows][64]: hi = RN(x), lo = RN(x - hi) (f32 only; lo may be null). One thread = 8
+// features. Feeds the tensor-core selection with TMA-loadable operands.
+template <typename T>
+__global__ void pack_rows_kernel(TensorRef in, int heads, int rows, __nv_bfloat16* __restrict__ hi,
+                                 __nv_bfloat16* __restrict__ lo) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // over heads*rows*8
+    if (i >= (int64_t)heads * rows * 8) return;
+    const int c = (int)(i & 7);
+    const int64_t hr = i >> 3;
+    const int h = (int)(hr / rows), r = (int)(hr - (int64_t)h * rows);
+    const T* src = reinterpret_cast<const T*>(in.data) + (int64_t)h * in.hs + (int64_t)r * in.rs + 8 * c;
+    __align__(16) __nv_bfloat16 vh[8], vl[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+        const float x = to_f32(src[e]);
+        vh[e] = __float2bfloat16_rn(x);
+        vl[e] = __float2bfloat16_rn(x - __bfloat162float(vh[e]));
+    }
+    *reinterpret_cast<uint4*>(hi + 8 * i) = *reinterpret_cast<const uint4*>(vh);
+    if (lo) *reinterpret_cast<uint4*>(lo + 8 * i) = *reinterpret_cast<const uint4*>(vl);
+}
+
 __global__ void upsample_kernel(const float* __restrict__ c, int64_t c_hs, int64_t c_rs, int heads,
                                 int dim, DevLayout L, float* o, int64_t o_hs, int64_t o_rs) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -117,6 +140,19 @@ cudaError_t launch_gate(const TensorRef& q, int heads, int rows, int dim, const 
         { gate_kernel<__nv_bfloat16><<<blocks, 32 * wpb, 0, st>>>(q, heads, rows, dim, w_g, g, g_hs, g_rs); note_launch(); }
     else
         { gate_kernel<float><<<blocks, 32 * wpb, 0, st>>>(q, heads, rows, dim, w_g, g, g_hs, g_rs); note_launch(); }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_pack_rows(const TensorRef& in, int heads, int rows, __nv_bfloat16* hi, __nv_bfloat16* lo,
+                             cudaStream_t st) {
+    const int64_t n = (int64_t)heads * rows * 8;
+    if (n == 0) return cudaSuccess;
+    const unsigned blocks = (unsigned)((n + 255) / 256);
+    if (in.dtype == GSA_DTYPE_F32)
+        pack_rows_kernel<float><<<blocks, 256, 0, st>>>(in, heads, rows, hi, lo);
+    else
+        pack_rows_kernel<__nv_bfloat16><<<blocks, 256, 0, st>>>(in, heads, rows, hi, nullptr);
+    note_launch();
     return cudaGetLastError();
 }
 

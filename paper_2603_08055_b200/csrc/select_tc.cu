@@ -81,6 +81,7 @@ constexpr int PREFETCH_AHEAD = SEL_PF;  // items of L2 prefetch ahead of the gat
 struct __align__(1024) SelSmem {
     uint8_t ring[NS][STAGE];
     uint8_t q[2][WIN];
+    uint8_t ql[2][WIN];       // split mode: the query tile's bf16 lo plane
     uint8_t wg[2][8192];      // W_g hi / lo, [a][j] 128B-swizzled
     uint8_t p[2][2][2 * P_QSTRIDE];  // [group parity][hi/lo] P^T: [q-group 2][key-chunk][8 rows][16 B]
     float red[2][4][16];      // cross-warp max / sum partials
@@ -111,6 +112,10 @@ struct SelTcParams {
     const float* prior_o;     // hybrid fast path: reference-frame softmax, merged by LSE (or null)
     const float* prior_lse;
     const uint8_t* wg_prep;  // [H][2][8192] bytes
+    // split: f32 Q/K/V as bf16 hi + lo planes (every window gathered twice, into two
+    // consecutive ring stages); S = Kh.Qh + Kl.Qh + Kh.Ql, O += Vh.Ph + Vh.Pl + Vl.Ph,
+    // G = Wgh.Qh + Wgl.Qh + Wgh.Ql. gate: fused gate + merge (else out = o_sel)
+    bool split, gate;
 };
 
 // Iterates this CTA's (item, group) sequence.
@@ -150,7 +155,9 @@ __device__ __forceinline__ void window_coords(const DevLayout& L, int wid, int& 
 
 __global__ void __launch_bounds__(NTHREADS, SEL_CTAS)
     select_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
-                     const __grid_constant__ CUtensorMap tm_v, const SelTcParams p) {
+                     const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_ql,
+                     const __grid_constant__ CUtensorMap tm_kl, const __grid_constant__ CUtensorMap tm_vl,
+                     const SelTcParams p) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     // keep the shared address space visible to the compiler (LDS/STS, not generic LD/ST)
     SelSmem& sm = *reinterpret_cast<SelSmem*>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
@@ -183,6 +190,11 @@ __global__ void __launch_bounds__(NTHREADS, SEL_CTAS)
         prefetch_tmap(&tm_q);
         prefetch_tmap(&tm_k);
         prefetch_tmap(&tm_v);
+        if (p.split) {
+            prefetch_tmap(&tm_ql);
+            prefetch_tmap(&tm_kl);
+            prefetch_tmap(&tm_vl);
+        }
     }
     if (warp == 1) tmem_alloc(&sm.tmem_base, TMEM_COLS);
     fence_proxy_async_smem();
@@ -206,7 +218,7 @@ __global__ void __launch_bounds__(NTHREADS, SEL_CTAS)
         auto load_chunks = [&](const GroupIt& it, const CUtensorMap* tm, bool with_prelude, int my_wid) {
             const int h = (int)(it.item / L.windows), w = (int)(it.item - (int64_t)h * L.windows);
             if (with_prelude) {
-                if (h != cur_head) {
+                if (p.gate && h != cur_head) {
                     // W_g of the new head: wait until every G MMA of the old head completed.
                     // wg_empty completes once per head (after its last item's G MMA), so
                     // this wait and that commit advance in lockstep: a parity wait is exact
@@ -222,10 +234,11 @@ __global__ void __launch_bounds__(NTHREADS, SEL_CTAS)
                 mbar_wait(&sm.q_empty[qb], qph[qb]);
                 qph[qb] ^= 1;
                 if (lane == 0) {
-                    mbar_arrive_expect_tx(&sm.q_full[qb], WIN);
+                    mbar_arrive_expect_tx(&sm.q_full[qb], p.split ? 2 * WIN : WIN);
                     int c1, c2;
                     window_coords(L, w, c1, c2);
                     tma_load_4d(&sm.q[qb][0], &tm_q, &sm.q_full[qb], 0, c1, c2, h);
+                    if (p.split) tma_load_4d(&sm.ql[qb][0], &tm_ql, &sm.q_full[qb], 0, c1, c2, h);
                 }
                 ++n_items;
             }
@@ -247,16 +260,19 @@ __global__ void __launch_bounds__(NTHREADS, SEL_CTAS)
                     }
                 }
             }
+            const CUtensorMap* tml = tm == &tm_k ? &tm_kl : &tm_vl;
             for (int c0 = 0; c0 < nw; c0 += 8) {
                 const int nc = min(8, nw - c0);
-                mbar_wait(&sm.empty[st], eph);
-                if (lane == 0) mbar_arrive_expect_tx(&sm.full[st], nc * WIN);
-                __syncwarp();
-                if (lane >= c0 && lane < c0 + nc)
-                    tma_load_4d(&sm.ring[st][(lane - c0) * WIN], tm, &sm.full[st], 0, c1, c2, h);
-                if (++st == NS) {
-                    st = 0;
-                    eph ^= 1;
+                for (int part = 0; part < (p.split ? 2 : 1); ++part) {  // split: hi stage, then lo stage
+                    mbar_wait(&sm.empty[st], eph);
+                    if (lane == 0) mbar_arrive_expect_tx(&sm.full[st], nc * WIN);
+                    __syncwarp();
+                    if (lane >= c0 && lane < c0 + nc)
+                        tma_load_4d(&sm.ring[st][(lane - c0) * WIN], part ? tml : tm, &sm.full[st], 0, c1, c2, h);
+                    if (++st == NS) {
+                        st = 0;
+                        eph ^= 1;
+                    }
                 }
             }
         };
@@ -318,30 +334,33 @@ __global__ void __launch_bounds__(NTHREADS, SEL_CTAS)
                 if (it.g == 0) {
                     mbar_wait(&sm.q_full[qb], qph[qb]);
                     qph[qb] ^= 1;
-                    if (h != cur_head) {
+                    if (p.gate && h != cur_head) {
                         mbar_wait(&sm.wg_full, wgph);
                         wgph ^= 1;
                         cur_head = h;
                     }
                     // G^T = Wg^T . Q^T (hi + lo), into the item's G buffer
                     const int gb = (int)(n_items % NGB);
-                    mbar_wait(&sm.g_empty[gb], (gphase >> gb) & 1u);
-                    gphase ^= 1u << gb;
-                    tc_fence_after();
+                    if (p.gate) {
+                        mbar_wait(&sm.g_empty[gb], (gphase >> gb) & 1u);
+                        gphase ^= 1u << gb;
+                        tc_fence_after();
 
-                    const uint32_t gcol = tmem + G_COL0 + 16u * (uint32_t)gb;
-                    // the last item of this head on this CTA releases W_g
-                    const int64_t nxt = it.item + gridDim.x;
-                    const bool last_of_head = nxt >= p.items || (int)(nxt / L.windows) != h;
-                    if (elect_one()) {
-                        for (int part = 0; part < 2; ++part)
-                            for (int ks = 0; ks < 4; ++ks)
-                                mma_bf16(gcol, umma_desc(smem_u32(&sm.wg[part][0]) + ks * 2048, 16, 1024, 2),
-                                         umma_desc(smem_u32(&sm.q[qb][0]) + ks * 32, 16, 1024, 2), id_o,
-                                         (part | ks) != 0);
-                        if (last_of_head) mma_commit(&sm.wg_empty);
+                        const uint32_t gcol = tmem + G_COL0 + 16u * (uint32_t)gb;
+                        // the last item of this head on this CTA releases W_g
+                        const int64_t nxt = it.item + gridDim.x;
+                        const bool last_of_head = nxt >= p.items || (int)(nxt / L.windows) != h;
+                        if (elect_one()) {
+                            for (int part = 0; part < (p.split ? 3 : 2); ++part)  // Wgh.Qh, Wgl.Qh (, Wgh.Ql)
+                                for (int ks = 0; ks < 4; ++ks)
+                                    mma_bf16(gcol, umma_desc(smem_u32(&sm.wg[part & 1][0]) + ks * 2048, 16, 1024, 2),
+                                             umma_desc(smem_u32(part == 2 ? &sm.ql[qb][0] : &sm.q[qb][0]) + ks * 32, 16,
+                                                       1024, 2),
+                                             id_o, (part | ks) != 0);
+                            if (last_of_head) mma_commit(&sm.wg_empty);
+                        }
+                        __syncwarp();
                     }
-                    __syncwarp();
                     ++n_items;
                 }
                 const int sb = (int)(jS & 1);
@@ -351,21 +370,39 @@ __global__ void __launch_bounds__(NTHREADS, SEL_CTAS)
                 const int nw = it.group_windows();
                 const uint32_t scol = tmem + (sb ? S_COL1 : S_COL0);
                 const uint64_t qdesc = umma_desc(smem_u32(&sm.q[qb][0]), 16, 1024, 2);
+                const uint64_t qldesc = umma_desc(smem_u32(&sm.ql[qb][0]), 16, 1024, 2);
                 for (int c0 = 0, c = 0; c0 < nw; c0 += 8, ++c) {
                     mbar_wait(&sm.full[st], fph);
-                    tc_fence_after();
-                    const uint64_t kdesc = umma_desc(smem_u32(&sm.ring[st][0]), 16, 1024, 2);
-                    if (elect_one()) {
-                        for (int ks = 0; ks < 4; ++ks)
-                            mma_bf16(scol + 16 * c, kdesc + (uint64_t)(ks * 2), qdesc + (uint64_t)(ks * 2), id_s,
-                                     ks != 0);
-                        mma_commit(&sm.empty[st]);
-                    }
-                    __syncwarp();
+                    const int st0 = st;
                     if (++st == NS) {
                         st = 0;
                         fph ^= 1;
                     }
+                    int st1 = st0;
+                    if (p.split) {  // the chunk's lo plane sits in the next stage
+                        mbar_wait(&sm.full[st], fph);
+                        st1 = st;
+                        if (++st == NS) {
+                            st = 0;
+                            fph ^= 1;
+                        }
+                    }
+                    tc_fence_after();
+                    const uint64_t kdesc = umma_desc(smem_u32(&sm.ring[st0][0]), 16, 1024, 2);
+                    const uint64_t kldesc = umma_desc(smem_u32(&sm.ring[st1][0]), 16, 1024, 2);
+                    if (elect_one()) {
+                        for (int ks = 0; ks < 4; ++ks) {
+                            mma_bf16(scol + 16 * c, kdesc + (uint64_t)(ks * 2), qdesc + (uint64_t)(ks * 2), id_s,
+                                     ks != 0);
+                            if (p.split) {
+                                mma_bf16(scol + 16 * c, kldesc + (uint64_t)(ks * 2), qdesc + (uint64_t)(ks * 2), id_s, 1);
+                                mma_bf16(scol + 16 * c, kdesc + (uint64_t)(ks * 2), qldesc + (uint64_t)(ks * 2), id_s, 1);
+                            }
+                        }
+                        mma_commit(&sm.empty[st0]);
+                        if (p.split) mma_commit(&sm.empty[st1]);
+                    }
+                    __syncwarp();
                 }
                 if (elect_one()) {
                     mma_commit(&sm.s_full[sb]);
@@ -385,8 +422,23 @@ __global__ void __launch_bounds__(NTHREADS, SEL_CTAS)
                 const uint64_t plo = umma_desc(smem_u32(&sm.p[pb][1][0]), 128, P_QSTRIDE, 0);
                 for (int c0 = 0, c = 0; c0 < nw; c0 += 8, ++c) {
                     mbar_wait(&sm.full[st], fph);
+                    const int st0 = st;
+                    if (++st == NS) {
+                        st = 0;
+                        fph ^= 1;
+                    }
+                    int st1 = st0;
+                    if (p.split) {
+                        mbar_wait(&sm.full[st], fph);
+                        st1 = st;
+                        if (++st == NS) {
+                            st = 0;
+                            fph ^= 1;
+                        }
+                    }
                     tc_fence_after();
-                    const uint64_t vdesc = umma_desc(smem_u32(&sm.ring[st][0]), 16, 1024, 2);
+                    const uint64_t vdesc = umma_desc(smem_u32(&sm.ring[st0][0]), 16, 1024, 2);
+                    const uint64_t vldesc = umma_desc(smem_u32(&sm.ring[st1][0]), 16, 1024, 2);
                     // descriptor start addresses are in 16-byte units
                     if (elect_one()) {
                         for (int ks = 0; ks < 8; ++ks) {
@@ -394,14 +446,12 @@ __global__ void __launch_bounds__(NTHREADS, SEL_CTAS)
                             const uint64_t po = (uint64_t)(c * 128 + ks * 16);
                             mma_bf16(ocol, va, phi + po, id_o, (c | ks) != 0);
                             if (!(kDebug & 1)) mma_bf16(ocol, va, plo + po, id_o, 1);
+                            if (p.split) mma_bf16(ocol, vldesc + (uint64_t)(ks * 128), phi + po, id_o, 1);
                         }
-                        mma_commit(&sm.empty[st]);
+                        mma_commit(&sm.empty[st0]);
+                        if (p.split) mma_commit(&sm.empty[st1]);
                     }
                     __syncwarp();
-                    if (++st == NS) {
-                        st = 0;
-                        fph ^= 1;
-                    }
                 }
                 if (elect_one()) mma_commit(&sm.o_full[pb]);
                 __syncwarp();
@@ -469,10 +519,15 @@ __global__ void __launch_bounds__(NTHREADS, SEL_CTAS)
             // ------------------------------- epilogue -------------------------------
             const int gb = (int)(n_fin_items % NGB);
             uint32_t grr[16];
-            tmem_ld_32x32b_x16(tmem + ((uint32_t)(32 * qd) << 16) + G_COL0 + 16u * (uint32_t)gb, grr);
-            tmem_wait_ld();
-            tc_fence_before();
-            mbar_arrive(&sm.g_empty[gb]);
+            if (p.gate) {
+                tmem_ld_32x32b_x16(tmem + ((uint32_t)(32 * qd) << 16) + G_COL0 + 16u * (uint32_t)gb, grr);
+                tmem_wait_ld();
+                tc_fence_before();
+                mbar_arrive(&sm.g_empty[gb]);
+            } else {
+#pragma unroll
+                for (int q = 0; q < 16; ++q) grr[q] = 0u;
+            }
             ++n_fin_items;
             // lanes 0-15 hold feature 16*qd+lane for all 16 queries; lanes 16-31 take
             // queries 8..15 of lane-16 so every lane writes 8 outputs
@@ -506,7 +561,7 @@ __global__ void __launch_bounds__(NTHREADS, SEL_CTAS)
                     sel = (w1 * p.prior_o[ti * 64 + jf_feat] + w2 * sel) / (w1 + w2);
                 }
                 const float g = __frcp_rn(1.0f + __expf(-z8[i]));
-                outh[(int64_t)tok * p.out_rs + jf_feat] = g * comp + (1.0f - g) * sel;
+                outh[(int64_t)tok * p.out_rs + jf_feat] = p.gate ? g * comp + (1.0f - g) * sel : sel;
                 if (p.o_sel_ctx || p.gate_ctx) {
                     const int64_t ti = (int64_t)h * L.image_tokens + tok;
                     if (p.o_sel_ctx) p.o_sel_ctx[ti * 64 + jf_feat] = sel;
@@ -527,7 +582,7 @@ __global__ void __launch_bounds__(NTHREADS, SEL_CTAS)
         while (it.valid(p)) {
             const int sb = (int)(j & 1);
             const int nkeys = it.group_windows() * 16;
-            if (it.g == 0) {  // the compressed-branch row this item merges with, a full item ahead
+            if (it.g == 0 && p.gate) {  // the compressed-branch row this item merges with, a full item ahead
                 const int ih = (int)(it.item / L.windows), iw = (int)(it.item - (int64_t)ih * L.windows);
                 const float cv = __ldg(p.o_comp + ((int64_t)ih * L.windows + iw) * 64 + 16 * qd + (lane & 15));
                 if (n_started & 1) comp_pf1 = cv;
@@ -760,24 +815,37 @@ bool tensor_ok(const TensorRef& t) {
 }  // namespace
 
 bool tc_select_supported(const SelectArgs& a) {
-    // every precondition of tc_select_gate_merge (TMA window maps: bf16 rows, 16-byte
-    // aligned strides and base), so a supported call never fails on shape grounds
+    // every precondition of tc_select (TMA window maps: bf16 rows, 16-byte aligned strides
+    // and base), so a supported call never fails on shape grounds. f32 inputs reach it as
+    // bf16 hi/lo planes (pack_select_inputs in abi.cu)
+    const bool split = a.ql.data != nullptr;
     return a.dim == 64 && a.L.s == 4 && a.Lkv.s == 4 && tensor_ok(a.q) && tensor_ok(a.k) && tensor_ok(a.v) &&
-           a.w_g && a.o_comp && a.wg_prep && get_encode() != nullptr;
+           (!split || (tensor_ok(a.ql) && tensor_ok(a.kl) && tensor_ok(a.vl))) &&
+           (!a.w_g || (a.o_comp && a.wg_prep)) && get_encode() != nullptr;
 }
 
 size_t tc_select_workspace_bytes(int heads) { return (size_t)heads * 16384; }
 
-cudaError_t tc_select_gate_merge(const SelectArgs& a, cudaStream_t st) {
-    if (!tensor_ok(a.q) || !tensor_ok(a.k) || !tensor_ok(a.v) || a.dim != 64 || a.L.s != 4 || !a.w_g ||
-        !a.o_comp || !a.wg_prep)
-        return cudaErrorNotSupported;
-    CUtensorMap tq, tk, tv;
+cudaError_t tc_select(const SelectArgs& a, cudaStream_t st) {
+    if (!tc_select_supported(a)) return cudaErrorNotSupported;
+    const bool split = a.ql.data != nullptr, gate = a.w_g != nullptr;
+    CUtensorMap tq, tk, tv, tql, tkl, tvl;
     if (!make_window_map(&tq, a.q, a.heads, a.L) || !make_window_map(&tk, a.k, a.heads, a.Lkv) ||
         !make_window_map(&tv, a.v, a.heads, a.Lkv))
         return cudaErrorNotSupported;
-    wg_prep_kernel<<<(a.heads * 4096 + 255) / 256, 256, 0, st>>>(a.w_g, a.heads, a.wg_prep);
-    note_launch();
+    if (split) {
+        if (!make_window_map(&tql, a.ql, a.heads, a.L) || !make_window_map(&tkl, a.kl, a.heads, a.Lkv) ||
+            !make_window_map(&tvl, a.vl, a.heads, a.Lkv))
+            return cudaErrorNotSupported;
+    } else {
+        tql = tq;
+        tkl = tk;
+        tvl = tv;
+    }
+    if (gate) {
+        wg_prep_kernel<<<(a.heads * 4096 + 255) / 256, 256, 0, st>>>(a.w_g, a.heads, a.wg_prep);
+        note_launch();
+    }
     SelTcParams p;
     p.heads = a.heads;
     p.L = a.L;
@@ -793,8 +861,10 @@ cudaError_t tc_select_gate_merge(const SelectArgs& a, cudaStream_t st) {
     p.o_sel_ctx = a.o_sel_ctx;
     p.prior_o = a.prior_o;
     p.prior_lse = a.prior_lse;
-    p.gate_ctx = a.gate_ctx;
+    p.gate_ctx = gate ? a.gate_ctx : nullptr;
     p.wg_prep = a.wg_prep;
+    p.split = split;
+    p.gate = gate;
     int dev = 0, nsm = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
@@ -802,7 +872,7 @@ cudaError_t tc_select_gate_merge(const SelectArgs& a, cudaStream_t st) {
     cudaError_t e = cudaFuncSetAttribute(select_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     const int grid = (int)std::min<int64_t>((int64_t)nsm * SEL_CTAS, p.items);
-    select_tc_kernel<<<grid, NTHREADS, smem, st>>>(tq, tk, tv, p);
+    select_tc_kernel<<<grid, NTHREADS, smem, st>>>(tq, tk, tv, tql, tkl, tvl, p);
     note_launch();
     return cudaGetLastError();
 }

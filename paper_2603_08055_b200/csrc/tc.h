@@ -50,10 +50,11 @@ cudaError_t tc_dense_f32(const gsa_tensor& q, int q_row_offset, int mq, const gs
                          float scale, float* out, int64_t out_hs, int64_t out_rs, float* lse, void* ws,
                          size_t ws_bytes, cudaStream_t st);
 
-// selection branch + gate + merge
+// selection branch (block_sparse_attention), with the gate + merge fused when a.w_g is set;
+// bf16 Q/K/V, or f32 as bf16 hi/lo planes (a.ql/kl/vl set: 3-term products)
 bool tc_select_supported(const SelectArgs& a);
 size_t tc_select_workspace_bytes(int heads);
-cudaError_t tc_select_gate_merge(const SelectArgs& a, cudaStream_t st);
+cudaError_t tc_select(const SelectArgs& a, cudaStream_t st);
 
 // dense projection of the stack driver: C[M][N] bf16 = A[M][K] . Bt[N][K]^T (gemm.cu);
 // N % 32 == 0, K % 64 == 0; and the stack's residual y = bf16(x + o)

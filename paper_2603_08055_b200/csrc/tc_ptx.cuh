@@ -68,9 +68,24 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
             if (dt > 10000000000ull) __trap();
         }
     }
-#else
+#elif defined(GSA_MBAR_SPIN)
     while (!mbar_try_wait(bar, parity)) {
     }
+#else
+    // suspend-time hint: the waiting warp sleeps until the phase completes (or the hint
+    // expires) instead of re-issuing the probe, leaving issue slots to the warps that work
+    uint32_t ok;
+    do {
+        asm volatile(
+            "{\n"
+            ".reg .pred P1;\n"
+            "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2, %3;\n"
+            "selp.b32 %0, 1, 0, P1;\n"
+            "}\n"
+            : "=r"(ok)
+            : "r"(smem_u32(bar)), "r"(parity), "r"(0x989680u)
+            : "memory");
+    } while (!ok);
 #endif
 }
 

@@ -289,6 +289,41 @@ def test_plan_and_block_sparse(gsa, orc, variant):
     assert np.abs(host(lse) - l_ref).max() < 1e-4
 
 
+def _strided_rows(x, dtype, row_stride):
+    """[H][M][64] values as a view with the given row stride (elements) of a wider buffer"""
+    H, M, d = x.shape
+    buf = torch.zeros(H, M, row_stride, dtype=dtype, device="cuda")
+    buf[:, :, :d] = torch.from_numpy(np.ascontiguousarray(x)).to("cuda", dtype)
+    return buf[:, :, :d]
+
+
+@pytest.mark.parametrize("dtype,row_stride", [("f32", 64), ("f32", 80), ("bf16", 72), ("bf16", 68)])
+def test_block_sparse_csr_plans_on_tensor_cores(gsa, orc, dtype, row_stride):
+    """block_sparse_attention (selection.hpp:63-136) with a caller-built CSR plan of ragged
+    rows (1 .. 70 windows: one to five 16-window groups, repeated ids allowed) on the
+    tensor-core selection kernel: bf16 rows gathered in place (row stride 72) or packed
+    (68: not a TMA stride), f32 rows as bf16 hi/lo planes with 3-term products."""
+    lt = (0, 4, 12, 16, 4)
+    L = Layout(*lt)
+    rng = np.random.default_rng(row_stride)
+    H, W = 3, L.num_windows
+    sizes = rng.integers(1, 71, size=H * W)
+    offs = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+    ids = rng.integers(0, W, size=int(offs[-1])).astype(np.int32)
+    x = [rng.standard_normal((H, L.image_tokens, 64)).astype(np.float32) for _ in range(3)]
+    if dtype == "bf16":
+        x = [orc.bf16_round(a) for a in x]
+    o_ref, l_ref = orc.block_sparse(*x, L, offs, ids, 0.125)
+    tdt = torch.float32 if dtype == "f32" else torch.bfloat16
+    q, kk, v = (_strided_rows(a, tdt, row_stride) for a in x)
+    gl = gsa.build_token_layout(*lt)
+    plan = gsa.SelectionPlan(H, W, torch.from_numpy(offs).cuda(), torch.from_numpy(ids).cuda(),
+                             torch.empty(0, dtype=torch.int32, device="cuda"))
+    out, lse = gsa.block_sparse_attention(q, kk, v, plan, gl, 0.125)
+    assert np.abs(host(out) - o_ref).max() < 1e-4
+    assert np.abs(host(lse) - l_ref).max() < 1e-4
+
+
 def test_empty_selection_raises(gsa):
     lt = (0, 1, 8, 8, 4)
     gl = gsa.build_token_layout(*lt)
