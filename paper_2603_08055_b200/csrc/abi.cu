@@ -229,12 +229,14 @@ int gsa_upsample_nearest(const gsa_tensor* coarse, const gsa_layout* layout, con
 
 static int dense_attention(const gsa_tensor* q, const gsa_tensor* k, const gsa_tensor* v, float scale,
                            const gsa_tensor* out, float* lse, int q_row_offset, int out_row_offset,
-                           int mq, cudaStream_t st, void* ws = nullptr, size_t ws_bytes = 0) {
+                           int mq, cudaStream_t st, void* ws = nullptr, size_t ws_bytes = 0,
+                           const __half* v16 = nullptr, const unsigned* vmax = nullptr) {
     if (mq == 0) return GSA_OK;
     if (k->rows == 0) return fail(GSA_ERR_SHAPE_MISMATCH, "tiled_attention: empty key set");
     if (tc_dense_supported(*q, *k, *v)) {
         GSA_CUDA(tc_dense_attention(*q, *k, *v, scale, q_row_offset, mq, static_cast<float*>(out->data),
-                                    out->head_stride, out->row_stride, out_row_offset, lse, ws, ws_bytes, st));
+                                    out->head_stride, out->row_stride, out_row_offset, lse, ws, ws_bytes, st, v16,
+                                    vmax));
         return GSA_OK;
     }
     if (q->dim == 64 && q->dtype == GSA_DTYPE_F32 && k->dtype == GSA_DTYPE_F32 && v->dtype == GSA_DTYPE_F32) {
@@ -450,33 +452,46 @@ static int run_select(SelectArgs a, cudaStream_t st) {
         GSA_CUDA(launch_select_f32(a, st));
         return GSA_OK;
     }
+    const bool f32 = a.q.dtype == GSA_DTYPE_F32;
+    const bool pack_qk = f32 || !tma_rows_ok(a.q) || !tma_rows_ok(a.k);
+    const bool make_v = a.v16.data == nullptr;
+    const int rq = a.L.image_tokens, rkv = a.Lkv.image_tokens, H = a.heads;
+    const size_t plane_q = (size_t)H * rq * 64, plane_kv = (size_t)H * rkv * 64, planes = f32 ? 2 : 1;
+    size_t bytes = 0;
+    if (pack_qk) bytes += (plane_q + plane_kv) * planes * 2;
+    if (make_v) bytes += plane_kv * planes * 2 + 256;
     void* mem = nullptr;
-    if (!tma_rows_ok(a.q) || !tma_rows_ok(a.k) || !tma_rows_ok(a.v)) {
-        const bool split = a.q.dtype == GSA_DTYPE_F32;
-        const int rq = a.L.image_tokens, rkv = a.Lkv.image_tokens, H = a.heads;
-        const size_t plane_q = (size_t)H * rq * 64, plane_kv = (size_t)H * rkv * 64;
-        const size_t elems = (plane_q + 2 * plane_kv) * (split ? 2 : 1);
-        GSA_CUDA(cudaMallocAsync(&mem, elems * sizeof(__nv_bfloat16), st));
-        __nv_bfloat16* base = static_cast<__nv_bfloat16*>(mem);
-        __nv_bfloat16* hq = base;
-        __nv_bfloat16* hk = hq + plane_q;
-        __nv_bfloat16* hv = hk + plane_kv;
-        __nv_bfloat16* lq = split ? hv + plane_kv : nullptr;
-        __nv_bfloat16* lk = split ? lq + plane_q : nullptr;
-        __nv_bfloat16* lv = split ? lk + plane_kv : nullptr;
-        GSA_CUDA(launch_pack_rows(a.q, H, rq, hq, lq, st));
-        GSA_CUDA(launch_pack_rows(a.k, H, rkv, hk, lk, st));
-        GSA_CUDA(launch_pack_rows(a.v, H, rkv, hv, lv, st));
-        auto plane = [](const __nv_bfloat16* p, int rows) {
-            return TensorRef{p, GSA_DTYPE_BF16, (int64_t)rows * 64, 64};
+    if (bytes) {
+        GSA_CUDA(cudaMallocAsync(&mem, bytes, st));
+        char* cur = static_cast<char*>(mem);
+        auto take = [&](size_t elems) {
+            void* r = cur;
+            cur += elems * 2;
+            return r;
         };
-        a.q = plane(hq, rq);
-        a.k = plane(hk, rkv);
-        a.v = plane(hv, rkv);
-        if (split) {
-            a.ql = plane(lq, rq);
-            a.kl = plane(lk, rkv);
-            a.vl = plane(lv, rkv);
+        auto plane = [](const void* p, int rows, int dt) { return TensorRef{p, dt, (int64_t)rows * 64, 64}; };
+        if (pack_qk) {
+            auto* hq = static_cast<__nv_bfloat16*>(take(plane_q));
+            auto* hk = static_cast<__nv_bfloat16*>(take(plane_kv));
+            auto* lq = f32 ? static_cast<__nv_bfloat16*>(take(plane_q)) : nullptr;
+            auto* lk = f32 ? static_cast<__nv_bfloat16*>(take(plane_kv)) : nullptr;
+            GSA_CUDA(launch_pack_rows(a.q, H, rq, hq, lq, st));
+            GSA_CUDA(launch_pack_rows(a.k, H, rkv, hk, lk, st));
+            a.q = plane(hq, rq, GSA_DTYPE_BF16);
+            a.k = plane(hk, rkv, GSA_DTYPE_BF16);
+            if (f32) {
+                a.ql = plane(lq, rq, GSA_DTYPE_BF16);
+                a.kl = plane(lk, rkv, GSA_DTYPE_BF16);
+            }
+        }
+        if (make_v) {
+            auto* hv = static_cast<__half*>(take(plane_kv));
+            auto* lv = f32 ? static_cast<__half*>(take(plane_kv)) : nullptr;
+            auto* vmax = reinterpret_cast<unsigned*>(cur);
+            GSA_CUDA(launch_v16(a.v, H, rkv, vmax, hv, lv, st));
+            a.v16 = plane(hv, rkv, kDtypeF16);
+            if (f32) a.v16l = plane(lv, rkv, kDtypeF16);
+            a.vmax = vmax;
         }
     }
     const cudaError_t e = tc_select(a, st);
@@ -601,6 +616,9 @@ struct LayerBufs {
     uint8_t* wg_prep;
     void* dense_ws;
     size_t dense_ws_bytes;
+    // V of all M rows as fp16 planes (the P.V operand of the special and selection kernels)
+    __half* v16;
+    unsigned* vmax;
 };
 
 size_t carve(const LayerPlan& lp, const gsa_context* ctx, char* base, size_t cap, bool dry, LayerBufs* b) {
@@ -619,8 +637,10 @@ size_t carve(const LayerPlan& lp, const gsa_context* ctx, char* base, size_t cap
     b->compress_ws_bytes = tc_compress_workspace_bytes(lp.heads, lp.W, lp.dim, lp.k_eff);
     b->compress_ws = c.take<char>(b->compress_ws_bytes);
     b->wg_prep = c.take<uint8_t>(tc_select_workspace_bytes(lp.heads));
-    b->dense_ws_bytes = tc_dense_workspace_bytes(lp.heads, lp.Ms, lp.Ms + lp.Mi);
+    b->dense_ws_bytes = tc_dense_workspace_bytes(lp.heads, lp.Ms, lp.Ms + lp.Mi, false);
     b->dense_ws = c.take<char>(b->dense_ws_bytes);
+    b->v16 = c.take<__half>((size_t)lp.heads * (lp.Ms + lp.Mi) * lp.dim);
+    b->vmax = c.take<unsigned>((size_t)lp.heads);
     b->kf = b->vf = nullptr;
     b->prior_o = b->prior_lse = nullptr;
     b->fa_ws = nullptr;
@@ -707,9 +727,13 @@ int gsa_forward(const gsa_tensor* q, const gsa_tensor* k, const gsa_tensor* v, c
     const int H = lp.heads, d = lp.dim;
     float* outp = static_cast<float*>(out->data);
 
-    // 1. special tokens: dense attention over all M keys (layer.hpp:201-202)
+    // 1. special tokens: dense attention over all M keys (layer.hpp:201-202). bf16 inputs:
+    // V is converted once to the fp16 P.V operand shared with the selection kernel
     stage_mark(0, st);
-    GSA_TRY(dense_attention(q, k, v, lp.scale, out, b.lse_spec, 0, 0, lp.Ms, st, b.dense_ws, b.dense_ws_bytes));
+    const bool v16_made = q->dtype == GSA_DTYPE_BF16 && d == 64 && lp.L.s == 4 && tc_dense_supported(*q, *k, *v);
+    if (v16_made) GSA_CUDA(launch_v16(ref_of(*v), H, lp.M, b.vmax, b.v16, nullptr, st));
+    GSA_TRY(dense_attention(q, k, v, lp.scale, out, b.lse_spec, 0, 0, lp.Ms, st, b.dense_ws, b.dense_ws_bytes,
+                            v16_made ? b.v16 : nullptr, v16_made ? b.vmax : nullptr));
     stage_mark(1, st);
 
     // 2. pool Q/K/V image rows (layer.hpp:204-206); on the tensor-core path the
@@ -762,6 +786,10 @@ int gsa_forward(const gsa_tensor* q, const gsa_tensor* k, const gsa_tensor* v, c
     a.o_sel_ctx = ctx ? ctx->o_sel : nullptr;
     a.gate_ctx = ctx ? ctx->gate : nullptr;
     a.wg_prep = b.wg_prep;
+    if (v16_made) {
+        a.v16 = TensorRef{b.v16 + (size_t)lp.Ms * 64, kDtypeF16, (int64_t)lp.M * 64, 64};
+        a.vmax = b.vmax;
+    }
     const bool tc_sel = tc_select_supported(a);
     if (tc_sel && params->variant == 1 && lp.n_forced > 0 && lp.k_eff > 0 && b.kf && q->dim == 64 &&
         tc_dense_supported(*q, *k, *v)) {
@@ -891,6 +919,8 @@ struct ShardBufs {
     void* dense_ws;
     size_t dense_ws_bytes;
     float* lse_spec;
+    __half* v16;  // V of all M rows as fp16 planes (P.V operand of the special + selection kernels)
+    unsigned* vmax;
     // hybrid fast path (hybrid_prior): reference-frame K/V copies, their dense softmax
     __nv_bfloat16 *kf, *vf;
     float *prior_o, *prior_lse;
@@ -906,9 +936,11 @@ size_t shard_carve(const ShardPlan& sp, char* base, bool dry, ShardBufs* b) {
     b->compress_ws_bytes = tc_compress_workspace_bytes_qk(g.heads, sp.W_g, g.W, g.dim, g.k_eff);
     b->compress_ws = c.take<char>(b->compress_ws_bytes);
     b->wg_prep = c.take<uint8_t>(tc_select_workspace_bytes(g.heads));
-    b->dense_ws_bytes = tc_dense_workspace_bytes(g.heads, sp.Ms_g, g.M);
+    b->dense_ws_bytes = tc_dense_workspace_bytes(g.heads, sp.Ms_g, g.M, false);
     b->dense_ws = c.take<char>(b->dense_ws_bytes);
     b->lse_spec = c.take<float>((size_t)g.heads * sp.Ms_g);
+    b->v16 = c.take<__half>((size_t)g.heads * g.M * g.dim);
+    b->vmax = c.take<unsigned>((size_t)g.heads);
     b->kf = b->vf = nullptr;
     b->prior_o = b->prior_lse = nullptr;
     b->fa_ws = nullptr;
@@ -1025,10 +1057,15 @@ int gsa_shard_attend(const gsa_tensor* q_own, const gsa_tensor* k_all, const gsa
     if (!workspace || need > ws_bytes + 256)
         return fail(GSA_ERR_WORKSPACE, "shard_attend: workspace %zu < %zu bytes", ws_bytes, need);
     cudaStream_t st = (cudaStream_t)stream;
+    // V as fp16 planes over all M rows, exactly as gsa_forward makes them (same per-head
+    // scale, so a sharded layer equals the unsharded one)
+    const bool v16_made = q_own->dtype == GSA_DTYPE_BF16 && d == 64 && g.L.s == 4 &&
+                          tc_dense_supported(*q_own, *k_all, *v_all) && (sp.Ms_g > 0 || sp.W_g > 0);
+    if (v16_made) GSA_CUDA(launch_v16(ref_of(*v_all), H, g.M, b.vmax, b.v16, nullptr, st));
     // own special rows: dense attention over all M keys (layer.hpp:80-96)
     if (sp.Ms_g > 0)
         GSA_TRY(dense_attention(q_own, k_all, v_all, g.scale, out_own, b.lse_spec, 0, 0, sp.Ms_g, st, b.dense_ws,
-                                b.dense_ws_bytes));
+                                b.dense_ws_bytes, v16_made ? b.v16 : nullptr, v16_made ? b.vmax : nullptr));
     if (sp.W_g == 0) return GSA_OK;
     if (params->variant == 1) GSA_CUDA(launch_forced(g.L, params->ref_stride, b.forced, b.mask, st));
     SelectArgs a{};
@@ -1047,6 +1084,10 @@ int gsa_shard_attend(const gsa_tensor* q_own, const gsa_tensor* k_all, const gsa
     a.w_g = static_cast<const float*>(w_g->data);
     a.o_comp = static_cast<const float*>(o_comp_own->data);
     a.wg_prep = b.wg_prep;
+    if (v16_made) {
+        a.v16 = TensorRef{b.v16 + (size_t)g.Ms * 64, kDtypeF16, (int64_t)g.M * 64, 64};
+        a.vmax = b.vmax;
+    }
     const bool tc_sel = tc_select_supported(a);
     if (tc_sel && params->variant == 1 && g.n_forced > 0 && g.k_eff > 0 && b.kf && d == 64 &&
         tc_dense_supported(*q_own, *k_all, *v_all)) {

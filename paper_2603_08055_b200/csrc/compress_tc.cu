@@ -158,8 +158,11 @@ __device__ __forceinline__ float topk_threshold(float tau, float eps) {
 __device__ __forceinline__ void setmaxnreg_inc() { asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(SM_REGS) : "memory"); }
 __device__ __forceinline__ void setmaxnreg_dec() { asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(PROD_REGS) : "memory"); }
 
+#ifndef COMP_POLY
+#define COMP_POLY 0  // exp2 of every COMP_POLY-th pair by polynomial on the FMA pipe (0: all on MUFU)
+#endif
 #ifndef COMP_STAGE
-#define COMP_STAGE 1  // candidates read back from a shared staging row (else a register select tree)
+#define COMP_STAGE 0  // 1: candidates read back from a shared staging row (measured: 71.0 vs 68.7 ms compress at V=1000 for the register select tree)
 #endif
 // The lowest set bit of m (m != 0): its index e and v[e], by a binary search over m's
 // halves fused with a 5-level select tree (COMP_STAGE 0).
@@ -676,7 +679,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     for (int e2 = 0; e2 < 16; ++e2) {
                         const float2 x = make_float2(__uint_as_float(v[2 * e2]), __uint_as_float(v[2 * e2 + 1]));
                         const float2 a = __ffma2_rn(x, c2v, nmc);
-                        const float2 pv = make_float2(ex2_approx(a.x), ex2_approx(a.y));
+                        const float2 pv = (COMP_POLY > 0 && e2 % COMP_POLY == COMP_POLY - 1)
+                                              ? exp2_poly2(a)
+                                              : make_float2(ex2_approx(a.x), ex2_approx(a.y));
                         lsum2[e2 & 1] = __fadd2_rn(lsum2[e2 & 1], pv);  // the denominator sums the exact f32 P
                         p16[e2] = pack_f16(pv.x, pv.y);
                     }

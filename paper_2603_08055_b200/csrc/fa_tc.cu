@@ -7,13 +7,18 @@
 //           128B-swizzled) through a 12-stage ring in the MMA's first-use order,
 //           plus L2 prefetches FA_PF tiles ahead.
 //   warp 9  MMA: S(n) = Q_w.K(t)^T  (M=128, N=128, K=64, into TMEM, 3 rotating
-//           S/P buffers, n = 2t + w), O_w += P(n).V(t) with P read from TMEM
-//           (A-from-TMEM form, P as bf16 hi + lo: 2 MMAs per 16-key step).
+//           S/P buffers, n = 2t + w), O_w += P(n).V16(t) with P read from TMEM
+//           (A-from-TMEM form, P and V in fp16: one MMA per 16-key step).
 //   warps 0-7  softmax, one warpgroup per query tile, one thread per query row =
 //           one TMEM lane: two passes per tile (row max over the loaded scores,
 //           then P chunk by chunk from a TMEM re-read), lazy rescale (only when
 //           the max grows by > 2^8; O is then rescaled in TMEM), P = exp2 via
-//           MUFU written back over S as bf16 hi/lo pairs; epilogue O/l and lse.
+//           MUFU written back over S as packed fp16 pairs; epilogue O/l and lse.
+// P.V in fp16: V (bf16) is converted once per call to fp16(v * 2^-e_h) with a per-head
+// power of two e_h from max |v| -- exact (bf16's 8-bit significands fit fp16's 11 and
+// the scale keeps them in range) -- so the only rounding is P's (2^-12 relative), one
+// MMA term instead of the two a bf16 hi + lo P needs (kind::f16 takes no mixed A/B
+// formats: an fp16 P against bf16 V is an illegal instruction, measured).
 // Split-KV (few query tiles, e.g. 5 specials/view) writes normalised partials
 // + lse that gsa_fa_combine merges.
 #include <cuda.h>
@@ -59,6 +64,10 @@ constexpr float RESCALE_LOG2 = 8.0f;
 #define FA_PB_UNROLL 4  // measured (special, V=1000): single pass 41.0 ms; two-pass x1 44.5, x2 41.8, x4 39.1-39.7
 #endif
 constexpr int PB_UNROLL = FA_PB_UNROLL;
+#ifndef FA_POLY
+#define FA_POLY 0  // exp2 of every FA_POLY-th pair by polynomial on the FMA pipe (0: all on MUFU)
+#endif
+
 #ifndef FA_PF
 #define FA_PF 24  // measured: special 41.3 -> 40.8 ms at V=1000
 #endif
@@ -84,7 +93,11 @@ struct FaParams {
     float* lse;       // [H][mq] (splits == 1)
     float* part_o;    // [splits][H][mq][64]
     float* part_lse;  // [splits][H][mq]
+    const unsigned* vmax;  // [H] max |v| (float bits): V16 = fp16(v * 2^-vexp(vmax))
 };
+
+// per-head power-of-two exponent that brings |v| <= vmax below 2^14 in fp16 (exact scaling)
+__device__ __forceinline__ int vexp(float vmax) { return vmax > 0.0f ? ilogbf(vmax) - 13 : 0; }
 
 __device__ __forceinline__ void setmaxnreg_inc() { asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(FA_SM_REGS) : "memory"); }
 __device__ __forceinline__ void setmaxnreg_dec() { asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(FA_PROD_REGS) : "memory"); }
@@ -171,7 +184,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         } else if (warp == 9 && T > 0) {
             // ================================ MMA ================================
             const uint32_t id_s = idesc_bf16(128, 128, 0, 0);
-            const uint32_t id_o = idesc_bf16(128, 64, 0, 1);
+            const uint32_t id_o = idesc_f16(128, 64, 0, 1);  // P (TMEM) and V (SMEM) in fp16
             auto wait_tile = [&](int s) {
                 mbar_wait(&sm.full[s % NS], (uint32_t)((s / NS) & 1));
                 tc_fence_after();
@@ -200,10 +213,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 const uint32_t o = tmem + O_COL0 + 64 * w, pb = tmem + 128 * (n % NSB);
                 if (elect_one()) {
                     for (int ks = 0; ks < 8; ++ks) {
-                        // P hi of keys 16ks..16ks+15: cols 32*(ks/2) + 8*(ks%2); lo 16 columns later
-                        const uint32_t a_hi = pb + 32 * (ks >> 1) + 8 * (ks & 1);
-                        mma_bf16_ts(o, a_hi, vd + 128 * ks, id_o, (t | ks) != 0);
-                        if (!(kDebug & 1)) mma_bf16_ts(o, a_hi + 16, vd + 128 * ks, id_o, 1);
+                        // P fp16 of keys 16ks..16ks+15: columns 32*(ks/2) + 8*(ks%2)
+                        mma_bf16_ts(o, pb + 32 * (ks >> 1) + 8 * (ks & 1), vd + 128 * ks, id_o, (t | ks) != 0);
                     }
                     mma_commit(&sm.o_done[w]);
                     if (t == T - 1) mma_commit(&sm.o_final[w]);
@@ -284,16 +295,15 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 }
             }
             const float mc = m_used * p.c2;
-            // P = hi + lo with hi = P truncated to bf16 (PRMT packs two), lo = P - hi rounded
+            // P packed as fp16 pairs over the first 16 columns of each 32-key chunk
             const float2 c2v = make_float2(p.c2, p.c2), nmc = make_float2(-mc, -mc);
-            const float2 neg1 = make_float2(-1.0f, -1.0f);
             float2 lsum2[2] = {make_float2(0.0f, 0.0f), make_float2(0.0f, 0.0f)};
             // FA_TWO_PASS: the 128 scores are live only through the max; the P pass re-reads
             // one 32-key chunk at a time from TMEM (fewer live registers, a chunk loop
             // unrolled by PB_UNROLL instead of a fully unrolled tile)
 #pragma unroll PB_UNROLL
             for (int c = 0; c < 4; ++c) {
-                uint32_t hi[16], lo[16];
+                uint32_t p16[16];
                 uint32_t vv[32];
                 if (FA_TWO_PASS) {
                     tmem_ld_32x32b_x32(s_base + 32 * c, vv);
@@ -305,16 +315,14 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     const uint32_t s1 = FA_TWO_PASS ? vv[2 * e2 + 1] : sr[c & 3][2 * e2 + 1];
                     const float2 x = make_float2(__uint_as_float(s0), __uint_as_float(s1));
                     const float2 a = __ffma2_rn(x, c2v, nmc);
-                    const float2 pv = (kDebug & 2) ? __ffma2_rn(a, c2v, c2v) : make_float2(ex2_approx(a.x), ex2_approx(a.y));
-                    lsum2[e2 & 1] = __fadd2_rn(lsum2[e2 & 1], pv);
-                    const uint32_t u0 = __float_as_uint(pv.x), u1 = __float_as_uint(pv.y);
-                    hi[e2] = __byte_perm(u0, u1, 0x7632);
-                    const float2 hf = make_float2(__uint_as_float(u0 & 0xffff0000u), __uint_as_float(u1 & 0xffff0000u));
-                    const float2 lf = __ffma2_rn(hf, neg1, pv);
-                    lo[e2] = pack_bf16(lf.x, lf.y);
+                    // FA_POLY: every FA_POLY-th pair on the FMA pipe instead of MUFU
+                    const float2 pv = (FA_POLY > 0 && e2 % FA_POLY == FA_POLY - 1)
+                                          ? exp2_poly2(a)
+                                          : make_float2(ex2_approx(a.x), ex2_approx(a.y));
+                    lsum2[e2 & 1] = __fadd2_rn(lsum2[e2 & 1], pv);  // the denominator sums the f32 P
+                    p16[e2] = pack_f16(pv.x, pv.y);
                 }
-                tmem_st_32x32b_x16(s_base + 32 * c, hi);
-                tmem_st_32x32b_x16(s_base + 32 * c + 16, lo);
+                tmem_st_32x32b_x16(s_base + 32 * c, p16);
             }
             const float2 ls = __fadd2_rn(lsum2[0], lsum2[1]);
             l += ls.x + ls.y;
@@ -332,7 +340,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         tmem_wait_ld();
         const int qrow = (qp * NWG + w) * 128 + row;
         if (qrow < p.mq) {
-            const float inv = 1.0f / l;
+            const float inv = ldexpf(1.0f / l, vexp(__uint_as_float(p.vmax[h])));  // undo the V16 scaling exactly
             const float lse = m_used * p.scale + logf(l);
             float* dst;
             if (p.splits == 1) {
@@ -437,23 +445,64 @@ int fa_splits(int qpairs, int heads, int kv_tiles) {
     return splits;
 }
 
-size_t tc_dense_workspace_bytes(int heads, int mq, int mk) {
+// workspace: [V16 fp16 H*mk*64][vmax H u32, padded to 256 B][split partials, when split]
+static size_t v16_bytes(int heads, int mk) { return ((size_t)heads * mk * 64 * 2 + 255) / 256 * 256; }
+static size_t vmax_bytes(int heads) { return ((size_t)heads * 4 + 255) / 256 * 256; }
+
+size_t tc_dense_workspace_bytes(int heads, int mq, int mk, bool with_v16) {
+    if (mq == 0) return 0;
     const int qpairs = (mq + 255) / 256, kv_tiles = (mk + 127) / 128;
     const int splits = fa_splits(qpairs, heads, kv_tiles);
-    if (splits == 1) return 0;
-    return (size_t)splits * heads * mq * 65 * sizeof(float) + 256;
+    const size_t base = with_v16 ? v16_bytes(heads, mk) + vmax_bytes(heads) : 0;
+    if (splits == 1) return base;
+    return base + (size_t)splits * heads * mq * 65 * sizeof(float) + 256;
 }
 
 cudaError_t tc_dense_attention(const gsa_tensor& q, const gsa_tensor& k, const gsa_tensor& v, float scale,
                                int q_row_offset, int mq, float* out, int64_t out_hs, int64_t out_rs,
-                               int out_row_offset, float* lse, void* ws, size_t ws_bytes, cudaStream_t st) {
+                               int out_row_offset, float* lse, void* ws, size_t ws_bytes, cudaStream_t st,
+                               const __half* v16_pre, const unsigned* vmax_pre) {
     if (mq == 0) return cudaSuccess;
+    // V as the fp16 P.V operand: the caller's V16 planes, else converted here (carved from
+    // the workspace, else allocated stream-ordered)
+    const int H = q.heads, mk = k.rows;
+    const size_t vb = v16_bytes(H, mk) + vmax_bytes(H);
+    void* vmem = nullptr;
+    bool owned = false;
+    char* wsb = static_cast<char*>(ws);
+    const __half* v16 = v16_pre;
+    const unsigned* vmax = vmax_pre;
+    if (!v16) {
+        if (ws && ws_bytes >= vb) {
+            vmem = ws;
+            wsb += vb;
+            ws_bytes -= vb;
+        } else {
+            cudaError_t ea = cudaMallocAsync(&vmem, vb, st);
+            if (ea != cudaSuccess) return ea;
+            owned = true;
+            wsb = nullptr;
+            ws_bytes = 0;
+        }
+        __half* v16w = static_cast<__half*>(vmem);
+        unsigned* vmaxw = reinterpret_cast<unsigned*>(static_cast<char*>(vmem) + v16_bytes(H, mk));
+        cudaError_t ec = launch_v16(TensorRef{v.data, v.dtype, v.head_stride, v.row_stride}, H, mk, vmaxw, v16w, nullptr, st);
+        if (ec != cudaSuccess) {
+            if (owned) cudaFreeAsync(vmem, st);
+            return ec;
+        }
+        v16 = v16w;
+        vmax = vmaxw;
+    }
     CUtensorMap tq, tk, tv;
     const char* qbase = static_cast<const char*>(q.data) + (size_t)q_row_offset * q.row_stride * 2;
     if (!make_rows_map(&tq, qbase, q.heads, mq, q.head_stride, q.row_stride) ||
         !make_rows_map(&tk, k.data, k.heads, k.rows, k.head_stride, k.row_stride) ||
-        !make_rows_map(&tv, v.data, v.heads, v.rows, v.head_stride, v.row_stride))
+        !make_rows_map(&tv, v16, H, mk, (int64_t)mk * 64, 64)) {
+        if (owned) cudaFreeAsync(vmem, st);
         return cudaErrorNotSupported;
+    }
+    ws = wsb;
     FaParams p{};
     p.heads = q.heads;
     p.mq = mq;
@@ -471,13 +520,17 @@ cudaError_t tc_dense_attention(const gsa_tensor& q, const gsa_tensor& k, const g
     p.out_hs = out_hs;
     p.out_rs = out_rs;
     p.lse = lse;
+    p.vmax = vmax;
     if (p.splits > 1) {
         p.part_o = static_cast<float*>(ws);
         p.part_lse = p.part_o + (size_t)p.splits * q.heads * mq * 64;
     }
     const size_t smem = sizeof(FaSmem) + 1024;
     cudaError_t e = cudaFuncSetAttribute(fa_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
+    if (e != cudaSuccess) {
+        if (owned) cudaFreeAsync(vmem, st);
+        return e;
+    }
     dim3 grid(qpairs, p.splits, q.heads);
     fa_tc_kernel<<<grid, NTHREADS, smem, st>>>(tq, tk, tv, p);
     note_launch();
@@ -487,6 +540,7 @@ cudaError_t tc_dense_attention(const gsa_tensor& q, const gsa_tensor& k, const g
                                                                         p.out, out_hs, out_rs, lse);
         note_launch();
     }
+    if (owned) cudaFreeAsync(vmem, st);
     return cudaGetLastError();
 }
 

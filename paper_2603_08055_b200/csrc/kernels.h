@@ -14,6 +14,9 @@ int report_error(int status, const char* msg);
 // gsa_set_stage_events: records stage event i (0..4) on st when enabled on this thread
 void stage_mark(int i, cudaStream_t st);
 
+// internal dtype tag (not in the C ABI): fp16 operand planes made by launch_v16
+constexpr int kDtypeF16 = 100;
+
 struct TensorRef {  // device view, element strides
     const void* data;
     int dtype;
@@ -62,7 +65,11 @@ cudaError_t launch_attn_f32(const AttnArgs& a, cudaStream_t st);
 // ---- selection branch on CUDA cores (select_f32.cu) ---------------------
 struct SelectArgs {
     TensorRef q, k, v;  // image rows
-    TensorRef ql, kl, vl;  // tensor-core path, f32 inputs: bf16 lo planes (q/k/v then hold the hi planes)
+    TensorRef ql, kl;   // tensor-core path, f32 inputs: bf16 lo planes (q/k then hold the hi planes)
+    // tensor-core path: V as fp16(v * 2^-vexp(vmax_h)) planes [H][rows][64] (v16l: the f32
+    // remainder, null for bf16 inputs), image rows of the key side; made by run_select when null
+    TensorRef v16, v16l;
+    const unsigned* vmax;
     int heads, dim;
     DevLayout L;        // query side: windows / tokens of q, rows, o_comp, out (a view shard's own frames)
     DevLayout Lkv;      // key side: the frames k/v cover and window ids refer to (== L unsharded)
@@ -95,6 +102,11 @@ cudaError_t launch_project(const float* x, int tokens, int C, const ProjectMats&
                            bool bf16_out, cudaStream_t st);
 
 // ---- gate, upsample, plan helpers (misc.cu) -----------------------------
+// V (f32 or bf16, any strides) -> per-head max |v| (float bits, vmax zeroed by the caller's
+// memset inside) and contiguous fp16 planes hi = fp16(v * 2^-e_h), lo = fp16(v * 2^-e_h - hi)
+// (lo only for f32 and when non-null), e_h = ilogb(vmax_h) - 13
+cudaError_t launch_v16(const TensorRef& v, int heads, int rows, unsigned* vmax, __half* hi, __half* lo,
+                       cudaStream_t st);
 // [H][rows][64] rows (f32 or bf16, any strides) -> contiguous bf16 hi (+ lo for f32) planes
 cudaError_t launch_pack_rows(const TensorRef& in, int heads, int rows, __nv_bfloat16* hi, __nv_bfloat16* lo,
                              cudaStream_t st);

@@ -2,6 +2,7 @@
 // (layer.hpp:99-119), nearest upsampling (compression.hpp:42-53), the hybrid
 // forced-window set (selection.cpp:7-27) and the CSR selection plan
 // (selection.cpp:29-67).
+#include <algorithm>
 #include <cub/device/device_scan.cuh>
 
 #include "kernels.h"
@@ -46,6 +47,45 @@ __global__ void pack_rows_kernel(TensorRef in, int heads, int rows, __nv_bfloat1
         const float x = to_f32(src[e]);
         vh[e] = __float2bfloat16_rn(x);
         vl[e] = __float2bfloat16_rn(x - __bfloat162float(vh[e]));
+    }
+    *reinterpret_cast<uint4*>(hi + 8 * i) = *reinterpret_cast<const uint4*>(vh);
+    if (lo) *reinterpret_cast<uint4*>(lo + 8 * i) = *reinterpret_cast<const uint4*>(vl);
+}
+
+__device__ __forceinline__ int v16_exp(float vmax) { return vmax > 0.0f ? ilogbf(vmax) - 13 : 0; }
+
+// max |v| per head (blockIdx.y): |x| bit patterns order like the values
+template <typename T>
+__global__ void vmax_kernel(TensorRef v, int rows, unsigned* vmax_bits) {
+    const int h = blockIdx.y;
+    unsigned mx = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < (int64_t)rows * 8;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int r = (int)(i >> 3), c = (int)(i & 7);
+        const T* src = reinterpret_cast<const T*>(v.data) + h * v.hs + r * v.rs + 8 * c;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) mx = max(mx, __float_as_uint(fabsf(to_f32(src[e]))));
+    }
+    mx = __reduce_max_sync(0xffffffffu, mx);
+    if ((threadIdx.x & 31) == 0) atomicMax(&vmax_bits[h], mx);
+}
+
+template <typename T>
+__global__ void v16_kernel(TensorRef v, int heads, int rows, const unsigned* __restrict__ vmax_bits,
+                           __half* __restrict__ hi, __half* __restrict__ lo) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // over heads*rows*8
+    if (i >= (int64_t)heads * rows * 8) return;
+    const int c = (int)(i & 7);
+    const int64_t hr = i >> 3;
+    const int h = (int)(hr / rows), r = (int)(hr - (int64_t)h * rows);
+    const float sc = ldexpf(1.0f, -v16_exp(__uint_as_float(vmax_bits[h])));
+    const T* src = reinterpret_cast<const T*>(v.data) + h * v.hs + (int64_t)r * v.rs + 8 * c;
+    __align__(16) __half vh[8], vl[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+        const float x = to_f32(src[e]) * sc;  // exact: power-of-two scale
+        vh[e] = __float2half_rn(x);
+        vl[e] = __float2half_rn(x - __half2float(vh[e]));
     }
     *reinterpret_cast<uint4*>(hi + 8 * i) = *reinterpret_cast<const uint4*>(vh);
     if (lo) *reinterpret_cast<uint4*>(lo + 8 * i) = *reinterpret_cast<const uint4*>(vl);
@@ -153,6 +193,23 @@ cudaError_t launch_pack_rows(const TensorRef& in, int heads, int rows, __nv_bflo
     else
         pack_rows_kernel<__nv_bfloat16><<<blocks, 256, 0, st>>>(in, heads, rows, hi, nullptr);
     note_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_v16(const TensorRef& v, int heads, int rows, unsigned* vmax, __half* hi, __half* lo,
+                       cudaStream_t st) {
+    cudaMemsetAsync(vmax, 0, (size_t)heads * 4, st);
+    if ((int64_t)heads * rows == 0) return cudaSuccess;
+    const int blocks = (int)std::min<int64_t>(((int64_t)rows * 8 + 255) / 256, 512);
+    const unsigned cb = (unsigned)(((int64_t)heads * rows * 8 + 255) / 256);
+    if (v.dtype == GSA_DTYPE_F32) {
+        vmax_kernel<float><<<dim3(blocks, heads), 256, 0, st>>>(v, rows, vmax);
+        v16_kernel<float><<<cb, 256, 0, st>>>(v, heads, rows, vmax, hi, lo);
+    } else {
+        vmax_kernel<__nv_bfloat16><<<dim3(blocks, heads), 256, 0, st>>>(v, rows, vmax);
+        v16_kernel<__nv_bfloat16><<<cb, 256, 0, st>>>(v, heads, rows, vmax, hi, nullptr);
+    }
+    note_launch(2);
     return cudaGetLastError();
 }
 

@@ -54,7 +54,7 @@ constexpr int kDebug = GSA_DEBUG_SELECT;
 // 1 CTA, 512-key groups, 8 stages 53 ms; 2 CTAs, 16-window groups, 3 stages 33 ms;
 // 2 CTAs with 8-window groups 42 ms.
 #ifndef SEL_NS
-#define SEL_NS 3
+#define SEL_NS 4
 #endif
 #ifndef SEL_CTAS
 #define SEL_CTAS 2
@@ -83,7 +83,7 @@ struct __align__(1024) SelSmem {
     uint8_t q[2][WIN];
     uint8_t ql[2][WIN];       // split mode: the query tile's bf16 lo plane
     uint8_t wg[2][8192];      // W_g hi / lo, [a][j] 128B-swizzled
-    uint8_t p[2][2][2 * P_QSTRIDE];  // [group parity][hi/lo] P^T: [q-group 2][key-chunk][8 rows][16 B]
+    uint8_t p[2][2 * P_QSTRIDE];  // [group parity] P^T fp16: [q-group 2][key-chunk][8 rows][16 B]
     float red[2][4][16];      // cross-warp max / sum partials
     float run_m[2][16];       // [group parity] running row max (raw score units)
     float run_l[2][16];       // [group parity] running denominator
@@ -97,8 +97,23 @@ struct __align__(1024) SelSmem {
     uint32_t tmem_base;
 };
 
+// n / d for n, d < 2^31 by a multiply-high (Granlund-Montgomery): the per-window and
+// per-item index math runs on every gathered window, where a hardware-less integer
+// division costs ~20 instructions
+struct FastDiv {
+    uint32_t d, m, s;
+    void init(uint32_t dd) {
+        d = dd;
+        s = 0;
+        while ((1u << s) < d) ++s;
+        m = (uint32_t)(((uint64_t(1) << 32) * ((uint64_t(1) << s) - d)) / d + 1);
+    }
+    __device__ __forceinline__ uint32_t div(uint32_t n) const { return (__umulhi(n, m) + n) >> s; }
+};
+
 struct SelTcParams {
     int heads;
+    FastDiv fd_windows, fd_wpf, fd_ww;  // L.windows (item -> head), L.wins_per_frame, L.wins_w
     DevLayout L;
     RowSource rows;
     float scale, c2;  // c2 = scale * log2(e)
@@ -112,11 +127,15 @@ struct SelTcParams {
     const float* prior_o;     // hybrid fast path: reference-frame softmax, merged by LSE (or null)
     const float* prior_lse;
     const uint8_t* wg_prep;  // [H][2][8192] bytes
-    // split: f32 Q/K/V as bf16 hi + lo planes (every window gathered twice, into two
-    // consecutive ring stages); S = Kh.Qh + Kl.Qh + Kh.Ql, O += Vh.Ph + Vh.Pl + Vl.Ph,
+    const unsigned* vmax;    // [H] max |v| (float bits): the V operand is fp16(v * 2^-vexp(vmax))
+    // split: f32 Q/K as bf16 hi + lo planes and V as fp16 hi + lo planes (every window
+    // gathered twice, into two consecutive ring stages); S = Kh.Qh + Kl.Qh + Kh.Ql,
+    // O += Vh.P + Vl.P,
     // G = Wgh.Qh + Wgl.Qh + Wgh.Ql. gate: fused gate + merge (else out = o_sel)
     bool split, gate;
 };
+
+__device__ __forceinline__ int vexp(float vmax) { return vmax > 0.0f ? ilogbf(vmax) - 13 : 0; }
 
 // Iterates this CTA's (item, group) sequence.
 struct GroupIt {
@@ -146,9 +165,9 @@ struct GroupIt {
     __device__ int group_windows() const { return min(GROUP_WIN, nwin - g * GROUP_WIN); }
 };
 
-__device__ __forceinline__ void window_coords(const DevLayout& L, int wid, int& c1, int& c2) {
-    const int f = wid / L.wins_per_frame, r = wid - f * L.wins_per_frame;
-    const int wr = r / L.wins_w, wc = r - wr * L.wins_w;
+__device__ __forceinline__ void window_coords(const DevLayout& L, const SelTcParams& p, int wid, int& c1, int& c2) {
+    const int f = (int)p.fd_wpf.div((uint32_t)wid), r = wid - f * L.wins_per_frame;
+    const int wr = (int)p.fd_ww.div((uint32_t)r), wc = r - wr * L.wins_w;
     c1 = wc * 4;
     c2 = f * L.grid_h + wr * 4;
 }
@@ -167,7 +186,7 @@ __global__ void __launch_bounds__(NTHREADS, SEL_CTAS)
     {
         uint4* z0 = reinterpret_cast<uint4*>(&sm.ring[0][0]);
         for (int i = threadIdx.x; i < (int)(sizeof(sm.ring) / 16); i += NTHREADS) z0[i] = make_uint4(0, 0, 0, 0);
-        uint4* z1 = reinterpret_cast<uint4*>(&sm.p[0][0][0]);
+        uint4* z1 = reinterpret_cast<uint4*>(&sm.p[0][0]);
         for (int i = threadIdx.x; i < (int)(sizeof(sm.p) / 16); i += NTHREADS) z1[i] = make_uint4(0, 0, 0, 0);
     }
     if (threadIdx.x == 0) {
@@ -216,7 +235,7 @@ __global__ void __launch_bounds__(NTHREADS, SEL_CTAS)
         int n_heads = 0;      // W_g loads issued
         int64_t n_items = 0;  // items whose Q/Wg prelude has been issued
         auto load_chunks = [&](const GroupIt& it, const CUtensorMap* tm, bool with_prelude, int my_wid) {
-            const int h = (int)(it.item / L.windows), w = (int)(it.item - (int64_t)h * L.windows);
+            const int h = (int)p.fd_windows.div((uint32_t)it.item), w = (int)(it.item - (int64_t)h * L.windows);
             if (with_prelude) {
                 if (p.gate && h != cur_head) {
                     // W_g of the new head: wait until every G MMA of the old head completed.
@@ -236,7 +255,7 @@ __global__ void __launch_bounds__(NTHREADS, SEL_CTAS)
                 if (lane == 0) {
                     mbar_arrive_expect_tx(&sm.q_full[qb], p.split ? 2 * WIN : WIN);
                     int c1, c2;
-                    window_coords(L, w, c1, c2);
+                    window_coords(L, p, w, c1, c2);
                     tma_load_4d(&sm.q[qb][0], &tm_q, &sm.q_full[qb], 0, c1, c2, h);
                     if (p.split) tma_load_4d(&sm.ql[qb][0], &tm_ql, &sm.q_full[qb], 0, c1, c2, h);
                 }
@@ -244,17 +263,17 @@ __global__ void __launch_bounds__(NTHREADS, SEL_CTAS)
             }
             const int nw = it.group_windows();
             int c1, c2;
-            window_coords(L, my_wid, c1, c2);
+            window_coords(L, p, my_wid, c1, c2);
             if (PREFETCH_AHEAD > 0 && tm == &tm_k && it.g == 0) {
                 // warm L2 with the K and V windows of the item PREFETCH_AHEAD items ahead: the
                 // ring holds about one item, so without this every item pays a DRAM round trip
                 const int64_t pi = it.item + (int64_t)PREFETCH_AHEAD * gridDim.x;
                 if (pi < p.items) {
-                    const int ph = (int)(pi / L.windows);
+                    const int ph = (int)p.fd_windows.div((uint32_t)pi);
                     const int64_t pn = p.rows.size(pi);
                     for (int64_t j = lane; j < pn; j += 32) {
                         int d1, d2;
-                        window_coords(L, p.rows.window(pi, j), d1, d2);
+                        window_coords(L, p, p.rows.window(pi, j), d1, d2);
                         tma_prefetch_4d(&tm_k, 0, d1, d2, ph);
                         tma_prefetch_4d(&tm_v, 0, d1, d2, ph);
                     }
@@ -319,7 +338,8 @@ __global__ void __launch_bounds__(NTHREADS, SEL_CTAS)
         // warp walks the stream (uniform descriptors); one elected lane issues.
         {
             const uint32_t id_s = idesc_bf16(128, 16, 0, 0);
-            const uint32_t id_o = idesc_bf16(64, 16, 1, 0);
+            const uint32_t id_o = idesc_bf16(64, 16, 1, 0);   // G^T = Wg^T . Q^T (bf16)
+            const uint32_t id_pv = idesc_f16(64, 16, 1, 0);  // O^T += V16^T . P16^T (fp16)
             int st = 0;
             uint32_t fph = 0;
             uint32_t qph[2] = {0, 0}, sph[2] = {1, 1}, pph[2] = {0, 0};
@@ -329,7 +349,7 @@ __global__ void __launch_bounds__(NTHREADS, SEL_CTAS)
             int64_t n_items = 0;
             int64_t jS = 0, jP = 0;  // global group indices of the next S / PV
             auto issue_S = [&](const GroupIt& it) {
-                const int h = (int)(it.item / L.windows);
+                const int h = (int)p.fd_windows.div((uint32_t)it.item);
                 const int qb = (int)((n_items - (it.g == 0 ? 0 : 1)) & 1);
                 if (it.g == 0) {
                     mbar_wait(&sm.q_full[qb], qph[qb]);
@@ -349,7 +369,7 @@ __global__ void __launch_bounds__(NTHREADS, SEL_CTAS)
                         const uint32_t gcol = tmem + G_COL0 + 16u * (uint32_t)gb;
                         // the last item of this head on this CTA releases W_g
                         const int64_t nxt = it.item + gridDim.x;
-                        const bool last_of_head = nxt >= p.items || (int)(nxt / L.windows) != h;
+                        const bool last_of_head = nxt >= p.items || (int)p.fd_windows.div((uint32_t)nxt) != h;
                         if (elect_one()) {
                             for (int part = 0; part < (p.split ? 3 : 2); ++part)  // Wgh.Qh, Wgl.Qh (, Wgh.Ql)
                                 for (int ks = 0; ks < 4; ++ks)
@@ -418,8 +438,7 @@ __global__ void __launch_bounds__(NTHREADS, SEL_CTAS)
                 tc_fence_after();
                 const int nw = it.group_windows();
                 const uint32_t ocol = tmem + (pb ? O_COL1 : O_COL0);
-                const uint64_t phi = umma_desc(smem_u32(&sm.p[pb][0][0]), 128, P_QSTRIDE, 0);
-                const uint64_t plo = umma_desc(smem_u32(&sm.p[pb][1][0]), 128, P_QSTRIDE, 0);
+                const uint64_t pdesc = umma_desc(smem_u32(&sm.p[pb][0]), 128, P_QSTRIDE, 0);
                 for (int c0 = 0, c = 0; c0 < nw; c0 += 8, ++c) {
                     mbar_wait(&sm.full[st], fph);
                     const int st0 = st;
@@ -444,9 +463,8 @@ __global__ void __launch_bounds__(NTHREADS, SEL_CTAS)
                         for (int ks = 0; ks < 8; ++ks) {
                             const uint64_t va = vdesc + (uint64_t)(ks * 128);
                             const uint64_t po = (uint64_t)(c * 128 + ks * 16);
-                            mma_bf16(ocol, va, phi + po, id_o, (c | ks) != 0);
-                            if (!(kDebug & 1)) mma_bf16(ocol, va, plo + po, id_o, 1);
-                            if (p.split) mma_bf16(ocol, vldesc + (uint64_t)(ks * 128), phi + po, id_o, 1);
+                            mma_bf16(ocol, va, pdesc + po, id_pv, (c | ks) != 0);
+                            if (p.split) mma_bf16(ocol, vldesc + (uint64_t)(ks * 128), pdesc + po, id_pv, 1);
                         }
                         mma_commit(&sm.empty[st0]);
                         if (p.split) mma_commit(&sm.empty[st1]);
@@ -540,18 +558,19 @@ __global__ void __launch_bounds__(NTHREADS, SEL_CTAS)
                 a8[i] = hi_half ? a_hi : acc[i];
                 z8[i] = hi_half ? z_hi : __uint_as_float(grr[i]);
             }
-            const int h = (int)(f.item / L.windows), w = (int)(f.item - (int64_t)h * L.windows);
+            const int h = (int)p.fd_windows.div((uint32_t)f.item), w = (int)(f.item - (int64_t)h * L.windows);
             const int jf_feat = 16 * qd + (lane & 15);
             const float comp = ((n_fin_items - 1) & 1) ? comp_pf1 : comp_pf0;
-            const int fr = w / L.wins_per_frame, rr = w - fr * L.wins_per_frame;
-            const int wr = rr / L.wins_w, wc = rr - wr * L.wins_w;
+            const float vscale = ldexpf(1.0f, vexp(__uint_as_float(p.vmax[h])));  // undo the V16 scaling
+            const int fr = (int)p.fd_wpf.div((uint32_t)w), rr = w - fr * L.wins_per_frame;
+            const int wr = (int)p.fd_ww.div((uint32_t)rr), wc = rr - wr * L.wins_w;
             const int tok0 = fr * L.tokens_per_frame + wr * 4 * L.grid_w + wc * 4;
             float* outh = p.out + (int64_t)h * p.out_hs;
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
                 const int q = i + 8 * hi_half;
                 const int tok = tok0 + (q >> 2) * L.grid_w + (q & 3);
-                float sel = a8[i] * __frcp_rn(sm.run_l[fb][q]);
+                float sel = a8[i] * __fdividef(vscale, sm.run_l[fb][q]);
                 if (p.prior_o) {  // merge with the reference-frame partial softmax (LSE weights)
                     const int64_t ti = (int64_t)h * L.image_tokens + tok;
                     const float l1 = p.prior_lse[ti];
@@ -560,7 +579,7 @@ __global__ void __launch_bounds__(NTHREADS, SEL_CTAS)
                     const float w1 = __expf(l1 - mm), w2 = __expf(l2 - mm);
                     sel = (w1 * p.prior_o[ti * 64 + jf_feat] + w2 * sel) / (w1 + w2);
                 }
-                const float g = __frcp_rn(1.0f + __expf(-z8[i]));
+                const float g = __fdividef(1.0f, 1.0f + __expf(-z8[i]));
                 outh[(int64_t)tok * p.out_rs + jf_feat] = p.gate ? g * comp + (1.0f - g) * sel : sel;
                 if (p.o_sel_ctx || p.gate_ctx) {
                     const int64_t ti = (int64_t)h * L.image_tokens + tok;
@@ -583,8 +602,8 @@ __global__ void __launch_bounds__(NTHREADS, SEL_CTAS)
             const int sb = (int)(j & 1);
             const int nkeys = it.group_windows() * 16;
             if (it.g == 0 && p.gate) {  // the compressed-branch row this item merges with, a full item ahead
-                const int ih = (int)(it.item / L.windows), iw = (int)(it.item - (int64_t)ih * L.windows);
-                const float cv = __ldg(p.o_comp + ((int64_t)ih * L.windows + iw) * 64 + 16 * qd + (lane & 15));
+                // o_comp is [H][W][64] with W = L.windows: row = item
+                const float cv = __ldg(p.o_comp + it.item * 64 + 16 * qd + (lane & 15));
                 if (n_started & 1) comp_pf1 = cv;
                 else comp_pf0 = cv;
                 ++n_started;
@@ -627,7 +646,7 @@ __global__ void __launch_bounds__(NTHREADS, SEL_CTAS)
 #pragma unroll
                     for (int e = 0; e < 8; ++e) {
                         const int key = 128 * c + 32 * qd + 16 * hf + t1 + 8 * ((e >> 1) & 1);
-                        if (key >= nkeys) s[c][hf][e] = -INFINITY;
+                        if (nkeys < GROUP_WIN * 16 && key >= nkeys) s[c][hf][e] = -INFINITY;
                         const int slot = (e & 1) | ((e >> 2) << 1);  // query 2*t0 + (e&1) + 8*(e>>2)
                         mx[slot] = fmaxf(mx[slot], s[c][hf][e]);
                     }
@@ -654,7 +673,7 @@ __global__ void __launch_bounds__(NTHREADS, SEL_CTAS)
                 const float gm = fmaxf(fmaxf(sm.red[0][0][q], sm.red[0][1][q]), fmaxf(sm.red[0][2][q], sm.red[0][3][q]));
                 const float mold = it.g == 0 ? -INFINITY : sm.run_m[ob][q];
                 const float mnew = fmaxf(mold, gm);
-                al[sl] = mold == -INFINITY ? 0.0f : exp2f((mold - mnew) * p.c2);
+                al[sl] = mold == -INFINITY ? 0.0f : ex2_approx((mold - mnew) * p.c2);
                 mq[sl] = mnew * p.c2;
                 if (stat_owner) {
                     sm.run_m[pb][q] = mnew;
@@ -662,8 +681,8 @@ __global__ void __launch_bounds__(NTHREADS, SEL_CTAS)
                 }
             }
             float sum[4] = {0.f, 0.f, 0.f, 0.f};
-            // P = exp(scale*(s - m)); stored as bf16 hi + lo through stmatrix.trans
-            const uint32_t pbase_hi = smem_u32(&sm.p[pb][0][0]), pbase_lo = smem_u32(&sm.p[pb][1][0]);
+            // P = exp(scale*(s - m)); stored as fp16 through stmatrix.trans
+            const uint32_t pbase = smem_u32(&sm.p[pb][0]);
             const int mi = lane >> 3, rr = lane & 7;
 #pragma unroll
             for (int c = 0; c < 4; ++c) {
@@ -678,20 +697,13 @@ __global__ void __launch_bounds__(NTHREADS, SEL_CTAS)
                         pv[e] = ex2_approx(fmaf(s[c][hf][e], p.c2, -mq[slot]));
                         sum[slot] += pv[e];
                     }
-                    // P = hi + lo: hi = P truncated to bf16 (one PRMT per pair), lo = P - hi rounded
-                    uint32_t hi[4], lo[4];
+                    uint32_t p16[4];
 #pragma unroll
-                    for (int e2 = 0; e2 < 4; ++e2) {
-                        const uint32_t u0 = __float_as_uint(pv[2 * e2]), u1 = __float_as_uint(pv[2 * e2 + 1]);
-                        hi[e2] = __byte_perm(u0, u1, 0x7632);
-                        lo[e2] = pack_bf16(pv[2 * e2] - __uint_as_float(u0 & 0xffff0000u),
-                                           pv[2 * e2 + 1] - __uint_as_float(u1 & 0xffff0000u));
-                    }
+                    for (int e2 = 0; e2 < 4; ++e2) p16[e2] = pack_f16(pv[2 * e2], pv[2 * e2 + 1]);
                     // matrix mi: keys +8*(mi&1), queries 8*(mi>>1); memory row rr = query
                     const int kc = (128 * c + 32 * qd + 16 * hf) / 8 + (mi & 1);
                     const uint32_t off = (uint32_t)((mi >> 1) * P_QSTRIDE + kc * 128 + rr * 16);
-                    stmatrix_x4_trans(pbase_hi + off, hi[0], hi[1], hi[2], hi[3]);
-                    stmatrix_x4_trans(pbase_lo + off, lo[0], lo[1], lo[2], lo[3]);
+                    stmatrix_x4_trans(pbase + off, p16[0], p16[1], p16[2], p16[3]);
                 }
             }
 #ifdef SELECT_PROF
@@ -807,8 +819,8 @@ bool make_window_map(CUtensorMap* m, const TensorRef& t, int heads, const DevLay
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-bool tensor_ok(const TensorRef& t) {
-    return t.dtype == GSA_DTYPE_BF16 && t.rs >= 64 && t.rs % 8 == 0 && t.hs % 8 == 0 &&
+bool tensor_ok(const TensorRef& t, int dtype = GSA_DTYPE_BF16) {
+    return t.dtype == dtype && t.rs >= 64 && t.rs % 8 == 0 && t.hs % 8 == 0 &&
            (reinterpret_cast<uintptr_t>(t.data) & 15) == 0;
 }
 
@@ -819,8 +831,9 @@ bool tc_select_supported(const SelectArgs& a) {
     // and base), so a supported call never fails on shape grounds. f32 inputs reach it as
     // bf16 hi/lo planes (pack_select_inputs in abi.cu)
     const bool split = a.ql.data != nullptr;
-    return a.dim == 64 && a.L.s == 4 && a.Lkv.s == 4 && tensor_ok(a.q) && tensor_ok(a.k) && tensor_ok(a.v) &&
-           (!split || (tensor_ok(a.ql) && tensor_ok(a.kl) && tensor_ok(a.vl))) &&
+    return a.dim == 64 && a.L.s == 4 && a.Lkv.s == 4 && tensor_ok(a.q) && tensor_ok(a.k) &&
+           tensor_ok(a.v16, kDtypeF16) && a.vmax &&
+           (!split || (tensor_ok(a.ql) && tensor_ok(a.kl) && tensor_ok(a.v16l, kDtypeF16))) &&
            (!a.w_g || (a.o_comp && a.wg_prep)) && get_encode() != nullptr;
 }
 
@@ -830,12 +843,13 @@ cudaError_t tc_select(const SelectArgs& a, cudaStream_t st) {
     if (!tc_select_supported(a)) return cudaErrorNotSupported;
     const bool split = a.ql.data != nullptr, gate = a.w_g != nullptr;
     CUtensorMap tq, tk, tv, tql, tkl, tvl;
+    // (the fp16 V planes move through the 2-byte bf16 map type bit for bit)
     if (!make_window_map(&tq, a.q, a.heads, a.L) || !make_window_map(&tk, a.k, a.heads, a.Lkv) ||
-        !make_window_map(&tv, a.v, a.heads, a.Lkv))
+        !make_window_map(&tv, a.v16, a.heads, a.Lkv))
         return cudaErrorNotSupported;
     if (split) {
         if (!make_window_map(&tql, a.ql, a.heads, a.L) || !make_window_map(&tkl, a.kl, a.heads, a.Lkv) ||
-            !make_window_map(&tvl, a.vl, a.heads, a.Lkv))
+            !make_window_map(&tvl, a.v16l, a.heads, a.Lkv))
             return cudaErrorNotSupported;
     } else {
         tql = tq;
@@ -853,6 +867,9 @@ cudaError_t tc_select(const SelectArgs& a, cudaStream_t st) {
     p.scale = a.scale;
     p.c2 = a.scale * 1.4426950408889634f;
     p.items = (int64_t)a.heads * a.L.windows;
+    p.fd_windows.init((uint32_t)a.L.windows);
+    p.fd_wpf.init((uint32_t)a.L.wins_per_frame);
+    p.fd_ww.init((uint32_t)a.L.wins_w);
     p.o_comp = a.o_comp;
     p.out = a.out;
     p.out_hs = a.out_hs;
@@ -865,6 +882,7 @@ cudaError_t tc_select(const SelectArgs& a, cudaStream_t st) {
     p.wg_prep = a.wg_prep;
     p.split = split;
     p.gate = gate;
+    p.vmax = a.vmax;
     int dev = 0, nsm = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);

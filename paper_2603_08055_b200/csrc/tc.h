@@ -14,10 +14,13 @@ constexpr int kMaxTopK = 10240;
 
 // dense attention (special tokens, tiled_attention, dense baseline)
 bool tc_dense_supported(const gsa_tensor& q, const gsa_tensor& k, const gsa_tensor& v);
-size_t tc_dense_workspace_bytes(int heads, int mq, int mk);
+// with_v16: room for converting V (false when the caller passes its V16 planes)
+size_t tc_dense_workspace_bytes(int heads, int mq, int mk, bool with_v16 = true);
+// V16/vmax: V already as fp16 planes [H][k.rows][64] (launch_v16), else converted here
 cudaError_t tc_dense_attention(const gsa_tensor& q, const gsa_tensor& k, const gsa_tensor& v, float scale,
                                int q_row_offset, int mq, float* out, int64_t out_hs, int64_t out_rs,
-                               int out_row_offset, float* lse, void* ws, size_t ws_bytes, cudaStream_t st);
+                               int out_row_offset, float* lse, void* ws, size_t ws_bytes, cudaStream_t st,
+                               const __half* v16 = nullptr, const unsigned* vmax = nullptr);
 
 // compressed attention + top-k over pooled f32 [H][W][d] tensors: tensor-core
 // approximate scores + exact re-scoring of the boundary candidates when

@@ -239,6 +239,27 @@ __device__ __forceinline__ void tmem_st_32x32b_x32(uint32_t taddr, const uint32_
         : "memory");
 }
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+// 2^x for a pair on the FMA pipe (MUFU offload, the FA4 trick): x = j + f, j = rint(x) by
+// the 1.5 * 2^23 add, f in [-0.5, 0.5], 2^f by a degree-4 near-minimax polynomial (max
+// relative error 2.6e-6, far below the fp16 rounding of P), 2^j added to the exponent
+// bits. x is clamped to >= -120 (masked keys are -inf): the result is then < 2^-119,
+// zero once P is rounded to fp16.
+__device__ __forceinline__ float2 exp2_poly2(float2 x) {
+    x.x = fmaxf(x.x, -120.0f);
+    x.y = fmaxf(x.y, -120.0f);
+    const float2 magic = make_float2(12582912.0f, 12582912.0f);
+    const float2 j = __fadd2_rn(x, magic);                                     // rint(x) in the low bits
+    const float2 jf = __fadd2_rn(j, make_float2(-12582912.0f, -12582912.0f));  // rint(x) as a float
+    const float2 f = __ffma2_rn(jf, make_float2(-1.0f, -1.0f), x);             // x - rint(x), exact
+    float2 p = __ffma2_rn(make_float2(0.009570099413394928f, 0.009570099413394928f), f,
+                          make_float2(0.05591786280274391f, 0.05591786280274391f));
+    p = __ffma2_rn(p, f, make_float2(0.240247443318367f, 0.240247443318367f));
+    p = __ffma2_rn(p, f, make_float2(0.6931217908859253f, 0.6931217908859253f));
+    p = __ffma2_rn(p, f, make_float2(0.9999992847442627f, 0.9999992847442627f));
+    // (bits(j) << 23) == rint(x) << 23 mod 2^32: the magic's own bits shift out
+    return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(j.x) << 23)),
+                       __int_as_float(__float_as_int(p.y) + (__float_as_int(j.y) << 23)));
+}
 __device__ __forceinline__ float ex2_approx(float x) {
     float y;
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));

@@ -13,6 +13,12 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 GOLDEN = os.path.join(ROOT, "tests", "golden")
 
+# Attention outputs of the tensor-core kernels: P (and V, scaled per head by a power of
+# two) enter the P.V products as fp16, so each output carries |dO| <= 2^-12 * max|v| of P
+# rounding (observed ~1e-4 .. 2e-4 abs on N(0,1) values). Asserted well inside the north
+# star's max-abs 2e-2 / rel-L2 1e-3 (BASELINE.json): max-abs 1e-3, rel-L2 1e-3.
+P16_ABS, P16_REL = 1e-3, 1e-3
+
 
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA B200 (sm_100a) device")

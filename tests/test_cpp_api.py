@@ -19,7 +19,7 @@ import subprocess
 import numpy as np
 import pytest
 
-from conftest import ROOT, rel_l2
+from conftest import P16_ABS, P16_REL, ROOT, rel_l2
 
 CPP = os.path.join(ROOT, "tests", "cpp")
 LIB = os.path.join(ROOT, "paper_2603_08055_b200", "libgsa_sm100.so")
@@ -86,10 +86,10 @@ def test_cpp_api_matches_reference(tmp_path, ref, lt, heads, model_dim, top_k, v
     np.testing.assert_array_equal(d["topk"], rf["topk"])
     np.testing.assert_array_equal(d["qc"].view(np.uint32), rf["qc"].view(np.uint32))
     # regression bounds inside the north star: O'_comp carries the fp16 P.V error
-    assert np.abs(d["out"] - rf["out"]).max() < 1e-3 and rel_l2(d["out"], rf["out"]) < 2e-4
+    assert np.abs(d["out"] - rf["out"]).max() < P16_ABS and rel_l2(d["out"], rf["out"]) < 5e-4
     assert rel_l2(d["o_comp"], rf["o_comp"]) < 1e-3
     assert np.abs(d["gate"] - rf["gate"]).max() < 1e-5
-    assert np.abs(d["o_sel"] - rf["o_sel"]).max() < 1e-4
+    assert np.abs(d["o_sel"] - rf["o_sel"]).max() < P16_ABS and rel_l2(d["o_sel"], rf["o_sel"]) < P16_REL
     offs, ids = ref.plan(rf["topk"], lt, variant, 2)
     np.testing.assert_array_equal(d["plan_offsets"], offs)
     np.testing.assert_array_equal(d["plan_ids"], ids)
@@ -112,14 +112,14 @@ def test_cpp_api_matches_reference(tmp_path, ref, lt, heads, model_dim, top_k, v
     assert rel_l2(d["op_o_comp"], oc) < 1e-3
     np.testing.assert_array_equal(d["op_plan_ids"], ids)
     osel, _ = ref.block_sparse(q[:, Ms:], k[:, Ms:], v[:, Ms:], lt, offs, ids, scale)
-    assert np.abs(d["op_o_sel"] - osel).max() < 1e-4
+    assert np.abs(d["op_o_sel"] - osel).max() < P16_ABS and rel_l2(d["op_o_sel"], osel) < P16_REL
     assert np.abs(d["op_gate"] - ref.gate(q[:, Ms:], d["w_g"])).max() < 1e-5
     np.testing.assert_array_equal(d["op_up"], ref.upsample(d["op_o_comp"], lt))
     if Ms:
         ospec, _ = ref.tiled_attention(q[:, :Ms], k, v, scale)
         # f32 operands: S on tensor cores from a 3-term bf16 split, P.V with P and V in fp16
         # (the compressed-branch kernel in softmax-only mode): ~2^-11 relative in the output
-        assert np.abs(d["op_o_spec"] - ospec).max() < 5e-4 and rel_l2(d["op_o_spec"], ospec) < 1e-3
+        assert np.abs(d["op_o_spec"] - ospec).max() < P16_ABS and rel_l2(d["op_o_spec"], ospec) < P16_REL
     # pinned plan = the plan gsa_forward realised: compressed branch without top-k
     assert np.abs(d["op_out_with_plan"] - rf["out"]).max() < 1e-3
     assert Mi > 0

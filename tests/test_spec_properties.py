@@ -24,7 +24,7 @@ from __future__ import annotations
 import numpy as np
 import pytest
 
-from conftest import rel_l2
+from conftest import P16_ABS, rel_l2
 
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
@@ -192,7 +192,7 @@ def test_gather_mask_equivalence_100_plans(gsa, ref):
                                  torch.empty(0, dtype=torch.int32, device="cuda"))
         out, lse = gsa.block_sparse_attention(dev(q, dt), dev(k, dt), dev(v, dt), plan, gl, 0.125)
         o_m, den = ref.masked_attention(q, k, v, lt, offs, ids, 0.125)
-        assert np.abs(out.cpu().numpy() - o_m).max() <= 1e-4, i
+        assert np.abs(out.cpu().numpy() - o_m).max() <= P16_ABS, i
         rel = np.abs(np.exp(lse.cpu().numpy().astype(np.float64)) / den - 1.0).max()
         assert rel <= 1e-5, (i, rel)
 

@@ -92,4 +92,4 @@ def test_stack_layer_within_tolerance_of_reference(gsa, ref):
     rf = ref.forward(f(q), f(k), f(v), f(st.w_g[1]), lt, top_k=8, variant=0, ref_stride=2)
     np.testing.assert_array_equal(ctx.topk.cpu().numpy(), rf["topk"])
     o = f(out)
-    assert np.abs(o - rf["out"]).max() < 1e-3 and rel_l2(o, rf["out"]) < 2e-4
+    assert np.abs(o - rf["out"]).max() < 1e-3 and rel_l2(o, rf["out"]) < 5e-4
