@@ -159,7 +159,7 @@ __device__ __forceinline__ void setmaxnreg_inc() { asm volatile("setmaxnreg.inc.
 __device__ __forceinline__ void setmaxnreg_dec() { asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(PROD_REGS) : "memory"); }
 
 #ifndef COMP_POLY
-#define COMP_POLY 0  // exp2 of every COMP_POLY-th pair by polynomial on the FMA pipe (0: all on MUFU)
+#define COMP_POLY 0  // exp2 of every COMP_POLY-th pair by polynomial on the FMA pipe (measured: 3, 4, 6 all slower -- K2 is not MUFU-bound)
 #endif
 #ifndef COMP_STAGE
 #define COMP_STAGE 0  // 1: candidates read back from a shared staging row (measured: 71.0 vs 68.7 ms compress at V=1000 for the register select tree)

@@ -65,7 +65,7 @@ constexpr float RESCALE_LOG2 = 8.0f;
 #endif
 constexpr int PB_UNROLL = FA_PB_UNROLL;
 #ifndef FA_POLY
-#define FA_POLY 0  // exp2 of every FA_POLY-th pair by polynomial on the FMA pipe (0: all on MUFU)
+#define FA_POLY 3  // exp2 of every FA_POLY-th pair by polynomial on the FMA pipe (measured at V=1000: special 35.3 -> 32.5 ms with 3; 0: all on MUFU)
 #endif
 
 #ifndef FA_PF
