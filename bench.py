@@ -289,6 +289,8 @@ def main():
     ap.add_argument("--topk", type=int, default=32)
     ap.add_argument("--e2e-heads-per-group", type=int, default=2,
                     help="e2e host pipeline granularity: heads per H2D / compute / D2H group")
+    ap.add_argument("--e2e-slots", type=int, default=2,
+                    help="e2e host pipeline device buffer sets (2: H2D of group g+2 waits for compute g)")
     ap.add_argument("--data", default="normal", choices=["normal", "clustered"],
                     help="synthetic Q/K/V: iid N(0,1) (worst case for selection locality) or per-view clusters")
     ap.add_argument("--layers", type=int, default=1,
@@ -330,7 +332,7 @@ def main():
     L = gsa.build_token_layout(*lt)
     params = gsa.GsaParams(window_s=S, top_k=TOPK, variant=1 if args.hybrid else 0,
                            ref_stride=args.hybrid if args.hybrid else 100)
-    geometry_default = (GRID_H, GRID_W, SPECIAL_PER_VIEW, TOPK, args.hybrid) == (36, 36, 5, 32, 0)
+    geometry_default = (GRID_H, GRID_W, SPECIAL_PER_VIEW, TOPK, args.hybrid, args.data) == (36, 36, 5, 32, 0, "normal")
     q, k, v, wg = synth_qkv(torch, args.views, data=args.data, seed=7, device=dev)
     out = torch.empty(HEADS, G["M"], DIM, device=dev)
     ws = gsa.Workspace()
@@ -427,8 +429,19 @@ def main():
             per_stage[n_] = {"ms": round(t_, 3), "tflops": round(flops[n_] / (t_ / 1e3) / 1e12, 1),
                              "tc_frac": round(flops[n_] / (t_ / 1e3) / 1e12 / tc_peak, 4)}
         if n_ in bytes_:
-            per_stage.setdefault(n_, {"ms": round(t_, 3)})["gbs"] = round(bytes_[n_] / (t_ / 1e3) / 1e9, 1)
-            per_stage[n_]["hbm_frac"] = round(bytes_[n_] / (t_ / 1e3) / 1e9 / hbm, 4)
+            gb = bytes_[n_] / (t_ / 1e3) / 1e9
+            if n_ == "select":  # algorithmic gathers: K + V windows per plan row, served by L2 or HBM
+                per_stage.setdefault(n_, {"ms": round(t_, 3)})["gather_gbs"] = round(gb, 1)
+            else:
+                per_stage.setdefault(n_, {"ms": round(t_, 3)})["gbs"] = round(gb, 1)
+                per_stage[n_]["hbm_frac"] = round(gb / hbm, 4)
+        if os.path.exists(prof) and world == 1 and geometry_default:
+            tr = json.load(open(prof)).get(n_)
+            if tr and tr.get("views") == args.views and n_ in per_stage:
+                # DRAM bytes per launch measured by ncu on this workload over this run's stage time
+                dg = tr["dram_gbytes_per_launch"] / (t_ / 1e3)
+                per_stage[n_]["dram_gbs_ncu_bytes"] = round(dg, 1)
+                per_stage[n_]["dram_frac"] = round(dg / hbm, 4)
 
     line = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
@@ -461,7 +474,7 @@ def main():
             dq = dk = dv = None
             # host -> host through the public API, pipelined over head groups
             # (H2D of group g+1 and D2H of group g-1 overlap the layer on group g)
-            pipe = gsa.HostPipeline(heads_per_group=args.e2e_heads_per_group, device=dev)
+            pipe = gsa.HostPipeline(heads_per_group=args.e2e_heads_per_group, device=dev, slots=args.e2e_slots)
 
             def e2e_step():
                 pipe.forward(hq, hk, hv, wg, L, params, hout)
@@ -500,6 +513,8 @@ def main():
         e_ms = float(te.item())
         line["e2e"] = {"value": M / (e_ms / 1e3), "unit": "tokens/s", "ms_per_step": e_ms,
                        "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h}
+        if not sharded:
+            line["e2e"]["pipeline"] = {"heads_per_group": args.e2e_heads_per_group, "slots": args.e2e_slots}
         del hq, hk, hv, hout, dq
 
     # the paper's sparse-vs-dense comparison on the same GPU: fastest library dense

@@ -497,15 +497,16 @@ class HostPipeline:
     Device buffers are allocated once per (shape, dtype) and reused.
     """
 
-    def __init__(self, heads_per_group: int = 2, device="cuda"):
+    def __init__(self, heads_per_group: int = 2, device="cuda", slots: int = 2):
         self.g = heads_per_group
+        self.slots = max(2, slots)  # device buffer sets (measured at V=1000: 2 and 3 equal, the copies are PCIe-bound)
         self.device = torch.device(device)
         self.s_in = torch.cuda.Stream(self.device)
         self.s_comp = torch.cuda.Stream(self.device)
         self.s_out = torch.cuda.Stream(self.device)
         self._bufs = None
         self._key = None
-        self.ws = [Workspace(), Workspace()]
+        self.ws = [Workspace() for _ in range(self.slots)]
 
     def _alloc(self, q, out_dtype=torch.float32):
         H, M, d = q.shape
@@ -514,7 +515,8 @@ class HostPipeline:
             g = min(self.g, H)
             mk = lambda dt: torch.empty(g, M, d, dtype=dt, device=self.device)  # noqa: E731
             # double-buffered device slots per head group
-            self._bufs = [dict(q=mk(q.dtype), k=mk(q.dtype), v=mk(q.dtype), out=mk(out_dtype)) for _ in range(2)]
+            self._bufs = [dict(q=mk(q.dtype), k=mk(q.dtype), v=mk(q.dtype), out=mk(out_dtype))
+                          for _ in range(self.slots)]
             self._key = key
         return self._bufs
 
@@ -541,22 +543,23 @@ class HostPipeline:
         cur = torch.cuda.current_stream(self.device)
         for s in (self.s_in, self.s_comp, self.s_out):
             s.wait_stream(cur)
+        S = self.slots
         for i, (h0, h1) in enumerate(groups):
-            b = bufs[i & 1]
+            b = bufs[i % S]
             n = h1 - h0
             with torch.cuda.stream(self.s_in):
-                if i >= 2:  # the slot's previous compute must be done reading it
-                    self.s_in.wait_event(ev_comp[i - 2])
+                if i >= S:  # the slot's previous compute must be done reading it
+                    self.s_in.wait_event(ev_comp[i - S])
                 b["q"][:n].copy_(q_host[h0:h1], non_blocking=True)
                 b["k"][:n].copy_(k_host[h0:h1], non_blocking=True)
                 b["v"][:n].copy_(v_host[h0:h1], non_blocking=True)
                 ev_in[i].record(self.s_in)
             with torch.cuda.stream(self.s_comp):
                 self.s_comp.wait_event(ev_in[i])
-                if i >= 2:  # the slot's previous output must be copied out
-                    self.s_comp.wait_event(ev_out[i - 2])
+                if i >= S:  # the slot's previous output must be copied out
+                    self.s_comp.wait_event(ev_out[i - S])
                 gsa_forward(b["q"][:n], b["k"][:n], b["v"][:n], w_g[h0:h1], layout, params,
-                            out=b["out"][:n], workspace=self.ws[i & 1])
+                            out=b["out"][:n], workspace=self.ws[i % S])
                 ev_comp[i].record(self.s_comp)
             with torch.cuda.stream(self.s_out):
                 self.s_out.wait_event(ev_comp[i])
