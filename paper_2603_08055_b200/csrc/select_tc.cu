@@ -73,6 +73,9 @@ constexpr int P_QSTRIDE = GROUP_WIN * 256; // bytes per 8-query half of a P^T bu
 constexpr uint32_t S_COLS = (GROUP_WIN / 8) * 16;
 constexpr uint32_t S_COL0 = 0, S_COL1 = S_COLS, O_COL0 = 2 * S_COLS, O_COL1 = O_COL0 + 16, G_COL0 = O_COL1 + 16;
 constexpr uint32_t TMEM_COLS = (G_COL0 + 16 * NGB <= 128) ? 128 : 256;  // power of two >= the layout
+#ifndef SEL_L2HINT
+#define SEL_L2HINT 0  // 1: K/V gathers evict_last, query tiles evict_first, outputs st.cs (measured neutral at V=1000)
+#endif
 #ifndef SEL_PF
 #define SEL_PF 0
 #endif
@@ -230,6 +233,7 @@ __global__ void __launch_bounds__(NTHREADS, SEL_CTAS)
         // window's TMA; lane 0 arms the stage barrier first.
         int st = 0;
         uint32_t eph = 1;  // empty barriers: first pass succeeds
+        const uint64_t pol_last = policy_evict_last(), pol_first = policy_evict_first();
         uint32_t qph[2] = {1, 1};
         int cur_head = -1;
         int n_heads = 0;      // W_g loads issued
@@ -256,8 +260,13 @@ __global__ void __launch_bounds__(NTHREADS, SEL_CTAS)
                     mbar_arrive_expect_tx(&sm.q_full[qb], p.split ? 2 * WIN : WIN);
                     int c1, c2;
                     window_coords(L, p, w, c1, c2);
-                    tma_load_4d(&sm.q[qb][0], &tm_q, &sm.q_full[qb], 0, c1, c2, h);
-                    if (p.split) tma_load_4d(&sm.ql[qb][0], &tm_ql, &sm.q_full[qb], 0, c1, c2, h);
+                    if (SEL_L2HINT) {
+                        tma_load_4d_hint(&sm.q[qb][0], &tm_q, &sm.q_full[qb], 0, c1, c2, h, pol_first);
+                        if (p.split) tma_load_4d_hint(&sm.ql[qb][0], &tm_ql, &sm.q_full[qb], 0, c1, c2, h, pol_first);
+                    } else {
+                        tma_load_4d(&sm.q[qb][0], &tm_q, &sm.q_full[qb], 0, c1, c2, h);
+                        if (p.split) tma_load_4d(&sm.ql[qb][0], &tm_ql, &sm.q_full[qb], 0, c1, c2, h);
+                    }
                 }
                 ++n_items;
             }
@@ -286,8 +295,13 @@ __global__ void __launch_bounds__(NTHREADS, SEL_CTAS)
                     mbar_wait(&sm.empty[st], eph);
                     if (lane == 0) mbar_arrive_expect_tx(&sm.full[st], nc * WIN);
                     __syncwarp();
-                    if (lane >= c0 && lane < c0 + nc)
-                        tma_load_4d(&sm.ring[st][(lane - c0) * WIN], part ? tml : tm, &sm.full[st], 0, c1, c2, h);
+                    if (lane >= c0 && lane < c0 + nc) {
+                        if (SEL_L2HINT)
+                            tma_load_4d_hint(&sm.ring[st][(lane - c0) * WIN], part ? tml : tm, &sm.full[st], 0, c1, c2, h,
+                                             pol_last);
+                        else
+                            tma_load_4d(&sm.ring[st][(lane - c0) * WIN], part ? tml : tm, &sm.full[st], 0, c1, c2, h);
+                    }
                     if (++st == NS) {
                         st = 0;
                         eph ^= 1;
@@ -580,7 +594,11 @@ __global__ void __launch_bounds__(NTHREADS, SEL_CTAS)
                     sel = (w1 * p.prior_o[ti * 64 + jf_feat] + w2 * sel) / (w1 + w2);
                 }
                 const float g = __fdividef(1.0f, 1.0f + __expf(-z8[i]));
-                outh[(int64_t)tok * p.out_rs + jf_feat] = p.gate ? g * comp + (1.0f - g) * sel : sel;
+                const float ov = p.gate ? g * comp + (1.0f - g) * sel : sel;
+                if (SEL_L2HINT)
+                    __stcs(outh + (int64_t)tok * p.out_rs + jf_feat, ov);  // streamed: keep L2 for the K/V gathers
+                else
+                    outh[(int64_t)tok * p.out_rs + jf_feat] = ov;
                 if (p.o_sel_ctx || p.gate_ctx) {
                     const int64_t ti = (int64_t)h * L.image_tokens + tok;
                     if (p.o_sel_ctx) p.o_sel_ctx[ti * 64 + jf_feat] = sel;
