@@ -679,7 +679,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     for (int e2 = 0; e2 < 16; ++e2) {
                         const float2 x = make_float2(__uint_as_float(v[2 * e2]), __uint_as_float(v[2 * e2 + 1]));
                         const float2 a = __ffma2_rn(x, c2v, nmc);
-                        const float2 pv = (COMP_POLY > 0 && e2 % COMP_POLY == COMP_POLY - 1)
+                        const float2 pv = (COMP_POLY > 0 && e2 % (COMP_POLY > 0 ? COMP_POLY : 1) == COMP_POLY - 1)
                                               ? exp2_poly2(a)
                                               : make_float2(ex2_approx(a.x), ex2_approx(a.y));
                         lsum2[e2 & 1] = __fadd2_rn(lsum2[e2 & 1], pv);  // the denominator sums the exact f32 P

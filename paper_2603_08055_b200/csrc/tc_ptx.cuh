@@ -60,7 +60,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     while (!mbar_try_wait(bar, parity)) {
         if ((++n & 1023) == 0) {
             const uint64_t dt = globaltimer_ns() - t0;
-            if (!reported && dt > 4000000000ull) {
+            if (!reported && dt > 4000000000ull && (threadIdx.x & 31) == 0) {  // one line per warp (printf buffer)
                 printf("gsa watchdog: block (%d,%d,%d) thread %d stuck on mbarrier smem+0x%x parity %u\n", blockIdx.x,
                        blockIdx.y, blockIdx.z, threadIdx.x, smem_u32(bar), parity);
                 reported = true;
