@@ -33,11 +33,6 @@ namespace {
 
 using namespace ptx;
 
-// bring-up switches, compile-time only (-DGSA_DEBUG_FA=<bits>; 0 in every shipped build)
-#ifndef GSA_DEBUG_FA
-#define GSA_DEBUG_FA 0
-#endif
-constexpr int kDebug = GSA_DEBUG_FA;
 
 #ifndef FA_NS
 #define FA_NS 12  // 12 x 16 KB: measured special 39.6 -> 39.1 ms at V=1000 (8 stages)

@@ -41,11 +41,6 @@ namespace {
 
 using namespace ptx;
 
-// bring-up switches, compile-time only (-DGSA_DEBUG_SELECT=<bits>; 0 in every shipped build)
-#ifndef GSA_DEBUG_SELECT
-#define GSA_DEBUG_SELECT 0
-#endif
-constexpr int kDebug = GSA_DEBUG_SELECT;
 
 // Two CTAs per SM (SEL_CTAS): the per-item chain (gather -> S -> softmax -> PV ->
 // epilogue) is latency-bound with one consumer warpgroup, so a second CTA hides it.
