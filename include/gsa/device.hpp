@@ -10,9 +10,11 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <cstring>
 #include <string>
+#include <thread>
 #include <type_traits>
 #include <vector>
 
@@ -106,6 +108,99 @@ class Buffer {
     size_t bytes_ = 0;
 };
 
+// Large host <-> device copies of pageable host memory: chunks cycle through two pinned
+// staging buffers so the DMA of one chunk overlaps the host-side copy of the other, and
+// each host-side copy is split over worker threads (one thread copies ~10 GB/s; PCIe moves
+// ~50). Small copies go straight through cudaMemcpy.
+class Staging {
+  public:
+    static constexpr size_t kChunk = size_t(64) << 20;
+    static constexpr size_t kDirect = size_t(8) << 20;  // below this: plain cudaMemcpy
+
+    static Staging& get() {
+        static Staging s;
+        return s;
+    }
+    void h2d(void* dev, const void* host, size_t bytes) {
+        if (bytes < kDirect) {
+            check_cuda(cudaMemcpy(dev, host, bytes, cudaMemcpyHostToDevice), "upload");
+            return;
+        }
+        init();
+        const char* src = static_cast<const char*>(host);
+        char* dst = static_cast<char*>(dev);
+        for (size_t off = 0, i = 0; off < bytes; off += kChunk, ++i) {
+            const size_t n = std::min(kChunk, bytes - off);
+            const int b = static_cast<int>(i & 1);
+            check_cuda(cudaEventSynchronize(done_[b]), "upload");  // the slot's previous DMA
+            par_copy(pinned_[b], src + off, n);
+            check_cuda(cudaMemcpyAsync(dst + off, pinned_[b], n, cudaMemcpyHostToDevice, stream_), "upload");
+            check_cuda(cudaEventRecord(done_[b], stream_), "upload");
+        }
+        check_cuda(cudaStreamSynchronize(stream_), "upload");
+    }
+    void d2h(void* host, const void* dev, size_t bytes) {
+        if (bytes < kDirect) {
+            check_cuda(cudaMemcpy(host, dev, bytes, cudaMemcpyDeviceToHost), "download");
+            return;
+        }
+        init();
+        check_cuda(cudaStreamSynchronize(nullptr), "download");  // results of the legacy stream
+        const char* src = static_cast<const char*>(dev);
+        char* dst = static_cast<char*>(host);
+        const size_t chunks = (bytes + kChunk - 1) / kChunk;
+        auto issue = [&](size_t i) {
+            const size_t off = i * kChunk, n = std::min(kChunk, bytes - off);
+            check_cuda(cudaMemcpyAsync(pinned_[i & 1], src + off, n, cudaMemcpyDeviceToHost, stream_), "download");
+            check_cuda(cudaEventRecord(done_[i & 1], stream_), "download");
+        };
+        issue(0);
+        for (size_t i = 0; i < chunks; ++i) {
+            if (i + 1 < chunks) issue(i + 1);  // (its slot's host copy finished in iteration i - 1)
+            check_cuda(cudaEventSynchronize(done_[i & 1]), "download");
+            const size_t off = i * kChunk;
+            par_copy(dst + off, pinned_[i & 1], std::min(kChunk, bytes - off));
+        }
+    }
+
+    // host-side copy split over worker threads
+    static void host_copy(void* dst, const void* src, size_t n) { par_copy(dst, src, n); }
+
+  private:
+    Staging() = default;
+    ~Staging() {
+        for (int b = 0; b < 2; ++b) {
+            if (pinned_[b]) cudaFreeHost(pinned_[b]);
+            if (done_[b]) cudaEventDestroy(done_[b]);
+        }
+        if (stream_) cudaStreamDestroy(stream_);
+    }
+    void init() {
+        if (stream_) return;
+        check_cuda(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "staging stream");
+        for (int b = 0; b < 2; ++b) {
+            check_cuda(cudaMallocHost(&pinned_[b], kChunk), "staging buffer");
+            check_cuda(cudaEventCreateWithFlags(&done_[b], cudaEventDisableTiming), "staging event");
+            check_cuda(cudaEventRecord(done_[b], stream_), "staging event");
+        }
+    }
+    static void par_copy(void* dst, const void* src, size_t n) {
+        const unsigned hw = std::max(1u, std::min(8u, std::thread::hardware_concurrency()));
+        const size_t part = (n / hw + 4095) & ~size_t(4095);
+        std::vector<std::thread> th;
+        for (unsigned t = 1; t < hw && t * part < n; ++t)
+            th.emplace_back([=] {
+                std::memcpy(static_cast<char*>(dst) + t * part, static_cast<const char*>(src) + t * part,
+                            std::min(part, n - t * part));
+            });
+        std::memcpy(dst, src, std::min(part, n));
+        for (auto& x : th) x.join();
+    }
+    cudaStream_t stream_ = nullptr;
+    void* pinned_[2] = {nullptr, nullptr};
+    cudaEvent_t done_[2] = {nullptr, nullptr};
+};
+
 // bf16 round-to-nearest-even of a finite float (NaN kept quiet)
 inline uint16_t bf16_bits(float x) {
     uint32_t u;
@@ -161,12 +256,14 @@ DeviceTensor upload(const Tensor<T>& t, bool operand = false) {
     const bool bf16 = operand && compute_precision() == Precision::kBf16;
     DeviceTensor d = alloc(t.heads, t.tokens, t.dim, bf16 ? GSA_DTYPE_BF16 : GSA_DTYPE_F32);
     if (t.data.empty()) return d;
-    if (bf16) {
-        std::vector<uint16_t> tmp(t.data.size());
-        for (size_t i = 0; i < tmp.size(); ++i) tmp[i] = bf16_bits(static_cast<float>(t.data[i]));
-        check_cuda(cudaMemcpy(d.buf.get(), tmp.data(), tmp.size() * 2, cudaMemcpyHostToDevice), "upload");
+    if (bf16) {  // f32 over the bus, rounded to bf16 (RNE) on the device
+        Buffer tmp(t.data.size() * 4);
+        Staging::get().h2d(tmp.get(), t.data.data(), t.data.size() * 4);
+        check(gsa_convert(tmp.get(), GSA_DTYPE_F32, d.buf.get(), GSA_DTYPE_BF16, static_cast<int64_t>(t.data.size()),
+                          nullptr));
+        sync();
     } else {
-        check_cuda(cudaMemcpy(d.buf.get(), t.data.data(), t.data.size() * 4, cudaMemcpyHostToDevice), "upload");
+        Staging::get().h2d(d.buf.get(), t.data.data(), t.data.size() * 4);
     }
     return d;
 }
@@ -174,26 +271,44 @@ DeviceTensor upload(const Tensor<T>& t, bool operand = false) {
 template <typename U>
 Buffer upload_vector(const std::vector<U>& v) {
     Buffer b(v.size() * sizeof(U));
-    if (!v.empty()) check_cuda(cudaMemcpy(b.get(), v.data(), v.size() * sizeof(U), cudaMemcpyHostToDevice), "upload");
+    if (!v.empty()) Staging::get().h2d(b.get(), v.data(), v.size() * sizeof(U));
     return b;
 }
 
 template <typename U>
 std::vector<U> download_vector(const void* src, size_t n) {
-    std::vector<U> v(n);
-    if (n) check_cuda(cudaMemcpy(v.data(), src, n * sizeof(U), cudaMemcpyDeviceToHost), "download");
+    std::vector<U> v;
+    gsa::detail::zero_vector(v, n);
+    if (n) Staging::get().d2h(v.data(), src, n * sizeof(U));
     return v;
+}
+
+// into a host tensor of d's shape the caller already holds (e.g. allocated on a worker thread)
+template <typename T>
+void download_into(Tensor<T>& t, const DeviceTensor& d) {
+    if (t.heads != d.heads || t.tokens != d.rows || t.dim != d.dim) t = Tensor<T>(d.heads, d.rows, d.dim);
+    if (t.data.empty()) return;
+    if (d.dtype == GSA_DTYPE_BF16) {  // widened to f32 on the device
+        Buffer tmp(t.data.size() * 4);
+        check(gsa_convert(d.buf.get(), GSA_DTYPE_BF16, tmp.get(), GSA_DTYPE_F32, static_cast<int64_t>(t.data.size()),
+                          nullptr));
+        Staging::get().d2h(t.data.data(), tmp.get(), t.data.size() * 4);
+    } else {
+        Staging::get().d2h(t.data.data(), d.buf.get(), t.data.size() * 4);
+    }
 }
 
 template <typename T>
 Tensor<T> download(const DeviceTensor& d) {
     Tensor<T> t(d.heads, d.rows, d.dim);
     if (t.data.empty()) return t;
-    if (d.dtype == GSA_DTYPE_BF16) {
-        const auto bits = download_vector<uint16_t>(d.buf.get(), t.data.size());
-        for (size_t i = 0; i < bits.size(); ++i) t.data[i] = static_cast<T>(bf16_to_float(bits[i]));
+    if (d.dtype == GSA_DTYPE_BF16) {  // widened to f32 on the device
+        Buffer tmp(t.data.size() * 4);
+        check(gsa_convert(d.buf.get(), GSA_DTYPE_BF16, tmp.get(), GSA_DTYPE_F32, static_cast<int64_t>(t.data.size()),
+                          nullptr));
+        Staging::get().d2h(t.data.data(), tmp.get(), t.data.size() * 4);
     } else {
-        check_cuda(cudaMemcpy(t.data.data(), d.buf.get(), t.data.size() * 4, cudaMemcpyDeviceToHost), "download");
+        Staging::get().d2h(t.data.data(), d.buf.get(), t.data.size() * 4);
     }
     return t;
 }

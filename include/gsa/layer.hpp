@@ -13,9 +13,11 @@
 
 #include <algorithm>
 #include <cmath>
+#include <future>
 #include <vector>
 
 #include "gsa/compression.hpp"
+
 #include "gsa/device.hpp"
 #include "gsa/layout.hpp"
 #include "gsa/selection.hpp"
@@ -157,11 +159,20 @@ GsaOutput<T> gsa_forward(const Tensor<T>& x, const TokenLayout& layout, const Gs
     ctx.layout = layout;
     ctx.params = params;
     ctx.weights = weights;
-    ctx.x = x;
+    ctx.x = Tensor<T>(x.heads, x.tokens, x.dim);  // the reference keeps a copy of X (layer.hpp:124-142)
+    device::Staging::host_copy(ctx.x.data.data(), x.data.data(), x.data.size() * sizeof(T));
 
-    auto qkv = detail::project_on_device(x, weights);
+    // the host tensors this call returns (~38 GB at 1000 views) are allocated and zero-filled
+    // on worker threads while X uploads and the GPU projects and runs the layer
     const int H = weights.heads(), d = weights.dim(), M = layout.total_tokens();
     const int Ms = layout.num_special, Mi = layout.image_tokens(), W = layout.num_windows();
+    auto host = [](int a, int b, int c) {
+        return std::async(std::launch::async, [=] { return Tensor<T>(a, b, c); });
+    };
+    auto h_q = host(H, M, d), h_k = host(H, M, d), h_v = host(H, M, d), h_out = host(H, M, d);
+    auto h_osel = host(H, Mi, d), h_gate = host(H, Mi, d);
+    auto h_qc = host(H, W, d), h_kc = host(H, W, d), h_vc = host(H, W, d), h_oc = host(H, W, d);
+    auto qkv = detail::project_on_device(x, weights);
     const int forced = params.variant == SelectionVariant::kHybrid
                            ? static_cast<int>(forced_frames(layout, params.ref_stride).size()) * layout.windows_per_frame()
                            : 0;
@@ -184,21 +195,31 @@ GsaOutput<T> gsa_forward(const Tensor<T>& x, const TokenLayout& layout, const Gs
     int k_eff = 0;
     device::check(gsa_forward(&a, &b, &c, &w, &lc, &pc, &o, &cx, &k_eff, ws.get(), ws_bytes, nullptr));
 
-    ctx.q = device::download<T>(qkv.q);
-    ctx.k = device::download<T>(qkv.k);
-    ctx.v = device::download<T>(qkv.v);
-    ctx.qc = device::download<T>(qc);
-    ctx.kc = device::download<T>(kc);
-    ctx.vc = device::download<T>(vc);
-    ctx.o_comp_coarse = device::download<T>(oc);
+    ctx.q = h_q.get();
+    device::download_into(ctx.q, qkv.q);
+    ctx.k = h_k.get();
+    device::download_into(ctx.k, qkv.k);
+    ctx.v = h_v.get();
+    device::download_into(ctx.v, qkv.v);
+    ctx.qc = h_qc.get();
+    device::download_into(ctx.qc, qc);
+    ctx.kc = h_kc.get();
+    device::download_into(ctx.kc, kc);
+    ctx.vc = h_vc.get();
+    device::download_into(ctx.vc, vc);
+    ctx.o_comp_coarse = h_oc.get();
+    device::download_into(ctx.o_comp_coarse, oc);
     ctx.lse_comp = device::download_f32<T>(lse_comp, static_cast<size_t>(H) * W);
     ctx.topk = TopkResult(H, W, k_eff);
     ctx.topk.indices = device::download_vector<int32_t>(topk.get(), static_cast<size_t>(H) * W * k_eff);
     ctx.plan = build_selection_plan(ctx.topk, layout, params.variant, params.ref_stride);
-    ctx.o_sel = device::download<T>(osel);
+    ctx.o_sel = h_osel.get();
+    device::download_into(ctx.o_sel, osel);
     ctx.lse_sel = device::download_f32<T>(lse_sel, static_cast<size_t>(H) * Mi);
-    ctx.gate_vals = device::download<T>(gv);
-    r.out = device::download<T>(out);
+    ctx.gate_vals = h_gate.get();
+    device::download_into(ctx.gate_vals, gv);
+    r.out = h_out.get();
+    device::download_into(r.out, out);
     ctx.o_spec = slice_rows(r.out, 0, Ms);
     ctx.lse_spec = device::download_f32<T>(lse_spec, static_cast<size_t>(H) * Ms);
     if (stats) {

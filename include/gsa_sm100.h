@@ -293,6 +293,11 @@ int gsa_project_qkv_bf16(const void* x, int tokens, int model_dim, int64_t ldx, 
                          void* qkv, int64_t ld_qkv, gsa_stream_t stream);
 int gsa_residual_bf16(const void* x, const float* o, void* y, int64_t n, gsa_stream_t stream);
 
+/* Element-wise dtype conversion of n contiguous elements on the device (f32 <-> bf16 with
+ * round-to-nearest-even, or a plain copy for equal dtypes): the host API converts its
+ * operands on the GPU instead of in host loops (Precision::kBf16 uploads, bf16 downloads). */
+int gsa_convert(const void* src, int src_dtype, void* dst, int dst_dtype, int64_t n, gsa_stream_t stream);
+
 /* KernelStats (types.hpp:78-86) in closed form for a gsa_forward call:
  * scores_computed = H*(Ms*M + W*W); keys_attended = sum over rows of
  * |row| * s^2 * s^2 (rows have width F + k_eff). */

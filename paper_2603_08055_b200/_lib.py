@@ -95,6 +95,7 @@ def load() -> C.CDLL:
     L.gsa_project_qkv.argtypes = [vp, i32, i32, vp, vp, vp, i32, i32, T, T, T, vp]
     L.gsa_project_qkv_bf16.argtypes = [vp, i32, i32, i64, vp, i32, vp, i64, vp]
     L.gsa_residual_bf16.argtypes = [vp, vp, vp, i64, vp]
+    L.gsa_convert.argtypes = [vp, i32, vp, i32, i64, vp]
     L.gsa_shard_of_rank.argtypes = [Lp, i32, i32, S]
     L.gsa_shard_gather_plan.argtypes = [Lp, i32, i32, i32, i64, C.POINTER(GsaGatherOp), i32, C.POINTER(C.c_int)]
     L.gsa_comm_get_unique_id.argtypes = [vp]
@@ -118,5 +119,5 @@ EXPORTED_SYMBOLS = [
     "gsa_set_stage_events", "gsa_launch_count", "gsa_shard_workspace_bytes", "gsa_shard_pool", "gsa_shard_compress",
     "gsa_shard_attend", "gsa_project_qkv", "gsa_shard_of_rank", "gsa_shard_gather_plan", "gsa_comm_get_unique_id",
     "gsa_comm_init", "gsa_comm_destroy", "gsa_shard_forward_workspace_bytes", "gsa_shard_forward",
-    "gsa_project_qkv_bf16", "gsa_residual_bf16",
+    "gsa_project_qkv_bf16", "gsa_residual_bf16", "gsa_convert",
 ]

@@ -1129,6 +1129,14 @@ int gsa_residual_bf16(const void* x, const float* o, void* y, int64_t n, gsa_str
     return GSA_OK;
 }
 
+int gsa_convert(const void* src, int src_dtype, void* dst, int dst_dtype, int64_t n, gsa_stream_t stream) {
+    if (n < 0 || (n && (!src || !dst))) return fail(GSA_ERR_GENERIC, "convert: null pointer or negative count");
+    auto ok = [](int t) { return t == GSA_DTYPE_F32 || t == GSA_DTYPE_BF16; };
+    if (!ok(src_dtype) || !ok(dst_dtype)) return fail(GSA_ERR_UNSUPPORTED, "convert: dtypes must be f32 or bf16");
+    GSA_CUDA(launch_convert(src, src_dtype, dst, dst_dtype, n, (cudaStream_t)stream));
+    return GSA_OK;
+}
+
 int gsa_project_qkv(const float* x, int tokens, int model_dim, const float* w_q, const float* w_k,
                     const float* w_v, int heads, int dim, const gsa_tensor* q, const gsa_tensor* k,
                     const gsa_tensor* v, gsa_stream_t stream) {

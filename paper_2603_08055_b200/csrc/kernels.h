@@ -107,6 +107,8 @@ cudaError_t launch_project(const float* x, int tokens, int C, const ProjectMats&
 // (lo only for f32 and when non-null), e_h = ilogb(vmax_h) - 13
 cudaError_t launch_v16(const TensorRef& v, int heads, int rows, unsigned* vmax, __half* hi, __half* lo,
                        cudaStream_t st);
+// n contiguous elements f32 <-> bf16 (RNE) or a same-dtype copy
+cudaError_t launch_convert(const void* src, int src_dtype, void* dst, int dst_dtype, int64_t n, cudaStream_t st);
 // [H][rows][64] rows (f32 or bf16, any strides) -> contiguous bf16 hi (+ lo for f32) planes
 cudaError_t launch_pack_rows(const TensorRef& in, int heads, int rows, __nv_bfloat16* hi, __nv_bfloat16* lo,
                              cudaStream_t st);

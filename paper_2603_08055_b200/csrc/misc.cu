@@ -196,6 +196,28 @@ cudaError_t launch_pack_rows(const TensorRef& in, int heads, int rows, __nv_bflo
     return cudaGetLastError();
 }
 
+__global__ void f32_to_bf16_kernel(const float* __restrict__ x, __nv_bfloat16* __restrict__ y, int64_t n) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        y[i] = __float2bfloat16_rn(x[i]);
+}
+__global__ void bf16_to_f32_kernel(const __nv_bfloat16* __restrict__ x, float* __restrict__ y, int64_t n) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        y[i] = __bfloat162float(x[i]);
+}
+
+cudaError_t launch_convert(const void* src, int src_dtype, void* dst, int dst_dtype, int64_t n, cudaStream_t st) {
+    if (n == 0) return cudaSuccess;
+    if (src_dtype == dst_dtype)
+        return cudaMemcpyAsync(dst, src, (size_t)n * (src_dtype == GSA_DTYPE_BF16 ? 2 : 4), cudaMemcpyDeviceToDevice, st);
+    const unsigned blocks = (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 32);
+    if (src_dtype == GSA_DTYPE_F32)
+        f32_to_bf16_kernel<<<blocks, 256, 0, st>>>(static_cast<const float*>(src), static_cast<__nv_bfloat16*>(dst), n);
+    else
+        bf16_to_f32_kernel<<<blocks, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(src), static_cast<float*>(dst), n);
+    note_launch();
+    return cudaGetLastError();
+}
+
 cudaError_t launch_v16(const TensorRef& v, int heads, int rows, unsigned* vmax, __half* hi, __half* lo,
                        cudaStream_t st) {
     cudaMemsetAsync(vmax, 0, (size_t)heads * 4, st);

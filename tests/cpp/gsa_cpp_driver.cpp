@@ -96,10 +96,25 @@ int time_forward(int views, int iters, bool bf16) {
         best = std::min(best, ms);
         sum += ms;
     }
+    // where the host->host time goes: the pinned staging rates, host allocation (the
+    // zero-filled std::vector every returned Tensor owns) and project_qkv (X up, Q/K/V down)
+    auto ms_of = [](auto&& f) {
+        const auto t0 = std::chrono::steady_clock::now();
+        f();
+        return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    };
+    const size_t nb = x.data.size() * sizeof(float);
+    gsa::device::Buffer dbuf(nb);
+    std::vector<float> hbuf(x.data.size());
+    const double h2d = ms_of([&] { gsa::device::Staging::get().h2d(dbuf.get(), x.data.data(), nb); });
+    const double d2h = ms_of([&] { gsa::device::Staging::get().d2h(hbuf.data(), dbuf.get(), nb); });
+    const double alloc = ms_of([&] { gsa::Tensor<float> t(1, layout.total_tokens(), model_dim); });
+    const double proj = ms_of([&] { auto pr = gsa::project_qkv(x, w); });
     std::printf("{\"views\": %d, \"tokens\": %d, \"precision\": \"%s\", \"iters\": %d, \"ms_mean\": %.3f, "
-                "\"ms_best\": %.3f, \"tokens_per_s\": %.1f}\n",
+                "\"ms_best\": %.3f, \"tokens_per_s\": %.1f, \"staging_h2d_gbs\": %.1f, \"staging_d2h_gbs\": %.1f, "
+                "\"host_alloc_gbs\": %.1f, \"project_qkv_ms\": %.1f}\n",
                 views, layout.total_tokens(), bf16 ? "bf16" : "f32", iters, sum / iters, best,
-                layout.total_tokens() / (sum / iters / 1e3));
+                layout.total_tokens() / (sum / iters / 1e3), nb / h2d / 1e6, nb / d2h / 1e6, nb / alloc / 1e6, proj);
     return 0;
 }
 
