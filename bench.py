@@ -413,6 +413,8 @@ def main():
         A = bytes_[dom] / (stage_ms[dom] / 1e3) / 1e9
         roof = {"kernel": dom, "bound": "hbm", "achieved": A, "peak": hbm, "unit": "GB/s", "frac": A / hbm,
                 "traffic": None, "peak_kind": peak_kind}
+        if dom == "select":  # gathers a plan row's windows: L2 hits count in the algorithmic bytes
+            roof["note"] = "achieved = algorithmic K/V gather bytes (L2 hits included); DRAM bytes in traffic when captured"
     else:
         A = flops[dom] / (stage_ms[dom] / 1e3) / 1e12
         roof = {"kernel": dom, "bound": "tensor", "achieved": A, "peak": tc_peak, "unit": "TFLOP/s",
