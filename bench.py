@@ -358,11 +358,12 @@ def main():
     # (special | pool | compress | select) or gsa_shard_forward (pool | Kc/Vc gather wait |
     # compress | attend)
     import ctypes
-    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(args.steps)]
+    # events 0-4: stage boundaries; 5-6: the compressed-attention kernel's own launch
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(7)] for _ in range(args.steps)]
     for row in ev:
         for e_ in row:
             e_.record()  # materialise the cudaEvent_t handles
-    handles = [(ctypes.c_void_p * 5)(*[e_.cuda_event for e_ in row]) for row in ev]
+    handles = [(ctypes.c_void_p * 7)(*[e_.cuda_event for e_ in row]) for row in ev]
     for _ in range(args.warmup):
         step_fn()
     torch.cuda.synchronize()
@@ -377,7 +378,7 @@ def main():
         torch.cuda.profiler.start()  # the timed region (ncu --profile-from-start off sees only it)
         start.record()
         for i in range(args.steps):
-            lib.gsa_set_stage_events(handles[i], 5)
+            lib.gsa_set_stage_events(handles[i], 7)
             step_fn()
         lib.gsa_set_stage_events(None, 0)
         stop.record()
@@ -386,6 +387,7 @@ def main():
     names = ("pool", "gather_kc", "compress", "attend") if sharded else ("special", "pool", "compress", "select")
     stage_ms = {n: sum(ev[i][j].elapsed_time(ev[i][j + 1]) for i in range(args.steps)) / args.steps
                 for j, n in enumerate(names)}
+    k2_ms = sum(ev[i][5].elapsed_time(ev[i][6]) for i in range(args.steps)) / args.steps  # compress_tc_kernel alone
     n1 = ctypes.c_uint64()
     lib.gsa_launch_count(ctypes.byref(n1))
     ms_local = start.elapsed_time(stop) / args.steps
@@ -415,6 +417,14 @@ def main():
                 "traffic": None, "peak_kind": peak_kind}
         if dom == "select":  # gathers a plan row's windows: L2 hits count in the algorithmic bytes
             roof["note"] = "achieved = algorithmic K/V gather bytes (L2 hits included); DRAM bytes in traffic when captured"
+    elif dom == "compress" and k2_ms > 0 and TOPK <= 128:  # (larger budgets select in largek_topk_kernel)
+        # the dominant kernel itself (compress_tc_kernel, CUDA events around its launch on its
+        # stream); the stage time (+ re-score and operand splits) is in stage_roofline
+        A = flops[dom] / (k2_ms / 1e3) / 1e12
+        roof = {"kernel": "compress_tc_kernel", "bound": "tensor", "achieved": A, "peak": tc_peak, "unit": "TFLOP/s",
+                "frac": A / tc_peak, "traffic": None, "peak_kind": peak_kind, "kernel_ms": round(k2_ms, 3),
+                "stage_ms": round(stage_ms[dom], 3), "stage_frac": round(flops[dom] / (stage_ms[dom] / 1e3) / 1e12 / tc_peak, 4),
+                "work": "4*64 flop per (query window, key window) pair per head (QK^T + PV, one MMA term each)"}
     else:
         A = flops[dom] / (stage_ms[dom] / 1e3) / 1e12
         roof = {"kernel": dom, "bound": "tensor", "achieved": A, "peak": tc_peak, "unit": "TFLOP/s",

@@ -314,7 +314,9 @@ int gsa_selection_sparsity(const gsa_layout* layout, const gsa_params* params, d
  * subsequent gsa_forward calls on this thread record cudaEvent_t events[0..4]
  * on `stream` at: start, after the special path, after pooling, after the
  * compressed attention + top-k, after selection/gate/merge (gsa_shard_forward: start,
- * after pooling, after the Kc/Vc gather, after the compressed branch, done). n = 0
+ * after pooling, after the Kc/Vc gather, after the compressed branch, done). With
+ * n >= 7, events[5] and events[6] also bracket the compressed-attention kernel launch
+ * itself (compress_tc_kernel), so its duration is measured on its own stream. n = 0
  * disables.
  * gsa_launch_count: kernels this library has launched since it was loaded. */
 int gsa_set_stage_events(void* const* events, int n);

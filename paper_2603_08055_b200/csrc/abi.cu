@@ -21,7 +21,7 @@ extern std::atomic<unsigned long long> g_launch_total;
 namespace {
 
 thread_local std::string g_msg;
-thread_local cudaEvent_t g_stage_events[5];
+thread_local cudaEvent_t g_stage_events[7];
 thread_local int g_n_stage_events = 0;
 
 
@@ -141,7 +141,7 @@ int report_error(int status, const char* msg) {
 }
 // gsa_set_stage_events instrumentation: record event i on `st` when enabled
 void stage_mark(int i, cudaStream_t st) {
-    if (g_n_stage_events >= 5) cudaEventRecord(g_stage_events[i], st);
+    if (g_n_stage_events > i) cudaEventRecord(g_stage_events[i], st);
 }
 }  // namespace gsa_sm100
 
@@ -1201,8 +1201,9 @@ int gsa_set_stage_events(void* const* events, int n) {
         g_n_stage_events = 0;
         return GSA_OK;
     }
-    for (int i = 0; i < 5; ++i) g_stage_events[i] = static_cast<cudaEvent_t>(events[i]);
-    g_n_stage_events = 5;
+    const int m = n >= 7 ? 7 : 5;
+    for (int i = 0; i < m; ++i) g_stage_events[i] = static_cast<cudaEvent_t>(events[i]);
+    g_n_stage_events = m;
     return GSA_OK;
 }
 

@@ -1788,7 +1788,9 @@ cudaError_t tc_compress_topk_splits(const CompressSplits* pre, const gsa_tensor&
     const size_t smem = sizeof(CompSmem) + 1024;
     cudaError_t e = cudaFuncSetAttribute(compress_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
+    stage_mark(5, st);  // (instrumentation: the kernel's own duration)
     compress_tc_kernel<<<dim3((Wq + 128 * NWG - 1) / (128 * NWG), H), NTHREADS, smem, st>>>(tqh, tql, tkh, tkl, tv16, p);
+    stage_mark(6, st);
     note_launch();
 #ifdef COMPRESS_PROF
     {
