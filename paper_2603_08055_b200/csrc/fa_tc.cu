@@ -311,7 +311,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     const float2 x = make_float2(__uint_as_float(s0), __uint_as_float(s1));
                     const float2 a = __ffma2_rn(x, c2v, nmc);
                     // FA_POLY: every FA_POLY-th pair on the FMA pipe instead of MUFU
-                    const float2 pv = (FA_POLY > 0 && e2 % FA_POLY == FA_POLY - 1)
+                    const float2 pv = (FA_POLY > 0 && e2 % (FA_POLY > 0 ? FA_POLY : 1) == FA_POLY - 1)
                                           ? exp2_poly2(a)
                                           : make_float2(ex2_approx(a.x), ex2_approx(a.y));
                     lsum2[e2 & 1] = __fadd2_rn(lsum2[e2 & 1], pv);  // the denominator sums the f32 P
