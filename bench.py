@@ -275,7 +275,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--views", type=int, default=int(os.environ.get("GSA_BENCH_VIEWS", "1000")))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--ref-sample-views", type=int, default=16)
+    ap.add_argument("--ref-sample-views", type=int, default=32,
+                    help="views in the CPU reference sample (its compress stage, extrapolated by W^2, dominates: a larger sample is a steadier estimate)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-parity", action="store_true", help="skip the post-timing sampled-row parity check")
     ap.add_argument("--e2e-cpp", default="", choices=["", "f32", "bf16"],
@@ -536,7 +537,7 @@ def main():
 
     if rank == 0 and not args.no_cpu_baseline:
         try:
-            line["cpu_baseline"] = {k_: v_ for k_, v_ in cpu_reference_sample(args.views).items()
+            line["cpu_baseline"] = {k_: v_ for k_, v_ in cpu_reference_sample(args.views, sample_views=args.ref_sample_views, repeats=5).items()
                                     if k_ in ("value", "unit", "cores", "kind", "sample", "extrapolated",
                                               "repeats", "spread")}
         except Exception as e:  # the baseline is reported, never required
