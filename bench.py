@@ -535,7 +535,7 @@ def main():
     if not args.no_dense and rank == 0:
         line["dense"] = dense_baseline(torch, q, k, v, ms)
 
-    if rank == 0 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:  # (the CPU baseline is an N=1 figure)
         try:
             line["cpu_baseline"] = {k_: v_ for k_, v_ in cpu_reference_sample(args.views, sample_views=args.ref_sample_views, repeats=5).items()
                                     if k_ in ("value", "unit", "cores", "kind", "sample", "extrapolated",
