@@ -13,7 +13,8 @@
 //           one TMEM lane: two passes per tile (row max over the loaded scores,
 //           then P chunk by chunk from a TMEM re-read), lazy rescale (only when
 //           the max grows by > 2^8; O is then rescaled in TMEM), P = exp2 via
-//           MUFU written back over S as packed fp16 pairs; epilogue O/l and lse.
+//           MUFU (every third pair by a polynomial on the FMA pipe, FA_POLY)
+//           written back over S as packed fp16 pairs; epilogue O/l and lse.
 // P.V in fp16: V (bf16) is converted once per call to fp16(v * 2^-e_h) with a per-head
 // power of two e_h from max |v| -- exact (bf16's 8-bit significands fit fp16's 11 and
 // the scale keeps them in range) -- so the only rounding is P's (2^-12 relative), one

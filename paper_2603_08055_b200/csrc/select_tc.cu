@@ -9,22 +9,26 @@
 // SM) walk the items head-major; inside a CTA the items' key windows form one
 // global stream of "groups" (<= GROUP_WIN = 16 windows = 256 keys each):
 //
-//   warp 0 (TMA)   : gathers each selected window of K and V straight from the
-//                    head-major [H][M][64] bf16 tensors with a 4-D tensor map
-//                    (box 64 x 4 x 4 = one 2 KB window, 128B-swizzled), 8
-//                    windows per 16 KB ring stage; Q tile per item; W_g (hi/lo
-//                    bf16 split, pre-swizzled) per head. Two CTAs per SM.
+//   warp 0 (TMA)   : gathers each selected window of K (bf16, straight from the
+//                    head-major [H][M][64] tensor) and of V (the layer's fp16 V16
+//                    planes: v * 2^-e_h per head, exact for bf16) with a 4-D tensor
+//                    map (box 64 x 4 x 4 = one 2 KB window, 128B-swizzled), 8
+//                    windows per 16 KB stage of a 4-stage ring; Q tile per item;
+//                    W_g (hi/lo bf16 split, pre-swizzled) per head.
 //   warp 1 (MMA)   : S^T[128 keys x 16 q] = K_chunk . Q^T   (M=128, N=16, K=64)
 //                    G^T[64 x 16]        = W_g^T . Q^T       (hi + lo, M=64)
-//                    O^T[64 x 16]       += V_chunk^T . P^T   (P hi + lo, M=64, K=16/step)
+//                    O^T[64 x 16]       += V16_chunk^T . P16^T (fp16, M=64, K=16/step)
 //                    accumulators in TMEM; S double-buffered across groups so
 //                    S(j+1) overlaps the softmax of group j.
 //   warps 2-5      : exact two-phase softmax over the whole group (keys are the
 //                    TMEM lanes: reductions = in-thread + 3 shuffles + 4-warp
-//                    smem), P written as bf16 hi/lo with stmatrix.trans straight
-//                    into the K-major B-operand layout; online rescale across
-//                    groups (hybrid rows); epilogue g = sigmoid(z),
-//                    out = g*O_comp[w] + (1-g)*O_sel in f32.
+//                    smem), P written as fp16 with stmatrix.trans straight into
+//                    the K-major B-operand layout; online rescale across groups
+//                    (long or hybrid rows); epilogue g = sigmoid(z),
+//                    out = g*O_comp[w] + (1-g)*2^e_h*O_sel in f32.
+// Modes: without W_g the plain block_sparse_attention operator (out = O_sel, any CSR
+// plan); `split`: f32 inputs as bf16 hi/lo Q, K and fp16 hi/lo V planes (3-term S and
+// G, 2-term P.V), each window gathered into two consecutive ring stages.
 //
 // HBM/L2-gather bound on iid inputs: 4 KB of K+V per selected window for
 // 65536 MACs (16 flop/B), see DESIGN.md.
