@@ -51,6 +51,7 @@ inline Precision& compute_precision() {
         case GSA_ERR_EMPTY_SELECTION: throw EmptySelection(msg);
         case GSA_ERR_UNSUPPORTED: throw Unsupported(msg);
         case GSA_ERR_CUDA: throw CudaError(msg);
+        case GSA_ERR_CONTEXT_MISMATCH: throw ContextMismatch(msg);
         default: throw GsaError(std::string(gsa_status_string(status)) + ": " + msg);
     }
 }

@@ -51,7 +51,8 @@ typedef enum {
     GSA_ERR_UNSUPPORTED = 10,       /* shape outside what the sm_100a kernels implement */
     GSA_ERR_CUDA = 11,              /* CUDA runtime / launch failure */
     GSA_ERR_WORKSPACE = 12,         /* workspace too small or misaligned */
-    GSA_ERR_NCCL = 13               /* NCCL failure in the multi-GPU layer (gsa_comm_*, gsa_shard_forward) */
+    GSA_ERR_NCCL = 13,              /* NCCL failure in the multi-GPU layer (gsa_comm_*, gsa_shard_forward) */
+    GSA_ERR_CONTEXT_MISMATCH = 14   /* ContextMismatch    errors.hpp:44  (gsa_backward's saved state) */
 } gsa_status;
 
 typedef enum { GSA_DTYPE_F32 = 0, GSA_DTYPE_BF16 = 1 } gsa_dtype;
@@ -309,6 +310,56 @@ int gsa_forward_stats(const gsa_layout* layout, const gsa_params* params, int he
  * image_tokens, attended = (|forced windows| + k_eff) * s^2 with k_eff = min(k,
  * selectable windows) (plain: min(k, num_windows) * s^2). Host arithmetic only. */
 int gsa_selection_sparsity(const gsa_layout* layout, const gsa_params* params, double* sparsity);
+
+/* ---------------------------------------------------------------------------
+ * Backward (gradients.hpp:14-265): the layer's manual backward with
+ * the top-k selection held constant, on CUDA cores in f32. Deterministic (every
+ * gradient element has one writer per kernel; no floating-point atomics).
+ *
+ * gsa_saved: the ForwardContext fields (layer.hpp:124-142) the backward reads, as
+ * device f32 arrays in gsa_context's shapes: qc/kc/vc/o_comp [H][W][d], lse_comp
+ * [H][W], o_sel/gate [H][Mi][d], lse_sel [H][Mi], lse_spec [H][Ms]; o_spec the
+ * special rows of the forward output ([H][Ms][d] view, e.g. the first Ms rows of
+ * gsa_forward's `out`); the selection plan as device CSR (gsa_build_selection_plan)
+ * with plan_entries = offsets[H*W]. */
+typedef struct {
+    const float *qc, *kc, *vc, *o_comp, *lse_comp;
+    const int64_t* plan_offsets;
+    const int32_t* plan_ids;
+    int64_t plan_entries;
+    const float *o_sel, *lse_sel, *gate;
+    gsa_tensor o_spec;
+    const float* lse_spec;
+} gsa_saved;
+
+/* gsa_backward (gradients.hpp:54-243, up to the projection): from the projected
+ * q/k/v (f32 or bf16, [H][M][d]), w_g f32 [H][d][d], the saved context and d_out f32
+ * [H][M][d], writes dq/dk/dv f32 [H][M][d] and dw_g f32 [H][d][d]. The plan is
+ * validated first (synchronises `stream`, like gsa_forward_with_plan). */
+size_t gsa_backward_workspace_bytes(const gsa_layout* layout, const gsa_params* params, int heads, int dim,
+                                    int64_t plan_entries, int qkv_dtype);
+int gsa_backward(const gsa_tensor* q, const gsa_tensor* k, const gsa_tensor* v, const gsa_tensor* w_g,
+                 const gsa_layout* layout, const gsa_params* params, const gsa_saved* saved,
+                 const gsa_tensor* d_out, const gsa_tensor* dq, const gsa_tensor* dk, const gsa_tensor* dv,
+                 float* dw_g, void* workspace, size_t workspace_bytes, gsa_stream_t stream);
+
+/* Projection backward (gradients.hpp:226-263): dw_q[h] = x^T dq[h] (likewise k, v) and
+ * dx = sum_h dq[h] w_q[h]^T + dk[h] w_k[h]^T + dv[h] w_v[h]^T. All device f32,
+ * contiguous: x / dx [tokens][model_dim], w_* / dw_* [H][model_dim][dim], dq/dk/dv
+ * [H][tokens][dim]. Row reductions are split and summed in a fixed order. */
+size_t gsa_project_backward_workspace_bytes(int tokens, int model_dim, int heads, int dim);
+int gsa_project_backward(const float* x, int tokens, int model_dim, const float* w_q, const float* w_k,
+                         const float* w_v, int heads, int dim, const float* dq, const float* dk, const float* dv,
+                         float* dx, float* dw_q, float* dw_k, float* dw_v, void* workspace, size_t workspace_bytes,
+                         gsa_stream_t stream);
+
+/* avg_pool_backward (gradients.hpp:21-34): out[h][t] = d_pooled[h][window_of(t)] / s^2;
+ * upsample_backward (gradients.hpp:37-49): out[h][w] = sum of d_fine over w's members
+ * in ascending token order. f32, bit-identical to the reference. */
+int gsa_avg_pool_backward(const gsa_tensor* d_pooled, const gsa_layout* layout, const gsa_tensor* out,
+                          gsa_stream_t stream);
+int gsa_upsample_backward(const gsa_tensor* d_fine, const gsa_layout* layout, const gsa_tensor* out,
+                          gsa_stream_t stream);
 
 /* Instrumentation (bench.py, profiling). gsa_set_stage_events: when n >= 5,
  * subsequent gsa_forward calls on this thread record cudaEvent_t events[0..4]

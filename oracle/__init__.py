@@ -474,6 +474,34 @@ class RefLib:
                                              self._p(w_v), C.c_int(H), C.c_int(d), self._p(q), self._p(k), self._p(v)))
         return q, k, v
 
+    def backward(self, x, w_q, w_k, w_v, w_g, lt, d_out, top_k=32, scale=0.0, variant=0, ref_stride=100,
+                 threads=8, f64=False):
+        """gsa_forward (layer.hpp:177-230) + gsa_backward (gradients.hpp:54-265) from X and the
+        weights: the forward output, its saved context (q/k/v, qc/kc/vc, o_comp, lse_comp, topk,
+        o_sel, lse_sel, gate, lse_spec) and the gradients dx, dw_q, dw_k, dw_v, dw_g."""
+        x, w_q, w_k, w_v, w_g, d_out = (np.ascontiguousarray(a, np.float32) for a in (x, w_q, w_k, w_v, w_g, d_out))
+        M, Cm = x.shape
+        H, _, d = w_q.shape
+        _, W, Mi = self.build_layout(*lt)
+        e = lambda *s: np.empty(s, np.float32)  # noqa: E731
+        r = dict(out=e(H, M, d), q=e(H, M, d), k=e(H, M, d), v=e(H, M, d), qc=e(H, W, d), kc=e(H, W, d),
+                 vc=e(H, W, d), o_comp=e(H, W, d), lse_comp=e(H, W), topk=np.empty(H * W * max(1, top_k), np.int32),
+                 o_sel=e(H, Mi, d), lse_sel=e(H, Mi), gate=e(H, Mi, d), lse_spec=e(H, lt[0]), dx=e(M, Cm),
+                 dw_q=e(H, Cm, d), dw_k=e(H, Cm, d), dw_v=e(H, Cm, d), dw_g=e(H, d, d))
+        ke = C.c_int()
+        ms = np.zeros(2, np.float64)
+        p = lambda n: self._p(r[n])  # noqa: E731
+        self._check(self.lib.gsa_ref_backward(
+            self._p(x), C.c_int(Cm), self._p(w_q), self._p(w_k), self._p(w_v), self._p(w_g), C.c_int(H), C.c_int(d),
+            *[C.c_int(a) for a in lt], C.c_int(top_k), C.c_double(scale), C.c_int(variant), C.c_int(ref_stride),
+            C.c_int(threads), C.c_int(int(f64)), self._p(d_out), p("out"), p("q"), p("k"), p("v"), p("qc"), p("kc"),
+            p("vc"), p("o_comp"), p("lse_comp"), p("topk"), C.byref(ke), p("o_sel"), p("lse_sel"), p("gate"),
+            p("lse_spec"), p("dx"), p("dw_q"), p("dw_k"), p("dw_v"), p("dw_g"), self._p(ms)))
+        r["k_eff"] = ke.value
+        r["topk"] = r["topk"][: H * W * ke.value].reshape(H, W, ke.value)
+        r["ms"] = dict(forward=ms[0], backward=ms[1])
+        return r
+
     def random_init(self, seed, lt, heads, dim, model_dim, clustered=False):
         M = self.build_layout(*lt)[2] + lt[0]
         q, k, v = (np.empty((heads, M, dim), np.float32) for _ in range(3))

@@ -22,6 +22,7 @@
 #include <vector>
 
 #include "gsa/compression.hpp"
+#include "gsa/gradients.hpp"
 #include "gsa/layer.hpp"
 #include "gsa/layout.hpp"
 #include "gsa/reference.hpp"
@@ -555,6 +556,74 @@ int gsa_ref_project(const float* x, int tokens, int model_dim, const float* wq, 
         from_tensor(p.q, q);
         from_tensor(p.k, k);
         from_tensor(p.v, v);
+    });
+}
+
+// gsa_forward (layer.hpp:177-230) then gsa_backward (gradients.hpp:54-265) on X / weights,
+// in f32 (f64 = 0) or in double (f64 = 1; inputs widened, results rounded back to f32).
+// Returns the forward output, the ForwardContext fields the device backward consumes (any
+// pointer may be NULL; topk holds H*W*k_eff ids) and the gradients GsaGradients. ms[0] /
+// ms[1]: forward / backward wall time.
+int gsa_ref_backward(const float* x, int model_dim, const float* wq, const float* wk, const float* wv,
+                     const float* wg, int heads, int dim, int ns, int nf, int gh, int gw, int s, int top_k,
+                     double scale_param, int variant, int ref_stride, int threads, int f64, const float* d_out,
+                     float* out, float* q, float* k, float* v, float* qc, float* kc, float* vc, float* o_comp,
+                     float* lse_comp, int32_t* topk, int* k_eff, float* o_sel, float* lse_sel, float* gate,
+                     float* lse_spec, float* dx, float* dwq, float* dwk, float* dwv, float* dwg, double* ms) {
+    auto run = [&](auto zero) {
+        using T = decltype(zero);
+        auto in = [](const float* p, int h, int t, int d) {
+            gsa::Tensor<T> r(h, t, d);
+            for (size_t i = 0; i < r.data.size(); ++i) r.data[i] = static_cast<T>(p[i]);
+            return r;
+        };
+        auto put = [](const gsa::Tensor<T>& t, float* p) {
+            if (p)
+                for (size_t i = 0; i < t.data.size(); ++i) p[i] = static_cast<float>(t.data[i]);
+        };
+        auto putv = [](const std::vector<T>& t, float* p) {
+            if (p)
+                for (size_t i = 0; i < t.size(); ++i) p[i] = static_cast<float>(t[i]);
+        };
+        auto l = gsa::build_token_layout(ns, nf, gh, gw, s);
+        gsa::GsaParams params = make_params(s, top_k, scale_param, variant, ref_stride, 16, 16);
+        const int m = l.total_tokens();
+        gsa::LayerWeights<T> w;
+        w.w_q = in(wq, heads, model_dim, dim);
+        w.w_k = in(wk, heads, model_dim, dim);
+        w.w_v = in(wv, heads, model_dim, dim);
+        w.w_g = in(wg, heads, dim, dim);
+        auto t0 = std::chrono::steady_clock::now();
+        auto fwd = gsa::gsa_forward(in(x, 1, m, model_dim), l, params, w, nullptr, threads);
+        if (ms) ms[0] = ms_since(t0);
+        t0 = std::chrono::steady_clock::now();
+        auto g = gsa::gsa_backward(fwd.saved, in(d_out, heads, m, dim), threads);
+        if (ms) ms[1] = ms_since(t0);
+        const auto& c = fwd.saved;
+        put(fwd.out, out);
+        put(c.q, q);
+        put(c.k, k);
+        put(c.v, v);
+        put(c.qc, qc);
+        put(c.kc, kc);
+        put(c.vc, vc);
+        put(c.o_comp_coarse, o_comp);
+        putv(c.lse_comp, lse_comp);
+        if (topk) std::copy(c.topk.indices.begin(), c.topk.indices.end(), topk);
+        if (k_eff) *k_eff = c.topk.k;
+        put(c.o_sel, o_sel);
+        putv(c.lse_sel, lse_sel);
+        put(c.gate_vals, gate);
+        putv(c.lse_spec, lse_spec);
+        put(g.dx, dx);
+        put(g.dw_q, dwq);
+        put(g.dw_k, dwk);
+        put(g.dw_v, dwv);
+        put(g.dw_g, dwg);
+    };
+    return guarded([&] {
+        if (f64) run(0.0);
+        else run(0.0f);
     });
 }
 

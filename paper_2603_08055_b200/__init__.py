@@ -25,6 +25,7 @@ from .gsa import (  # noqa: E402
     TokenLayout, Unsupported, Workspace, ZeroSizeError, avg_pool_tokens, block_sparse_attention, build_selection_plan,
     build_token_layout, forced_windows_of, forward_stats, fused_compressed_attention_topk, gate, gsa_forward,
     gsa_forward_with_plan, project_qkv, resolved_scale, selection_sparsity, special_token_attention, tiled_attention, upsample_nearest,
+    ContextMismatch, GsaGradients, avg_pool_backward, gsa_backward, layer_backward, project_backward, upsample_backward,
 )
 
 __all__ = [
@@ -33,5 +34,6 @@ __all__ = [
     "SelectionPlan", "ShapeMismatch", "TokenLayout", "Unsupported", "Workspace", "ZeroSizeError", "avg_pool_tokens",
     "block_sparse_attention", "build_selection_plan", "build_token_layout", "forced_windows_of", "forward_stats",
     "fused_compressed_attention_topk", "gate", "gsa_forward", "gsa_forward_with_plan", "project_qkv", "resolved_scale",
-    "selection_sparsity", "special_token_attention", "tiled_attention", "upsample_nearest",
+    "selection_sparsity", "special_token_attention", "tiled_attention", "upsample_nearest", "ContextMismatch",
+    "GsaGradients", "avg_pool_backward", "gsa_backward", "layer_backward", "project_backward", "upsample_backward",
 ]

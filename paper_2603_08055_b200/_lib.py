@@ -40,6 +40,14 @@ class GsaGatherOp(C.Structure):
     _fields_ = [("buffer", C.c_int32), ("phase", C.c_int32), ("offset", C.c_int64), ("count", C.c_int64)]
 
 
+class GsaSavedC(C.Structure):
+    """gsa_saved: the ForwardContext fields gsa_backward reads (device pointers)."""
+    _fields_ = [("qc", C.c_void_p), ("kc", C.c_void_p), ("vc", C.c_void_p), ("o_comp", C.c_void_p),
+                ("lse_comp", C.c_void_p), ("plan_offsets", C.c_void_p), ("plan_ids", C.c_void_p),
+                ("plan_entries", C.c_int64), ("o_sel", C.c_void_p), ("lse_sel", C.c_void_p), ("gate", C.c_void_p),
+                ("o_spec", GsaTensor), ("lse_spec", C.c_void_p)]
+
+
 class GsaContextC(C.Structure):
     _fields_ = [(n, C.c_void_p) for n in ("qc", "kc", "vc", "o_comp", "lse_comp", "topk", "o_sel", "lse_sel",
                                           "gate", "lse_spec")]
@@ -106,6 +114,15 @@ def load() -> C.CDLL:
     L.gsa_shard_forward.argtypes = [vp, T, T, T, T, Lp, P, T, vp, vp, C.c_size_t, vp]
     L.gsa_set_stage_events.argtypes = [C.POINTER(C.c_void_p), i32]
     L.gsa_launch_count.argtypes = [C.POINTER(C.c_uint64)]
+    L.gsa_backward_workspace_bytes.restype = C.c_size_t
+    L.gsa_backward_workspace_bytes.argtypes = [Lp, P, i32, i32, i64, i32]
+    L.gsa_backward.argtypes = [T, T, T, T, Lp, P, C.POINTER(GsaSavedC), T, T, T, T, vp, vp, C.c_size_t, vp]
+    L.gsa_project_backward_workspace_bytes.restype = C.c_size_t
+    L.gsa_project_backward_workspace_bytes.argtypes = [i32, i32, i32, i32]
+    L.gsa_project_backward.argtypes = [vp, i32, i32, vp, vp, vp, i32, i32, vp, vp, vp, vp, vp, vp, vp, vp,
+                                       C.c_size_t, vp]
+    L.gsa_avg_pool_backward.argtypes = [T, Lp, T, vp]
+    L.gsa_upsample_backward.argtypes = [T, Lp, T, vp]
     _lib = L
     return L
 
@@ -119,5 +136,7 @@ EXPORTED_SYMBOLS = [
     "gsa_set_stage_events", "gsa_launch_count", "gsa_shard_workspace_bytes", "gsa_shard_pool", "gsa_shard_compress",
     "gsa_shard_attend", "gsa_project_qkv", "gsa_shard_of_rank", "gsa_shard_gather_plan", "gsa_comm_get_unique_id",
     "gsa_comm_init", "gsa_comm_destroy", "gsa_shard_forward_workspace_bytes", "gsa_shard_forward",
-    "gsa_project_qkv_bf16", "gsa_residual_bf16", "gsa_convert",
+    "gsa_project_qkv_bf16", "gsa_residual_bf16", "gsa_convert", "gsa_backward_workspace_bytes", "gsa_backward",
+    "gsa_project_backward_workspace_bytes", "gsa_project_backward", "gsa_avg_pool_backward",
+    "gsa_upsample_backward",
 ]

@@ -165,6 +165,7 @@ const char* gsa_status_string(int s) {
         case GSA_ERR_CUDA: return "CudaError";
         case GSA_ERR_WORKSPACE: return "WorkspaceError";
         case GSA_ERR_NCCL: return "NcclError";
+        case GSA_ERR_CONTEXT_MISMATCH: return "ContextMismatch";
         default: return "unknown";
     }
 }
@@ -1193,6 +1194,320 @@ int gsa_selection_sparsity(const gsa_layout* layout, const gsa_params* p, double
     const int k_eff = p->top_k < sel ? p->top_k : sel;
     const double attended = (double)(nf + k_eff) * L.s * L.s;  // forced ++ dynamic, deduplicated
     *sparsity = L.image_tokens > 0 ? 1.0 - attended / (double)L.image_tokens : 0.0;
+    return GSA_OK;
+}
+
+// ------------------------------------------------------------------ backward
+
+}  // extern "C"
+
+namespace {
+
+FMat fmat_of(const gsa_tensor& t, int row_offset = 0) {
+    return FMat{static_cast<const float*>(t.data) + (int64_t)row_offset * t.row_stride, t.head_stride, t.row_stride};
+}
+FOut fout_of(const gsa_tensor& t, int row_offset = 0) {
+    return FOut{static_cast<float*>(t.data) + (int64_t)row_offset * t.row_stride, t.head_stride, t.row_stride};
+}
+
+struct BwdBufs {
+    float *q32, *k32, *v32;
+    float *ds, *dz, *d_oc, *dqc, *dkc, *dvc, *d_sel, *d_comp, *d_spec;
+    unsigned long long *keys, *keys_sorted;
+    int64_t *counts, *inv_offsets;
+    int32_t* inv_q;
+    void* tmp;
+    size_t tmp_bytes;
+    float* part;
+    int splits;
+};
+
+size_t carve_bwd(const DevLayout& L, int Ms, int H, int d, int64_t E, bool convert, char* base, size_t cap,
+                 bool dry, BwdBufs* b) {
+    Carver c{base, cap, 0, dry};
+    const int64_t M = Ms + (int64_t)L.image_tokens, Mi = L.image_tokens, W = L.windows;
+    b->q32 = b->k32 = b->v32 = nullptr;
+    if (convert) {
+        b->q32 = c.take<float>((size_t)H * M * d);
+        b->k32 = c.take<float>((size_t)H * M * d);
+        b->v32 = c.take<float>((size_t)H * M * d);
+    }
+    b->ds = c.take<float>((size_t)H * Mi * d);
+    b->dz = c.take<float>((size_t)H * Mi * d);
+    b->d_oc = c.take<float>((size_t)H * W * d);
+    b->dqc = c.take<float>((size_t)H * W * d);
+    b->dkc = c.take<float>((size_t)H * W * d);
+    b->dvc = c.take<float>((size_t)H * W * d);
+    b->d_sel = c.take<float>((size_t)H * Mi);
+    b->d_comp = c.take<float>((size_t)H * W);
+    b->d_spec = c.take<float>((size_t)H * (Ms > 0 ? Ms : 1));
+    b->keys = c.take<unsigned long long>((size_t)E);
+    b->keys_sorted = c.take<unsigned long long>((size_t)E);
+    b->counts = c.take<int64_t>((size_t)H * W);
+    b->inv_offsets = c.take<int64_t>((size_t)H * W + 1);
+    b->inv_q = c.take<int32_t>((size_t)E);
+    b->tmp_bytes = inverse_plan_tmp_bytes((int64_t)H * W, E);
+    b->tmp = c.take<char>(b->tmp_bytes);
+    b->splits = atb_splits(H, d, d, Mi);
+    b->part = c.take<float>((size_t)H * b->splits * d * d);
+    return c.used;
+}
+
+}  // namespace
+
+extern "C" {
+
+size_t gsa_backward_workspace_bytes(const gsa_layout* layout, const gsa_params* params, int heads, int dim,
+                                    int64_t plan_entries, int qkv_dtype) {
+    (void)params;
+    if (check_layout(layout) != GSA_OK || heads < 0 || dim < 1 || plan_entries < 0) return 0;
+    const DevLayout L = make_dev_layout(*layout);
+    BwdBufs b;
+    return carve_bwd(L, layout->num_special, heads, dim, plan_entries, qkv_dtype != GSA_DTYPE_F32, nullptr, 0, true,
+                     &b) + 256;
+}
+
+int gsa_backward(const gsa_tensor* q, const gsa_tensor* k, const gsa_tensor* v, const gsa_tensor* w_g,
+                 const gsa_layout* layout, const gsa_params* params, const gsa_saved* sv,
+                 const gsa_tensor* d_out, const gsa_tensor* dq, const gsa_tensor* dk, const gsa_tensor* dv,
+                 float* dw_g, void* workspace, size_t ws_bytes, gsa_stream_t stream) {
+    // gsa_backward (gradients.hpp:54-75): shapes of dO and the saved context
+    const gsa_tensor* o = d_out;
+    GSA_TRY(check_tensor(o, "d_out", false));
+    LayerPlan lp;
+    GSA_TRY(layer_checks(q, k, v, w_g, layout, params, o, &lp, true));
+    if (!sv) return fail(GSA_ERR_GENERIC, "gsa_backward: null saved context");
+    if (!sv->qc || !sv->kc || !sv->vc || !sv->o_comp || !sv->lse_comp || !sv->o_sel || !sv->lse_sel || !sv->gate ||
+        (lp.Ms > 0 && (!sv->lse_spec || !sv->o_spec.data)))
+        return fail(GSA_ERR_CONTEXT_MISMATCH, "gsa_backward: saved context is incomplete");
+    if (lp.Ms > 0 && (sv->o_spec.dtype != GSA_DTYPE_F32 || sv->o_spec.heads != lp.heads ||
+                      sv->o_spec.rows != lp.Ms || sv->o_spec.dim != lp.dim))
+        return fail(GSA_ERR_CONTEXT_MISMATCH, "gsa_backward: o_spec must be f32 [H][Ms][d]");
+    GSA_TRY(check_f32_out(dq, "dq", lp.heads, lp.M, lp.dim));
+    GSA_TRY(check_f32_out(dk, "dk", lp.heads, lp.M, lp.dim));
+    GSA_TRY(check_f32_out(dv, "dv", lp.heads, lp.M, lp.dim));
+    if (!dw_g) return fail(GSA_ERR_GENERIC, "gsa_backward: null dw_g");
+    const int H = lp.heads, d = lp.dim, W = lp.W, Ms = lp.Ms;
+    const int64_t rows = (int64_t)H * W;
+    cudaStream_t st = (cudaStream_t)stream;
+    const bool convert = q->dtype != GSA_DTYPE_F32;
+    BwdBufs b;
+    const size_t need = carve_bwd(lp.L, Ms, H, d, sv->plan_entries, convert, static_cast<char*>(workspace), ws_bytes,
+                                  false, &b);
+    if (need > ws_bytes + 256) return fail(GSA_ERR_WORKSPACE, "gsa_backward: workspace %zu < %zu", ws_bytes, need);
+    if (rows == 0) return GSA_OK;
+    GSA_TRY(validate_plan(sv->plan_offsets, sv->plan_ids, rows, W, "gsa_backward", st));
+    int64_t total = 0;
+    GSA_CUDA(cudaMemcpyAsync(&total, sv->plan_offsets + rows, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    GSA_CUDA(cudaStreamSynchronize(st));
+    if (total != sv->plan_entries)
+        return fail(GSA_ERR_CONTEXT_MISMATCH, "gsa_backward: plan holds %lld entries, saved.plan_entries = %lld",
+                    (long long)total, (long long)sv->plan_entries);
+
+    FMat Q = fmat_of(*q), K = fmat_of(*k), V = fmat_of(*v);
+    if (convert) {
+        const int64_t hs = (int64_t)lp.M * d;
+        GSA_CUDA(launch_to_f32(ref_of(*q), H, lp.M, d, b.q32, st));
+        GSA_CUDA(launch_to_f32(ref_of(*k), H, lp.M, d, b.k32, st));
+        GSA_CUDA(launch_to_f32(ref_of(*v), H, lp.M, d, b.v32, st));
+        Q = FMat{b.q32, hs, d};
+        K = FMat{b.k32, hs, d};
+        V = FMat{b.v32, hs, d};
+    }
+    const FMat dO = fmat_of(*d_out);
+    const FOut dQ = fout_of(*dq), dK = fout_of(*dk), dV = fout_of(*dv);
+    const int64_t whs = (int64_t)W * d;
+
+    // 1. gate fuse + upsample backward (gradients.hpp:96-128)
+    GateBwdArgs g{};
+    g.dout = dO;
+    g.gate = sv->gate;
+    g.o_sel = sv->o_sel;
+    g.o_comp = sv->o_comp;
+    g.w_g = static_cast<const float*>(w_g->data);
+    g.L = lp.L;
+    g.dim = d;
+    g.ds = b.ds;
+    g.dz = b.dz;
+    g.d_oc = b.d_oc;
+    g.d_sel = b.d_sel;
+    g.d_comp = b.d_comp;
+    g.dq = dQ;
+    GSA_CUDA(launch_gate_bwd(g, H, st));
+
+    // 2. compressed attention backward over the windows (gradients.hpp:130-155)
+    DenseBwdArgs c{};
+    c.q = FMat{sv->qc, whs, d};
+    c.k = FMat{sv->kc, whs, d};
+    c.v = FMat{sv->vc, whs, d};
+    c.dout = FMat{b.d_oc, whs, d};
+    c.lse = sv->lse_comp;
+    c.lse_hs = W;
+    c.D = b.d_comp;
+    c.D_hs = W;
+    c.nq = c.nk = W;
+    c.dim = d;
+    c.scale = lp.scale;
+    c.dq = FOut{b.dqc, whs, d};
+    c.dk = FOut{b.dkc, whs, d};
+    c.dv = FOut{b.dvc, whs, d};
+    c.accumulate = false;
+    GSA_CUDA(launch_dense_bwd(c, H, st));
+
+    // 3. pooling backward into the image rows (gradients.hpp:157-169)
+    PoolBwdArgs pb{};
+    pb.heads = H;
+    pb.rows = lp.M;
+    pb.dim = d;
+    pb.L = lp.L;
+    pb.inv = 1.0f / (float)(lp.L.s * lp.L.s);
+    pb.dqc = b.dqc;
+    pb.dkc = b.dkc;
+    pb.dvc = b.dvc;
+    pb.dq = dQ;
+    pb.dk = dK;
+    pb.dv = dV;
+    GSA_CUDA(launch_pool_bwd(pb, st));
+
+    // 4. selection backward over the detached plan (gradients.hpp:171-195)
+    GSA_CUDA(launch_inverse_plan(sv->plan_offsets, sv->plan_ids, rows, W, sv->plan_entries, b.keys, b.keys_sorted,
+                                 b.counts, b.inv_offsets, b.inv_q, b.tmp, b.tmp_bytes, st));
+    SelBwdArgs sa{};
+    sa.q = Q;
+    sa.k = K;
+    sa.v = V;
+    sa.ds = b.ds;
+    sa.lse = sv->lse_sel;
+    sa.D = b.d_sel;
+    sa.offsets = sv->plan_offsets;
+    sa.ids = sv->plan_ids;
+    sa.inv_offsets = b.inv_offsets;
+    sa.inv_q = b.inv_q;
+    sa.L = lp.L;
+    sa.dim = d;
+    sa.scale = lp.scale;
+    sa.dq = dQ;
+    sa.dk = dK;
+    sa.dv = dV;
+    GSA_CUDA(launch_sel_bwd(sa, H, st));
+
+    // 5. special rows: dense backward over every key (gradients.hpp:197-222)
+    if (Ms > 0) {
+        const FMat oS = fmat_of(sv->o_spec);
+        GSA_CUDA(launch_rowdot(dO, oS, H, Ms, d, b.d_spec, st));
+        DenseBwdArgs sp{};
+        sp.q = Q;
+        sp.k = K;
+        sp.v = V;
+        sp.dout = dO;
+        sp.lse = sv->lse_spec;
+        sp.lse_hs = Ms;
+        sp.D = b.d_spec;
+        sp.D_hs = Ms;
+        sp.nq = Ms;
+        sp.nk = lp.M;
+        sp.dim = d;
+        sp.scale = lp.scale;
+        sp.dk = dK;  // key side first, accumulated into every row
+        sp.dv = dV;
+        sp.accumulate = true;
+        GSA_CUDA(launch_dense_bwd(sp, H, st));
+        sp.dk = FOut{nullptr, 0, 0};
+        sp.dv = FOut{nullptr, 0, 0};
+        sp.dq = dQ;  // the special rows' only dQ term: written
+        sp.accumulate = false;
+        GSA_CUDA(launch_dense_bwd(sp, H, st));
+    }
+
+    // 6. dW_g = Q_img^T dz per head (gradients.hpp:112-113)
+    AtbArgs at{};
+    at.A = Q.p + (int64_t)Ms * Q.rs;
+    at.a_hs = Q.hs;
+    at.a_rs = Q.rs;
+    at.B = b.dz;
+    at.b_hs = (int64_t)lp.Mi * d;
+    at.b_rs = d;
+    at.R = d;
+    at.N = d;
+    at.rows = lp.Mi;
+    at.splits = b.splits;
+    at.part = b.part;
+    GSA_CUDA(launch_atb(at, H, dw_g, st));
+    return GSA_OK;
+}
+
+size_t gsa_project_backward_workspace_bytes(int tokens, int model_dim, int heads, int dim) {
+    if (tokens < 0 || model_dim < 1 || heads < 0 || dim < 1) return 0;
+    return (size_t)heads * atb_splits(heads, model_dim, dim, tokens) * model_dim * dim * sizeof(float) + 256;
+}
+
+int gsa_project_backward(const float* x, int tokens, int model_dim, const float* w_q, const float* w_k,
+                         const float* w_v, int heads, int dim, const float* dq, const float* dk, const float* dv,
+                         float* dx, float* dw_q, float* dw_k, float* dw_v, void* workspace, size_t ws_bytes,
+                         gsa_stream_t stream) {
+    if (tokens < 0 || model_dim < 1 || heads < 1 || dim < 1)
+        return fail(GSA_ERR_SHAPE_MISMATCH, "project_backward: bad extents");
+    if (!x || !w_q || !w_k || !w_v || !dq || !dk || !dv || !dx || !dw_q || !dw_k || !dw_v)
+        return fail(GSA_ERR_GENERIC, "project_backward: null pointer");
+    const size_t need = gsa_project_backward_workspace_bytes(tokens, model_dim, heads, dim);
+    if (ws_bytes + 256 < need || (need > 256 && !workspace))
+        return fail(GSA_ERR_WORKSPACE, "project_backward: workspace %zu < %zu", ws_bytes, need);
+    cudaStream_t st = (cudaStream_t)stream;
+    const float* g[3] = {dq, dk, dv};
+    float* dw[3] = {dw_q, dw_k, dw_v};
+    for (int i = 0; i < 3; ++i) {
+        AtbArgs a{};
+        a.A = x;
+        a.a_hs = 0;
+        a.a_rs = model_dim;
+        a.B = g[i];
+        a.b_hs = (int64_t)tokens * dim;
+        a.b_rs = dim;
+        a.R = model_dim;
+        a.N = dim;
+        a.rows = tokens;
+        a.splits = atb_splits(heads, model_dim, dim, tokens);
+        a.part = static_cast<float*>(workspace);
+        GSA_CUDA(launch_atb(a, heads, dw[i], st));
+    }
+    DxArgs a{};
+    a.g[0] = dq;
+    a.g[1] = dk;
+    a.g[2] = dv;
+    a.w[0] = w_q;
+    a.w[1] = w_k;
+    a.w[2] = w_v;
+    a.heads = heads;
+    a.dim = dim;
+    a.C = model_dim;
+    a.tokens = tokens;
+    a.dx = dx;
+    GSA_CUDA(launch_dx_gemm(a, st));
+    return GSA_OK;
+}
+
+int gsa_avg_pool_backward(const gsa_tensor* d_pooled, const gsa_layout* layout, const gsa_tensor* out,
+                          gsa_stream_t stream) {
+    GSA_TRY(check_layout(layout));
+    GSA_TRY(check_tensor(d_pooled, "d_pooled", false));
+    const DevLayout L = make_dev_layout(*layout);
+    // gradients.hpp:23-24
+    if (d_pooled->rows != L.windows) return fail(GSA_ERR_SHAPE_MISMATCH, "avg_pool_backward: rows != num windows");
+    GSA_TRY(check_f32_out(out, "out", d_pooled->heads, L.image_tokens, d_pooled->dim));
+    GSA_CUDA(launch_pool_adjoint(fmat_of(*d_pooled), d_pooled->heads, d_pooled->dim, L,
+                                 1.0f / (float)(L.s * L.s), fout_of(*out), (cudaStream_t)stream));
+    return GSA_OK;
+}
+
+int gsa_upsample_backward(const gsa_tensor* d_fine, const gsa_layout* layout, const gsa_tensor* out,
+                          gsa_stream_t stream) {
+    GSA_TRY(check_layout(layout));
+    GSA_TRY(check_tensor(d_fine, "d_fine", false));
+    const DevLayout L = make_dev_layout(*layout);
+    // gradients.hpp:39-40
+    if (d_fine->rows != L.image_tokens) return fail(GSA_ERR_SHAPE_MISMATCH, "upsample_backward: rows != image tokens");
+    GSA_TRY(check_f32_out(out, "out", d_fine->heads, L.windows, d_fine->dim));
+    GSA_CUDA(launch_window_sum(fmat_of(*d_fine), d_fine->heads, d_fine->dim, L, fout_of(*out), (cudaStream_t)stream));
     return GSA_OK;
 }
 

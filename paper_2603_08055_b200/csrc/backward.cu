@@ -1,0 +1,887 @@
+// backward.cu — the layer backward (gsa_backward, gradients.hpp:54-265) and the
+// projection backward, on CUDA cores in f32.
+//
+// The backward of each branch is the flash-style recomputation the reference
+// uses: probabilities are rebuilt from the saved log-sum-exp rows,
+// p = exp(scale * q.k - lse), dS = p * (dO.v - D) * scale with D = dO.o, and the
+// top-k selection is a constant (gradients.hpp:52-54). Every gradient is
+// produced by exactly one owner thread per element and kernels touching the same
+// output run in a fixed stream order, so the result is deterministic without
+// floating-point atomics:
+//
+//   gate_bwd         gate fuse (gradients.hpp:96-119): dS_sel = (1-g) dO, dz =
+//                    g(1-g)(O_comp - O_sel) dO, dq_img = W_g dz (written), the
+//                    window sums of g dO (upsample backward, :122-128) and the D
+//                    rows of both branches
+//   dense_bwd_dkdv   FlashAttention-2 key-side pass (one CTA per 64 keys, loop over
+//   dense_bwd_dq     every query tile) and query-side pass: the compressed branch
+//                    (:131-155, windows x windows) and the special rows (:197-222,
+//                    Ms queries x all M keys)
+//   pool_bwd         pooled-gradient scatter (avg-pool adjoint, :158-169)
+//   sel_bwd_dq       selection branch (:172-194) query side, one CTA per (head, query
+//                    window), keys gathered from the plan row like the forward
+//   sel_bwd_dkdv     key side, one CTA per (head, key window), queries from the
+//                    INVERSE plan (the windows whose plan row holds it, ascending),
+//                    built by a radix sort of (head, key window, query window)
+//   atb / atb_reduce dW = A^T B split over rows with a fixed-order reduction of the
+//                    partials (dW_g = Q_img^T dz, dW_{q,k,v} = X^T dQ/dK/dV)
+//   dx_gemm          dX = sum_h dQ_h W_q,h^T + dK_h W_k,h^T + dV_h W_v,h^T (:245-263)
+//
+// All tiles use the same register blocking: 256 threads as a 16 x 16 grid, thread
+// (ty, tx) owning rows ty + 16 i and columns tx + 16 j, so every shared-memory read is
+// either a broadcast or 16 distinct padded rows (conflict-free).
+#include <cub/device/device_radix_sort.cuh>
+
+#include "kernels.h"
+
+namespace gsa_sm100 {
+namespace {
+
+constexpr int BT = 256;  // threads per CTA
+constexpr int TB = 64;   // dense tiles: 64 queries x 64 keys
+
+// ------------------------------------------------------------------ gate fuse
+template <int DP>
+__global__ void __launch_bounds__(BT) gate_bwd_kernel(GateBwdArgs a) {
+    extern __shared__ __align__(16) float sm[];
+    const DevLayout& L = a.L;
+    const int dim = a.dim, s2 = L.s * L.s, W = L.windows, Mi = L.image_tokens, Ms = L.num_special;
+    float* wg = sm;                   // [dim][DP+1]
+    float* dz = wg + DP * (DP + 1);   // [s2][DP]
+    float* dcf = dz + s2 * DP;        // [s2][DP]  g * dO (upsample-backward terms)
+    float* pr = dcf + s2 * DP;        // [s2][DP]  dS_sel * O_sel (D_sel terms)
+    float* red = pr + s2 * DP;        // [DP]      dO_comp * O_comp (D_comp terms)
+    const int h = blockIdx.x / W, w = blockIdx.x - h * W;
+    const int tid = threadIdx.x;
+
+    const float* wgh = a.w_g + (int64_t)h * dim * dim;
+    for (int e = tid; e < dim * dim; e += BT) wg[(e / dim) * (DP + 1) + e % dim] = wgh[e];
+    const float* comp = a.o_comp + ((int64_t)h * W + w) * dim;
+    for (int e = tid; e < s2 * dim; e += BT) {
+        const int m = e / dim, j = e - m * dim;
+        const int i = L.member(w, m);
+        const int64_t r = ((int64_t)h * Mi + i) * dim + j;
+        const float go = a.dout.p[(int64_t)h * a.dout.hs + (int64_t)(Ms + i) * a.dout.rs + j];
+        const float g = a.gate[r], sel = a.o_sel[r];
+        const float ds = (1.0f - g) * go;
+        const float dzv = g * (1.0f - g) * ((comp[j] - sel) * go);
+        a.ds[r] = ds;
+        a.dz[r] = dzv;
+        dz[m * DP + j] = dzv;
+        dcf[m * DP + j] = g * go;
+        pr[m * DP + j] = ds * sel;
+    }
+    __syncthreads();
+    // upsample backward: window sum of g * dO in ascending member order
+    for (int j = tid; j < dim; j += BT) {
+        float acc = 0.0f;
+        for (int m = 0; m < s2; ++m) acc += dcf[m * DP + j];
+        a.d_oc[((int64_t)h * W + w) * dim + j] = acc;
+        red[j] = acc * comp[j];
+    }
+    // D_sel rows: one warp per member row
+    const int warp = tid >> 5, lane = tid & 31;
+    for (int m = warp; m < s2; m += BT / 32) {
+        float acc = 0.0f;
+        for (int j = lane; j < dim; j += 32) acc += pr[m * DP + j];
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (lane == 0) a.d_sel[(int64_t)h * Mi + L.member(w, m)] = acc;
+    }
+    // dq_img = W_g dz (gradients.hpp:108-117), written: the first contribution to dQ
+    for (int e = tid; e < s2 * dim; e += BT) {
+        const int m = e / dim, c = e - m * dim;
+        float acc = 0.0f;
+        for (int j = 0; j < dim; ++j) acc += wg[c * (DP + 1) + j] * dz[m * DP + j];
+        a.dq.p[(int64_t)h * a.dq.hs + (int64_t)(Ms + L.member(w, m)) * a.dq.rs + c] = acc;
+    }
+    __syncthreads();
+    if (warp == 0) {
+        float acc = 0.0f;
+        for (int j = lane; j < dim; j += 32) acc += red[j];
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (lane == 0) a.d_comp[(int64_t)h * W + w] = acc;
+    }
+}
+
+// ---------------------------------------------------------- dense attention
+template <int DP>
+__device__ __forceinline__ void load_tile(float* dst, const FMat& m, int h, int64_t r0, int64_t rows, int dim) {
+    for (int e = threadIdx.x; e < TB * DP; e += BT) {
+        const int r = e / DP, j = e - r * DP;
+        float x = 0.0f;
+        if (r0 + r < rows && j < dim) x = m.p[(int64_t)h * m.hs + (r0 + r) * m.rs + j];
+        dst[r * (DP + 1) + j] = x;
+    }
+}
+
+// S and dP for the 64 x 64 tile: rows ty + 16 i of Qs / dOs, columns tx + 16 j of Ks / Vs;
+// stores P and dS = P (dP - D) scale; invalid keys (col >= kn) get P = 0.
+template <int DP>
+__device__ __forceinline__ void score_tile(const float* Qs, const float* dOs, const float* Ks, const float* Vs,
+                                           const float* lse, const float* D, int kn, float scale, float* Ps,
+                                           float* dSs) {
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    float s[4][4], dp[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) s[i][j] = dp[i][j] = 0.0f;
+#pragma unroll 4
+    for (int d = 0; d < DP; ++d) {
+        float qv[4], ov[4], kv[4], vv[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            qv[i] = Qs[(ty + 16 * i) * (DP + 1) + d];
+            ov[i] = dOs[(ty + 16 * i) * (DP + 1) + d];
+            kv[i] = Ks[(tx + 16 * i) * (DP + 1) + d];
+            vv[i] = Vs[(tx + 16 * i) * (DP + 1) + d];
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                s[i][j] = fmaf(qv[i], kv[j], s[i][j]);
+                dp[i][j] = fmaf(ov[i], vv[j], dp[i][j]);
+            }
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int q = ty + 16 * i;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int k = tx + 16 * j;
+            const float p = k < kn ? expf(s[i][j] * scale - lse[q]) : 0.0f;
+            Ps[q * (TB + 1) + k] = p;
+            dSs[q * (TB + 1) + k] = p * (dp[i][j] - D[q]) * scale;
+        }
+    }
+}
+
+template <int DP>
+__device__ __forceinline__ void load_stats(float* lse_s, float* D_s, const DenseBwdArgs& a, int h, int64_t q0) {
+    for (int r = threadIdx.x; r < TB; r += BT) {
+        const int64_t q = q0 + r;
+        const bool ok = q < a.nq;
+        lse_s[r] = ok ? a.lse[(int64_t)h * a.lse_hs + q] : INFINITY;  // exp(-inf) = 0 for padding rows
+        D_s[r] = ok ? a.D[(int64_t)h * a.D_hs + q] : 0.0f;
+    }
+}
+
+// key side: one CTA per (64 keys, head); dK, dV accumulated over every query tile
+template <int DP>
+__global__ void __launch_bounds__(BT) dense_bwd_dkdv_kernel(DenseBwdArgs a) {
+    extern __shared__ __align__(16) float sm[];
+    constexpr int RS = TB * (DP + 1);
+    float* Ks = sm;
+    float* Vs = Ks + RS;
+    float* Qs = Vs + RS;
+    float* dOs = Qs + RS;
+    float* Ps = dOs + RS;            // [TB][TB+1]
+    float* dSs = Ps + TB * (TB + 1);
+    float* lse_s = dSs + TB * (TB + 1);
+    float* D_s = lse_s + TB;
+    const int h = blockIdx.y;
+    const int64_t k0 = (int64_t)blockIdx.x * TB;
+    const int kn = (int)min((int64_t)TB, a.nk - k0);
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    constexpr int NJ = DP / 16;
+    load_tile<DP>(Ks, a.k, h, k0, a.nk, a.dim);
+    load_tile<DP>(Vs, a.v, h, k0, a.nk, a.dim);
+    float adk[4][NJ], adv[4][NJ];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) adk[i][j] = adv[i][j] = 0.0f;
+
+    for (int64_t q0 = 0; q0 < a.nq; q0 += TB) {
+        __syncthreads();
+        load_tile<DP>(Qs, a.q, h, q0, a.nq, a.dim);
+        load_tile<DP>(dOs, a.dout, h, q0, a.nq, a.dim);
+        load_stats<DP>(lse_s, D_s, a, h, q0);
+        __syncthreads();
+        score_tile<DP>(Qs, dOs, Ks, Vs, lse_s, D_s, kn, a.scale, Ps, dSs);
+        __syncthreads();
+#pragma unroll 2
+        for (int q = 0; q < TB; ++q) {
+            float p[4], ds[4], od[NJ], qd[NJ];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                p[i] = Ps[q * (TB + 1) + ty + 16 * i];
+                ds[i] = dSs[q * (TB + 1) + ty + 16 * i];
+            }
+#pragma unroll
+            for (int j = 0; j < NJ; ++j) {
+                od[j] = dOs[q * (DP + 1) + tx + 16 * j];
+                qd[j] = Qs[q * (DP + 1) + tx + 16 * j];
+            }
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < NJ; ++j) {
+                    adv[i][j] = fmaf(p[i], od[j], adv[i][j]);
+                    adk[i][j] = fmaf(ds[i], qd[j], adk[i][j]);
+                }
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int k = ty + 16 * i;
+        if (k >= kn) continue;
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) {
+            const int c = tx + 16 * j;
+            if (c >= a.dim) continue;
+            float* pk = a.dk.p + (int64_t)h * a.dk.hs + (k0 + k) * a.dk.rs + c;
+            float* pv = a.dv.p + (int64_t)h * a.dv.hs + (k0 + k) * a.dv.rs + c;
+            *pk = a.accumulate ? *pk + adk[i][j] : adk[i][j];
+            *pv = a.accumulate ? *pv + adv[i][j] : adv[i][j];
+        }
+    }
+}
+
+// query side: one CTA per (64 queries, head); dQ accumulated over every key tile
+template <int DP>
+__global__ void __launch_bounds__(BT) dense_bwd_dq_kernel(DenseBwdArgs a) {
+    extern __shared__ __align__(16) float sm[];
+    constexpr int RS = TB * (DP + 1);
+    float* Qs = sm;
+    float* dOs = Qs + RS;
+    float* Ks = dOs + RS;
+    float* Vs = Ks + RS;
+    float* Ps = Vs + RS;
+    float* dSs = Ps + TB * (TB + 1);
+    float* lse_s = dSs + TB * (TB + 1);
+    float* D_s = lse_s + TB;
+    const int h = blockIdx.y;
+    const int64_t q0 = (int64_t)blockIdx.x * TB;
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    constexpr int NJ = DP / 16;
+    load_tile<DP>(Qs, a.q, h, q0, a.nq, a.dim);
+    load_tile<DP>(dOs, a.dout, h, q0, a.nq, a.dim);
+    load_stats<DP>(lse_s, D_s, a, h, q0);
+    float adq[4][NJ];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) adq[i][j] = 0.0f;
+
+    for (int64_t k0 = 0; k0 < a.nk; k0 += TB) {
+        const int kn = (int)min((int64_t)TB, a.nk - k0);
+        __syncthreads();
+        load_tile<DP>(Ks, a.k, h, k0, a.nk, a.dim);
+        load_tile<DP>(Vs, a.v, h, k0, a.nk, a.dim);
+        __syncthreads();
+        score_tile<DP>(Qs, dOs, Ks, Vs, lse_s, D_s, kn, a.scale, Ps, dSs);
+        __syncthreads();
+#pragma unroll 2
+        for (int k = 0; k < TB; ++k) {
+            float ds[4], kd[NJ];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) ds[i] = dSs[(ty + 16 * i) * (TB + 1) + k];
+#pragma unroll
+            for (int j = 0; j < NJ; ++j) kd[j] = Ks[k * (DP + 1) + tx + 16 * j];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < NJ; ++j) adq[i][j] = fmaf(ds[i], kd[j], adq[i][j]);
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int64_t q = q0 + ty + 16 * i;
+        if (q >= a.nq) continue;
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) {
+            const int c = tx + 16 * j;
+            if (c >= a.dim) continue;
+            float* p = a.dq.p + (int64_t)h * a.dq.hs + q * a.dq.rs + c;
+            *p = a.accumulate ? *p + adq[i][j] : adq[i][j];
+        }
+    }
+}
+
+// ------------------------------------------------------------ pool adjoint
+// dq_img += dQc[w] / s^2; dk_img = dKc[w] / s^2; dv_img = dVc[w] / s^2; special rows of
+// dk / dv zeroed (the special pass accumulates into every row afterwards)
+__global__ void pool_bwd_kernel(PoolBwdArgs a) {
+    const int64_t n = (int64_t)a.heads * a.rows * a.dim;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+        const int j = (int)(e % a.dim);
+        const int64_t t = (e / a.dim) % a.rows;
+        const int h = (int)(e / ((int64_t)a.dim * a.rows));
+        const int64_t ok = (int64_t)h * a.dk.hs + t * a.dk.rs + j, ov = (int64_t)h * a.dv.hs + t * a.dv.rs + j;
+        if (t < a.L.num_special) {
+            a.dk.p[ok] = 0.0f;
+            a.dv.p[ov] = 0.0f;
+            continue;
+        }
+        const int w = a.L.window_of_token((int)(t - a.L.num_special));
+        const int64_t c = ((int64_t)h * a.L.windows + w) * a.dim + j;
+        float* pq = a.dq.p + (int64_t)h * a.dq.hs + t * a.dq.rs + j;
+        *pq += a.dqc[c] * a.inv;
+        a.dk.p[ok] = a.dkc[c] * a.inv;
+        a.dv.p[ov] = a.dvc[c] * a.inv;
+    }
+}
+
+// -------------------------------------------------------- selection branch
+template <int DP>
+__device__ __forceinline__ float dot_rows(const float* a, const float* b) {
+    float acc = 0.0f;
+#pragma unroll 8
+    for (int d = 0; d < DP; ++d) acc = fmaf(a[d], b[d], acc);
+    return acc;
+}
+
+constexpr int CK = 64;  // keys (or queries) staged per chunk
+
+// query side: CTA per (head, query window); the s^2 queries share the plan row
+template <int DP>
+__global__ void __launch_bounds__(BT) sel_bwd_dq_kernel(SelBwdArgs a) {
+    extern __shared__ __align__(16) float sm[];
+    const DevLayout& L = a.L;
+    const int dim = a.dim, s2 = L.s * L.s, W = L.windows, Mi = L.image_tokens, Ms = L.num_special;
+    constexpr int RP = DP + 1;
+    float* Qs = sm;               // [s2][RP]
+    float* dOs = Qs + s2 * RP;    // [s2][RP]  dS_sel rows
+    float* Ks = dOs + s2 * RP;    // [CK][RP]
+    float* Vs = Ks + CK * RP;     // [CK][RP]
+    float* dSs = Vs + CK * RP;    // [s2][CK+1]
+    float* lse_s = dSs + s2 * (CK + 1);
+    float* D_s = lse_s + s2;
+    __shared__ int ktok[CK];
+    const int64_t row = blockIdx.x;
+    const int h = (int)(row / W), w = (int)(row - (int64_t)h * W);
+    const int tid = threadIdx.x;
+    for (int e = tid; e < s2 * DP; e += BT) {
+        const int m = e / DP, j = e - m * DP;
+        const int i = L.member(w, m);
+        Qs[m * RP + j] = j < dim ? a.q.p[(int64_t)h * a.q.hs + (int64_t)(Ms + i) * a.q.rs + j] : 0.0f;
+        dOs[m * RP + j] = j < dim ? a.ds[((int64_t)h * Mi + i) * dim + j] : 0.0f;
+    }
+    for (int m = tid; m < s2; m += BT) {
+        const int i = L.member(w, m);
+        lse_s[m] = a.lse[(int64_t)h * Mi + i];
+        D_s[m] = a.D[(int64_t)h * Mi + i];
+    }
+    constexpr int R = CK * DP / BT;  // accumulator slots per thread (covers s2 <= 64)
+    float acc[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) acc[r] = 0.0f;
+
+    const int64_t nkeys = (a.offsets[row + 1] - a.offsets[row]) * s2;
+    const int32_t* ids = a.ids + a.offsets[row];
+    for (int64_t k0 = 0; k0 < nkeys; k0 += CK) {
+        const int kn = (int)min((int64_t)CK, nkeys - k0);
+        __syncthreads();
+        if (tid < CK) {
+            const int64_t kk = k0 + tid;
+            ktok[tid] = tid < kn ? L.member(ids[kk / s2], (int)(kk % s2)) : 0;
+        }
+        __syncthreads();
+        for (int e = tid; e < CK * DP; e += BT) {
+            const int r = e / DP, j = e - r * DP;
+            float kx = 0.0f, vx = 0.0f;
+            if (r < kn && j < dim) {
+                const int64_t t = Ms + ktok[r];
+                kx = a.k.p[(int64_t)h * a.k.hs + t * a.k.rs + j];
+                vx = a.v.p[(int64_t)h * a.v.hs + t * a.v.rs + j];
+            }
+            Ks[r * RP + j] = kx;
+            Vs[r * RP + j] = vx;
+        }
+        __syncthreads();
+        for (int e = tid; e < s2 * CK; e += BT) {
+            const int m = e / CK, c = e - m * CK;
+            float ds = 0.0f;
+            if (c < kn) {
+                const float p = expf(dot_rows<DP>(Qs + m * RP, Ks + c * RP) * a.scale - lse_s[m]);
+                ds = p * (dot_rows<DP>(dOs + m * RP, Vs + c * RP) - D_s[m]) * a.scale;
+            }
+            dSs[m * (CK + 1) + c] = ds;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const int e = tid + r * BT;
+            const int m = e / DP, j = e - m * DP;
+            if (m < s2) {
+                float x = acc[r];
+                for (int c = 0; c < kn; ++c) x = fmaf(dSs[m * (CK + 1) + c], Ks[c * RP + j], x);
+                acc[r] = x;
+            }
+        }
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int e = tid + r * BT;
+        const int m = e / DP, j = e - m * DP;
+        if (m < s2 && j < dim) a.dq.p[(int64_t)h * a.dq.hs + (int64_t)(Ms + L.member(w, m)) * a.dq.rs + j] += acc[r];
+    }
+}
+
+// key side: CTA per (head, key window); the query windows come from the inverse plan
+template <int DP>
+__global__ void __launch_bounds__(BT) sel_bwd_dkdv_kernel(SelBwdArgs a) {
+    extern __shared__ __align__(16) float sm[];
+    const DevLayout& L = a.L;
+    const int dim = a.dim, s2 = L.s * L.s, W = L.windows, Mi = L.image_tokens, Ms = L.num_special;
+    constexpr int RP = DP + 1;
+    float* Ks = sm;               // [s2][RP]
+    float* Vs = Ks + s2 * RP;     // [s2][RP]
+    float* Qs = Vs + s2 * RP;     // [CK][RP]
+    float* dOs = Qs + CK * RP;    // [CK][RP]
+    float* Ps = dOs + CK * RP;    // [CK][s2+1]
+    float* dSs = Ps + CK * (s2 + 1);
+    float* lse_s = dSs + CK * (s2 + 1);
+    float* D_s = lse_s + CK;
+    __shared__ int qtok[CK];
+    const int64_t row = blockIdx.x;
+    const int h = (int)(row / W), w = (int)(row - (int64_t)h * W);
+    const int tid = threadIdx.x;
+    for (int e = tid; e < s2 * DP; e += BT) {
+        const int m = e / DP, j = e - m * DP;
+        const int64_t t = Ms + L.member(w, m);
+        Ks[m * RP + j] = j < dim ? a.k.p[(int64_t)h * a.k.hs + t * a.k.rs + j] : 0.0f;
+        Vs[m * RP + j] = j < dim ? a.v.p[(int64_t)h * a.v.hs + t * a.v.rs + j] : 0.0f;
+    }
+    constexpr int R = CK * DP / BT;
+    float acck[R], accv[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) acck[r] = accv[r] = 0.0f;
+
+    const int64_t nq = (a.inv_offsets[row + 1] - a.inv_offsets[row]) * s2;
+    const int32_t* qwins = a.inv_q + a.inv_offsets[row];
+    for (int64_t q0 = 0; q0 < nq; q0 += CK) {
+        const int qn = (int)min((int64_t)CK, nq - q0);
+        __syncthreads();
+        if (tid < CK) {
+            const int64_t qq = q0 + tid;
+            const int i = tid < qn ? L.member(qwins[qq / s2], (int)(qq % s2)) : 0;
+            qtok[tid] = i;
+            lse_s[tid] = tid < qn ? a.lse[(int64_t)h * Mi + i] : INFINITY;
+            D_s[tid] = tid < qn ? a.D[(int64_t)h * Mi + i] : 0.0f;
+        }
+        __syncthreads();
+        for (int e = tid; e < CK * DP; e += BT) {
+            const int r = e / DP, j = e - r * DP;
+            float qx = 0.0f, ox = 0.0f;
+            if (r < qn && j < dim) {
+                const int i = qtok[r];
+                qx = a.q.p[(int64_t)h * a.q.hs + (int64_t)(Ms + i) * a.q.rs + j];
+                ox = a.ds[((int64_t)h * Mi + i) * dim + j];
+            }
+            Qs[r * RP + j] = qx;
+            dOs[r * RP + j] = ox;
+        }
+        __syncthreads();
+        for (int e = tid; e < CK * s2; e += BT) {
+            const int r = e / s2, c = e - r * s2;
+            float p = 0.0f, ds = 0.0f;
+            if (r < qn) {
+                p = expf(dot_rows<DP>(Qs + r * RP, Ks + c * RP) * a.scale - lse_s[r]);
+                ds = p * (dot_rows<DP>(dOs + r * RP, Vs + c * RP) - D_s[r]) * a.scale;
+            }
+            Ps[r * (s2 + 1) + c] = p;
+            dSs[r * (s2 + 1) + c] = ds;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const int e = tid + r * BT;
+            const int c = e / DP, j = e - c * DP;
+            if (c < s2) {
+                float xk = acck[r], xv = accv[r];
+                for (int q = 0; q < qn; ++q) {
+                    xv = fmaf(Ps[q * (s2 + 1) + c], dOs[q * RP + j], xv);
+                    xk = fmaf(dSs[q * (s2 + 1) + c], Qs[q * RP + j], xk);
+                }
+                acck[r] = xk;
+                accv[r] = xv;
+            }
+        }
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int e = tid + r * BT;
+        const int c = e / DP, j = e - c * DP;
+        if (c < s2 && j < dim) {
+            const int64_t t = Ms + L.member(w, c);
+            a.dk.p[(int64_t)h * a.dk.hs + t * a.dk.rs + j] += acck[r];
+            a.dv.p[(int64_t)h * a.dv.hs + t * a.dv.rs + j] += accv[r];
+        }
+    }
+}
+
+// inverse plan: one sort key (head * W + key window) << 32 | query window per plan entry
+__global__ void inv_keys_kernel(const int64_t* offsets, const int32_t* ids, int64_t rows, int W,
+                                unsigned long long* keys, unsigned long long* counts) {
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= rows) return;
+    const int64_t h = r / W, qw = r - h * W;
+    for (int64_t e = offsets[r]; e < offsets[r + 1]; ++e) {
+        const unsigned long long hk = (unsigned long long)(h * W + ids[e]);
+        keys[e] = (hk << 32) | (unsigned long long)qw;
+        atomicAdd(counts + hk, 1ull);  // integer counts: order-independent
+    }
+}
+
+__global__ void inv_extract_kernel(const unsigned long long* keys, int64_t n, int32_t* q) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e < n) q[e] = (int32_t)(keys[e] & 0xffffffffull);
+}
+
+// ------------------------------------------------------------- small GEMMs
+// part[h][split] (R x N) = A[h][rows of split]^T B[h][rows of split]
+__global__ void __launch_bounds__(BT) atb_kernel(AtbArgs a) {
+    __shared__ float As[16][TB + 1], Bs[16][TB + 1];
+    const int tilesN = (a.N + TB - 1) / TB;
+    const int r0 = (blockIdx.x / tilesN) * TB, n0 = (blockIdx.x % tilesN) * TB;
+    const int split = blockIdx.y, h = blockIdx.z;
+    const int64_t m_begin = (int64_t)split * a.chunk, m_end = min(a.rows, m_begin + a.chunk);
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    const float* A = a.A + (int64_t)h * a.a_hs;
+    const float* B = a.B + (int64_t)h * a.b_hs;
+    float acc[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = 0.0f;
+    for (int64_t m0 = m_begin; m0 < m_end; m0 += 16) {
+        __syncthreads();
+        for (int e = threadIdx.x; e < 16 * TB; e += BT) {
+            const int kk = e / TB, c = e - kk * TB;
+            const int64_t m = m0 + kk;
+            As[kk][c] = (m < m_end && r0 + c < a.R) ? A[m * a.a_rs + r0 + c] : 0.0f;
+            Bs[kk][c] = (m < m_end && n0 + c < a.N) ? B[m * a.b_rs + n0 + c] : 0.0f;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int kk = 0; kk < 16; ++kk) {
+            float av[4], bv[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                av[i] = As[kk][ty + 16 * i];
+                bv[i] = Bs[kk][tx + 16 * i];
+            }
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
+        }
+    }
+    float* P = a.part + ((int64_t)h * a.splits + split) * a.R * a.N;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int r = r0 + ty + 16 * i;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int n = n0 + tx + 16 * j;
+            if (r < a.R && n < a.N) P[(int64_t)r * a.N + n] = acc[i][j];
+        }
+    }
+}
+
+__global__ void atb_reduce_kernel(const float* part, int splits, int64_t per_head, int64_t total, float* out) {
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t h = e / per_head, r = e - h * per_head;
+        const float* p = part + h * splits * per_head + r;
+        float acc = 0.0f;
+        for (int s = 0; s < splits; ++s) acc += p[(int64_t)s * per_head];
+        out[e] = acc;
+    }
+}
+
+// dX[m][c] = sum over (matrix, head, j) of G[mat][h][m][j] * W[mat][h][c][j]
+__global__ void __launch_bounds__(BT) dx_gemm_kernel(DxArgs a) {
+    __shared__ float As[16][TB + 1], Bs[16][TB + 1];
+    const int tilesC = (a.C + TB - 1) / TB;
+    const int64_t m0 = (int64_t)(blockIdx.x / tilesC) * TB;
+    const int c0 = (blockIdx.x % tilesC) * TB;
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    float acc[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = 0.0f;
+    for (int mat = 0; mat < 3; ++mat)
+        for (int h = 0; h < a.heads; ++h) {
+            const float* G = a.g[mat] + (int64_t)h * a.tokens * a.dim;
+            const float* Wm = a.w[mat] + (int64_t)h * a.C * a.dim;
+            for (int j0 = 0; j0 < a.dim; j0 += 16) {
+                __syncthreads();
+                for (int e = threadIdx.x; e < 16 * TB; e += BT) {
+                    const int r = e / 16, kk = e - r * 16;
+                    const int j = j0 + kk;
+                    As[kk][r] = (m0 + r < a.tokens && j < a.dim) ? G[(m0 + r) * a.dim + j] : 0.0f;
+                    Bs[kk][r] = (c0 + r < a.C && j < a.dim) ? Wm[(int64_t)(c0 + r) * a.dim + j] : 0.0f;
+                }
+                __syncthreads();
+#pragma unroll
+                for (int kk = 0; kk < 16; ++kk) {
+                    float av[4], bv[4];
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        av[i] = As[kk][ty + 16 * i];
+                        bv[i] = Bs[kk][tx + 16 * i];
+                    }
+#pragma unroll
+                    for (int i = 0; i < 4; ++i)
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
+                }
+            }
+        }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int64_t m = m0 + ty + 16 * i;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int c = c0 + tx + 16 * j;
+            if (m < a.tokens && c < a.C) a.dx[m * a.C + c] = acc[i][j];
+        }
+    }
+}
+
+// strided f32 / bf16 rows -> contiguous f32 [H][rows][dim]
+template <typename T>
+__global__ void to_f32_kernel(TensorRef in, int heads, int64_t rows, int dim, float* out) {
+    const int64_t n = (int64_t)heads * rows * dim;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+        const int j = (int)(e % dim);
+        const int64_t r = (e / dim) % rows;
+        const int64_t h = e / ((int64_t)dim * rows);
+        out[e] = to_f32(reinterpret_cast<const T*>(in.data)[h * in.hs + r * in.rs + j]);
+    }
+}
+
+// f32 [H][Ms][d] . [H][Ms][d] row dots (D of the special rows)
+__global__ void rowdot_kernel(FMat a, FMat b, int heads, int rows, int dim, float* out) {
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (warp >= (int64_t)heads * rows) return;
+    const int h = (int)(warp / rows), r = (int)(warp % rows);
+    const float* x = a.p + (int64_t)h * a.hs + (int64_t)r * a.rs;
+    const float* y = b.p + (int64_t)h * b.hs + (int64_t)r * b.rs;
+    float acc = 0.0f;
+    for (int j = lane; j < dim; j += 32) acc += x[j] * y[j];
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) out[warp] = acc;
+}
+
+// avg_pool_backward (gradients.hpp:21-34): out[h][t] = in[h][window_of(t)] * (1/s^2)
+__global__ void pool_adjoint_kernel(FMat in, int heads, int dim, DevLayout L, float inv, FOut out) {
+    const int64_t n = (int64_t)heads * L.image_tokens * dim;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+        const int j = (int)(e % dim);
+        const int t = (int)((e / dim) % L.image_tokens);
+        const int64_t h = e / ((int64_t)dim * L.image_tokens);
+        out.p[h * out.hs + (int64_t)t * out.rs + j] =
+            __fmul_rn(in.p[h * in.hs + (int64_t)L.window_of_token(t) * in.rs + j], inv);
+    }
+}
+
+// upsample_backward (gradients.hpp:37-49): member rows summed in ascending token order
+__global__ void window_sum_kernel(FMat in, int heads, int dim, DevLayout L, FOut out) {
+    const int64_t n = (int64_t)heads * L.windows * dim;
+    const int s2 = L.s * L.s;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+        const int j = (int)(e % dim);
+        const int w = (int)((e / dim) % L.windows);
+        const int64_t h = e / ((int64_t)dim * L.windows);
+        float acc = 0.0f;
+        for (int m = 0; m < s2; ++m) acc = __fadd_rn(acc, in.p[h * in.hs + (int64_t)L.member(w, m) * in.rs + j]);
+        out.p[h * out.hs + (int64_t)w * out.rs + j] = acc;
+    }
+}
+
+unsigned grid_for(int64_t n, int threads = 256) {
+    const int64_t b = (n + threads - 1) / threads;
+    return (unsigned)(b < 148 * 64 ? (b > 0 ? b : 1) : 148 * 64);
+}
+
+template <int DP>
+size_t dense_smem() {
+    return (size_t)(4 * TB * (DP + 1) + 2 * TB * (TB + 1) + 2 * TB) * sizeof(float);
+}
+
+template <int DP>
+cudaError_t dense_bwd_dp(const DenseBwdArgs& a, int heads, cudaStream_t st) {
+    const size_t smem = dense_smem<DP>();
+    cudaError_t e = cudaFuncSetAttribute(dense_bwd_dkdv_kernel<DP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(dense_bwd_dq_kernel<DP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    if (a.dk.p) {
+        dense_bwd_dkdv_kernel<DP><<<dim3((unsigned)((a.nk + TB - 1) / TB), heads), BT, smem, st>>>(a);
+        note_launch();
+    }
+    if (a.dq.p) {
+        dense_bwd_dq_kernel<DP><<<dim3((unsigned)((a.nq + TB - 1) / TB), heads), BT, smem, st>>>(a);
+        note_launch();
+    }
+    return cudaGetLastError();
+}
+
+template <int DP>
+cudaError_t gate_bwd_dp(const GateBwdArgs& a, int heads, cudaStream_t st) {
+    const int s2 = a.L.s * a.L.s;
+    const size_t smem = (size_t)(DP * (DP + 1) + 3 * s2 * DP + DP) * sizeof(float);
+    cudaError_t e = cudaFuncSetAttribute(gate_bwd_kernel<DP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    gate_bwd_kernel<DP><<<(unsigned)((int64_t)heads * a.L.windows), BT, smem, st>>>(a);
+    note_launch();
+    return cudaGetLastError();
+}
+
+template <int DP>
+cudaError_t sel_bwd_dp(const SelBwdArgs& a, int heads, cudaStream_t st) {
+    const int s2 = a.L.s * a.L.s;
+    const int64_t rows = (int64_t)heads * a.L.windows;
+    const size_t smem_q = (size_t)(2 * s2 * (DP + 1) + 2 * CK * (DP + 1) + s2 * (CK + 1) + 2 * s2) * sizeof(float);
+    const size_t smem_k = (size_t)(2 * s2 * (DP + 1) + 2 * CK * (DP + 1) + 2 * CK * (s2 + 1) + 2 * CK) * sizeof(float);
+    cudaError_t e = cudaFuncSetAttribute(sel_bwd_dq_kernel<DP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_q);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(sel_bwd_dkdv_kernel<DP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_k);
+    if (e != cudaSuccess) return e;
+    sel_bwd_dq_kernel<DP><<<(unsigned)rows, BT, smem_q, st>>>(a);
+    sel_bwd_dkdv_kernel<DP><<<(unsigned)rows, BT, smem_k, st>>>(a);
+    note_launch(2);
+    return cudaGetLastError();
+}
+
+int dp_of(int dim) { return dim <= 32 ? 32 : dim <= 64 ? 64 : 128; }
+
+}  // namespace
+
+cudaError_t launch_gate_bwd(const GateBwdArgs& a, int heads, cudaStream_t st) {
+    if ((int64_t)heads * a.L.windows == 0) return cudaSuccess;
+    switch (dp_of(a.dim)) {
+        case 32: return gate_bwd_dp<32>(a, heads, st);
+        case 64: return gate_bwd_dp<64>(a, heads, st);
+        default: return gate_bwd_dp<128>(a, heads, st);
+    }
+}
+
+cudaError_t launch_dense_bwd(const DenseBwdArgs& a, int heads, cudaStream_t st) {
+    if (heads == 0 || a.nq == 0 || a.nk == 0) return cudaSuccess;
+    switch (dp_of(a.dim)) {
+        case 32: return dense_bwd_dp<32>(a, heads, st);
+        case 64: return dense_bwd_dp<64>(a, heads, st);
+        default: return dense_bwd_dp<128>(a, heads, st);
+    }
+}
+
+cudaError_t launch_pool_bwd(const PoolBwdArgs& a, cudaStream_t st) {
+    const int64_t n = (int64_t)a.heads * a.rows * a.dim;
+    if (n == 0) return cudaSuccess;
+    pool_bwd_kernel<<<grid_for(n), 256, 0, st>>>(a);
+    note_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_sel_bwd(const SelBwdArgs& a, int heads, cudaStream_t st) {
+    if ((int64_t)heads * a.L.windows == 0) return cudaSuccess;
+    switch (dp_of(a.dim)) {
+        case 32: return sel_bwd_dp<32>(a, heads, st);
+        case 64: return sel_bwd_dp<64>(a, heads, st);
+        default: return sel_bwd_dp<128>(a, heads, st);
+    }
+}
+
+size_t inverse_plan_tmp_bytes(int64_t rows, int64_t entries) {
+    size_t sort_bytes = 0;
+    cub::DeviceRadixSort::SortKeys(nullptr, sort_bytes, (const unsigned long long*)nullptr,
+                                   (unsigned long long*)nullptr, (int64_t)entries, 0, 64);
+    const size_t scan = scan_offsets_tmp_bytes(rows);
+    return (sort_bytes > scan ? sort_bytes : scan) + 256;
+}
+
+cudaError_t launch_inverse_plan(const int64_t* offsets, const int32_t* ids, int64_t rows, int W, int64_t entries,
+                                unsigned long long* keys, unsigned long long* keys_sorted, int64_t* counts,
+                                int64_t* inv_offsets, int32_t* inv_q, void* tmp, size_t tmp_bytes,
+                                cudaStream_t st) {
+    cudaError_t e = cudaMemsetAsync(counts, 0, (size_t)rows * sizeof(int64_t), st);
+    if (e != cudaSuccess) return e;
+    if (rows == 0) return cudaSuccess;
+    inv_keys_kernel<<<(unsigned)((rows + 255) / 256), 256, 0, st>>>(offsets, ids, rows, W, keys,
+                                                                  reinterpret_cast<unsigned long long*>(counts));
+    note_launch();
+    int hi_bits = 1;
+    while ((int64_t(1) << hi_bits) < rows) ++hi_bits;
+    size_t tb = tmp_bytes;
+    e = cub::DeviceRadixSort::SortKeys(tmp, tb, keys, keys_sorted, entries, 0, 32 + hi_bits, st);
+    if (e != cudaSuccess) return e;
+    e = launch_scan_offsets(counts, rows, inv_offsets, tmp, tmp_bytes, st);
+    if (e != cudaSuccess) return e;
+    if (entries) {
+        inv_extract_kernel<<<(unsigned)((entries + 255) / 256), 256, 0, st>>>(keys_sorted, entries, inv_q);
+        note_launch();
+    }
+    return cudaGetLastError();
+}
+
+int atb_splits(int heads, int R, int N, int64_t rows) {
+    const int64_t tiles = (int64_t)heads * ((R + TB - 1) / TB) * ((N + TB - 1) / TB);
+    int64_t s = (2 * 148 + tiles - 1) / tiles;
+    const int64_t max_s = (rows + 511) / 512;
+    if (s > max_s) s = max_s;
+    if (s > 64) s = 64;
+    return (int)(s < 1 ? 1 : s);
+}
+
+cudaError_t launch_atb(AtbArgs a, int heads, float* out, cudaStream_t st) {
+    if (heads == 0 || a.R == 0 || a.N == 0) return cudaSuccess;
+    a.chunk = (a.rows + a.splits - 1) / a.splits;
+    a.chunk = (a.chunk + 15) / 16 * 16;
+    const unsigned tiles = (unsigned)(((a.R + TB - 1) / TB) * ((a.N + TB - 1) / TB));
+    atb_kernel<<<dim3(tiles, a.splits, heads), BT, 0, st>>>(a);
+    const int64_t per_head = (int64_t)a.R * a.N, total = per_head * heads;
+    atb_reduce_kernel<<<grid_for(total), 256, 0, st>>>(a.part, a.splits, per_head, total, out);
+    note_launch(2);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_dx_gemm(const DxArgs& a, cudaStream_t st) {
+    if (a.tokens == 0 || a.C == 0) return cudaSuccess;
+    const int64_t tiles = ((a.tokens + TB - 1) / TB) * (int64_t)((a.C + TB - 1) / TB);
+    dx_gemm_kernel<<<(unsigned)tiles, BT, 0, st>>>(a);
+    note_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_to_f32(const TensorRef& in, int heads, int64_t rows, int dim, float* out, cudaStream_t st) {
+    const int64_t n = (int64_t)heads * rows * dim;
+    if (n == 0) return cudaSuccess;
+    if (in.dtype == GSA_DTYPE_BF16) to_f32_kernel<__nv_bfloat16><<<grid_for(n), 256, 0, st>>>(in, heads, rows, dim, out);
+    else to_f32_kernel<float><<<grid_for(n), 256, 0, st>>>(in, heads, rows, dim, out);
+    note_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_pool_adjoint(const FMat& in, int heads, int dim, const DevLayout& L, float inv, const FOut& out,
+                                cudaStream_t st) {
+    const int64_t n = (int64_t)heads * L.image_tokens * dim;
+    if (n == 0) return cudaSuccess;
+    pool_adjoint_kernel<<<grid_for(n), 256, 0, st>>>(in, heads, dim, L, inv, out);
+    note_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_window_sum(const FMat& in, int heads, int dim, const DevLayout& L, const FOut& out, cudaStream_t st) {
+    const int64_t n = (int64_t)heads * L.windows * dim;
+    if (n == 0) return cudaSuccess;
+    window_sum_kernel<<<grid_for(n), 256, 0, st>>>(in, heads, dim, L, out);
+    note_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_rowdot(const FMat& a, const FMat& b, int heads, int rows, int dim, float* out, cudaStream_t st) {
+    const int64_t n = (int64_t)heads * rows * 32;
+    if (n == 0) return cudaSuccess;
+    rowdot_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(a, b, heads, rows, dim, out);
+    note_launch();
+    return cudaGetLastError();
+}
+
+}  // namespace gsa_sm100

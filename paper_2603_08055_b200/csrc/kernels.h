@@ -131,4 +131,91 @@ size_t scan_offsets_tmp_bytes(int64_t n);
 cudaError_t launch_plan_check(const int64_t* offsets, int64_t rows, const int32_t* ids, int n_windows, int* flag,
                               cudaStream_t st);
 
+// ---- layer backward (backward.cu), f32 ------------------------------------
+struct FMat {  // read-only f32 [H][rows][d] view, element strides
+    const float* p;
+    int64_t hs, rs;
+};
+struct FOut {  // writable f32 [H][rows][d] view
+    float* p;
+    int64_t hs, rs;
+};
+// gate fuse + upsample backward, one CTA per (head, window)
+struct GateBwdArgs {
+    FMat dout;                    // [H][M][d] (image rows at num_special..)
+    const float *gate, *o_sel;    // [H][Mi][d]
+    const float *o_comp, *w_g;    // [H][W][d], [H][d][d]
+    DevLayout L;
+    int dim;
+    float *ds, *dz;               // [H][Mi][d]: (1-g) dO, g(1-g)(O_comp-O_sel) dO
+    float *d_oc, *d_sel, *d_comp; // [H][W][d] window sums of g dO; D rows [H][Mi], [H][W]
+    FOut dq;                      // image rows written with W_g dz
+};
+cudaError_t launch_gate_bwd(const GateBwdArgs& a, int heads, cudaStream_t st);
+// FlashAttention-2 style backward of dense softmax attention from saved LSE rows;
+// dq / dk (+dv) passes run when the pointer is non-null
+struct DenseBwdArgs {
+    FMat q, k, v, dout;
+    const float *lse, *D;
+    int64_t lse_hs, D_hs;
+    int64_t nq, nk;
+    int dim;
+    float scale;
+    FOut dq, dk, dv;
+    bool accumulate;  // += into the outputs instead of =
+};
+cudaError_t launch_dense_bwd(const DenseBwdArgs& a, int heads, cudaStream_t st);
+struct PoolBwdArgs {
+    int heads;
+    int64_t rows;  // all M rows of dq/dk/dv
+    int dim;
+    DevLayout L;
+    float inv;
+    const float *dqc, *dkc, *dvc;  // [H][W][d]
+    FOut dq, dk, dv;
+};
+cudaError_t launch_pool_bwd(const PoolBwdArgs& a, cudaStream_t st);
+struct SelBwdArgs {
+    FMat q, k, v;                  // full rows (image rows at num_special..)
+    const float *ds, *lse, *D;     // [H][Mi][d], [H][Mi], [H][Mi]
+    const int64_t* offsets;        // plan CSR [H*W+1]
+    const int32_t* ids;
+    const int64_t* inv_offsets;    // inverse plan CSR [H*W+1]: query windows per key window
+    const int32_t* inv_q;
+    DevLayout L;
+    int dim;
+    float scale;
+    FOut dq, dk, dv;               // accumulated into (image rows)
+};
+cudaError_t launch_sel_bwd(const SelBwdArgs& a, int heads, cudaStream_t st);
+size_t inverse_plan_tmp_bytes(int64_t rows, int64_t entries);
+cudaError_t launch_inverse_plan(const int64_t* offsets, const int32_t* ids, int64_t rows, int W, int64_t entries,
+                                unsigned long long* keys, unsigned long long* keys_sorted, int64_t* counts,
+                                int64_t* inv_offsets, int32_t* inv_q, void* tmp, size_t tmp_bytes,
+                                cudaStream_t st);
+// out[h] (R x N) = A[h]^T B[h] over `rows` rows, split `splits` ways with a fixed-order reduction
+struct AtbArgs {
+    const float *A, *B;
+    int64_t a_hs, a_rs, b_hs, b_rs;
+    int R, N;
+    int64_t rows, chunk;
+    int splits;
+    float* part;  // [H][splits][R][N]
+};
+int atb_splits(int heads, int R, int N, int64_t rows);
+cudaError_t launch_atb(AtbArgs a, int heads, float* out, cudaStream_t st);
+struct DxArgs {
+    const float* g[3];  // dQ, dK, dV [H][tokens][d] contiguous
+    const float* w[3];  // W_q, W_k, W_v [H][C][d]
+    int heads, dim, C;
+    int64_t tokens;
+    float* dx;          // [tokens][C]
+};
+cudaError_t launch_dx_gemm(const DxArgs& a, cudaStream_t st);
+cudaError_t launch_to_f32(const TensorRef& in, int heads, int64_t rows, int dim, float* out, cudaStream_t st);
+cudaError_t launch_pool_adjoint(const FMat& in, int heads, int dim, const DevLayout& L, float inv, const FOut& out,
+                                cudaStream_t st);
+cudaError_t launch_window_sum(const FMat& in, int heads, int dim, const DevLayout& L, const FOut& out, cudaStream_t st);
+cudaError_t launch_rowdot(const FMat& a, const FMat& b, int heads, int rows, int dim, float* out, cudaStream_t st);
+
 }  // namespace gsa_sm100

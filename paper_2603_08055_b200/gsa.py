@@ -17,7 +17,7 @@ from typing import Optional
 import torch
 
 from . import _lib
-from ._lib import GsaContextC, GsaLayout, GsaParamsC, GsaTensor
+from ._lib import GsaContextC, GsaLayout, GsaParamsC, GsaSavedC, GsaTensor
 
 
 # ----------------------------------------------------------------- errors
@@ -69,9 +69,13 @@ class WorkspaceError(GsaError):
     pass
 
 
+class ContextMismatch(GsaError):
+    pass
+
+
 _STATUS = {1: GsaError, 2: ShapeMismatch, 3: DivisibilityError, 4: ZeroSizeError, 5: IndexOutOfRange,
            6: NonFiniteInput, 7: InvalidTiling, 8: InvalidStride, 9: EmptySelection, 10: Unsupported,
-           11: CudaError, 12: WorkspaceError, 13: GsaError}
+           11: CudaError, 12: WorkspaceError, 13: GsaError, 14: ContextMismatch}
 
 
 def _check(rc: int) -> None:
@@ -449,6 +453,92 @@ def gsa_forward_with_plan(q, k, v, w_g, layout: TokenLayout, params: GsaParams, 
                                    C.byref(_desc(w_g.contiguous())), C.byref(lc), C.byref(pc), _ptr(plan.offsets),
                                    _ptr(plan.window_ids), C.byref(_desc(out)), _ptr(ws), ws.numel(), _stream()))
     return out
+
+
+# ----------------------------------------------------------------- backward
+def avg_pool_backward(d_pooled: torch.Tensor, layout: TokenLayout) -> torch.Tensor:
+    """gradients.hpp:21-34: [H, W, d] -> [H, Mi, d], each member row = its window's row / s^2."""
+    H, _, d = d_pooled.shape
+    out = _empty(H, layout.image_tokens, d, device=d_pooled.device)
+    _check(_lib.load().gsa_avg_pool_backward(C.byref(_desc(d_pooled)), C.byref(layout.c()), C.byref(_desc(out)),
+                                             _stream()))
+    return out
+
+
+def upsample_backward(d_fine: torch.Tensor, layout: TokenLayout) -> torch.Tensor:
+    """gradients.hpp:37-49: [H, Mi, d] -> [H, W, d], member rows summed per window."""
+    H, _, d = d_fine.shape
+    out = _empty(H, layout.num_windows, d, device=d_fine.device)
+    _check(_lib.load().gsa_upsample_backward(C.byref(_desc(d_fine)), C.byref(layout.c()), C.byref(_desc(out)),
+                                             _stream()))
+    return out
+
+
+def gsa_backward(q, k, v, w_g, layout: TokenLayout, params: GsaParams, ctx: ForwardContext, out: torch.Tensor,
+                 d_out: torch.Tensor, plan: Optional[SelectionPlan] = None, workspace: Optional[Workspace] = None):
+    """gsa_backward (gradients.hpp:54-243) up to the projection: the layer's gradients with
+    respect to the projected q/k/v and to W_g, with the top-k held constant. `ctx` and `out`
+    are what gsa_forward(..., context=True) returned for the same q/k/v; the plan is rebuilt
+    from ctx.topk unless given. Returns (dq, dk, dv, dw_g), f32."""
+    L = _lib.load()
+    H, M, d = q.shape
+    dev = q.device
+    if plan is None:
+        plan = build_selection_plan(ctx.topk, layout, params.variant, params.ref_stride)
+    Ms = layout.num_special
+    lc, pc = layout.c(), params.c()
+    E = int(plan.window_ids.numel())
+    ws_bytes = L.gsa_backward_workspace_bytes(C.byref(lc), C.byref(pc), H, d, E, _desc(q).dtype)
+    ws = (workspace or _default_workspace(dev)).get(ws_bytes, dev)
+    saved = GsaSavedC(ctx.qc.data_ptr(), ctx.kc.data_ptr(), ctx.vc.data_ptr(), ctx.o_comp_coarse.data_ptr(),
+                      ctx.lse_comp.data_ptr(), plan.offsets.data_ptr(), plan.window_ids.data_ptr(), E,
+                      ctx.o_sel.data_ptr(), ctx.lse_sel.data_ptr(), ctx.gate_vals.data_ptr(), _desc(out[:, :Ms]),
+                      ctx.lse_spec.data_ptr() if Ms else None)
+    d_out = d_out.float()
+    dq, dk, dv = (_empty(H, M, d, device=dev) for _ in range(3))
+    dw_g = _empty(H, d, d, device=dev)
+    _check(L.gsa_backward(C.byref(_desc(q)), C.byref(_desc(k)), C.byref(_desc(v)), C.byref(_desc(w_g.contiguous())),
+                          C.byref(lc), C.byref(pc), C.byref(saved), C.byref(_desc(d_out)), C.byref(_desc(dq)),
+                          C.byref(_desc(dk)), C.byref(_desc(dv)), _ptr(dw_g), _ptr(ws), ws.numel(), _stream()))
+    return dq, dk, dv, dw_g
+
+
+def project_backward(x, w_q, w_k, w_v, dq, dk, dv):
+    """Projection backward (gradients.hpp:226-263): dW_* = X^T dY per head and
+    dX = sum_h dQ W_q^T + dK W_k^T + dV W_v^T. Returns (dx, dw_q, dw_k, dw_v), f32."""
+    L = _lib.load()
+    x, w_q, w_k, w_v, dq, dk, dv = (t.float().contiguous() for t in (x, w_q, w_k, w_v, dq, dk, dv))
+    if x.dim() == 3:
+        x = x.reshape(x.shape[-2], x.shape[-1])
+    T, Cm = x.shape
+    H, _, d = w_q.shape
+    dx = _empty(T, Cm, device=x.device)
+    dws = [_empty(H, Cm, d, device=x.device) for _ in range(3)]
+    ws = torch.empty(L.gsa_project_backward_workspace_bytes(T, Cm, H, d), dtype=torch.uint8, device=x.device)
+    _check(L.gsa_project_backward(_ptr(x), T, Cm, _ptr(w_q), _ptr(w_k), _ptr(w_v), H, d, _ptr(dq), _ptr(dk), _ptr(dv),
+                                  _ptr(dx), *[_ptr(t) for t in dws], _ptr(ws), ws.numel(), _stream()))
+    return (dx, *dws)
+
+
+@dataclass
+class GsaGradients:
+    """gradients.hpp:14-19."""
+    dx: torch.Tensor    # [tokens, model_dim]
+    dw_q: torch.Tensor  # [H, model_dim, d]
+    dw_k: torch.Tensor
+    dw_v: torch.Tensor
+    dw_g: torch.Tensor  # [H, d, d]
+
+
+def layer_backward(x, w_q, w_k, w_v, w_g, layout: TokenLayout, params: GsaParams, d_out,
+                   workspace: Optional[Workspace] = None) -> tuple[torch.Tensor, GsaGradients]:
+    """gsa_forward (layer.hpp:177-230) from X then gsa_backward (gradients.hpp:54-265):
+    the full layer gradient with respect to X and every weight. Returns (out, grads)."""
+    q, k, v = project_qkv(x, w_q, w_k, w_v)
+    out, ctx = gsa_forward(q, k, v, w_g, layout, params, context=True, workspace=workspace)
+    dq, dk, dv, dw_g = gsa_backward(q, k, v, w_g, layout, params, ctx, out, d_out, workspace=workspace)
+    dx, dwq, dwk, dwv = project_backward(x, w_q, w_k, w_v, dq, dk, dv)
+    return out, GsaGradients(dx, dwq, dwk, dwv, dw_g)
 
 
 def forward_stats(layout: TokenLayout, params: GsaParams, heads: int) -> tuple[int, int]:
