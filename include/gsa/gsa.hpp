@@ -5,6 +5,7 @@
 #include "gsa/compression.hpp"
 #include "gsa/device.hpp"
 #include "gsa/errors.hpp"
+#include "gsa/gradients.hpp"
 #include "gsa/layer.hpp"
 #include "gsa/layout.hpp"
 #include "gsa/selection.hpp"

@@ -193,6 +193,21 @@ int main(int argc, char** argv) {
                                          static_cast<int64_t>(stats.keys_attended.load())};
         dump("stats", st, "i64", {2});
 
+        // ---- the layer backward (gradients.hpp:54-265) with a random upstream gradient
+        {
+            const gsa::Tensor<float> d_out = random_tensor(heads, layout.total_tokens(), dim, 1.0f, 6);
+            const gsa::GsaGradients<float> g = gsa::gsa_backward(r.saved, d_out, 8);
+            dump("d_out", d_out);
+            dump("dx", g.dx);
+            dump("dw_q", g.dw_q);
+            dump("dw_k", g.dw_k);
+            dump("dw_v", g.dw_v);
+            dump("dw_g", g.dw_g);
+            expect_throw<gsa::ContextMismatch>("backward_shape", [&] {
+                gsa::gsa_backward(r.saved, gsa::Tensor<float>(heads, layout.total_tokens() - 1, dim));
+            });
+        }
+
         // ---- the per-branch operators on the projected tensors
         const float scale = gsa::resolved_scale<float>(p, dim);
         auto parts = gsa::partition_qkv(r.saved.q, r.saved.k, r.saved.v, layout);
