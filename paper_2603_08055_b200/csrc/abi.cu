@@ -1220,6 +1220,8 @@ struct BwdBufs {
     size_t tmp_bytes;
     float* part;
     int splits;
+    float* spec_dq_part;  // key-split partial dQ of the special rows
+    int spec_splits;
 };
 
 size_t carve_bwd(const DevLayout& L, int Ms, int H, int d, int64_t E, bool convert, char* base, size_t cap,
@@ -1250,6 +1252,8 @@ size_t carve_bwd(const DevLayout& L, int Ms, int H, int d, int64_t E, bool conve
     b->tmp = c.take<char>(b->tmp_bytes);
     b->splits = atb_splits(H, d, d, Mi);
     b->part = c.take<float>((size_t)H * b->splits * d * d);
+    b->spec_splits = Ms > 0 ? dense_dq_splits(H, Ms, M) : 1;
+    b->spec_dq_part = b->spec_splits > 1 ? c.take<float>((size_t)b->spec_splits * H * Ms * d) : nullptr;
     return c.used;
 }
 
@@ -1416,6 +1420,8 @@ int gsa_backward(const gsa_tensor* q, const gsa_tensor* k, const gsa_tensor* v, 
         sp.dv = FOut{nullptr, 0, 0};
         sp.dq = dQ;  // the special rows' only dQ term: written
         sp.accumulate = false;
+        sp.k_splits = b.spec_splits;
+        sp.dq_part = b.spec_dq_part;
         GSA_CUDA(launch_dense_bwd(sp, H, st));
     }
 

@@ -104,44 +104,57 @@ __global__ void __launch_bounds__(BT) gate_bwd_kernel(GateBwdArgs a) {
 }
 
 // ---------------------------------------------------------- dense attention
+// Tiles of 64 rows padded to DP + 4 floats (16-byte aligned rows: float4 reads, and 16
+// consecutive rows start 4 banks apart, so a float4 read of 16 rows takes the minimum
+// two wavefronts). P / dS tiles are 64 x 68.
+constexpr int PT = TB + 4;
+
 template <int DP>
 __device__ __forceinline__ void load_tile(float* dst, const FMat& m, int h, int64_t r0, int64_t rows, int dim) {
+    constexpr int RP = DP + 4;
     for (int e = threadIdx.x; e < TB * DP; e += BT) {
         const int r = e / DP, j = e - r * DP;
         float x = 0.0f;
         if (r0 + r < rows && j < dim) x = m.p[(int64_t)h * m.hs + (r0 + r) * m.rs + j];
-        dst[r * (DP + 1) + j] = x;
+        dst[r * RP + j] = x;
     }
 }
 
-// S and dP for the 64 x 64 tile: rows ty + 16 i of Qs / dOs, columns tx + 16 j of Ks / Vs;
-// stores P and dS = P (dP - D) scale; invalid keys (col >= kn) get P = 0.
-template <int DP>
+__device__ __forceinline__ float4 ld4(const float* p) { return *reinterpret_cast<const float4*>(p); }
+__device__ __forceinline__ float dot4(float4 a, float4 b, float c) {
+    return fmaf(a.w, b.w, fmaf(a.z, b.z, fmaf(a.y, b.y, fmaf(a.x, b.x, c))));
+}
+
+// S and dP of the 64 x 64 tile (thread: query rows ty + 16 i, keys tx + 16 j), then
+// P = exp(scale S - lse) and dS = P (dP - D) scale into Ps / dSs, either [q][k]
+// (TRANS = false) or [k][q]; keys >= kn get P = dS = 0.
+template <int DP, bool TRANS>
 __device__ __forceinline__ void score_tile(const float* Qs, const float* dOs, const float* Ks, const float* Vs,
                                            const float* lse, const float* D, int kn, float scale, float* Ps,
                                            float* dSs) {
+    constexpr int RP = DP + 4;
     const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
     float s[4][4], dp[4][4];
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j) s[i][j] = dp[i][j] = 0.0f;
-#pragma unroll 4
-    for (int d = 0; d < DP; ++d) {
-        float qv[4], ov[4], kv[4], vv[4];
+#pragma unroll 2
+    for (int d = 0; d < DP; d += 4) {
+        float4 qv[4], ov[4], kv[4], vv[4];
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-            qv[i] = Qs[(ty + 16 * i) * (DP + 1) + d];
-            ov[i] = dOs[(ty + 16 * i) * (DP + 1) + d];
-            kv[i] = Ks[(tx + 16 * i) * (DP + 1) + d];
-            vv[i] = Vs[(tx + 16 * i) * (DP + 1) + d];
+            qv[i] = ld4(Qs + (ty + 16 * i) * RP + d);
+            ov[i] = ld4(dOs + (ty + 16 * i) * RP + d);
+            kv[i] = ld4(Ks + (tx + 16 * i) * RP + d);
+            vv[i] = ld4(Vs + (tx + 16 * i) * RP + d);
         }
 #pragma unroll
         for (int i = 0; i < 4; ++i)
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
-                s[i][j] = fmaf(qv[i], kv[j], s[i][j]);
-                dp[i][j] = fmaf(ov[i], vv[j], dp[i][j]);
+                s[i][j] = dot4(qv[i], kv[j], s[i][j]);
+                dp[i][j] = dot4(ov[i], vv[j], dp[i][j]);
             }
     }
 #pragma unroll
@@ -151,13 +164,13 @@ __device__ __forceinline__ void score_tile(const float* Qs, const float* dOs, co
         for (int j = 0; j < 4; ++j) {
             const int k = tx + 16 * j;
             const float p = k < kn ? expf(s[i][j] * scale - lse[q]) : 0.0f;
-            Ps[q * (TB + 1) + k] = p;
-            dSs[q * (TB + 1) + k] = p * (dp[i][j] - D[q]) * scale;
+            const int at = TRANS ? k * PT + q : q * PT + k;
+            Ps[at] = p;
+            dSs[at] = p * (dp[i][j] - D[q]) * scale;
         }
     }
 }
 
-template <int DP>
 __device__ __forceinline__ void load_stats(float* lse_s, float* D_s, const DenseBwdArgs& a, int h, int64_t q0) {
     for (int r = threadIdx.x; r < TB; r += BT) {
         const int64_t q = q0 + r;
@@ -167,136 +180,150 @@ __device__ __forceinline__ void load_stats(float* lse_s, float* D_s, const Dense
     }
 }
 
-// key side: one CTA per (64 keys, head); dK, dV accumulated over every query tile
+// rows 4 ty + i (i < 4) x features 4 tx + 64 c (c < DP / 64, 4 each) of an accumulator tile
+template <int DP>
+__device__ __forceinline__ void store_rows(float (*acc)[DP / 16], const FOut& o, int h, int64_t r0, int64_t rows,
+                                           int dim, bool accumulate) {
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int64_t r = r0 + 4 * ty + i;
+        if (r >= rows) continue;
+        float* row = o.p + (int64_t)h * o.hs + r * o.rs;
+#pragma unroll
+        for (int c = 0; c < DP / 64; ++c)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int j = 64 * c + 4 * tx + e;
+                if (j < dim) row[j] = accumulate ? row[j] + acc[i][4 * c + e] : acc[i][4 * c + e];
+            }
+    }
+}
+
+// key side: one CTA per (64 keys, head); dK, dV accumulated over every query tile.
+// Accumulators: keys 4 ty + i, features 4 tx + 64 c + e.
 template <int DP>
 __global__ void __launch_bounds__(BT) dense_bwd_dkdv_kernel(DenseBwdArgs a) {
     extern __shared__ __align__(16) float sm[];
-    constexpr int RS = TB * (DP + 1);
+    constexpr int RP = DP + 4, RS = TB * RP, NC = DP / 64, NA = DP / 16;
     float* Ks = sm;
     float* Vs = Ks + RS;
     float* Qs = Vs + RS;
     float* dOs = Qs + RS;
-    float* Ps = dOs + RS;            // [TB][TB+1]
-    float* dSs = Ps + TB * (TB + 1);
-    float* lse_s = dSs + TB * (TB + 1);
+    float* Ps = dOs + RS;  // [q][k]
+    float* dSs = Ps + TB * PT;
+    float* lse_s = dSs + TB * PT;
     float* D_s = lse_s + TB;
     const int h = blockIdx.y;
     const int64_t k0 = (int64_t)blockIdx.x * TB;
     const int kn = (int)min((int64_t)TB, a.nk - k0);
     const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-    constexpr int NJ = DP / 16;
     load_tile<DP>(Ks, a.k, h, k0, a.nk, a.dim);
     load_tile<DP>(Vs, a.v, h, k0, a.nk, a.dim);
-    float adk[4][NJ], adv[4][NJ];
+    float adk[4][NA], adv[4][NA];
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < NJ; ++j) adk[i][j] = adv[i][j] = 0.0f;
+        for (int j = 0; j < NA; ++j) adk[i][j] = adv[i][j] = 0.0f;
 
     for (int64_t q0 = 0; q0 < a.nq; q0 += TB) {
         __syncthreads();
         load_tile<DP>(Qs, a.q, h, q0, a.nq, a.dim);
         load_tile<DP>(dOs, a.dout, h, q0, a.nq, a.dim);
-        load_stats<DP>(lse_s, D_s, a, h, q0);
+        load_stats(lse_s, D_s, a, h, q0);
         __syncthreads();
-        score_tile<DP>(Qs, dOs, Ks, Vs, lse_s, D_s, kn, a.scale, Ps, dSs);
+        score_tile<DP, false>(Qs, dOs, Ks, Vs, lse_s, D_s, kn, a.scale, Ps, dSs);
         __syncthreads();
 #pragma unroll 2
         for (int q = 0; q < TB; ++q) {
-            float p[4], ds[4], od[NJ], qd[NJ];
+            const float4 p = ld4(Ps + q * PT + 4 * ty), ds = ld4(dSs + q * PT + 4 * ty);
+            const float pv[4] = {p.x, p.y, p.z, p.w}, dv[4] = {ds.x, ds.y, ds.z, ds.w};
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                p[i] = Ps[q * (TB + 1) + ty + 16 * i];
-                ds[i] = dSs[q * (TB + 1) + ty + 16 * i];
+            for (int c = 0; c < NC; ++c) {
+                const float4 o = ld4(dOs + q * RP + 64 * c + 4 * tx), x = ld4(Qs + q * RP + 64 * c + 4 * tx);
+                const float ov[4] = {o.x, o.y, o.z, o.w}, xv[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        adv[i][4 * c + e] = fmaf(pv[i], ov[e], adv[i][4 * c + e]);
+                        adk[i][4 * c + e] = fmaf(dv[i], xv[e], adk[i][4 * c + e]);
+                    }
             }
-#pragma unroll
-            for (int j = 0; j < NJ; ++j) {
-                od[j] = dOs[q * (DP + 1) + tx + 16 * j];
-                qd[j] = Qs[q * (DP + 1) + tx + 16 * j];
-            }
-#pragma unroll
-            for (int i = 0; i < 4; ++i)
-#pragma unroll
-                for (int j = 0; j < NJ; ++j) {
-                    adv[i][j] = fmaf(p[i], od[j], adv[i][j]);
-                    adk[i][j] = fmaf(ds[i], qd[j], adk[i][j]);
-                }
         }
     }
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        const int k = ty + 16 * i;
-        if (k >= kn) continue;
-#pragma unroll
-        for (int j = 0; j < NJ; ++j) {
-            const int c = tx + 16 * j;
-            if (c >= a.dim) continue;
-            float* pk = a.dk.p + (int64_t)h * a.dk.hs + (k0 + k) * a.dk.rs + c;
-            float* pv = a.dv.p + (int64_t)h * a.dv.hs + (k0 + k) * a.dv.rs + c;
-            *pk = a.accumulate ? *pk + adk[i][j] : adk[i][j];
-            *pv = a.accumulate ? *pv + adv[i][j] : adv[i][j];
-        }
-    }
+    if (a.dk.p) store_rows<DP>(adk, a.dk, h, k0, a.nk, a.dim, a.accumulate);
+    if (a.dv.p) store_rows<DP>(adv, a.dv, h, k0, a.nk, a.dim, a.accumulate);
 }
 
-// query side: one CTA per (64 queries, head); dQ accumulated over every key tile
+// query side: one CTA per (64 queries, head, key split); dQ accumulated over the split's
+// key tiles, written (or, with splits, stored as a partial the reduction sums in order)
 template <int DP>
 __global__ void __launch_bounds__(BT) dense_bwd_dq_kernel(DenseBwdArgs a) {
     extern __shared__ __align__(16) float sm[];
-    constexpr int RS = TB * (DP + 1);
+    constexpr int RP = DP + 4, RS = TB * RP, NC = DP / 64, NA = DP / 16;
     float* Qs = sm;
     float* dOs = Qs + RS;
     float* Ks = dOs + RS;
     float* Vs = Ks + RS;
     float* Ps = Vs + RS;
-    float* dSs = Ps + TB * (TB + 1);
-    float* lse_s = dSs + TB * (TB + 1);
+    float* dSs = Ps + TB * PT;  // [k][q]
+    float* lse_s = dSs + TB * PT;
     float* D_s = lse_s + TB;
-    const int h = blockIdx.y;
+    const int h = blockIdx.z, split = blockIdx.y;
     const int64_t q0 = (int64_t)blockIdx.x * TB;
     const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-    constexpr int NJ = DP / 16;
     load_tile<DP>(Qs, a.q, h, q0, a.nq, a.dim);
     load_tile<DP>(dOs, a.dout, h, q0, a.nq, a.dim);
-    load_stats<DP>(lse_s, D_s, a, h, q0);
-    float adq[4][NJ];
+    load_stats(lse_s, D_s, a, h, q0);
+    float adq[4][NA];
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < NJ; ++j) adq[i][j] = 0.0f;
+        for (int j = 0; j < NA; ++j) adq[i][j] = 0.0f;
 
-    for (int64_t k0 = 0; k0 < a.nk; k0 += TB) {
-        const int kn = (int)min((int64_t)TB, a.nk - k0);
+    const int64_t kb = (int64_t)split * a.k_chunk, ke = min(a.nk, kb + a.k_chunk);
+    for (int64_t k0 = kb; k0 < ke; k0 += TB) {
+        const int kn = (int)min((int64_t)TB, ke - k0);
         __syncthreads();
-        load_tile<DP>(Ks, a.k, h, k0, a.nk, a.dim);
-        load_tile<DP>(Vs, a.v, h, k0, a.nk, a.dim);
+        load_tile<DP>(Ks, a.k, h, k0, ke, a.dim);
+        load_tile<DP>(Vs, a.v, h, k0, ke, a.dim);
         __syncthreads();
-        score_tile<DP>(Qs, dOs, Ks, Vs, lse_s, D_s, kn, a.scale, Ps, dSs);
+        score_tile<DP, true>(Qs, dOs, Ks, Vs, lse_s, D_s, kn, a.scale, Ps, dSs);
         __syncthreads();
 #pragma unroll 2
         for (int k = 0; k < TB; ++k) {
-            float ds[4], kd[NJ];
+            const float4 ds = ld4(dSs + k * PT + 4 * ty);
+            const float dv[4] = {ds.x, ds.y, ds.z, ds.w};
 #pragma unroll
-            for (int i = 0; i < 4; ++i) ds[i] = dSs[(ty + 16 * i) * (TB + 1) + k];
+            for (int c = 0; c < NC; ++c) {
+                const float4 x = ld4(Ks + k * RP + 64 * c + 4 * tx);
+                const float xv[4] = {x.x, x.y, x.z, x.w};
 #pragma unroll
-            for (int j = 0; j < NJ; ++j) kd[j] = Ks[k * (DP + 1) + tx + 16 * j];
+                for (int i = 0; i < 4; ++i)
 #pragma unroll
-            for (int i = 0; i < 4; ++i)
-#pragma unroll
-                for (int j = 0; j < NJ; ++j) adq[i][j] = fmaf(ds[i], kd[j], adq[i][j]);
+                    for (int e = 0; e < 4; ++e) adq[i][4 * c + e] = fmaf(dv[i], xv[e], adq[i][4 * c + e]);
+            }
         }
     }
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        const int64_t q = q0 + ty + 16 * i;
-        if (q >= a.nq) continue;
-#pragma unroll
-        for (int j = 0; j < NJ; ++j) {
-            const int c = tx + 16 * j;
-            if (c >= a.dim) continue;
-            float* p = a.dq.p + (int64_t)h * a.dq.hs + q * a.dq.rs + c;
-            *p = a.accumulate ? *p + adq[i][j] : adq[i][j];
-        }
+    if (a.k_splits > 1) {
+        const FOut part{a.dq_part + (int64_t)split * a.heads * a.nq * a.dim, a.nq * a.dim, a.dim};
+        store_rows<DP>(adq, part, h, q0, a.nq, a.dim, false);
+    } else {
+        store_rows<DP>(adq, a.dq, h, q0, a.nq, a.dim, a.accumulate);
+    }
+}
+
+// dQ from the key-split partials, summed in split order
+__global__ void dq_reduce_kernel(DenseBwdArgs a) {
+    const int64_t n = (int64_t)a.heads * a.nq * a.dim, stride = n;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+        const int j = (int)(e % a.dim);
+        const int64_t q = (e / a.dim) % a.nq, h = e / ((int64_t)a.dim * a.nq);
+        float acc = 0.0f;
+        for (int s = 0; s < a.k_splits; ++s) acc += a.dq_part[s * stride + e];
+        float* o = a.dq.p + h * a.dq.hs + q * a.dq.rs + j;
+        *o = a.accumulate ? *o + acc : acc;
     }
 }
 
@@ -513,6 +540,188 @@ __global__ void __launch_bounds__(BT) sel_bwd_dkdv_kernel(SelBwdArgs a) {
     }
 }
 
+// s = 4 fast path of both selection passes, register-tiled: a CTA (128 threads) owns the
+// 16 rows of one window (the FIXED side: its queries, or with KEYSIDE its keys) and streams
+// the GATHERED side in chunks of 64 rows (4 windows of the plan row, or of the inverse plan
+// row). Per chunk:
+//   S = A1 . B1^T and T = A2 . B2^T (16 x 64; thread: fixed rows la + 4 i, gathered rows
+//   16 warp + lb + 8 j), P = exp(scale S - lse), dS = P (T - D) scale -> X (and P -> Y)
+//   stored [gathered][fixed];
+//   out1 += X^T B1 (and out2 += Y^T B2) (thread: fixed rows 4 la + i, features
+//   warp DP/4 + lb DP/32 + e).
+// dq pass:   A1 = Q, A2 = dS_sel rows, B1 = K, B2 = V; stats by fixed row; out1 = dQ.
+// dkdv pass: A1 = K, A2 = V, B1 = Q, B2 = dS_sel rows; stats by gathered row; out1 = dK,
+//            out2 = dV.
+// Every shared read is a broadcast or 4 / 8 consecutive padded rows (one wavefront).
+constexpr int SF = 16, SG = 64, ST = 128, XP = SF + 4;
+
+__device__ __forceinline__ float4 ldg4(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
+
+template <int DP, bool KEYSIDE>
+__global__ void __launch_bounds__(ST) sel16_bwd_kernel(SelBwdArgs a) {
+    extern __shared__ __align__(16) float sm[];
+    constexpr int RP = DP + 4, ND = DP / 32, C4 = DP / 4;
+    float* A1 = sm;
+    float* A2 = A1 + SF * RP;
+    float* B1 = A2 + SF * RP;
+    float* B2 = B1 + SG * RP;
+    float* X = B2 + SG * RP;
+    float* Y = X + SG * XP;
+    __shared__ int gtok[SG];
+    __shared__ float st_lse[SG], st_D[SG];
+    const DevLayout& L = a.L;
+    const int dim = a.dim, W = L.windows, Mi = L.image_tokens, Ms = L.num_special;
+    const int64_t row = blockIdx.x;
+    const int h = (int)(row / W), w = (int)(row - (int64_t)h * W);
+    const int tid = threadIdx.x, warp = tid >> 5, la = (tid & 31) >> 3, lb = tid & 7;
+    const float* dsb = a.ds + (int64_t)h * Mi * dim;
+
+    for (int e = tid; e < SF * C4; e += ST) {
+        const int r = e / C4, c = (e - r * C4) * 4;
+        const int i = L.member(w, r);
+        float4 v1 = make_float4(0.f, 0.f, 0.f, 0.f), v2 = v1;
+        if (c < dim) {
+            const int64_t t = Ms + i;
+            if (KEYSIDE) {
+                v1 = ldg4(a.k.p + (int64_t)h * a.k.hs + t * a.k.rs + c);
+                v2 = ldg4(a.v.p + (int64_t)h * a.v.hs + t * a.v.rs + c);
+            } else {
+                v1 = ldg4(a.q.p + (int64_t)h * a.q.hs + t * a.q.rs + c);
+                v2 = ldg4(dsb + (int64_t)i * dim + c);
+            }
+        }
+        *reinterpret_cast<float4*>(A1 + r * RP + c) = v1;
+        *reinterpret_cast<float4*>(A2 + r * RP + c) = v2;
+    }
+    __shared__ float f_lse[SF], f_D[SF];
+    if (!KEYSIDE && tid < SF) {
+        const int i = L.member(w, tid);
+        f_lse[tid] = a.lse[(int64_t)h * Mi + i];
+        f_D[tid] = a.D[(int64_t)h * Mi + i];
+    }
+    float o1[4][ND], o2[4][ND];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int e = 0; e < ND; ++e) o1[i][e] = o2[i][e] = 0.0f;
+
+    const int64_t beg = KEYSIDE ? a.inv_offsets[row] : a.offsets[row];
+    const int64_t n = ((KEYSIDE ? a.inv_offsets[row + 1] : a.offsets[row + 1]) - beg) * SF;
+    const int32_t* list = (KEYSIDE ? a.inv_q : a.ids) + beg;
+    for (int64_t g0 = 0; g0 < n; g0 += SG) {
+        const int gn = (int)min((int64_t)SG, n - g0);
+        __syncthreads();
+        if (tid < SG) {
+            int t = 0;
+            if (tid < gn) {
+                const int64_t gg = g0 + tid;
+                t = L.member(list[gg / SF], (int)(gg % SF));
+            }
+            gtok[tid] = t;
+            if (KEYSIDE) {
+                st_lse[tid] = tid < gn ? a.lse[(int64_t)h * Mi + t] : INFINITY;
+                st_D[tid] = tid < gn ? a.D[(int64_t)h * Mi + t] : 0.0f;
+            }
+        }
+        __syncthreads();
+        for (int e = tid; e < SG * C4; e += ST) {
+            const int r = e / C4, c = (e - r * C4) * 4;
+            float4 v1 = make_float4(0.f, 0.f, 0.f, 0.f), v2 = v1;
+            if (r < gn && c < dim) {
+                const int i = gtok[r];
+                const int64_t t = Ms + i;
+                if (KEYSIDE) {
+                    v1 = ldg4(a.q.p + (int64_t)h * a.q.hs + t * a.q.rs + c);
+                    v2 = ldg4(dsb + (int64_t)i * dim + c);
+                } else {
+                    v1 = ldg4(a.k.p + (int64_t)h * a.k.hs + t * a.k.rs + c);
+                    v2 = ldg4(a.v.p + (int64_t)h * a.v.hs + t * a.v.rs + c);
+                }
+            }
+            *reinterpret_cast<float4*>(B1 + r * RP + c) = v1;
+            *reinterpret_cast<float4*>(B2 + r * RP + c) = v2;
+        }
+        __syncthreads();
+        float sv[4][2], tv[4][2];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 2; ++j) sv[i][j] = tv[i][j] = 0.0f;
+#pragma unroll 4
+        for (int d = 0; d < DP; d += 4) {
+            float4 a1[4], a2[4], b1[2], b2[2];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                a1[i] = ld4(A1 + (la + 4 * i) * RP + d);
+                a2[i] = ld4(A2 + (la + 4 * i) * RP + d);
+            }
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                b1[j] = ld4(B1 + (16 * warp + lb + 8 * j) * RP + d);
+                b2[j] = ld4(B2 + (16 * warp + lb + 8 * j) * RP + d);
+            }
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 2; ++j) {
+                    sv[i][j] = dot4(a1[i], b1[j], sv[i][j]);
+                    tv[i][j] = dot4(a2[i], b2[j], tv[i][j]);
+                }
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                const int f = la + 4 * i, g = 16 * warp + lb + 8 * j;
+                const float lse = KEYSIDE ? st_lse[g] : f_lse[f];
+                const float Dv = KEYSIDE ? st_D[g] : f_D[f];
+                const float p = g < gn ? expf(sv[i][j] * a.scale - lse) : 0.0f;
+                X[g * XP + f] = p * (tv[i][j] - Dv) * a.scale;
+                if (KEYSIDE) Y[g * XP + f] = p;
+            }
+        __syncthreads();
+        const int d0 = warp * (DP / 4) + lb * ND;
+        for (int g = 0; g < gn; ++g) {
+            const float4 x = ld4(X + g * XP + 4 * la);
+            const float xv[4] = {x.x, x.y, x.z, x.w};
+            float c1[ND];
+#pragma unroll
+            for (int e = 0; e < ND; ++e) c1[e] = B1[g * RP + d0 + e];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int e = 0; e < ND; ++e) o1[i][e] = fmaf(xv[i], c1[e], o1[i][e]);
+            if (KEYSIDE) {
+                const float4 y = ld4(Y + g * XP + 4 * la);
+                const float yv[4] = {y.x, y.y, y.z, y.w};
+                float c2[ND];
+#pragma unroll
+                for (int e = 0; e < ND; ++e) c2[e] = B2[g * RP + d0 + e];
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+#pragma unroll
+                    for (int e = 0; e < ND; ++e) o2[i][e] = fmaf(yv[i], c2[e], o2[i][e]);
+            }
+        }
+    }
+    const int d0 = warp * (DP / 4) + lb * ND;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int64_t t = Ms + L.member(w, 4 * la + i);
+#pragma unroll
+        for (int e = 0; e < ND; ++e) {
+            const int j = d0 + e;
+            if (j >= dim) continue;
+            if (KEYSIDE) {
+                a.dk.p[(int64_t)h * a.dk.hs + t * a.dk.rs + j] += o1[i][e];
+                a.dv.p[(int64_t)h * a.dv.hs + t * a.dv.rs + j] += o2[i][e];
+            } else {
+                a.dq.p[(int64_t)h * a.dq.hs + t * a.dq.rs + j] += o1[i][e];
+            }
+        }
+    }
+}
+
 // inverse plan: one sort key (head * W + key window) << 32 | query window per plan entry
 __global__ void inv_keys_kernel(const int64_t* offsets, const int32_t* ids, int64_t rows, int W,
                                 unsigned long long* keys, unsigned long long* counts) {
@@ -702,23 +911,32 @@ unsigned grid_for(int64_t n, int threads = 256) {
 
 template <int DP>
 size_t dense_smem() {
-    return (size_t)(4 * TB * (DP + 1) + 2 * TB * (TB + 1) + 2 * TB) * sizeof(float);
+    return (size_t)(4 * TB * (DP + 4) + 2 * TB * PT + 2 * TB) * sizeof(float);
 }
 
 template <int DP>
-cudaError_t dense_bwd_dp(const DenseBwdArgs& a, int heads, cudaStream_t st) {
+cudaError_t dense_bwd_dp(DenseBwdArgs a, int heads, cudaStream_t st) {
     const size_t smem = dense_smem<DP>();
     cudaError_t e = cudaFuncSetAttribute(dense_bwd_dkdv_kernel<DP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     e = cudaFuncSetAttribute(dense_bwd_dq_kernel<DP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    if (a.dk.p) {
+    a.heads = heads;
+    if (a.dk.p || a.dv.p) {
         dense_bwd_dkdv_kernel<DP><<<dim3((unsigned)((a.nk + TB - 1) / TB), heads), BT, smem, st>>>(a);
         note_launch();
     }
     if (a.dq.p) {
-        dense_bwd_dq_kernel<DP><<<dim3((unsigned)((a.nq + TB - 1) / TB), heads), BT, smem, st>>>(a);
+        const int64_t qtiles = (a.nq + TB - 1) / TB, ktiles = (a.nk + TB - 1) / TB;
+        if (a.k_splits < 1 || !a.dq_part) a.k_splits = 1;
+        a.k_chunk = (ktiles + a.k_splits - 1) / a.k_splits * TB;
+        a.k_splits = (int)((a.nk + a.k_chunk - 1) / a.k_chunk);
+        dense_bwd_dq_kernel<DP><<<dim3((unsigned)qtiles, a.k_splits, heads), BT, smem, st>>>(a);
         note_launch();
+        if (a.k_splits > 1) {
+            dq_reduce_kernel<<<grid_for((int64_t)heads * a.nq * a.dim), 256, 0, st>>>(a);
+            note_launch();
+        }
     }
     return cudaGetLastError();
 }
@@ -763,13 +981,20 @@ cudaError_t launch_gate_bwd(const GateBwdArgs& a, int heads, cudaStream_t st) {
     }
 }
 
+// key splits for the query-side pass when there are too few query tiles to fill the GPU
+// (the special rows: Ms / 64 tiles per head), each split at least 16 key tiles
+int dense_dq_splits(int heads, int64_t nq, int64_t nk) {
+    const int64_t ctas = (int64_t)heads * ((nq + TB - 1) / TB);
+    const int64_t want = (4 * 148 + ctas - 1) / ctas;
+    const int64_t cap = ((nk + TB - 1) / TB) / 16;
+    int64_t s = want < cap ? want : cap;
+    return (int)(s < 1 ? 1 : s > 64 ? 64 : s);
+}
+
 cudaError_t launch_dense_bwd(const DenseBwdArgs& a, int heads, cudaStream_t st) {
     if (heads == 0 || a.nq == 0 || a.nk == 0) return cudaSuccess;
-    switch (dp_of(a.dim)) {
-        case 32: return dense_bwd_dp<32>(a, heads, st);
-        case 64: return dense_bwd_dp<64>(a, heads, st);
-        default: return dense_bwd_dp<128>(a, heads, st);
-    }
+    // feature tiling 4 tx + 64 c needs DP >= 64 (padding columns are zero)
+    return a.dim <= 64 ? dense_bwd_dp<64>(a, heads, st) : dense_bwd_dp<128>(a, heads, st);
 }
 
 cudaError_t launch_pool_bwd(const PoolBwdArgs& a, cudaStream_t st) {
@@ -780,8 +1005,37 @@ cudaError_t launch_pool_bwd(const PoolBwdArgs& a, cudaStream_t st) {
     return cudaGetLastError();
 }
 
+namespace {
+
+template <int DP>
+cudaError_t sel16_bwd_dp(const SelBwdArgs& a, int heads, cudaStream_t st) {
+    const int64_t rows = (int64_t)heads * a.L.windows;
+    const size_t smem = (size_t)((2 * SF + 2 * SG) * (DP + 4) + 2 * SG * XP) * sizeof(float);
+    cudaError_t e = cudaFuncSetAttribute(sel16_bwd_kernel<DP, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(sel16_bwd_kernel<DP, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    sel16_bwd_kernel<DP, false><<<(unsigned)rows, ST, smem, st>>>(a);
+    sel16_bwd_kernel<DP, true><<<(unsigned)rows, ST, smem, st>>>(a);
+    note_launch(2);
+    return cudaGetLastError();
+}
+
+bool aligned4(const FMat& m) {
+    return (reinterpret_cast<uintptr_t>(m.p) & 15) == 0 && m.hs % 4 == 0 && m.rs % 4 == 0;
+}
+
+}  // namespace
+
 cudaError_t launch_sel_bwd(const SelBwdArgs& a, int heads, cudaStream_t st) {
     if ((int64_t)heads * a.L.windows == 0) return cudaSuccess;
+    if (a.L.s == 4 && a.dim % 4 == 0 && aligned4(a.q) && aligned4(a.k) && aligned4(a.v)) {
+        switch (dp_of(a.dim)) {
+            case 32: return sel16_bwd_dp<32>(a, heads, st);
+            case 64: return sel16_bwd_dp<64>(a, heads, st);
+            default: return sel16_bwd_dp<128>(a, heads, st);
+        }
+    }
     switch (dp_of(a.dim)) {
         case 32: return sel_bwd_dp<32>(a, heads, st);
         case 64: return sel_bwd_dp<64>(a, heads, st);

@@ -163,7 +163,14 @@ struct DenseBwdArgs {
     float scale;
     FOut dq, dk, dv;
     bool accumulate;  // += into the outputs instead of =
+    // query side split over keys (k_splits > 1): partial dQ [k_splits][H][nq][dim] in dq_part,
+    // summed in split order by a reduction (dense_dq_splits picks the count)
+    int k_splits;
+    float* dq_part;
+    int64_t k_chunk;  // set by the launcher
+    int heads;        // set by the launcher
 };
+int dense_dq_splits(int heads, int64_t nq, int64_t nk);
 cudaError_t launch_dense_bwd(const DenseBwdArgs& a, int heads, cudaStream_t st);
 struct PoolBwdArgs {
     int heads;
