@@ -190,6 +190,123 @@ def run_reference_arm(args):
 
 
 # ------------------------------------------------------------- GPU arm
+def run_backward(args):
+    """the layer backward on one GPU (--backward; not the headline metric).
+    One step = gsa_backward (gradients.hpp:54-243: gate fuse, upsample / pooling adjoints,
+    compressed, selection and special attention backward from the saved LSE rows, dW_g)
+    + gsa_project_backward (gradients.hpp:226-263: dW_q/k/v = X^T dY, dX) at model_dim
+    --model-dim, from one forward's saved context, everything resident in HBM. f32 on CUDA
+    cores: the roofline is the nominal FP32 FMA peak. cpu_baseline: the reference's own
+    gsa_forward + gsa_backward (oracle/_ref) on a 4-view sample with all host threads,
+    next to this GPU path on the same sample."""
+    import ctypes
+
+    import torch
+
+    import paper_2603_08055_b200 as gsa
+    from paper_2603_08055_b200 import _lib
+
+    torch.cuda.set_device(0)
+    lib = _lib.load()
+    V, C = args.views, args.model_dim
+    lt = layout_for(V)
+    G = geometry(V)
+    L = gsa.build_token_layout(*lt)
+    params = gsa.GsaParams(window_s=S, top_k=TOPK)
+
+    def instance(views, cm, seed=7):
+        ltv = layout_for(views)
+        Lv = gsa.build_token_layout(*ltv)
+        q, k, v, wg = synth_qkv(torch, views, seed=seed)
+        out, ctx = gsa.gsa_forward(q, k, v, wg, Lv, params, context=True)
+        plan = gsa.build_selection_plan(ctx.topk, Lv, 0, 100)
+        gen = torch.Generator(device="cuda").manual_seed(seed + 1)
+        d_out = torch.randn(out.shape, generator=gen, device="cuda")
+        M = out.shape[1]
+        x = torch.randn(M, cm, generator=gen, device="cuda")
+        w = [torch.randn(HEADS, cm, DIM, generator=gen, device="cuda") / cm ** 0.5 for _ in range(3)]
+        return Lv, q, k, v, wg, out, ctx, plan, d_out, x, w
+
+    Lv, q, k, v, wg, out, ctx, plan, d_out, x, w = instance(V, C)
+    ws = gsa.Workspace()
+
+    def step(evs=None):
+        if evs:
+            evs[0].record()
+        dq, dk, dv, dwg = gsa.gsa_backward(q, k, v, wg, Lv, params, ctx, out, d_out, plan=plan, workspace=ws)
+        if evs:
+            evs[1].record()
+        gsa.project_backward(x, *w, dq, dk, dv)
+        if evs:
+            evs[2].record()
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    n0 = ctypes.c_uint64()
+    lib.gsa_launch_count(ctypes.byref(n0))
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    with ClockSampler(0) as clk:
+        torch.cuda.synchronize()
+        for i in range(args.steps):
+            step(evs[i])
+        torch.cuda.synchronize()
+    n1 = ctypes.c_uint64()
+    lib.gsa_launch_count(ctypes.byref(n1))
+    attn_ms = statistics.median(e[0].elapsed_time(e[1]) for e in evs)
+    proj_ms = statistics.median(e[1].elapsed_time(e[2]) for e in evs)
+    total_ms = sum(e[0].elapsed_time(e[2]) for e in evs) / args.steps
+    E = int(plan.window_ids.numel())
+    # FlashAttention-2 accounting: 5 GEMM-like passes of 2 d flops per score (S, dP recomputed,
+    # dV, dK, dQ); scores: compressed H W^2, special H Ms M, selection entries * s^4
+    attn_flops = 5 * 2 * DIM * (HEADS * G["W"] ** 2 + HEADS * G["Ms"] * G["M"] + E * S ** 4)
+    proj_flops = 2 * 2 * 3 * G["M"] * C * HEADS * DIM
+    fp32_peak = 148 * 128 * 2 * 1.965e9 / 1e12
+    line = {"metric": f"GSA layer backward (dX, dW_q/k/v/g) at {V} views", "value": G["M"] / (total_ms / 1e3),
+            "unit": "tokens/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (torch N(0,1) bf16 Q/K/V, f32 X / W / dO), resident in HBM",
+            "config": {"workload": f"backward of 1 GSA layer, {V} views x ({SPECIAL_PER_VIEW} specials + {GRID_H}x{GRID_W} "
+                                   f"patches) = {G['M']} tokens, 16 heads x 64, s=4, top-{TOPK}, plain, model_dim {C}",
+                       "views": V, "tokens": G["M"], "windows": G["W"], "plan_entries": E, "model_dim": C,
+                       "parallelism": "1 GPU", "l2": "inputs larger than L2 (no flush)"},
+            "stage_ms": {"attention_backward": round(attn_ms, 3), "projection_backward": round(proj_ms, 3)},
+            "roofline": {"kernel": "attention backward (dense + selection passes, CUDA cores)", "bound": "fp32",
+                         "achieved": attn_flops / attn_ms / 1e9, "peak": fp32_peak, "unit": "TFLOP/s",
+                         "frac": attn_flops / attn_ms / 1e9 / fp32_peak, "traffic": None,
+                         "peak_kind": "nominal (148 SMs x 128 FP32 lanes x 2 x 1.965 GHz)"},
+            "projection_tflops": round(proj_flops / proj_ms / 1e9, 2),
+            "gpu_launches": int(n1.value - n0.value), "clocks": clk.summary()}
+    if not args.no_cpu_baseline:
+        from oracle import RefLib
+        if RefLib.available():
+            sv = 4
+            Ls, qs, ks, vs, wgs, outs, ctxs, plans, dos, xs, ws_ = instance(sv, C, seed=9)
+            ts = []
+            for _ in range(3):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                gsa.gsa_forward(qs, ks, vs, wgs, Ls, params, context=True)
+                g = gsa.gsa_backward(qs, ks, vs, wgs, Ls, params, ctxs, outs, dos, plan=plans)
+                gsa.project_backward(xs, *ws_, *g[:3])
+                e1.record()
+                torch.cuda.synchronize()
+                ts.append(e0.elapsed_time(e1))
+            threads = os.cpu_count() or 1
+            t0 = time.perf_counter()
+            r = RefLib().backward(xs.cpu().numpy(), *[t.cpu().numpy() for t in ws_], wgs.cpu().numpy(),
+                                  layout_for(sv), dos.cpu().numpy(), top_k=TOPK, threads=threads)
+            wall = time.perf_counter() - t0
+            Ms = geometry(sv)["M"]
+            ref_ms = r["ms"]["forward"] + r["ms"]["backward"]
+            line["cpu_baseline"] = {"value": Ms / (ref_ms / 1e3), "unit": "tokens/s", "cores": threads,
+                                    "kind": "reference",
+                                    "sample": f"reference gsa_forward + gsa_backward (f32) at {sv} views (M={Ms}), "
+                                              f"model_dim {C}, {ref_ms / 1e3:.1f} s ({wall:.1f} s wall incl. copies)",
+                                    "gpu_same_sample_tokens_per_s": Ms / (statistics.median(ts) / 1e3)}
+    print(json.dumps(line), flush=True)
+
+
 def run_stack(args):
     """BASELINE configs[2] on one GPU: an L-layer global-attention stack. One step
     = L x (X . W_qkv on the library tcgen05 GEMM -> GSA layer on strided head views -> head
@@ -296,6 +413,9 @@ def main():
                     help="synthetic Q/K/V: iid N(0,1) (worst case for selection locality) or per-view clusters")
     ap.add_argument("--layers", type=int, default=1,
                     help="L > 1: an L-layer stack (BASELINE configs[2]); each layer = fused QKV GEMM + GSA layer")
+    ap.add_argument("--backward", action="store_true",
+                    help="time the layer backward (gsa_backward + gsa_project_backward) instead of the forward")
+    ap.add_argument("--model-dim", type=int, default=1024, help="--backward: model_dim of X / W_q,k,v")
     ap.add_argument("--hybrid", type=int, default=0, metavar="REF_STRIDE",
                     help="hybrid selection with reference frames every REF_STRIDE views (0 = plain)")
     args = ap.parse_args()
@@ -306,6 +426,8 @@ def main():
         return run_reference_arm(args)
     if args.layers > 1:
         return run_stack(args)
+    if args.backward:
+        return run_backward(args)
 
     import torch
     import torch.distributed as dist

@@ -15,11 +15,15 @@ the launching stream after >= 1 warm-up per size; the workload of each size is
 seeded by seed' = hash(seed, frames). --precision f32|bf16 (f64 is
 rejected: there is no f64 path on the tensor cores). --threads and GSA_THREADS are
 accepted and ignored (the kernels are grids, results do not depend on them).
---backward is out of scope (the layer is inference-only).
+--backward ("backward benchmarked under a separate flag"): with --mode gsa,
+each row times gsa_backward (gradients.hpp:54-243, the top-k detached) on the saved
+context of one forward, rows labelled mode "gsa-backward"; other modes have no backward.
 
 --verify runs the self-contained identities of SPEC.md:545-549 on the GPU path:
 dense degeneration (s=1, k=W, no specials == dense attention), tiling invariance
-and scale invariance of the top-k indices, the closed-form work counters. The
+and scale invariance of the top-k indices, the closed-form work counters; the
+gradient suite: dO = 0 gives zero gradients, 2 dO exactly
+twice them, repeated backward calls agree bitwise, pool / upsample adjointness. The
 reference-equivalence suites (fused vs the unmodified reference) are the test
 suite's job (tests/test_spec_properties.py): this tool never links the oracle.
 """
@@ -90,7 +94,7 @@ def _time(torch, fn, repeats):
 
 
 def run_benchmark(mode, frames_list, grid, s, k, variant, ref_stride, heads, dim, precision, seed, repeats,
-                  specials_per_frame=0):
+                  specials_per_frame=0, backward=False):
     """One row per frame count; an out-of-memory size is a row with
     empty timing columns, not a crash."""
     import torch
@@ -106,12 +110,21 @@ def run_benchmark(mode, frames_list, grid, s, k, variant, ref_stride, heads, dim
         lt = (specials_per_frame * nf, nf, grid[0], grid[1], s)
         L = gsa.build_token_layout(*lt)
         p = gsa.GsaParams(window_s=s, top_k=k, variant=variant, ref_stride=ref_stride)
-        row = {"mode": mode, "frames": nf, "image_tokens": L.image_tokens, "window_s": s, "top_k": k,
+        row = {"mode": mode + ("-backward" if backward else ""), "frames": nf, "image_tokens": L.image_tokens, "window_s": s, "top_k": k,
                "variant": "hybrid" if variant else "plain", "repeats": repeats}
         try:
             q, kk, v, wg = _inputs(torch, lt, heads, dim, dtype, size_seed(seed, nf))
             scale = gsa.resolved_scale(p, dim)
-            if mode == "dense":
+            if backward:
+                if mode != "gsa":
+                    raise ValueError(f"--backward: mode {mode} has no backward (use --mode gsa)")
+                out, ctx = gsa.gsa_forward(q, kk, v, wg, L, p, context=True)
+                plan = gsa.build_selection_plan(ctx.topk, L, variant, ref_stride)
+                d_out = torch.randn(out.shape, generator=torch.Generator(device="cuda").manual_seed(seed),
+                                    device="cuda")
+                ws = gsa.Workspace()
+                fn = lambda: gsa.gsa_backward(q, kk, v, wg, L, p, ctx, out, d_out, plan=plan, workspace=ws)  # noqa: E731
+            elif mode == "dense":
                 fn = lambda: gsa.tiled_attention(q, kk, v, scale)  # noqa: E731
             elif mode == "gsa":
                 fn = lambda: gsa.gsa_forward(q, kk, v, wg, L, p)  # noqa: E731
@@ -178,6 +191,29 @@ def run_verification(suite, seed, heads=2, dim=64):
         W, M = L.num_windows, L.total_tokens
         ok = sc == heads * (lt[0] * M + W * W) and ka == heads * W * 12 * 16 * 16
         results.append(("work_counters_closed_form", ok, 0))
+    if suite in ("gradient", "all"):
+        lt = (3, 4, 16, 16, 4)
+        L = gsa.build_token_layout(*lt)
+        p = gsa.GsaParams(top_k=6)
+        q, k, v, wg = _inputs(torch, lt, heads, dim, torch.float32, size_seed(seed, 11))
+        out, ctx = gsa.gsa_forward(q, k, v, wg, L, p, context=True)
+        d_out = torch.randn(out.shape, generator=torch.Generator(device="cuda").manual_seed(seed), device="cuda")
+        g1 = gsa.gsa_backward(q, k, v, wg, L, p, ctx, out, d_out)
+        g1b = gsa.gsa_backward(q, k, v, wg, L, p, ctx, out, d_out)
+        g2 = gsa.gsa_backward(q, k, v, wg, L, p, ctx, out, 2 * d_out)
+        g0 = gsa.gsa_backward(q, k, v, wg, L, p, ctx, out, torch.zeros_like(d_out))
+        results.append(("gradient_zero_upstream", all(not torch.any(z) for z in g0), 0))
+        worst = max(float((2 * a - b).abs().max()) for a, b in zip(g1, g2))
+        results.append(("gradient_linearity", worst == 0.0, worst))
+        results.append(("gradient_determinism", all(torch.equal(a, b) for a, b in zip(g1, g1b)), 0))
+        x = torch.randn(heads, L.image_tokens, dim, device="cuda")
+        y = torch.randn(heads, L.num_windows, dim, device="cuda")
+        lhs = float((gsa.avg_pool_tokens(x, L).double() * y.double()).sum())
+        rhs = float((x.double() * gsa.avg_pool_backward(y, L).double()).sum())
+        lhs2 = float((gsa.upsample_nearest(y, L).double() * x.double()).sum())
+        rhs2 = float((y.double() * gsa.upsample_backward(x, L).double()).sum())
+        worst = max(abs(lhs - rhs), abs(lhs2 - rhs2))
+        results.append(("pool_upsample_adjointness", worst <= 1e-3, worst))
     return results
 
 
@@ -200,7 +236,7 @@ def main(argv=None):
     ap.add_argument("--repeats", type=int, default=5)
     ap.add_argument("--threads", type=int, default=int(os.environ.get("GSA_THREADS", "1")))
     ap.add_argument("--csv")
-    ap.add_argument("--verify", choices=["oracle", "topk", "all"])
+    ap.add_argument("--verify", choices=["oracle", "topk", "gradient", "all"])
     ap.add_argument("--backward", action="store_true")
     a = ap.parse_args(argv)
     if a.config:
@@ -216,8 +252,8 @@ def main(argv=None):
                 raise SystemExit(f"ConfigParseError: unknown key {key!r}")
             cur = getattr(a, attr)
             setattr(a, attr, type(cur)(val) if cur is not None and not isinstance(cur, bool) else val)
-    if a.backward:
-        raise SystemExit("--backward: the sm_100a layer is inference-only (DESIGN.md §8)")
+    if a.backward and a.mode != "gsa":
+        raise SystemExit(f"--backward: mode {a.mode} has no backward (only the gsa layer does)")
     if a.verify:
         ok_all = True
         for name, ok, worst in run_verification(a.verify, a.seed):
@@ -227,7 +263,8 @@ def main(argv=None):
     gh, gw = (int(x) for x in a.grid.split("x"))
     frames = [int(x) for x in a.frames.split(",") if x]
     rows = run_benchmark(a.mode, frames, (gh, gw), a.window, a.topk, 1 if a.variant == "hybrid" else 0,
-                         a.ref_stride, a.heads, a.dim, a.precision, a.seed, a.repeats, a.specials_per_frame)
+                         a.ref_stride, a.heads, a.dim, a.precision, a.seed, a.repeats, a.specials_per_frame,
+                         a.backward)
     out = open(a.csv, "w", newline="") if a.csv else sys.stdout
     w = csv.DictWriter(out, fieldnames=CSV_COLUMNS)
     w.writeheader()

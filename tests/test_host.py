@@ -39,13 +39,13 @@ def test_bench_cli_exponent_fit_and_seeds():
 
 
 def test_bench_cli_csv_schema_and_flags(tmp_path):
-    """The CSV header is SPEC's exact column order; f64 / --backward are
-    rejected loudly rather than silently downgraded."""
+    """The CSV header is SPEC's exact column order; f64 and --backward on a
+    mode without a backward are rejected loudly rather than silently downgraded."""
     from paper_2603_08055_b200 import cli
     assert cli.CSV_COLUMNS == ["mode", "frames", "image_tokens", "window_s", "top_k", "variant", "repeats",
                                "median_s", "mean_s", "stddev_s"]
     with pytest.raises(SystemExit):
-        cli.main(["--backward"])
+        cli.main(["--backward", "--mode", "dense"])
     cfg = tmp_path / "c.cfg"
     cfg.write_text("bogus_key = 3\n")
     with pytest.raises(SystemExit):
