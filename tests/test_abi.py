@@ -109,3 +109,42 @@ def test_forward_stats_closed_form():
     sc, ka = gsa.forward_stats(L, gsa.GsaParams(), 16)
     assert sc == 13_379_584
     assert ka == 84_934_656
+
+
+def test_backward_host_validation(lib):
+    """gsa_backward / gsa_project_backward / the pool adjoints reject bad calls on the host
+    (before any device work) with the reference's classes: ContextMismatch for an
+    incomplete saved context (errors.hpp:44), ShapeMismatch for a dO of the wrong shape
+    (gradients.hpp:66-67) and for adjoint inputs of the wrong row count (:23-24, :39-40)."""
+    import paper_2603_08055_b200 as gsa
+    from paper_2603_08055_b200._lib import GsaSavedC, GsaTensor
+    L = gsa.build_token_layout(2, 2, 8, 8, 4)
+    H, d, M, W, Mi = 2, 64, L.total_tokens, L.num_windows, L.image_tokens
+    fake = 256  # never dereferenced: validation fails first
+
+    def t(rows, dim=d, heads=H, dtype=0):
+        return GsaTensor(fake, dtype, heads, rows, dim, rows * dim, dim)
+
+    p = gsa.GsaParams(top_k=2).c()
+    lc = L.c()
+    wg = GsaTensor(fake, 0, H, d, d, d * d, d)
+    full = GsaSavedC(*([fake] * 5), fake, fake, H * W * 2, fake, fake, fake, t(2), fake)
+    empty = GsaSavedC()
+    q = t(M)
+
+    def bwd(saved, d_out):
+        return lib.gsa_backward(C.byref(q), C.byref(q), C.byref(q), C.byref(wg), C.byref(lc), C.byref(p),
+                                C.byref(saved), C.byref(d_out), C.byref(t(M)), C.byref(t(M)), C.byref(t(M)),
+                                C.c_void_p(fake), None, 0, None)
+
+    assert bwd(empty, t(M)) == 14                     # ContextMismatch: incomplete context
+    assert bwd(full, t(M - 1)) == 2                   # ShapeMismatch: dO rows
+    bad_spec = GsaSavedC(*([fake] * 5), fake, fake, H * W * 2, fake, fake, fake, t(1), fake)
+    assert bwd(bad_spec, t(M)) == 14                  # o_spec must be [H][Ms][d]
+    assert bwd(full, t(M)) == 12                      # WorkspaceError: no workspace given
+    assert lib.gsa_avg_pool_backward(C.byref(t(W + 1)), C.byref(lc), C.byref(t(Mi)), None) == 2
+    assert lib.gsa_upsample_backward(C.byref(t(Mi - 1)), C.byref(lc), C.byref(t(W)), None) == 2
+    assert lib.gsa_project_backward(None, M, 32, None, None, None, H, d, None, None, None, None, None, None, None,
+                                    None, 0, None) == 1  # null pointers: GsaError
+    assert lib.gsa_backward_workspace_bytes(C.byref(lc), C.byref(p), H, d, H * W * 2, 1) > \
+        lib.gsa_backward_workspace_bytes(C.byref(lc), C.byref(p), H, d, H * W * 2, 0)  # bf16 adds f32 copies
