@@ -1222,11 +1222,40 @@ struct BwdBufs {
     int splits;
     float* spec_dq_part;  // key-split partial dQ of the special rows
     int spec_splits;
+    // tensor-core dense passes: bf16 hi (+ lo for f32 operands) planes [H][rows][64] of the
+    // compressed branch (Qc, Kc, Vc, dO_comp: W rows) and the special rows (Q, dO: Ms rows;
+    // K, V: M rows)
+    bool tc;
+    __nv_bfloat16 *c_h[4], *c_l[4], *s_h[4], *s_l[4];
 };
+
+// the dense backward passes run on tcgen05 at head dim 64 (bwd_tc.cu), on CUDA cores otherwise
+bool bwd_use_tc(int d) { return tc_bwd_supported(d); }
+
+// f32 rows the tensor-core epilogue writes as float4
+bool aligned_rows(const gsa_tensor& t) {
+    return t.row_stride % 4 == 0 && t.head_stride % 4 == 0 && (reinterpret_cast<uintptr_t>(t.data) & 15) == 0;
+}
 
 size_t carve_bwd(const DevLayout& L, int Ms, int H, int d, int64_t E, bool convert, char* base, size_t cap,
                  bool dry, BwdBufs* b) {
     Carver c{base, cap, 0, dry};
+    b->tc = bwd_use_tc(d);
+    for (int i = 0; i < 4; ++i) b->c_h[i] = b->c_l[i] = b->s_h[i] = b->s_l[i] = nullptr;
+    if (b->tc) {
+        const int64_t Mt = Ms + (int64_t)L.image_tokens, Wt = L.windows;
+        for (int i = 0; i < 4; ++i) {
+            b->c_h[i] = c.take<__nv_bfloat16>((size_t)H * Wt * 64);
+            b->c_l[i] = c.take<__nv_bfloat16>((size_t)H * Wt * 64);
+        }
+        if (Ms > 0)
+            for (int i = 0; i < 4; ++i) {
+                const int64_t rows = (i == 1 || i == 2) ? Mt : Ms;  // Q, K, V, dO
+                b->s_h[i] = c.take<__nv_bfloat16>((size_t)H * rows * 64);
+                // bf16 Q / K / V are exact as one plane; dO (f32) always splits
+                if (convert == false || i == 3) b->s_l[i] = c.take<__nv_bfloat16>((size_t)H * rows * 64);
+            }
+    }
     const int64_t M = Ms + (int64_t)L.image_tokens, Mi = L.image_tokens, W = L.windows;
     b->q32 = b->k32 = b->v32 = nullptr;
     if (convert) {
@@ -1252,7 +1281,7 @@ size_t carve_bwd(const DevLayout& L, int Ms, int H, int d, int64_t E, bool conve
     b->tmp = c.take<char>(b->tmp_bytes);
     b->splits = atb_splits(H, d, d, Mi);
     b->part = c.take<float>((size_t)H * b->splits * d * d);
-    b->spec_splits = Ms > 0 ? dense_dq_splits(H, Ms, M) : 1;
+    b->spec_splits = Ms > 0 ? (b->tc ? tc_bwd_dq_splits(H, Ms, M) : dense_dq_splits(H, Ms, M)) : 1;
     b->spec_dq_part = b->spec_splits > 1 ? c.take<float>((size_t)b->spec_splits * H * Ms * d) : nullptr;
     return c.used;
 }
@@ -1356,7 +1385,38 @@ int gsa_backward(const gsa_tensor* q, const gsa_tensor* k, const gsa_tensor* v, 
     c.dk = FOut{b.dkc, whs, d};
     c.dv = FOut{b.dvc, whs, d};
     c.accumulate = false;
-    GSA_CUDA(launch_dense_bwd(c, H, st));
+    if (b.tc) {
+        // operand planes (bf16 hi + lo of the f32 pooled tensors and of dO_comp)
+        const float* src[4] = {sv->qc, sv->kc, sv->vc, b.d_oc};
+        for (int i = 0; i < 4; ++i)
+            GSA_CUDA(launch_pack_rows(TensorRef{src[i], GSA_DTYPE_F32, whs, d}, H, W, b.c_h[i], b.c_l[i], st));
+        BwdTcArgs t{};
+        t.heads = H;
+        t.n_q = t.n_k = W;
+        t.scale = lp.scale;
+        t.q_hi = b.c_h[0];
+        t.q_lo = b.c_l[0];
+        t.k_hi = b.c_h[1];
+        t.k_lo = b.c_l[1];
+        t.v_hi = b.c_h[2];
+        t.v_lo = b.c_l[2];
+        t.do_hi = b.c_h[3];
+        t.do_lo = b.c_l[3];
+        t.lse = sv->lse_comp;
+        t.D = b.d_comp;
+        t.dq = b.dqc;
+        t.dq_hs = whs;
+        t.dq_rs = d;
+        t.dk = b.dkc;
+        t.dk_hs = whs;
+        t.dk_rs = d;
+        t.dv = b.dvc;
+        t.dv_hs = whs;
+        t.dv_rs = d;
+        GSA_CUDA(launch_bwd_tc(t, st));
+    } else {
+        GSA_CUDA(launch_dense_bwd(c, H, st));
+    }
 
     // 3. pooling backward into the image rows (gradients.hpp:157-169)
     PoolBwdArgs pb{};
@@ -1412,17 +1472,55 @@ int gsa_backward(const gsa_tensor* q, const gsa_tensor* k, const gsa_tensor* v, 
         sp.nk = lp.M;
         sp.dim = d;
         sp.scale = lp.scale;
-        sp.dk = dK;  // key side first, accumulated into every row
-        sp.dv = dV;
-        sp.accumulate = true;
-        GSA_CUDA(launch_dense_bwd(sp, H, st));
-        sp.dk = FOut{nullptr, 0, 0};
-        sp.dv = FOut{nullptr, 0, 0};
-        sp.dq = dQ;  // the special rows' only dQ term: written
-        sp.accumulate = false;
-        sp.k_splits = b.spec_splits;
-        sp.dq_part = b.spec_dq_part;
-        GSA_CUDA(launch_dense_bwd(sp, H, st));
+        if (b.tc && aligned_rows(*dq) && aligned_rows(*dk) && aligned_rows(*dv)) {
+            // planes: Q / dO of the special rows, K / V of every row (lo only for f32)
+            const TensorRef refs[4] = {ref_of(*q), ref_of(*k), ref_of(*v),
+                                       TensorRef{d_out->data, GSA_DTYPE_F32, d_out->head_stride, d_out->row_stride}};
+            const int rows[4] = {Ms, lp.M, lp.M, Ms};
+            for (int i = 0; i < 4; ++i)
+                GSA_CUDA(launch_pack_rows(refs[i], H, rows[i], b.s_h[i], refs[i].dtype == GSA_DTYPE_F32 ? b.s_l[i] : nullptr,
+                                          st));
+            BwdTcArgs t{};
+            t.heads = H;
+            t.n_q = Ms;
+            t.n_k = lp.M;
+            t.scale = lp.scale;
+            t.q_hi = b.s_h[0];
+            t.q_lo = q->dtype == GSA_DTYPE_F32 ? b.s_l[0] : nullptr;
+            t.k_hi = b.s_h[1];
+            t.k_lo = k->dtype == GSA_DTYPE_F32 ? b.s_l[1] : nullptr;
+            t.v_hi = b.s_h[2];
+            t.v_lo = v->dtype == GSA_DTYPE_F32 ? b.s_l[2] : nullptr;
+            t.do_hi = b.s_h[3];
+            t.do_lo = b.s_l[3];
+            t.lse = sv->lse_spec;
+            t.D = b.d_spec;
+            t.dk = dK.p;  // key side: accumulated into every row
+            t.dk_hs = dK.hs;
+            t.dk_rs = dK.rs;
+            t.dv = dV.p;
+            t.dv_hs = dV.hs;
+            t.dv_rs = dV.rs;
+            t.accumulate_kv = true;
+            t.dq = dQ.p;  // the special rows' only dQ term: written
+            t.dq_hs = dQ.hs;
+            t.dq_rs = dQ.rs;
+            t.dq_part = b.spec_dq_part;
+            t.dq_splits = b.spec_splits;
+            GSA_CUDA(launch_bwd_tc(t, st));
+        } else {
+            sp.dk = dK;  // key side first, accumulated into every row
+            sp.dv = dV;
+            sp.accumulate = true;
+            GSA_CUDA(launch_dense_bwd(sp, H, st));
+            sp.dk = FOut{nullptr, 0, 0};
+            sp.dv = FOut{nullptr, 0, 0};
+            sp.dq = dQ;  // the special rows' only dQ term: written
+            sp.accumulate = false;
+            sp.k_splits = b.tc ? 1 : b.spec_splits;  // (tc: the partial buffer is sized for its own splits)
+            sp.dq_part = b.spec_dq_part;
+            GSA_CUDA(launch_dense_bwd(sp, H, st));
+        }
     }
 
     // 6. dW_g = Q_img^T dz per head (gradients.hpp:112-113)

@@ -1,0 +1,406 @@
+// bwd_tc.cu — the dense passes of the layer backward (gradients.hpp:130-155 compressed
+// branch, :197-222 special rows) on tcgen05 tensor cores, head dim 64.
+//
+// One kernel, two roles (FlashAttention-2 split, probabilities rebuilt from the saved
+// LSE rows). A CTA owns 128 FIXED rows (TMEM lanes) and streams the other side in tiles
+// of 128:
+//   key side   (KEYSIDE): fixed = keys, stream = queries
+//       S^T = K Q^T, dP^T = V dO^T  -> P^T = exp(scale S^T - lse[q]), dS^T = P^T (dP^T - D[q]) scale
+//       dV += P^T dO, dK += dS^T Q
+//   query side: fixed = queries, stream = keys (optionally split over key ranges)
+//       S = Q K^T, dP = dO V^T      -> P = exp(scale S - lse[q]), dS = P (dP - D[q]) scale
+//       dQ += dS K
+// Precision: every f32 operand enters as bf16 hi + lo planes (|x - hi - lo| <= 2^-16 |x|)
+// and products take the hi.hi + hi.lo + lo.hi terms, terms with an all-zero lo plane
+// (bf16 inputs) skipped; P and dS are written back into TMEM as bf16 hi + lo pairs over
+// the S / dP columns they replace and feed the output MMAs as A-from-TMEM operands. The
+// result is f32-accurate (the CUDA-core kernels' tolerance), deterministic (each output
+// row has one CTA) and accumulated in TMEM.
+//
+// Warp roles (192 threads): warps 0-3 one thread per fixed row (TMEM lane): the
+// exponentials, the hi/lo splits, the epilogue; warp 4 TMA (fixed tiles once, streamed
+// tiles through a 2-stage ring); warp 5 MMA issue (one elected lane).
+// TMEM columns: S 0-127, dP 128-255, out1 256-319, out2 320-383 (512 allocated).
+#define GSA_WATCHDOG 1  // bring-up: a pipeline bug traps after ~10 s instead of hanging
+#include <cuda.h>
+
+#include "tc.h"
+#include "tc_ptx.cuh"
+#include "tma_util.cuh"
+
+namespace gsa_sm100 {
+namespace {
+
+using namespace ptx;
+
+constexpr int BT_THREADS = 192;
+constexpr int TILE = 16384;  // 128 rows x 64 bf16, 128B-swizzled
+constexpr int NSTAGE = 2;
+constexpr uint32_t T_S = 0, T_DP = 128, T_O1 = 256, T_O2 = 320, T_COLS = 512;
+
+struct __align__(1024) BwdSmem {
+    uint8_t fixed[4][TILE];           // A1 hi, A1 lo, A2 hi, A2 lo
+    uint8_t ring[NSTAGE][4][TILE];    // B1 hi, B1 lo, B2 hi, B2 lo
+    float st_lse[2][128], st_D[2][128];
+    uint64_t fixed_full, full[NSTAGE], empty[NSTAGE], s_full, p_full, done;
+    uint32_t tmem_base;
+};
+
+struct BwdTcParams {
+    int64_t n_fixed, n_stream;  // rows of the fixed / streamed side
+    int64_t s_chunk;            // streamed rows per split (multiple of 128)
+    int heads;
+    float scale, c2;            // c2 = scale * log2(e)
+    bool a1_lo, a2_lo, b1_lo, b2_lo;
+    const float *lse, *D;       // by query: [H][n_q]
+    // outputs: KEYSIDE out1 = dV, out2 = dK; query side out1 = dQ (or the split's partial)
+    float *o1, *o2;
+    int64_t o1_hs, o1_rs, o2_hs, o2_rs;
+    float* part;                // query side, splits > 1: [split][H][n_fixed][64]
+    int splits;
+    bool accumulate;
+};
+
+template <bool KEYSIDE>
+__global__ void __launch_bounds__(BT_THREADS, 1)
+    bwd_tc_kernel(const __grid_constant__ CUtensorMap tm_a1h, const __grid_constant__ CUtensorMap tm_a1l,
+                  const __grid_constant__ CUtensorMap tm_a2h, const __grid_constant__ CUtensorMap tm_a2l,
+                  const __grid_constant__ CUtensorMap tm_b1h, const __grid_constant__ CUtensorMap tm_b1l,
+                  const __grid_constant__ CUtensorMap tm_b2h, const __grid_constant__ CUtensorMap tm_b2l,
+                  const BwdTcParams p) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    BwdSmem& sm = *reinterpret_cast<BwdSmem*>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
+    const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
+    const int fixed_tile = blockIdx.x, split = blockIdx.y, h = blockIdx.z;
+    const int64_t s_begin = (int64_t)split * p.s_chunk;
+    const int64_t s_end = min(p.n_stream, s_begin + p.s_chunk);
+    const int T = (int)((s_end - s_begin + 127) / 128);
+
+    if (threadIdx.x == 0) {
+        mbar_init(&sm.fixed_full, 1);
+        for (int i = 0; i < NSTAGE; ++i) {
+            mbar_init(&sm.full[i], 1);
+            mbar_init(&sm.empty[i], 1);
+        }
+        mbar_init(&sm.s_full, 1);
+        mbar_init(&sm.p_full, 128);
+        mbar_init(&sm.done, 1);
+        fence_barrier_init();
+    }
+    if (warp == 5) tmem_alloc(&sm.tmem_base, T_COLS);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = sm.tmem_base;
+
+    if (warp == 4) {
+        // ================================ TMA ================================
+        if (T > 0 && elect_one()) {
+            const uint32_t fb = TILE * (2 + (p.a1_lo ? 1 : 0) + (p.a2_lo ? 1 : 0));
+            mbar_arrive_expect_tx(&sm.fixed_full, fb);
+            const int r0 = fixed_tile * 128;
+            tma_load_3d(&sm.fixed[0][0], &tm_a1h, &sm.fixed_full, 0, r0, h);
+            if (p.a1_lo) tma_load_3d(&sm.fixed[1][0], &tm_a1l, &sm.fixed_full, 0, r0, h);
+            tma_load_3d(&sm.fixed[2][0], &tm_a2h, &sm.fixed_full, 0, r0, h);
+            if (p.a2_lo) tma_load_3d(&sm.fixed[3][0], &tm_a2l, &sm.fixed_full, 0, r0, h);
+            const uint32_t sb = TILE * (2 + (p.b1_lo ? 1 : 0) + (p.b2_lo ? 1 : 0));
+            for (int j = 0; j < T; ++j) {
+                const int st = j % NSTAGE;
+                mbar_wait(&sm.empty[st], (uint32_t)(((j / NSTAGE) & 1) ^ 1));
+                mbar_arrive_expect_tx(&sm.full[st], sb);
+                const int c1 = (int)(s_begin + (int64_t)j * 128);
+                tma_load_3d(&sm.ring[st][0][0], &tm_b1h, &sm.full[st], 0, c1, h);
+                if (p.b1_lo) tma_load_3d(&sm.ring[st][1][0], &tm_b1l, &sm.full[st], 0, c1, h);
+                tma_load_3d(&sm.ring[st][2][0], &tm_b2h, &sm.full[st], 0, c1, h);
+                if (p.b2_lo) tma_load_3d(&sm.ring[st][3][0], &tm_b2l, &sm.full[st], 0, c1, h);
+            }
+        }
+        __syncwarp();
+    } else if (warp == 5) {
+        // ================================ MMA ================================
+        const uint32_t id_s = idesc_bf16(128, 128, 0, 0);
+        const uint32_t id_o = idesc_bf16(128, 64, 0, 1);  // A (P / dS) from TMEM, B MN-major
+        auto kdesc = [](const uint8_t* t) { return umma_desc(smem_u32(t), 16, 1024, 2); };
+        if (T > 0) {
+            mbar_wait(&sm.fixed_full, 0);
+            tc_fence_after();
+        }
+        const uint64_t a1h = kdesc(sm.fixed[0]), a1l = kdesc(sm.fixed[1]);
+        const uint64_t a2h = kdesc(sm.fixed[2]), a2l = kdesc(sm.fixed[3]);
+        for (int j = 0; j < T; ++j) {
+            const int st = j % NSTAGE;
+            mbar_wait(&sm.full[st], (uint32_t)((j / NSTAGE) & 1));
+            tc_fence_after();
+            const uint64_t b1h = kdesc(sm.ring[st][0]), b1l = kdesc(sm.ring[st][1]);
+            const uint64_t b2h = kdesc(sm.ring[st][2]), b2l = kdesc(sm.ring[st][3]);
+            if (elect_one()) {
+                // S = A1 B1^T and dP = A2 B2^T over d = 64 (4 k-steps of 16)
+                for (int ks = 0; ks < 4; ++ks) {
+                    const uint32_t acc = ks != 0;
+                    mma_bf16(tmem + T_S, a1h + 2 * ks, b1h + 2 * ks, id_s, acc);
+                    if (p.b1_lo) mma_bf16(tmem + T_S, a1h + 2 * ks, b1l + 2 * ks, id_s, 1);
+                    if (p.a1_lo) mma_bf16(tmem + T_S, a1l + 2 * ks, b1h + 2 * ks, id_s, 1);
+                    mma_bf16(tmem + T_DP, a2h + 2 * ks, b2h + 2 * ks, id_s, acc);
+                    if (p.b2_lo) mma_bf16(tmem + T_DP, a2h + 2 * ks, b2l + 2 * ks, id_s, 1);
+                    if (p.a2_lo) mma_bf16(tmem + T_DP, a2l + 2 * ks, b2h + 2 * ks, id_s, 1);
+                }
+                mma_commit(&sm.s_full);
+            }
+            __syncwarp();
+            mbar_wait(&sm.p_full, (uint32_t)(j & 1));
+            tc_fence_after();
+            if (elect_one()) {
+                // outputs over the 128 streamed rows (8 k-steps of 16): the A chunk of k-step ks
+                // holds hi pairs at columns 32 (ks/2) + 8 (ks%2), lo pairs 16 columns further
+                for (int ks = 0; ks < 8; ++ks) {
+                    const uint32_t col = 32 * (ks >> 1) + 8 * (ks & 1);
+                    const uint32_t acc0 = (j | ks) != 0;
+                    if (KEYSIDE) {
+                        // dV += P^T dO (B2), dK += dS^T Q (B1)
+                        const uint64_t vh = b2h + 128 * ks, vl = b2l + 128 * ks;
+                        mma_bf16_ts(tmem + T_O1, tmem + T_S + col, vh, id_o, acc0);
+                        if (p.b2_lo) mma_bf16_ts(tmem + T_O1, tmem + T_S + col, vl, id_o, 1);
+                        mma_bf16_ts(tmem + T_O1, tmem + T_S + col + 16, vh, id_o, 1);
+                        const uint64_t qh = b1h + 128 * ks, ql = b1l + 128 * ks;
+                        mma_bf16_ts(tmem + T_O2, tmem + T_DP + col, qh, id_o, acc0);
+                        if (p.b1_lo) mma_bf16_ts(tmem + T_O2, tmem + T_DP + col, ql, id_o, 1);
+                        mma_bf16_ts(tmem + T_O2, tmem + T_DP + col + 16, qh, id_o, 1);
+                    } else {
+                        // dQ += dS K (B1)
+                        const uint64_t kh = b1h + 128 * ks, kl = b1l + 128 * ks;
+                        mma_bf16_ts(tmem + T_O1, tmem + T_DP + col, kh, id_o, acc0);
+                        if (p.b1_lo) mma_bf16_ts(tmem + T_O1, tmem + T_DP + col, kl, id_o, 1);
+                        mma_bf16_ts(tmem + T_O1, tmem + T_DP + col + 16, kh, id_o, 1);
+                    }
+                }
+                mma_commit(&sm.empty[st]);
+                if (j == T - 1) mma_commit(&sm.done);
+            }
+            __syncwarp();
+        }
+    } else {
+        // ===================== rows: exponentials, splits, epilogue =====================
+        const int row = 32 * warp + lane;
+        const uint32_t lane_base = tmem + ((uint32_t)(32 * warp) << 16);
+        const int64_t grow = (int64_t)fixed_tile * 128 + row;
+        float lse_r = 0.0f, D_r = 0.0f;
+        if (!KEYSIDE) {
+            const bool ok = grow < p.n_fixed;
+            lse_r = ok ? p.lse[(int64_t)h * p.n_fixed + grow] : 0.0f;
+            D_r = ok ? p.D[(int64_t)h * p.n_fixed + grow] : 0.0f;
+        }
+        for (int j = 0; j < T; ++j) {
+            const int sb = j & 1;
+            if (KEYSIDE) {
+                // the 128 streamed queries' lse / D, shared by every key row
+                const int64_t q = s_begin + (int64_t)j * 128 + row;
+                const bool ok = q < s_end;
+                sm.st_lse[sb][row] = ok ? p.lse[(int64_t)h * p.n_stream + q] * 1.4426950408889634f : INFINITY;
+                sm.st_D[sb][row] = ok ? p.D[(int64_t)h * p.n_stream + q] : 0.0f;
+                named_bar_sync(1, 128);
+            }
+            mbar_wait(&sm.s_full, (uint32_t)(j & 1));
+            __syncwarp();
+            tc_fence_after();
+#pragma unroll 1
+            for (int c = 0; c < 4; ++c) {
+                uint32_t sv[32], dv[32];
+                tmem_ld_32x32b_x32(lane_base + T_S + 32 * c, sv);
+                tmem_ld_32x32b_x32(lane_base + T_DP + 32 * c, dv);
+                tmem_wait_ld();
+                uint32_t ph[16], pl[16], dh[16], dl[16];
+#pragma unroll
+                for (int e2 = 0; e2 < 16; ++e2) {
+                    float pv[2], dsv[2];
+#pragma unroll
+                    for (int u = 0; u < 2; ++u) {
+                        const int e = 2 * e2 + u;
+                        const float l2 = KEYSIDE ? sm.st_lse[sb][32 * c + e] : lse_r * 1.4426950408889634f;
+                        const float Dv = KEYSIDE ? sm.st_D[sb][32 * c + e] : D_r;
+                        const float pr = ex2_approx(fmaf(__uint_as_float(sv[e]), p.c2, -l2));
+                        pv[u] = pr;
+                        dsv[u] = pr * (__uint_as_float(dv[e]) - Dv) * p.scale;
+                    }
+                    const __nv_bfloat162 phb = __floats2bfloat162_rn(pv[0], pv[1]);
+                    const __nv_bfloat162 dhb = __floats2bfloat162_rn(dsv[0], dsv[1]);
+                    const float2 phf = __bfloat1622float2(phb), dhf = __bfloat1622float2(dhb);
+                    ph[e2] = *reinterpret_cast<const uint32_t*>(&phb);
+                    dh[e2] = *reinterpret_cast<const uint32_t*>(&dhb);
+                    pl[e2] = pack_bf16(pv[0] - phf.x, pv[1] - phf.y);
+                    dl[e2] = pack_bf16(dsv[0] - dhf.x, dsv[1] - dhf.y);
+                }
+                if (KEYSIDE) {
+                    tmem_st_32x32b_x16(lane_base + T_S + 32 * c, ph);
+                    tmem_st_32x32b_x16(lane_base + T_S + 32 * c + 16, pl);
+                }
+                tmem_st_32x32b_x16(lane_base + T_DP + 32 * c, dh);
+                tmem_st_32x32b_x16(lane_base + T_DP + 32 * c + 16, dl);
+            }
+            tmem_wait_st();
+            tc_fence_before();
+            mbar_arrive(&sm.p_full);
+        }
+        // ------------------------------- epilogue -------------------------------
+        if (T > 0) {
+            mbar_wait(&sm.done, 0);
+            __syncwarp();
+            tc_fence_after();
+            for (int o = 0; o < (KEYSIDE ? 2 : 1); ++o) {
+                uint32_t v[2][32];
+                const uint32_t col = o == 0 ? T_O1 : T_O2;
+                tmem_ld_32x32b_x32(lane_base + col, v[0]);
+                tmem_ld_32x32b_x32(lane_base + col + 32, v[1]);
+                tmem_wait_ld();
+                if (grow < p.n_fixed) {
+                    float* dst;
+                    bool acc = p.accumulate;
+                    if (!KEYSIDE && p.splits > 1) {
+                        dst = p.part + (((int64_t)split * p.heads + h) * p.n_fixed + grow) * 64;
+                        acc = false;
+                    } else if (o == 0) {
+                        dst = p.o1 + (int64_t)h * p.o1_hs + grow * p.o1_rs;
+                    } else {
+                        dst = p.o2 + (int64_t)h * p.o2_hs + grow * p.o2_rs;
+                    }
+#pragma unroll
+                    for (int half = 0; half < 2; ++half)
+#pragma unroll
+                        for (int e = 0; e < 32; e += 4) {
+                            float4 x = make_float4(__uint_as_float(v[half][e]), __uint_as_float(v[half][e + 1]),
+                                                   __uint_as_float(v[half][e + 2]), __uint_as_float(v[half][e + 3]));
+                            float4* d4 = reinterpret_cast<float4*>(dst + 32 * half + e);
+                            if (acc) {
+                                const float4 y = *d4;
+                                x.x += y.x;
+                                x.y += y.y;
+                                x.z += y.z;
+                                x.w += y.w;
+                            }
+                            *d4 = x;
+                        }
+                }
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 5) {
+        tc_fence_after();
+        tmem_dealloc(tmem, T_COLS);
+    }
+}
+
+// dQ from the key-split partials, summed in split order
+__global__ void bwd_tc_reduce_kernel(const float* part, int splits, int heads, int64_t rows, float* out, int64_t hs,
+                                     int64_t rs, bool accumulate) {
+    const int64_t n = (int64_t)heads * rows * 64;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+        const int j = (int)(e & 63);
+        const int64_t r = (e >> 6) % rows, h = (e >> 6) / rows;
+        float acc = 0.0f;
+        for (int s = 0; s < splits; ++s) acc += part[(int64_t)s * n + e];
+        float* o = out + h * hs + r * rs + j;
+        *o = accumulate ? *o + acc : acc;
+    }
+}
+
+bool make_plane_map(CUtensorMap* m, const __nv_bfloat16* plane, int heads, int64_t rows) {
+    // contiguous [H][rows][64] bf16; an absent plane maps the hi plane (never loaded)
+    return make_rows_tmap(m, plane, heads, (int)rows, rows * 64, 64);
+}
+
+}  // namespace
+
+bool tc_bwd_supported(int dim) { return dim == 64 && tmap_encode_fn() != nullptr; }
+
+int tc_bwd_dq_splits(int heads, int64_t n_q, int64_t n_k) {
+    const int64_t ctas = (int64_t)heads * ((n_q + 127) / 128);
+    int64_t s = (2 * 148 + ctas - 1) / ctas;
+    const int64_t cap = ((n_k + 127) / 128) / 8;  // >= 8 key tiles per split
+    if (s > cap) s = cap;
+    return (int)(s < 1 ? 1 : s > 64 ? 64 : s);
+}
+
+cudaError_t launch_bwd_tc(const BwdTcArgs& a, cudaStream_t st) {
+    if (a.heads == 0 || a.n_q == 0 || a.n_k == 0) return cudaSuccess;
+    CUtensorMap m[8];
+    const bool ok = make_plane_map(&m[0], a.q_hi, a.heads, a.n_q) &&
+                    make_plane_map(&m[1], a.q_lo ? a.q_lo : a.q_hi, a.heads, a.n_q) &&
+                    make_plane_map(&m[2], a.do_hi, a.heads, a.n_q) &&
+                    make_plane_map(&m[3], a.do_lo ? a.do_lo : a.do_hi, a.heads, a.n_q) &&
+                    make_plane_map(&m[4], a.k_hi, a.heads, a.n_k) &&
+                    make_plane_map(&m[5], a.k_lo ? a.k_lo : a.k_hi, a.heads, a.n_k) &&
+                    make_plane_map(&m[6], a.v_hi, a.heads, a.n_k) &&
+                    make_plane_map(&m[7], a.v_lo ? a.v_lo : a.v_hi, a.heads, a.n_k);
+    if (!ok) return cudaErrorNotSupported;
+    const size_t smem = sizeof(BwdSmem) + 1024;
+    cudaError_t e = cudaFuncSetAttribute(bwd_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(bwd_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    const float LOG2E = 1.4426950408889634f;
+    if (a.dk) {
+        // key side: fixed = K (A1) / V (A2), stream = Q (B1) / dO (B2)
+        BwdTcParams p{};
+        p.n_fixed = a.n_k;
+        p.n_stream = a.n_q;
+        p.s_chunk = (a.n_q + 127) / 128 * 128;
+        p.heads = a.heads;
+        p.scale = a.scale;
+        p.c2 = a.scale * LOG2E;
+        p.a1_lo = a.k_lo != nullptr;
+        p.a2_lo = a.v_lo != nullptr;
+        p.b1_lo = a.q_lo != nullptr;
+        p.b2_lo = a.do_lo != nullptr;
+        p.lse = a.lse;
+        p.D = a.D;
+        p.o1 = a.dv;
+        p.o1_hs = a.dv_hs;
+        p.o1_rs = a.dv_rs;
+        p.o2 = a.dk;
+        p.o2_hs = a.dk_hs;
+        p.o2_rs = a.dk_rs;
+        p.splits = 1;
+        p.accumulate = a.accumulate_kv;
+        bwd_tc_kernel<true><<<dim3((unsigned)((a.n_k + 127) / 128), 1, a.heads), BT_THREADS, smem, st>>>(
+            m[4], m[5], m[6], m[7], m[0], m[1], m[2], m[3], p);
+        note_launch();
+    }
+    if (a.dq) {
+        // query side: fixed = Q (A1) / dO (A2), stream = K (B1) / V (B2)
+        BwdTcParams p{};
+        p.n_fixed = a.n_q;
+        p.n_stream = a.n_k;
+        const int splits = a.dq_part ? a.dq_splits : 1;
+        const int64_t ktiles = (a.n_k + 127) / 128;
+        p.s_chunk = (ktiles + splits - 1) / splits * 128;
+        p.splits = (int)((a.n_k + p.s_chunk - 1) / p.s_chunk);
+        p.heads = a.heads;
+        p.scale = a.scale;
+        p.c2 = a.scale * LOG2E;
+        p.a1_lo = a.q_lo != nullptr;
+        p.a2_lo = a.do_lo != nullptr;
+        p.b1_lo = a.k_lo != nullptr;
+        p.b2_lo = a.v_lo != nullptr;
+        p.lse = a.lse;
+        p.D = a.D;
+        p.o1 = a.dq;
+        p.o1_hs = a.dq_hs;
+        p.o1_rs = a.dq_rs;
+        p.part = a.dq_part;
+        p.accumulate = a.accumulate_q;
+        bwd_tc_kernel<false><<<dim3((unsigned)((a.n_q + 127) / 128), p.splits, a.heads), BT_THREADS, smem, st>>>(
+            m[0], m[1], m[2], m[3], m[4], m[5], m[6], m[7], p);
+        note_launch();
+        if (p.splits > 1) {
+            const int64_t n = (int64_t)a.heads * a.n_q * 64;
+            const unsigned blocks = (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 16);
+            bwd_tc_reduce_kernel<<<blocks, 256, 0, st>>>(a.dq_part, p.splits, a.heads, a.n_q, a.dq, a.dq_hs, a.dq_rs,
+                                                          a.accumulate_q);
+            note_launch();
+        }
+    }
+    return cudaGetLastError();
+}
+
+}  // namespace gsa_sm100

@@ -66,4 +66,27 @@ cudaError_t tc_gemm_bf16(const __nv_bfloat16* a, int64_t lda, const __nv_bfloat1
                          int64_t ldc, int M, int N, int K, cudaStream_t st);
 cudaError_t launch_residual_bf16(const __nv_bfloat16* x, const float* o, __nv_bfloat16* y, int64_t n, cudaStream_t st);
 
+// dense passes of the layer backward (bwd_tc.cu), head dim 64: operands as contiguous bf16
+// planes [H][rows][64] (hi, plus lo for f32 operands; lo == nullptr: the operand is exactly
+// bf16); dK/dV (key side) and/or dQ (query side, optionally split over keys into dq_part
+// [splits][H][n_q][64] and reduced in order) as f32 rows with 16-byte aligned strides
+struct BwdTcArgs {
+    int heads;
+    int64_t n_q, n_k;
+    float scale;
+    const __nv_bfloat16 *q_hi, *q_lo, *k_hi, *k_lo, *v_hi, *v_lo, *do_hi, *do_lo;
+    const float *lse, *D;  // [H][n_q]
+    float* dq;
+    int64_t dq_hs, dq_rs;
+    bool accumulate_q;
+    float* dq_part;
+    int dq_splits;
+    float *dk, *dv;
+    int64_t dk_hs, dk_rs, dv_hs, dv_rs;
+    bool accumulate_kv;
+};
+bool tc_bwd_supported(int dim);
+int tc_bwd_dq_splits(int heads, int64_t n_q, int64_t n_k);
+cudaError_t launch_bwd_tc(const BwdTcArgs& a, cudaStream_t st);
+
 }  // namespace gsa_sm100
