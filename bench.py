@@ -195,8 +195,9 @@ def run_backward(args):
     One step = gsa_backward (gradients.hpp:54-243: gate fuse, upsample / pooling adjoints,
     compressed, selection and special attention backward from the saved LSE rows, dW_g)
     + gsa_project_backward (gradients.hpp:226-263: dW_q/k/v = X^T dY, dX) at model_dim
-    --model-dim, from one forward's saved context, everything resident in HBM. f32 on CUDA
-    cores: the roofline is the nominal FP32 FMA peak. cpu_baseline: the reference's own
+    --model-dim, from one forward's saved context, everything resident in HBM. Stage times
+    from the library's events; the roofline is the longest stage's (tcgen05 dense passes vs
+    the bf16 peak, selection passes vs the FP32 FMA peak). cpu_baseline: the reference's own
     gsa_forward + gsa_backward (oracle/_ref) on a 4-view sample with all host threads,
     next to this GPU path on the same sample."""
     import ctypes
@@ -230,10 +231,14 @@ def run_backward(args):
     Lv, q, k, v, wg, out, ctx, plan, d_out, x, w = instance(V, C)
     ws = gsa.Workspace()
 
-    def step(evs=None):
+    def step(evs=None, stage=None):
         if evs:
             evs[0].record()
+        if stage is not None:
+            lib.gsa_set_stage_events(stage, 7)
         dq, dk, dv, dwg = gsa.gsa_backward(q, k, v, wg, Lv, params, ctx, out, d_out, plan=plan, workspace=ws)
+        if stage is not None:
+            lib.gsa_set_stage_events(None, 0)
         if evs:
             evs[1].record()
         gsa.project_backward(x, *w, dq, dk, dv)
@@ -246,10 +251,15 @@ def run_backward(args):
     n0 = ctypes.c_uint64()
     lib.gsa_launch_count(ctypes.byref(n0))
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    sev = [[torch.cuda.Event(enable_timing=True) for _ in range(7)] for _ in range(args.steps)]
+    for row in sev:
+        for e_ in row:
+            e_.record()  # materialise the cudaEvent_t handles
+    handles = [(ctypes.c_void_p * 7)(*[e_.cuda_event for e_ in row]) for row in sev]
     with ClockSampler(0) as clk:
         torch.cuda.synchronize()
         for i in range(args.steps):
-            step(evs[i])
+            step(evs[i], handles[i])
         torch.cuda.synchronize()
     n1 = ctypes.c_uint64()
     lib.gsa_launch_count(ctypes.byref(n1))
@@ -262,6 +272,19 @@ def run_backward(args):
     attn_flops = 5 * 2 * DIM * (HEADS * G["W"] ** 2 + HEADS * G["Ms"] * G["M"] + E * S ** 4)
     proj_flops = 2 * 2 * 3 * G["M"] * C * HEADS * DIM
     fp32_peak = 148 * 128 * 2 * 1.965e9 / 1e12
+    names = ("gate", "compressed", "selection", "special", "dw_g")
+    stage_ms = {n: statistics.median(sev[i][j].elapsed_time(sev[i][j + 1]) for i in range(args.steps))
+                for j, n in enumerate(names)}
+    _, tc_peak, _, peak_kind = load_peaks()
+    # useful work per stage (FlashAttention-2 accounting, one MMA term: issued tensor work is
+    # up to 3x this with the bf16 hi/lo operand splits)
+    work = {"compressed": (5 * 2 * DIM * HEADS * G["W"] ** 2, "tensor", tc_peak),
+            "special": (5 * 2 * DIM * HEADS * G["Ms"] * G["M"], "tensor", tc_peak),
+            "selection": (5 * 2 * DIM * E * S ** 4, "fp32", fp32_peak)}
+    stage_roofline = {n: {"ms": round(stage_ms[n], 3), "tflops": round(f / stage_ms[n] / 1e9, 1), "bound": b,
+                          "frac": round(f / stage_ms[n] / 1e9 / pk, 4)} for n, (f, b, pk) in work.items()}
+    dom = max(work, key=lambda n: stage_ms[n])
+    f_dom, b_dom, pk_dom = work[dom]
     line = {"metric": f"GSA layer backward (dX, dW_q/k/v/g) at {V} views", "value": G["M"] / (total_ms / 1e3),
             "unit": "tokens/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
@@ -270,11 +293,16 @@ def run_backward(args):
                                    f"patches) = {G['M']} tokens, 16 heads x 64, s=4, top-{TOPK}, plain, model_dim {C}",
                        "views": V, "tokens": G["M"], "windows": G["W"], "plan_entries": E, "model_dim": C,
                        "parallelism": "1 GPU", "l2": "inputs larger than L2 (no flush)"},
-            "stage_ms": {"attention_backward": round(attn_ms, 3), "projection_backward": round(proj_ms, 3)},
-            "roofline": {"kernel": "attention backward (dense + selection passes, CUDA cores)", "bound": "fp32",
-                         "achieved": attn_flops / attn_ms / 1e9, "peak": fp32_peak, "unit": "TFLOP/s",
-                         "frac": attn_flops / attn_ms / 1e9 / fp32_peak, "traffic": None,
-                         "peak_kind": "nominal (148 SMs x 128 FP32 lanes x 2 x 1.965 GHz)"},
+            "stage_ms": {"attention_backward": round(attn_ms, 3), "projection_backward": round(proj_ms, 3),
+                         **{n: round(v_, 3) for n, v_ in stage_ms.items()}},
+            "stage_roofline": stage_roofline,
+            "attention_backward_tflops": round(attn_flops / attn_ms / 1e9, 1),
+            "roofline": {"kernel": {"compressed": "bwd_tc_kernel (compressed branch)", "special":
+                                    "bwd_tc_kernel (special rows)", "selection": "sel16_bwd_kernel"}[dom],
+                         "bound": b_dom, "achieved": f_dom / stage_ms[dom] / 1e9, "peak": pk_dom, "unit": "TFLOP/s",
+                         "frac": f_dom / stage_ms[dom] / 1e9 / pk_dom, "traffic": None,
+                         "peak_kind": (f"{peak_kind} bf16 dense" if b_dom == "tensor" else
+                                       "nominal FP32 (148 SMs x 128 lanes x 2 x 1.965 GHz)")},
             "projection_tflops": round(proj_flops / proj_ms / 1e9, 2),
             "gpu_launches": int(n1.value - n0.value), "clocks": clk.summary()}
     if not args.no_cpu_baseline:

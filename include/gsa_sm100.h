@@ -368,7 +368,9 @@ int gsa_upsample_backward(const gsa_tensor* d_fine, const gsa_layout* layout, co
  * after pooling, after the Kc/Vc gather, after the compressed branch, done). With
  * n >= 7, events[5] and events[6] also bracket the compressed-attention kernel launch
  * itself (compress_tc_kernel), so its duration is measured on its own stream. n = 0
- * disables.
+ * disables. gsa_backward records events[0..5]: start (after validation), after the gate
+ * fuse, after the compressed-branch dense passes, after pooling + selection backward,
+ * after the special rows, done (dW_g).
  * gsa_launch_count: kernels this library has launched since it was loaded. */
 int gsa_set_stage_events(void* const* events, int n);
 int gsa_launch_count(uint64_t* count);

@@ -1337,6 +1337,7 @@ int gsa_backward(const gsa_tensor* q, const gsa_tensor* k, const gsa_tensor* v, 
         return fail(GSA_ERR_CONTEXT_MISMATCH, "gsa_backward: plan holds %lld entries, saved.plan_entries = %lld",
                     (long long)total, (long long)sv->plan_entries);
 
+    stage_mark(0, st);
     FMat Q = fmat_of(*q), K = fmat_of(*k), V = fmat_of(*v);
     if (convert) {
         const int64_t hs = (int64_t)lp.M * d;
@@ -1367,6 +1368,7 @@ int gsa_backward(const gsa_tensor* q, const gsa_tensor* k, const gsa_tensor* v, 
     g.d_comp = b.d_comp;
     g.dq = dQ;
     GSA_CUDA(launch_gate_bwd(g, H, st));
+    stage_mark(1, st);
 
     // 2. compressed attention backward over the windows (gradients.hpp:130-155)
     DenseBwdArgs c{};
@@ -1418,6 +1420,7 @@ int gsa_backward(const gsa_tensor* q, const gsa_tensor* k, const gsa_tensor* v, 
         GSA_CUDA(launch_dense_bwd(c, H, st));
     }
 
+    stage_mark(2, st);
     // 3. pooling backward into the image rows (gradients.hpp:157-169)
     PoolBwdArgs pb{};
     pb.heads = H;
@@ -1454,6 +1457,7 @@ int gsa_backward(const gsa_tensor* q, const gsa_tensor* k, const gsa_tensor* v, 
     sa.dk = dK;
     sa.dv = dV;
     GSA_CUDA(launch_sel_bwd(sa, H, st));
+    stage_mark(3, st);
 
     // 5. special rows: dense backward over every key (gradients.hpp:197-222)
     if (Ms > 0) {
@@ -1523,6 +1527,7 @@ int gsa_backward(const gsa_tensor* q, const gsa_tensor* k, const gsa_tensor* v, 
         }
     }
 
+    stage_mark(4, st);
     // 6. dW_g = Q_img^T dz per head (gradients.hpp:112-113)
     AtbArgs at{};
     at.A = Q.p + (int64_t)Ms * Q.rs;
@@ -1537,6 +1542,7 @@ int gsa_backward(const gsa_tensor* q, const gsa_tensor* k, const gsa_tensor* v, 
     at.splits = b.splits;
     at.part = b.part;
     GSA_CUDA(launch_atb(at, H, dw_g, st));
+    stage_mark(5, st);
     return GSA_OK;
 }
 
