@@ -1548,6 +1548,7 @@ int gsa_backward(const gsa_tensor* q, const gsa_tensor* k, const gsa_tensor* v, 
 
 size_t gsa_project_backward_workspace_bytes(int tokens, int model_dim, int heads, int dim) {
     if (tokens < 0 || model_dim < 1 || heads < 0 || dim < 1) return 0;
+    if (tc_proj_bwd_supported(dim, model_dim)) return tc_proj_bwd_workspace_bytes(tokens, model_dim, heads) + 256;
     return (size_t)heads * atb_splits(heads, model_dim, dim, tokens) * model_dim * dim * sizeof(float) + 256;
 }
 
@@ -1565,6 +1566,15 @@ int gsa_project_backward(const float* x, int tokens, int model_dim, const float*
     cudaStream_t st = (cudaStream_t)stream;
     const float* g[3] = {dq, dk, dv};
     float* dw[3] = {dw_q, dw_k, dw_v};
+    if (tc_proj_bwd_supported(dim, model_dim) && ((reinterpret_cast<uintptr_t>(dx) | reinterpret_cast<uintptr_t>(dw_q) |
+                                                   reinterpret_cast<uintptr_t>(dw_k) | reinterpret_cast<uintptr_t>(dw_v)) &
+                                                  15) == 0) {
+        // tensor cores (bf16 hi / lo planes, 3-term products); the workspace holds the planes
+        const float* wm[3] = {w_q, w_k, w_v};
+        void* base = reinterpret_cast<void*>((reinterpret_cast<uintptr_t>(workspace) + 255) & ~uintptr_t(255));
+        GSA_CUDA(launch_proj_bwd_tc(x, tokens, model_dim, wm, heads, g, dx, dw, base, st));
+        return GSA_OK;
+    }
     for (int i = 0; i < 3; ++i) {
         AtbArgs a{};
         a.A = x;

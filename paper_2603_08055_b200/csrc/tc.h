@@ -89,4 +89,11 @@ bool tc_bwd_supported(int dim);
 int tc_bwd_dq_splits(int heads, int64_t n_q, int64_t n_k);
 cudaError_t launch_bwd_tc(const BwdTcArgs& a, cudaStream_t st);
 
+// projection backward (proj_bwd_tc.cu), head dim 64: dX = sum G W^T and dW = X^T G with
+// f32 operands as bf16 hi / lo planes (3-term products); scratch from the caller
+bool tc_proj_bwd_supported(int dim, int model_dim);
+size_t tc_proj_bwd_workspace_bytes(int tokens, int model_dim, int heads);
+cudaError_t launch_proj_bwd_tc(const float* x, int tokens, int C, const float* const w[3], int heads,
+                               const float* const g[3], float* dx, float* const dw[3], void* ws, cudaStream_t st);
+
 }  // namespace gsa_sm100

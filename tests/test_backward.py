@@ -147,18 +147,22 @@ def test_backward_bf16_inputs_equal_f32_values(gsa):
         assert torch.equal(x, y)
 
 
-def test_project_backward_matches_float64(gsa):
+@pytest.mark.parametrize("T,Cm,H,d", [(300, 80, 3, 32), (300, 80, 3, 64), (1001, 264, 2, 64)])
+def test_project_backward_matches_float64(gsa, T, Cm, H, d):
+    """d = 64 runs on the tensor cores (bf16 hi / lo planes, 3-term products: ~1e-5 relative),
+    other head dims on CUDA cores (f32 FMA); token counts not a multiple of 8 / 128 and model
+    dims not a multiple of 128 exercise the padded and partial tiles."""
     rng = np.random.default_rng(11)
-    T, Cm, H, d = 300, 80, 3, 32
     x = rng.standard_normal((T, Cm)).astype(np.float32)
     w = [rng.standard_normal((H, Cm, d)).astype(np.float32) for _ in range(3)]
     g = [rng.standard_normal((H, T, d)).astype(np.float32) for _ in range(3)]
     dx, *dws = gsa.project_backward(dev(x), *[dev(t) for t in w], *[dev(t) for t in g])
     x64 = x.astype(np.float64)
     want_dx = sum(np.einsum("htj,haj->ta", gi.astype(np.float64), wi.astype(np.float64)) for gi, wi in zip(g, w))
-    assert rel_l2(host(dx), want_dx) < 1e-6
+    tol = 2e-5 if d == 64 else 1e-6
+    assert rel_l2(host(dx), want_dx) < tol
     for dw, gi in zip(dws, g):
-        assert rel_l2(host(dw), np.einsum("ta,htj->haj", x64, gi.astype(np.float64))) < 1e-6
+        assert rel_l2(host(dw), np.einsum("ta,htj->haj", x64, gi.astype(np.float64))) < tol
 
 
 @pytest.mark.parametrize("lt", [(3, 2, 8, 8, 4), (0, 3, 6, 12, 2), (1, 1, 16, 16, 8)])
