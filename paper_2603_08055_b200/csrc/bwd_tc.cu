@@ -21,7 +21,6 @@
 // exponentials, the hi/lo splits, the epilogue; warp 4 TMA (fixed tiles once, streamed
 // tiles through a 2-stage ring); warp 5 MMA issue (one elected lane).
 // TMEM columns: S 0-127, dP 128-255, out1 256-319, out2 320-383 (512 allocated).
-#define GSA_WATCHDOG 1  // bring-up: a pipeline bug traps after ~10 s instead of hanging
 #include <cuda.h>
 
 #include "tc.h"
