@@ -1227,6 +1227,7 @@ struct BwdBufs {
     // K, V: M rows)
     bool tc;
     __nv_bfloat16 *c_h[4], *c_l[4], *s_h[4], *s_l[4];
+    __nv_bfloat16 *ds_h, *ds_l;  // dS_sel (the selection passes' upstream gradient) [H][Mi][64]
 };
 
 // the dense backward passes run on tcgen05 at head dim 64 (bwd_tc.cu), on CUDA cores otherwise
@@ -1242,19 +1243,23 @@ size_t carve_bwd(const DevLayout& L, int Ms, int H, int d, int64_t E, bool conve
     Carver c{base, cap, 0, dry};
     b->tc = bwd_use_tc(d);
     for (int i = 0; i < 4; ++i) b->c_h[i] = b->c_l[i] = b->s_h[i] = b->s_l[i] = nullptr;
+    b->ds_h = b->ds_l = nullptr;
     if (b->tc) {
         const int64_t Mt = Ms + (int64_t)L.image_tokens, Wt = L.windows;
         for (int i = 0; i < 4; ++i) {
             b->c_h[i] = c.take<__nv_bfloat16>((size_t)H * Wt * 64);
             b->c_l[i] = c.take<__nv_bfloat16>((size_t)H * Wt * 64);
         }
-        if (Ms > 0)
-            for (int i = 0; i < 4; ++i) {
-                const int64_t rows = (i == 1 || i == 2) ? Mt : Ms;  // Q, K, V, dO
-                b->s_h[i] = c.take<__nv_bfloat16>((size_t)H * rows * 64);
-                // bf16 Q / K / V are exact as one plane; dO (f32) always splits
-                if (convert == false || i == 3) b->s_l[i] = c.take<__nv_bfloat16>((size_t)H * rows * 64);
-            }
+        // Q / K / V of every row (the special rows' dense passes and the selection passes),
+        // dO of the special rows; bf16 Q / K / V are exact as one plane, dO (f32) always splits
+        for (int i = 0; i < 4; ++i) {
+            const int64_t rows = i < 3 ? Mt : Ms;
+            if (rows == 0) continue;
+            b->s_h[i] = c.take<__nv_bfloat16>((size_t)H * rows * 64);
+            if (convert == false || i == 3) b->s_l[i] = c.take<__nv_bfloat16>((size_t)H * rows * 64);
+        }
+        b->ds_h = c.take<__nv_bfloat16>((size_t)H * L.image_tokens * 64);
+        b->ds_l = c.take<__nv_bfloat16>((size_t)H * L.image_tokens * 64);
     }
     const int64_t M = Ms + (int64_t)L.image_tokens, Mi = L.image_tokens, W = L.windows;
     b->q32 = b->k32 = b->v32 = nullptr;
@@ -1368,6 +1373,13 @@ int gsa_backward(const gsa_tensor* q, const gsa_tensor* k, const gsa_tensor* v, 
     g.d_comp = b.d_comp;
     g.dq = dQ;
     GSA_CUDA(launch_gate_bwd(g, H, st));
+    if (b.tc) {
+        // tensor-core operand planes of Q / K / V (all rows) and of dS_sel
+        const TensorRef refs[3] = {ref_of(*q), ref_of(*k), ref_of(*v)};
+        for (int i = 0; i < 3; ++i)
+            GSA_CUDA(launch_pack_rows(refs[i], H, lp.M, b.s_h[i], refs[i].dtype == GSA_DTYPE_F32 ? b.s_l[i] : nullptr, st));
+        GSA_CUDA(launch_pack_rows(TensorRef{b.ds, GSA_DTYPE_F32, (int64_t)lp.Mi * d, d}, H, lp.Mi, b.ds_h, b.ds_l, st));
+    }
     stage_mark(1, st);
 
     // 2. compressed attention backward over the windows (gradients.hpp:130-155)
@@ -1456,7 +1468,40 @@ int gsa_backward(const gsa_tensor* q, const gsa_tensor* k, const gsa_tensor* v, 
     sa.dq = dQ;
     sa.dk = dK;
     sa.dv = dV;
-    GSA_CUDA(launch_sel_bwd(sa, H, st));
+    if (b.tc && tc_sel_bwd_supported(d, lp.L.s)) {
+        SelBwdTcArgs t{};
+        t.L = lp.L;
+        t.heads = H;
+        t.scale = lp.scale;
+        const int64_t phs = (int64_t)lp.M * 64, img = (int64_t)Ms * 64;  // image row 0 of the all-row planes
+        auto plane = [&](const __nv_bfloat16* base) { return BwdPlane{base ? base + img : nullptr, phs, 64}; };
+        t.q_hi = plane(b.s_h[0]);
+        t.q_lo = plane(b.s_l[0]);
+        t.k_hi = plane(b.s_h[1]);
+        t.k_lo = plane(b.s_l[1]);
+        t.v_hi = plane(b.s_h[2]);
+        t.v_lo = plane(b.s_l[2]);
+        t.ds_hi = BwdPlane{b.ds_h, (int64_t)lp.Mi * 64, 64};
+        t.ds_lo = BwdPlane{b.ds_l, (int64_t)lp.Mi * 64, 64};
+        t.lse = sv->lse_sel;
+        t.D = b.d_sel;
+        t.offsets = sv->plan_offsets;
+        t.ids = sv->plan_ids;
+        t.inv_offsets = b.inv_offsets;
+        t.inv_q = b.inv_q;
+        t.dq = dQ.p;
+        t.dq_hs = dQ.hs;
+        t.dq_rs = dQ.rs;
+        t.dk = dK.p;
+        t.dk_hs = dK.hs;
+        t.dk_rs = dK.rs;
+        t.dv = dV.p;
+        t.dv_hs = dV.hs;
+        t.dv_rs = dV.rs;
+        GSA_CUDA(launch_sel_bwd_tc(t, st));
+    } else {
+        GSA_CUDA(launch_sel_bwd(sa, H, st));
+    }
     stage_mark(3, st);
 
     // 5. special rows: dense backward over every key (gradients.hpp:197-222)
@@ -1477,18 +1522,15 @@ int gsa_backward(const gsa_tensor* q, const gsa_tensor* k, const gsa_tensor* v, 
         sp.dim = d;
         sp.scale = lp.scale;
         if (b.tc && aligned_rows(*dq) && aligned_rows(*dk) && aligned_rows(*dv)) {
-            // planes: Q / dO of the special rows, K / V of every row (lo only for f32)
-            const TensorRef refs[4] = {ref_of(*q), ref_of(*k), ref_of(*v),
-                                       TensorRef{d_out->data, GSA_DTYPE_F32, d_out->head_stride, d_out->row_stride}};
-            const int rows[4] = {Ms, lp.M, lp.M, Ms};
-            for (int i = 0; i < 4; ++i)
-                GSA_CUDA(launch_pack_rows(refs[i], H, rows[i], b.s_h[i], refs[i].dtype == GSA_DTYPE_F32 ? b.s_l[i] : nullptr,
-                                          st));
+            // planes: Q / K / V packed after the gate; dO of the special rows here
+            GSA_CUDA(launch_pack_rows(TensorRef{d_out->data, GSA_DTYPE_F32, d_out->head_stride, d_out->row_stride}, H, Ms,
+                                      b.s_h[3], b.s_l[3], st));
             BwdTcArgs t{};
             t.heads = H;
             t.n_q = Ms;
             t.n_k = lp.M;
             t.scale = lp.scale;
+            t.q_hs = (int64_t)lp.M * 64;  // the special rows of the all-row Q plane
             t.q_hi = b.s_h[0];
             t.q_lo = q->dtype == GSA_DTYPE_F32 ? b.s_l[0] : nullptr;
             t.k_hi = b.s_h[1];

@@ -303,9 +303,10 @@ __global__ void bwd_tc_reduce_kernel(const float* part, int splits, int heads, i
     }
 }
 
-bool make_plane_map(CUtensorMap* m, const __nv_bfloat16* plane, int heads, int64_t rows) {
-    // contiguous [H][rows][64] bf16; an absent plane maps the hi plane (never loaded)
-    return make_rows_tmap(m, plane, heads, (int)rows, rows * 64, 64);
+bool make_plane_map(CUtensorMap* m, const __nv_bfloat16* plane, int heads, int64_t rows, int64_t hs) {
+    // [H][rows][64] bf16 planes (head stride hs, or rows * 64); an absent plane maps the hi
+    // plane (never loaded)
+    return make_rows_tmap(m, plane, heads, (int)rows, hs ? hs : rows * 64, 64);
 }
 
 }  // namespace
@@ -323,14 +324,14 @@ int tc_bwd_dq_splits(int heads, int64_t n_q, int64_t n_k) {
 cudaError_t launch_bwd_tc(const BwdTcArgs& a, cudaStream_t st) {
     if (a.heads == 0 || a.n_q == 0 || a.n_k == 0) return cudaSuccess;
     CUtensorMap m[8];
-    const bool ok = make_plane_map(&m[0], a.q_hi, a.heads, a.n_q) &&
-                    make_plane_map(&m[1], a.q_lo ? a.q_lo : a.q_hi, a.heads, a.n_q) &&
-                    make_plane_map(&m[2], a.do_hi, a.heads, a.n_q) &&
-                    make_plane_map(&m[3], a.do_lo ? a.do_lo : a.do_hi, a.heads, a.n_q) &&
-                    make_plane_map(&m[4], a.k_hi, a.heads, a.n_k) &&
-                    make_plane_map(&m[5], a.k_lo ? a.k_lo : a.k_hi, a.heads, a.n_k) &&
-                    make_plane_map(&m[6], a.v_hi, a.heads, a.n_k) &&
-                    make_plane_map(&m[7], a.v_lo ? a.v_lo : a.v_hi, a.heads, a.n_k);
+    const bool ok = make_plane_map(&m[0], a.q_hi, a.heads, a.n_q, a.q_hs) &&
+                    make_plane_map(&m[1], a.q_lo ? a.q_lo : a.q_hi, a.heads, a.n_q, a.q_hs) &&
+                    make_plane_map(&m[2], a.do_hi, a.heads, a.n_q, a.do_hs) &&
+                    make_plane_map(&m[3], a.do_lo ? a.do_lo : a.do_hi, a.heads, a.n_q, a.do_hs) &&
+                    make_plane_map(&m[4], a.k_hi, a.heads, a.n_k, a.k_hs) &&
+                    make_plane_map(&m[5], a.k_lo ? a.k_lo : a.k_hi, a.heads, a.n_k, a.k_hs) &&
+                    make_plane_map(&m[6], a.v_hi, a.heads, a.n_k, a.v_hs) &&
+                    make_plane_map(&m[7], a.v_lo ? a.v_lo : a.v_hi, a.heads, a.n_k, a.v_hs);
     if (!ok) return cudaErrorNotSupported;
     const size_t smem = sizeof(BwdSmem) + 1024;
     cudaError_t e = cudaFuncSetAttribute(bwd_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -75,6 +75,7 @@ struct BwdTcArgs {
     int64_t n_q, n_k;
     float scale;
     const __nv_bfloat16 *q_hi, *q_lo, *k_hi, *k_lo, *v_hi, *v_lo, *do_hi, *do_lo;
+    int64_t q_hs, k_hs, v_hs, do_hs;  // plane head strides in elements (0: rows * 64)
     const float *lse, *D;  // [H][n_q]
     float* dq;
     int64_t dq_hs, dq_rs;
@@ -95,5 +96,28 @@ bool tc_proj_bwd_supported(int dim, int model_dim);
 size_t tc_proj_bwd_workspace_bytes(int tokens, int model_dim, int heads);
 cudaError_t launch_proj_bwd_tc(const float* x, int tokens, int C, const float* const w[3], int heads,
                                const float* const g[3], float* dx, float* const dw[3], void* ws, cudaStream_t st);
+
+// selection-branch backward (sel_bwd_tc.cu), head dim 64, window side 4: bf16 planes of the
+// image rows (row 0 = image token 0; lo.p == nullptr: no lo plane), dS_sel hi / lo, the plan
+// and its inverse; dq / dk / dv rows (specials first) are accumulated into
+struct BwdPlane {
+    const __nv_bfloat16* p;
+    int64_t hs, rs;
+};
+struct SelBwdTcArgs {
+    DevLayout L;
+    int heads;
+    float scale;
+    BwdPlane q_hi, q_lo, k_hi, k_lo, v_hi, v_lo, ds_hi, ds_lo;
+    const float *lse, *D;  // [H][Mi]
+    const int64_t* offsets;
+    const int32_t* ids;
+    const int64_t* inv_offsets;
+    const int32_t* inv_q;
+    float *dq, *dk, *dv;
+    int64_t dq_hs, dq_rs, dk_hs, dk_rs, dv_hs, dv_rs;
+};
+bool tc_sel_bwd_supported(int dim, int s);
+cudaError_t launch_sel_bwd_tc(const SelBwdTcArgs& a, cudaStream_t st);
 
 }  // namespace gsa_sm100
