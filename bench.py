@@ -197,7 +197,7 @@ def run_backward(args):
     + gsa_project_backward (gradients.hpp:226-263: dW_q/k/v = X^T dY, dX) at model_dim
     --model-dim, from one forward's saved context, everything resident in HBM. Stage times
     from the library's events; the roofline is the longest stage's (tcgen05 dense passes vs
-    the bf16 peak, selection passes vs the FP32 FMA peak). cpu_baseline: the reference's own
+    the bf16 peak, the gather-bound selection passes vs HBM). cpu_baseline: the reference's own
     gsa_forward + gsa_backward (oracle/_ref) on a 4-view sample with all host threads,
     next to this GPU path on the same sample."""
     import ctypes
@@ -271,20 +271,26 @@ def run_backward(args):
     # dV, dK, dQ); scores: compressed H W^2, special H Ms M, selection entries * s^4
     attn_flops = 5 * 2 * DIM * (HEADS * G["W"] ** 2 + HEADS * G["Ms"] * G["M"] + E * S ** 4)
     proj_flops = 2 * 2 * 3 * G["M"] * C * HEADS * DIM
-    fp32_peak = 148 * 128 * 2 * 1.965e9 / 1e12
     names = ("gate", "compressed", "selection", "special", "dw_g")
     stage_ms = {n: statistics.median(sev[i][j].elapsed_time(sev[i][j + 1]) for i in range(args.steps))
                 for j, n in enumerate(names)}
-    _, tc_peak, _, peak_kind = load_peaks()
+    hbm_peak, tc_peak, _, peak_kind = load_peaks()
     # useful work per stage (FlashAttention-2 accounting, one MMA term: issued tensor work is
-    # up to 3x this with the bf16 hi/lo operand splits)
+    # up to 3x this with the bf16 hi/lo operand splits); the selection passes are bound by
+    # their window gathers: per plan entry K + V (dQ pass) and Q + dS_sel hi / lo (dK/dV
+    # pass), 2 KB per bf16 window plane
+    sel_bytes = E * 2048 * (2 + 3)
     work = {"compressed": (5 * 2 * DIM * HEADS * G["W"] ** 2, "tensor", tc_peak),
             "special": (5 * 2 * DIM * HEADS * G["Ms"] * G["M"], "tensor", tc_peak),
-            "selection": (5 * 2 * DIM * E * S ** 4, "fp32", fp32_peak)}
-    stage_roofline = {n: {"ms": round(stage_ms[n], 3), "tflops": round(f / stage_ms[n] / 1e9, 1), "bound": b,
-                          "frac": round(f / stage_ms[n] / 1e9 / pk, 4)} for n, (f, b, pk) in work.items()}
+            "selection": (sel_bytes, "hbm", hbm_peak)}
+    stage_roofline = {n: {"ms": round(stage_ms[n], 3), "bound": b,
+                          ("gbs" if b == "hbm" else "tflops"): round(f / stage_ms[n] / 1e9 * (1e3 if b == "hbm" else 1), 1),
+                          "frac": round(f / stage_ms[n] / 1e9 * (1e3 if b == "hbm" else 1) / pk, 4)}
+                      for n, (f, b, pk) in work.items()}
+    stage_roofline["selection"]["tflops"] = round(5 * 2 * DIM * E * S ** 4 / stage_ms["selection"] / 1e9, 1)
     dom = max(work, key=lambda n: stage_ms[n])
     f_dom, b_dom, pk_dom = work[dom]
+    unit_scale = 1e3 if b_dom == "hbm" else 1
     line = {"metric": f"GSA layer backward (dX, dW_q/k/v/g) at {V} views", "value": G["M"] / (total_ms / 1e3),
             "unit": "tokens/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
@@ -298,11 +304,11 @@ def run_backward(args):
             "stage_roofline": stage_roofline,
             "attention_backward_tflops": round(attn_flops / attn_ms / 1e9, 1),
             "roofline": {"kernel": {"compressed": "bwd_tc_kernel (compressed branch)", "special":
-                                    "bwd_tc_kernel (special rows)", "selection": "sel16_bwd_kernel"}[dom],
-                         "bound": b_dom, "achieved": f_dom / stage_ms[dom] / 1e9, "peak": pk_dom, "unit": "TFLOP/s",
-                         "frac": f_dom / stage_ms[dom] / 1e9 / pk_dom, "traffic": None,
-                         "peak_kind": (f"{peak_kind} bf16 dense" if b_dom == "tensor" else
-                                       "nominal FP32 (148 SMs x 128 lanes x 2 x 1.965 GHz)")},
+                                    "bwd_tc_kernel (special rows)", "selection": "sel_bwd_tc_kernel"}[dom],
+                         "bound": b_dom, "achieved": f_dom / stage_ms[dom] / 1e9 * unit_scale, "peak": pk_dom,
+                         "unit": "GB/s" if b_dom == "hbm" else "TFLOP/s",
+                         "frac": f_dom / stage_ms[dom] / 1e9 * unit_scale / pk_dom, "traffic": None,
+                         "peak_kind": f"{peak_kind} " + ("HBM copy" if b_dom == "hbm" else "bf16 dense")},
             "projection_tflops": round(proj_flops / proj_ms / 1e9, 2),
             "gpu_launches": int(n1.value - n0.value), "clocks": clk.summary()}
     if not args.no_cpu_baseline:

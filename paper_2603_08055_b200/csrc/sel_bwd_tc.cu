@@ -19,7 +19,6 @@
 // bf16 planes in shared memory (no-swizzle core-matrix layout: [row group of 8][16-byte
 // column chunk][8 rows][16 B]). Outputs accumulate in TMEM and are added to dq / dk / dv
 // by the one CTA that owns those rows.
-#define GSA_WATCHDOG 1  // bring-up: a pipeline bug traps after ~10 s instead of hanging
 #include <cuda.h>
 
 #include "tc.h"
