@@ -33,15 +33,18 @@ namespace {
 using namespace ptx;
 
 constexpr int BT_THREADS = 192;
-constexpr int TILE = 16384;  // 128 rows x 64 bf16, 128B-swizzled
-constexpr int NSTAGE = 2;
-constexpr uint32_t T_S = 0, T_DP = 128, T_O1 = 256, T_O2 = 320, T_COLS = 512;
+constexpr int TILE = 16384;  // 128 rows x 64 bf16, 128B-swizzled (fixed side)
+constexpr int STILE = 8192;  // 64 rows x 64 bf16 (streamed side)
+constexpr int SROWS = 64;    // streamed rows per step
+constexpr int NSTAGE = 4;
+// TMEM: [step parity] S (64 columns) and dP (64 columns); the output accumulators
+constexpr uint32_t T_S = 0, T_DP = 64, T_BUF = 128, T_O1 = 256, T_O2 = 320, T_COLS = 512;
 
 struct __align__(1024) BwdSmem {
     uint8_t fixed[4][TILE];           // A1 hi, A1 lo, A2 hi, A2 lo
-    uint8_t ring[NSTAGE][4][TILE];    // B1 hi, B1 lo, B2 hi, B2 lo
-    float st_lse[2][128], st_D[2][128];
-    uint64_t fixed_full, full[NSTAGE], empty[NSTAGE], s_full, p_full, done;
+    uint8_t ring[NSTAGE][4][STILE];   // B1 hi, B1 lo, B2 hi, B2 lo
+    float st_lse[2][SROWS], st_D[2][SROWS];
+    uint64_t fixed_full, full[NSTAGE], empty[NSTAGE], s_full[2], p_full[2], done;
     uint32_t tmem_base;
 };
 
@@ -60,6 +63,9 @@ struct BwdTcParams {
     bool accumulate;
 };
 
+// Streamed steps of 64 rows; S / dP of step j+1 are issued (into the other TMEM buffer)
+// before the output MMAs of step j, so the row threads' exponentials of one step overlap
+// the tensor work of the next.
 template <bool KEYSIDE>
 __global__ void __launch_bounds__(BT_THREADS, 1)
     bwd_tc_kernel(const __grid_constant__ CUtensorMap tm_a1h, const __grid_constant__ CUtensorMap tm_a1l,
@@ -73,7 +79,7 @@ __global__ void __launch_bounds__(BT_THREADS, 1)
     const int fixed_tile = blockIdx.x, split = blockIdx.y, h = blockIdx.z;
     const int64_t s_begin = (int64_t)split * p.s_chunk;
     const int64_t s_end = min(p.n_stream, s_begin + p.s_chunk);
-    const int T = (int)((s_end - s_begin + 127) / 128);
+    const int T = (int)((s_end - s_begin + SROWS - 1) / SROWS);
 
     if (threadIdx.x == 0) {
         mbar_init(&sm.fixed_full, 1);
@@ -81,8 +87,10 @@ __global__ void __launch_bounds__(BT_THREADS, 1)
             mbar_init(&sm.full[i], 1);
             mbar_init(&sm.empty[i], 1);
         }
-        mbar_init(&sm.s_full, 1);
-        mbar_init(&sm.p_full, 128);
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&sm.s_full[i], 1);
+            mbar_init(&sm.p_full[i], 128);
+        }
         mbar_init(&sm.done, 1);
         fence_barrier_init();
     }
@@ -102,12 +110,12 @@ __global__ void __launch_bounds__(BT_THREADS, 1)
             if (p.a1_lo) tma_load_3d(&sm.fixed[1][0], &tm_a1l, &sm.fixed_full, 0, r0, h);
             tma_load_3d(&sm.fixed[2][0], &tm_a2h, &sm.fixed_full, 0, r0, h);
             if (p.a2_lo) tma_load_3d(&sm.fixed[3][0], &tm_a2l, &sm.fixed_full, 0, r0, h);
-            const uint32_t sb = TILE * (2 + (p.b1_lo ? 1 : 0) + (p.b2_lo ? 1 : 0));
+            const uint32_t sb = STILE * (2 + (p.b1_lo ? 1 : 0) + (p.b2_lo ? 1 : 0));
             for (int j = 0; j < T; ++j) {
                 const int st = j % NSTAGE;
                 mbar_wait(&sm.empty[st], (uint32_t)(((j / NSTAGE) & 1) ^ 1));
                 mbar_arrive_expect_tx(&sm.full[st], sb);
-                const int c1 = (int)(s_begin + (int64_t)j * 128);
+                const int c1 = (int)(s_begin + (int64_t)j * SROWS);
                 tma_load_3d(&sm.ring[st][0][0], &tm_b1h, &sm.full[st], 0, c1, h);
                 if (p.b1_lo) tma_load_3d(&sm.ring[st][1][0], &tm_b1l, &sm.full[st], 0, c1, h);
                 tma_load_3d(&sm.ring[st][2][0], &tm_b2h, &sm.full[st], 0, c1, h);
@@ -117,7 +125,7 @@ __global__ void __launch_bounds__(BT_THREADS, 1)
         __syncwarp();
     } else if (warp == 5) {
         // ================================ MMA ================================
-        const uint32_t id_s = idesc_bf16(128, 128, 0, 0);
+        const uint32_t id_s = idesc_bf16(128, SROWS, 0, 0);
         const uint32_t id_o = idesc_bf16(128, 64, 0, 1);  // A (P / dS) from TMEM, B MN-major
         auto kdesc = [](const uint8_t* t) { return umma_desc(smem_u32(t), 16, 1024, 2); };
         if (T > 0) {
@@ -126,50 +134,59 @@ __global__ void __launch_bounds__(BT_THREADS, 1)
         }
         const uint64_t a1h = kdesc(sm.fixed[0]), a1l = kdesc(sm.fixed[1]);
         const uint64_t a2h = kdesc(sm.fixed[2]), a2l = kdesc(sm.fixed[3]);
-        for (int j = 0; j < T; ++j) {
+        auto issue_S = [&](int j) {
             const int st = j % NSTAGE;
             mbar_wait(&sm.full[st], (uint32_t)((j / NSTAGE) & 1));
             tc_fence_after();
             const uint64_t b1h = kdesc(sm.ring[st][0]), b1l = kdesc(sm.ring[st][1]);
             const uint64_t b2h = kdesc(sm.ring[st][2]), b2l = kdesc(sm.ring[st][3]);
+            const uint32_t ts = tmem + T_S + T_BUF * (j & 1), td = tmem + T_DP + T_BUF * (j & 1);
             if (elect_one()) {
                 // S = A1 B1^T and dP = A2 B2^T over d = 64 (4 k-steps of 16)
                 for (int ks = 0; ks < 4; ++ks) {
                     const uint32_t acc = ks != 0;
-                    mma_bf16(tmem + T_S, a1h + 2 * ks, b1h + 2 * ks, id_s, acc);
-                    if (p.b1_lo) mma_bf16(tmem + T_S, a1h + 2 * ks, b1l + 2 * ks, id_s, 1);
-                    if (p.a1_lo) mma_bf16(tmem + T_S, a1l + 2 * ks, b1h + 2 * ks, id_s, 1);
-                    mma_bf16(tmem + T_DP, a2h + 2 * ks, b2h + 2 * ks, id_s, acc);
-                    if (p.b2_lo) mma_bf16(tmem + T_DP, a2h + 2 * ks, b2l + 2 * ks, id_s, 1);
-                    if (p.a2_lo) mma_bf16(tmem + T_DP, a2l + 2 * ks, b2h + 2 * ks, id_s, 1);
+                    mma_bf16(ts, a1h + 2 * ks, b1h + 2 * ks, id_s, acc);
+                    if (p.b1_lo) mma_bf16(ts, a1h + 2 * ks, b1l + 2 * ks, id_s, 1);
+                    if (p.a1_lo) mma_bf16(ts, a1l + 2 * ks, b1h + 2 * ks, id_s, 1);
+                    mma_bf16(td, a2h + 2 * ks, b2h + 2 * ks, id_s, acc);
+                    if (p.b2_lo) mma_bf16(td, a2h + 2 * ks, b2l + 2 * ks, id_s, 1);
+                    if (p.a2_lo) mma_bf16(td, a2l + 2 * ks, b2h + 2 * ks, id_s, 1);
                 }
-                mma_commit(&sm.s_full);
+                mma_commit(&sm.s_full[j & 1]);
             }
             __syncwarp();
-            mbar_wait(&sm.p_full, (uint32_t)(j & 1));
+        };
+        if (T > 0) issue_S(0);
+        for (int j = 0; j < T; ++j) {
+            if (j + 1 < T) issue_S(j + 1);
+            const int st = j % NSTAGE, pb = j & 1;
+            mbar_wait(&sm.p_full[pb], (uint32_t)((j >> 1) & 1));
             tc_fence_after();
+            const uint64_t b1h = kdesc(sm.ring[st][0]), b1l = kdesc(sm.ring[st][1]);
+            const uint64_t b2h = kdesc(sm.ring[st][2]), b2l = kdesc(sm.ring[st][3]);
+            const uint32_t ts = tmem + T_S + T_BUF * pb, td = tmem + T_DP + T_BUF * pb;
             if (elect_one()) {
-                // outputs over the 128 streamed rows (8 k-steps of 16): the A chunk of k-step ks
+                // outputs over the 64 streamed rows (4 k-steps of 16): the A chunk of k-step ks
                 // holds hi pairs at columns 32 (ks/2) + 8 (ks%2), lo pairs 16 columns further
-                for (int ks = 0; ks < 8; ++ks) {
+                for (int ks = 0; ks < 4; ++ks) {
                     const uint32_t col = 32 * (ks >> 1) + 8 * (ks & 1);
                     const uint32_t acc0 = (j | ks) != 0;
                     if (KEYSIDE) {
                         // dV += P^T dO (B2), dK += dS^T Q (B1)
                         const uint64_t vh = b2h + 128 * ks, vl = b2l + 128 * ks;
-                        mma_bf16_ts(tmem + T_O1, tmem + T_S + col, vh, id_o, acc0);
-                        if (p.b2_lo) mma_bf16_ts(tmem + T_O1, tmem + T_S + col, vl, id_o, 1);
-                        mma_bf16_ts(tmem + T_O1, tmem + T_S + col + 16, vh, id_o, 1);
+                        mma_bf16_ts(tmem + T_O1, ts + col, vh, id_o, acc0);
+                        if (p.b2_lo) mma_bf16_ts(tmem + T_O1, ts + col, vl, id_o, 1);
+                        mma_bf16_ts(tmem + T_O1, ts + col + 16, vh, id_o, 1);
                         const uint64_t qh = b1h + 128 * ks, ql = b1l + 128 * ks;
-                        mma_bf16_ts(tmem + T_O2, tmem + T_DP + col, qh, id_o, acc0);
-                        if (p.b1_lo) mma_bf16_ts(tmem + T_O2, tmem + T_DP + col, ql, id_o, 1);
-                        mma_bf16_ts(tmem + T_O2, tmem + T_DP + col + 16, qh, id_o, 1);
+                        mma_bf16_ts(tmem + T_O2, td + col, qh, id_o, acc0);
+                        if (p.b1_lo) mma_bf16_ts(tmem + T_O2, td + col, ql, id_o, 1);
+                        mma_bf16_ts(tmem + T_O2, td + col + 16, qh, id_o, 1);
                     } else {
                         // dQ += dS K (B1)
                         const uint64_t kh = b1h + 128 * ks, kl = b1l + 128 * ks;
-                        mma_bf16_ts(tmem + T_O1, tmem + T_DP + col, kh, id_o, acc0);
-                        if (p.b1_lo) mma_bf16_ts(tmem + T_O1, tmem + T_DP + col, kl, id_o, 1);
-                        mma_bf16_ts(tmem + T_O1, tmem + T_DP + col + 16, kh, id_o, 1);
+                        mma_bf16_ts(tmem + T_O1, td + col, kh, id_o, acc0);
+                        if (p.b1_lo) mma_bf16_ts(tmem + T_O1, td + col, kl, id_o, 1);
+                        mma_bf16_ts(tmem + T_O1, td + col + 16, kh, id_o, 1);
                     }
                 }
                 mma_commit(&sm.empty[st]);
@@ -182,30 +199,33 @@ __global__ void __launch_bounds__(BT_THREADS, 1)
         const int row = 32 * warp + lane;
         const uint32_t lane_base = tmem + ((uint32_t)(32 * warp) << 16);
         const int64_t grow = (int64_t)fixed_tile * 128 + row;
-        float lse_r = 0.0f, D_r = 0.0f;
+        float l2_r = 0.0f, D_r = 0.0f;
         if (!KEYSIDE) {
             const bool ok = grow < p.n_fixed;
-            lse_r = ok ? p.lse[(int64_t)h * p.n_fixed + grow] : 0.0f;
+            l2_r = ok ? p.lse[(int64_t)h * p.n_fixed + grow] * 1.4426950408889634f : 0.0f;
             D_r = ok ? p.D[(int64_t)h * p.n_fixed + grow] : 0.0f;
         }
         for (int j = 0; j < T; ++j) {
-            const int sb = j & 1;
+            const int pb = j & 1;
             if (KEYSIDE) {
-                // the 128 streamed queries' lse / D, shared by every key row
-                const int64_t q = s_begin + (int64_t)j * 128 + row;
-                const bool ok = q < s_end;
-                sm.st_lse[sb][row] = ok ? p.lse[(int64_t)h * p.n_stream + q] * 1.4426950408889634f : INFINITY;
-                sm.st_D[sb][row] = ok ? p.D[(int64_t)h * p.n_stream + q] : 0.0f;
+                // the 64 streamed queries' lse / D, shared by every key row
+                if (row < SROWS) {
+                    const int64_t q = s_begin + (int64_t)j * SROWS + row;
+                    const bool ok = q < s_end;
+                    sm.st_lse[pb][row] = ok ? p.lse[(int64_t)h * p.n_stream + q] * 1.4426950408889634f : INFINITY;
+                    sm.st_D[pb][row] = ok ? p.D[(int64_t)h * p.n_stream + q] : 0.0f;
+                }
                 named_bar_sync(1, 128);
             }
-            mbar_wait(&sm.s_full, (uint32_t)(j & 1));
+            mbar_wait(&sm.s_full[pb], (uint32_t)((j >> 1) & 1));
             __syncwarp();
             tc_fence_after();
+            const uint32_t ts = lane_base + T_S + T_BUF * pb, td = lane_base + T_DP + T_BUF * pb;
 #pragma unroll 1
-            for (int c = 0; c < 4; ++c) {
+            for (int c = 0; c < SROWS / 32; ++c) {
                 uint32_t sv[32], dv[32];
-                tmem_ld_32x32b_x32(lane_base + T_S + 32 * c, sv);
-                tmem_ld_32x32b_x32(lane_base + T_DP + 32 * c, dv);
+                tmem_ld_32x32b_x32(ts + 32 * c, sv);
+                tmem_ld_32x32b_x32(td + 32 * c, dv);
                 tmem_wait_ld();
                 uint32_t ph[16], pl[16], dh[16], dl[16];
 #pragma unroll
@@ -214,8 +234,8 @@ __global__ void __launch_bounds__(BT_THREADS, 1)
 #pragma unroll
                     for (int u = 0; u < 2; ++u) {
                         const int e = 2 * e2 + u;
-                        const float l2 = KEYSIDE ? sm.st_lse[sb][32 * c + e] : lse_r * 1.4426950408889634f;
-                        const float Dv = KEYSIDE ? sm.st_D[sb][32 * c + e] : D_r;
+                        const float l2 = KEYSIDE ? sm.st_lse[pb][32 * c + e] : l2_r;
+                        const float Dv = KEYSIDE ? sm.st_D[pb][32 * c + e] : D_r;
                         const float pr = ex2_approx(fmaf(__uint_as_float(sv[e]), p.c2, -l2));
                         pv[u] = pr;
                         dsv[u] = pr * (__uint_as_float(dv[e]) - Dv) * p.scale;
@@ -229,15 +249,15 @@ __global__ void __launch_bounds__(BT_THREADS, 1)
                     dl[e2] = pack_bf16(dsv[0] - dhf.x, dsv[1] - dhf.y);
                 }
                 if (KEYSIDE) {
-                    tmem_st_32x32b_x16(lane_base + T_S + 32 * c, ph);
-                    tmem_st_32x32b_x16(lane_base + T_S + 32 * c + 16, pl);
+                    tmem_st_32x32b_x16(ts + 32 * c, ph);
+                    tmem_st_32x32b_x16(ts + 32 * c + 16, pl);
                 }
-                tmem_st_32x32b_x16(lane_base + T_DP + 32 * c, dh);
-                tmem_st_32x32b_x16(lane_base + T_DP + 32 * c + 16, dl);
+                tmem_st_32x32b_x16(td + 32 * c, dh);
+                tmem_st_32x32b_x16(td + 32 * c + 16, dl);
             }
             tmem_wait_st();
             tc_fence_before();
-            mbar_arrive(&sm.p_full);
+            mbar_arrive(&sm.p_full[pb]);
         }
         // ------------------------------- epilogue -------------------------------
         if (T > 0) {
@@ -303,10 +323,18 @@ __global__ void bwd_tc_reduce_kernel(const float* part, int splits, int heads, i
     }
 }
 
-bool make_plane_map(CUtensorMap* m, const __nv_bfloat16* plane, int heads, int64_t rows, int64_t hs) {
-    // [H][rows][64] bf16 planes (head stride hs, or rows * 64); an absent plane maps the hi
-    // plane (never loaded)
-    return make_rows_tmap(m, plane, heads, (int)rows, hs ? hs : rows * 64, 64);
+bool make_plane_map(CUtensorMap* m, const __nv_bfloat16* plane, int heads, int64_t rows, int64_t hs, int box_rows) {
+    // [H][rows][64] bf16 planes (head stride hs, or rows * 64), boxes of box_rows x 64 (128B
+    // swizzle); an absent plane maps the hi plane (never loaded)
+    TmapEncodeFn enc = tmap_encode_fn();
+    if (!enc || rows <= 0) return false;
+    cuuint64_t dims[3] = {64, (cuuint64_t)rows, (cuuint64_t)heads};
+    cuuint64_t strides[2] = {128, (cuuint64_t)(hs ? hs : rows * 64) * 2};
+    cuuint32_t box[3] = {64, (cuuint32_t)box_rows, 1};
+    cuuint32_t es[3] = {1, 1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<__nv_bfloat16*>(plane), dims, strides, box, es,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 }  // namespace
@@ -323,16 +351,22 @@ int tc_bwd_dq_splits(int heads, int64_t n_q, int64_t n_k) {
 
 cudaError_t launch_bwd_tc(const BwdTcArgs& a, cudaStream_t st) {
     if (a.heads == 0 || a.n_q == 0 || a.n_k == 0) return cudaSuccess;
-    CUtensorMap m[8];
-    const bool ok = make_plane_map(&m[0], a.q_hi, a.heads, a.n_q, a.q_hs) &&
-                    make_plane_map(&m[1], a.q_lo ? a.q_lo : a.q_hi, a.heads, a.n_q, a.q_hs) &&
-                    make_plane_map(&m[2], a.do_hi, a.heads, a.n_q, a.do_hs) &&
-                    make_plane_map(&m[3], a.do_lo ? a.do_lo : a.do_hi, a.heads, a.n_q, a.do_hs) &&
-                    make_plane_map(&m[4], a.k_hi, a.heads, a.n_k, a.k_hs) &&
-                    make_plane_map(&m[5], a.k_lo ? a.k_lo : a.k_hi, a.heads, a.n_k, a.k_hs) &&
-                    make_plane_map(&m[6], a.v_hi, a.heads, a.n_k, a.v_hs) &&
-                    make_plane_map(&m[7], a.v_lo ? a.v_lo : a.v_hi, a.heads, a.n_k, a.v_hs);
-    if (!ok) return cudaErrorNotSupported;
+    // [0..7]: Q hi/lo, dO hi/lo, K hi/lo, V hi/lo as FIXED operands (128-row boxes);
+    // [8..15]: the same as STREAMED operands (64-row boxes)
+    CUtensorMap m[16];
+    bool ok = true;
+    for (int f = 0; f < 2; ++f) {
+        const int br = f == 0 ? 128 : SROWS;
+        CUtensorMap* mm = m + 8 * f;
+        ok = ok && make_plane_map(&mm[0], a.q_hi, a.heads, a.n_q, a.q_hs, br) &&
+             make_plane_map(&mm[1], a.q_lo ? a.q_lo : a.q_hi, a.heads, a.n_q, a.q_hs, br) &&
+             make_plane_map(&mm[2], a.do_hi, a.heads, a.n_q, a.do_hs, br) &&
+             make_plane_map(&mm[3], a.do_lo ? a.do_lo : a.do_hi, a.heads, a.n_q, a.do_hs, br) &&
+             make_plane_map(&mm[4], a.k_hi, a.heads, a.n_k, a.k_hs, br) &&
+             make_plane_map(&mm[5], a.k_lo ? a.k_lo : a.k_hi, a.heads, a.n_k, a.k_hs, br) &&
+             make_plane_map(&mm[6], a.v_hi, a.heads, a.n_k, a.v_hs, br) &&
+             make_plane_map(&mm[7], a.v_lo ? a.v_lo : a.v_hi, a.heads, a.n_k, a.v_hs, br);
+    }
     const size_t smem = sizeof(BwdSmem) + 1024;
     cudaError_t e = cudaFuncSetAttribute(bwd_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
@@ -363,7 +397,7 @@ cudaError_t launch_bwd_tc(const BwdTcArgs& a, cudaStream_t st) {
         p.splits = 1;
         p.accumulate = a.accumulate_kv;
         bwd_tc_kernel<true><<<dim3((unsigned)((a.n_k + 127) / 128), 1, a.heads), BT_THREADS, smem, st>>>(
-            m[4], m[5], m[6], m[7], m[0], m[1], m[2], m[3], p);
+            m[4], m[5], m[6], m[7], m[8], m[9], m[10], m[11], p);
         note_launch();
     }
     if (a.dq) {
@@ -390,7 +424,7 @@ cudaError_t launch_bwd_tc(const BwdTcArgs& a, cudaStream_t st) {
         p.part = a.dq_part;
         p.accumulate = a.accumulate_q;
         bwd_tc_kernel<false><<<dim3((unsigned)((a.n_q + 127) / 128), p.splits, a.heads), BT_THREADS, smem, st>>>(
-            m[0], m[1], m[2], m[3], m[4], m[5], m[6], m[7], p);
+            m[0], m[1], m[2], m[3], m[12], m[13], m[14], m[15], p);
         note_launch();
         if (p.splits > 1) {
             const int64_t n = (int64_t)a.heads * a.n_q * 64;
