@@ -361,16 +361,24 @@ __global__ void __launch_bounds__(SB_THREADS, 1)
             tc_fence_before();
             mbar_arrive(&sm.acc_free);
             if (lane < 16) {  // M = 64: feature 16 warp + lane lives in lane `lane` of warp `warp`
+                // the window's 16 rows: all loads first, then the stores (no load waits on a
+                // store to a row the compiler cannot prove distinct)
                 const int f = 16 * warp + lane;
+                const int64_t t0 = L.num_special + L.member(w, 0);
+                float* b1 = p.o1 + (int64_t)h * p.o1_hs + f;
+                float* b2 = KEYSIDE ? p.o2 + (int64_t)h * p.o2_hs + f : nullptr;
+                float x1[16], x2[16];
 #pragma unroll
                 for (int n = 0; n < 16; ++n) {
-                    const int64_t t = L.num_special + L.member(w, n);
-                    float* d1 = p.o1 + (int64_t)h * p.o1_hs + t * p.o1_rs + f;
-                    *d1 += __uint_as_float(o1[n]);
-                    if (KEYSIDE) {
-                        float* d2 = p.o2 + (int64_t)h * p.o2_hs + t * p.o2_rs + f;
-                        *d2 += __uint_as_float(o2[n]);
-                    }
+                    const int64_t t = t0 + (n >> 2) * L.grid_w + (n & 3);  // member n of the window
+                    x1[n] = b1[t * p.o1_rs];
+                    if (KEYSIDE) x2[n] = b2[t * p.o2_rs];
+                }
+#pragma unroll
+                for (int n = 0; n < 16; ++n) {
+                    const int64_t t = t0 + (n >> 2) * L.grid_w + (n & 3);
+                    b1[t * p.o1_rs] = x1[n] + __uint_as_float(o1[n]);
+                    if (KEYSIDE) b2[t * p.o2_rs] = x2[n] + __uint_as_float(o2[n]);
                 }
             }
             ++ic;
