@@ -281,22 +281,25 @@ __global__ void __launch_bounds__(BT_THREADS, 1)
                     } else {
                         dst = p.o2 + (int64_t)h * p.o2_hs + grow * p.o2_rs;
                     }
+                    float4* d4 = reinterpret_cast<float4*>(dst);
+                    float4 y[16];
+                    if (acc) {  // every load before the first store: the 16 loads overlap
 #pragma unroll
-                    for (int half = 0; half < 2; ++half)
+                        for (int e = 0; e < 16; ++e) y[e] = d4[e];
+                    }
 #pragma unroll
-                        for (int e = 0; e < 32; e += 4) {
-                            float4 x = make_float4(__uint_as_float(v[half][e]), __uint_as_float(v[half][e + 1]),
-                                                   __uint_as_float(v[half][e + 2]), __uint_as_float(v[half][e + 3]));
-                            float4* d4 = reinterpret_cast<float4*>(dst + 32 * half + e);
-                            if (acc) {
-                                const float4 y = *d4;
-                                x.x += y.x;
-                                x.y += y.y;
-                                x.z += y.z;
-                                x.w += y.w;
-                            }
-                            *d4 = x;
+                    for (int e = 0; e < 16; ++e) {
+                        const uint32_t* u = &v[e >> 3][4 * (e & 7)];
+                        float4 x = make_float4(__uint_as_float(u[0]), __uint_as_float(u[1]), __uint_as_float(u[2]),
+                                               __uint_as_float(u[3]));
+                        if (acc) {
+                            x.x += y[e].x;
+                            x.y += y[e].y;
+                            x.z += y[e].z;
+                            x.w += y[e].w;
                         }
+                        d4[e] = x;
+                    }
                 }
             }
         }
