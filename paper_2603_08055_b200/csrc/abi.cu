@@ -1345,13 +1345,19 @@ int gsa_backward(const gsa_tensor* q, const gsa_tensor* k, const gsa_tensor* v, 
     stage_mark(0, st);
     FMat Q = fmat_of(*q), K = fmat_of(*k), V = fmat_of(*v);
     if (convert) {
+        // f32 copies for the CUDA-core kernels: Q always (dW_g = Q_img^T dz); K and V only when
+        // a CUDA-core attention pass will read them (the tensor-core passes read bf16 planes)
+        const bool kv32 = !b.tc || !tc_sel_bwd_supported(d, lp.L.s) || !aligned_rows(*dq) || !aligned_rows(*dk) ||
+                          !aligned_rows(*dv);
         const int64_t hs = (int64_t)lp.M * d;
         GSA_CUDA(launch_to_f32(ref_of(*q), H, lp.M, d, b.q32, st));
-        GSA_CUDA(launch_to_f32(ref_of(*k), H, lp.M, d, b.k32, st));
-        GSA_CUDA(launch_to_f32(ref_of(*v), H, lp.M, d, b.v32, st));
         Q = FMat{b.q32, hs, d};
-        K = FMat{b.k32, hs, d};
-        V = FMat{b.v32, hs, d};
+        if (kv32) {
+            GSA_CUDA(launch_to_f32(ref_of(*k), H, lp.M, d, b.k32, st));
+            GSA_CUDA(launch_to_f32(ref_of(*v), H, lp.M, d, b.v32, st));
+            K = FMat{b.k32, hs, d};
+            V = FMat{b.v32, hs, d};
+        }
     }
     const FMat dO = fmat_of(*d_out);
     const FOut dQ = fout_of(*dq), dK = fout_of(*dk), dV = fout_of(*dv);

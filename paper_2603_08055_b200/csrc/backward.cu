@@ -39,6 +39,7 @@ namespace {
 
 constexpr int BT = 256;  // threads per CTA
 constexpr int TB = 64;   // dense tiles: 64 queries x 64 keys
+constexpr int GATE_WPC = 8;  // windows per CTA in the gate-fuse backward
 
 // ------------------------------------------------------------------ gate fuse
 template <int DP>
@@ -51,55 +52,60 @@ __global__ void __launch_bounds__(BT) gate_bwd_kernel(GateBwdArgs a) {
     float* dcf = dz + s2 * DP;        // [s2][DP]  g * dO (upsample-backward terms)
     float* pr = dcf + s2 * DP;        // [s2][DP]  dS_sel * O_sel (D_sel terms)
     float* red = pr + s2 * DP;        // [DP]      dO_comp * O_comp (D_comp terms)
-    const int h = blockIdx.x / W, w = blockIdx.x - h * W;
+    // a CTA takes GATE_WPC consecutive windows of one head: W_g is staged once for all of them
+    const int nblk = (W + GATE_WPC - 1) / GATE_WPC;
+    const int h = blockIdx.x / nblk, w0 = (blockIdx.x - h * nblk) * GATE_WPC;
     const int tid = threadIdx.x;
 
     const float* wgh = a.w_g + (int64_t)h * dim * dim;
     for (int e = tid; e < dim * dim; e += BT) wg[(e / dim) * (DP + 1) + e % dim] = wgh[e];
-    const float* comp = a.o_comp + ((int64_t)h * W + w) * dim;
-    for (int e = tid; e < s2 * dim; e += BT) {
-        const int m = e / dim, j = e - m * dim;
-        const int i = L.member(w, m);
-        const int64_t r = ((int64_t)h * Mi + i) * dim + j;
-        const float go = a.dout.p[(int64_t)h * a.dout.hs + (int64_t)(Ms + i) * a.dout.rs + j];
-        const float g = a.gate[r], sel = a.o_sel[r];
-        const float ds = (1.0f - g) * go;
-        const float dzv = g * (1.0f - g) * ((comp[j] - sel) * go);
-        a.ds[r] = ds;
-        a.dz[r] = dzv;
-        dz[m * DP + j] = dzv;
-        dcf[m * DP + j] = g * go;
-        pr[m * DP + j] = ds * sel;
-    }
-    __syncthreads();
-    // upsample backward: window sum of g * dO in ascending member order
-    for (int j = tid; j < dim; j += BT) {
-        float acc = 0.0f;
-        for (int m = 0; m < s2; ++m) acc += dcf[m * DP + j];
-        a.d_oc[((int64_t)h * W + w) * dim + j] = acc;
-        red[j] = acc * comp[j];
-    }
-    // D_sel rows: one warp per member row
-    const int warp = tid >> 5, lane = tid & 31;
-    for (int m = warp; m < s2; m += BT / 32) {
-        float acc = 0.0f;
-        for (int j = lane; j < dim; j += 32) acc += pr[m * DP + j];
-        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        if (lane == 0) a.d_sel[(int64_t)h * Mi + L.member(w, m)] = acc;
-    }
-    // dq_img = W_g dz (gradients.hpp:108-117), written: the first contribution to dQ
-    for (int e = tid; e < s2 * dim; e += BT) {
-        const int m = e / dim, c = e - m * dim;
-        float acc = 0.0f;
-        for (int j = 0; j < dim; ++j) acc += wg[c * (DP + 1) + j] * dz[m * DP + j];
-        a.dq.p[(int64_t)h * a.dq.hs + (int64_t)(Ms + L.member(w, m)) * a.dq.rs + c] = acc;
-    }
-    __syncthreads();
-    if (warp == 0) {
-        float acc = 0.0f;
-        for (int j = lane; j < dim; j += 32) acc += red[j];
-        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        if (lane == 0) a.d_comp[(int64_t)h * W + w] = acc;
+    for (int w = w0; w < min(W, w0 + GATE_WPC); ++w) {
+        __syncthreads();  // W_g staged; the previous window's smem rows consumed
+        const float* comp = a.o_comp + ((int64_t)h * W + w) * dim;
+        for (int e = tid; e < s2 * dim; e += BT) {
+            const int m = e / dim, j = e - m * dim;
+            const int i = L.member(w, m);
+            const int64_t r = ((int64_t)h * Mi + i) * dim + j;
+            const float go = a.dout.p[(int64_t)h * a.dout.hs + (int64_t)(Ms + i) * a.dout.rs + j];
+            const float g = a.gate[r], sel = a.o_sel[r];
+            const float ds = (1.0f - g) * go;
+            const float dzv = g * (1.0f - g) * ((comp[j] - sel) * go);
+            a.ds[r] = ds;
+            a.dz[r] = dzv;
+            dz[m * DP + j] = dzv;
+            dcf[m * DP + j] = g * go;
+            pr[m * DP + j] = ds * sel;
+        }
+        __syncthreads();
+        // upsample backward: window sum of g * dO in ascending member order
+        for (int j = tid; j < dim; j += BT) {
+            float acc = 0.0f;
+            for (int m = 0; m < s2; ++m) acc += dcf[m * DP + j];
+            a.d_oc[((int64_t)h * W + w) * dim + j] = acc;
+            red[j] = acc * comp[j];
+        }
+        // D_sel rows: one warp per member row
+        const int warp = tid >> 5, lane = tid & 31;
+        for (int m = warp; m < s2; m += BT / 32) {
+            float acc = 0.0f;
+            for (int j = lane; j < dim; j += 32) acc += pr[m * DP + j];
+            for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+            if (lane == 0) a.d_sel[(int64_t)h * Mi + L.member(w, m)] = acc;
+        }
+        // dq_img = W_g dz (gradients.hpp:108-117), written: the first contribution to dQ
+        for (int e = tid; e < s2 * dim; e += BT) {
+            const int m = e / dim, c = e - m * dim;
+            float acc = 0.0f;
+            for (int j = 0; j < dim; ++j) acc += wg[c * (DP + 1) + j] * dz[m * DP + j];
+            a.dq.p[(int64_t)h * a.dq.hs + (int64_t)(Ms + L.member(w, m)) * a.dq.rs + c] = acc;
+        }
+        __syncthreads();
+        if (warp == 0) {
+            float acc = 0.0f;
+            for (int j = lane; j < dim; j += 32) acc += red[j];
+            for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+            if (lane == 0) a.d_comp[(int64_t)h * W + w] = acc;
+        }
     }
 }
 
@@ -947,7 +953,7 @@ cudaError_t gate_bwd_dp(const GateBwdArgs& a, int heads, cudaStream_t st) {
     const size_t smem = (size_t)(DP * (DP + 1) + 3 * s2 * DP + DP) * sizeof(float);
     cudaError_t e = cudaFuncSetAttribute(gate_bwd_kernel<DP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    gate_bwd_kernel<DP><<<(unsigned)((int64_t)heads * a.L.windows), BT, smem, st>>>(a);
+    gate_bwd_kernel<DP><<<(unsigned)((int64_t)heads * ((a.L.windows + GATE_WPC - 1) / GATE_WPC)), BT, smem, st>>>(a);
     note_launch();
     return cudaGetLastError();
 }
