@@ -345,11 +345,20 @@ bool make_plane_map(CUtensorMap* m, const __nv_bfloat16* plane, int heads, int64
 bool tc_bwd_supported(int dim) { return dim == 64 && tmap_encode_fn() != nullptr; }
 
 int tc_bwd_dq_splits(int heads, int64_t n_q, int64_t n_k) {
+    // key splits of the query-side pass (few query tiles: the special rows): the count that
+    // minimises waves / split (the last wave's idle SMs), each split >= 8 key tiles
     const int64_t ctas = (int64_t)heads * ((n_q + 127) / 128);
-    int64_t s = (2 * 148 + ctas - 1) / ctas;
-    const int64_t cap = ((n_k + 127) / 128) / 8;  // >= 8 key tiles per split
-    if (s > cap) s = cap;
-    return (int)(s < 1 ? 1 : s > 64 ? 64 : s);
+    const int64_t cap = std::max<int64_t>(1, std::min<int64_t>(16, ((n_k + 127) / 128) / 8));
+    int best = 1;
+    double best_cost = 1e30;
+    for (int64_t s = 1; s <= cap; ++s) {
+        const double cost = (double)((ctas * s + 147) / 148) / (double)s;
+        if (cost < best_cost * 0.98) {
+            best_cost = cost;
+            best = (int)s;
+        }
+    }
+    return best;
 }
 
 cudaError_t launch_bwd_tc(const BwdTcArgs& a, cudaStream_t st) {
