@@ -199,12 +199,13 @@ __global__ void __launch_bounds__(BT_THREADS, 1)
         const int row = 32 * warp + lane;
         const uint32_t lane_base = tmem + ((uint32_t)(32 * warp) << 16);
         const int64_t grow = (int64_t)fixed_tile * 128 + row;
-        float l2_r = 0.0f, D_r = 0.0f;
+        float nl2_r = 0.0f, nD_r = 0.0f;  // -lse * log2(e), -D of this (query) row
         if (!KEYSIDE) {
             const bool ok = grow < p.n_fixed;
-            l2_r = ok ? p.lse[(int64_t)h * p.n_fixed + grow] * 1.4426950408889634f : 0.0f;
-            D_r = ok ? p.D[(int64_t)h * p.n_fixed + grow] : 0.0f;
+            nl2_r = ok ? -p.lse[(int64_t)h * p.n_fixed + grow] * 1.4426950408889634f : 0.0f;
+            nD_r = ok ? -p.D[(int64_t)h * p.n_fixed + grow] : 0.0f;
         }
+        const float2 c2v = make_float2(p.c2, p.c2), scv = make_float2(p.scale, p.scale), m1 = make_float2(-1.0f, -1.0f);
         for (int j = 0; j < T; ++j) {
             const int pb = j & 1;
             if (KEYSIDE) {
@@ -212,8 +213,8 @@ __global__ void __launch_bounds__(BT_THREADS, 1)
                 if (row < SROWS) {
                     const int64_t q = s_begin + (int64_t)j * SROWS + row;
                     const bool ok = q < s_end;
-                    sm.st_lse[pb][row] = ok ? p.lse[(int64_t)h * p.n_stream + q] * 1.4426950408889634f : INFINITY;
-                    sm.st_D[pb][row] = ok ? p.D[(int64_t)h * p.n_stream + q] : 0.0f;
+                    sm.st_lse[pb][row] = ok ? -p.lse[(int64_t)h * p.n_stream + q] * 1.4426950408889634f : -INFINITY;
+                    sm.st_D[pb][row] = ok ? -p.D[(int64_t)h * p.n_stream + q] : 0.0f;
                 }
                 named_bar_sync(1, 128);
             }
@@ -230,23 +231,25 @@ __global__ void __launch_bounds__(BT_THREADS, 1)
                 uint32_t ph[16], pl[16], dh[16], dl[16];
 #pragma unroll
                 for (int e2 = 0; e2 < 16; ++e2) {
-                    float pv[2], dsv[2];
-#pragma unroll
-                    for (int u = 0; u < 2; ++u) {
-                        const int e = 2 * e2 + u;
-                        const float l2 = KEYSIDE ? sm.st_lse[pb][32 * c + e] : l2_r;
-                        const float Dv = KEYSIDE ? sm.st_D[pb][32 * c + e] : D_r;
-                        const float pr = ex2_approx(fmaf(__uint_as_float(sv[e]), p.c2, -l2));
-                        pv[u] = pr;
-                        dsv[u] = pr * (__uint_as_float(dv[e]) - Dv) * p.scale;
-                    }
-                    const __nv_bfloat162 phb = __floats2bfloat162_rn(pv[0], pv[1]);
-                    const __nv_bfloat162 dhb = __floats2bfloat162_rn(dsv[0], dsv[1]);
-                    const float2 phf = __bfloat1622float2(phb), dhf = __bfloat1622float2(dhb);
+                    // pairs on the packed f32x2 pipe; the statistics are stored negated
+                    const float2 nl = KEYSIDE ? *reinterpret_cast<const float2*>(&sm.st_lse[pb][32 * c + 2 * e2])
+                                              : make_float2(nl2_r, nl2_r);
+                    const float2 nd = KEYSIDE ? *reinterpret_cast<const float2*>(&sm.st_D[pb][32 * c + 2 * e2])
+                                              : make_float2(nD_r, nD_r);
+                    const float2 a2 = __ffma2_rn(make_float2(__uint_as_float(sv[2 * e2]), __uint_as_float(sv[2 * e2 + 1])),
+                                                 c2v, nl);
+                    const float2 pv = make_float2(ex2_approx(a2.x), ex2_approx(a2.y));
+                    const float2 t2 = __fadd2_rn(make_float2(__uint_as_float(dv[2 * e2]), __uint_as_float(dv[2 * e2 + 1])), nd);
+                    const float2 dsv = __fmul2_rn(__fmul2_rn(pv, t2), scv);
+                    const __nv_bfloat162 phb = __float22bfloat162_rn(pv);
+                    const __nv_bfloat162 dhb = __float22bfloat162_rn(dsv);
+                    const float2 plo = __ffma2_rn(__bfloat1622float2(phb), m1, pv);
+                    const float2 dlo = __ffma2_rn(__bfloat1622float2(dhb), m1, dsv);
                     ph[e2] = *reinterpret_cast<const uint32_t*>(&phb);
                     dh[e2] = *reinterpret_cast<const uint32_t*>(&dhb);
-                    pl[e2] = pack_bf16(pv[0] - phf.x, pv[1] - phf.y);
-                    dl[e2] = pack_bf16(dsv[0] - dhf.x, dsv[1] - dhf.y);
+                    const __nv_bfloat162 plb = __float22bfloat162_rn(plo), dlb = __float22bfloat162_rn(dlo);
+                    pl[e2] = *reinterpret_cast<const uint32_t*>(&plb);
+                    dl[e2] = *reinterpret_cast<const uint32_t*>(&dlb);
                 }
                 if (KEYSIDE) {
                     tmem_st_32x32b_x16(ts + 32 * c, ph);
