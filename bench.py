@@ -229,19 +229,25 @@ def run_backward(args):
         return Lv, q, k, v, wg, out, ctx, plan, d_out, x, w
 
     Lv, q, k, v, wg, out, ctx, plan, d_out, x, w = instance(V, C)
-    ws = gsa.Workspace()
+    ws, pws = gsa.Workspace(), gsa.Workspace()
+    # gradient buffers allocated once (like the forward's `out`): the step times the kernels
+    # and the API calls, not the caching allocator
+    g_att = tuple(torch.empty(HEADS, G["M"], DIM, device="cuda") for _ in range(3)) + \
+        (torch.empty(HEADS, DIM, DIM, device="cuda"),)
+    g_proj = (torch.empty(G["M"], C, device="cuda"),) + tuple(torch.empty(HEADS, C, DIM, device="cuda") for _ in range(3))
 
     def step(evs=None, stage=None):
         if evs:
             evs[0].record()
         if stage is not None:
             lib.gsa_set_stage_events(stage, 7)
-        dq, dk, dv, dwg = gsa.gsa_backward(q, k, v, wg, Lv, params, ctx, out, d_out, plan=plan, workspace=ws)
+        dq, dk, dv, dwg = gsa.gsa_backward(q, k, v, wg, Lv, params, ctx, out, d_out, plan=plan, workspace=ws,
+                                           grads=g_att)
         if stage is not None:
             lib.gsa_set_stage_events(None, 0)
         if evs:
             evs[1].record()
-        gsa.project_backward(x, *w, dq, dk, dv)
+        gsa.project_backward(x, *w, dq, dk, dv, workspace=pws, grads=g_proj)
         if evs:
             evs[2].record()
 

@@ -1222,6 +1222,7 @@ struct BwdBufs {
     int splits;
     float* spec_dq_part;  // key-split partial dQ of the special rows
     int spec_splits;
+    int* check;           // plan validation flag
     // tensor-core dense passes: bf16 hi (+ lo for f32 operands) planes [H][rows][64] of the
     // compressed branch (Qc, Kc, Vc, dO_comp: W rows) and the special rows (Q, dO: Ms rows;
     // K, V: M rows)
@@ -1286,6 +1287,7 @@ size_t carve_bwd(const DevLayout& L, int Ms, int H, int d, int64_t E, bool conve
     b->tmp = c.take<char>(b->tmp_bytes);
     b->splits = atb_splits(H, d, d, Mi);
     b->part = c.take<float>((size_t)H * b->splits * d * d);
+    b->check = c.take<int>(1);
     b->spec_splits = Ms > 0 ? (b->tc ? tc_bwd_dq_splits(H, Ms, M) : dense_dq_splits(H, Ms, M)) : 1;
     b->spec_dq_part = b->spec_splits > 1 ? c.take<float>((size_t)b->spec_splits * H * Ms * d) : nullptr;
     return c.used;
@@ -1334,13 +1336,22 @@ int gsa_backward(const gsa_tensor* q, const gsa_tensor* k, const gsa_tensor* v, 
                                   false, &b);
     if (need > ws_bytes + 256) return fail(GSA_ERR_WORKSPACE, "gsa_backward: workspace %zu < %zu", ws_bytes, need);
     if (rows == 0) return GSA_OK;
-    GSA_TRY(validate_plan(sv->plan_offsets, sv->plan_ids, rows, W, "gsa_backward", st));
-    int64_t total = 0;
-    GSA_CUDA(cudaMemcpyAsync(&total, sv->plan_offsets + rows, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-    GSA_CUDA(cudaStreamSynchronize(st));
-    if (total != sv->plan_entries)
-        return fail(GSA_ERR_CONTEXT_MISMATCH, "gsa_backward: plan holds %lld entries, saved.plan_entries = %lld",
-                    (long long)total, (long long)sv->plan_entries);
+    // plan validation (like gsa_forward_with_plan's) and its entry count: one round trip,
+    // the flag in the caller's workspace (no allocation)
+    if (!sv->plan_offsets || !sv->plan_ids) return fail(GSA_ERR_GENERIC, "gsa_backward: null plan");
+    {
+        GSA_CUDA(cudaMemsetAsync(b.check, 0, sizeof(int), st));
+        GSA_CUDA(launch_plan_check(sv->plan_offsets, rows, sv->plan_ids, W, b.check, st));
+        struct { int flag; int pad; int64_t total; } hb{0, 0, 0};
+        GSA_CUDA(cudaMemcpyAsync(&hb.flag, b.check, sizeof(int), cudaMemcpyDeviceToHost, st));
+        GSA_CUDA(cudaMemcpyAsync(&hb.total, sv->plan_offsets + rows, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+        GSA_CUDA(cudaStreamSynchronize(st));
+        if (hb.flag & 1) return fail(GSA_ERR_EMPTY_SELECTION, "gsa_backward: empty plan row");
+        if (hb.flag & 2) return fail(GSA_ERR_INDEX_OUT_OF_RANGE, "gsa_backward: plan window id outside [0, %d)", W);
+        if (hb.total != sv->plan_entries)
+            return fail(GSA_ERR_CONTEXT_MISMATCH, "gsa_backward: plan holds %lld entries, saved.plan_entries = %lld",
+                        (long long)hb.total, (long long)sv->plan_entries);
+    }
 
     stage_mark(0, st);
     FMat Q = fmat_of(*q), K = fmat_of(*k), V = fmat_of(*v);

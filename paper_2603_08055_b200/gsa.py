@@ -475,11 +475,13 @@ def upsample_backward(d_fine: torch.Tensor, layout: TokenLayout) -> torch.Tensor
 
 
 def gsa_backward(q, k, v, w_g, layout: TokenLayout, params: GsaParams, ctx: ForwardContext, out: torch.Tensor,
-                 d_out: torch.Tensor, plan: Optional[SelectionPlan] = None, workspace: Optional[Workspace] = None):
+                 d_out: torch.Tensor, plan: Optional[SelectionPlan] = None, workspace: Optional[Workspace] = None,
+                 grads: Optional[tuple] = None):
     """gsa_backward (gradients.hpp:54-243) up to the projection: the layer's gradients with
     respect to the projected q/k/v and to W_g, with the top-k held constant. `ctx` and `out`
     are what gsa_forward(..., context=True) returned for the same q/k/v; the plan is rebuilt
-    from ctx.topk unless given. Returns (dq, dk, dv, dw_g), f32."""
+    from ctx.topk unless given; `grads` = (dq, dk, dv, dw_g) f32 buffers to write into.
+    Returns (dq, dk, dv, dw_g), f32."""
     L = _lib.load()
     H, M, d = q.shape
     dev = q.device
@@ -495,26 +497,35 @@ def gsa_backward(q, k, v, w_g, layout: TokenLayout, params: GsaParams, ctx: Forw
                       ctx.o_sel.data_ptr(), ctx.lse_sel.data_ptr(), ctx.gate_vals.data_ptr(), _desc(out[:, :Ms]),
                       ctx.lse_spec.data_ptr() if Ms else None)
     d_out = d_out.float()
-    dq, dk, dv = (_empty(H, M, d, device=dev) for _ in range(3))
-    dw_g = _empty(H, d, d, device=dev)
+    if grads is None:
+        dq, dk, dv = (_empty(H, M, d, device=dev) for _ in range(3))
+        dw_g = _empty(H, d, d, device=dev)
+    else:
+        dq, dk, dv, dw_g = grads
     _check(L.gsa_backward(C.byref(_desc(q)), C.byref(_desc(k)), C.byref(_desc(v)), C.byref(_desc(w_g.contiguous())),
                           C.byref(lc), C.byref(pc), C.byref(saved), C.byref(_desc(d_out)), C.byref(_desc(dq)),
                           C.byref(_desc(dk)), C.byref(_desc(dv)), _ptr(dw_g), _ptr(ws), ws.numel(), _stream()))
     return dq, dk, dv, dw_g
 
 
-def project_backward(x, w_q, w_k, w_v, dq, dk, dv):
+def project_backward(x, w_q, w_k, w_v, dq, dk, dv, workspace: Optional[Workspace] = None, grads: Optional[tuple] = None):
     """Projection backward (gradients.hpp:226-263): dW_* = X^T dY per head and
-    dX = sum_h dQ W_q^T + dK W_k^T + dV W_v^T. Returns (dx, dw_q, dw_k, dw_v), f32."""
+    dX = sum_h dQ W_q^T + dK W_k^T + dV W_v^T. `grads` = (dx, dw_q, dw_k, dw_v) f32 buffers
+    to write into. Returns (dx, dw_q, dw_k, dw_v), f32."""
     L = _lib.load()
     x, w_q, w_k, w_v, dq, dk, dv = (t.float().contiguous() for t in (x, w_q, w_k, w_v, dq, dk, dv))
     if x.dim() == 3:
         x = x.reshape(x.shape[-2], x.shape[-1])
     T, Cm = x.shape
     H, _, d = w_q.shape
-    dx = _empty(T, Cm, device=x.device)
-    dws = [_empty(H, Cm, d, device=x.device) for _ in range(3)]
-    ws = torch.empty(L.gsa_project_backward_workspace_bytes(T, Cm, H, d), dtype=torch.uint8, device=x.device)
+    if grads is None:
+        dx = _empty(T, Cm, device=x.device)
+        dws = [_empty(H, Cm, d, device=x.device) for _ in range(3)]
+    else:
+        dx, dws = grads[0], list(grads[1:])
+    nbytes = L.gsa_project_backward_workspace_bytes(T, Cm, H, d)
+    ws = (workspace.get(nbytes, x.device) if workspace is not None
+          else torch.empty(nbytes, dtype=torch.uint8, device=x.device))
     _check(L.gsa_project_backward(_ptr(x), T, Cm, _ptr(w_q), _ptr(w_k), _ptr(w_v), H, d, _ptr(dq), _ptr(dk), _ptr(dv),
                                   _ptr(dx), *[_ptr(t) for t in dws], _ptr(ws), ws.numel(), _stream()))
     return (dx, *dws)
