@@ -213,14 +213,15 @@ def run_backward(args):
     lt = layout_for(V)
     G = geometry(V)
     L = gsa.build_token_layout(*lt)
-    params = gsa.GsaParams(window_s=S, top_k=TOPK)
+    params = gsa.GsaParams(window_s=S, top_k=TOPK, variant=1 if args.hybrid else 0,
+                           ref_stride=args.hybrid if args.hybrid else 100)
 
     def instance(views, cm, seed=7):
         ltv = layout_for(views)
         Lv = gsa.build_token_layout(*ltv)
         q, k, v, wg = synth_qkv(torch, views, seed=seed)
         out, ctx = gsa.gsa_forward(q, k, v, wg, Lv, params, context=True)
-        plan = gsa.build_selection_plan(ctx.topk, Lv, 0, 100)
+        plan = gsa.build_selection_plan(ctx.topk, Lv, params.variant, params.ref_stride)
         gen = torch.Generator(device="cuda").manual_seed(seed + 1)
         d_out = torch.randn(out.shape, generator=gen, device="cuda")
         M = out.shape[1]
@@ -302,7 +303,9 @@ def run_backward(args):
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (torch N(0,1) bf16 Q/K/V, f32 X / W / dO), resident in HBM",
             "config": {"workload": f"backward of 1 GSA layer, {V} views x ({SPECIAL_PER_VIEW} specials + {GRID_H}x{GRID_W} "
-                                   f"patches) = {G['M']} tokens, 16 heads x 64, s=4, top-{TOPK}, plain, model_dim {C}",
+                                   f"patches) = {G['M']} tokens, 16 heads x 64, s=4, top-{TOPK}, "
+                                   f"{'hybrid (reference frames every %d views)' % args.hybrid if args.hybrid else 'plain'}, "
+                                   f"model_dim {C}",
                        "views": V, "tokens": G["M"], "windows": G["W"], "plan_entries": E, "model_dim": C,
                        "parallelism": "1 GPU", "l2": "inputs larger than L2 (no flush)"},
             "stage_ms": {"attention_backward": round(attn_ms, 3), "projection_backward": round(proj_ms, 3),

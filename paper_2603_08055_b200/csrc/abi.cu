@@ -1223,6 +1223,15 @@ struct BwdBufs {
     float* spec_dq_part;  // key-split partial dQ of the special rows
     int spec_splits;
     int* check;           // plan validation flag
+    // hybrid fast path (tensor cores): the forced windows' keys run as a dense pass, the
+    // selection passes walk the plan without them
+    int n_ff;             // forced frames (0: off)
+    int64_t n_fr;         // forced rows per head
+    uint8_t* fmask;
+    int64_t *dyn_sizes, *dyn_offsets;
+    int32_t* dyn_ids;
+    __nv_bfloat16 *fk_h, *fk_l, *fv_h, *fv_l;
+    float *gk, *gv;
     // tensor-core dense passes: bf16 hi (+ lo for f32 operands) planes [H][rows][64] of the
     // compressed branch (Qc, Kc, Vc, dO_comp: W rows) and the special rows (Q, dO: Ms rows;
     // K, V: M rows)
@@ -1239,7 +1248,14 @@ bool aligned_rows(const gsa_tensor& t) {
     return t.row_stride % 4 == 0 && t.head_stride % 4 == 0 && (reinterpret_cast<uintptr_t>(t.data) & 15) == 0;
 }
 
-size_t carve_bwd(const DevLayout& L, int Ms, int H, int d, int64_t E, bool convert, char* base, size_t cap,
+// forced frames of the hybrid fast path: reference frames every ref_stride frames, when the
+// selection passes run on the tensor cores (0 otherwise)
+int bwd_forced_frames(const DevLayout& L, const gsa_params* p, int d) {
+    if (!p || p->variant != 1 || p->ref_stride < 1 || !tc_bwd_supported(d) || !tc_sel_bwd_supported(d, L.s)) return 0;
+    return (L.num_frames + p->ref_stride - 1) / p->ref_stride;
+}
+
+size_t carve_bwd(const DevLayout& L, int Ms, int H, int d, int64_t E, bool convert, int n_ff, char* base, size_t cap,
                  bool dry, BwdBufs* b) {
     Carver c{base, cap, 0, dry};
     b->tc = bwd_use_tc(d);
@@ -1287,7 +1303,29 @@ size_t carve_bwd(const DevLayout& L, int Ms, int H, int d, int64_t E, bool conve
     b->tmp = c.take<char>(b->tmp_bytes);
     b->splits = atb_splits(H, d, d, Mi);
     b->part = c.take<float>((size_t)H * b->splits * d * d);
-    b->check = c.take<int>(1);
+    b->check = c.take<int>(4);
+    b->n_ff = b->tc ? n_ff : 0;
+    b->n_fr = (int64_t)b->n_ff * L.tokens_per_frame;
+    b->fmask = nullptr;
+    b->dyn_sizes = b->dyn_offsets = nullptr;
+    b->dyn_ids = nullptr;
+    b->fk_h = b->fk_l = b->fv_h = b->fv_l = nullptr;
+    b->gk = b->gv = nullptr;
+    if (b->n_ff > 0) {
+        const size_t rows = (size_t)H * L.windows, fr = (size_t)H * b->n_fr * 64;
+        b->fmask = c.take<uint8_t>((size_t)L.windows);
+        b->dyn_sizes = c.take<int64_t>(rows);
+        b->dyn_offsets = c.take<int64_t>(rows + 1);
+        b->dyn_ids = c.take<int32_t>((size_t)(E > 0 ? E : 1));
+        b->fk_h = c.take<__nv_bfloat16>(fr);
+        b->fv_h = c.take<__nv_bfloat16>(fr);
+        if (!convert) {
+            b->fk_l = c.take<__nv_bfloat16>(fr);
+            b->fv_l = c.take<__nv_bfloat16>(fr);
+        }
+        b->gk = c.take<float>(fr);
+        b->gv = c.take<float>(fr);
+    }
     b->spec_splits = Ms > 0 ? (b->tc ? tc_bwd_dq_splits(H, Ms, M) : dense_dq_splits(H, Ms, M)) : 1;
     b->spec_dq_part = b->spec_splits > 1 ? c.take<float>((size_t)b->spec_splits * H * Ms * d) : nullptr;
     return c.used;
@@ -1299,11 +1337,11 @@ extern "C" {
 
 size_t gsa_backward_workspace_bytes(const gsa_layout* layout, const gsa_params* params, int heads, int dim,
                                     int64_t plan_entries, int qkv_dtype) {
-    (void)params;
     if (check_layout(layout) != GSA_OK || heads < 0 || dim < 1 || plan_entries < 0) return 0;
     const DevLayout L = make_dev_layout(*layout);
     BwdBufs b;
-    return carve_bwd(L, layout->num_special, heads, dim, plan_entries, qkv_dtype != GSA_DTYPE_F32, nullptr, 0, true,
+    return carve_bwd(L, layout->num_special, heads, dim, plan_entries, qkv_dtype != GSA_DTYPE_F32,
+                     bwd_forced_frames(L, params, dim), nullptr, 0, true,
                      &b) + 256;
 }
 
@@ -1332,20 +1370,31 @@ int gsa_backward(const gsa_tensor* q, const gsa_tensor* k, const gsa_tensor* v, 
     cudaStream_t st = (cudaStream_t)stream;
     const bool convert = q->dtype != GSA_DTYPE_F32;
     BwdBufs b;
-    const size_t need = carve_bwd(lp.L, Ms, H, d, sv->plan_entries, convert, static_cast<char*>(workspace), ws_bytes,
+    const size_t need = carve_bwd(lp.L, Ms, H, d, sv->plan_entries, convert, bwd_forced_frames(lp.L, params, d),
+                                  static_cast<char*>(workspace), ws_bytes,
                                   false, &b);
     if (need > ws_bytes + 256) return fail(GSA_ERR_WORKSPACE, "gsa_backward: workspace %zu < %zu", ws_bytes, need);
     if (rows == 0) return GSA_OK;
     // plan validation (like gsa_forward_with_plan's) and its entry count: one round trip,
     // the flag in the caller's workspace (no allocation)
     if (!sv->plan_offsets || !sv->plan_ids) return fail(GSA_ERR_GENERIC, "gsa_backward: null plan");
+    int64_t dyn_entries = 0;
     {
         GSA_CUDA(cudaMemsetAsync(b.check, 0, sizeof(int), st));
         GSA_CUDA(launch_plan_check(sv->plan_offsets, rows, sv->plan_ids, W, b.check, st));
-        struct { int flag; int pad; int64_t total; } hb{0, 0, 0};
+        struct { int flag; int pad; int64_t total, dyn_total; } hb{0, 0, 0, 0};
+        if (b.n_ff > 0) {
+            // hybrid: the plan without the forced windows (ids outside [0, W) count as kept and
+            // are reported by the check below before anything reads them)
+            GSA_CUDA(launch_forced(lp.L, params->ref_stride, nullptr, b.fmask, st));
+            GSA_CUDA(launch_plan_drop(sv->plan_offsets, sv->plan_ids, rows, b.fmask, W, b.dyn_sizes, b.dyn_offsets,
+                                      b.dyn_ids, b.tmp, b.tmp_bytes, st));
+            GSA_CUDA(cudaMemcpyAsync(&hb.dyn_total, b.dyn_offsets + rows, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+        }
         GSA_CUDA(cudaMemcpyAsync(&hb.flag, b.check, sizeof(int), cudaMemcpyDeviceToHost, st));
         GSA_CUDA(cudaMemcpyAsync(&hb.total, sv->plan_offsets + rows, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
         GSA_CUDA(cudaStreamSynchronize(st));
+        dyn_entries = hb.dyn_total;
         if (hb.flag & 1) return fail(GSA_ERR_EMPTY_SELECTION, "gsa_backward: empty plan row");
         if (hb.flag & 2) return fail(GSA_ERR_INDEX_OUT_OF_RANGE, "gsa_backward: plan window id outside [0, %d)", W);
         if (hb.total != sv->plan_entries)
@@ -1466,8 +1515,11 @@ int gsa_backward(const gsa_tensor* q, const gsa_tensor* k, const gsa_tensor* v, 
     GSA_CUDA(launch_pool_bwd(pb, st));
 
     // 4. selection backward over the detached plan (gradients.hpp:171-195)
-    GSA_CUDA(launch_inverse_plan(sv->plan_offsets, sv->plan_ids, rows, W, sv->plan_entries, b.keys, b.keys_sorted,
-                                 b.counts, b.inv_offsets, b.inv_q, b.tmp, b.tmp_bytes, st));
+    const int64_t* sel_offsets = b.n_ff > 0 ? b.dyn_offsets : sv->plan_offsets;
+    const int32_t* sel_ids = b.n_ff > 0 ? b.dyn_ids : sv->plan_ids;
+    const int64_t sel_entries = b.n_ff > 0 ? dyn_entries : sv->plan_entries;
+    GSA_CUDA(launch_inverse_plan(sel_offsets, sel_ids, rows, W, sel_entries, b.keys, b.keys_sorted, b.counts,
+                                 b.inv_offsets, b.inv_q, b.tmp, b.tmp_bytes, st));
     SelBwdArgs sa{};
     sa.q = Q;
     sa.k = K;
@@ -1502,8 +1554,8 @@ int gsa_backward(const gsa_tensor* q, const gsa_tensor* k, const gsa_tensor* v, 
         t.ds_lo = BwdPlane{b.ds_l, (int64_t)lp.Mi * 64, 64};
         t.lse = sv->lse_sel;
         t.D = b.d_sel;
-        t.offsets = sv->plan_offsets;
-        t.ids = sv->plan_ids;
+        t.offsets = sel_offsets;
+        t.ids = sel_ids;
         t.inv_offsets = b.inv_offsets;
         t.inv_q = b.inv_q;
         t.dq = dQ.p;
@@ -1516,6 +1568,47 @@ int gsa_backward(const gsa_tensor* q, const gsa_tensor* k, const gsa_tensor* v, 
         t.dv_hs = dV.hs;
         t.dv_rs = dV.rs;
         GSA_CUDA(launch_sel_bwd_tc(t, st));
+        if (b.n_ff > 0) {
+            // the forced windows' keys: a dense pass of every image query over the forced-frame
+            // rows (their P from the same total LSE rows), gathered contiguously
+            const int rs = params->ref_stride;
+            GSA_CUDA(launch_forced_gather(b.s_h[1], (int64_t)lp.M * 64, H, lp.L, rs, b.n_fr, b.fk_h, st));
+            GSA_CUDA(launch_forced_gather(b.s_h[2], (int64_t)lp.M * 64, H, lp.L, rs, b.n_fr, b.fv_h, st));
+            if (b.fk_l) {
+                GSA_CUDA(launch_forced_gather(b.s_l[1], (int64_t)lp.M * 64, H, lp.L, rs, b.n_fr, b.fk_l, st));
+                GSA_CUDA(launch_forced_gather(b.s_l[2], (int64_t)lp.M * 64, H, lp.L, rs, b.n_fr, b.fv_l, st));
+            }
+            BwdTcArgs f{};
+            f.heads = H;
+            f.n_q = lp.Mi;
+            f.n_k = b.n_fr;
+            f.scale = lp.scale;
+            f.q_hi = b.s_h[0] + img;
+            f.q_lo = b.s_l[0] ? b.s_l[0] + img : nullptr;
+            f.q_hs = phs;
+            f.do_hi = b.ds_h;
+            f.do_lo = b.ds_l;
+            f.do_hs = (int64_t)lp.Mi * 64;
+            f.k_hi = b.fk_h;
+            f.k_lo = b.fk_l;
+            f.v_hi = b.fv_h;
+            f.v_lo = b.fv_l;
+            f.lse = sv->lse_sel;
+            f.D = b.d_sel;
+            f.dq = dQ.p + (int64_t)Ms * dQ.rs;  // image rows
+            f.dq_hs = dQ.hs;
+            f.dq_rs = dQ.rs;
+            f.accumulate_q = true;
+            f.dk = b.gk;
+            f.dk_hs = b.n_fr * 64;
+            f.dk_rs = 64;
+            f.dv = b.gv;
+            f.dv_hs = b.n_fr * 64;
+            f.dv_rs = 64;
+            f.accumulate_kv = false;
+            GSA_CUDA(launch_bwd_tc(f, st));
+            GSA_CUDA(launch_forced_scatter_add(b.gk, b.gv, H, lp.L, rs, b.n_fr, dK, dV, st));
+        }
     } else {
         GSA_CUDA(launch_sel_bwd(sa, H, st));
     }

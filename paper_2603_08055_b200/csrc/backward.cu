@@ -910,6 +910,57 @@ __global__ void window_sum_kernel(FMat in, int heads, int dim, DevLayout L, FOut
     }
 }
 
+// ------------------------------------------------ hybrid fast path (forced windows)
+// the plan without its forced windows: per-row counts, then the kept ids in row order
+// (ids outside [0, W) are kept: the caller's plan check reports them before anything reads them)
+__device__ __forceinline__ bool dropped(const uint8_t* mask, int W, int32_t id) {
+    return id >= 0 && id < W && mask[id];
+}
+__global__ void plan_drop_count_kernel(const int64_t* offsets, const int32_t* ids, int64_t rows, const uint8_t* mask,
+                                       int W, int64_t* sizes) {
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= rows) return;
+    int64_t n = 0;
+    for (int64_t e = offsets[r]; e < offsets[r + 1]; ++e) n += dropped(mask, W, ids[e]) ? 0 : 1;
+    sizes[r] = n;
+}
+__global__ void plan_drop_fill_kernel(const int64_t* offsets, const int32_t* ids, int64_t rows, const uint8_t* mask,
+                                      int W, const int64_t* out_offsets, int32_t* out_ids) {
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= rows) return;
+    int64_t o = out_offsets[r];
+    for (int64_t e = offsets[r]; e < offsets[r + 1]; ++e)
+        if (!dropped(mask, W, ids[e])) out_ids[o++] = ids[e];
+}
+
+// rows of the forced frames (every ref_stride-th frame, all its tokens) of [H][M][64] bf16
+// planes -> contiguous [H][n_ff * tokens_per_frame][64]; 16 bytes per thread
+__global__ void forced_gather_kernel(const __nv_bfloat16* src, int64_t src_hs, int heads, DevLayout L, int ref_stride,
+                                     int64_t rows, __nv_bfloat16* dst) {
+    const int64_t n = (int64_t)heads * rows * 8;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+        const int c = (int)(e & 7);
+        const int64_t i = (e >> 3) % rows, h = (e >> 3) / rows;
+        const int64_t f = (i / L.tokens_per_frame) * ref_stride, t = i % L.tokens_per_frame;
+        const int64_t sr = L.num_special + f * L.tokens_per_frame + t;
+        reinterpret_cast<uint4*>(dst + (h * rows + i) * 64)[c] = reinterpret_cast<const uint4*>(src + h * src_hs + sr * 64)[c];
+    }
+}
+
+// dK / dV of the forced rows (contiguous [H][rows][64] f32) added to their rows of dk / dv
+__global__ void forced_scatter_add_kernel(const float* gk, const float* gv, int heads, DevLayout L, int ref_stride,
+                                          int64_t rows, FOut dk, FOut dv) {
+    const int64_t n = (int64_t)heads * rows * 64;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+        const int j = (int)(e & 63);
+        const int64_t i = (e >> 6) % rows, h = (e >> 6) / rows;
+        const int64_t f = (i / L.tokens_per_frame) * ref_stride, t = i % L.tokens_per_frame;
+        const int64_t r = L.num_special + f * L.tokens_per_frame + t;
+        dk.p[h * dk.hs + r * dk.rs + j] += gk[e];
+        dv.p[h * dv.hs + r * dv.rs + j] += gv[e];
+    }
+}
+
 unsigned grid_for(int64_t n, int threads = 256) {
     const int64_t b = (n + threads - 1) / threads;
     return (unsigned)(b < 148 * 64 ? (b > 0 ? b : 1) : 148 * 64);
@@ -1132,6 +1183,38 @@ cudaError_t launch_window_sum(const FMat& in, int heads, int dim, const DevLayou
     const int64_t n = (int64_t)heads * L.windows * dim;
     if (n == 0) return cudaSuccess;
     window_sum_kernel<<<grid_for(n), 256, 0, st>>>(in, heads, dim, L, out);
+    note_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_plan_drop(const int64_t* offsets, const int32_t* ids, int64_t rows, const uint8_t* mask, int W,
+                             int64_t* sizes, int64_t* out_offsets, int32_t* out_ids, void* tmp, size_t tmp_bytes,
+                             cudaStream_t st) {
+    if (rows == 0) return cudaSuccess;
+    const unsigned b = (unsigned)((rows + 255) / 256);
+    plan_drop_count_kernel<<<b, 256, 0, st>>>(offsets, ids, rows, mask, W, sizes);
+    note_launch();
+    cudaError_t e = launch_scan_offsets(sizes, rows, out_offsets, tmp, tmp_bytes, st);
+    if (e != cudaSuccess) return e;
+    plan_drop_fill_kernel<<<b, 256, 0, st>>>(offsets, ids, rows, mask, W, out_offsets, out_ids);
+    note_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_forced_gather(const __nv_bfloat16* src, int64_t src_hs, int heads, const DevLayout& L, int ref_stride,
+                                 int64_t rows, __nv_bfloat16* dst, cudaStream_t st) {
+    const int64_t n = (int64_t)heads * rows * 8;
+    if (n == 0) return cudaSuccess;
+    forced_gather_kernel<<<grid_for(n), 256, 0, st>>>(src, src_hs, heads, L, ref_stride, rows, dst);
+    note_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_forced_scatter_add(const float* gk, const float* gv, int heads, const DevLayout& L, int ref_stride,
+                                      int64_t rows, const FOut& dk, const FOut& dv, cudaStream_t st) {
+    const int64_t n = (int64_t)heads * rows * 64;
+    if (n == 0) return cudaSuccess;
+    forced_scatter_add_kernel<<<grid_for(n), 256, 0, st>>>(gk, gv, heads, L, ref_stride, rows, dk, dv);
     note_launch();
     return cudaGetLastError();
 }

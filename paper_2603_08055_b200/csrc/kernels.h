@@ -223,6 +223,15 @@ cudaError_t launch_to_f32(const TensorRef& in, int heads, int64_t rows, int dim,
 cudaError_t launch_pool_adjoint(const FMat& in, int heads, int dim, const DevLayout& L, float inv, const FOut& out,
                                 cudaStream_t st);
 cudaError_t launch_window_sum(const FMat& in, int heads, int dim, const DevLayout& L, const FOut& out, cudaStream_t st);
+// hybrid backward: the plan without its forced windows (mask[w] = 1 for forced), forced-frame
+// rows of bf16 planes gathered contiguously, their dK / dV added back to dk / dv
+cudaError_t launch_plan_drop(const int64_t* offsets, const int32_t* ids, int64_t rows, const uint8_t* mask, int W,
+                             int64_t* sizes, int64_t* out_offsets, int32_t* out_ids, void* tmp, size_t tmp_bytes,
+                             cudaStream_t st);
+cudaError_t launch_forced_gather(const __nv_bfloat16* src, int64_t src_hs, int heads, const DevLayout& L, int ref_stride,
+                                 int64_t rows, __nv_bfloat16* dst, cudaStream_t st);
+cudaError_t launch_forced_scatter_add(const float* gk, const float* gv, int heads, const DevLayout& L, int ref_stride,
+                                      int64_t rows, const FOut& dk, const FOut& dv, cudaStream_t st);
 cudaError_t launch_rowdot(const FMat& a, const FMat& b, int heads, int rows, int dim, float* out, cudaStream_t st);
 
 }  // namespace gsa_sm100

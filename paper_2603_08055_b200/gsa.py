@@ -309,7 +309,8 @@ def build_selection_plan(topk: torch.Tensor, layout: TokenLayout, variant: int, 
     L = _lib.load()
     topk = topk.to(torch.int32).contiguous()
     H, W, k = topk.shape
-    F = layout.num_windows if variant == HYBRID else 0
+    # row width bound: forced windows (reference frames every ref_stride frames) ++ top-k
+    F = len(range(0, layout.num_frames, max(ref_stride, 1))) * layout.windows_per_frame if variant == HYBRID else 0
     cap = max(1, H * W * (k + F))
     offsets = torch.empty(H * W + 1, dtype=torch.int64, device=topk.device)
     ids = torch.empty(cap, dtype=torch.int32, device=topk.device)

@@ -69,6 +69,7 @@ CASES = [  # layout (ns, nf, gh, gw, s), heads, dim, top_k, variant, ref_stride
     ((3, 4, 8, 8, 2), 2, 32, 5, 1, 2),
     ((5, 2, 12, 12, 4), 3, 64, 4, 1, 1),
     ((1, 2, 8, 16, 8), 2, 128, 1, 0, 100),
+    ((2, 5, 8, 8, 4), 2, 64, 3, 1, 2),  # hybrid fast path: forced frames 0, 2, 4 as a dense pass
 ]
 
 
@@ -92,7 +93,7 @@ def test_backward_kernels_on_reference_context(gsa, ref, lt, H, d, top_k, varian
         assert np.abs(got - want).max() < KERNEL_REL * 10 * max(1.0, np.abs(want).max()), name
 
 
-@pytest.mark.parametrize("lt,H,d,top_k,variant,ref_stride", CASES[:4])
+@pytest.mark.parametrize("lt,H,d,top_k,variant,ref_stride", CASES[:4] + CASES[5:])
 def test_layer_backward_from_x_matches_reference(gsa, ref, lt, H, d, top_k, variant, ref_stride):
     rng = np.random.default_rng(7 + sum(lt))
     M = lt[0] + lt[1] * lt[2] * lt[3]
