@@ -206,17 +206,26 @@ __global__ void __launch_bounds__(BT_THREADS, 1)
             nD_r = ok ? -p.D[(int64_t)h * p.n_fixed + grow] : 0.0f;
         }
         const float2 c2v = make_float2(p.c2, p.c2), scv = make_float2(p.scale, p.scale), m1 = make_float2(-1.0f, -1.0f);
+        // KEYSIDE: streamed queries' (-lse log2 e, -D) for the next step, in registers
+        float nxt_l = -INFINITY, nxt_d = 0.0f;
+        auto load_stats = [&](int jj) {
+            const int64_t q = s_begin + (int64_t)jj * SROWS + row;
+            const bool ok = jj < T && q < s_end;
+            nxt_l = ok ? -p.lse[(int64_t)h * p.n_stream + q] * 1.4426950408889634f : -INFINITY;
+            nxt_d = ok ? -p.D[(int64_t)h * p.n_stream + q] : 0.0f;
+        };
+        if (KEYSIDE && row < SROWS) load_stats(0);
         for (int j = 0; j < T; ++j) {
             const int pb = j & 1;
             if (KEYSIDE) {
-                // the 64 streamed queries' lse / D, shared by every key row
+                // the 64 streamed queries' lse / D, shared by every key row: loaded one step
+                // ahead (the global-load latency overlaps the previous step), published here
                 if (row < SROWS) {
-                    const int64_t q = s_begin + (int64_t)j * SROWS + row;
-                    const bool ok = q < s_end;
-                    sm.st_lse[pb][row] = ok ? -p.lse[(int64_t)h * p.n_stream + q] * 1.4426950408889634f : -INFINITY;
-                    sm.st_D[pb][row] = ok ? -p.D[(int64_t)h * p.n_stream + q] : 0.0f;
+                    sm.st_lse[pb][row] = nxt_l;
+                    sm.st_D[pb][row] = nxt_d;
                 }
                 named_bar_sync(1, 128);
+                if (row < SROWS) load_stats(j + 1);
             }
             mbar_wait(&sm.s_full[pb], (uint32_t)((j >> 1) & 1));
             __syncwarp();
