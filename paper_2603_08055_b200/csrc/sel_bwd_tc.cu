@@ -279,6 +279,7 @@ __global__ void __launch_bounds__(SB_THREADS, 1)
         // ===================== gathered rows: P, dS, epilogue =====================
         const int r = 32 * warp + lane;  // gathered row of the chunk = TMEM lane
         const uint32_t lb = tmem + ((uint32_t)(32 * warp) << 16);
+        const float2 c2v = make_float2(p.c2, p.c2), scv = make_float2(p.scale, p.scale), m1 = make_float2(-1.0f, -1.0f);
         int gc = 0, ic = 0;
         Off on = offs(blockIdx.x);
         for (int64_t item = blockIdx.x; item < p.rows; item += G) {
@@ -293,8 +294,8 @@ __global__ void __launch_bounds__(SB_THREADS, 1)
             if (!KEYSIDE) {
                 if (r < 16) {
                     const int t = L.member(w, r);
-                    sm.own_lse[sb][r] = p.lse[(int64_t)h * L.image_tokens + t] * 1.4426950408889634f;
-                    sm.own_D[sb][r] = p.D[(int64_t)h * L.image_tokens + t];
+                    sm.own_lse[sb][r] = -p.lse[(int64_t)h * L.image_tokens + t] * 1.4426950408889634f;
+                    sm.own_D[sb][r] = -p.D[(int64_t)h * L.image_tokens + t];
                 }
                 named_bar_sync(1, 128);
             }
@@ -326,24 +327,35 @@ __global__ void __launch_bounds__(SB_THREADS, 1)
                 // the output MMAs of chunk gc - 2 read this X / Y buffer: wait before overwriting
                 if (gc >= 2) mbar_wait(&sm.o_done[xb], (uint32_t)(((gc - 2) >> 1) & 1));
 #pragma unroll
-                for (int n = 0; n < 16; ++n) {
-                    const float l2 = KEYSIDE ? lse2 : sm.own_lse[sb][n];
-                    const float Dv = KEYSIDE ? Dg : sm.own_D[sb][n];
-                    float pr = 0.0f, ds = 0.0f;
+                for (int n2 = 0; n2 < 8; ++n2) {
+                    // pairs of own rows on the packed f32x2 pipe (the statistics stored negated)
+                    const float2 nl = KEYSIDE ? make_float2(-lse2, -lse2)
+                                              : *reinterpret_cast<const float2*>(&sm.own_lse[sb][2 * n2]);
+                    const float2 nd = KEYSIDE ? make_float2(-Dg, -Dg)
+                                              : *reinterpret_cast<const float2*>(&sm.own_D[sb][2 * n2]);
+                    float2 pv = make_float2(0.0f, 0.0f), dsv = pv;
                     if (valid) {
-                        pr = ex2_approx(fmaf(__uint_as_float(sv[n]), p.c2, -l2));
-                        ds = pr * (__uint_as_float(dv[n]) - Dv) * p.scale;
+                        const float2 a2 = __ffma2_rn(make_float2(__uint_as_float(sv[2 * n2]), __uint_as_float(sv[2 * n2 + 1])),
+                                                     c2v, nl);
+                        pv = make_float2(ex2_approx(a2.x), ex2_approx(a2.y));
+                        const float2 t2 =
+                            __fadd2_rn(make_float2(__uint_as_float(dv[2 * n2]), __uint_as_float(dv[2 * n2 + 1])), nd);
+                        dsv = __fmul2_rn(__fmul2_rn(pv, t2), scv);
                     }
-                    const __nv_bfloat16 dh = __float2bfloat16_rn(ds);
-                    const __nv_bfloat16 dl = __float2bfloat16_rn(ds - __bfloat162float(dh));
-                    const uint32_t off = bx_off(n, r);
-                    *reinterpret_cast<__nv_bfloat16*>(sm.bx[xb][0] + off) = dh;
-                    *reinterpret_cast<__nv_bfloat16*>(sm.bx[xb][1] + off) = dl;
+                    const __nv_bfloat162 dh = __float22bfloat162_rn(dsv);
+                    const __nv_bfloat162 dl = __float22bfloat162_rn(__ffma2_rn(__bfloat1622float2(dh), m1, dsv));
+                    const uint32_t o0 = bx_off(2 * n2, r), o1 = bx_off(2 * n2 + 1, r);
+                    *reinterpret_cast<__nv_bfloat16*>(sm.bx[xb][0] + o0) = dh.x;
+                    *reinterpret_cast<__nv_bfloat16*>(sm.bx[xb][0] + o1) = dh.y;
+                    *reinterpret_cast<__nv_bfloat16*>(sm.bx[xb][1] + o0) = dl.x;
+                    *reinterpret_cast<__nv_bfloat16*>(sm.bx[xb][1] + o1) = dl.y;
                     if (KEYSIDE) {
-                        const __nv_bfloat16 ph = __float2bfloat16_rn(pr);
-                        const __nv_bfloat16 pl = __float2bfloat16_rn(pr - __bfloat162float(ph));
-                        *reinterpret_cast<__nv_bfloat16*>(sm.bx[xb][2] + off) = ph;
-                        *reinterpret_cast<__nv_bfloat16*>(sm.bx[xb][3] + off) = pl;
+                        const __nv_bfloat162 ph = __float22bfloat162_rn(pv);
+                        const __nv_bfloat162 pl = __float22bfloat162_rn(__ffma2_rn(__bfloat1622float2(ph), m1, pv));
+                        *reinterpret_cast<__nv_bfloat16*>(sm.bx[xb][2] + o0) = ph.x;
+                        *reinterpret_cast<__nv_bfloat16*>(sm.bx[xb][2] + o1) = ph.y;
+                        *reinterpret_cast<__nv_bfloat16*>(sm.bx[xb][3] + o0) = pl.x;
+                        *reinterpret_cast<__nv_bfloat16*>(sm.bx[xb][3] + o1) = pl.y;
                     }
                 }
                 fence_proxy_async_smem();
