@@ -1,5 +1,8 @@
-// backward.cu — the layer backward (gsa_backward, gradients.hpp:54-265) and the
-// projection backward, on CUDA cores in f32.
+// backward.cu — the CUDA-core side of the layer backward (gsa_backward, gradients.hpp:
+// 54-265): the elementwise steps every call runs, and the attention / projection passes for
+// the shapes the tensor-core kernels do not take (head dim != 64, window side != 4). At
+// d = 64, s = 4 the dense passes run in bwd_tc.cu, the selection passes in sel_bwd_tc.cu and
+// the projection backward in proj_bwd_tc.cu.
 //
 // The backward of each branch is the flash-style recomputation the reference
 // uses: probabilities are rebuilt from the saved log-sum-exp rows,
@@ -7,27 +10,29 @@
 // top-k selection is a constant (gradients.hpp:52-54). Every gradient is
 // produced by exactly one owner thread per element and kernels touching the same
 // output run in a fixed stream order, so the result is deterministic without
-// floating-point atomics:
+// floating-point atomics.
 //
+// Every call:
 //   gate_bwd         gate fuse (gradients.hpp:96-119): dS_sel = (1-g) dO, dz =
 //                    g(1-g)(O_comp - O_sel) dO, dq_img = W_g dz (written), the
 //                    window sums of g dO (upsample backward, :122-128) and the D
-//                    rows of both branches
+//                    rows of both branches (8 windows per CTA, W_g staged once)
+//   pool_bwd         pooled-gradient scatter (avg-pool adjoint, :158-169)
+//   inverse plan     (head, key window, query window) keys radix-sorted: each key
+//                    window's query windows, ascending (the selection key-side passes)
+//   atb / atb_reduce dW = A^T B split over rows with a fixed-order reduction of the
+//                    partials (dW_g = Q_img^T dz)
+//   hybrid helpers   the plan without its forced windows, forced-frame row gathers and
+//                    the scatter-add of their dK / dV
+// Other shapes:
 //   dense_bwd_dkdv   FlashAttention-2 key-side pass (one CTA per 64 keys, loop over
 //   dense_bwd_dq     every query tile) and query-side pass: the compressed branch
-//                    (:131-155, windows x windows) and the special rows (:197-222,
-//                    Ms queries x all M keys)
-//   pool_bwd         pooled-gradient scatter (avg-pool adjoint, :158-169)
-//   sel_bwd_dq       selection branch (:172-194) query side, one CTA per (head, query
-//                    window), keys gathered from the plan row like the forward
-//   sel_bwd_dkdv     key side, one CTA per (head, key window), queries from the
-//                    INVERSE plan (the windows whose plan row holds it, ascending),
-//                    built by a radix sort of (head, key window, query window)
-//   atb / atb_reduce dW = A^T B split over rows with a fixed-order reduction of the
-//                    partials (dW_g = Q_img^T dz, dW_{q,k,v} = X^T dQ/dK/dV)
-//   dx_gemm          dX = sum_h dQ_h W_q,h^T + dK_h W_k,h^T + dV_h W_v,h^T (:245-263)
+//                    (:131-155, windows x windows) and the special rows (:197-222)
+//   sel16_bwd / sel_bwd_dq / sel_bwd_dkdv  selection branch (:172-194) over the plan
+//                    and its inverse
+//   atb, dx_gemm     projection backward (:245-263)
 //
-// All tiles use the same register blocking: 256 threads as a 16 x 16 grid, thread
+// The dense tiles use one register blocking: 256 threads as a 16 x 16 grid, thread
 // (ty, tx) owning rows ty + 16 i and columns tx + 16 j, so every shared-memory read is
 // either a broadcast or 16 distinct padded rows (conflict-free).
 #include <cub/device/device_radix_sort.cuh>
