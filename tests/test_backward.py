@@ -200,3 +200,25 @@ def test_backward_rejects_mismatched_context(gsa):
     bad = gsa.SelectionPlan(plan.heads, plan.rows, plan.offsets, plan.window_ids[:-1], plan.forced_windows)
     with pytest.raises(gsa.ContextMismatch):
         gsa.gsa_backward(q, k, v, wg, L, p, ctx, out, torch.zeros_like(out), plan=bad)
+
+
+@pytest.mark.parametrize("variant,ref_stride", [(0, 100), (1, 8)])
+def test_layer_backward_16_views_matches_reference(gsa, ref, variant, ref_stride):
+    """The VGGT geometry at 16 views (5 specials + 36x36 patches per view: M = 20,816, W = 1,296,
+    top-32): plan rows of 4 gathered chunks, inverse-plan rows of every length, 80 special rows,
+    key splits, hybrid forced frames 0 and 8 — the tensor-core backward from X against the
+    reference's gsa_backward."""
+    rng = np.random.default_rng(16 + variant)
+    lt = (80, 16, 36, 36, 4)
+    M = lt[0] + lt[1] * lt[2] * lt[3]
+    H, Cm, d = 2, 128, 64
+    x = rng.standard_normal((M, Cm)).astype(np.float32)
+    (wq, wk, wv), wg = weights(rng, H, Cm, d)
+    d_out = rng.standard_normal((H, M, d)).astype(np.float32)
+    r = ref.backward(x, wq, wk, wv, wg, lt, d_out, top_k=32, variant=variant, ref_stride=ref_stride, threads=16)
+    L = gsa.build_token_layout(*lt)
+    p = gsa.GsaParams(window_s=4, top_k=32, variant=variant, ref_stride=ref_stride)
+    out, grads = gsa.layer_backward(dev(x), dev(wq), dev(wk), dev(wv), dev(wg), L, p, dev(d_out))
+    assert rel_l2(host(out), r["out"]) < 1e-3
+    for name in ("dx", "dw_q", "dw_k", "dw_v", "dw_g"):
+        assert rel_l2(host(getattr(grads, name)), r[name]) < E2E_REL, name
