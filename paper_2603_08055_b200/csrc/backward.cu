@@ -52,8 +52,8 @@ __global__ void __launch_bounds__(BT) gate_bwd_kernel(GateBwdArgs a) {
     extern __shared__ __align__(16) float sm[];
     const DevLayout& L = a.L;
     const int dim = a.dim, s2 = L.s * L.s, W = L.windows, Mi = L.image_tokens, Ms = L.num_special;
-    float* wg = sm;                   // [dim][DP+1]
-    float* dz = wg + DP * (DP + 1);   // [s2][DP]
+    float* wg = sm;                   // [DP][DP+4]: W_g^T (wg[j][c] = W_g[c][j])
+    float* dz = wg + DP * (DP + 4);   // [s2][DP]
     float* dcf = dz + s2 * DP;        // [s2][DP]  g * dO (upsample-backward terms)
     float* pr = dcf + s2 * DP;        // [s2][DP]  dS_sel * O_sel (D_sel terms)
     float* red = pr + s2 * DP;        // [DP]      dO_comp * O_comp (D_comp terms)
@@ -63,9 +63,17 @@ __global__ void __launch_bounds__(BT) gate_bwd_kernel(GateBwdArgs a) {
     const int tid = threadIdx.x;
 
     const float* wgh = a.w_g + (int64_t)h * dim * dim;
-    for (int e = tid; e < dim * dim; e += BT) wg[(e / dim) * (DP + 1) + e % dim] = wgh[e];
+    // W_g^T, zero-padded to DP x DP (rows of DP + 1 floats would break float4 alignment:
+    // use DP + 4 like the dense tiles)
+    for (int e = tid; e < DP * DP; e += BT) {
+        const int j = e / DP, c = e - j * DP;
+        wg[j * (DP + 4) + c] = (j < dim && c < dim) ? wgh[c * dim + j] : 0.0f;
+    }
     for (int w = w0; w < min(W, w0 + GATE_WPC); ++w) {
         __syncthreads();  // W_g staged; the previous window's smem rows consumed
+        if (dim < DP)
+            for (int e = tid; e < s2 * DP; e += BT)
+                if (e % DP >= dim) dz[e] = 0.0f;
         const float* comp = a.o_comp + ((int64_t)h * W + w) * dim;
         for (int e = tid; e < s2 * dim; e += BT) {
             const int m = e / dim, j = e - m * dim;
@@ -97,12 +105,29 @@ __global__ void __launch_bounds__(BT) gate_bwd_kernel(GateBwdArgs a) {
             for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
             if (lane == 0) a.d_sel[(int64_t)h * Mi + L.member(w, m)] = acc;
         }
-        // dq_img = W_g dz (gradients.hpp:108-117), written: the first contribution to dQ
-        for (int e = tid; e < s2 * dim; e += BT) {
-            const int m = e / dim, c = e - m * dim;
-            float acc = 0.0f;
-            for (int j = 0; j < dim; ++j) acc += wg[c * (DP + 1) + j] * dz[m * DP + j];
-            a.dq.p[(int64_t)h * a.dq.hs + (int64_t)(Ms + L.member(w, m)) * a.dq.rs + c] = acc;
+        // dq_img = W_g dz (gradients.hpp:108-117), written: the first contribution to dQ.
+        // Thread: one member row x 4 consecutive features; float4 reads of dz and W_g^T rows
+        for (int e = tid; e < s2 * (DP / 4); e += BT) {
+            const int m = e / (DP / 4), c0 = 4 * (e - m * (DP / 4));
+            float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 4
+            for (int j = 0; j < DP; j += 4) {
+                const float4 z = *reinterpret_cast<const float4*>(dz + m * DP + j);
+                const float zz[4] = {z.x, z.y, z.z, z.w};
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const float4 wv = *reinterpret_cast<const float4*>(wg + (j + u) * (DP + 4) + c0);
+                    acc.x = fmaf(wv.x, zz[u], acc.x);
+                    acc.y = fmaf(wv.y, zz[u], acc.y);
+                    acc.z = fmaf(wv.z, zz[u], acc.z);
+                    acc.w = fmaf(wv.w, zz[u], acc.w);
+                }
+            }
+            float* dst = a.dq.p + (int64_t)h * a.dq.hs + (int64_t)(Ms + L.member(w, m)) * a.dq.rs + c0;
+            const float av[4] = {acc.x, acc.y, acc.z, acc.w};
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (c0 + u < dim) dst[u] = av[u];
         }
         __syncthreads();
         if (warp == 0) {
@@ -1006,7 +1031,7 @@ cudaError_t dense_bwd_dp(DenseBwdArgs a, int heads, cudaStream_t st) {
 template <int DP>
 cudaError_t gate_bwd_dp(const GateBwdArgs& a, int heads, cudaStream_t st) {
     const int s2 = a.L.s * a.L.s;
-    const size_t smem = (size_t)(DP * (DP + 1) + 3 * s2 * DP + DP) * sizeof(float);
+    const size_t smem = (size_t)(DP * (DP + 4) + 3 * s2 * DP + DP) * sizeof(float);
     cudaError_t e = cudaFuncSetAttribute(gate_bwd_kernel<DP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     gate_bwd_kernel<DP><<<(unsigned)((int64_t)heads * ((a.L.windows + GATE_WPC - 1) / GATE_WPC)), BT, smem, st>>>(a);
